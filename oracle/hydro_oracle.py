@@ -1,0 +1,354 @@
+"""Plain, slow, obviously-correct CPU oracle for Hydro's eddy hot path (arXiv 2403.14902).
+
+TEST INFRASTRUCTURE ONLY -- imported solely by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs.  It shares no code with the CUDA
+path (paper_2403_14902_b200/) and imports nothing from it.  Inputs come from
+``synth`` (which holds no method arithmetic).  Arithmetic is float64 numpy unless
+the method fixes another precision (bf16 crop values, f32 area division).
+
+What it computes (PAPER.md citations; "R<n>" = numbered reading in DESIGN.md §2):
+
+* the query result: ``SELECT id, bbox ... WHERE p_1 AND ... AND p_P`` (PAPER.md:43-49,
+  276-282) -- every predicate evaluated on every tuple, no short-circuit, rows kept in
+  input (ascending id) order (R18);
+* per-predicate verdicts, each a pure function of the tuple:
+  LABEL_EQ, HASH (R5, stand-in for the synthetic 10/20 ms predicates,
+  PAPER.md:550-552), LINEAR = argmax(W . Crop(frame, bbox) + b) == target (PAPER.md:47-48,
+  286-288; R9-R14, R19);
+* eddy statistics: count-based selectivity, measured cost,
+  the score ``cost / (1 - selectivity)`` and its lowest-first order,
+  the decayed fold (R4), the closed-form expected cost (R20);
+* the sequential short-circuit evaluation with eager materialization (PAPER.md:227,
+  251-253) used to pin order independence and the STATIC counters.
+
+Pins: tests/test_oracle.py checks every function here against something other than
+itself (published hash vectors, torch's interpolate / adaptive_avg_pool2d, one-hot and
+constant-frame closed forms, brute force over all orders, the paper's printed numbers).
+Parity unpinned: none of the functions below.  Measured cycle costs (an input to the
+fold) are not reproducible and are taken from the GPU's own report (DESIGN.md §2 R6).
+"""
+from __future__ import annotations
+
+import itertools
+import math
+from typing import Dict, List, Sequence
+
+import numpy as np
+
+CROP = 64
+K_FEATURES = CROP * CROP * 3
+
+# --------------------------------------------------------------------------------------
+# HASH predicate (R5): SplitMix64 (Steele/Lea/Flood) + murmur3 fmix32 rounds.
+
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_SM_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_SM_M2 = np.uint64(0x94D049BB133111EB)
+_FM_M1 = np.uint32(0x85EBCA6B)
+_FM_M2 = np.uint32(0xC2B2AE35)
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """z = x + golden; z = (z ^ z>>30) * M1; z = (z ^ z>>27) * M2; return z ^ z>>31 (mod 2**64)."""
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = x + _GOLDEN
+        z = (z ^ (z >> np.uint64(30))) * _SM_M1
+        z = (z ^ (z >> np.uint64(27))) * _SM_M2
+        return z ^ (z >> np.uint64(31))
+
+
+def fmix32(h: np.ndarray) -> np.ndarray:
+    """murmur3 finaliser: h^=h>>16; h*=0x85EBCA6B; h^=h>>13; h*=0xC2B2AE35; h^=h>>16 (mod 2**32)."""
+    h = np.asarray(h, dtype=np.uint32)
+    with np.errstate(over="ignore"):
+        h = h ^ (h >> np.uint32(16))
+        h = h * _FM_M1
+        h = h ^ (h >> np.uint32(13))
+        h = h * _FM_M2
+        return h ^ (h >> np.uint32(16))
+
+
+def bbox_wh(bbox: np.ndarray):
+    b = np.asarray(bbox, dtype=np.int64)
+    return b[:, 2] - b[:, 0], b[:, 3] - b[:, 1]
+
+
+def hash_units(pred: Dict, bbox: np.ndarray) -> np.ndarray:
+    """units(t) = units, or ceil(w*h / units_per_area) when units_per_area > 0 (cfg4)."""
+    n = len(bbox)
+    if pred.get("units_per_area", 0) > 0:
+        w, h = bbox_wh(bbox)
+        upa = int(pred["units_per_area"])
+        return np.maximum((w * h + upa - 1) // upa, 1)
+    return np.full(n, int(pred["units"]), dtype=np.int64)
+
+
+def hash_verdict(pred: Dict, ids: np.ndarray, bbox: np.ndarray) -> np.ndarray:
+    """v(t): h = hi32(splitmix64(id ^ seed)); for r < units(t): h = fmix32(h + r); h < T(t)."""
+    ids = np.asarray(ids, dtype=np.uint64)
+    units = hash_units(pred, bbox)
+    h = (splitmix64(ids ^ np.uint64(pred["seed"])) >> np.uint64(32)).astype(np.uint32)
+    with np.errstate(over="ignore"):
+        for r in range(int(units.max(initial=0))):
+            h = np.where(r < units, fmix32(h + np.uint32(r)), h)
+    t0, t1 = pred["threshold"]
+    T = np.where(ids >= np.uint64(pred["drift_id"]), np.uint64(t1), np.uint64(t0))
+    return h.astype(np.uint64) < T
+
+
+def label_verdict(pred: Dict, label: np.ndarray) -> np.ndarray:
+    """Object.label = 'dog'."""
+    return np.asarray(label).astype(np.int64) == int(pred["label"])
+
+
+# --------------------------------------------------------------------------------------
+# Crop(frame, bbox) -> 64x64x3 (size and interpolation: R10)
+
+
+def crop_nearest(frames: np.ndarray, frame_id: np.ndarray, bbox: np.ndarray) -> np.ndarray:
+    """NEAREST_EXACT: sy = y0 + ((2dy+1)h) // 128, sx = x0 + ((2dx+1)w) // 128; -> uint8 [n,64,64,3]."""
+    b = np.asarray(bbox, dtype=np.int64)
+    x0, y0 = b[:, 0], b[:, 1]
+    w, h = bbox_wh(b)
+    d = np.arange(CROP, dtype=np.int64)
+    sy = y0[:, None] + ((2 * d[None, :] + 1) * h[:, None]) // (2 * CROP)
+    sx = x0[:, None] + ((2 * d[None, :] + 1) * w[:, None]) // (2 * CROP)
+    f = np.asarray(frame_id, dtype=np.int64)
+    return frames[f[:, None, None], sy[:, :, None], sx[:, None, :]]
+
+
+def f32_to_bf16_rne(x: np.ndarray) -> np.ndarray:
+    """Round float32 to bfloat16 (nearest, ties to even); returned as float32 holding the bf16 value."""
+    bits = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    bias = np.uint64(0x7FFF) + ((bits >> np.uint64(16)) & np.uint64(1))
+    r = ((bits + bias) >> np.uint64(16)) << np.uint64(16)
+    return r.astype(np.uint32).view(np.float32)
+
+
+def crop_area(frames: np.ndarray, frame_id: np.ndarray, bbox: np.ndarray) -> np.ndarray:
+    """AREA: bin [y0 + dy*h//64, y0 + ceil((dy+1)h/64)) x same in x; value = bf16_rne(f32(sum)/f32(count)).
+
+    Returns float32 [n,64,64,3] holding bf16 values (R10, R19).  Sums are exact int64.
+    """
+    b = np.asarray(bbox, dtype=np.int64)
+    out = np.empty((len(b), CROP, CROP, 3), dtype=np.float32)
+    d = np.arange(CROP, dtype=np.int64)
+    for i in range(len(b)):
+        x0, y0, x1, y1 = (int(v) for v in b[i])
+        w, h = x1 - x0, y1 - y0
+        img = frames[int(frame_id[i]), y0:y1, x0:x1, :].astype(np.int64)
+        sat = np.zeros((h + 1, w + 1, 3), dtype=np.int64)  # summed-area table
+        sat[1:, 1:] = img.cumsum(0).cumsum(1)
+        ys, ye = (d * h) // CROP, ((d + 1) * h + CROP - 1) // CROP
+        xs, xe = (d * w) // CROP, ((d + 1) * w + CROP - 1) // CROP
+        s = (sat[ye[:, None], xe[None, :]] - sat[ys[:, None], xe[None, :]]
+             - sat[ye[:, None], xs[None, :]] + sat[ys[:, None], xs[None, :]])
+        cnt = ((ye - ys)[:, None] * (xe - xs)[None, :])[:, :, None]
+        out[i] = f32_to_bf16_rne(s.astype(np.float32) / cnt.astype(np.float32))
+    return out
+
+
+def crop_features(pred: Dict, frames, frame_id, bbox) -> np.ndarray:
+    """x[(dy*64+dx)*3+ch] (HWC flatten of the crop; R10) as float64 [n, 12288]."""
+    if pred.get("crop_mode", "nearest") == "area":
+        c = crop_area(frames, frame_id, bbox)
+    else:
+        c = crop_nearest(frames, frame_id, bbox)
+    return c.reshape(len(bbox), K_FEATURES).astype(np.float64)
+
+
+# --------------------------------------------------------------------------------------
+# LINEAR classifier predicate (stand-in for DogBreed/DogColorClassifier, R12-R14)
+
+
+def linear_logits(pred: Dict, x: np.ndarray) -> np.ndarray:
+    """z_c = sum_k x_k W[c][k] + b[c] in float64 from the exact bf16 W and f32 b."""
+    W = np.asarray(pred["weight"].float().numpy() if hasattr(pred["weight"], "float") else pred["weight"],
+                   dtype=np.float64)
+    b = np.asarray(pred["bias"].numpy() if hasattr(pred["bias"], "numpy") else pred["bias"],
+                   dtype=np.float64)
+    return x @ W.T + b[None, :]
+
+
+def argmax_first(z: np.ndarray) -> np.ndarray:
+    """argmax over classes, lowest index on ties (R12)."""
+    best = np.zeros(z.shape[0], dtype=np.int64)
+    for c in range(1, z.shape[1]):
+        best = np.where(z[:, c] > z[np.arange(z.shape[0]), best], c, best)
+    return best
+
+
+def margin(z: np.ndarray, target: int) -> np.ndarray:
+    """m = z_target - max_{c != target} z_c."""
+    others = np.delete(z, target, axis=1)
+    return z[:, target] - others.max(axis=1)
+
+
+def linear_verdict(pred: Dict, frames, frame_id, bbox, chunk=512, return_logits=False):
+    out, logits = [], []
+    for a in range(0, len(bbox), chunk):
+        x = crop_features(pred, frames, frame_id[a:a + chunk], bbox[a:a + chunk])
+        z = linear_logits(pred, x)
+        out.append(argmax_first(z) == int(pred["target"]))
+        if return_logits:
+            logits.append(z)
+    v = np.concatenate(out) if out else np.zeros(0, dtype=bool)
+    if return_logits:
+        return v, (np.concatenate(logits) if logits else np.zeros((0, int(pred["n_classes"]))))
+    return v
+
+
+# --------------------------------------------------------------------------------------
+# Evaluate-all and the query result ("iff it passes all filters")
+
+
+def as_numpy_tuples(t) -> Dict[str, np.ndarray]:
+    """Accepts synth.Tuples or a dict; returns numpy columns (id u64, frame_id, bbox int64, label)."""
+    if isinstance(t, dict):
+        return t
+    return dict(id=t.id.cpu().numpy().astype(np.uint64), frame_id=t.frame_id.cpu().numpy().astype(np.int64),
+                bbox=t.bbox.cpu().numpy().astype(np.int64), label=t.label.cpu().numpy().astype(np.int64))
+
+
+def predicate_verdict(pred: Dict, tup: Dict[str, np.ndarray], frames=None) -> np.ndarray:
+    kind = pred["kind"]
+    if kind == "label_eq":
+        return label_verdict(pred, tup["label"])
+    if kind == "hash":
+        return hash_verdict(pred, tup["id"], tup["bbox"])
+    if kind == "linear":
+        return linear_verdict(pred, frames, tup["frame_id"], tup["bbox"])
+    raise ValueError(kind)
+
+
+def evaluate_all(preds: Sequence[Dict], tuples, frames=None) -> np.ndarray:
+    """Verdict matrix V[k, i] = p_k(t_i) for every predicate and every tuple (no short-circuit)."""
+    tup = as_numpy_tuples(tuples)
+    n = len(tup["id"])
+    V = np.zeros((len(preds), n), dtype=bool)
+    for k, p in enumerate(preds):
+        V[k] = predicate_verdict(p, tup, frames)
+    return V
+
+
+def query_result(tuples, V: np.ndarray):
+    """R = [(id, bbox) for t in tuples if AND_k V[k, t]] in input order."""
+    tup = as_numpy_tuples(tuples)
+    keep = np.all(V, axis=0) if len(V) else np.ones(len(tup["id"]), dtype=bool)
+    return tup["id"][keep], tup["bbox"][keep], keep
+
+
+# --------------------------------------------------------------------------------------
+# Eager-materialization short-circuit evaluation of one routing batch in a given order
+# ("dropped immediately", 251-253)
+
+
+def sequential_eval(V: np.ndarray, order: Sequence[int]):
+    """Run predicates in ``order`` on the alive set only; returns (in_k, pass_k, alive mask)."""
+    P, n = V.shape
+    alive = np.ones(n, dtype=bool)
+    n_in = np.zeros(P, dtype=np.int64)
+    n_pass = np.zeros(P, dtype=np.int64)
+    for k in order:
+        n_in[k] = int(alive.sum())
+        alive = alive & V[k]
+        n_pass[k] = int(alive.sum())
+    return n_in, n_pass, alive
+
+
+# --------------------------------------------------------------------------------------
+# Statistics, score, order (R1-R4, R20)
+
+
+def selectivity(s_in: float, s_pass: float, prior: float = 0.5) -> float:
+    """passed / in; prior when nothing observed (R3)."""
+    return prior if s_in <= 0 else s_pass / s_in
+
+
+def cost_per_tuple(s_in: float, s_cost: float, declared: float) -> float:
+    """cost / in (PAPER.md:248, 422 'ms per tuple'); declared cost when nothing observed (R3)."""
+    return declared if s_in <= 0 else s_cost / s_in
+
+
+def score(c: float, s: float) -> float:
+    """Hellerstein rank c / (1 - s): 0 when c == 0, +inf when s >= 1 (R1)."""
+    if c == 0.0:
+        return 0.0
+    if s >= 1.0:
+        return math.inf
+    return c / (1.0 - s)
+
+
+def policy_key(policy: str, c: float, s: float) -> float:
+    """score-driven (default), cost-driven, selectivity-driven."""
+    if policy in ("score", "static"):
+        return score(c, s)
+    if policy == "cost":
+        return c
+    if policy == "selectivity":
+        return s
+    raise ValueError(policy)
+
+
+def order_by_key(keys: Sequence[float]) -> List[int]:
+    """Lowest key first; ties -> lowest predicate id (R2)."""
+    return sorted(range(len(keys)), key=lambda k: (keys[k], k))
+
+
+def expected_cost(order: Sequence[int], c: Sequence[float], s: Sequence[float]) -> float:
+    """E(pi) = sum_i c_{pi_i} * prod_{j<i} s_{pi_j} per input tuple (independent predicates, R20)."""
+    e, p = 0.0, 1.0
+    for k in order:
+        e += c[k] * p
+        p *= s[k]
+    return e
+
+
+def realized_cost(n_in: Sequence[int], c: Sequence[float]) -> float:
+    """sum_k c_k * in_k."""
+    return float(sum(ci * ni for ci, ni in zip(c, n_in)))
+
+
+class FoldState:
+    """Decayed statistics S <- gamma*S + delta, applied per predicate only when delta_in > 0 (R4).
+
+    gamma = 1 gives the paper's plain cumulative counts.
+    """
+
+    def __init__(self, n_pred: int, gamma: float, declared_cost: Sequence[float], prior: float = 0.5):
+        self.s_in = [0.0] * n_pred
+        self.s_pass = [0.0] * n_pred
+        self.s_cost = [0.0] * n_pred
+        self.gamma = gamma
+        self.declared = list(declared_cost)
+        self.prior = prior
+
+    def fold(self, d_in, d_pass, d_cost):
+        for k in range(len(self.s_in)):
+            if d_in[k] > 0:
+                self.s_in[k] = self.gamma * self.s_in[k] + float(d_in[k])
+                self.s_pass[k] = self.gamma * self.s_pass[k] + float(d_pass[k])
+                self.s_cost[k] = self.gamma * self.s_cost[k] + float(d_cost[k])
+
+    def sel(self):
+        return [selectivity(a, b, self.prior) for a, b in zip(self.s_in, self.s_pass)]
+
+    def cost(self):
+        return [cost_per_tuple(a, c, d) for a, c, d in zip(self.s_in, self.s_cost, self.declared)]
+
+    def order(self, policy="score"):
+        c, s = self.cost(), self.sel()
+        return order_by_key([policy_key(policy, ci, si) for ci, si in zip(c, s)])
+
+
+def brute_force_best_orders(c: Sequence[float], s: Sequence[float]):
+    """All orders minimising E(pi) (exhaustive, for pins on tiny inputs)."""
+    best, arg = math.inf, []
+    for perm in itertools.permutations(range(len(c))):
+        e = expected_cost(perm, c, s)
+        if e < best - 1e-12 * max(1.0, abs(best) if best < math.inf else 1.0):
+            best, arg = e, [perm]
+        elif abs(e - best) <= 1e-12 * max(1.0, abs(best)):
+            arg.append(perm)
+    return best, arg

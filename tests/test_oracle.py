@@ -1,0 +1,294 @@
+"""Pins for the CPU oracle (-m "not gpu").  Each test checks oracle/ against something other
+than itself: published hash vectors, torch's interpolate / adaptive_avg_pool2d, closed forms,
+brute force over all orders, and numbers printed in PAPER.md (tests/golden/paper_pins.json).
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import Tuples, hash_pred, make_frames, make_tuples, workload
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_pins.json")))
+
+
+# ----------------------------------------------------------------------------- HASH (R5)
+
+def test_splitmix64_published_sequence():
+    g = 0x9E3779B97F4A7C15
+    seq = [int(O.splitmix64(np.uint64((i * g) % 2 ** 64))) for i in range(3)]
+    assert seq == [int(v, 16) for v in GOLD["hash_vectors"]["splitmix64_seq0"]]
+
+
+def test_fmix32_published_vectors():
+    for k, v in GOLD["hash_vectors"]["fmix32"].items():
+        assert int(O.fmix32(np.uint32(int(k, 16)))) == int(v, 16)
+
+
+@pytest.mark.parametrize("sel", [0.1, 0.5, 0.9, 0.254])
+@pytest.mark.parametrize("units", [1, 4])
+def test_hash_selectivity_binomial_band(sel, units):
+    n = 200_000
+    p = hash_pred(7, sel, units=units)
+    ids = np.arange(n, dtype=np.uint64)
+    bbox = np.tile(np.array([[0, 0, 8, 8]]), (n, 1))
+    rate = O.hash_verdict(p, ids, bbox).mean()
+    assert abs(rate - sel) < 5 * math.sqrt(sel * (1 - sel) / n)
+
+
+def test_hash_threshold_extremes_and_drift():
+    ids = np.arange(1000, dtype=np.uint64)
+    bbox = np.tile(np.array([[0, 0, 8, 8]]), (1000, 1))
+    assert O.hash_verdict(hash_pred(3, 1.0), ids, bbox).all()      # T = 2**32 passes all
+    assert not O.hash_verdict(hash_pred(3, 0.0), ids, bbox).any()  # T = 0 passes none
+    p = hash_pred(3, 1.0, sel_after=0.0, drift_id=500)
+    v = O.hash_verdict(p, ids, bbox)
+    assert v[:500].all() and not v[500:].any()
+
+
+def test_hash_rounds_are_fmix_of_plus_r():
+    # units = 2 is fmix32(fmix32(h0 + 0) + 1) with h0 = hi32(splitmix64(id ^ seed)), written out
+    # independently with Python ints.
+    seed, i = 99, 12345
+    M64, M32 = 2 ** 64 - 1, 2 ** 32 - 1
+
+    def sm(x):
+        z = (x + 0x9E3779B97F4A7C15) & M64
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+        return z ^ (z >> 31)
+
+    def fm(h):
+        h ^= h >> 16; h = (h * 0x85EBCA6B) & M32; h ^= h >> 13; h = (h * 0xC2B2AE35) & M32
+        return h ^ (h >> 16)
+
+    h = fm((fm(sm(i ^ seed) >> 32) + 1) & M32)
+    for T in (h, h + 1):
+        p = dict(kind="hash", seed=seed, threshold=(T, T), drift_id=2 ** 63 - 1, units=2, units_per_area=0)
+        assert bool(O.hash_verdict(p, np.array([i], np.uint64), np.array([[0, 0, 1, 1]]))[0]) == (h < T)
+
+
+def test_hash_units_per_area():
+    p = hash_pred(5, 0.5, units_per_area=4096)
+    bbox = np.array([[0, 0, 64, 64], [0, 0, 65, 64], [0, 0, 1, 1], [0, 0, 256, 256]])
+    assert O.hash_units(p, bbox).tolist() == [1, 2, 1, 16]
+
+
+def test_cfg1_counts():
+    g = GOLD["cfg1_counts"]
+    w = workload("cfg1")
+    V = O.evaluate_all(w.preds, w.tuples())
+    assert V[0].sum() == g["A_pass"] and V[1].sum() == g["B_pass"] and V.all(0).sum() == g["A_and_B"]
+    n_in, n_pass, _ = O.sequential_eval(V, [0, 1])
+    assert n_in.tolist() == [10000, g["A_pass"]] and n_pass.tolist() == [g["A_pass"], g["A_and_B"]]
+
+
+# ----------------------------------------------------------------------------- crops (R10)
+
+def _torch_crop(frame, b):
+    x0, y0, x1, y1 = (int(v) for v in b)
+    return torch.from_numpy(frame[y0:y1, x0:x1, :].copy()).permute(2, 0, 1)[None].double()
+
+
+def test_crop_nearest_matches_torch_nearest_exact():
+    F = make_frames(3, 4, 96, 128).numpy()
+    t = make_tuples(3, 0, 300, n_frames=4, frame_h=96, frame_w=128, w_min=8, n_octaves=4)
+    tup = O.as_numpy_tuples(t)
+    mine = O.crop_nearest(F, tup["frame_id"], tup["bbox"])
+    for i in range(len(tup["id"])):
+        ref = torch.nn.functional.interpolate(_torch_crop(F[tup["frame_id"][i]], tup["bbox"][i]),
+                                              size=(64, 64), mode="nearest-exact")
+        assert np.array_equal(mine[i], ref[0].permute(1, 2, 0).numpy().astype(np.uint8))
+
+
+def test_bf16_rounding_matches_torch():
+    x = np.random.default_rng(0).standard_normal(100_000).astype(np.float32) * 300
+    x = np.concatenate([x, np.float32([0.5, 1.5, 127.75, 255.0, 1 / 3, 2 / 3])])
+    ref = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(O.f32_to_bf16_rne(x), ref)
+
+
+def test_crop_area_matches_adaptive_avg_pool():
+    F = make_frames(4, 3, 96, 128).numpy()
+    t = make_tuples(4, 0, 60, n_frames=3, frame_h=96, frame_w=128, w_min=8, n_octaves=4)
+    tup = O.as_numpy_tuples(t)
+    mine = O.crop_area(F, tup["frame_id"], tup["bbox"])
+    worst = 0.0
+    for i in range(len(tup["id"])):
+        ref = torch.nn.functional.adaptive_avg_pool2d(_torch_crop(F[tup["frame_id"][i]], tup["bbox"][i]), 64)
+        ref = ref[0].permute(1, 2, 0).numpy()
+        # exact mean vs the f32 division + bf16 rounding: within half a bf16 ulp (+ f32 slack)
+        ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(ref), 1e-30))) - 7)
+        worst = max(worst, float(np.max(np.abs(mine[i] - ref) / ulp)))
+    assert worst <= 0.5 + 1e-3
+
+
+# ----------------------------------------------------------------------------- LINEAR (R12)
+
+def test_logits_one_hot_rows_select_crop_pixels():
+    """W[c] = e_{k_c} -> z_c = x[k_c] + b_c; k = (dy*64+dx)*3+ch; x from torch nearest-exact."""
+    F = make_frames(5, 2, 96, 128).numpy()
+    t = make_tuples(5, 0, 40, n_frames=2, frame_h=96, frame_w=128, w_min=8, n_octaves=4)
+    tup = O.as_numpy_tuples(t)
+    picks = [(0, 0, 0), (0, 63, 2), (63, 0, 1), (17, 42, 2), (63, 63, 0), (31, 5, 1)]
+    W = np.zeros((len(picks), O.K_FEATURES), np.float32)
+    for c, (dy, dx, ch) in enumerate(picks):
+        W[c, (dy * 64 + dx) * 3 + ch] = 1.0
+    b = np.arange(len(picks), dtype=np.float32) * 0.5
+    pred = dict(kind="linear", weight=torch.from_numpy(W).to(torch.bfloat16), bias=torch.from_numpy(b),
+                target=0, n_classes=len(picks), crop_mode="nearest")
+    z = O.linear_logits(pred, O.crop_features(pred, F, tup["frame_id"], tup["bbox"]))
+    for i in range(len(tup["id"])):
+        ref = torch.nn.functional.interpolate(_torch_crop(F[tup["frame_id"][i]], tup["bbox"][i]),
+                                              size=(64, 64), mode="nearest-exact")[0]
+        for c, (dy, dx, ch) in enumerate(picks):
+            assert z[i, c] == float(ref[ch, dy, dx]) + b[c]
+
+
+def test_logits_constant_frame_closed_form():
+    F = np.full((1, 96, 128, 3), 7, np.uint8)
+    t = make_tuples(6, 0, 10, n_frames=1, frame_h=96, frame_w=128, w_min=8)
+    tup = O.as_numpy_tuples(t)
+    p = workload("cfg2").preds[2]
+    z = O.linear_logits(p, O.crop_features(p, F, tup["frame_id"], tup["bbox"]))
+    ref = 7.0 * p["weight"].double().sum(1).numpy() + p["bias"].double().numpy()
+    assert np.array_equal(z, np.tile(ref, (10, 1)))
+
+
+def test_argmax_lowest_index_on_ties_and_margin():
+    z = np.array([[1.0, 3.0, 3.0], [5.0, 5.0, 1.0], [0.0, -1.0, 2.0]])
+    assert O.argmax_first(z).tolist() == [1, 0, 2]
+    assert O.margin(z, 1).tolist() == [0.0, 0.0, -3.0]
+
+
+def test_generator_makes_half_integer_target_margins():
+    """R12: integer logits + 0.5 on the target bias -> |margin| >= 0.5 for every tuple."""
+    w = workload("cfg2", small=True)
+    F = w.frames().numpy()
+    t = w.tuples(n=300)
+    tup = O.as_numpy_tuples(t)
+    for p in w.preds[1:]:
+        _, z = O.linear_verdict(p, F, tup["frame_id"], tup["bbox"], return_logits=True)
+        m = O.margin(z, p["target"])
+        assert np.all(np.abs(m) >= 0.5) and np.all(np.abs(z) < 2 ** 22)
+        assert np.all(np.mod(z[:, p["target"]], 1.0) == 0.5)
+
+
+# ----------------------------------------------------------------------------- AND / order
+
+def test_and_is_order_independent_brute_force():
+    rng = np.random.default_rng(1)
+    V = rng.random((4, 500)) < np.array([[0.3], [0.6], [0.9], [0.5]])
+    ref = V.all(0)
+    for perm in itertools.permutations(range(4)):
+        n_in, n_pass, alive = O.sequential_eval(V, perm)
+        assert np.array_equal(alive, ref)
+        assert n_in[perm[0]] == 500 and n_pass[perm[-1]] == ref.sum()
+
+
+def test_and_order_independent_on_real_predicates():
+    w = workload("cfg2", small=True)
+    F = w.frames().numpy()
+    t = w.tuples(n=400)
+    V = O.evaluate_all(w.preds, t, F)
+    ids, _, keep = O.query_result(t, V)
+    for perm in itertools.permutations(range(3)):
+        assert np.array_equal(O.sequential_eval(V, perm)[2], keep)
+    # n = 1 reduces to a plain filter
+    assert np.array_equal(O.sequential_eval(V[:1], [0])[2], V[0])
+
+
+# ----------------------------------------------------------------------------- rank / E / fold
+
+def test_paper_score_example():
+    g = GOLD["routing_example"]
+    sb = O.score(g["breed"]["cost"], g["breed"]["selectivity"])
+    sc = O.score(g["colour"]["cost"], g["colour"]["selectivity"])
+    assert sb == pytest.approx(g["score_breed"]) and sc == pytest.approx(g["score_colour"]) and sb < sc
+
+
+def test_paper_uc1_first_choice_per_policy():
+    g = GOLD["uc1"]
+    names = ["breed", "colour"]
+    c = [g["breed"]["cost"], g["colour"]["cost"]]
+    s = [g["breed"]["selectivity"], g["colour"]["selectivity"]]
+    for pol, first in g["first_under"].items():
+        keys = [O.policy_key(pol, ci, si) for ci, si in zip(c, s)]
+        assert names[O.order_by_key(keys)[0]] == first
+
+
+@pytest.mark.parametrize("case", ["case1", "case2"])
+def test_paper_table1_colour_first(case):
+    g = GOLD["table1"][case]
+    c = [g["breed"]["cost"], g["colour"]["cost"]]
+    s = [g["breed"]["selectivity"], g["colour"]["selectivity"]]
+    for pol in ("score", "cost"):
+        assert O.order_by_key([O.policy_key(pol, ci, si) for ci, si in zip(c, s)])[0] == 1
+
+
+def test_sequential_timeline_closed_form():
+    """Sequential (one resource) variant of PAPER.md:349-359: breed-first 2+0.1*1 = 2.1/item -> 21
+    units for 10 items < colour-first 1+0.6*2 = 2.2 -> 22: the score order is optimal."""
+    g = GOLD["routing_example"]
+    c = [g["breed"]["cost"], g["colour"]["cost"]]
+    s = [g["breed"]["selectivity"], g["colour"]["selectivity"]]
+    assert O.expected_cost([0, 1], c, s) * g["items"] == pytest.approx(21.0)
+    assert O.expected_cost([1, 0], c, s) * g["items"] == pytest.approx(22.0)
+    assert O.order_by_key([O.score(ci, si) for ci, si in zip(c, s)]) == [0, 1]
+
+
+def test_expected_cost_equals_enumeration_over_outcomes():
+    """E(pi) vs exact enumeration over all 2**n independent verdict vectors (brute force)."""
+    rng = np.random.default_rng(2)
+    for _ in range(50):
+        n = int(rng.integers(1, 6))
+        c, s = rng.random(n) * 10, rng.random(n)
+        order = list(rng.permutation(n))
+        tot = 0.0
+        for bits in itertools.product([0, 1], repeat=n):
+            pr = np.prod([s[k] if bits[k] else 1 - s[k] for k in range(n)])
+            cost = 0.0
+            for k in order:
+                cost += c[k]
+                if not bits[k]:
+                    break
+            tot += pr * cost
+        assert O.expected_cost(order, c, s) == pytest.approx(tot, rel=1e-12)
+
+
+def test_score_order_minimises_expected_cost_brute_force():
+    """Hellerstein: sorting by c/(1-s) attains min_pi E(pi)."""
+    rng = np.random.default_rng(3)
+    for _ in range(2000):
+        n = int(rng.integers(1, 7))
+        c = rng.random(n) * 10
+        s = rng.random(n) * 0.999
+        best, _ = O.brute_force_best_orders(c, s)
+        order = O.order_by_key([O.score(ci, si) for ci, si in zip(c, s)])
+        assert O.expected_cost(order, c, s) <= best * (1 + 1e-12) + 1e-12
+
+
+def test_score_special_cases():
+    assert O.score(0.0, 0.7) == 0.0
+    assert O.score(0.0, 1.0) == 0.0
+    assert O.score(3.0, 1.0) == math.inf
+    assert O.score(5.0, 0.0) == 5.0
+    assert O.order_by_key([1.0, 1.0, 0.5]) == [2, 0, 1]  # ties -> lowest id
+
+
+def test_fold_gamma_one_is_plain_counts_and_priors():
+    f = O.FoldState(2, 1.0, declared_cost=[3.0, 7.0])
+    assert f.sel() == [0.5, 0.5] and f.cost() == [3.0, 7.0]
+    f.fold([1000, 0], [254, 0], [35110.0, 0.0])
+    f.fold([1000, 0], [254, 0], [35110.0, 0.0])
+    assert f.sel()[0] == pytest.approx(0.254) and f.cost()[0] == pytest.approx(35.11)
+    assert f.sel()[1] == 0.5 and f.cost()[1] == 7.0  # unchanged when delta_in == 0
+    g = O.FoldState(1, 0.5, declared_cost=[1.0])
+    g.fold([100], [10], [100.0])
+    g.fold([100], [90], [300.0])
+    assert g.s_in == [150.0] and g.s_pass == [95.0] and g.s_cost == [350.0]
