@@ -1,0 +1,248 @@
+/*
+ * hydro.h -- C ABI of the B200-native eddy hot path of Hydro (arXiv 2403.14902).
+ *
+ * The library evaluates a CONJUNCTION of (expensive) UDF predicates over a stream of
+ * detection tuples, the way Hydro's Eddy does:
+ *   SELECT id, bbox FROM video ... WHERE p_1 AND ... AND p_P
+ * Per submitted routing batch it
+ *   1. orders the predicates by cost / (1 - selectivity), lowest first,
+ *   2. runs the next predicate only on the still-alive tuples and drops failures at once
+ *      ("eager materialization"),
+ *   3. folds per-predicate pass counts and measured costs into running statistics
+ *      (PAPER.md:247-249, 416), which fix the order of the next batch.
+ * A warmup slice is first evaluated on every predicate.
+ *
+ * Every step runs in CUDA kernels for sm_100a on the context's stream; the host never
+ * synchronises inside a batch (the order lives in device memory).  Readings of points the
+ * paper leaves open are numbered R1..R24 in DESIGN.md §2 and cited below.
+ *
+ * Conventions
+ *  - Every function returns hydro_status: HYDRO_OK (0) or a negative error.  No C++
+ *    exception crosses the ABI.  hydro_last_error() returns a thread-local message for the
+ *    last failure on the calling thread.
+ *  - CUDA / NCCL errors raised by asynchronous work are sticky per context and are reported
+ *    (HYDRO_ECUDA / HYDRO_ENCCL) by the next call that synchronises (typically collect).
+ *  - A context is bound to one device and one stream and is NOT thread-safe (like a cuBLAS
+ *    handle); one rank per process, one context per thread.
+ *  - Pointers are plain host or device addresses as stated per argument.  The caller owns
+ *    every buffer it passes; the library owns its internal device buffers.
+ */
+#ifndef HYDRO_H
+#define HYDRO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t hydro_status;
+enum {
+  HYDRO_OK = 0,
+  HYDRO_EINVAL = -1, /* invalid argument (value, size, pointer or layout)                */
+  HYDRO_ENOMEM = -2, /* device or host allocation failed                                  */
+  HYDRO_ECUDA = -3,  /* CUDA runtime error (sticky; message via hydro_last_error)         */
+  HYDRO_ENCCL = -4,  /* NCCL error (sticky)                                               */
+  HYDRO_ESTATE = -5, /* call out of lifecycle order (e.g. add_predicate after a submit)   */
+  HYDRO_ERANGE = -6, /* caller's output buffer too small; *count holds the needed size    */
+  HYDRO_EBUSY = -7   /* all in-flight batch slots hold uncollected results                */
+};
+
+/* Routing policy. */
+enum {
+  HYDRO_POLICY_SCORE = 0,       /* default: cost / (1 - selectivity), lowest first */
+  HYDRO_POLICY_STATIC = 1,      /* "Best Reordering": declared cost / selectivity, never updated
+                                   (PAPER.md:412-413); no warmup */
+  HYDRO_POLICY_FIXED_ORDER = 2, /* "No Reordering" / test hook: the order set by
+                                   hydro_set_fixed_order (default: add order) */
+  HYDRO_POLICY_COST = 3,        /* cost only */
+  HYDRO_POLICY_SELECTIVITY = 4  /* selectivity only */
+};
+
+/* Where the per-tuple cost of a predicate comes from (R6). */
+enum {
+  HYDRO_COST_MEASURED = 0, /* SM-cycles per tuple measured in the kernels (clock64) */
+  HYDRO_COST_DECLARED = 1  /* the declared_cost of the predicate; selectivity is still measured */
+};
+
+/* Predicate kinds (R5, R12-R14). */
+enum {
+  HYDRO_PRED_LABEL_EQ = 0, /* label == label_value                                          */
+  HYDRO_PRED_HASH = 1,     /* synthetic predicate with set selectivity and per-tuple cost (R5) */
+  HYDRO_PRED_LINEAR = 2    /* argmax(W . Crop(frame, bbox) + b) == target (R10-R14, R19)     */
+};
+
+enum { HYDRO_CROP_NEAREST = 0, HYDRO_CROP_AREA = 1 }; /* R10 */
+
+#define HYDRO_MAX_PREDICATES 8
+#define HYDRO_CROP 64
+#define HYDRO_FEATURES 12288 /* 64 * 64 * 3, feature k = (dy*64 + dx)*3 + ch (R10) */
+#define HYDRO_MAX_CLASSES 128
+
+typedef struct hydro_ctx hydro_ctx; /* opaque */
+
+typedef struct {
+  int32_t device;            /* CUDA device ordinal                                           */
+  void* stream;              /* cudaStream_t to run on (e.g. torch.cuda.current_stream());
+                                NULL = a library-owned non-blocking stream                    */
+  int32_t policy;            /* HYDRO_POLICY_*                       (default SCORE)          */
+  int32_t cost_source;       /* HYDRO_COST_*                         (default MEASURED)       */
+  double decay_gamma;        /* S <- gamma*S + delta per fold, in (0,1] (default 0.5; 1 = plain
+                                counts) (R4)                                   */
+  double prior_selectivity;  /* selectivity with no observation (default 0.5) (R3)           */
+  int64_t warmup_tuples;     /* warmup slice of the first batch: evaluated on every predicate
+                                without short-circuit (default 65536; 0 disables) (R8)       */
+  int64_t max_batch_tuples;  /* largest batch accepted (default 1<<20, max 1<<30)             */
+  int32_t max_inflight;      /* uncollected batches held at once (default 4)                 */
+  int32_t rank, world;       /* data-parallel rank / world size (default 0 / 1)              */
+  int32_t sync_every;        /* world > 1: fold (after an NCCL all-reduce of the statistics
+                                deltas) every sync_every batches (default 1)                  */
+  const void* nccl_unique_id;/* world > 1: the 128-byte ncclUniqueId from
+                                hydro_nccl_unique_id() on rank 0, broadcast by the caller    */
+  const uint8_t* frames;     /* DEVICE frame pool, HWC uint8 [n_frames][frame_h][frame_w][3],
+                                BORROWED for the context's lifetime (R11); may be NULL when no
+                                LINEAR predicate is used                                      */
+  int32_t n_frames, frame_h, frame_w; /* frame_w % 4 == 0                                    */
+} hydro_config;
+
+typedef struct {
+  int32_t kind;               /* HYDRO_PRED_*                                                  */
+  /* LABEL_EQ */
+  int32_t label_value;        /* e.g. 16 = COCO 'dog' (R15)                                   */
+  /* HASH (R5):  h = hi32(splitmix64(id ^ seed)); repeat units(t) times h = fmix32(h + r);
+     pass iff h < T(t), T(t) = threshold[id >= drift_id], T in [0, 2^32]                      */
+  uint64_t seed;
+  uint64_t threshold[2];
+  uint64_t drift_id;          /* UINT64_MAX: no drift                                         */
+  int32_t units;              /* rounds per tuple (>= 0) when units_per_area == 0             */
+  int32_t units_per_area;     /* > 0: units(t) = ceil(w*h / units_per_area) (cfg4)            */
+  /* LINEAR (R12-R14): z = W x + b over the 64x64x3 crop x; pass iff argmax z == target
+     (lowest index on ties).  Weights are COPIED at add time.                                 */
+  const uint16_t* weight_bf16;/* bf16 bits, row-major [n_classes][HYDRO_FEATURES]             */
+  const float* bias;          /* [n_classes]                                                   */
+  int32_t weights_on_device;  /* 1: weight_bf16 / bias are device pointers, 0: host pointers  */
+  int32_t n_classes;          /* 2 .. HYDRO_MAX_CLASSES                                        */
+  int32_t target;             /* 0 .. n_classes-1                                              */
+  int32_t crop_mode;          /* HYDRO_CROP_*                                                  */
+  /* statistics priors (STATIC policy values; DECLARED cost source; used before any fold)    */
+  double declared_cost;       /* > 0, same unit as the measured cost for a mixed SCORE policy  */
+  double declared_selectivity;/* in [0, 1]                                                     */
+} hydro_predicate_desc;
+
+/* One routing batch of detection tuples, SoA (D1).  bbox is [n][4]
+   u16 (x0, y0, x1, y1), half-open, inside the frame, w, h >= 1 (R9).  frame_id < n_frames.  */
+typedef struct {
+  const uint64_t* id;
+  const uint32_t* frame_id;
+  const uint16_t* bbox;
+  const uint16_t* label;
+  int64_t n;
+  int32_t on_device;          /* 1: DEVICE columns, BORROWED until the batch is collected
+                                   (not validated: out-of-range values are clamped in-kernel);
+                                 0: HOST columns, validated and copied before return          */
+} hydro_tuples;
+
+typedef struct {
+  int64_t tuples_in;          /* cumulative tuples routed to the predicate (all batches)      */
+  int64_t tuples_passed;      /* cumulative tuples it passed                                   */
+  double cost_per_tuple;      /* current estimate c (SM-cycles per tuple, or declared)         */
+  double selectivity;         /* current estimate s                                            */
+  double rank;                /* policy key (c/(1-s) for SCORE)                                */
+  int32_t position;           /* position in the current order (0 = first)                     */
+  double s_in, s_pass, s_cost;/* decayed counters S (R4)                                       */
+  double cost_raw_total;      /* cumulative measured raw cycles                                */
+} hydro_pred_stats;
+
+/* Per-batch record, available after the batch completed (hydro_batch_info). */
+typedef struct {
+  int64_t n_tuples;
+  int64_t n_results;
+  int64_t warmup_tuples;      /* size of the warmup slice evaluated on every predicate (R8)   */
+  int32_t order_used[HYDRO_MAX_PREDICATES]; /* order for the post-warmup part of the batch    */
+  int64_t tuples_in[HYDRO_MAX_PREDICATES];  /* this batch's counters (warmup included)         */
+  int64_t tuples_passed[HYDRO_MAX_PREDICATES];
+  double cost_raw[HYDRO_MAX_PREDICATES];
+  int32_t n_pred;
+} hydro_batch_report;
+
+/* ---------------------------------------------------------------------------------------- */
+
+const char* hydro_version(void);
+const char* hydro_last_error(void);
+
+/* Fills *cfg with the defaults listed above (device 0, NULL stream, SCORE, MEASURED ...). */
+hydro_status hydro_config_default(hydro_config* cfg);
+
+/* world > 1 only: writes a fresh 128-byte ncclUniqueId to out128 (host).  Call on rank 0 and
+   broadcast it to the other ranks before hydro_create. */
+hydro_status hydro_nccl_unique_id(void* out128);
+
+/* Creates a context on cfg->device.  EINVAL on bad sizes; ENOMEM; ENCCL when the communicator
+   cannot be formed (world > 1; collective over all ranks). */
+hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out);
+
+/* Registers predicate number *pred_id = 0, 1, 2 ... (call order = the conjunction's textual
+   order = the FIXED_ORDER default).  At most HYDRO_MAX_PREDICATES.  ESTATE after the first
+   submit.  EINVAL: n_classes out of range, target outside [0, n_classes), threshold > 2^32,
+   negative units, LINEAR without a frame pool, declared values out of range. */
+hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* desc, int32_t* pred_id);
+
+/* FIXED_ORDER policy: sets the order (a permutation of 0..P-1).  EINVAL if not a permutation. */
+hydro_status hydro_set_fixed_order(hydro_ctx* ctx, const int32_t* order, int32_t n);
+
+/* Enqueues one routing batch on the context's stream and returns its id (0, 1, 2 ...).
+   Asynchronous: returns before the GPU work finishes.  n == 0 is legal (0 results).
+   EINVAL: n > max_batch_tuples, NULL columns, invalid host tuples.  EBUSY: max_inflight
+   batches are uncollected.  The results are the passing (id, bbox) rows in input order. */
+hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* tuples, int64_t* batch_id);
+
+/* Blocks until batch_id finished and returns its result count. */
+hydro_status hydro_batch_count(hydro_ctx* ctx, int64_t batch_id, int64_t* count);
+
+/* Blocks until batch_id finished, then copies its rows: ids[count] (u64) and bboxes[count][4]
+   (u16), in input order, to HOST (out_on_device = 0) or DEVICE (1) buffers, and releases the
+   batch slot.  capacity < count: ERANGE with *count set and the batch kept. */
+hydro_status hydro_collect_results(hydro_ctx* ctx, int64_t batch_id, uint64_t* ids, uint16_t* bboxes,
+                                   int64_t capacity, int64_t* count, int32_t out_on_device);
+
+/* Releases a batch slot without copying (results dropped). */
+hydro_status hydro_release_batch(hydro_ctx* ctx, int64_t batch_id);
+
+/* Per-batch counters and the order used (after the batch finished). */
+hydro_status hydro_batch_info(hydro_ctx* ctx, int64_t batch_id, hydro_batch_report* out);
+
+/* Snapshot of predicate pred_id's statistics after the last fold (synchronises the stream). */
+hydro_status hydro_get_stats(hydro_ctx* ctx, int32_t pred_id, hydro_pred_stats* out);
+
+/* Current order (synchronises): order[0..P-1]; *n = P. */
+hydro_status hydro_get_order(hydro_ctx* ctx, int32_t* order, int32_t* n);
+
+/* Waits for all enqueued work of the context. */
+hydro_status hydro_synchronize(hydro_ctx* ctx);
+
+/* Number of kernels the library has launched so far (evidence for bench "gpu_launches"). */
+hydro_status hydro_launch_count(hydro_ctx* ctx, int64_t* launches);
+
+/* Kernel timing (CUDA events on the context stream around every launch of the kind):
+   enable = 1 starts recording (and clears), 0 stops.  kind: 0 = route/compact kernel (K1),
+   1 = classifier kernel (K4), 2 = fold (K5).  hydro_kernel_time synchronises and returns the
+   summed milliseconds and the number of launches recorded since the last enable. */
+hydro_status hydro_set_kernel_timing(hydro_ctx* ctx, int32_t enable);
+hydro_status hydro_kernel_time(hydro_ctx* ctx, int32_t kind, double* total_ms, int64_t* launches);
+
+/* Destroys the context (synchronises first).  Safe on NULL. */
+hydro_status hydro_destroy(hydro_ctx* ctx);
+
+/* ---- debug hooks (tests) ---------------------------------------------------------------- */
+
+/* Runs predicate pred_id's LINEAR kernel on every tuple of the DEVICE batch `tuples`
+   (no short-circuit, statistics untouched) and writes, when non-NULL, the f32 logits
+   logits_out[n][n_classes] (device) and the bf16 crop features crops_out[n][HYDRO_FEATURES]
+   (device, bf16 bits) plus the verdicts verdict_out[n] (device, uint8 0/1).  Synchronises. */
+hydro_status hydro_debug_linear(hydro_ctx* ctx, int32_t pred_id, const hydro_tuples* tuples,
+                                float* logits_out, uint16_t* crops_out, uint8_t* verdict_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYDRO_H */

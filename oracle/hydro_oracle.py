@@ -316,7 +316,9 @@ class FoldState:
     gamma = 1 gives the paper's plain cumulative counts.
     """
 
-    def __init__(self, n_pred: int, gamma: float, declared_cost: Sequence[float], prior: float = 0.5):
+    def __init__(self, n_pred: int, gamma: float, declared_cost: Sequence[float], prior: float = 0.5,
+                 cost_source: str = "measured"):
+        self.cost_source = cost_source  # "declared": c is always the declared cost (R6)
         self.s_in = [0.0] * n_pred
         self.s_pass = [0.0] * n_pred
         self.s_cost = [0.0] * n_pred
@@ -335,6 +337,8 @@ class FoldState:
         return [selectivity(a, b, self.prior) for a, b in zip(self.s_in, self.s_pass)]
 
     def cost(self):
+        if self.cost_source == "declared":
+            return list(self.declared)
         return [cost_per_tuple(a, c, d) for a, c, d in zip(self.s_in, self.s_cost, self.declared)]
 
     def order(self, policy="score"):

@@ -1,0 +1,270 @@
+// Internal device-side state, kernel parameter blocks and PTX helpers of libhydro.
+// sm_100a only.  Nothing here is shared with oracle/ (DESIGN.md §1).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/hydro.h"
+
+namespace hydro {
+
+constexpr int kMaxPred = HYDRO_MAX_PREDICATES;
+constexpr int kCrop = HYDRO_CROP;
+constexpr int kFeatures = HYDRO_FEATURES;   // 12288
+constexpr int kKBlock = 64;                 // bf16 elements per UMMA K-block row (128 B)
+constexpr int kNumKBlocks = kFeatures / kKBlock;  // 192
+constexpr int kKBlocksPerGroup = 3;         // one crop row (64 px x 3 ch = 192 el) per stage
+constexpr int kGroups = kNumKBlocks / kKBlocksPerGroup;  // 64 crop rows
+
+// ---- K1 (route / filter / compact) geometry
+constexpr int kRouteThreads = 256;
+constexpr int kRouteItems = 8;                              // positions per thread
+constexpr int kRouteTile = kRouteThreads * kRouteItems;     // 2048 positions per tile
+
+// ---- K4 (classifier) geometry
+constexpr int kTileM = 128;                                 // UMMA M (cta_group::1)
+constexpr int kConvWarps = 8;                               // gather/convert warps
+constexpr int kEpiWarps = 4;                                // TMEM quadrant warps 0..3
+constexpr int kLoaderWarp = 4;
+constexpr int kMmaWarp = 5;
+constexpr int kConvWarp0 = 6;
+constexpr int kClsWarps = kConvWarp0 + kConvWarps;          // 14
+constexpr int kClsThreads = kClsWarps * 32;                 // 448
+constexpr int kAStageBytes = kKBlocksPerGroup * kTileM * 128;  // 49152
+constexpr int kClsSmemBytes = 232448;                       // 227 KB opt-in maximum
+
+enum PredKind : int32_t { kLabelEq = HYDRO_PRED_LABEL_EQ, kHash = HYDRO_PRED_HASH, kLinear = HYDRO_PRED_LINEAR };
+
+struct PredDev {
+  int32_t kind;
+  int32_t label_value;
+  uint64_t seed;
+  uint64_t thr0, thr1;
+  uint64_t drift_id;
+  int32_t units, units_per_area;
+  const uint8_t* w_tiled;   // LINEAR: [192 kblk][n_pad rows][128 B SW128-swizzled]
+  const float* bias;        // [n_pad] (padding rows: -inf never wins; they are skipped anyway)
+  int32_t n_classes, n_pad, target, crop_mode;
+};
+
+// Device-resident eddy state (one per context).  d_* are the atomically accumulated deltas of
+// the running batch; pend_* the deltas waiting for the next fold (multi-GPU: all-reduced).
+struct DevState {
+  int32_t n_pred;
+  int32_t policy;
+  int32_t cost_source;
+  int32_t pad0;
+  double gamma;
+  double prior;
+  int32_t kind[kMaxPred];
+  int32_t order[kMaxPred];
+  int32_t position[kMaxPred];
+  double declared_cost[kMaxPred];
+  double declared_sel[kMaxPred];
+  double cost_norm[kMaxPred];         // raw cycles -> SM-cycles
+  unsigned long long d_in[kMaxPred], d_pass[kMaxPred], d_cost[kMaxPred];
+  unsigned long long pend[3 * kMaxPred];   // in[8], pass[8], cost[8]  (NCCL all-reduce buffer)
+  unsigned long long tot_in[kMaxPred], tot_pass[kMaxPred];
+  double tot_cost[kMaxPred];
+  double s_in[kMaxPred], s_pass[kMaxPred], s_cost[kMaxPred];
+  double sel[kMaxPred], cost[kMaxPred], key[kMaxPred];
+  unsigned int k1_tile_ctr, k1_done_ctr;
+};
+
+struct BatchRec {
+  unsigned int warm_count;    // survivors of the warmup slice (written first in the output)
+  unsigned int total_count;   // all survivors of the batch
+  int32_t order_used[kMaxPred];
+  unsigned long long d_in[kMaxPred], d_pass[kMaxPred], d_cost[kMaxPred];
+};
+
+enum OutMode : int32_t { kOutList = 0, kOutEmit = 1, kOutBitmap = 2 };
+
+struct RouteParams {
+  // ---- input positions: RANGE (list_in == nullptr): idx = range_base + p, p < range_n;
+  //      LIST: idx = list_in[p], p < *count_in
+  const uint32_t* list_in;
+  const uint32_t* count_in;
+  uint32_t range_base, range_n;
+  const uint32_t* and_bits[kMaxPred];  // verdict bitmaps (bit p) ANDed into the alive mask
+  int32_t n_and;
+  // ---- which predicates: dispatch (device order) or explicit
+  int32_t dispatch;   // 1: hop = `hop`, decide on device from order[]; 0: explicit below
+  int32_t hop;
+  int32_t explicit_pred;  // dispatch == 0: -1 = none, else evaluate this single predicate
+  // ---- hop-indexed workspace (dispatch mode)
+  uint32_t* lists;        // list h at lists + h * list_stride  (h = 1..P)
+  uint64_t list_stride;
+  uint32_t* counts;       // counts[h]
+  uint32_t* bits;         // K4 verdicts of hop h at bits + h * bits_stride
+  uint64_t bits_stride;
+  // ---- output (explicit mode, or dispatch EMIT)
+  int32_t out_mode;
+  uint32_t* list_out;
+  uint32_t* count_out;
+  uint32_t* bitmap_out;
+  uint64_t* out_ids;
+  uint64_t* out_bbox;
+  uint32_t* emit_count;          // EMIT: *emit_count = *emit_offset + survivors
+  const uint32_t* emit_offset;   // nullable
+  // ---- columns
+  const uint64_t* id;
+  const uint32_t* frame_id;
+  const uint64_t* bbox;          // 4 x u16 packed
+  const uint16_t* label;
+  // ---- state
+  DevState* st;
+  const PredDev* preds;
+  unsigned long long* lb_status;
+  uint32_t epoch;
+  int32_t collect_stats;
+};
+
+struct ClsParams {
+  int32_t dispatch;       // 1: hop from device order; 0: explicit_pred
+  int32_t hop;
+  int32_t explicit_pred;
+  const uint32_t* list_in;    // explicit mode input (nullptr: range)
+  const uint32_t* count_in;
+  uint32_t range_base, range_n;
+  uint32_t* lists;
+  uint64_t list_stride;
+  uint32_t* counts;
+  uint32_t* bits;
+  uint64_t bits_stride;
+  uint32_t* bits_out;         // explicit mode output bitmap
+  const uint32_t* frame_id;
+  const uint64_t* bbox;
+  const uint8_t* frames;
+  int32_t n_frames, frame_h, frame_w;
+  DevState* st;
+  const PredDev* preds;
+  float* dbg_logits;      // [pos][n_classes]
+  uint16_t* dbg_crops;    // [pos][12288]
+  uint8_t* dbg_verdict;   // [pos]
+  int32_t collect_stats;
+};
+
+// ------------------------------------------------------------------------------------------
+// device helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// async proxy / TMA bulk copy (1D) global -> shared, completion on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// tcgen05
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t smem_addr) {
+  // SM100 shared-memory matrix descriptor, K-major, 128B swizzle:
+  // start>>4 [0,14) | LBO=1 (16 B) [16,30) | SBO=1024>>4 [32,46) | version 1 [46,48) | layout 2 [61,64)
+  return static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(2) << 61);
+}
+
+__device__ __forceinline__ uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
+  // kind::f16 instruction descriptor: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
+  // K-major A/B (bits 15,16 = 0), N>>3 [17,23), M>>4 [24,29)
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+__device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 lanes x 32 bit, 16 consecutive columns per thread
+__device__ __forceinline__ void tc_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ---- method arithmetic on device (independent of oracle/, written from DESIGN.md R5)
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  return h ^ (h >> 16);
+}
+
+}  // namespace hydro
+
+// kernels (defined in k_route.cu / k_classifier.cu), launched by runtime.cu
+__global__ void hydro_route_kernel(hydro::RouteParams p);
+__global__ void hydro_classifier_kernel(hydro::ClsParams p);
+__global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode);
+__global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad);

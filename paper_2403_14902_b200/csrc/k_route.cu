@@ -1,0 +1,431 @@
+// K1: route / filter / compact kernel, K5: statistics fold + rank + order, weight re-layout.
+//
+// K1 evaluates a maximal run of cheap predicates (LABEL_EQ, HASH) in the device-resident order
+// on the still-alive positions of a routing batch, drops failing tuples at once (eager
+// materialization) with an order-preserving single-pass compaction
+// (warp ballot/popc + block scan + decoupled look-back across tiles), and accumulates the
+// per-predicate in / pass / cycle counters the eddy folds.
+// It also applies the verdict bitmap left by a classifier hop (K4), and emits the final
+// (id, bbox) rows (the query's projection).
+//
+// K5 folds the counters: S <- gamma*S + delta (R4), s = S_pass/S_in,
+// c = S_cost/S_in, key = c/(1-s), stable order by (key, id)
+// (R1, R2).
+#include "hydro_internal.cuh"
+
+using namespace hydro;
+
+namespace {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr uint32_t kFlagAgg = 1, kFlagIncl = 2;
+
+__device__ __forceinline__ unsigned long long lb_pack(uint32_t epoch, uint32_t flag, uint32_t v) {
+  return (static_cast<unsigned long long>(epoch) << 32) | (static_cast<unsigned long long>(flag) << 30) |
+         static_cast<unsigned long long>(v & 0x3FFFFFFFu);
+}
+
+// Decoupled look-back (single-pass scan): publishes this tile's count, returns the number of
+// survivors of all earlier tiles.  Tiles are claimed in increasing order from an atomic
+// counter, so every predecessor is owned by a running CTA (no deadlock).
+__device__ uint32_t lookback_prefix(unsigned long long* status, uint32_t t, uint32_t total, uint32_t epoch) {
+  if (t == 0) {
+    st_release_u64(&status[0], lb_pack(epoch, kFlagIncl, total));
+    return 0;
+  }
+  st_release_u64(&status[t], lb_pack(epoch, kFlagAgg, total));
+  uint32_t prefix = 0;
+  int j = static_cast<int>(t) - 1;
+  while (true) {
+    unsigned long long v = ld_acquire_u64(&status[j]);
+    uint32_t e = static_cast<uint32_t>(v >> 32);
+    uint32_t flag = static_cast<uint32_t>(v >> 30) & 3u;
+    if (e != epoch || flag == 0) {
+      __nanosleep(20);
+      continue;
+    }
+    prefix += static_cast<uint32_t>(v & 0x3FFFFFFFu);
+    if (flag == kFlagIncl) break;
+    --j;
+  }
+  st_release_u64(&status[t], lb_pack(epoch, kFlagIncl, prefix + total));
+  return prefix;
+}
+
+__device__ __forceinline__ bool hash_pass(const PredDev& pd, uint64_t id, uint64_t bb) {
+  int units = pd.units;
+  if (pd.units_per_area > 0) {
+    int w = static_cast<int>((bb >> 32) & 0xFFFF) - static_cast<int>(bb & 0xFFFF);
+    int h = static_cast<int>((bb >> 48) & 0xFFFF) - static_cast<int>((bb >> 16) & 0xFFFF);
+    int area = max(w, 1) * max(h, 1);
+    units = max((area + pd.units_per_area - 1) / pd.units_per_area, 1);
+  }
+  uint32_t h = static_cast<uint32_t>(splitmix64(id ^ pd.seed) >> 32);
+  for (int r = 0; r < units; ++r) h = fmix32(h + static_cast<uint32_t>(r));
+  uint64_t T = (id >= pd.drift_id) ? pd.thr1 : pd.thr0;
+  return static_cast<uint64_t>(h) < T;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams p) {
+  __shared__ PredDev s_pred[kMaxPred];
+  __shared__ int32_t s_run_id[kMaxPred];
+  __shared__ unsigned long long s_in[kMaxPred], s_pass[kMaxPred], s_cost[kMaxPred];
+  __shared__ uint32_t s_warp_tot[kRouteThreads / 32], s_warp_excl[kRouteThreads / 32];
+  __shared__ uint32_t s_tile, s_prefix, s_emit_off;
+  __shared__ int32_t s_work, s_nrun, s_out_mode, s_n_and;
+  __shared__ const uint32_t* s_list_in;
+  __shared__ const uint32_t* s_and[kMaxPred];
+  __shared__ uint32_t s_count, s_range_base;
+  __shared__ uint32_t* s_list_out;
+  __shared__ uint32_t* s_count_out;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  DevState* st = p.st;
+
+  if (tid == 0) {
+    int32_t work = 1, nrun = 0, out_mode = p.out_mode, n_and = 0;
+    const uint32_t* list_in = p.list_in;
+    uint32_t count = 0, base = p.range_base;
+    uint32_t* list_out = p.list_out;
+    uint32_t* count_out = p.count_out;
+    if (p.dispatch) {
+      const int P = st->n_pred, h = p.hop;
+      if (h == 0) {
+        work = (P == 0) || (st->kind[st->order[0]] != kLinear);
+      } else {
+        work = (h <= P) && (st->kind[st->order[h - 1]] == kLinear);
+      }
+      if (work) {
+        // input of this launch = input of hop (h-1) filtered by its bitmap, or the range (h = 0)
+        const int in_h = (h == 0) ? 0 : h - 1;
+        if (in_h == 0) {
+          list_in = nullptr;
+          count = p.range_n;
+        } else {
+          list_in = p.lists + static_cast<uint64_t>(in_h) * p.list_stride;
+          count = p.counts[in_h];
+        }
+        if (h > 0) {
+          s_and[0] = p.bits + static_cast<uint64_t>(h - 1) * p.bits_stride;
+          n_and = 1;
+        }
+        while (h + nrun < P && st->kind[st->order[h + nrun]] != kLinear) {
+          s_run_id[nrun] = st->order[h + nrun];
+          ++nrun;
+        }
+        if (h + nrun >= P) {
+          out_mode = kOutEmit;
+        } else {
+          out_mode = kOutList;
+          list_out = p.lists + static_cast<uint64_t>(h + nrun) * p.list_stride;
+          count_out = p.counts + (h + nrun);
+        }
+      }
+    } else {
+      count = list_in ? *p.count_in : p.range_n;
+      n_and = p.n_and;
+      for (int a = 0; a < n_and; ++a) s_and[a] = p.and_bits[a];
+      if (p.explicit_pred >= 0) {
+        s_run_id[0] = p.explicit_pred;
+        nrun = 1;
+      }
+    }
+    s_work = work;
+    s_nrun = nrun;
+    s_out_mode = out_mode;
+    s_n_and = n_and;
+    s_list_in = list_in;
+    s_count = count;
+    s_range_base = base;
+    s_list_out = list_out;
+    s_count_out = count_out;
+    s_emit_off = (out_mode == kOutEmit && p.emit_offset) ? *p.emit_offset : 0u;
+  }
+  __syncthreads();
+  if (!s_work) return;
+  const int nrun = s_nrun;
+  if (tid < nrun) {
+    s_pred[tid] = p.preds[s_run_id[tid]];
+    s_in[tid] = 0;
+    s_pass[tid] = 0;
+    s_cost[tid] = 0;
+  }
+  const uint32_t count = s_count;
+  const uint32_t num_tiles = (count + kRouteTile - 1) / kRouteTile;
+  const int out_mode = s_out_mode;
+  const int n_and = s_n_and;
+  const uint32_t* list_in = s_list_in;
+  const uint32_t base = s_range_base;
+  if (num_tiles == 0 && blockIdx.x == 0 && tid == 0) {
+    if (out_mode == kOutEmit) *p.emit_count = s_emit_off;
+    else if (out_mode == kOutList) *s_count_out = 0;
+  }
+  __syncthreads();
+
+  for (;;) {
+    if (tid == 0) s_tile = atomicAdd(&st->k1_tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t t = s_tile;
+    if (t >= num_tiles) break;
+    const uint32_t p0 = t * kRouteTile + tid * kRouteItems;
+    uint32_t idx[kRouteItems];
+    uint32_t mask = 0;
+    if (list_in) {
+      if (p0 + kRouteItems <= count) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(list_in + p0));
+        const uint4 b = __ldg(reinterpret_cast<const uint4*>(list_in + p0 + 4));
+        idx[0] = a.x; idx[1] = a.y; idx[2] = a.z; idx[3] = a.w;
+        idx[4] = b.x; idx[5] = b.y; idx[6] = b.z; idx[7] = b.w;
+        mask = 0xFFu;
+      } else {
+#pragma unroll
+        for (int j = 0; j < kRouteItems; ++j) {
+          idx[j] = 0;
+          if (p0 + j < count) {
+            idx[j] = __ldg(list_in + p0 + j);
+            mask |= 1u << j;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kRouteItems; ++j) {
+        idx[j] = base + p0 + j;
+        if (p0 + j < count) mask |= 1u << j;
+      }
+    }
+    for (int a = 0; a < n_and; ++a) {
+      if (mask) mask &= (__ldg(s_and[a] + (p0 >> 5)) >> (p0 & 31)) & 0xFFu;
+    }
+    const bool contiguous = (list_in == nullptr) && (mask == 0xFFu) && (((base + p0) & 7u) == 0);
+
+    for (int r = 0; r < nrun; ++r) {
+      const PredDev& pd = s_pred[r];
+      const long long t0 = clock64();
+      const uint32_t in_mask = mask;
+      if (mask) {
+        if (pd.kind == kLabelEq) {
+          const uint16_t want = static_cast<uint16_t>(pd.label_value);
+          if (contiguous && ((reinterpret_cast<uintptr_t>(p.label + base + p0) & 15u) == 0)) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.label + base + p0));
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < kRouteItems; ++j) {
+              const uint16_t l = static_cast<uint16_t>(w[j >> 1] >> (16 * (j & 1)));
+              if (l != want) mask &= ~(1u << j);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < kRouteItems; ++j)
+              if ((mask >> j) & 1u)
+                if (__ldg(p.label + idx[j]) != want) mask &= ~(1u << j);
+          }
+        } else {  // kHash
+          uint64_t ids[kRouteItems];
+          if (contiguous && ((reinterpret_cast<uintptr_t>(p.id + base + p0) & 15u) == 0)) {
+            const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p.id + base + p0);
+#pragma unroll
+            for (int j = 0; j < kRouteItems / 2; ++j) {
+              const ulonglong2 v = __ldg(q + j);
+              ids[2 * j] = v.x;
+              ids[2 * j + 1] = v.y;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < kRouteItems; ++j) ids[j] = ((mask >> j) & 1u) ? __ldg(p.id + idx[j]) : 0ull;
+          }
+#pragma unroll
+          for (int j = 0; j < kRouteItems; ++j) {
+            if ((mask >> j) & 1u) {
+              const uint64_t bb = pd.units_per_area > 0 ? __ldg(p.bbox + idx[j]) : 0ull;
+              if (!hash_pass(pd, ids[j], bb)) mask &= ~(1u << j);
+            }
+          }
+        }
+      }
+      const long long t1 = clock64();
+      if (p.collect_stats) {
+        const uint32_t ci = __reduce_add_sync(kFull, __popc(in_mask));
+        const uint32_t cp = __reduce_add_sync(kFull, __popc(mask));
+        if (lane == 0) {
+          atomicAdd(&s_in[r], static_cast<unsigned long long>(ci));
+          atomicAdd(&s_pass[r], static_cast<unsigned long long>(cp));
+          atomicAdd(&s_cost[r], static_cast<unsigned long long>(t1 - t0));
+        }
+      }
+    }
+
+    if (out_mode == kOutBitmap) {
+      uint32_t b = mask << (8 * (lane & 3));
+      b |= __shfl_xor_sync(kFull, b, 1);
+      b |= __shfl_xor_sync(kFull, b, 2);
+      if ((lane & 3) == 0 && p0 < count) p.bitmap_out[p0 >> 5] = b;
+      __syncthreads();  // s_tile reuse
+      continue;
+    }
+
+    // ---- order-preserving compaction: warp scan -> block scan -> decoupled look-back
+    const uint32_t c = __popc(mask);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp_tot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t v = lane < kRouteThreads / 32 ? s_warp_tot[lane] : 0u;
+      uint32_t s = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, s, o);
+        if (lane >= o) s += y;
+      }
+      if (lane < kRouteThreads / 32) s_warp_excl[lane] = s - v;
+      const uint32_t tile_total = __shfl_sync(kFull, s, kRouteThreads / 32 - 1);
+      if (lane == 0) {
+        const uint32_t prefix = lookback_prefix(p.lb_status, t, tile_total, p.epoch);
+        s_prefix = prefix;
+        if (t == num_tiles - 1) {
+          if (out_mode == kOutEmit) *p.emit_count = s_emit_off + prefix + tile_total;
+          else *s_count_out = prefix + tile_total;
+        }
+      }
+    }
+    __syncthreads();
+    uint32_t pos = s_prefix + s_warp_excl[warp] + (x - c);
+    if (out_mode == kOutList) {
+      uint32_t* out = s_list_out;
+#pragma unroll
+      for (int j = 0; j < kRouteItems; ++j)
+        if ((mask >> j) & 1u) out[pos++] = idx[j];
+    } else {  // emit (id, bbox)
+      pos += s_emit_off;
+#pragma unroll
+      for (int j = 0; j < kRouteItems; ++j) {
+        if ((mask >> j) & 1u) {
+          p.out_ids[pos] = __ldg(p.id + idx[j]);
+          p.out_bbox[pos] = __ldg(p.bbox + idx[j]);
+          ++pos;
+        }
+      }
+    }
+    __syncthreads();  // s_tile / s_prefix / s_warp_* reuse
+  }
+
+  __syncthreads();
+  if (p.collect_stats && tid < nrun) {
+    const int k = s_run_id[tid];
+    atomicAdd(&st->d_in[k], s_in[tid]);
+    atomicAdd(&st->d_pass[k], s_pass[tid]);
+    atomicAdd(&st->d_cost[k], s_cost[tid]);
+  }
+  if (tid == 0) {
+    __threadfence();
+    const uint32_t prev = atomicAdd(&st->k1_done_ctr, 1u);
+    if (prev == gridDim.x - 1) {  // last CTA: self-reset the tile counters for the next launch
+      st->k1_tile_ctr = 0;
+      st->k1_done_ctr = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K5: fold.  mode bit 0 = PREP (deltas -> batch record + pending), bit 1 = APPLY (pending ->
+// decayed statistics -> keys -> order), bit 2 = RECORD (order used by this batch's chain).
+
+__device__ __forceinline__ double policy_key(int policy, double c, double s) {
+  if (policy == HYDRO_POLICY_COST) return c;
+  if (policy == HYDRO_POLICY_SELECTIVITY) return s;
+  if (c == 0.0) return 0.0;                      // R1
+  if (s >= 1.0) return __longlong_as_double(0x7FF0000000000000ll);  // +inf (R1)
+  return c / (1.0 - s);
+}
+
+__global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int P = st->n_pred;
+  if (mode & 4) {
+    for (int k = 0; k < kMaxPred; ++k) rec->order_used[k] = k < P ? st->order[k] : -1;
+  }
+  if (mode & 1) {
+    for (int k = 0; k < P; ++k) {
+      const unsigned long long di = st->d_in[k], dp = st->d_pass[k], dc = st->d_cost[k];
+      rec->d_in[k] += di;
+      rec->d_pass[k] += dp;
+      rec->d_cost[k] += dc;
+      st->pend[k] += di;
+      st->pend[kMaxPred + k] += dp;
+      st->pend[2 * kMaxPred + k] += dc;
+      st->tot_in[k] += di;
+      st->tot_pass[k] += dp;
+      st->tot_cost[k] += static_cast<double>(dc);
+      st->d_in[k] = st->d_pass[k] = st->d_cost[k] = 0;
+    }
+  }
+  if (mode & 2) {
+    const double g = st->gamma;
+    for (int k = 0; k < P; ++k) {
+      const unsigned long long di = st->pend[k];
+      if (di > 0) {  // R4: fold only observed predicates
+        st->s_in[k] = g * st->s_in[k] + static_cast<double>(di);
+        st->s_pass[k] = g * st->s_pass[k] + static_cast<double>(st->pend[kMaxPred + k]);
+        st->s_cost[k] = g * st->s_cost[k] + static_cast<double>(st->pend[2 * kMaxPred + k]) * st->cost_norm[k];
+      }
+      st->pend[k] = st->pend[kMaxPred + k] = st->pend[2 * kMaxPred + k] = 0;
+    }
+    for (int k = 0; k < P; ++k) {
+      double s, c;
+      if (st->policy == HYDRO_POLICY_STATIC) {
+        s = st->declared_sel[k];
+        c = st->declared_cost[k];
+      } else {
+        s = st->s_in[k] > 0.0 ? st->s_pass[k] / st->s_in[k] : st->prior;  // PAPER.md:416, R3
+        c = (st->cost_source == HYDRO_COST_DECLARED || st->s_in[k] <= 0.0) ? st->declared_cost[k]
+                                                                             : st->s_cost[k] / st->s_in[k];
+      }
+      st->sel[k] = s;
+      st->cost[k] = c;
+      st->key[k] = policy_key(st->policy, c, s);
+    }
+    if (st->policy != HYDRO_POLICY_FIXED_ORDER) {
+      int ord[kMaxPred];
+      for (int k = 0; k < P; ++k) ord[k] = k;
+      for (int i = 1; i < P; ++i) {  // stable insertion sort by (key, id): R2
+        const int v = ord[i];
+        int j = i - 1;
+        while (j >= 0 && st->key[ord[j]] > st->key[v]) {
+          ord[j + 1] = ord[j];
+          --j;
+        }
+        ord[j + 1] = v;
+      }
+      for (int i = 0; i < P; ++i) st->order[i] = ord[i];
+    }
+    for (int i = 0; i < P; ++i) st->position[st->order[i]] = i;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Weight re-layout: W[C][12288] bf16 row-major -> [192 K-blocks][n_pad rows][128 B] with the
+// 128-byte swizzle applied (16-byte chunk c of row n stored at chunk c ^ (n & 7)), i.e. the exact
+// shared-memory image UMMA reads, so one 1-D bulk copy per stage lands it.  Rows >= C are 0.
+__global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad) {
+  const uint64_t total = static_cast<uint64_t>(kNumKBlocks) * n_pad * 8;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t c = static_cast<uint32_t>(i & 7);
+    const uint64_t rowi = i >> 3;
+    const uint32_t n = static_cast<uint32_t>(rowi % n_pad);
+    const uint32_t kb = static_cast<uint32_t>(rowi / n_pad);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (static_cast<int32_t>(n) < n_classes)
+      v = *reinterpret_cast<const uint4*>(w + static_cast<uint64_t>(n) * kFeatures + kb * kKBlock + c * 8);
+    uint8_t* dst = w_tiled + (static_cast<uint64_t>(kb) * n_pad + n) * 128 + ((c ^ (n & 7)) << 4);
+    *reinterpret_cast<uint4*>(dst) = v;
+  }
+}

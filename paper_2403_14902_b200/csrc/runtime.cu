@@ -1,0 +1,831 @@
+// libhydro host runtime: the C ABI of include/hydro.h.
+//
+// Per routing batch the runtime enqueues a FIXED launch skeleton on the
+// context stream; which predicate each hop evaluates is decided on the device from the order
+// the previous fold wrote (no host synchronisation inside a batch):
+//   [first batch] warmup slice: every predicate on the slice (bitmaps) -> AND + emit -> fold
+//   for hop h = 0 .. P-1:   K1(h)  route/compact (cheap predicates, bitmap of hop h-1)
+//                           K4(h)  classifier hop (exits unless order[h] is LINEAR)
+//   K1(P)   final compaction + emit of (id, bbox) in input order
+//   K5      fold (+ NCCL all-reduce of the deltas when world > 1)
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "hydro_internal.cuh"
+
+using namespace hydro;
+
+static thread_local std::string g_last_error;
+
+static hydro_status set_err(hydro_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+#define CU(expr)                                                                                   \
+  do {                                                                                             \
+    cudaError_t _e = (expr);                                                                       \
+    if (_e != cudaSuccess) {                                                                       \
+      return ctx_fail(ctx, HYDRO_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));       \
+    }                                                                                              \
+  } while (0)
+
+namespace {
+
+struct PredHost {
+  hydro_predicate_desc desc;
+  uint8_t* w_tiled = nullptr;
+  float* bias = nullptr;
+  int n_pad = 0;
+};
+
+struct Slot {
+  bool busy = false;
+  int64_t batch_id = -1;
+  int64_t n = 0;
+  int64_t warm_n = 0;
+  cudaEvent_t done = nullptr;
+  uint64_t* out_ids = nullptr;
+  uint64_t* out_bbox = nullptr;
+  BatchRec* rec = nullptr;
+  BatchRec rec_host{};
+  bool rec_valid = false;
+  // staging for host input
+  uint64_t* s_id = nullptr;
+  uint32_t* s_frame = nullptr;
+  uint64_t* s_bbox = nullptr;
+  uint16_t* s_label = nullptr;
+};
+
+struct TimedLaunch {
+  cudaEvent_t a, b;
+  int kind;
+};
+
+}  // namespace
+
+struct hydro_ctx {
+  hydro_config cfg{};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 0;
+  int k1_occ = 1;
+  std::vector<PredHost> preds;
+  bool frozen = false;
+  bool warmup_pending = true;
+  hydro_status sticky = HYDRO_OK;
+  std::string sticky_msg;
+  // device state
+  DevState* st = nullptr;
+  PredDev* preds_dev = nullptr;
+  uint32_t* lists = nullptr;
+  uint64_t list_stride = 0;
+  uint32_t* counts = nullptr;
+  uint32_t* bits = nullptr;
+  uint64_t bits_stride = 0;
+  uint32_t* warm_bits = nullptr;
+  unsigned long long* lb_status = nullptr;
+  uint32_t* zero_word = nullptr;
+  std::vector<Slot> slots;
+  int64_t next_batch = 0;
+  uint32_t epoch = 1;
+  int64_t launches = 0;
+  int64_t since_sync = 0;
+  ncclComm_t comm = nullptr;
+  int32_t fixed_order[kMaxPred];
+  bool fixed_order_set = false;
+  // timing
+  bool timing = false;
+  std::vector<TimedLaunch> timed;
+  std::vector<cudaEvent_t> event_pool;
+};
+
+static hydro_status ctx_fail(hydro_ctx* ctx, hydro_status s, const std::string& msg) {
+  if (ctx && (s == HYDRO_ECUDA || s == HYDRO_ENCCL) && ctx->sticky == HYDRO_OK) {
+    ctx->sticky = s;
+    ctx->sticky_msg = msg;
+  }
+  return set_err(s, msg);
+}
+
+static hydro_status check_sticky(hydro_ctx* ctx) {
+  if (ctx->sticky != HYDRO_OK) return set_err(ctx->sticky, ctx->sticky_msg);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ctx_fail(ctx, HYDRO_ECUDA, std::string("async CUDA error: ") + cudaGetErrorString(e));
+  return HYDRO_OK;
+}
+
+static cudaEvent_t get_event(hydro_ctx* ctx) {
+  if (!ctx->event_pool.empty()) {
+    cudaEvent_t e = ctx->event_pool.back();
+    ctx->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+template <typename F>
+static hydro_status timed_launch(hydro_ctx* ctx, int kind, F&& launch) {
+  TimedLaunch tl{};
+  if (ctx->timing) {
+    tl.a = get_event(ctx);
+    tl.b = get_event(ctx);
+    tl.kind = kind;
+    cudaEventRecord(tl.a, ctx->stream);
+  }
+  launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return ctx_fail(ctx, HYDRO_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  ctx->launches += 1;
+  if (ctx->timing) {
+    cudaEventRecord(tl.b, ctx->stream);
+    ctx->timed.push_back(tl);
+  }
+  return HYDRO_OK;
+}
+
+static int next_pow2_pad(int c) {  // n_pad: multiple of 16 >= c
+  return ((c + 15) / 16) * 16;
+}
+
+// ------------------------------------------------------------------------------------------
+
+extern "C" {
+
+const char* hydro_version(void) { return "hydro-b200 0.1 (sm_100a)"; }
+const char* hydro_last_error(void) { return g_last_error.c_str(); }
+
+hydro_status hydro_config_default(hydro_config* cfg) {
+  if (!cfg) return set_err(HYDRO_EINVAL, "cfg is NULL");
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->device = 0;
+  cfg->stream = nullptr;
+  cfg->policy = HYDRO_POLICY_SCORE;
+  cfg->cost_source = HYDRO_COST_MEASURED;
+  cfg->decay_gamma = 0.5;
+  cfg->prior_selectivity = 0.5;
+  cfg->warmup_tuples = 65536;
+  cfg->max_batch_tuples = 1 << 20;
+  cfg->max_inflight = 4;
+  cfg->rank = 0;
+  cfg->world = 1;
+  cfg->sync_every = 1;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_nccl_unique_id(void* out128) {
+  if (!out128) return set_err(HYDRO_EINVAL, "out128 is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return set_err(HYDRO_ENCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  std::memcpy(out128, &id, 128);
+  return HYDRO_OK;
+}
+
+hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
+  if (!cfg || !out) return set_err(HYDRO_EINVAL, "NULL argument");
+  hydro_ctx* ctx = nullptr;
+  if (cfg->max_batch_tuples < 1 || cfg->max_batch_tuples > (1 << 30))
+    return set_err(HYDRO_EINVAL, "max_batch_tuples must be in [1, 2^30]");
+  if (cfg->max_inflight < 1 || cfg->max_inflight > 64) return set_err(HYDRO_EINVAL, "max_inflight in [1, 64]");
+  if (!(cfg->decay_gamma > 0.0 && cfg->decay_gamma <= 1.0)) return set_err(HYDRO_EINVAL, "decay_gamma in (0, 1]");
+  if (!(cfg->prior_selectivity >= 0.0 && cfg->prior_selectivity <= 1.0))
+    return set_err(HYDRO_EINVAL, "prior_selectivity in [0, 1]");
+  if (cfg->policy < 0 || cfg->policy > 4) return set_err(HYDRO_EINVAL, "unknown policy");
+  if (cfg->cost_source < 0 || cfg->cost_source > 1) return set_err(HYDRO_EINVAL, "unknown cost_source");
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return set_err(HYDRO_EINVAL, "bad rank/world");
+  if (cfg->world > 1 && !cfg->nccl_unique_id) return set_err(HYDRO_EINVAL, "world > 1 needs nccl_unique_id");
+  if (cfg->sync_every < 1) return set_err(HYDRO_EINVAL, "sync_every >= 1");
+  if (cfg->frames) {
+    if (cfg->n_frames < 1 || cfg->frame_h < 1 || cfg->frame_w < 1 || (cfg->frame_w % 4) != 0 ||
+        cfg->frame_h > 65535 || cfg->frame_w > 65535)
+      return set_err(HYDRO_EINVAL, "frame pool: n_frames, frame_h >= 1; frame_w % 4 == 0; dims <= 65535");
+    if (static_cast<double>(cfg->n_frames) * cfg->frame_h * cfg->frame_w * 3 >= 4294967296.0)
+      return set_err(HYDRO_EINVAL, "frame pool must be < 4 GiB");
+  }
+  ctx = new hydro_ctx();
+  ctx->cfg = *cfg;
+  CU(cudaSetDevice(cfg->device));
+  CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+  if (cfg->stream) {
+    ctx->stream = static_cast<cudaStream_t>(cfg->stream);
+  } else {
+    CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->k1_occ, hydro_route_kernel, kRouteThreads, 0));
+  if (ctx->k1_occ < 1) ctx->k1_occ = 1;
+  CU(cudaFuncSetAttribute(hydro_classifier_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
+  CU(cudaMalloc(&ctx->st, sizeof(DevState)));
+  CU(cudaMemset(ctx->st, 0, sizeof(DevState)));
+  CU(cudaMalloc(&ctx->preds_dev, sizeof(PredDev) * kMaxPred));
+  CU(cudaMalloc(&ctx->zero_word, 16));
+  CU(cudaMemset(ctx->zero_word, 0, 16));
+  if (cfg->world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank);
+    if (r != ncclSuccess) {
+      hydro_status s = set_err(HYDRO_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      hydro_destroy(ctx);
+      return s;
+    }
+  }
+  ctx->warmup_pending = (cfg->warmup_tuples > 0) && (cfg->policy == HYDRO_POLICY_SCORE ||
+                                                     cfg->policy == HYDRO_POLICY_COST ||
+                                                     cfg->policy == HYDRO_POLICY_SELECTIVITY);
+  *out = ctx;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, int32_t* pred_id) {
+  if (!ctx || !d) return set_err(HYDRO_EINVAL, "NULL argument");
+  if (ctx->frozen) return set_err(HYDRO_ESTATE, "add_predicate after the first submit");
+  if (static_cast<int>(ctx->preds.size()) >= kMaxPred) return set_err(HYDRO_EINVAL, "too many predicates (max 8)");
+  if (!(d->declared_cost >= 0.0) || !(d->declared_selectivity >= 0.0 && d->declared_selectivity <= 1.0))
+    return set_err(HYDRO_EINVAL, "declared_cost >= 0, declared_selectivity in [0, 1]");
+  PredHost ph;
+  ph.desc = *d;
+  if (d->kind == HYDRO_PRED_LABEL_EQ) {
+    if (d->label_value < 0 || d->label_value > 65535) return set_err(HYDRO_EINVAL, "label_value out of u16 range");
+  } else if (d->kind == HYDRO_PRED_HASH) {
+    if (d->threshold[0] > (1ull << 32) || d->threshold[1] > (1ull << 32))
+      return set_err(HYDRO_EINVAL, "threshold must be <= 2^32");
+    if (d->units < 0 || d->units_per_area < 0) return set_err(HYDRO_EINVAL, "units must be >= 0");
+  } else if (d->kind == HYDRO_PRED_LINEAR) {
+    if (!ctx->cfg.frames) return set_err(HYDRO_EINVAL, "LINEAR predicate needs the frame pool in hydro_config");
+    if (d->n_classes < 2 || d->n_classes > HYDRO_MAX_CLASSES) return set_err(HYDRO_EINVAL, "n_classes in [2, 128]");
+    if (d->target < 0 || d->target >= d->n_classes) return set_err(HYDRO_EINVAL, "target outside [0, n_classes)");
+    if (!d->weight_bf16 || !d->bias) return set_err(HYDRO_EINVAL, "LINEAR needs weight_bf16 and bias");
+    if (d->crop_mode != HYDRO_CROP_NEAREST)
+      return set_err(HYDRO_EINVAL, "crop_mode: only HYDRO_CROP_NEAREST is implemented in this build");
+    const int C = d->n_classes;
+    ph.n_pad = next_pow2_pad(C);
+    const size_t wbytes = static_cast<size_t>(C) * kFeatures * 2;
+    uint16_t* wdev = nullptr;
+    CU(cudaMalloc(&wdev, wbytes));
+    CU(cudaMemcpyAsync(wdev, d->weight_bf16, wbytes, d->weights_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaMalloc(&ph.w_tiled, static_cast<size_t>(kNumKBlocks) * ph.n_pad * 128));
+    CU(cudaMalloc(&ph.bias, sizeof(float) * HYDRO_MAX_CLASSES));
+    CU(cudaMemsetAsync(ph.bias, 0, sizeof(float) * HYDRO_MAX_CLASSES, ctx->stream));
+    CU(cudaMemcpyAsync(ph.bias, d->bias, sizeof(float) * C,
+                       d->weights_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, ph.w_tiled, C, ph.n_pad);
+    ctx->launches += 1;
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaFree(wdev));
+  } else {
+    return set_err(HYDRO_EINVAL, "unknown predicate kind");
+  }
+  ctx->preds.push_back(ph);
+  if (pred_id) *pred_id = static_cast<int32_t>(ctx->preds.size() - 1);
+  return HYDRO_OK;
+}
+
+hydro_status hydro_set_fixed_order(hydro_ctx* ctx, const int32_t* order, int32_t n) {
+  if (!ctx || !order) return set_err(HYDRO_EINVAL, "NULL argument");
+  const int P = static_cast<int>(ctx->preds.size());
+  if (n != P) return set_err(HYDRO_EINVAL, "order length != number of predicates");
+  std::vector<int> seen(P, 0);
+  for (int i = 0; i < P; ++i) {
+    if (order[i] < 0 || order[i] >= P || seen[order[i]]) return set_err(HYDRO_EINVAL, "order is not a permutation");
+    seen[order[i]] = 1;
+  }
+  for (int i = 0; i < P; ++i) ctx->fixed_order[i] = order[i];
+  ctx->fixed_order_set = true;
+  if (ctx->frozen) {  // update the device order in stream order
+    int32_t pos[kMaxPred];
+    for (int i = 0; i < P; ++i) pos[order[i]] = i;
+    CU(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, order), ctx->fixed_order, sizeof(int32_t) * P, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, position), pos, sizeof(int32_t) * P, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  return HYDRO_OK;
+}
+
+static hydro_status freeze(hydro_ctx* ctx) {
+  if (ctx->frozen) return HYDRO_OK;
+  const int P = static_cast<int>(ctx->preds.size());
+  const uint64_t maxb = static_cast<uint64_t>(ctx->cfg.max_batch_tuples);
+  // host-side initial state
+  DevState h{};
+  h.n_pred = P;
+  h.policy = ctx->cfg.policy;
+  h.cost_source = ctx->cfg.cost_source;
+  h.gamma = ctx->cfg.decay_gamma;
+  h.prior = ctx->cfg.prior_selectivity;
+  const double k1_norm = 1.0 / (static_cast<double>(ctx->k1_occ) * (kRouteThreads / 32));
+  std::vector<PredDev> pd(kMaxPred);
+  for (int k = 0; k < P; ++k) {
+    const hydro_predicate_desc& d = ctx->preds[k].desc;
+    h.kind[k] = d.kind;
+    h.declared_cost[k] = d.declared_cost;
+    h.declared_sel[k] = d.declared_selectivity;
+    h.cost_norm[k] = d.kind == HYDRO_PRED_LINEAR ? 1.0 : k1_norm;
+    PredDev& q = pd[k];
+    q.kind = d.kind;
+    q.label_value = d.label_value;
+    q.seed = d.seed;
+    q.thr0 = d.threshold[0];
+    q.thr1 = d.threshold[1];
+    q.drift_id = d.drift_id;
+    q.units = d.units;
+    q.units_per_area = d.units_per_area;
+    q.w_tiled = ctx->preds[k].w_tiled;
+    q.bias = ctx->preds[k].bias;
+    q.n_classes = d.n_classes;
+    q.n_pad = ctx->preds[k].n_pad;
+    q.target = d.target;
+    q.crop_mode = d.crop_mode;
+  }
+  // initial order: declared statistics (SCORE/COST/SEL before warmup; STATIC), or add order
+  for (int k = 0; k < P; ++k) {
+    double c = h.declared_cost[k], s = h.declared_sel[k];
+    double key;
+    if (h.policy == HYDRO_POLICY_COST) key = c;
+    else if (h.policy == HYDRO_POLICY_SELECTIVITY) key = s;
+    else key = (c == 0.0) ? 0.0 : (s >= 1.0 ? INFINITY : c / (1.0 - s));
+    h.key[k] = key;
+    h.sel[k] = s;
+    h.cost[k] = c;
+    h.order[k] = k;
+  }
+  if (h.policy == HYDRO_POLICY_FIXED_ORDER) {
+    if (ctx->fixed_order_set)
+      for (int i = 0; i < P; ++i) h.order[i] = ctx->fixed_order[i];
+  } else {
+    std::stable_sort(h.order, h.order + P, [&](int a, int b) { return h.key[a] < h.key[b]; });
+  }
+  for (int i = 0; i < P; ++i) h.position[h.order[i]] = i;
+  CU(cudaMemcpy(ctx->st, &h, sizeof(h), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->preds_dev, pd.data(), sizeof(PredDev) * kMaxPred, cudaMemcpyHostToDevice));
+  // workspace
+  ctx->list_stride = (maxb + 7) & ~7ull;
+  CU(cudaMalloc(&ctx->lists, sizeof(uint32_t) * ctx->list_stride * (P + 1)));
+  CU(cudaMalloc(&ctx->counts, sizeof(uint32_t) * (kMaxPred + 2)));
+  CU(cudaMemset(ctx->counts, 0, sizeof(uint32_t) * (kMaxPred + 2)));
+  ctx->bits_stride = ((maxb + 31) / 32 + 3) & ~3ull;
+  CU(cudaMalloc(&ctx->bits, sizeof(uint32_t) * ctx->bits_stride * std::max(P, 1)));
+  CU(cudaMalloc(&ctx->warm_bits, sizeof(uint32_t) * ctx->bits_stride * std::max(P, 1)));
+  const uint64_t max_tiles = (maxb + kRouteTile - 1) / kRouteTile + 1;
+  CU(cudaMalloc(&ctx->lb_status, sizeof(unsigned long long) * max_tiles));
+  CU(cudaMemset(ctx->lb_status, 0, sizeof(unsigned long long) * max_tiles));
+  ctx->slots.resize(ctx->cfg.max_inflight);
+  for (Slot& s : ctx->slots) {
+    CU(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    CU(cudaMalloc(&s.out_ids, sizeof(uint64_t) * maxb));
+    CU(cudaMalloc(&s.out_bbox, sizeof(uint64_t) * maxb));
+    CU(cudaMalloc(&s.rec, sizeof(BatchRec)));
+  }
+  ctx->frozen = true;
+  return HYDRO_OK;
+}
+
+static hydro_status ensure_staging(hydro_ctx* ctx, Slot& s) {
+  if (s.s_id) return HYDRO_OK;
+  const uint64_t maxb = static_cast<uint64_t>(ctx->cfg.max_batch_tuples);
+  CU(cudaMalloc(&s.s_id, sizeof(uint64_t) * maxb));
+  CU(cudaMalloc(&s.s_frame, sizeof(uint32_t) * maxb));
+  CU(cudaMalloc(&s.s_bbox, sizeof(uint64_t) * maxb));
+  CU(cudaMalloc(&s.s_label, sizeof(uint16_t) * maxb + 16));
+  return HYDRO_OK;
+}
+
+static RouteParams route_base(hydro_ctx* ctx, const uint64_t* id, const uint32_t* fr, const uint64_t* bb,
+                              const uint16_t* lab) {
+  RouteParams r{};
+  r.lists = ctx->lists;
+  r.list_stride = ctx->list_stride;
+  r.counts = ctx->counts;
+  r.bits = ctx->bits;
+  r.bits_stride = ctx->bits_stride;
+  r.id = id;
+  r.frame_id = fr;
+  r.bbox = bb;
+  r.label = lab;
+  r.st = ctx->st;
+  r.preds = ctx->preds_dev;
+  r.lb_status = ctx->lb_status;
+  r.collect_stats = 1;
+  r.explicit_pred = -1;
+  return r;
+}
+
+static ClsParams cls_base(hydro_ctx* ctx, const uint32_t* fr, const uint64_t* bb) {
+  ClsParams c{};
+  c.lists = ctx->lists;
+  c.list_stride = ctx->list_stride;
+  c.counts = ctx->counts;
+  c.bits = ctx->bits;
+  c.bits_stride = ctx->bits_stride;
+  c.frame_id = fr;
+  c.bbox = bb;
+  c.frames = ctx->cfg.frames;
+  c.n_frames = ctx->cfg.n_frames;
+  c.frame_h = ctx->cfg.frame_h;
+  c.frame_w = ctx->cfg.frame_w;
+  c.st = ctx->st;
+  c.preds = ctx->preds_dev;
+  c.collect_stats = 1;
+  c.explicit_pred = -1;
+  return c;
+}
+
+static int route_grid(hydro_ctx* ctx, uint64_t positions) {
+  const uint64_t tiles = (positions + kRouteTile - 1) / kRouteTile;
+  const uint64_t cap = static_cast<uint64_t>(ctx->num_sms) * ctx->k1_occ;
+  return static_cast<int>(std::max<uint64_t>(1, std::min(tiles, cap)));
+}
+
+static hydro_status launch_route(hydro_ctx* ctx, RouteParams r, uint64_t max_positions) {
+  r.epoch = ctx->epoch++;
+  if (ctx->epoch == 0) ctx->epoch = 1;
+  const int grid = route_grid(ctx, max_positions);
+  return timed_launch(ctx, 0, [&] { hydro_route_kernel<<<grid, kRouteThreads, 0, ctx->stream>>>(r); });
+}
+
+static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_positions) {
+  const uint64_t tiles = (max_positions + kTileM - 1) / kTileM;
+  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctx->num_sms)));
+  return timed_launch(ctx, 1, [&] {
+    hydro_classifier_kernel<<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
+  });
+}
+
+static hydro_status launch_fold(hydro_ctx* ctx, BatchRec* rec, int mode) {
+  return timed_launch(ctx, 2, [&] { hydro_fold_kernel<<<1, 32, 0, ctx->stream>>>(ctx->st, rec, mode); });
+}
+
+static hydro_status fold_and_sync(hydro_ctx* ctx, BatchRec* rec, int record, bool force_sync) {
+  hydro_status s;
+  if (ctx->cfg.world == 1) return launch_fold(ctx, rec, 1 | 2 | (record ? 4 : 0));
+  if ((s = launch_fold(ctx, rec, 1 | (record ? 4 : 0))) != HYDRO_OK) return s;
+  ctx->since_sync += record ? 1 : 0;
+  if (force_sync || ctx->since_sync >= ctx->cfg.sync_every) {
+    void* pend = reinterpret_cast<char*>(ctx->st) + offsetof(DevState, pend);
+    ncclResult_t r = ncclAllReduce(pend, pend, 3 * kMaxPred, ncclUint64, ncclSum, ctx->comm,
+                                   ctx->stream);
+    if (r != ncclSuccess) return ctx_fail(ctx, HYDRO_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+    ctx->since_sync = 0;
+    return launch_fold(ctx, rec, 2);
+  }
+  return HYDRO_OK;
+}
+
+static hydro_status validate_host_tuples(hydro_ctx* ctx, const hydro_tuples* t) {
+  const bool frames = ctx->cfg.frames != nullptr;
+  for (int64_t i = 0; i < t->n; ++i) {
+    const uint16_t* b = t->bbox + 4 * i;
+    if (!(b[0] < b[2] && b[1] < b[3])) return set_err(HYDRO_EINVAL, "bbox must satisfy x0 < x1 and y0 < y1");
+    if (frames) {
+      if (b[2] > ctx->cfg.frame_w || b[3] > ctx->cfg.frame_h) return set_err(HYDRO_EINVAL, "bbox outside the frame");
+      if (t->frame_id[i] >= static_cast<uint32_t>(ctx->cfg.n_frames))
+        return set_err(HYDRO_EINVAL, "frame_id >= n_frames");
+    }
+  }
+  return HYDRO_OK;
+}
+
+hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* batch_id) {
+  if (!ctx || !t) return set_err(HYDRO_EINVAL, "NULL argument");
+  hydro_status s = check_sticky(ctx);
+  if (s != HYDRO_OK) return s;
+  if (t->n < 0 || t->n > ctx->cfg.max_batch_tuples) return set_err(HYDRO_EINVAL, "n must be in [0, max_batch_tuples]");
+  if (t->n > 0 && (!t->id || !t->frame_id || !t->bbox || !t->label)) return set_err(HYDRO_EINVAL, "NULL column");
+  if ((s = freeze(ctx)) != HYDRO_OK) return s;
+  int si = -1;
+  for (int i = 0; i < static_cast<int>(ctx->slots.size()); ++i)
+    if (!ctx->slots[i].busy) {
+      si = i;
+      break;
+    }
+  if (si < 0) return set_err(HYDRO_EBUSY, "all in-flight batch slots hold uncollected results");
+  Slot& sl = ctx->slots[si];
+  const uint64_t n = static_cast<uint64_t>(t->n);
+  const uint64_t* id = t->id;
+  const uint32_t* fr = t->frame_id;
+  const uint64_t* bb = reinterpret_cast<const uint64_t*>(t->bbox);
+  const uint16_t* lab = t->label;
+  if (!t->on_device && n > 0) {
+    if ((s = validate_host_tuples(ctx, t)) != HYDRO_OK) return s;
+    if ((s = ensure_staging(ctx, sl)) != HYDRO_OK) return s;
+    CU(cudaMemcpyAsync(sl.s_id, t->id, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(sl.s_frame, t->frame_id, 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(sl.s_bbox, t->bbox, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(sl.s_label, t->label, 2 * n, cudaMemcpyHostToDevice, ctx->stream));
+    id = sl.s_id;
+    fr = sl.s_frame;
+    bb = sl.s_bbox;
+    lab = sl.s_label;
+  }
+  CU(cudaMemsetAsync(sl.rec, 0, sizeof(BatchRec), ctx->stream));
+  const int P = static_cast<int>(ctx->preds.size());
+  uint64_t warm = 0;
+  if (ctx->warmup_pending) {
+    // ---- warmup slice (R8): every predicate on the slice, no short-circuit
+    warm = std::min<uint64_t>(n, static_cast<uint64_t>(ctx->cfg.warmup_tuples));
+    for (int k = 0; k < P; ++k) {
+      uint32_t* wb = ctx->warm_bits + static_cast<uint64_t>(k) * ctx->bits_stride;
+      if (ctx->preds[k].desc.kind == HYDRO_PRED_LINEAR) {
+        ClsParams c = cls_base(ctx, fr, bb);
+        c.dispatch = 0;
+        c.explicit_pred = k;
+        c.list_in = nullptr;
+        c.range_base = 0;
+        c.range_n = static_cast<uint32_t>(warm);
+        c.bits_out = wb;
+        if ((s = launch_cls(ctx, c, warm)) != HYDRO_OK) return s;
+      } else {
+        RouteParams r = route_base(ctx, id, fr, bb, lab);
+        r.dispatch = 0;
+        r.explicit_pred = k;
+        r.range_base = 0;
+        r.range_n = static_cast<uint32_t>(warm);
+        r.out_mode = kOutBitmap;
+        r.bitmap_out = wb;
+        if ((s = launch_route(ctx, r, warm)) != HYDRO_OK) return s;
+      }
+    }
+    RouteParams r = route_base(ctx, id, fr, bb, lab);
+    r.dispatch = 0;
+    r.range_base = 0;
+    r.range_n = static_cast<uint32_t>(warm);
+    r.n_and = P;
+    for (int k = 0; k < P; ++k) r.and_bits[k] = ctx->warm_bits + static_cast<uint64_t>(k) * ctx->bits_stride;
+    r.out_mode = kOutEmit;
+    r.out_ids = sl.out_ids;
+    r.out_bbox = sl.out_bbox;
+    r.emit_count = &sl.rec->warm_count;
+    r.emit_offset = nullptr;
+    r.collect_stats = 0;
+    if ((s = launch_route(ctx, r, warm)) != HYDRO_OK) return s;
+    if ((s = fold_and_sync(ctx, sl.rec, 0, true)) != HYDRO_OK) return s;
+    ctx->warmup_pending = false;
+  }
+  // ---- the eddy chain on the rest of the batch
+  const uint32_t rest_base = static_cast<uint32_t>(warm);
+  const uint32_t rest_n = static_cast<uint32_t>(n - warm);
+  for (int h = 0; h <= P; ++h) {
+    RouteParams r = route_base(ctx, id, fr, bb, lab);
+    r.dispatch = 1;
+    r.hop = h;
+    r.range_base = rest_base;
+    r.range_n = rest_n;
+    r.out_ids = sl.out_ids;
+    r.out_bbox = sl.out_bbox;
+    r.emit_count = &sl.rec->total_count;
+    r.emit_offset = &sl.rec->warm_count;
+    if ((s = launch_route(ctx, r, rest_n)) != HYDRO_OK) return s;
+    if (h < P) {
+      ClsParams c = cls_base(ctx, fr, bb);
+      c.dispatch = 1;
+      c.hop = h;
+      c.range_base = rest_base;
+      c.range_n = rest_n;
+      if ((s = launch_cls(ctx, c, rest_n)) != HYDRO_OK) return s;
+    }
+  }
+  if ((s = fold_and_sync(ctx, sl.rec, 1, false)) != HYDRO_OK) return s;
+  CU(cudaEventRecord(sl.done, ctx->stream));
+  sl.busy = true;
+  sl.batch_id = ctx->next_batch++;
+  sl.n = static_cast<int64_t>(n);
+  sl.warm_n = static_cast<int64_t>(warm);
+  sl.rec_valid = false;
+  if (batch_id) *batch_id = sl.batch_id;
+  return HYDRO_OK;
+}
+
+static Slot* find_slot(hydro_ctx* ctx, int64_t batch_id) {
+  for (Slot& s : ctx->slots)
+    if (s.busy && s.batch_id == batch_id) return &s;
+  return nullptr;
+}
+
+static hydro_status wait_slot(hydro_ctx* ctx, Slot* sl) {
+  CU(cudaEventSynchronize(sl->done));
+  hydro_status s = check_sticky(ctx);
+  if (s != HYDRO_OK) return s;
+  if (!sl->rec_valid) {
+    CU(cudaMemcpy(&sl->rec_host, sl->rec, sizeof(BatchRec), cudaMemcpyDeviceToHost));
+    sl->rec_valid = true;
+  }
+  return HYDRO_OK;
+}
+
+hydro_status hydro_batch_count(hydro_ctx* ctx, int64_t batch_id, int64_t* count) {
+  if (!ctx || !count) return set_err(HYDRO_EINVAL, "NULL argument");
+  Slot* sl = find_slot(ctx, batch_id);
+  if (!sl) return set_err(HYDRO_EINVAL, "unknown or already collected batch id");
+  hydro_status s = wait_slot(ctx, sl);
+  if (s != HYDRO_OK) return s;
+  *count = sl->rec_host.total_count;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_collect_results(hydro_ctx* ctx, int64_t batch_id, uint64_t* ids, uint16_t* bboxes,
+                                   int64_t capacity, int64_t* count, int32_t out_on_device) {
+  if (!ctx || !count) return set_err(HYDRO_EINVAL, "NULL argument");
+  Slot* sl = find_slot(ctx, batch_id);
+  if (!sl) return set_err(HYDRO_EINVAL, "unknown or already collected batch id");
+  hydro_status s = wait_slot(ctx, sl);
+  if (s != HYDRO_OK) return s;
+  const int64_t c = sl->rec_host.total_count;
+  *count = c;
+  if (capacity < c) return set_err(HYDRO_ERANGE, "capacity < result count");
+  if (c > 0) {
+    if (!ids || !bboxes) return set_err(HYDRO_EINVAL, "NULL output buffer");
+    const cudaMemcpyKind k = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CU(cudaMemcpyAsync(ids, sl->out_ids, 8 * c, k, ctx->stream));
+    CU(cudaMemcpyAsync(bboxes, sl->out_bbox, 8 * c, k, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  sl->busy = false;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_release_batch(hydro_ctx* ctx, int64_t batch_id) {
+  if (!ctx) return set_err(HYDRO_EINVAL, "NULL argument");
+  Slot* sl = find_slot(ctx, batch_id);
+  if (!sl) return set_err(HYDRO_EINVAL, "unknown or already collected batch id");
+  CU(cudaEventSynchronize(sl->done));
+  sl->busy = false;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_batch_info(hydro_ctx* ctx, int64_t batch_id, hydro_batch_report* out) {
+  if (!ctx || !out) return set_err(HYDRO_EINVAL, "NULL argument");
+  Slot* sl = find_slot(ctx, batch_id);
+  if (!sl) return set_err(HYDRO_EINVAL, "unknown or already collected batch id (call before collect)");
+  hydro_status s = wait_slot(ctx, sl);
+  if (s != HYDRO_OK) return s;
+  std::memset(out, 0, sizeof(*out));
+  const BatchRec& r = sl->rec_host;
+  out->n_tuples = sl->n;
+  out->n_results = r.total_count;
+  out->warmup_tuples = sl->warm_n;
+  out->n_pred = static_cast<int32_t>(ctx->preds.size());
+  for (int k = 0; k < kMaxPred; ++k) {
+    out->order_used[k] = r.order_used[k];
+    out->tuples_in[k] = static_cast<int64_t>(r.d_in[k]);
+    out->tuples_passed[k] = static_cast<int64_t>(r.d_pass[k]);
+    out->cost_raw[k] = static_cast<double>(r.d_cost[k]);
+  }
+  return HYDRO_OK;
+}
+
+static hydro_status read_state(hydro_ctx* ctx, DevState* h) {
+  if (!ctx->frozen) return set_err(HYDRO_ESTATE, "no batch submitted yet");
+  CU(cudaStreamSynchronize(ctx->stream));
+  hydro_status s = check_sticky(ctx);
+  if (s != HYDRO_OK) return s;
+  CU(cudaMemcpy(h, ctx->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+  return HYDRO_OK;
+}
+
+hydro_status hydro_get_stats(hydro_ctx* ctx, int32_t k, hydro_pred_stats* out) {
+  if (!ctx || !out) return set_err(HYDRO_EINVAL, "NULL argument");
+  if (k < 0 || k >= static_cast<int32_t>(ctx->preds.size())) return set_err(HYDRO_EINVAL, "bad pred id");
+  DevState h;
+  hydro_status s = read_state(ctx, &h);
+  if (s != HYDRO_OK) return s;
+  out->tuples_in = static_cast<int64_t>(h.tot_in[k]);
+  out->tuples_passed = static_cast<int64_t>(h.tot_pass[k]);
+  out->cost_per_tuple = h.cost[k];
+  out->selectivity = h.sel[k];
+  out->rank = h.key[k];
+  out->position = h.position[k];
+  out->s_in = h.s_in[k];
+  out->s_pass = h.s_pass[k];
+  out->s_cost = h.s_cost[k];
+  out->cost_raw_total = h.tot_cost[k];
+  return HYDRO_OK;
+}
+
+hydro_status hydro_get_order(hydro_ctx* ctx, int32_t* order, int32_t* n) {
+  if (!ctx || !order || !n) return set_err(HYDRO_EINVAL, "NULL argument");
+  DevState h;
+  hydro_status s = read_state(ctx, &h);
+  if (s != HYDRO_OK) return s;
+  *n = h.n_pred;
+  for (int i = 0; i < h.n_pred; ++i) order[i] = h.order[i];
+  return HYDRO_OK;
+}
+
+hydro_status hydro_synchronize(hydro_ctx* ctx) {
+  if (!ctx) return set_err(HYDRO_EINVAL, "NULL argument");
+  CU(cudaStreamSynchronize(ctx->stream));
+  return check_sticky(ctx);
+}
+
+hydro_status hydro_launch_count(hydro_ctx* ctx, int64_t* launches) {
+  if (!ctx || !launches) return set_err(HYDRO_EINVAL, "NULL argument");
+  *launches = ctx->launches;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_set_kernel_timing(hydro_ctx* ctx, int32_t enable) {
+  if (!ctx) return set_err(HYDRO_EINVAL, "NULL argument");
+  CU(cudaStreamSynchronize(ctx->stream));
+  for (TimedLaunch& t : ctx->timed) {
+    ctx->event_pool.push_back(t.a);
+    ctx->event_pool.push_back(t.b);
+  }
+  ctx->timed.clear();
+  ctx->timing = enable != 0;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_kernel_time(hydro_ctx* ctx, int32_t kind, double* total_ms, int64_t* launches) {
+  if (!ctx || !total_ms || !launches) return set_err(HYDRO_EINVAL, "NULL argument");
+  CU(cudaStreamSynchronize(ctx->stream));
+  double tot = 0.0;
+  int64_t nl = 0;
+  for (TimedLaunch& t : ctx->timed) {
+    if (t.kind != kind) continue;
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, t.a, t.b));
+    tot += ms;
+    ++nl;
+  }
+  *total_ms = tot;
+  *launches = nl;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_debug_linear(hydro_ctx* ctx, int32_t k, const hydro_tuples* t, float* logits_out,
+                                uint16_t* crops_out, uint8_t* verdict_out) {
+  if (!ctx || !t) return set_err(HYDRO_EINVAL, "NULL argument");
+  if (k < 0 || k >= static_cast<int32_t>(ctx->preds.size()) || ctx->preds[k].desc.kind != HYDRO_PRED_LINEAR)
+    return set_err(HYDRO_EINVAL, "pred_id is not a LINEAR predicate");
+  if (!t->on_device) return set_err(HYDRO_EINVAL, "debug_linear needs device tuples");
+  if (t->n < 0 || t->n > ctx->cfg.max_batch_tuples) return set_err(HYDRO_EINVAL, "bad n");
+  hydro_status s = freeze(ctx);
+  if (s != HYDRO_OK) return s;
+  ClsParams c = cls_base(ctx, t->frame_id, reinterpret_cast<const uint64_t*>(t->bbox));
+  c.dispatch = 0;
+  c.explicit_pred = k;
+  c.range_base = 0;
+  c.range_n = static_cast<uint32_t>(t->n);
+  c.bits_out = ctx->warm_bits;
+  c.dbg_logits = logits_out;
+  c.dbg_crops = crops_out;
+  c.dbg_verdict = verdict_out;
+  c.collect_stats = 0;
+  if ((s = launch_cls(ctx, c, static_cast<uint64_t>(t->n))) != HYDRO_OK) return s;
+  CU(cudaStreamSynchronize(ctx->stream));
+  return check_sticky(ctx);
+}
+
+hydro_status hydro_destroy(hydro_ctx* ctx) {
+  if (!ctx) return HYDRO_OK;
+  cudaSetDevice(ctx->cfg.device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (Slot& s : ctx->slots) {
+    if (s.done) cudaEventDestroy(s.done);
+    cudaFree(s.out_ids);
+    cudaFree(s.out_bbox);
+    cudaFree(s.rec);
+    cudaFree(s.s_id);
+    cudaFree(s.s_frame);
+    cudaFree(s.s_bbox);
+    cudaFree(s.s_label);
+  }
+  for (PredHost& p : ctx->preds) {
+    cudaFree(p.w_tiled);
+    cudaFree(p.bias);
+  }
+  for (TimedLaunch& t : ctx->timed) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  cudaFree(ctx->st);
+  cudaFree(ctx->preds_dev);
+  cudaFree(ctx->lists);
+  cudaFree(ctx->counts);
+  cudaFree(ctx->bits);
+  cudaFree(ctx->warm_bits);
+  cudaFree(ctx->lb_status);
+  cudaFree(ctx->zero_word);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return HYDRO_OK;
+}
+
+}  // extern "C"

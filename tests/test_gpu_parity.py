@@ -1,0 +1,269 @@
+"""GPU parity: the CUDA path (through the C ABI) against oracle/ on the same seeded inputs.
+
+Bars: result rows (id, bbox) and per-predicate counters bit-exact; classifier
+crops bit-exact; logits within 1e-2 absolute of the f64 oracle (north_star tolerance); orders
+equal to the oracle's fold replay where the costs are deterministic.
+"""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import hash_pred, label_pred, workload
+from tests.gpu_helpers import ensure_built, expected_batch_counters, make_eddy, oracle_result, run_stream
+
+pytestmark = pytest.mark.gpu
+LOGIT_TOL = 1e-2  # north_star: classifier logits within 1e-2 absolute before thresholding
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    ensure_built()
+
+
+@pytest.fixture(scope="module")
+def small_dog():
+    w = workload("cfg2", small=True, n=6000)
+    frames = w.frames()
+    return w, frames, frames.cuda()
+
+
+def _assert_rows(ids, bbs, ref_ids, ref_bbox):
+    assert ids.shape == ref_ids.shape, (ids.shape, ref_ids.shape)
+    assert np.array_equal(ids, ref_ids)
+    assert np.array_equal(bbs, ref_bbox)
+
+
+# ------------------------------------------------------------------------------------- cfg1
+
+def test_cfg1_static_two_hash_predicates_exact():
+    w = workload("cfg1")
+    t = w.tuples()
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, None)
+    e = make_eddy(w, None)
+    ids, bbs, infos = run_stream(e, t.to("cuda"), w.batch_tuples)
+    _assert_rows(ids, bbs, ref_ids, ref_bbox)
+    info = infos[0]
+    assert info["order_used"] == [0, 1]
+    assert info["tuples_in"] == [10000, 5039] and info["tuples_passed"] == [5039, 534]
+    assert info["n_results"] == 534
+    e.close()
+
+
+# ------------------------------------------------------------------------------ classifier
+
+@pytest.mark.parametrize("pred_index", [1, 2])
+def test_linear_crops_logits_verdicts(small_dog, pred_index):
+    w, frames, frames_dev = small_dog
+    n = 700  # 6 M-tiles, ragged tail
+    t = w.tuples(n=n)
+    p = w.preds[pred_index]
+    e = make_eddy(w, frames_dev, policy="fixed", warmup=0)
+    td = t.to("cuda")
+    C = p["n_classes"]
+    logits = torch.full((n, C), float("nan"), device="cuda")
+    crops = torch.zeros((n, O.K_FEATURES), dtype=torch.int16, device="cuda")
+    verdict = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    e.debug_linear(pred_index, td, logits, crops, verdict)
+    tup = O.as_numpy_tuples(t)
+    fr = frames.numpy()
+    ref_crop = O.crop_nearest(fr, tup["frame_id"], tup["bbox"]).reshape(n, -1)
+    got_crop = crops.view(torch.bfloat16).float().cpu().numpy()
+    assert np.array_equal(got_crop, ref_crop.astype(np.float32))
+    v_ref, z_ref = O.linear_verdict(p, fr, tup["frame_id"], tup["bbox"], return_logits=True)
+    z = logits.double().cpu().numpy()
+    err = np.abs(z - z_ref).max()
+    assert err <= LOGIT_TOL, err
+    assert np.array_equal(verdict.cpu().numpy().astype(bool), v_ref)
+    e.close()
+
+
+# ------------------------------------------------------------------------- forced orders
+
+def _mixed_workload():
+    w = workload("cfg2", small=True, n=5000)
+    w.preds = w.preds + [hash_pred(77, 0.6, units=3, name="H")]
+    return w
+
+
+def test_every_forced_order_gives_the_oracle_result_and_counters():
+    w = _mixed_workload()
+    frames = w.frames()
+    t = w.tuples()
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, frames.numpy())
+    fd, td = frames.cuda(), t.to("cuda")
+    for perm in itertools.permutations(range(len(w.preds))):
+        e = make_eddy(w, fd, policy="fixed", warmup=0, max_batch=8192)
+        e.set_fixed_order(perm)
+        ids, bbs, infos = run_stream(e, td, 8192)
+        _assert_rows(ids, bbs, ref_ids, ref_bbox)
+        n_in, n_pass, _ = O.sequential_eval(V, perm)
+        assert infos[0]["order_used"] == list(perm)
+        assert infos[0]["tuples_in"] == n_in.tolist(), perm
+        assert infos[0]["tuples_passed"] == n_pass.tolist(), perm
+        e.close()
+
+
+# ------------------------------------------------------------------ adaptive SCORE policy
+
+def test_score_policy_multi_batch_counters_and_fold_replay(small_dog):
+    """Declared costs (deterministic) + measured selectivities: every batch's order and counters
+    equal the oracle's fold replay (R4) and eager-materialization counts."""
+    w, frames, frames_dev = small_dog
+    t = w.tuples(n=20000)
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, frames.numpy())
+    batch, warm = 3000, 1024
+    e = make_eddy(w, frames_dev, policy="score", cost_source="declared", warmup=warm, max_batch=batch)
+    ids, bbs, infos = run_stream(e, t.to("cuda"), batch)
+    _assert_rows(ids, bbs, ref_ids, ref_bbox)
+    fold = O.FoldState(len(w.preds), 0.5, [p["declared_cost"] for p in w.preds], cost_source="declared")
+    for b, info in enumerate(infos):
+        Vb = V[:, b * batch:(b + 1) * batch]
+        wb = warm if b == 0 else 0
+        if wb:
+            fold.fold([wb] * len(w.preds), Vb[:, :wb].sum(1), [0] * len(w.preds))
+        assert info["order_used"] == fold.order("score"), b
+        n_in, n_pass = expected_batch_counters(Vb, info["order_used"], wb)
+        assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist(), b
+        d_in = n_in - (wb if wb else 0)
+        d_pass = n_pass - (Vb[:, :wb].sum(1) if wb else 0)
+        fold.fold(d_in, d_pass, [0] * len(w.preds))
+    assert e.order() == fold.order("score")
+    for k in range(len(w.preds)):
+        s = e.stats(k)
+        assert s["selectivity"] == pytest.approx(fold.sel()[k], rel=1e-12)
+    e.close()
+
+
+def test_cfg3_selectivity_drift_reorders():
+    w = workload("cfg3", n=1_000_000)
+    t = w.tuples()
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, None)
+    e = make_eddy(w, None, policy="score", warmup=65536, max_batch=w.batch_tuples)
+    ids, bbs, infos = run_stream(e, t.to("cuda"), w.batch_tuples)
+    _assert_rows(ids, bbs, ref_ids, ref_bbox)
+    drift_batch = 500_000 // w.batch_tuples
+    orders = [i["order_used"] for i in infos]
+    for b in range(1, drift_batch):
+        assert orders[b][-1] == 0, (b, orders[b])      # P0 (sel 0.9) last before the drift
+    for b in range(drift_batch + 2, len(orders)):
+        assert orders[b][0] == 0, (b, orders[b])       # P0 (sel 0.1) first within 2 batches
+    for b, info in enumerate(infos):
+        Vb = V[:, b * w.batch_tuples:(b + 1) * w.batch_tuples]
+        n_in, n_pass = expected_batch_counters(Vb, info["order_used"], 65536 if b == 0 else 0)
+        assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist()
+    e.close()
+
+
+# -------------------------------------------------------------------------- edge cases
+
+def test_edge_cases_empty_single_allfail_host_input(small_dog):
+    w, frames, frames_dev = small_dog
+    t = w.tuples(n=3000)
+    V, ref_ids, ref_bbox, keep = oracle_result(w, t, frames.numpy())
+    e = make_eddy(w, frames_dev, policy="score", warmup=0, max_batch=4096)
+    # empty batch
+    b = e.submit(t.slice(0, 0).to("cuda"))
+    assert e.count(b) == 0
+    e.collect(b)
+    # a single tuple, both a passing and a failing one
+    for i in (int(np.argmax(keep)), int(np.argmin(keep))):
+        b = e.submit(t.slice(i, i + 1).to("cuda"))
+        ids, _ = e.collect(b)
+        assert ids.numpy().astype(np.uint64).tolist() == ([int(t.id[i])] if keep[i] else [])
+    # all-fail batch: only failing tuples
+    fail = np.where(~keep)[0][:777]
+    b = e.submit(t.select(torch.from_numpy(fail)).to("cuda"))
+    assert e.count(b) == 0
+    e.collect(b)
+    # host-input path == device path == oracle
+    b1 = e.submit(t)
+    b2 = e.submit(t.to("cuda"))
+    i1, bb1 = e.collect(b1)
+    i2, bb2 = e.collect(b2)
+    assert np.array_equal(i1.numpy().astype(np.uint64), ref_ids) and np.array_equal(i2.numpy(), i1.numpy())
+    assert np.array_equal(bb1.numpy().astype(np.int64), ref_bbox) and np.array_equal(bb2.numpy(), bb1.numpy())
+    e.close()
+
+
+def test_errors_erange_ebusy_einval(small_dog):
+    from paper_2403_14902_b200 import hydro as H
+
+    w, frames, frames_dev = small_dog
+    t = w.tuples(n=3000).to("cuda")
+    e = make_eddy(w, frames_dev, warmup=0, max_batch=4096, max_inflight=2)
+    b0 = e.submit(t)
+    b1 = e.submit(t)
+    with pytest.raises(H.HydroError) as ex:
+        e.submit(t)
+    assert ex.value.status == H.HYDRO_EBUSY
+    n = e.count(b0)
+    ids = torch.empty(max(n, 1), dtype=torch.int64)
+    bb = torch.empty((max(n, 1), 4), dtype=torch.int16)
+    if n > 0:
+        with pytest.raises(H.HydroError) as ex:
+            H.hydro_collect_results(e.ctx, b0, ids.data_ptr(), bb.data_ptr(), n - 1, 0)
+        assert ex.value.status == H.HYDRO_ERANGE
+    e.collect(b0)
+    e.collect(b1)
+    with pytest.raises(H.HydroError) as ex:
+        e.submit(w.tuples(n=5000).to("cuda"))  # > max_batch
+    assert ex.value.status == H.HYDRO_EINVAL
+    bad = w.tuples(n=10)
+    bad.bbox[3, 2] = bad.bbox[3, 0]  # empty bbox on the host path
+    with pytest.raises(H.HydroError) as ex:
+        e.submit(bad)
+    assert ex.value.status == H.HYDRO_EINVAL
+    with pytest.raises(H.HydroError) as ex:
+        e.add_predicate(label_pred())
+    assert ex.value.status == H.HYDRO_ESTATE
+    e.close()
+
+
+# ---------------------------------------------------------------- full-size (BASELINE sizes)
+
+def test_route_full_scale_label_and_hash_exact():
+    """R-route shape (label + 2 hash predicates) at 2M tuples: bit-exact against the oracle."""
+    w = workload("cfg2", n=2_000_000)
+    w.preds = [label_pred(), hash_pred(31, 0.5, units=1), hash_pred(32, 0.5, units=1)]
+    t = w.tuples()
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, None)
+    e = make_eddy(w, None, policy="score", warmup=65536, max_batch=1 << 20)
+    ids, bbs, infos = run_stream(e, t.to("cuda"), 1 << 20)
+    _assert_rows(ids, bbs, ref_ids, ref_bbox)
+    e.close()
+
+
+def test_cfg2_full_size_sampled_parity():
+    """cfg2 at BASELINE size (1M tuples, 1024 x 720p frames) in the bench's launch configuration;
+    rows checked against the oracle one by one on samples of survivors and non-survivors."""
+    w = workload("cfg2")
+    frames_dev = w.frames(device="cuda")
+    t = w.tuples()
+    e = make_eddy(w, frames_dev, policy="score", warmup=65536, max_batch=1 << 20)
+    ids, bbs, infos = run_stream(e, t.to("cuda"), 1 << 20)
+    assert np.all(np.diff(ids.astype(np.int64)) > 0)  # input order, no duplicates
+    all_ids = t.id.numpy()
+    pos = np.searchsorted(all_ids, ids.astype(np.int64))
+    assert np.array_equal(t.bbox.numpy()[pos].astype(np.int64), bbs)
+    rng = np.random.default_rng(0)
+    in_res = np.zeros(len(all_ids), bool)
+    in_res[pos] = True
+    samp = np.concatenate([rng.choice(np.where(in_res)[0], 1500, replace=False),
+                           rng.choice(np.where(~in_res)[0], 1500, replace=False)])
+    samp.sort()
+    sub = t.select(torch.from_numpy(samp))
+    fids = np.unique(sub.frame_id.numpy())
+    fr = np.zeros((w.n_frames, w.frame_h, w.frame_w, 3), np.uint8)
+    fr[fids] = w.frames(frame_ids=fids).numpy()
+    V = O.evaluate_all(w.preds, sub, fr)
+    assert np.array_equal(V.all(0), in_res[samp])
+    # counters of the single batch equal the oracle's on the label stage (exact, cheap)
+    lab = (t.label.numpy() == 16)
+    info = infos[0]
+    assert info["tuples_passed"][0] == int(lab.sum())
+    e.close()
