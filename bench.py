@@ -1,0 +1,360 @@
+"""Benchmark: tuples/s through the 3-predicate UDF conjunction (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Workload (BASELINE.json configs[1] / SURVEY.md §8 cfg2): 1M synthetic dog-query detections per
+GPU per step -- label = 'dog' AND DogBreed(Crop) = 'great dane' AND DogColor(Crop) = 'black' with
+linear heads on 64x64 nearest crops of a 1024-frame 720p HWC uint8 pool (PAPER.md:43-49,
+276-288).  A step = one routing batch of 1M tuples through the whole eddy hot path (order,
+label / classifier hops with eager compaction, emit of (id, bbox), fold).  N > 1: one process
+per GPU (torchrun), contiguous per-rank id shards (weak scaling), NCCL all-reduce of the
+statistics deltas inside libhydro.
+
+value  : device-timed (CUDA events on the context stream), inputs resident in HBM.
+e2e    : same metric through the C ABI with pinned HOST tuple columns (H2D inside the timed
+         region) and results copied back to pinned host memory (D2H), host wall clock.
+roofline: the classifier kernel (K4), HBM-bound: algorithmic bytes = (12288 sampled crop bytes
+         + 16 B metadata) per classifier-input tuple, over the kernel's summed
+         CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tuples/sec through 3-predicate UDF conjunction at 1/2/4/8 B200; % HBM/tensor roofline"
+UNIT = "tuples/s"
+TUPLES_PER_STEP = 1_000_000
+ROTATING_BATCHES = 6          # 6 x 22 MB of tuple columns + 2.83 GB frames: inputs larger than L2
+K4_BYTES_PER_TUPLE = 12288 + 16
+WORKLOAD = ("cfg2: 1M dog-query detections per GPU per step; label='dog' AND breed(C=120) AND "
+            "colour(C=10) linear heads on 64x64 nearest crops; 1024 x 720x1280x3 u8 frame pool")
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_oracle_rate(w, tuples_cpu, frames_host, seconds: float = 15.0, min_tuples: int = 256):
+    """Oracle (as it stands) on host cores over a bounded contiguous sample of the workload."""
+    import numpy as np
+
+    import oracle as O
+    from threadpoolctl import threadpool_info
+
+    cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    chunk, done, t0 = 512, 0, time.perf_counter()
+    while True:
+        sub = tuples_cpu.slice(done, done + chunk)
+        O.evaluate_all(w.preds, sub, frames_host)
+        done += len(sub)
+        el = time.perf_counter() - t0
+        if (el >= seconds and done >= min_tuples) or done >= len(tuples_cpu):
+            break
+    return done / el, done, el, cores
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on the host (rank 0 only), same metric/config."""
+    world, rank, local = _dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle as O
+    from synth import workload
+    from threadpoolctl import threadpool_info
+
+    w = workload("cfg2")
+    per_step = 4096
+    t = w.tuples(n=per_step * 4)
+    fids = np.unique(t.frame_id.numpy())
+    frames = np.zeros((w.n_frames, w.frame_h, w.frame_w, 3), np.uint8)
+    frames[fids] = w.frames(frame_ids=fids).numpy()
+    cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    times = []
+    for s in range(args.warmup + args.steps):
+        sub = t.slice((s % 4) * per_step, (s % 4 + 1) * per_step)
+        t0 = time.perf_counter()
+        O.evaluate_all(w.preds, sub, frames)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    el = sum(times)
+    value = per_step * len(times) / el
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * el / len(times),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": WORKLOAD, "tuples_per_step": per_step,
+                                           "parallelism": "host cores (numpy/OpenBLAS)"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": f"{per_step} tuples per step of the cfg2 workload, every predicate on every tuple"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    from paper_2403_14902_b200 import build as B
+    from paper_2403_14902_b200 import hydro as H
+    from synth import shard_range, workload
+
+    world, rank, local = _dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        B.build()
+    if dist:
+        dist.barrier()
+    w = workload("cfg2")
+    frames = w.frames(device="cuda")
+    uid = None
+    if world > 1:
+        obj = [H.hydro_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    stream = torch.cuda.current_stream()
+    e = H.Eddy(frames=frames, policy="score", warmup_tuples=65536, max_batch_tuples=1 << 20,
+               max_inflight=4, rank=rank, world=world, sync_every=1, nccl_unique_id=uid, stream=stream)
+    for p in w.preds:
+        e.add_predicate(p)
+    # per-rank contiguous shard of each step's id range (weak scaling: 1M tuples per GPU per step)
+    batches = []
+    for b in range(ROTATING_BATCHES):
+        start = (b * world + rank) * TUPLES_PER_STEP
+        batches.append(w.tuples(id_start=start, n=TUPLES_PER_STEP, device="cuda"))
+    res_ids = torch.empty(1 << 20, dtype=torch.int64, device="cuda")
+    res_bb = torch.empty((1 << 20, 4), dtype=torch.int16, device="cuda")
+
+    def collect_dev(bid):
+        return H.hydro_collect_results(e.ctx, bid, res_ids.data_ptr(), res_bb.data_ptr(), 1 << 20, 1)
+
+    def run_steps(k, offset):
+        pend = []
+        for s in range(k):
+            pend.append(e.submit(batches[(offset + s) % ROTATING_BATCHES]))
+            if len(pend) >= 3:
+                collect_dev(pend.pop(0))
+        for bid in pend:
+            collect_dev(bid)
+
+    lin = [k for k, p in enumerate(w.preds) if p["kind"] == "linear"]
+
+    def lin_in():
+        return sum(e.stats(k)["tuples_in"] for k in lin)
+
+    run_steps(max(args.warmup, 3), 0)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches0 = e.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ev0.record(stream)
+        run_steps(args.steps, 1)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = e.launch_count() - launches0
+    if dist:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+        dist.barrier()
+    value = world * TUPLES_PER_STEP * args.steps / (ms / 1000.0)
+
+    # ---- kernel timing pass (separate, untimed for `value`): K4 share + achieved bandwidth
+    in0 = lin_in()
+    e.set_kernel_timing(True)
+    run_steps(args.steps, 2)
+    k4_ms, k4_n = e.kernel_time(1)
+    k1_ms, k1_n = e.kernel_time(0)
+    k5_ms, k5_n = e.kernel_time(2)
+    e.set_kernel_timing(False)
+    k4_tuples = lin_in() - in0
+    k4_bytes = k4_tuples * K4_BYTES_PER_TUPLE
+    peaks = _peaks()
+    achieved = k4_bytes / (k4_ms / 1000.0) / 1e9 if k4_ms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "k4_dram_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the C ABI with pinned host buffers
+    host_batches = [batches[b].to("cpu", pin=True) for b in range(2)]
+    out_ids = torch.empty(1 << 20, dtype=torch.int64).pin_memory()
+    out_bb = torch.empty((1 << 20, 4), dtype=torch.int16).pin_memory()
+    h2d = host_batches[0].nbytes()
+    d2h = []
+
+    def e2e_steps(k):
+        pend = []
+        for s in range(k):
+            pend.append(e.submit(host_batches[s % 2]))
+            if len(pend) >= 2:
+                n = H.hydro_collect_results(e.ctx, pend.pop(0), out_ids.data_ptr(), out_bb.data_ptr(), 1 << 20, 0)
+                d2h.append(16 * n)
+        for bid in pend:
+            n = H.hydro_collect_results(e.ctx, bid, out_ids.data_ptr(), out_bb.data_ptr(), 1 << 20, 0)
+            d2h.append(16 * n)
+
+    e2e_steps(2)
+    d2h.clear()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e2e_steps(args.steps)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if dist:
+        tt = torch.tensor([el], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+    e2e_value = world * TUPLES_PER_STEP * args.steps / el
+
+    order = e.order()
+    sel = {w.preds[k]["name"]: round(e.stats(k)["selectivity"], 4) for k in range(len(w.preds))}
+    cost = {w.preds[k]["name"]: round(e.stats(k)["cost_per_tuple"], 2) for k in range(len(w.preds))}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        fr_host = frames.cpu().numpy()
+        tc = batches[0].slice(0, 200_000).to("cpu")
+        rate, done, secs, cores = cpu_oracle_rate(w, tc, fr_host, seconds=args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"first {done} tuples of the step's 1M-tuple batch ({secs:.1f} s of CPU work), every "
+                         f"predicate on every tuple, f64 numpy/OpenBLAS"}
+    e.close()
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+               "config": {"workload": WORKLOAD, "tuples_per_step": world * TUPLES_PER_STEP,
+                          "batch_tuples": TUPLES_PER_STEP, "policy": "score (cost/(1-sel)), measured costs",
+                          "l2": "inputs larger than L2: 2.83 GB frame pool + 6 rotating 22 MB tuple batches",
+                          "parallelism": f"dp{world}", "final_order": [w.preds[k]["name"] for k in order],
+                          "selectivity": sel, "cost_sm_cycles_per_tuple": cost},
+               "roofline": {"kernel": "hydro_classifier_kernel (K4: crop gather + tcgen05 linear head)",
+                            "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                            "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                            "algorithmic_bytes_per_launch": k4_bytes / max(k4_n, 1),
+                            "avg_launch_ms": k4_ms / max(k4_n, 1), "launches": k4_n,
+                            "share_of_step": k4_ms / max(k4_ms + k1_ms + k5_ms, 1e-9),
+                            "k1_ms_per_step": k1_ms / args.steps, "k4_ms_per_step": k4_ms / args.steps,
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"},
+               "cpu_baseline": cpu,
+               "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": int(sum(d2h) / max(len(d2h), 1))},
+               "clocks": clk.summary(), "gpu_launches": launches}
+        print(json.dumps(out))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hydro", choices=["hydro", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

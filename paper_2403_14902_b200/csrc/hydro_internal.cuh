@@ -24,13 +24,20 @@ constexpr int kRouteTile = kRouteThreads * kRouteItems;     // 2048 positions pe
 // ---- K4 (classifier) geometry
 constexpr int kTileM = 128;                                 // UMMA M (cta_group::1)
 constexpr int kConvWarps = 8;                               // gather/convert warps
+constexpr int kConvRows = kTileM / kConvWarps;              // 16 consecutive rows per converter warp
 constexpr int kEpiWarps = 4;                                // TMEM quadrant warps 0..3
-constexpr int kLoaderWarp = 4;
-constexpr int kMmaWarp = 5;
+constexpr int kLoaderWarp = 4;                              // weights (bulk copy) + L2 prefetch
+constexpr int kMmaWarp = 5;                                 // TMEM alloc + tcgen05.mma issue
 constexpr int kConvWarp0 = 6;
 constexpr int kClsWarps = kConvWarp0 + kConvWarps;          // 14
 constexpr int kClsThreads = kClsWarps * 32;                 // 448
-constexpr int kAStageBytes = kKBlocksPerGroup * kTileM * 128;  // 49152
+constexpr int kAKBlockBytes = kTileM * 128;                 // one 128 x 64 fp16 K-block: 16 KB
+constexpr int kARing = 6;                                   // A K-block stages (2 crop rows)
+constexpr int kBRing = 3;                                   // B K-block stages
+constexpr int kMaxSegBytes = 784;                           // 3*255 + 16-byte alignment slack
+constexpr int kQuadDepth = 2;                               // quads staged ahead per converter warp
+constexpr int kQuadSlots = kQuadDepth + 1;
+constexpr int kQuadSlotBytes = 4 * kMaxSegBytes;            // 4 rows x worst-case segment
 constexpr int kClsSmemBytes = 232448;                       // 227 KB opt-in maximum
 
 enum PredKind : int32_t { kLabelEq = HYDRO_PRED_LABEL_EQ, kHash = HYDRO_PRED_HASH, kLinear = HYDRO_PRED_LINEAR };
@@ -45,6 +52,8 @@ struct PredDev {
   const uint8_t* w_tiled;   // LINEAR: [192 kblk][n_pad rows][128 B SW128-swizzled]
   const float* bias;        // [n_pad] (padding rows: -inf never wins; they are skipped anyway)
   int32_t n_classes, n_pad, target, crop_mode;
+  int32_t a_fp16;           // 1: operands staged as fp16 (weights exactly representable), 0: bf16
+  int32_t pad_;
 };
 
 // Device-resident eddy state (one per context).  d_* are the atomically accumulated deltas of
@@ -185,6 +194,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// long waits: the hint lets the warp sleep in hardware instead of re-polling
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAITS_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
 // async proxy / TMA bulk copy (1D) global -> shared, completion on an mbarrier
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -212,10 +235,11 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t smem_addr) {
          (static_cast<uint64_t>(2) << 61);
 }
 
-__device__ __forceinline__ uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
-  // kind::f16 instruction descriptor: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1,
+__device__ __forceinline__ uint32_t idesc_f16_f32(uint32_t M, uint32_t N, bool bf16) {
+  // kind::f16 instruction descriptor: D f32 [4,6)=1, A/B format [7,10)/[10,13) (0 = f16, 1 = bf16),
   // K-major A/B (bits 15,16 = 0), N>>3 [17,23), M>>4 [24,29)
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
+  const uint32_t f = bf16 ? 1u : 0u;
+  return (1u << 4) | (f << 7) | (f << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
 __device__ __forceinline__ void tc_mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -265,6 +289,8 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
 
 // kernels (defined in k_route.cu / k_classifier.cu), launched by runtime.cu
 __global__ void hydro_route_kernel(hydro::RouteParams p);
+template <bool kDbg>
 __global__ void hydro_classifier_kernel(hydro::ClsParams p);
 __global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode);
-__global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad);
+__global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,
+                                          int32_t to_fp16, int32_t* inexact);

@@ -1,19 +1,22 @@
-// K4: fused Crop(frame, bbox) -> 64x64 resize gather -> bf16 linear-head GEMM on tcgen05 tensor
-// cores -> argmax verdict (readings R10-R14, R19 in DESIGN.md §2).
+// K4: fused Crop(frame, bbox) -> 64x64 resize gather -> linear-head GEMM on tcgen05 tensor cores
+// -> argmax verdict (readings R10-R14, R19 in DESIGN.md §2).
 //
-// One persistent CTA per SM walks M-tiles of 128 alive tuples.  Per tile the K = 12288 features
-// are streamed as 64 crop rows ("groups"); a group is one 64-pixel crop row x 3 channels =
-// 3 UMMA K-blocks of 64 bf16.  Warp roles:
+// One persistent CTA per SM walks M-tiles of 128 alive tuples.  The K = 12288 features of a tile
+// are streamed as 64 crop rows ("groups") of 3 UMMA K-blocks (64 elements = 128 B per row).
+// Warp roles:
 //   warps 0-3  epilogue: tcgen05.ld the fp32 accumulator (TMEM lane = tuple), + bias, argmax,
 //              verdict ballot -> bitmap, pass counters
-//   warp  4    loader: 1-D bulk copy (TMA engine) of the pre-swizzled weight K-blocks into the
-//              stage's B buffer; L2 prefetch of upcoming crop-row segments
-//   warp  5    MMA: allocates TMEM, one elected thread issues tcgen05.mma (M=128, N=n_pad,
-//              K=16) x 12 per group, tcgen05.commit releases the stage / publishes the tile
-//   warps 6-13 converters: nearest-exact source pixel fetch (sy = y0 + ((2dy+1)h)>>7,
-//              sx = x0 + ((2dx+1)w)>>7), exact u8 -> bf16, st.shared into the 128B-swizzled
-//              K-major A stage, fence.proxy.async, mbarrier arrive.
-// The A tile never touches HBM: only the sampled frame bytes are read.
+//   warp  4    loader: 1-D bulk copies (TMA engine) of the pre-swizzled weight K-blocks into the B
+//              ring; L2 prefetch of the crop-row segments a few groups ahead
+//   warp  5    MMA: TMEM alloc; one thread issues tcgen05.mma (M=128, N=n_pad, K=16) x 4 per
+//              K-block, tcgen05.commit releases A / B stages and publishes finished tiles
+//   warps 6-13 converters: stage each tuple's source row segment [3*x0 & ~15, roundup16(3*x1))
+//              of frame row sy = y0 + ((2dy+1)h)>>7 into shared memory with coalesced 16-byte
+//              cp.async (two 4-row quads ahead); then 8 lanes x 8 output pixels per crop row,
+//              4 rows per warp instruction; nearest-exact pixel selection sx = x0 + ((2dx+1)w)>>7,
+//              exact u8 -> fp16 (PRMT 0x64vv = 1024+v, HSUB2 1024) or bf16, 128-bit st.shared
+//              into the 128B-swizzled K-major A ring (conflict-free), fence.proxy.async, arrive.
+// The A operand never touches HBM: only the crop-row segments of the frames are read.
 #include "hydro_internal.cuh"
 
 using namespace hydro;
@@ -21,11 +24,9 @@ using namespace hydro;
 namespace {
 
 struct ClsCtrl {
-  uint64_t full_a[4];
-  uint64_t full_b[4];
-  uint64_t empty[4];
-  uint64_t tfull[2];
-  uint64_t tempty[2];
+  uint64_t full_a[kARing], empty_a[kARing];
+  uint64_t full_b[kBRing], empty_b[kBRing];
+  uint64_t tfull[2], tempty[2];
   uint32_t tmem_base;
   uint32_t pad;
   float bias[HYDRO_MAX_CLASSES];
@@ -37,11 +38,34 @@ __device__ __forceinline__ uint32_t bf16_bits_of_byte(uint32_t b) {
   return __float_as_uint(f) >> 16;
 }
 
-__device__ __forceinline__ uint32_t ldg32(const uint8_t* p) { return __ldg(reinterpret_cast<const uint32_t*>(p)); }
+__device__ __forceinline__ uint32_t f16x2_sub(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t bf16x2_of_bytes(uint32_t lo, uint32_t hi) {
+  const float flo = __uint_as_float(0x4B000000u | lo) - 8388608.0f;
+  const float fhi = __uint_as_float(0x4B000000u | hi) - 8388608.0f;
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(fhi), "f"(flo));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 
 struct RowMeta {  // per alive tuple of the tile
-  uint32_t frame_off;  // byte offset of frame row 0
-  int32_t x0, y0, w, h;
+  uint32_t row0;     // byte offset of (frame, y0, 0) in the frame pool
+  uint32_t seg_lo;   // 16-byte aligned start of the crop's byte span inside a frame row
+  uint32_t seg_len;  // bytes to stage per crop row (multiple of 16), 0 when invalid
+  int32_t x0, w, h;
   int32_t valid;
 };
 
@@ -61,22 +85,97 @@ __device__ __forceinline__ RowMeta load_meta(const ClsParams& p, const uint32_t*
   y0 = min(y0, p.frame_h - 1);
   x1 = max(min(x1, p.frame_w), x0 + 1);
   y1 = max(min(y1, p.frame_h), y0 + 1);
-  m.frame_off = fid * static_cast<uint32_t>(p.frame_h * p.frame_w * 3);
+  const uint32_t pitch = static_cast<uint32_t>(p.frame_w * 3);
+  m.row0 = fid * static_cast<uint32_t>(p.frame_h) * pitch + static_cast<uint32_t>(y0) * pitch;
+  m.seg_lo = (3u * x0) & ~15u;
+  m.seg_len = ((3u * x1 + 15u) & ~15u) - m.seg_lo;  // frame_w % 16 == 0 keeps this inside the row
   m.x0 = x0;
-  m.y0 = y0;
   m.w = x1 - x0;
   m.h = y1 - y0;
   return m;
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// per-thread L2 prefetch of one line (a regular LSU op: unlike the uniform-datapath
+// cp.async.bulk.prefetch it does not serialise across the lanes of a warp)
+__device__ __forceinline__ void prefetch_line_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 
 }  // namespace
 
+// One quad (4 crop rows x 8 lanes) of output pixels: lane (r, j) produces pixels 8j .. 8j+7 of
+// row m from its staged segment `seg` (smem address).  po[q] packs the byte offsets (relative to
+// the segment) of pixels 8j+2q and 8j+2q+1.  Branch-free: both words around a pixel are always
+// read (the slots carry slack), the funnel shift uses the wrap mode (shift = 8*o mod 32).
+template <bool kFp16, bool kDbg>
+__device__ __forceinline__ void convert_quad(uint32_t seg, const uint32_t (&po)[4], uint32_t row_base, uint32_t j,
+                                             uint32_t m, uint16_t* dbg) {
+  uint32_t px[8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const uint32_t o = h2 ? (po[q] >> 16) : (po[q] & 0xFFFFu);
+      const uint32_t a = (seg + o) & ~3u;
+      const uint32_t w0 = lds32(a);
+      const uint32_t w1 = lds32(a + 4);
+      px[2 * q + h2] = __funnelshift_r(w0, w1, o << 3);
+    }
+  }
+  uint32_t e[12];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t p0 = px[2 * q], p1 = px[2 * q + 1];
+    if (kFp16) {
+      const uint32_t K = 0x64646464u;  // fp16 0x64vv == 1024 + v exactly
+      e[3 * q + 0] = f16x2_sub(__byte_perm(p0, K, 0x4140), 0x64006400u);
+      e[3 * q + 1] = f16x2_sub(__byte_perm(__byte_perm(p0, p1, 0x0042), K, 0x4140), 0x64006400u);
+      e[3 * q + 2] = f16x2_sub(__byte_perm(p1, K, 0x4241), 0x64006400u);
+    } else {
+      e[3 * q + 0] = bf16x2_of_bytes(p0 & 0xFF, (p0 >> 8) & 0xFF);
+      e[3 * q + 1] = bf16x2_of_bytes((p0 >> 16) & 0xFF, p1 & 0xFF);
+      e[3 * q + 2] = bf16x2_of_bytes((p1 >> 8) & 0xFF, (p1 >> 16) & 0xFF);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const uint32_t c = 3u * j + t;  // 16-byte chunk of the 192-element crop row
+    const uint32_t addr = row_base + (c >> 3) * kAKBlockBytes + (((c & 7u) ^ (m & 7u)) << 4);
+    sts128(addr, e[4 * t], e[4 * t + 1], e[4 * t + 2], e[4 * t + 3]);
+  }
+  if (kDbg) {
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      dbg[3 * kk + 0] = static_cast<uint16_t>(bf16_bits_of_byte(px[kk] & 0xFF));
+      dbg[3 * kk + 1] = static_cast<uint16_t>(bf16_bits_of_byte((px[kk] >> 8) & 0xFF));
+      dbg[3 * kk + 2] = static_cast<uint16_t>(bf16_bits_of_byte((px[kk] >> 16) & 0xFF));
+    }
+  }
+}
+
 extern __shared__ __align__(1024) uint8_t hydro_cls_smem[];
 
+template <bool kDbg>
 __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsParams p) {
   DevState* st = p.st;
   // ---- dispatch (uniform across the CTA: every thread reads the same device words)
@@ -108,25 +207,33 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   const long long t_start = clock64();
   const PredDev& pdg = p.preds[pred];
   const int n_classes = pdg.n_classes, n_pad = pdg.n_pad, target = pdg.target;
+  const bool fp16 = pdg.a_fp16 != 0;
   const uint8_t* w_tiled = pdg.w_tiled;
   const int n_alloc = n_pad <= 32 ? 32 : (n_pad <= 64 ? 64 : 128);
   const uint32_t tmem_cols = 2u * n_alloc;
-  const uint32_t b_stage_bytes = kKBlocksPerGroup * n_pad * 128;
-  const uint32_t stage_bytes = (kAStageBytes + b_stage_bytes + 1023u) & ~1023u;
+  const uint32_t b_stage_bytes = static_cast<uint32_t>(n_pad) * 128u;
+  const uint32_t row_pitch = static_cast<uint32_t>(p.frame_w * 3);
 
-  // ---- shared memory carve-up (1024-aligned for the 128B swizzle)
+  // ---- shared memory carve-up: [A ring][B ring][ctrl][staging ring]
   const uint32_t raw = smem_u32(hydro_cls_smem);
   uint8_t* smem = hydro_cls_smem + (((raw + 1023u) & ~1023u) - raw);
-  const uint32_t avail = kClsSmemBytes - 1024u - static_cast<uint32_t>(sizeof(ClsCtrl)) - 64u;
-  const uint32_t S = min(4u, avail / stage_bytes);
-  ClsCtrl* ctrl = reinterpret_cast<ClsCtrl*>(smem + S * stage_bytes);
+  const uint32_t a_ring = smem_u32(smem);
+  const uint32_t b_ring = a_ring + kARing * kAKBlockBytes;
+  const uint32_t ctrl_off = kARing * kAKBlockBytes + kBRing * b_stage_bytes;
+  ClsCtrl* ctrl = reinterpret_cast<ClsCtrl*>(smem + ctrl_off);
+  const uint32_t stg_off = (ctrl_off + static_cast<uint32_t>(sizeof(ClsCtrl)) + 15u) & ~15u;
+  uint8_t* staging = smem + stg_off;
+  const uint32_t staging_addr = smem_u32(staging);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (uint32_t s = 0; s < S; ++s) {
+    for (int s = 0; s < kARing; ++s) {
       mbar_init(&ctrl->full_a[s], kConvWarps);
+      mbar_init(&ctrl->empty_a[s], 1);
+    }
+    for (int s = 0; s < kBRing; ++s) {
       mbar_init(&ctrl->full_b[s], 1);
-      mbar_init(&ctrl->empty[s], 1);
+      mbar_init(&ctrl->empty_b[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&ctrl->tfull[a], 1);
@@ -147,9 +254,10 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   const uint32_t tmem_base = ctrl->tmem_base;
 
   if (warp == kLoaderWarp) {
-    // ===================== loader: weights (bulk copy) + L2 prefetch of crop rows
-    constexpr int kPrefetchGroups = 3;
-    uint32_t it = 0;
+    // ===================== loader: weight K-blocks (bulk copy) + L2 prefetch of crop rows
+    constexpr int kPrefetchGroups = 4;
+    const uint64_t pol_w = policy_evict_last();  // weights are re-read by every tile: keep them in L2
+    uint32_t itb = 0;
     for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       RowMeta mr[4];
 #pragma unroll
@@ -158,23 +266,23 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           if (!mr[r].valid) continue;
-          const int sy = mr[r].y0 + (((2 * g + 1) * mr[r].h) >> 7);
-          const uint8_t* row = p.frames + mr[r].frame_off + static_cast<uint32_t>(sy) * (p.frame_w * 3);
-          const uint32_t a = (3u * mr[r].x0) & ~15u;
-          const uint32_t e = (3u * (mr[r].x0 + mr[r].w) + 15u) & ~15u;
-          const uint32_t row_bytes = static_cast<uint32_t>(p.frame_w * 3);
-          prefetch_l2(row + a, min(e, row_bytes) - a);
+          const uint32_t sy = static_cast<uint32_t>(((2 * g + 1) * mr[r].h) >> 7);
+          const uint8_t* a = p.frames + mr[r].row0 + sy * row_pitch + mr[r].seg_lo;
+          for (uint32_t c = 0; c < mr[r].seg_len; c += 128u) prefetch_line_l2(a + c);
         }
       };
       for (int g = 0; g < kPrefetchGroups; ++g) prefetch_group(g);
-      for (int g = 0; g < kGroups; ++g, ++it) {
-        if (g + kPrefetchGroups < kGroups) prefetch_group(g + kPrefetchGroups);
-        const uint32_t s = it % S, ph = (it / S) & 1u;
+      for (int kb = 0; kb < kNumKBlocks; ++kb, ++itb) {
+        if (kb % kKBlocksPerGroup == 0) {
+          const int g = kb / kKBlocksPerGroup + kPrefetchGroups;
+          if (g < kGroups) prefetch_group(g);
+        }
         if (lane == 0) {
-          mbar_wait(&ctrl->empty[s], ph ^ 1u);
-          uint8_t* bdst = smem + s * stage_bytes + kAStageBytes;
+          const uint32_t s = itb % kBRing, ph = (itb / kBRing) & 1u;
+          mbar_wait(&ctrl->empty_b[s], ph ^ 1u);
           mbar_arrive_expect_tx(&ctrl->full_b[s], b_stage_bytes);
-          bulk_g2s(bdst, w_tiled + static_cast<uint64_t>(g) * b_stage_bytes, b_stage_bytes, &ctrl->full_b[s]);
+          bulk_g2s_hint(smem + (b_ring - a_ring) + s * b_stage_bytes, w_tiled + static_cast<uint64_t>(kb) * b_stage_bytes,
+                        b_stage_bytes, &ctrl->full_b[s], pol_w);
         }
         __syncwarp();
       }
@@ -182,115 +290,122 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (single thread)
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(kTileM, static_cast<uint32_t>(n_pad));
-      uint32_t it = 0, tl = 0;
+      const uint32_t idesc = idesc_f16_f32(kTileM, static_cast<uint32_t>(n_pad), !fp16);
+      uint32_t itb = 0, gg = 0, tl = 0;
       for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl) {
         const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
-        mbar_wait(&ctrl->tempty[acc], aph ^ 1u);
+        mbar_wait_sleep(&ctrl->tempty[acc], aph ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * static_cast<uint32_t>(n_alloc);
-        for (int g = 0; g < kGroups; ++g, ++it) {
-          const uint32_t s = it % S, ph = (it / S) & 1u;
-          mbar_wait(&ctrl->full_a[s], ph);
-          mbar_wait(&ctrl->full_b[s], ph);
-          tc_fence_after();
-          const uint32_t a_base = smem_u32(smem + s * stage_bytes);
-          const uint32_t b_base = a_base + kAStageBytes;
+        for (int g = 0; g < kGroups; ++g, ++gg) {
+          const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph2 = (gg >> 1) & 1u;
 #pragma unroll
-          for (int kb = 0; kb < kKBlocksPerGroup; ++kb) {
+          for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr, ++itb) {
+            const uint32_t sa = set + kbr;
+            const uint32_t sb = itb % kBRing, bph = (itb / kBRing) & 1u;
+            mbar_wait(&ctrl->full_a[sa], aph2);
+            mbar_wait(&ctrl->full_b[sb], bph);
+            tc_fence_after();
+            const uint32_t a_addr = a_ring + sa * kAKBlockBytes;
+            const uint32_t b_addr = b_ring + sb * b_stage_bytes;
 #pragma unroll
             for (int kk = 0; kk < kKBlock / 16; ++kk) {
-              const uint64_t ad = desc_sw128(a_base + kb * (kTileM * 128) + kk * 32);
-              const uint64_t bd = desc_sw128(b_base + kb * (n_pad * 128) + kk * 32);
-              tc_mma_bf16(d_tmem, ad, bd, idesc, (g | kb | kk) != 0 ? 1u : 0u);
+              tc_mma_bf16(d_tmem, desc_sw128(a_addr + kk * 32), desc_sw128(b_addr + kk * 32), idesc,
+                          (g | kbr | kk) != 0 ? 1u : 0u);
             }
+            tc_commit(&ctrl->empty_a[sa]);
+            tc_commit(&ctrl->empty_b[sb]);
           }
-          tc_commit(&ctrl->empty[s]);
         }
         tc_commit(&ctrl->tfull[acc]);
       }
     }
     __syncwarp();
   } else if (warp >= kConvWarp0) {
-    // ===================== converters: gather + u8->bf16 + swizzled st.shared
-    const int cw = warp - kConvWarp0;  // rows m = cw + 8*i, i = 0..15
-    constexpr int kRows = kTileM / kConvWarps;  // 16
-    constexpr int kBatch = 8;
-    const uint32_t row_pitch = static_cast<uint32_t>(p.frame_w * 3);
-    uint32_t it = 0;
+    // ===================== converters: cp.async-staged segments -> pixels -> swizzled A ring
+    // Warp cu owns rows 16*cu .. 16*cu+15; it walks them as "quads" of 4 rows (one warp
+    // instruction = 4 rows x 8 lanes x 8 output pixels).  Quad k's source segments are
+    // copied (16-byte cp.async, coalesced per row) kQuadDepth quads ahead into fixed slots.
+    const int cu = warp - kConvWarp0;
+    const int r = lane >> 3, j = lane & 7;  // row-in-quad and 8-pixel block (pixels 8j .. 8j+7)
+    const uint32_t slots = staging_addr + static_cast<uint32_t>(cu) * (kQuadSlots * kQuadSlotBytes);
+    uint32_t gg = 0;
     for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      // lane i < 16 holds the metadata of row cw + 8*i
-      RowMeta my = load_meta(p, list_in, base, tile * kTileM + cw + kConvWarps * (lane & 15), count);
-      if (lane >= kRows) my.valid = 0;
-      for (int g = 0; g < kGroups; ++g, ++it) {
-        const uint32_t s = it % S, ph = (it / S) & 1u;
-        mbar_wait(&ctrl->empty[s], ph ^ 1u);
-        uint8_t* a_stage = smem + s * stage_bytes;
+      // rows' metadata: lane l < 16 holds row 16*cu + l
+      const RowMeta mm = load_meta(p, list_in, base, tile * kTileM + cu * kConvRows + (lane & 15),
+                                   lane < 16 ? count : 0u);
+      const uint32_t my_src = mm.row0 + mm.seg_lo;                 // + sy * pitch per crop row
+      const uint32_t my_len = (lane < 16 && mm.valid) ? mm.seg_len : 0u;
+      const uint32_t my_h = static_cast<uint32_t>(mm.h);
+      uint32_t po[4][4];
+      bool valid[4];
 #pragma unroll
-        for (int i0 = 0; i0 < kRows; i0 += kBatch) {
-          uint32_t w00[kBatch], w01[kBatch], w10[kBatch], w11[kBatch], sh0[kBatch], sh1[kBatch];
-          int valid[kBatch];
+      for (int it = 0; it < 4; ++it) {
+        const int src = 4 * it + r;
+        valid[it] = __shfl_sync(0xFFFFFFFFu, mm.valid, src) != 0;
+        const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src);
+        const uint32_t w = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src);
+        const uint32_t slo = __shfl_sync(0xFFFFFFFFu, mm.seg_lo, src);
 #pragma unroll
-          for (int b = 0; b < kBatch; ++b) {
-            const int src = i0 + b;
-            valid[b] = __shfl_sync(0xFFFFFFFFu, my.valid, src);
-            const uint32_t foff = __shfl_sync(0xFFFFFFFFu, my.frame_off, src);
-            const int x0 = __shfl_sync(0xFFFFFFFFu, my.x0, src);
-            const int y0 = __shfl_sync(0xFFFFFFFFu, my.y0, src);
-            const int w = __shfl_sync(0xFFFFFFFFu, my.w, src);
-            const int h = __shfl_sync(0xFFFFFFFFu, my.h, src);
-            w00[b] = w01[b] = w10[b] = w11[b] = 0;
-            sh0[b] = sh1[b] = 0;
-            if (valid[b]) {
-              const int sy = y0 + (((2 * g + 1) * h) >> 7);
-              const uint8_t* row = p.frames + foff + static_cast<uint32_t>(sy) * row_pitch;
-              const int dx0 = 2 * lane;
-              const int sx0 = x0 + (((2 * dx0 + 1) * w) >> 7);
-              const int sx1 = x0 + (((2 * dx0 + 3) * w) >> 7);
-              const uint32_t o0 = 3u * sx0, o1 = 3u * sx1;
-              w00[b] = ldg32(row + (o0 & ~3u));
-              if ((o0 & 3u) > 1u) w01[b] = ldg32(row + (o0 & ~3u) + 4);
-              w10[b] = ldg32(row + (o1 & ~3u));
-              if ((o1 & 3u) > 1u) w11[b] = ldg32(row + (o1 & ~3u) + 4);
-              sh0[b] = 8u * (o0 & 3u);
-              sh1[b] = 8u * (o1 & 3u);
-            }
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t dx0 = 8u * j + 2u * q;
+          const uint32_t o0 = 3u * (x0 + (((2u * dx0 + 1u) * w) >> 7)) - slo;
+          const uint32_t o1 = 3u * (x0 + (((2u * dx0 + 3u) * w) >> 7)) - slo;
+          po[it][q] = o0 | (o1 << 16);
+        }
+      }
+      // stage quad k = 4*g + it of this tile into slot k % kQuadSlots
+      auto stage_quad = [&](int k) {
+        if (k < kGroups * 4) {
+          const int g = k >> 2, it = k & 3;
+          const uint32_t dst0 = slots + static_cast<uint32_t>(k % kQuadSlots) * kQuadSlotBytes;
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) {
+            const int src_lane = 4 * it + rr;
+            const uint32_t len = __shfl_sync(0xFFFFFFFFu, my_len, src_lane);
+            const uint32_t off = __shfl_sync(0xFFFFFFFFu, my_src, src_lane);
+            const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
+            const uint8_t* src = p.frames + off + (((2u * g + 1u) * h) >> 7) * row_pitch;
+            const uint32_t dst = dst0 + rr * kMaxSegBytes;
+            const uint32_t c0 = 16u * lane, c1 = c0 + 512u;  // segments are <= 784 bytes
+            if (c0 < len) cp_async16(dst + c0, src + c0);
+            if (c1 < len) cp_async16(dst + c1, src + c1);
           }
+        }
+        cp_async_commit();  // one group per quad (possibly empty) keeps wait_group counting uniform
+      };
 #pragma unroll
-          for (int b = 0; b < kBatch; ++b) {
-            if (!valid[b]) continue;
-            const int m = cw + kConvWarps * (i0 + b);
-            const uint32_t px0 = __funnelshift_r(w00[b], w01[b], sh0[b]);
-            const uint32_t px1 = __funnelshift_r(w10[b], w11[b], sh1[b]);
-            uint32_t e[6];
-            e[0] = bf16_bits_of_byte(px0 & 0xFF);
-            e[1] = bf16_bits_of_byte((px0 >> 8) & 0xFF);
-            e[2] = bf16_bits_of_byte((px0 >> 16) & 0xFF);
-            e[3] = bf16_bits_of_byte(px1 & 0xFF);
-            e[4] = bf16_bits_of_byte((px1 >> 8) & 0xFF);
-            e[5] = bf16_bits_of_byte((px1 >> 16) & 0xFF);
-            const uint32_t row_off = static_cast<uint32_t>(m >> 3) * 1024u + static_cast<uint32_t>(m & 7) * 128u;
+      for (int k = 0; k < kQuadDepth; ++k) stage_quad(k);
+      for (int g = 0; g < kGroups; ++g, ++gg) {
+        const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph = (gg >> 1) & 1u;
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
-              const uint32_t el = 6u * lane + 2u * q;    // element within the 192-element crop row
-              const uint32_t kb = el >> 6;
-              const uint32_t byte = (el & 63u) * 2u;
-              const uint32_t chunk = (byte >> 4) ^ static_cast<uint32_t>(m & 7);
-              const uint32_t off = kb * (kTileM * 128u) + row_off + (chunk << 4) + (byte & 15u);
-              *reinterpret_cast<uint32_t*>(a_stage + off) = e[2 * q] | (e[2 * q + 1] << 16);
-            }
-            if (p.dbg_crops) {
-              const uint32_t pos = tile * kTileM + m;
-              uint16_t* d = p.dbg_crops + static_cast<uint64_t>(pos) * kFeatures + g * 192 + 6 * lane;
+        for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_wait(&ctrl->empty_a[set + kbr], aph ^ 1u);
+        const uint32_t a_set = a_ring + set * kAKBlockBytes;
 #pragma unroll
-              for (int j = 0; j < 6; ++j) d[j] = static_cast<uint16_t>(e[j]);
-            }
+        for (int it = 0; it < 4; ++it) {
+          const int k = 4 * g + it;
+          stage_quad(k + kQuadDepth);
+          cp_async_wait<kQuadDepth>();  // this thread's copies of quad k have landed
+          __syncwarp();                 // ... and every lane's
+          if (valid[it]) {
+            const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * it + r);
+            const uint32_t seg = slots + static_cast<uint32_t>(k % kQuadSlots) * kQuadSlotBytes + r * kMaxSegBytes;
+            const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
+            uint16_t* dbg = kDbg ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + m) * kFeatures + g * 192 + 24 * j
+                                 : nullptr;
+            if (fp16) convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
+            else convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
           }
+          __syncwarp();  // slot k % kQuadSlots is refilled kQuadDepth quads later
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ctrl->full_a[s]);
+        if (lane == 0) {
+#pragma unroll
+          for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_arrive(&ctrl->full_a[set + kbr]);
+        }
       }
+      cp_async_wait<0>();
     }
   } else {
     // ===================== epilogue warps 0..3 (TMEM lane quadrant = warp)
@@ -298,7 +413,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     uint32_t n_in = 0, n_pass = 0, tl = 0;
     for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl) {
       const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
-      mbar_wait(&ctrl->tfull[acc], aph);
+      mbar_wait_sleep(&ctrl->tfull[acc], aph);
       tc_fence_after();
       const int m = q * 32 + lane;
       const uint32_t pos = tile * kTileM + m;
@@ -311,15 +426,15 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
         tc_ld_32x32b_x16(taddr + c0, v);
         tc_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int c = c0 + j;
+        for (int jj = 0; jj < 16; ++jj) {
+          const int c = c0 + jj;
           if (c < n_classes) {
-            const float z = __uint_as_float(v[j]) + ctrl->bias[c];
+            const float z = __uint_as_float(v[jj]) + ctrl->bias[c];
             if (z > best) {  // strict: lowest index wins ties (R12)
               best = z;
               bi = c;
             }
-            if (p.dbg_logits && valid) p.dbg_logits[static_cast<uint64_t>(pos) * n_classes + c] = z;
+            if (kDbg && p.dbg_logits && valid) p.dbg_logits[static_cast<uint64_t>(pos) * n_classes + c] = z;
           }
         }
       }
@@ -330,7 +445,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       const uint32_t bv = __ballot_sync(0xFFFFFFFFu, verdict);
       const uint32_t bvalid = __ballot_sync(0xFFFFFFFFu, valid);
       if (lane == 0 && bvalid) bits_out[tile * (kTileM / 32) + q] = bv;
-      if (p.dbg_verdict && valid) p.dbg_verdict[pos] = verdict ? 1 : 0;
+      if (kDbg && p.dbg_verdict && valid) p.dbg_verdict[pos] = verdict ? 1 : 0;
       n_in += __popc(bvalid);
       n_pass += __popc(bv);
     }
@@ -349,3 +464,6 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     atomicAdd(&st->d_cost[pred], static_cast<unsigned long long>(clock64() - t_start));
   }
 }
+
+template __global__ void hydro_classifier_kernel<false>(ClsParams p);
+template __global__ void hydro_classifier_kernel<true>(ClsParams p);

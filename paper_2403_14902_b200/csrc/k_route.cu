@@ -11,6 +11,8 @@
 // K5 folds the counters: S <- gamma*S + delta (R4), s = S_pass/S_in,
 // c = S_cost/S_in, key = c/(1-s), stable order by (key, id)
 // (R1, R2).
+#include <cuda_fp16.h>
+
 #include "hydro_internal.cuh"
 
 using namespace hydro;
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
   __shared__ unsigned long long s_in[kMaxPred], s_pass[kMaxPred], s_cost[kMaxPred];
   __shared__ uint32_t s_warp_tot[kRouteThreads / 32], s_warp_excl[kRouteThreads / 32];
   __shared__ uint32_t s_tile, s_prefix, s_emit_off;
-  __shared__ int32_t s_work, s_nrun, s_out_mode, s_n_and;
+  __shared__ int32_t s_work, s_nrun, s_out_mode, s_n_and, s_need_id, s_need_bbox, s_need_label;
   __shared__ const uint32_t* s_list_in;
   __shared__ const uint32_t* s_and[kMaxPred];
   __shared__ uint32_t s_count, s_range_base;
@@ -152,6 +154,21 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
     s_pass[tid] = 0;
     s_cost[tid] = 0;
   }
+  if (tid == 0) {
+    int need_id = 0, need_bbox = 0, need_label = 0;
+    for (int r = 0; r < nrun; ++r) {
+      const PredDev& q = p.preds[s_run_id[r]];
+      if (q.kind == kHash) {
+        need_id = 1;
+        if (q.units_per_area > 0) need_bbox = 1;
+      } else {
+        need_label = 1;
+      }
+    }
+    s_need_id = need_id;
+    s_need_bbox = need_bbox;
+    s_need_label = need_label;
+  }
   const uint32_t count = s_count;
   const uint32_t num_tiles = (count + kRouteTile - 1) / kRouteTile;
   const int out_mode = s_out_mode;
@@ -201,46 +218,59 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
     }
     const bool contiguous = (list_in == nullptr) && (mask == 0xFFu) && (((base + p0) & 7u) == 0);
 
+    // columns the run needs, loaded once for the alive items (outside the per-predicate timing)
+    uint64_t ids[kRouteItems];
+    uint64_t bbs[kRouteItems];
+    uint32_t labs[kRouteItems / 2];
+    if (mask) {
+      if (s_need_id) {
+        if (contiguous && ((reinterpret_cast<uintptr_t>(p.id + base + p0) & 15u) == 0)) {
+          const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p.id + base + p0);
+#pragma unroll
+          for (int j = 0; j < kRouteItems / 2; ++j) {
+            const ulonglong2 v = __ldg(q + j);
+            ids[2 * j] = v.x;
+            ids[2 * j + 1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < kRouteItems; ++j) ids[j] = ((mask >> j) & 1u) ? __ldg(p.id + idx[j]) : 0ull;
+        }
+      }
+      if (s_need_bbox) {
+#pragma unroll
+        for (int j = 0; j < kRouteItems; ++j) bbs[j] = ((mask >> j) & 1u) ? __ldg(p.bbox + idx[j]) : 0ull;
+      }
+      if (s_need_label) {
+        if (contiguous && ((reinterpret_cast<uintptr_t>(p.label + base + p0) & 15u) == 0)) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.label + base + p0));
+          labs[0] = v.x; labs[1] = v.y; labs[2] = v.z; labs[3] = v.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < kRouteItems / 2; ++j) {
+            const uint32_t lo = ((mask >> (2 * j)) & 1u) ? __ldg(p.label + idx[2 * j]) : 0u;
+            const uint32_t hi = ((mask >> (2 * j + 1)) & 1u) ? __ldg(p.label + idx[2 * j + 1]) : 0u;
+            labs[j] = lo | (hi << 16);
+          }
+        }
+      }
+    }
+
     for (int r = 0; r < nrun; ++r) {
       const PredDev& pd = s_pred[r];
       const long long t0 = clock64();
       const uint32_t in_mask = mask;
       if (mask) {
         if (pd.kind == kLabelEq) {
-          const uint16_t want = static_cast<uint16_t>(pd.label_value);
-          if (contiguous && ((reinterpret_cast<uintptr_t>(p.label + base + p0) & 15u) == 0)) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.label + base + p0));
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          const uint32_t want = static_cast<uint32_t>(pd.label_value) & 0xFFFFu;
 #pragma unroll
-            for (int j = 0; j < kRouteItems; ++j) {
-              const uint16_t l = static_cast<uint16_t>(w[j >> 1] >> (16 * (j & 1)));
-              if (l != want) mask &= ~(1u << j);
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < kRouteItems; ++j)
-              if ((mask >> j) & 1u)
-                if (__ldg(p.label + idx[j]) != want) mask &= ~(1u << j);
-          }
+          for (int j = 0; j < kRouteItems; ++j)
+            if (((labs[j >> 1] >> (16 * (j & 1))) & 0xFFFFu) != want) mask &= ~(1u << j);
         } else {  // kHash
-          uint64_t ids[kRouteItems];
-          if (contiguous && ((reinterpret_cast<uintptr_t>(p.id + base + p0) & 15u) == 0)) {
-            const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p.id + base + p0);
-#pragma unroll
-            for (int j = 0; j < kRouteItems / 2; ++j) {
-              const ulonglong2 v = __ldg(q + j);
-              ids[2 * j] = v.x;
-              ids[2 * j + 1] = v.y;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < kRouteItems; ++j) ids[j] = ((mask >> j) & 1u) ? __ldg(p.id + idx[j]) : 0ull;
-          }
 #pragma unroll
           for (int j = 0; j < kRouteItems; ++j) {
             if ((mask >> j) & 1u) {
-              const uint64_t bb = pd.units_per_area > 0 ? __ldg(p.bbox + idx[j]) : 0ull;
-              if (!hash_pass(pd, ids[j], bb)) mask &= ~(1u << j);
+              if (!hash_pass(pd, ids[j], pd.units_per_area > 0 ? bbs[j] : 0ull)) mask &= ~(1u << j);
             }
           }
         }
@@ -252,7 +282,9 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
         if (lane == 0) {
           atomicAdd(&s_in[r], static_cast<unsigned long long>(ci));
           atomicAdd(&s_pass[r], static_cast<unsigned long long>(cp));
-          atomicAdd(&s_cost[r], static_cast<unsigned long long>(t1 - t0));
+          // dense-equivalent cost: SIMT lanes without an alive item idle, so the warp's cycles are
+          // charged in proportion to its occupancy (ci of 256 items); SM-cycles = raw / (256 * warps/SM)
+          atomicAdd(&s_cost[r], static_cast<unsigned long long>(t1 - t0) * ci);
         }
       }
     }
@@ -414,7 +446,10 @@ __global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode) {
 // Weight re-layout: W[C][12288] bf16 row-major -> [192 K-blocks][n_pad rows][128 B] with the
 // 128-byte swizzle applied (16-byte chunk c of row n stored at chunk c ^ (n & 7)), i.e. the exact
 // shared-memory image UMMA reads, so one 1-D bulk copy per stage lands it.  Rows >= C are 0.
-__global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad) {
+// to_fp16 = 1 re-encodes every weight as fp16 (identical value) and raises *inexact if any bf16
+// weight is not exactly representable in fp16 (the runtime then re-tiles as bf16).
+__global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,
+                                          int32_t to_fp16, int32_t* inexact) {
   const uint64_t total = static_cast<uint64_t>(kNumKBlocks) * n_pad * 8;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -423,8 +458,21 @@ __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, i
     const uint32_t n = static_cast<uint32_t>(rowi % n_pad);
     const uint32_t kb = static_cast<uint32_t>(rowi / n_pad);
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (static_cast<int32_t>(n) < n_classes)
+    if (static_cast<int32_t>(n) < n_classes) {
       v = *reinterpret_cast<const uint4*>(w + static_cast<uint64_t>(n) * kFeatures + kb * kKBlock + c * 8);
+      if (to_fp16) {
+        uint32_t* u = reinterpret_cast<uint32_t*>(&v);
+        int bad = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float lo = __uint_as_float(u[j] << 16), hi = __uint_as_float(u[j] & 0xFFFF0000u);
+          const __half hl = __float2half_rn(lo), hh = __float2half_rn(hi);
+          bad |= (__half2float(hl) != lo) | (__half2float(hh) != hi);
+          u[j] = static_cast<uint32_t>(__half_as_ushort(hl)) | (static_cast<uint32_t>(__half_as_ushort(hh)) << 16);
+        }
+        if (bad) atomicOr(inexact, 1);
+      }
+    }
     uint8_t* dst = w_tiled + (static_cast<uint64_t>(kb) * n_pad + n) * 128 + ((c ^ (n & 7)) << 4);
     *reinterpret_cast<uint4*>(dst) = v;
   }

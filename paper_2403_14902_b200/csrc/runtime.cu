@@ -46,6 +46,7 @@ struct PredHost {
   uint8_t* w_tiled = nullptr;
   float* bias = nullptr;
   int n_pad = 0;
+  int a_fp16 = 0;
 };
 
 struct Slot {
@@ -209,9 +210,10 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   if (cfg->world > 1 && !cfg->nccl_unique_id) return set_err(HYDRO_EINVAL, "world > 1 needs nccl_unique_id");
   if (cfg->sync_every < 1) return set_err(HYDRO_EINVAL, "sync_every >= 1");
   if (cfg->frames) {
-    if (cfg->n_frames < 1 || cfg->frame_h < 1 || cfg->frame_w < 1 || (cfg->frame_w % 4) != 0 ||
+    if (cfg->n_frames < 1 || cfg->frame_h < 1 || cfg->frame_w < 1 || (cfg->frame_w % 16) != 0 ||
         cfg->frame_h > 65535 || cfg->frame_w > 65535)
-      return set_err(HYDRO_EINVAL, "frame pool: n_frames, frame_h >= 1; frame_w % 4 == 0; dims <= 65535");
+      return set_err(HYDRO_EINVAL, "frame pool: n_frames, frame_h >= 1; frame_w % 16 == 0; dims <= 65535");
+    if ((reinterpret_cast<uintptr_t>(cfg->frames) & 15u) != 0) return set_err(HYDRO_EINVAL, "frames must be 16-byte aligned");
     if (static_cast<double>(cfg->n_frames) * cfg->frame_h * cfg->frame_w * 3 >= 4294967296.0)
       return set_err(HYDRO_EINVAL, "frame pool must be < 4 GiB");
   }
@@ -227,7 +229,8 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   }
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->k1_occ, hydro_route_kernel, kRouteThreads, 0));
   if (ctx->k1_occ < 1) ctx->k1_occ = 1;
-  CU(cudaFuncSetAttribute(hydro_classifier_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
+  CU(cudaFuncSetAttribute(hydro_classifier_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
+  CU(cudaFuncSetAttribute(hydro_classifier_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
   CU(cudaMalloc(&ctx->st, sizeof(DevState)));
   CU(cudaMemset(ctx->st, 0, sizeof(DevState)));
   CU(cudaMalloc(&ctx->preds_dev, sizeof(PredDev) * kMaxPred));
@@ -283,10 +286,23 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
     CU(cudaMemsetAsync(ph.bias, 0, sizeof(float) * HYDRO_MAX_CLASSES, ctx->stream));
     CU(cudaMemcpyAsync(ph.bias, d->bias, sizeof(float) * C,
                        d->weights_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
-    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, ph.w_tiled, C, ph.n_pad);
+    // stage operands as fp16 when every weight is exactly representable (u8 pixels always are):
+    // same products, cheaper u8 -> fp16 operand construction in K4
+    CU(cudaMemsetAsync(ctx->zero_word + 1, 0, sizeof(int32_t), ctx->stream));
+    int32_t* inexact = reinterpret_cast<int32_t*>(ctx->zero_word + 1);
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, ph.w_tiled, C, ph.n_pad, 1, inexact);
     ctx->launches += 1;
     CU(cudaGetLastError());
+    int32_t bad = 0;
+    CU(cudaMemcpyAsync(&bad, inexact, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
+    ph.a_fp16 = bad ? 0 : 1;
+    if (bad) {
+      hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, ph.w_tiled, C, ph.n_pad, 0, inexact);
+      ctx->launches += 1;
+      CU(cudaGetLastError());
+      CU(cudaStreamSynchronize(ctx->stream));
+    }
     CU(cudaFree(wdev));
   } else {
     return set_err(HYDRO_EINVAL, "unknown predicate kind");
@@ -328,7 +344,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
   h.cost_source = ctx->cfg.cost_source;
   h.gamma = ctx->cfg.decay_gamma;
   h.prior = ctx->cfg.prior_selectivity;
-  const double k1_norm = 1.0 / (static_cast<double>(ctx->k1_occ) * (kRouteThreads / 32));
+  const double k1_norm = 1.0 / (256.0 * static_cast<double>(ctx->k1_occ) * (kRouteThreads / 32));
   std::vector<PredDev> pd(kMaxPred);
   for (int k = 0; k < P; ++k) {
     const hydro_predicate_desc& d = ctx->preds[k].desc;
@@ -351,6 +367,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
     q.n_pad = ctx->preds[k].n_pad;
     q.target = d.target;
     q.crop_mode = d.crop_mode;
+    q.a_fp16 = ctx->preds[k].a_fp16;
   }
   // initial order: declared statistics (SCORE/COST/SEL before warmup; STATIC), or add order
   for (int k = 0; k < P; ++k) {
@@ -462,7 +479,10 @@ static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_
   const uint64_t tiles = (max_positions + kTileM - 1) / kTileM;
   const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctx->num_sms)));
   return timed_launch(ctx, 1, [&] {
-    hydro_classifier_kernel<<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
+    if (c.dbg_crops || c.dbg_logits || c.dbg_verdict)
+      hydro_classifier_kernel<true><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
+    else
+      hydro_classifier_kernel<false><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
   });
 }
 
