@@ -14,8 +14,8 @@
 //              of frame row sy = y0 + ((2dy+1)h)>>7 into shared memory with coalesced 16-byte
 //              cp.async (two 4-row quads ahead); then 8 lanes x 8 output pixels per crop row,
 //              4 rows per warp instruction; nearest-exact pixel selection sx = x0 + ((2dx+1)w)>>7,
-//              exact u8 -> fp16 (PRMT 0x64vv = 1024+v, HSUB2 1024) or bf16, 128-bit st.shared
-//              into the 128B-swizzled K-major A ring (conflict-free), fence.proxy.async, arrive.
+//              exact u8 -> fp16 (PRMT 0x64vv = 1024+v, HSUB2 1024) or bf16, st.shared into the
+//              128B-swizzled K-major A ring (conflict-free), fence.proxy.async, arrive.
 // The A operand never touches HBM: only the crop-row segments of the frames are read.
 #include "hydro_internal.cuh"
 
@@ -56,6 +56,9 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
@@ -163,7 +166,7 @@ __device__ __forceinline__ void convert_quad(uint32_t seg, const uint32_t (&po)[
     const uint32_t addr = row_base + (c >> 3) * kAKBlockBytes + (((c & 7u) ^ (m & 7u)) << 4);
     sts128(addr, e[4 * t], e[4 * t + 1], e[4 * t + 2], e[4 * t + 3]);
   }
-  if (kDbg) {
+  if (kDbg && dbg) {
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
       dbg[3 * kk + 0] = static_cast<uint16_t>(bf16_bits_of_byte(px[kk] & 0xFF));
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     const int cu = warp - kConvWarp0;
     const int r = lane >> 3, j = lane & 7;  // row-in-quad and 8-pixel block (pixels 8j .. 8j+7)
     const uint32_t slots = staging_addr + static_cast<uint32_t>(cu) * (kQuadSlots * kQuadSlotBytes);
+    const uint8_t* frames = p.frames;
     uint32_t gg = 0;
     for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       // rows' metadata: lane l < 16 holds row 16*cu + l
@@ -338,11 +342,9 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       const uint32_t my_len = (lane < 16 && mm.valid) ? mm.seg_len : 0u;
       const uint32_t my_h = static_cast<uint32_t>(mm.h);
       uint32_t po[4][4];
-      bool valid[4];
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
         const int src = 4 * it + r;
-        valid[it] = __shfl_sync(0xFFFFFFFFu, mm.valid, src) != 0;
         const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src);
         const uint32_t w = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src);
         const uint32_t slo = __shfl_sync(0xFFFFFFFFu, mm.seg_lo, src);
@@ -354,28 +356,30 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
           po[it][q] = o0 | (o1 << 16);
         }
       }
-      // stage quad k = 4*g + it of this tile into slot k % kQuadSlots
-      auto stage_quad = [&](int k) {
+      // Stage quad k = 4*g + it (rows 4*it .. 4*it+3 of this warp, crop row g) into slot k % kQuadSlots:
+      // lanes 8r .. 8r+7 copy row r's segment in 16-byte chunks j + 8c (c < 7: segments <= 784 B).
+      auto stage_quad = [&](int k, uint32_t slot) {
         if (k < kGroups * 4) {
           const int g = k >> 2, it = k & 3;
-          const uint32_t dst0 = slots + static_cast<uint32_t>(k % kQuadSlots) * kQuadSlotBytes;
+          const int src_lane = 4 * it + r;
+          const uint32_t len = __shfl_sync(0xFFFFFFFFu, my_len, src_lane);
+          const uint32_t off = __shfl_sync(0xFFFFFFFFu, my_src, src_lane);
+          const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
+          const uint8_t* src = frames + (off + (((2u * g + 1u) * h) >> 7) * row_pitch + 16u * j);
+          const uint32_t dst = slots + slot * kQuadSlotBytes + r * kMaxSegBytes + 16u * j;
+          const uint32_t nch = len >> 4;
 #pragma unroll
-          for (int rr = 0; rr < 4; ++rr) {
-            const int src_lane = 4 * it + rr;
-            const uint32_t len = __shfl_sync(0xFFFFFFFFu, my_len, src_lane);
-            const uint32_t off = __shfl_sync(0xFFFFFFFFu, my_src, src_lane);
-            const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
-            const uint8_t* src = p.frames + off + (((2u * g + 1u) * h) >> 7) * row_pitch;
-            const uint32_t dst = dst0 + rr * kMaxSegBytes;
-            const uint32_t c0 = 16u * lane, c1 = c0 + 512u;  // segments are <= 784 bytes
-            if (c0 < len) cp_async16(dst + c0, src + c0);
-            if (c1 < len) cp_async16(dst + c1, src + c1);
-          }
+          for (int c = 0; c < 7; ++c)
+            if (j + 8u * c < nch) cp_async16(dst + 128u * c, src + 128u * c);
         }
         cp_async_commit();  // one group per quad (possibly empty) keeps wait_group counting uniform
       };
+      uint32_t slot_stage = 0, slot_use = 0;
 #pragma unroll
-      for (int k = 0; k < kQuadDepth; ++k) stage_quad(k);
+      for (int k = 0; k < kQuadDepth; ++k) {
+        stage_quad(k, slot_stage);
+        slot_stage = slot_stage + 1 == kQuadSlots ? 0 : slot_stage + 1;
+      }
       for (int g = 0; g < kGroups; ++g, ++gg) {
         const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph = (gg >> 1) & 1u;
 #pragma unroll
@@ -383,20 +387,21 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
         const uint32_t a_set = a_ring + set * kAKBlockBytes;
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
-          const int k = 4 * g + it;
-          stage_quad(k + kQuadDepth);
+          stage_quad(4 * g + it + kQuadDepth, slot_stage);
+          slot_stage = slot_stage + 1 == kQuadSlots ? 0 : slot_stage + 1;
           cp_async_wait<kQuadDepth>();  // this thread's copies of quad k have landed
           __syncwarp();                 // ... and every lane's
-          if (valid[it]) {
-            const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * it + r);
-            const uint32_t seg = slots + static_cast<uint32_t>(k % kQuadSlots) * kQuadSlotBytes + r * kMaxSegBytes;
-            const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
-            uint16_t* dbg = kDbg ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + m) * kFeatures + g * 192 + 24 * j
-                                 : nullptr;
-            if (fp16) convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
-            else convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
-          }
-          __syncwarp();  // slot k % kQuadSlots is refilled kQuadDepth quads later
+          // rows past the tile's count convert stale bytes into A rows whose results are masked
+          const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * it + r);
+          const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kMaxSegBytes;
+          const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
+          uint16_t* dbg = (kDbg && p.dbg_crops && tile * kTileM + m < count)
+                              ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + m) * kFeatures + g * 192 + 24 * j
+                              : nullptr;
+          if (fp16) convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
+          else convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
+          slot_use = slot_use + 1 == kQuadSlots ? 0 : slot_use + 1;
+          __syncwarp();  // the slot is refilled kQuadDepth quads later
         }
         fence_proxy_async_smem();
         __syncwarp();
