@@ -48,58 +48,58 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons polled through NVML every 5 ms during the timed region."""
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self._stop = threading.Event()
+        self.ok = False
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis and vis.split(",")[0].isdigit() else self.index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.ok = False
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((mhz, rs))
+            except Exception:
+                pass
+            self._stop.wait(0.005)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.ok:
+            self.t.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:]):
-                if v.lower() in ("active", "1"):
-                    reasons.add(n)
-        if not sm:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        nv = self.nv
+        names = {"hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+                 "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+                 "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+                 "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4)}
+        reasons = sorted({n for _, rs in self.samples for n, bit in names.items() if rs & bit})
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
 
 
 def _dist_env():
@@ -172,7 +172,8 @@ def run_gpu(args):
 
     from paper_2403_14902_b200 import build as B
     from paper_2403_14902_b200 import hydro as H
-    from synth import shard_range, workload
+    from paper_2403_14902_b200.dist import broadcast_unique_id, max_over_ranks, shard_ids
+    from synth import workload
 
     world, rank, local = _dist_env()
     if world != args.gpus:
@@ -189,11 +190,7 @@ def run_gpu(args):
         dist.barrier()
     w = workload("cfg2")
     frames = w.frames(device="cuda")
-    uid = None
-    if world > 1:
-        obj = [H.hydro_nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+    uid = broadcast_unique_id(dist, rank, H.hydro_nccl_unique_id) if world > 1 else None
     stream = torch.cuda.current_stream()
     e = H.Eddy(frames=frames, policy="score", warmup_tuples=65536, max_batch_tuples=1 << 20,
                max_inflight=4, rank=rank, world=world, sync_every=1, nccl_unique_id=uid, stream=stream)
@@ -202,7 +199,7 @@ def run_gpu(args):
     # per-rank contiguous shard of each step's id range (weak scaling: 1M tuples per GPU per step)
     batches = []
     for b in range(ROTATING_BATCHES):
-        start = (b * world + rank) * TUPLES_PER_STEP
+        start, _ = shard_ids(TUPLES_PER_STEP, rank, world, b)
         batches.append(w.tuples(id_start=start, n=TUPLES_PER_STEP, device="cuda"))
     res_ids = torch.empty(1 << 20, dtype=torch.int64, device="cuda")
     res_bb = torch.empty((1 << 20, 4), dtype=torch.int16, device="cuda")
@@ -241,9 +238,7 @@ def run_gpu(args):
     ms = ev0.elapsed_time(ev1)
     launches = e.launch_count() - launches0
     if dist:
-        tt = torch.tensor([ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = max_over_ranks(ms, dist, "cuda")
         dist.barrier()
     value = world * TUPLES_PER_STEP * args.steps / (ms / 1000.0)
 
@@ -295,9 +290,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     el = time.perf_counter() - t0
     if dist:
-        tt = torch.tensor([el], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        el = float(tt.item())
+        el = max_over_ranks(el, dist, "cuda")
     e2e_value = world * TUPLES_PER_STEP * args.steps / el
 
     order = e.order()
