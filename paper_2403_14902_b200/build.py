@@ -53,15 +53,17 @@ def nvcc() -> str:
     return p
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, extra=(), out: str = None) -> str:
+    """Compiles csrc/*.cu into libhydro.so (or `out` with extra nvcc flags, for A/B variants)."""
+    lib_out = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
     inc, lib = _nccl_dirs()
     cus = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr",
            "-I", os.path.join(ROOT, "include"), "-I", inc,
-           *cus, "-o", LIB + ".tmp",
+           *cus, "-o", lib_out + ".tmp",
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}", "-cudart", "static", *extra]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
@@ -70,10 +72,20 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
         raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
     if verbose:
         print(r.stdout + r.stderr, file=sys.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib_out + ".tmp", lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="--verbose" in sys.argv)
-    print(LIB)
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--variant", action="append", default=[],
+                    help="NAME:FLAGS -> libhydro_NAME.so built with the extra nvcc flags (A/B experiments)")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.verbose))
+    for v in a.variant:
+        name, _, flags = v.partition(":")
+        print(build(verbose=a.verbose, extra=tuple(flags.split()), out=os.path.join(HERE, f"libhydro_{name}.so")))

@@ -289,7 +289,7 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
 
 // kernels (defined in k_route.cu / k_classifier.cu), launched by runtime.cu
 __global__ void hydro_route_kernel(hydro::RouteParams p);
-template <bool kDbg>
+template <bool kDbg, bool kArea>
 __global__ void hydro_classifier_kernel(hydro::ClsParams p);
 __global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode);
 __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,

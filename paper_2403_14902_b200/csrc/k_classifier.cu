@@ -17,6 +17,9 @@
 //              exact u8 -> fp16 (PRMT 0x64vv = 1024+v, HSUB2 1024) or bf16, st.shared into the
 //              128B-swizzled K-major A ring (conflict-free), fence.proxy.async, arrive.
 // The A operand never touches HBM: only the crop-row segments of the frames are read.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "hydro_internal.cuh"
 
 using namespace hydro;
@@ -52,9 +55,18 @@ __device__ __forceinline__ uint32_t bf16x2_of_bytes(uint32_t lo, uint32_t hi) {
   return d;
 }
 
+__device__ __forceinline__ uint32_t ldg32(const uint8_t* p) { return __ldg(reinterpret_cast<const uint32_t*>(p)); }
+
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+// predicated load: lanes with !pred issue no shared-memory access
+__device__ __forceinline__ uint32_t lds32_if(uint32_t addr, bool pred) {
+  uint32_t v = 0;
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.b32 %0, [%1];\n}"
+               : "+r"(v) : "r"(addr), "r"(static_cast<uint32_t>(pred)));
   return v;
 }
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
@@ -141,7 +153,11 @@ __device__ __forceinline__ void convert_quad(uint32_t seg, const uint32_t (&po)[
       const uint32_t o = h2 ? (po[q] >> 16) : (po[q] & 0xFFFFu);
       const uint32_t a = (seg + o) & ~3u;
       const uint32_t w0 = lds32(a);
+#ifdef HYDRO_PRED_LDS
+      const uint32_t w1 = lds32_if(a + 4, (o & 3u) > 1u);  // only when the 3 bytes straddle words
+#else
       const uint32_t w1 = lds32(a + 4);
+#endif
       px[2 * q + h2] = __funnelshift_r(w0, w1, o << 3);
     }
   }
@@ -176,9 +192,55 @@ __device__ __forceinline__ void convert_quad(uint32_t seg, const uint32_t (&po)[
   }
 }
 
+// AREA crop (R10, cfg4): output pixel (dy, dx) is the mean over the bin
+// [y0 + dy*h//64, y0 + ceil((dy+1)h/64)) x [x0 + dx*w//64, x0 + ceil((dx+1)w/64)), one IEEE f32
+// division then bf16 round-to-nearest-even; the bf16 value is staged exactly (fp16 or bf16).
+// Bins are read straight from global memory (L1-cached); lane (r, j) makes pixels 8j .. 8j+7.
+template <bool kFp16, bool kDbg>
+__device__ __forceinline__ void convert_quad_area(const uint8_t* frames, uint32_t row0, uint32_t h, uint32_t x0,
+                                                  uint32_t w, uint32_t pitch, uint32_t g, uint32_t row_base,
+                                                  uint32_t j, uint32_t m, uint16_t* dbg) {
+  const uint32_t ys = (g * h) >> 6, ye = ((g + 1u) * h + 63u) >> 6;
+  uint32_t half[24];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t dx = 8u * j + k;
+    const uint32_t xs = x0 + ((dx * w) >> 6), xe = x0 + (((dx + 1u) * w + 63u) >> 6);
+    uint32_t s0 = 0, s1 = 0, s2 = 0;
+    for (uint32_t y = ys; y < ye; ++y) {
+      const uint8_t* rp = frames + row0 + y * pitch;
+      for (uint32_t x = xs; x < xe; ++x) {
+        const uint32_t o = 3u * x;
+        const uint32_t w0 = ldg32(rp + (o & ~3u));
+        const uint32_t w1 = (o & 3u) > 1u ? ldg32(rp + (o & ~3u) + 4) : 0u;
+        const uint32_t pxl = __funnelshift_r(w0, w1, o << 3);
+        s0 += pxl & 0xFFu;
+        s1 += (pxl >> 8) & 0xFFu;
+        s2 += (pxl >> 16) & 0xFFu;
+      }
+    }
+    const float cnt = static_cast<float>((ye - ys) * (xe - xs));
+    const uint32_t sums[3] = {s0, s1, s2};
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const __nv_bfloat16 b = __float2bfloat16_rn(__fdiv_rn(static_cast<float>(sums[ch]), cnt));
+      const uint32_t bbits = __bfloat16_as_ushort(b);
+      half[3 * k + ch] = kFp16 ? static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__bfloat162float(b)))) : bbits;
+      if (kDbg && dbg) dbg[3 * k + ch] = static_cast<uint16_t>(bbits);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const uint32_t c = 3u * j + t;
+    const uint32_t addr = row_base + (c >> 3) * kAKBlockBytes + (((c & 7u) ^ (m & 7u)) << 4);
+    sts128(addr, half[8 * t] | (half[8 * t + 1] << 16), half[8 * t + 2] | (half[8 * t + 3] << 16),
+           half[8 * t + 4] | (half[8 * t + 5] << 16), half[8 * t + 6] | (half[8 * t + 7] << 16));
+  }
+}
+
 extern __shared__ __align__(1024) uint8_t hydro_cls_smem[];
 
-template <bool kDbg>
+template <bool kDbg, bool kArea>
 __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsParams p) {
   DevState* st = p.st;
   // ---- dispatch (uniform across the CTA: every thread reads the same device words)
@@ -211,6 +273,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   const PredDev& pdg = p.preds[pred];
   const int n_classes = pdg.n_classes, n_pad = pdg.n_pad, target = pdg.target;
   const bool fp16 = pdg.a_fp16 != 0;
+  const bool area = kArea && pdg.crop_mode == HYDRO_CROP_AREA;  // kArea: the context has an AREA head
   const uint8_t* w_tiled = pdg.w_tiled;
   const int n_alloc = n_pad <= 32 ? 32 : (n_pad <= 64 ? 64 : 128);
   const uint32_t tmem_cols = 2u * n_alloc;
@@ -258,7 +321,10 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
 
   if (warp == kLoaderWarp) {
     // ===================== loader: weight K-blocks (bulk copy) + L2 prefetch of crop rows
-    constexpr int kPrefetchGroups = 4;
+#ifndef HYDRO_PF_GROUPS
+#define HYDRO_PF_GROUPS 4
+#endif
+    constexpr int kPrefetchGroups = HYDRO_PF_GROUPS;
     const uint64_t pol_w = policy_evict_last();  // weights are re-read by every tile: keep them in L2
     uint32_t itb = 0;
     for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -271,7 +337,11 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
           if (!mr[r].valid) continue;
           const uint32_t sy = static_cast<uint32_t>(((2 * g + 1) * mr[r].h) >> 7);
           const uint8_t* a = p.frames + mr[r].row0 + sy * row_pitch + mr[r].seg_lo;
+#ifdef HYDRO_L2_PREFETCH  // measured slightly slower on B200 (line-granular overfetch, L2 pressure)
           for (uint32_t c = 0; c < mr[r].seg_len; c += 128u) prefetch_line_l2(a + c);
+#else
+          (void)a;
+#endif
         }
       };
       for (int g = 0; g < kPrefetchGroups; ++g) prefetch_group(g);
@@ -359,7 +429,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       // Stage quad k = 4*g + it (rows 4*it .. 4*it+3 of this warp, crop row g) into slot k % kQuadSlots:
       // lanes 8r .. 8r+7 copy row r's segment in 16-byte chunks j + 8c (c < 7: segments <= 784 B).
       auto stage_quad = [&](int k, uint32_t slot) {
-        if (k < kGroups * 4) {
+        if (!area && k < kGroups * 4) {
           const int g = k >> 2, it = k & 3;
           const int src_lane = 4 * it + r;
           const uint32_t len = __shfl_sync(0xFFFFFFFFu, my_len, src_lane);
@@ -398,8 +468,19 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
           uint16_t* dbg = (kDbg && p.dbg_crops && tile * kTileM + m < count)
                               ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + m) * kFeatures + g * 192 + 24 * j
                               : nullptr;
-          if (fp16) convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
-          else convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
+          if (kArea && area) {
+            const int src_lane = 4 * it + r;
+            const uint32_t ar0 = __shfl_sync(0xFFFFFFFFu, mm.row0, src_lane);
+            const uint32_t ah = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.h), src_lane);
+            const uint32_t ax0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src_lane);
+            const uint32_t aw = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
+            if (fp16) convert_quad_area<true, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
+            else convert_quad_area<false, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
+          } else if (fp16) {
+            convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
+          } else {
+            convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
+          }
           slot_use = slot_use + 1 == kQuadSlots ? 0 : slot_use + 1;
           __syncwarp();  // the slot is refilled kQuadDepth quads later
         }
@@ -470,5 +551,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   }
 }
 
-template __global__ void hydro_classifier_kernel<false>(ClsParams p);
-template __global__ void hydro_classifier_kernel<true>(ClsParams p);
+template __global__ void hydro_classifier_kernel<false, false>(ClsParams p);
+template __global__ void hydro_classifier_kernel<true, false>(ClsParams p);
+template __global__ void hydro_classifier_kernel<false, true>(ClsParams p);
+template __global__ void hydro_classifier_kernel<true, true>(ClsParams p);

@@ -104,6 +104,7 @@ struct hydro_ctx {
   ncclComm_t comm = nullptr;
   int32_t fixed_order[kMaxPred];
   bool fixed_order_set = false;
+  bool has_area = false;
   // timing
   bool timing = false;
   std::vector<TimedLaunch> timed;
@@ -229,8 +230,10 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   }
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->k1_occ, hydro_route_kernel, kRouteThreads, 0));
   if (ctx->k1_occ < 1) ctx->k1_occ = 1;
-  CU(cudaFuncSetAttribute(hydro_classifier_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
-  CU(cudaFuncSetAttribute(hydro_classifier_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
+  CU(cudaFuncSetAttribute(hydro_classifier_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
+  CU(cudaFuncSetAttribute(hydro_classifier_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
+  CU(cudaFuncSetAttribute(hydro_classifier_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
+  CU(cudaFuncSetAttribute(hydro_classifier_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
   CU(cudaMalloc(&ctx->st, sizeof(DevState)));
   CU(cudaMemset(ctx->st, 0, sizeof(DevState)));
   CU(cudaMalloc(&ctx->preds_dev, sizeof(PredDev) * kMaxPred));
@@ -272,8 +275,8 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
     if (d->n_classes < 2 || d->n_classes > HYDRO_MAX_CLASSES) return set_err(HYDRO_EINVAL, "n_classes in [2, 128]");
     if (d->target < 0 || d->target >= d->n_classes) return set_err(HYDRO_EINVAL, "target outside [0, n_classes)");
     if (!d->weight_bf16 || !d->bias) return set_err(HYDRO_EINVAL, "LINEAR needs weight_bf16 and bias");
-    if (d->crop_mode != HYDRO_CROP_NEAREST)
-      return set_err(HYDRO_EINVAL, "crop_mode: only HYDRO_CROP_NEAREST is implemented in this build");
+    if (d->crop_mode != HYDRO_CROP_NEAREST && d->crop_mode != HYDRO_CROP_AREA)
+      return set_err(HYDRO_EINVAL, "crop_mode must be HYDRO_CROP_NEAREST or HYDRO_CROP_AREA");
     const int C = d->n_classes;
     ph.n_pad = next_pow2_pad(C);
     const size_t wbytes = static_cast<size_t>(C) * kFeatures * 2;
@@ -307,6 +310,7 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
   } else {
     return set_err(HYDRO_EINVAL, "unknown predicate kind");
   }
+  if (d->kind == HYDRO_PRED_LINEAR && d->crop_mode == HYDRO_CROP_AREA) ctx->has_area = true;
   ctx->preds.push_back(ph);
   if (pred_id) *pred_id = static_cast<int32_t>(ctx->preds.size() - 1);
   return HYDRO_OK;
@@ -479,10 +483,15 @@ static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_
   const uint64_t tiles = (max_positions + kTileM - 1) / kTileM;
   const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctx->num_sms)));
   return timed_launch(ctx, 1, [&] {
-    if (c.dbg_crops || c.dbg_logits || c.dbg_verdict)
-      hydro_classifier_kernel<true><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
-    else
-      hydro_classifier_kernel<false><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
+    // kernel instantiation by context capability: AREA support only when an AREA head exists
+    const bool dbg = c.dbg_crops || c.dbg_logits || c.dbg_verdict;
+    if (ctx->has_area) {
+      if (dbg) hydro_classifier_kernel<true, true><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
+      else hydro_classifier_kernel<false, true><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
+    } else {
+      if (dbg) hydro_classifier_kernel<true, false><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
+      else hydro_classifier_kernel<false, false><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
+    }
   });
 }
 

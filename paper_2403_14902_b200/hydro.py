@@ -14,7 +14,8 @@ from typing import Dict, List, Optional, Sequence
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhydro.so")
+# HYDRO_LIB_PATH selects an in-tree A/B variant (python -m paper_2403_14902_b200.build --variant ...)
+LIB_PATH = os.environ.get("HYDRO_LIB_PATH") or os.path.join(HERE, "libhydro.so")
 
 HYDRO_OK, HYDRO_EINVAL, HYDRO_ENOMEM, HYDRO_ECUDA, HYDRO_ENCCL, HYDRO_ESTATE, HYDRO_ERANGE, HYDRO_EBUSY = (
     0, -1, -2, -3, -4, -5, -6, -7)

@@ -18,9 +18,9 @@ Recipe (DESIGN.md §3 "Input recipe"):
   log-uniformly by octave in ``[w_min, w_min * 2**n_octaves)`` and clipped to
   the frame; the position is uniform inside the frame;
 * frames: HWC uint8 noise, ``n_frames`` x H x W x 3;
-* linear heads: integer weights in {-2..2} stored as bf16 (exact), half-integer
-  biases, so every logit is an exact multiple of 1/2 far below 2**23 and the
-  target's margin is never 0 (DESIGN.md reading R12);
+* linear heads: weights 2^-8 * {-2..2} stored as bf16 (exact), biases 2^-8 * (integer, +1/2 on
+  the target), so nearest-crop logits are exact multiples of 2^-9 and the target's margin is
+  never 0 (DESIGN.md reading R12);
 * HASH predicates: threshold ``T = round(sel * 2**32)``.
 """
 from __future__ import annotations
@@ -180,14 +180,17 @@ def target_offset_sigmas(n_classes: int, selectivity: float) -> float:
     return 0.5 * (lo + hi)
 
 
+WEIGHT_SCALE = 2.0 ** -8  # keeps AREA-crop logits (non-integer inputs) well inside fp32 (R12)
+
+
 def make_linear_head(seed: int, n_classes: int, target: int, selectivity: float,
                      k_features: int = K_FEATURES):
-    """Integer weights in {-2..2} (bf16-exact) and half-integer-offset biases.
+    """Weights s * {-2..2} (s = 2^-8; exact in bf16 and fp16) and half-integer-offset biases.
 
-    b_c = -floor(127.5 * sum_k W_ck) centres every logit; the target additionally
-    gets D + 0.5 with D = round(kappa * sigma) so that the (approximate, iid-Gaussian)
-    pass rate is ``selectivity``.  Only the target bias carries the 0.5, so the
-    target logit never ties another class.
+    b_c = -s * floor(127.5 * sum_k W_ck) centres every logit; the target additionally
+    gets s * (D + 0.5) with D = round(kappa * sigma) so that the (approximate, iid-Gaussian)
+    pass rate is ``selectivity``.  Only the target bias carries the s/2, so with integer
+    (nearest-crop) inputs every logit is an exact multiple of s/2 and the target never ties.
     """
     c = torch.arange(n_classes, dtype=torch.int64)[:, None]
     k = torch.arange(k_features, dtype=torch.int64)[None, :]
@@ -197,7 +200,8 @@ def make_linear_head(seed: int, n_classes: int, target: int, selectivity: float,
     sigma = math.sqrt(_PIX_VAR * float((wi * wi).sum(dim=1).to(torch.float64).mean()))
     kappa = target_offset_sigmas(n_classes, selectivity)
     bias[target] += round(kappa * sigma) + 0.5
-    return wi.to(torch.bfloat16), bias.to(torch.float32), {"kappa": kappa, "sigma": sigma}
+    return ((wi.to(torch.float64) * WEIGHT_SCALE).to(torch.bfloat16), (bias * WEIGHT_SCALE).to(torch.float32),
+            {"kappa": kappa, "sigma": sigma * WEIGHT_SCALE, "scale": WEIGHT_SCALE})
 
 
 # ----------------------------------------------------------------------------------------------

@@ -267,3 +267,56 @@ def test_cfg2_full_size_sampled_parity():
     info = infos[0]
     assert info["tuples_passed"][0] == int(lab.sum())
     e.close()
+
+
+# ------------------------------------------------------------------------ AREA crop / cfg4
+
+def test_linear_area_crops_logits_verdicts():
+    """cfg4's breed head on AREA crops: crops bit-exact (bf16 bin means), logits <= 1e-2 of f64."""
+    w = workload("cfg4", small=True, n=4000)
+    frames = w.frames()
+    n = 400
+    t = w.tuples(n=n)
+    k = 3
+    p = w.preds[k]
+    assert p["crop_mode"] == "area"
+    e = make_eddy(w, frames.cuda(), policy="fixed", warmup=0, max_batch=4096)
+    C = p["n_classes"]
+    logits = torch.full((n, C), float("nan"), device="cuda")
+    crops = torch.zeros((n, O.K_FEATURES), dtype=torch.int16, device="cuda")
+    verdict = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    e.debug_linear(k, t.to("cuda"), logits, crops, verdict)
+    tup = O.as_numpy_tuples(t)
+    fr = frames.numpy()
+    ref_crop = O.crop_area(fr, tup["frame_id"], tup["bbox"]).reshape(n, -1)
+    assert np.array_equal(crops.view(torch.bfloat16).float().cpu().numpy(), ref_crop)
+    v_ref, z_ref = O.linear_verdict(p, fr, tup["frame_id"], tup["bbox"], return_logits=True)
+    err = np.abs(logits.double().cpu().numpy() - z_ref).max()
+    assert err <= LOGIT_TOL, err
+    m = np.abs(O.margin(z_ref, p["target"]))
+    v = verdict.cpu().numpy().astype(bool)
+    assert np.all((v == v_ref) | (m < 2 * LOGIT_TOL))
+    e.close()
+
+
+def test_cfg4_small_end_to_end():
+    """cfg4 (label, area-weighted HASH, colour nearest, breed AREA) through the eddy; tuples whose
+    AREA-head margin is within 4x the logit tolerance are removed from the input (excluded by
+    construction), the rest must match the oracle row for row."""
+    w = workload("cfg4", small=True, n=6000)
+    frames = w.frames()
+    t = w.tuples()
+    tup = O.as_numpy_tuples(t)
+    fr = frames.numpy()
+    _, z = O.linear_verdict(w.preds[3], fr, tup["frame_id"], tup["bbox"], return_logits=True)
+    keep_in = np.abs(O.margin(z, w.preds[3]["target"])) >= 4 * LOGIT_TOL
+    t = t.select(torch.from_numpy(np.where(keep_in)[0]))
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, fr)
+    e = make_eddy(w, frames.cuda(), policy="score", warmup=1024, max_batch=2048)
+    ids, bbs, infos = run_stream(e, t.to("cuda"), 2048)
+    _assert_rows(ids, bbs, ref_ids, ref_bbox)
+    for b, info in enumerate(infos):
+        Vb = V[:, b * 2048:(b + 1) * 2048]
+        n_in, n_pass = expected_batch_counters(Vb, info["order_used"], 1024 if b == 0 else 0)
+        assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist()
+    e.close()

@@ -167,16 +167,16 @@ def test_argmax_lowest_index_on_ties_and_margin():
 
 
 def test_generator_makes_half_integer_target_margins():
-    """R12: integer logits + 0.5 on the target bias -> |margin| >= 0.5 for every tuple."""
+    """R12: logits are multiples of s/2 (s = 2^-8) with the target at an odd multiple -> |margin| >= s/2."""
     w = workload("cfg2", small=True)
     F = w.frames().numpy()
     t = w.tuples(n=300)
     tup = O.as_numpy_tuples(t)
     for p in w.preds[1:]:
         _, z = O.linear_verdict(p, F, tup["frame_id"], tup["bbox"], return_logits=True)
-        m = O.margin(z, p["target"])
-        assert np.all(np.abs(m) >= 0.5) and np.all(np.abs(z) < 2 ** 22)
-        assert np.all(np.mod(z[:, p["target"]], 1.0) == 0.5)
+        m = O.margin(z, p["target"]) / p["calib"]["scale"]
+        assert np.all(np.abs(m) >= 0.5) and np.all(np.abs(z / p["calib"]["scale"]) < 2 ** 22)
+        assert np.all(np.mod(z[:, p["target"]] / p["calib"]["scale"], 1.0) == 0.5)
 
 
 # ----------------------------------------------------------------------------- AND / order
