@@ -249,6 +249,7 @@ def run_gpu(args):
     k4_ms, k4_n = e.kernel_time(1)
     k1_ms, k1_n = e.kernel_time(0)
     k5_ms, k5_n = e.kernel_time(2)
+    k2c_ms, k2c_n = e.kernel_time(3)
     e.set_kernel_timing(False)
     k4_tuples = lin_in() - in0
     k4_bytes = k4_tuples * K4_BYTES_PER_TUPLE
@@ -319,7 +320,8 @@ def run_gpu(args):
                             "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                             "algorithmic_bytes_per_launch": k4_bytes / max(k4_n, 1),
                             "avg_launch_ms": k4_ms / max(k4_n, 1), "launches": k4_n,
-                            "share_of_step": k4_ms / max(k4_ms + k1_ms + k5_ms, 1e-9),
+                            "share_of_step": k4_ms / max(k4_ms + k1_ms + k5_ms + k2c_ms, 1e-9),
+                            "k2_ms_per_step": k2c_ms / args.steps,
                             "k1_ms_per_step": k1_ms / args.steps, "k4_ms_per_step": k4_ms / args.steps,
                             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"},
                "cpu_baseline": cpu,
@@ -332,6 +334,79 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
+def run_route(args):
+    """--workload rroute: evidence run for the route/compaction kernel K1 (SURVEY.md §8(d) R-route):
+    label='dog' (0.5) AND HASH (0.5, 1 unit) AND HASH (0.5, 1 unit) over 16M-tuple batches (352 MB of
+    columns per batch, far above L2), 96M tuples per step.  All three predicates are cheap, so one K1
+    launch per batch runs the whole chain and emits (id, bbox).  Algorithmic bytes per input tuple:
+    label 2 B + id 8 B (the fused run loads ids once for every alive position) + 16 B per emitted row."""
+    import torch
+
+    from paper_2403_14902_b200 import build as B
+    from paper_2403_14902_b200 import hydro as H
+    from synth import hash_pred, label_pred, workload
+
+    torch.cuda.set_device(0)
+    B.build()
+    batch, nb = 1 << 24, 6
+    w = workload("cfg2", n=batch)
+    w.preds = [label_pred(), hash_pred(31, 0.5, units=1), hash_pred(32, 0.5, units=1)]
+    stream = torch.cuda.current_stream()
+    e = H.Eddy(policy="score", warmup_tuples=65536, max_batch_tuples=batch, max_inflight=4, stream=stream)
+    for p in w.preds:
+        e.add_predicate(p)
+    batches = [w.tuples(id_start=b * batch, n=batch, device="cuda") for b in range(nb)]
+    res_ids = torch.empty(batch, dtype=torch.int64, device="cuda")
+    res_bb = torch.empty((batch, 4), dtype=torch.int16, device="cuda")
+    outs = []
+
+    def run_steps(k):
+        pend = []
+        for s in range(k * nb):
+            pend.append(e.submit(batches[s % nb]))
+            if len(pend) >= 3:
+                outs.append(H.hydro_collect_results(e.ctx, pend.pop(0), res_ids.data_ptr(), res_bb.data_ptr(), batch, 1))
+        for bid in pend:
+            outs.append(H.hydro_collect_results(e.ctx, bid, res_ids.data_ptr(), res_bb.data_ptr(), batch, 1))
+
+    run_steps(max(args.warmup, 3))
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    outs.clear()
+    with ClockSampler(0) as clk:
+        ev0.record(stream)
+        run_steps(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    n_out = sum(outs)
+    e.set_kernel_timing(True)
+    outs.clear()
+    run_steps(args.steps)
+    k1_ms, k1_n = e.kernel_time(0)
+    k2_ms, k2_n = e.kernel_time(3)
+    e.set_kernel_timing(False)
+    tuples = args.steps * nb * batch
+    alg_bytes = tuples * (2 + 8) + 16 * sum(outs)
+    peaks = _peaks()
+    achieved = alg_bytes / ((k1_ms + k2_ms) / 1000.0) / 1e9
+    out = {"metric": "tuples/s through the 3-predicate cheap conjunction (R-route evidence for K1+K2)",
+           "value": tuples / (ms / 1000.0), "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "u64", "data": "synthetic",
+           "config": {"workload": "R-route: label=dog AND hash(0.5) AND hash(0.5), 16M-tuple batches x 6 per step",
+                      "l2": "inputs larger than L2 (352 MB of columns per batch)", "results_per_step": n_out // max(args.steps, 1)},
+           "roofline": {"kernel": "hydro_route_kernel + hydro_compact_kernel (K1 evaluate + K2 compact/emit)",
+                        "bound": "hbm", "achieved": achieved,
+                        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                        "traffic": None, "algorithmic_bytes_per_tuple": 10 + 16 * sum(outs) / tuples,
+                        "k1_ms_per_step": k1_ms / args.steps, "k2_ms_per_step": k2_ms / args.steps,
+                        "k1_launches": k1_n, "k2_launches": k2_n},
+           "clocks": clk.summary()}
+    e.close()
+    print(json.dumps(out))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -340,11 +415,15 @@ def main():
     ap.add_argument("--impl", default="hydro", choices=["hydro", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute"],
+                    help="cfg2 = the BASELINE metric (default); rroute = K1 HBM evidence run")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "rroute":
+        run_route(args)
     else:
         run_gpu(args)
 

@@ -224,8 +224,8 @@ hydro_status hydro_synchronize(hydro_ctx* ctx);
 hydro_status hydro_launch_count(hydro_ctx* ctx, int64_t* launches);
 
 /* Kernel timing (CUDA events on the context stream around every launch of the kind):
-   enable = 1 starts recording (and clears), 0 stops.  kind: 0 = route/compact kernel (K1),
-   1 = classifier kernel (K4), 2 = fold (K5).  hydro_kernel_time synchronises and returns the
+   enable = 1 starts recording (and clears), 0 stops.  kind: 0 = route kernel (K1, cheap
+   predicates), 1 = classifier kernel (K4), 2 = fold (K5), 3 = compaction / emit kernel (K2).  hydro_kernel_time synchronises and returns the
    summed milliseconds and the number of launches recorded since the last enable. */
 hydro_status hydro_set_kernel_timing(hydro_ctx* ctx, int32_t enable);
 hydro_status hydro_kernel_time(hydro_ctx* ctx, int32_t kind, double* total_ms, int64_t* launches);

@@ -18,7 +18,10 @@ constexpr int kGroups = kNumKBlocks / kKBlocksPerGroup;  // 64 crop rows
 
 // ---- K1 (route / filter / compact) geometry
 constexpr int kRouteThreads = 256;
-constexpr int kRouteItems = 8;                              // positions per thread
+#ifndef HYDRO_K1_ITEMS
+#define HYDRO_K1_ITEMS 8
+#endif
+constexpr int kRouteItems = HYDRO_K1_ITEMS;                 // positions per thread
 constexpr int kRouteTile = kRouteThreads * kRouteItems;     // 2048 positions per tile
 
 // ---- K4 (classifier) geometry
@@ -77,7 +80,7 @@ struct DevState {
   double tot_cost[kMaxPred];
   double s_in[kMaxPred], s_pass[kMaxPred], s_cost[kMaxPred];
   double sel[kMaxPred], cost[kMaxPred], key[kMaxPred];
-  unsigned int k1_tile_ctr, k1_done_ctr;
+  unsigned int pad1, pad2;
 };
 
 struct BatchRec {
@@ -87,8 +90,9 @@ struct BatchRec {
   unsigned long long d_in[kMaxPred], d_pass[kMaxPred], d_cost[kMaxPred];
 };
 
-enum OutMode : int32_t { kOutList = 0, kOutEmit = 1, kOutBitmap = 2 };
-
+// K1: evaluate a run of cheap predicates -> verdict bitmap (bit per input position) + survivors
+// per 2048-position segment.  K2: compact (input positions, bitmap, segment counts) -> the next
+// alive list or the emitted (id, bbox) rows.  No inter-CTA waiting in either kernel.
 struct RouteParams {
   // ---- input positions: RANGE (list_in == nullptr): idx = range_base + p, p < range_n;
   //      LIST: idx = list_in[p], p < *count_in
@@ -98,36 +102,54 @@ struct RouteParams {
   const uint32_t* and_bits[kMaxPred];  // verdict bitmaps (bit p) ANDed into the alive mask
   int32_t n_and;
   // ---- which predicates: dispatch (device order) or explicit
-  int32_t dispatch;   // 1: hop = `hop`, decide on device from order[]; 0: explicit below
+  int32_t dispatch;       // 1: hop = `hop`, decided on device from order[]; 0: explicit below
   int32_t hop;
   int32_t explicit_pred;  // dispatch == 0: -1 = none, else evaluate this single predicate
   // ---- hop-indexed workspace (dispatch mode)
   uint32_t* lists;        // list h at lists + h * list_stride  (h = 1..P)
   uint64_t list_stride;
   uint32_t* counts;       // counts[h]
-  uint32_t* bits;         // K4 verdicts of hop h at bits + h * bits_stride
+  uint32_t* bits;         // verdicts of hop h at bits + h * bits_stride
   uint64_t bits_stride;
-  // ---- output (explicit mode, or dispatch EMIT)
-  int32_t out_mode;
-  uint32_t* list_out;
-  uint32_t* count_out;
-  uint32_t* bitmap_out;
-  uint64_t* out_ids;
-  uint64_t* out_bbox;
-  uint32_t* emit_count;          // EMIT: *emit_count = *emit_offset + survivors
-  const uint32_t* emit_offset;   // nullable
+  // ---- outputs
+  uint32_t* bitmap_out;   // explicit mode
+  uint32_t* seg_counts;   // survivors per 2048-position segment
   // ---- columns
   const uint64_t* id;
   const uint32_t* frame_id;
-  const uint64_t* bbox;          // 4 x u16 packed
+  const uint64_t* bbox;   // 4 x u16 packed
   const uint16_t* label;
   // ---- state
   DevState* st;
   const PredDev* preds;
-  unsigned long long* lb_status;
-  uint32_t epoch;
   int32_t collect_stats;
 };
+
+struct CompactParams {
+  int32_t dispatch;       // 1: hop from device order; 0: explicit
+  int32_t hop;
+  const uint32_t* list_in;  // explicit: nullptr = range
+  const uint32_t* count_in;
+  uint32_t range_base, range_n;
+  const uint32_t* bits_in;  // explicit
+  const uint32_t* seg_counts;
+  uint32_t* lists;
+  uint64_t list_stride;
+  uint32_t* counts;
+  const uint32_t* bits;
+  uint64_t bits_stride;
+  int32_t emit;             // explicit: 1 = emit rows, 0 = write list_out / count_out
+  uint32_t* list_out;
+  uint32_t* count_out;
+  uint64_t* out_ids;
+  uint64_t* out_bbox;
+  uint32_t* emit_count;        // *emit_count = *emit_offset + survivors
+  const uint32_t* emit_offset; // nullable
+  const uint64_t* id;
+  const uint64_t* bbox;
+  DevState* st;
+};
+constexpr int kCompactSegs = 16;  // 2048-position segments per K2 CTA
 
 struct ClsParams {
   int32_t dispatch;       // 1: hop from device order; 0: explicit_pred
@@ -142,6 +164,7 @@ struct ClsParams {
   uint32_t* bits;
   uint64_t bits_stride;
   uint32_t* bits_out;         // explicit mode output bitmap
+  uint32_t* seg_counts;       // survivors per 2048-position segment (atomically accumulated; zeroed by the host)
   const uint32_t* frame_id;
   const uint64_t* bbox;
   const uint8_t* frames;
@@ -289,6 +312,7 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
 
 // kernels (defined in k_route.cu / k_classifier.cu), launched by runtime.cu
 __global__ void hydro_route_kernel(hydro::RouteParams p);
+__global__ void hydro_compact_kernel(hydro::CompactParams p);
 template <bool kDbg, bool kArea>
 __global__ void hydro_classifier_kernel(hydro::ClsParams p);
 __global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode);

@@ -1,12 +1,13 @@
-// K1: route / filter / compact kernel, K5: statistics fold + rank + order, weight re-layout.
+// K1: route kernel (evaluate a run of cheap predicates), K2: compaction / emit, K5: statistics
+// fold + rank + order, weight re-layout.
 //
 // K1 evaluates a maximal run of cheap predicates (LABEL_EQ, HASH) in the device-resident order
-// on the still-alive positions of a routing batch, drops failing tuples at once (eager
-// materialization) with an order-preserving single-pass compaction
-// (warp ballot/popc + block scan + decoupled look-back across tiles), and accumulates the
-// per-predicate in / pass / cycle counters the eddy folds.
-// It also applies the verdict bitmap left by a classifier hop (K4), and emits the final
-// (id, bbox) rows (the query's projection).
+// on the still-alive positions of a routing batch and writes a verdict bitmap plus the survivors
+// per 2048-position segment, accumulating the per-predicate in / pass / cycle counters the eddy
+// folds.  K2 then drops the failing tuples at once (eager
+// materialization): an order-preserving compaction of the hop's input
+// positions into the next alive list, or the emitted (id, bbox) rows (the query's projection,
+// PAPER.md:44, 277).  K2 runs after every evaluator (K1 or the classifier K4).
 //
 // K5 folds the counters: S <- gamma*S + delta (R4), s = S_pass/S_in,
 // c = S_cost/S_in, key = c/(1-s), stable order by (key, id)
@@ -20,39 +21,6 @@ using namespace hydro;
 namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
-constexpr uint32_t kFlagAgg = 1, kFlagIncl = 2;
-
-__device__ __forceinline__ unsigned long long lb_pack(uint32_t epoch, uint32_t flag, uint32_t v) {
-  return (static_cast<unsigned long long>(epoch) << 32) | (static_cast<unsigned long long>(flag) << 30) |
-         static_cast<unsigned long long>(v & 0x3FFFFFFFu);
-}
-
-// Decoupled look-back (single-pass scan): publishes this tile's count, returns the number of
-// survivors of all earlier tiles.  Tiles are claimed in increasing order from an atomic
-// counter, so every predecessor is owned by a running CTA (no deadlock).
-__device__ uint32_t lookback_prefix(unsigned long long* status, uint32_t t, uint32_t total, uint32_t epoch) {
-  if (t == 0) {
-    st_release_u64(&status[0], lb_pack(epoch, kFlagIncl, total));
-    return 0;
-  }
-  st_release_u64(&status[t], lb_pack(epoch, kFlagAgg, total));
-  uint32_t prefix = 0;
-  int j = static_cast<int>(t) - 1;
-  while (true) {
-    unsigned long long v = ld_acquire_u64(&status[j]);
-    uint32_t e = static_cast<uint32_t>(v >> 32);
-    uint32_t flag = static_cast<uint32_t>(v >> 30) & 3u;
-    if (e != epoch || flag == 0) {
-      __nanosleep(20);
-      continue;
-    }
-    prefix += static_cast<uint32_t>(v & 0x3FFFFFFFu);
-    if (flag == kFlagIncl) break;
-    --j;
-  }
-  st_release_u64(&status[t], lb_pack(epoch, kFlagIncl, prefix + total));
-  return prefix;
-}
 
 __device__ __forceinline__ bool hash_pass(const PredDev& pd, uint64_t id, uint64_t bb) {
   int units = pd.units;
@@ -68,62 +36,58 @@ __device__ __forceinline__ bool hash_pass(const PredDev& pd, uint64_t id, uint64
   return static_cast<uint64_t>(h) < T;
 }
 
+// Which hop-h evaluator ran (device order): returns the first predicate's kind, and the cheap run
+// length in *run (0 when hop h is LINEAR or K1 has nothing to do).
+__device__ __forceinline__ bool k1_runs(const DevState* st, int h, int* run) {
+  const int P = st->n_pred;
+  *run = 0;
+  if (P == 0) return h == 0;
+  if (h >= P || st->kind[st->order[h]] == kLinear) return false;
+  if (h > 0 && st->kind[st->order[h - 1]] != kLinear) return false;  // inside a run started earlier
+  int r = 0;
+  while (h + r < P && st->kind[st->order[h + r]] != kLinear) ++r;
+  *run = r;
+  return true;
+}
+
 }  // namespace
 
+// ------------------------------------------------------------------------------------------
+// K1: evaluate.  Persistent grid, tile t = positions [2048 t, 2048 t + 2048); thread = 8 positions.
 __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams p) {
   __shared__ PredDev s_pred[kMaxPred];
   __shared__ int32_t s_run_id[kMaxPred];
   __shared__ unsigned long long s_in[kMaxPred], s_pass[kMaxPred], s_cost[kMaxPred];
-  __shared__ uint32_t s_warp_tot[kRouteThreads / 32], s_warp_excl[kRouteThreads / 32];
-  __shared__ uint32_t s_tile, s_prefix, s_emit_off;
-  __shared__ int32_t s_work, s_nrun, s_out_mode, s_n_and, s_need_id, s_need_bbox, s_need_label;
+  __shared__ uint32_t s_warp_cnt[kRouteThreads / 32];
+  __shared__ int32_t s_work, s_nrun, s_n_and, s_need_id, s_need_bbox, s_need_label;
   __shared__ const uint32_t* s_list_in;
   __shared__ const uint32_t* s_and[kMaxPred];
+  __shared__ uint32_t* s_bits_out;
   __shared__ uint32_t s_count, s_range_base;
-  __shared__ uint32_t* s_list_out;
-  __shared__ uint32_t* s_count_out;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   DevState* st = p.st;
 
   if (tid == 0) {
-    int32_t work = 1, nrun = 0, out_mode = p.out_mode, n_and = 0;
+    int32_t work = 1, nrun = 0, n_and = 0;
     const uint32_t* list_in = p.list_in;
-    uint32_t count = 0, base = p.range_base;
-    uint32_t* list_out = p.list_out;
-    uint32_t* count_out = p.count_out;
+    uint32_t count = 0;
+    uint32_t* bits_out = p.bitmap_out;
     if (p.dispatch) {
-      const int P = st->n_pred, h = p.hop;
-      if (h == 0) {
-        work = (P == 0) || (st->kind[st->order[0]] != kLinear);
-      } else {
-        work = (h <= P) && (st->kind[st->order[h - 1]] == kLinear);
-      }
+      const int h = p.hop;
+      int run = 0;
+      work = k1_runs(st, h, &run);
       if (work) {
-        // input of this launch = input of hop (h-1) filtered by its bitmap, or the range (h = 0)
-        const int in_h = (h == 0) ? 0 : h - 1;
-        if (in_h == 0) {
+        if (h == 0) {
           list_in = nullptr;
           count = p.range_n;
         } else {
-          list_in = p.lists + static_cast<uint64_t>(in_h) * p.list_stride;
-          count = p.counts[in_h];
+          list_in = p.lists + static_cast<uint64_t>(h) * p.list_stride;
+          count = p.counts[h];
         }
-        if (h > 0) {
-          s_and[0] = p.bits + static_cast<uint64_t>(h - 1) * p.bits_stride;
-          n_and = 1;
-        }
-        while (h + nrun < P && st->kind[st->order[h + nrun]] != kLinear) {
-          s_run_id[nrun] = st->order[h + nrun];
-          ++nrun;
-        }
-        if (h + nrun >= P) {
-          out_mode = kOutEmit;
-        } else {
-          out_mode = kOutList;
-          list_out = p.lists + static_cast<uint64_t>(h + nrun) * p.list_stride;
-          count_out = p.counts + (h + nrun);
-        }
+        for (int r = 0; r < run; ++r) s_run_id[r] = st->order[h + r];
+        nrun = run;
+        bits_out = p.bits + static_cast<uint64_t>(h) * p.bits_stride;
       }
     } else {
       count = list_in ? *p.count_in : p.range_n;
@@ -134,27 +98,6 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
         nrun = 1;
       }
     }
-    s_work = work;
-    s_nrun = nrun;
-    s_out_mode = out_mode;
-    s_n_and = n_and;
-    s_list_in = list_in;
-    s_count = count;
-    s_range_base = base;
-    s_list_out = list_out;
-    s_count_out = count_out;
-    s_emit_off = (out_mode == kOutEmit && p.emit_offset) ? *p.emit_offset : 0u;
-  }
-  __syncthreads();
-  if (!s_work) return;
-  const int nrun = s_nrun;
-  if (tid < nrun) {
-    s_pred[tid] = p.preds[s_run_id[tid]];
-    s_in[tid] = 0;
-    s_pass[tid] = 0;
-    s_cost[tid] = 0;
-  }
-  if (tid == 0) {
     int need_id = 0, need_bbox = 0, need_label = 0;
     for (int r = 0; r < nrun; ++r) {
       const PredDev& q = p.preds[s_run_id[r]];
@@ -165,27 +108,44 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
         need_label = 1;
       }
     }
+    s_work = work;
+    s_nrun = nrun;
+    s_n_and = n_and;
+    s_list_in = list_in;
+    s_count = count;
+    s_range_base = p.range_base;
+    s_bits_out = bits_out;
     s_need_id = need_id;
     s_need_bbox = need_bbox;
     s_need_label = need_label;
   }
+  __syncthreads();
+  if (!s_work) {
+    // hop h is a classifier hop: clear the segment counts its K4 accumulates into
+    if (p.dispatch && p.hop < st->n_pred && st->kind[st->order[p.hop]] == kLinear) {
+      const uint32_t n = p.hop == 0 ? p.range_n : p.counts[p.hop];
+      const uint32_t nseg = (n + kRouteTile - 1) / kRouteTile;
+      for (uint32_t i = blockIdx.x * kRouteThreads + tid; i < nseg; i += gridDim.x * kRouteThreads) p.seg_counts[i] = 0;
+    }
+    return;
+  }
+  const int nrun = s_nrun;
+  if (tid < nrun) {
+    s_pred[tid] = p.preds[s_run_id[tid]];
+    s_in[tid] = 0;
+    s_pass[tid] = 0;
+    s_cost[tid] = 0;
+  }
+  __syncthreads();
   const uint32_t count = s_count;
   const uint32_t num_tiles = (count + kRouteTile - 1) / kRouteTile;
-  const int out_mode = s_out_mode;
   const int n_and = s_n_and;
   const uint32_t* list_in = s_list_in;
   const uint32_t base = s_range_base;
-  if (num_tiles == 0 && blockIdx.x == 0 && tid == 0) {
-    if (out_mode == kOutEmit) *p.emit_count = s_emit_off;
-    else if (out_mode == kOutList) *s_count_out = 0;
-  }
-  __syncthreads();
+  uint32_t* bits_out = s_bits_out;
+  const bool need_id = s_need_id, need_bbox = s_need_bbox, need_label = s_need_label;
 
-  for (;;) {
-    if (tid == 0) s_tile = atomicAdd(&st->k1_tile_ctr, 1u);
-    __syncthreads();
-    const uint32_t t = s_tile;
-    if (t >= num_tiles) break;
+  for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
     const uint32_t p0 = t * kRouteTile + tid * kRouteItems;
     uint32_t idx[kRouteItems];
     uint32_t mask = 0;
@@ -223,7 +183,7 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
     uint64_t bbs[kRouteItems];
     uint32_t labs[kRouteItems / 2];
     if (mask) {
-      if (s_need_id) {
+      if (need_id) {
         if (contiguous && ((reinterpret_cast<uintptr_t>(p.id + base + p0) & 15u) == 0)) {
           const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p.id + base + p0);
 #pragma unroll
@@ -237,11 +197,11 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
           for (int j = 0; j < kRouteItems; ++j) ids[j] = ((mask >> j) & 1u) ? __ldg(p.id + idx[j]) : 0ull;
         }
       }
-      if (s_need_bbox) {
+      if (need_bbox) {
 #pragma unroll
         for (int j = 0; j < kRouteItems; ++j) bbs[j] = ((mask >> j) & 1u) ? __ldg(p.bbox + idx[j]) : 0ull;
       }
-      if (s_need_label) {
+      if (need_label) {
         if (contiguous && ((reinterpret_cast<uintptr_t>(p.label + base + p0) & 15u) == 0)) {
           const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.label + base + p0));
           labs[0] = v.x; labs[1] = v.y; labs[2] = v.z; labs[3] = v.w;
@@ -289,16 +249,124 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
       }
     }
 
-    if (out_mode == kOutBitmap) {
-      uint32_t b = mask << (8 * (lane & 3));
-      b |= __shfl_xor_sync(kFull, b, 1);
-      b |= __shfl_xor_sync(kFull, b, 2);
-      if ((lane & 3) == 0 && p0 < count) p.bitmap_out[p0 >> 5] = b;
-      __syncthreads();  // s_tile reuse
-      continue;
+    // verdict bitmap (4 threads per 32-bit word) and the tile's survivor count
+    uint32_t wbits = mask << (8 * (lane & 3));
+    wbits |= __shfl_xor_sync(kFull, wbits, 1);
+    wbits |= __shfl_xor_sync(kFull, wbits, 2);
+    if ((lane & 3) == 0 && p0 < count) bits_out[p0 >> 5] = wbits;
+    const uint32_t wc = __reduce_add_sync(kFull, __popc(mask));
+    if (lane == 0) s_warp_cnt[warp] = wc;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t tot = 0;
+#pragma unroll
+      for (int w = 0; w < kRouteThreads / 32; ++w) tot += s_warp_cnt[w];
+      p.seg_counts[t] = tot;
     }
+    __syncthreads();
+  }
 
-    // ---- order-preserving compaction: warp scan -> block scan -> decoupled look-back
+  if (p.collect_stats && tid < nrun) {
+    const int k = s_run_id[tid];
+    atomicAdd(&st->d_in[k], s_in[tid]);
+    atomicAdd(&st->d_pass[k], s_pass[tid]);
+    atomicAdd(&st->d_cost[k], s_cost[tid]);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K2: order-preserving compaction (eager materialization).  CTA c owns
+// segments [16c, 16c + 16); its output offset is the sum of all earlier segments' counts (<= a few
+// thousand L2-resident words), so no CTA ever waits for another.  Within a segment: warp ballot /
+// popc + block scan; survivors are written in input order.
+__global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactParams p) {
+  __shared__ uint32_t s_warp_tot[kRouteThreads / 32], s_warp_excl[kRouteThreads / 32];
+  __shared__ uint32_t s_red[kRouteThreads / 32];
+  __shared__ int32_t s_work, s_emit;
+  __shared__ const uint32_t* s_list_in;
+  __shared__ const uint32_t* s_bits;
+  __shared__ uint32_t* s_list_out;
+  __shared__ uint32_t* s_count_out;
+  __shared__ uint32_t s_count, s_emit_off;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    int32_t work = 1, emit = p.emit;
+    const uint32_t* list_in = p.list_in;
+    const uint32_t* bits = p.bits_in;
+    uint32_t* list_out = p.list_out;
+    uint32_t* count_out = p.count_out;
+    uint32_t count = 0;
+    if (p.dispatch) {
+      const DevState* st = p.st;
+      const int h = p.hop, P = st->n_pred;
+      int run = 0;
+      int next;
+      if (k1_runs(st, h, &run)) {
+        next = h + run;
+      } else if (h < P && st->kind[st->order[h]] == kLinear) {
+        next = h + 1;
+      } else {
+        work = 0;
+        next = 0;
+      }
+      if (work) {
+        if (h == 0) {
+          list_in = nullptr;
+          count = p.range_n;
+        } else {
+          list_in = p.lists + static_cast<uint64_t>(h) * p.list_stride;
+          count = p.counts[h];
+        }
+        bits = p.bits + static_cast<uint64_t>(h) * p.bits_stride;
+        emit = next >= P;
+        if (!emit) {
+          list_out = p.lists + static_cast<uint64_t>(next) * p.list_stride;
+          count_out = p.counts + next;
+        }
+      }
+    } else {
+      count = list_in ? *p.count_in : p.range_n;
+    }
+    s_work = work;
+    s_emit = emit;
+    s_list_in = list_in;
+    s_bits = bits;
+    s_list_out = list_out;
+    s_count_out = count_out;
+    s_count = count;
+    s_emit_off = (emit && p.emit_offset) ? *p.emit_offset : 0u;
+  }
+  __syncthreads();
+  if (!s_work) return;
+  const uint32_t count = s_count;
+  const uint32_t nseg = (count + kRouteTile - 1) / kRouteTile;
+  const uint32_t seg0 = blockIdx.x * kCompactSegs;
+  const bool emit = s_emit;
+  const uint32_t* list_in = s_list_in;
+  const uint32_t* bits = s_bits;
+  const uint32_t base = p.range_base;
+  if (seg0 >= nseg && !(nseg == 0 && blockIdx.x == 0)) return;
+
+  // output offset of this CTA: survivors of every earlier segment
+  uint32_t part = 0;
+  for (uint32_t s = tid; s < seg0; s += kRouteThreads) part += __ldg(p.seg_counts + s);
+  part = __reduce_add_sync(kFull, part);
+  if (lane == 0) s_red[warp] = part;
+  __syncthreads();
+  uint32_t prefix = 0;
+#pragma unroll
+  for (int w = 0; w < kRouteThreads / 32; ++w) prefix += s_red[w];
+  prefix += s_emit_off;
+
+  const uint32_t seg1 = min(seg0 + kCompactSegs, nseg);
+  for (uint32_t sgi = seg0; sgi < seg1; ++sgi) {
+    const uint32_t p0 = sgi * kRouteTile + tid * kRouteItems;
+    uint32_t mask = 0;
+    if (p0 < count) {
+      mask = (__ldg(bits + (p0 >> 5)) >> (p0 & 31)) & 0xFFu;
+      if (p0 + kRouteItems > count) mask &= (1u << (count - p0)) - 1u;
+    }
     const uint32_t c = __popc(mask);
     uint32_t x = c;
 #pragma unroll
@@ -310,59 +378,43 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
     __syncthreads();
     if (warp == 0) {
       const uint32_t v = lane < kRouteThreads / 32 ? s_warp_tot[lane] : 0u;
-      uint32_t s = v;
+      uint32_t sc = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, s, o);
-        if (lane >= o) s += y;
+        const uint32_t y = __shfl_up_sync(kFull, sc, o);
+        if (lane >= o) sc += y;
       }
-      if (lane < kRouteThreads / 32) s_warp_excl[lane] = s - v;
-      const uint32_t tile_total = __shfl_sync(kFull, s, kRouteThreads / 32 - 1);
-      if (lane == 0) {
-        const uint32_t prefix = lookback_prefix(p.lb_status, t, tile_total, p.epoch);
-        s_prefix = prefix;
-        if (t == num_tiles - 1) {
-          if (out_mode == kOutEmit) *p.emit_count = s_emit_off + prefix + tile_total;
-          else *s_count_out = prefix + tile_total;
-        }
-      }
+      if (lane < kRouteThreads / 32) s_warp_excl[lane] = sc - v;
+      if (lane == kRouteThreads / 32 - 1) s_warp_tot[0] = sc;  // segment total (read after the barrier)
     }
     __syncthreads();
-    uint32_t pos = s_prefix + s_warp_excl[warp] + (x - c);
-    if (out_mode == kOutList) {
-      uint32_t* out = s_list_out;
+    uint32_t pos = prefix + s_warp_excl[warp] + (x - c);
+    const uint32_t seg_total = s_warp_tot[0];
+    if (mask) {
+      if (!emit) {
 #pragma unroll
-      for (int j = 0; j < kRouteItems; ++j)
-        if ((mask >> j) & 1u) out[pos++] = idx[j];
-    } else {  // emit (id, bbox)
-      pos += s_emit_off;
+        for (int j = 0; j < kRouteItems; ++j)
+          if ((mask >> j) & 1u) s_list_out[pos++] = list_in ? __ldg(list_in + p0 + j) : base + p0 + j;
+      } else {
 #pragma unroll
-      for (int j = 0; j < kRouteItems; ++j) {
-        if ((mask >> j) & 1u) {
-          p.out_ids[pos] = __ldg(p.id + idx[j]);
-          p.out_bbox[pos] = __ldg(p.bbox + idx[j]);
-          ++pos;
+        for (int j = 0; j < kRouteItems; ++j) {
+          if ((mask >> j) & 1u) {
+            const uint32_t idx = list_in ? __ldg(list_in + p0 + j) : base + p0 + j;
+            p.out_ids[pos] = __ldg(p.id + idx);
+            p.out_bbox[pos] = __ldg(p.bbox + idx);
+            ++pos;
+          }
         }
       }
     }
-    __syncthreads();  // s_tile / s_prefix / s_warp_* reuse
+    prefix += seg_total;
+    __syncthreads();  // s_warp_* reuse
   }
-
-  __syncthreads();
-  if (p.collect_stats && tid < nrun) {
-    const int k = s_run_id[tid];
-    atomicAdd(&st->d_in[k], s_in[tid]);
-    atomicAdd(&st->d_pass[k], s_pass[tid]);
-    atomicAdd(&st->d_cost[k], s_cost[tid]);
-  }
-  if (tid == 0) {
-    __threadfence();
-    const uint32_t prev = atomicAdd(&st->k1_done_ctr, 1u);
-    if (prev == gridDim.x - 1) {  // last CTA: self-reset the tile counters for the next launch
-      st->k1_tile_ctr = 0;
-      st->k1_done_ctr = 0;
-      __threadfence();
-    }
+  // the CTA holding the last segment publishes the count
+  const bool last = (nseg == 0) ? (blockIdx.x == 0) : (seg1 == nseg);
+  if (last && tid == 0) {
+    if (emit) *p.emit_count = prefix;
+    else *s_count_out = prefix;
   }
 }
 

@@ -94,11 +94,11 @@ struct hydro_ctx {
   uint32_t* bits = nullptr;
   uint64_t bits_stride = 0;
   uint32_t* warm_bits = nullptr;
-  unsigned long long* lb_status = nullptr;
+  uint32_t* seg_counts = nullptr;
+  uint32_t* warm_and = nullptr;
   uint32_t* zero_word = nullptr;
   std::vector<Slot> slots;
   int64_t next_batch = 0;
-  uint32_t epoch = 1;
   int64_t launches = 0;
   int64_t since_sync = 0;
   ncclComm_t comm = nullptr;
@@ -402,9 +402,10 @@ static hydro_status freeze(hydro_ctx* ctx) {
   ctx->bits_stride = ((maxb + 31) / 32 + 3) & ~3ull;
   CU(cudaMalloc(&ctx->bits, sizeof(uint32_t) * ctx->bits_stride * std::max(P, 1)));
   CU(cudaMalloc(&ctx->warm_bits, sizeof(uint32_t) * ctx->bits_stride * std::max(P, 1)));
-  const uint64_t max_tiles = (maxb + kRouteTile - 1) / kRouteTile + 1;
-  CU(cudaMalloc(&ctx->lb_status, sizeof(unsigned long long) * max_tiles));
-  CU(cudaMemset(ctx->lb_status, 0, sizeof(unsigned long long) * max_tiles));
+  const uint64_t max_segs = (maxb + kRouteTile - 1) / kRouteTile + 1;
+  CU(cudaMalloc(&ctx->seg_counts, sizeof(uint32_t) * max_segs));
+  CU(cudaMemset(ctx->seg_counts, 0, sizeof(uint32_t) * max_segs));
+  CU(cudaMalloc(&ctx->warm_and, sizeof(uint32_t) * ctx->bits_stride));
   ctx->slots.resize(ctx->cfg.max_inflight);
   for (Slot& s : ctx->slots) {
     CU(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
@@ -434,16 +435,32 @@ static RouteParams route_base(hydro_ctx* ctx, const uint64_t* id, const uint32_t
   r.counts = ctx->counts;
   r.bits = ctx->bits;
   r.bits_stride = ctx->bits_stride;
+  r.seg_counts = ctx->seg_counts;
   r.id = id;
   r.frame_id = fr;
   r.bbox = bb;
   r.label = lab;
   r.st = ctx->st;
   r.preds = ctx->preds_dev;
-  r.lb_status = ctx->lb_status;
   r.collect_stats = 1;
   r.explicit_pred = -1;
   return r;
+}
+
+static CompactParams compact_base(hydro_ctx* ctx, const uint64_t* id, const uint64_t* bb, Slot& sl) {
+  CompactParams c{};
+  c.seg_counts = ctx->seg_counts;
+  c.lists = ctx->lists;
+  c.list_stride = ctx->list_stride;
+  c.counts = ctx->counts;
+  c.bits = ctx->bits;
+  c.bits_stride = ctx->bits_stride;
+  c.out_ids = sl.out_ids;
+  c.out_bbox = sl.out_bbox;
+  c.id = id;
+  c.bbox = bb;
+  c.st = ctx->st;
+  return c;
 }
 
 static ClsParams cls_base(hydro_ctx* ctx, const uint32_t* fr, const uint64_t* bb) {
@@ -461,6 +478,7 @@ static ClsParams cls_base(hydro_ctx* ctx, const uint32_t* fr, const uint64_t* bb
   c.frame_w = ctx->cfg.frame_w;
   c.st = ctx->st;
   c.preds = ctx->preds_dev;
+  c.seg_counts = ctx->seg_counts;
   c.collect_stats = 1;
   c.explicit_pred = -1;
   return c;
@@ -468,15 +486,23 @@ static ClsParams cls_base(hydro_ctx* ctx, const uint32_t* fr, const uint64_t* bb
 
 static int route_grid(hydro_ctx* ctx, uint64_t positions) {
   const uint64_t tiles = (positions + kRouteTile - 1) / kRouteTile;
+#ifdef HYDRO_K1_ONE_TILE_PER_CTA
+  const uint64_t cap = 1u << 20;
+#else
   const uint64_t cap = static_cast<uint64_t>(ctx->num_sms) * ctx->k1_occ;
+#endif
   return static_cast<int>(std::max<uint64_t>(1, std::min(tiles, cap)));
 }
 
-static hydro_status launch_route(hydro_ctx* ctx, RouteParams r, uint64_t max_positions) {
-  r.epoch = ctx->epoch++;
-  if (ctx->epoch == 0) ctx->epoch = 1;
+static hydro_status launch_route(hydro_ctx* ctx, const RouteParams& r, uint64_t max_positions) {
   const int grid = route_grid(ctx, max_positions);
   return timed_launch(ctx, 0, [&] { hydro_route_kernel<<<grid, kRouteThreads, 0, ctx->stream>>>(r); });
+}
+
+static hydro_status launch_compact(hydro_ctx* ctx, const CompactParams& c, uint64_t max_positions) {
+  const uint64_t segs = (max_positions + kRouteTile - 1) / kRouteTile;
+  const int grid = static_cast<int>(std::max<uint64_t>(1, (segs + kCompactSegs - 1) / kCompactSegs));
+  return timed_launch(ctx, 3, [&] { hydro_compact_kernel<<<grid, kRouteThreads, 0, ctx->stream>>>(c); });
 }
 
 static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_positions) {
@@ -584,40 +610,42 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
         r.explicit_pred = k;
         r.range_base = 0;
         r.range_n = static_cast<uint32_t>(warm);
-        r.out_mode = kOutBitmap;
         r.bitmap_out = wb;
         if ((s = launch_route(ctx, r, warm)) != HYDRO_OK) return s;
       }
     }
+    // AND of the P verdict bitmaps -> K2 emits the slice's rows first in the batch output
     RouteParams r = route_base(ctx, id, fr, bb, lab);
     r.dispatch = 0;
     r.range_base = 0;
     r.range_n = static_cast<uint32_t>(warm);
     r.n_and = P;
     for (int k = 0; k < P; ++k) r.and_bits[k] = ctx->warm_bits + static_cast<uint64_t>(k) * ctx->bits_stride;
-    r.out_mode = kOutEmit;
-    r.out_ids = sl.out_ids;
-    r.out_bbox = sl.out_bbox;
-    r.emit_count = &sl.rec->warm_count;
-    r.emit_offset = nullptr;
+    r.bitmap_out = ctx->warm_and;
     r.collect_stats = 0;
     if ((s = launch_route(ctx, r, warm)) != HYDRO_OK) return s;
+    CompactParams c = compact_base(ctx, id, bb, sl);
+    c.dispatch = 0;
+    c.range_base = 0;
+    c.range_n = static_cast<uint32_t>(warm);
+    c.bits_in = ctx->warm_and;
+    c.emit = 1;
+    c.emit_count = &sl.rec->warm_count;
+    c.emit_offset = nullptr;
+    if ((s = launch_compact(ctx, c, warm)) != HYDRO_OK) return s;
     if ((s = fold_and_sync(ctx, sl.rec, 0, true)) != HYDRO_OK) return s;
     ctx->warmup_pending = false;
   }
-  // ---- the eddy chain on the rest of the batch
+  // ---- the eddy chain on the rest of the batch: per hop, the evaluator (K1 for a run of cheap
+  // predicates, or K4 for a classifier) then K2 compaction into the next hop's alive list / emit
   const uint32_t rest_base = static_cast<uint32_t>(warm);
   const uint32_t rest_n = static_cast<uint32_t>(n - warm);
-  for (int h = 0; h <= P; ++h) {
+  for (int h = 0; h < std::max(P, 1); ++h) {
     RouteParams r = route_base(ctx, id, fr, bb, lab);
     r.dispatch = 1;
     r.hop = h;
     r.range_base = rest_base;
     r.range_n = rest_n;
-    r.out_ids = sl.out_ids;
-    r.out_bbox = sl.out_bbox;
-    r.emit_count = &sl.rec->total_count;
-    r.emit_offset = &sl.rec->warm_count;
     if ((s = launch_route(ctx, r, rest_n)) != HYDRO_OK) return s;
     if (h < P) {
       ClsParams c = cls_base(ctx, fr, bb);
@@ -627,6 +655,14 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
       c.range_n = rest_n;
       if ((s = launch_cls(ctx, c, rest_n)) != HYDRO_OK) return s;
     }
+    CompactParams k2 = compact_base(ctx, id, bb, sl);
+    k2.dispatch = 1;
+    k2.hop = h;
+    k2.range_base = rest_base;
+    k2.range_n = rest_n;
+    k2.emit_count = &sl.rec->total_count;
+    k2.emit_offset = &sl.rec->warm_count;
+    if ((s = launch_compact(ctx, k2, rest_n)) != HYDRO_OK) return s;
   }
   if ((s = fold_and_sync(ctx, sl.rec, 1, false)) != HYDRO_OK) return s;
   CU(cudaEventRecord(sl.done, ctx->stream));
@@ -849,7 +885,8 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
   cudaFree(ctx->counts);
   cudaFree(ctx->bits);
   cudaFree(ctx->warm_bits);
-  cudaFree(ctx->lb_status);
+  cudaFree(ctx->seg_counts);
+  cudaFree(ctx->warm_and);
   cudaFree(ctx->zero_word);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
