@@ -139,7 +139,10 @@ typedef struct {
   int64_t n;
   int32_t on_device;          /* 1: DEVICE columns, BORROWED until the batch is collected
                                    (not validated: out-of-range values are clamped in-kernel);
-                                 0: HOST columns, validated and copied before return          */
+                                 0: HOST columns (pinned memory recommended), validated on the
+                                   host, then uploaded asynchronously on the context's copy
+                                   stream so batch k+1's upload overlaps batch k's kernels:
+                                   BORROWED until the batch is collected                       */
 } hydro_tuples;
 
 typedef struct {
@@ -193,7 +196,8 @@ hydro_status hydro_set_fixed_order(hydro_ctx* ctx, const int32_t* order, int32_t
 /* Enqueues one routing batch on the context's stream and returns its id (0, 1, 2 ...).
    Asynchronous: returns before the GPU work finishes.  n == 0 is legal (0 results).
    EINVAL: n > max_batch_tuples, NULL columns, invalid host tuples.  EBUSY: max_inflight
-   batches are uncollected.  The results are the passing (id, bbox) rows in input order. */
+   batches are uncollected.  The results are the passing (id, bbox) rows in input order.
+   The columns (host or device) must stay valid until the batch is collected or released. */
 hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* tuples, int64_t* batch_id);
 
 /* Blocks until batch_id finished and returns its result count. */

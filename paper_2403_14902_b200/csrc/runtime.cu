@@ -55,6 +55,7 @@ struct Slot {
   int64_t n = 0;
   int64_t warm_n = 0;
   cudaEvent_t done = nullptr;
+  cudaEvent_t uploaded = nullptr;
   uint64_t* out_ids = nullptr;
   uint64_t* out_bbox = nullptr;
   BatchRec* rec = nullptr;
@@ -77,6 +78,7 @@ struct TimedLaunch {
 struct hydro_ctx {
   hydro_config cfg{};
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host -> device uploads of batch k+1 overlap batch k
   bool own_stream = false;
   int num_sms = 0;
   int k1_occ = 1;
@@ -228,6 +230,7 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
     CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     ctx->own_stream = true;
   }
+  CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->k1_occ, hydro_route_kernel, kRouteThreads, 0));
   if (ctx->k1_occ < 1) ctx->k1_occ = 1;
   CU(cudaFuncSetAttribute(hydro_classifier_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
@@ -409,6 +412,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
   ctx->slots.resize(ctx->cfg.max_inflight);
   for (Slot& s : ctx->slots) {
     CU(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&s.uploaded, cudaEventDisableTiming));
     CU(cudaMalloc(&s.out_ids, sizeof(uint64_t) * maxb));
     CU(cudaMalloc(&s.out_bbox, sizeof(uint64_t) * maxb));
     CU(cudaMalloc(&s.rec, sizeof(BatchRec)));
@@ -578,10 +582,13 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
   if (!t->on_device && n > 0) {
     if ((s = validate_host_tuples(ctx, t)) != HYDRO_OK) return s;
     if ((s = ensure_staging(ctx, sl)) != HYDRO_OK) return s;
-    CU(cudaMemcpyAsync(sl.s_id, t->id, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaMemcpyAsync(sl.s_frame, t->frame_id, 4 * n, cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaMemcpyAsync(sl.s_bbox, t->bbox, 8 * n, cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaMemcpyAsync(sl.s_label, t->label, 2 * n, cudaMemcpyHostToDevice, ctx->stream));
+    // upload on the copy stream (overlaps the previous batch's kernels); the compute stream waits
+    CU(cudaMemcpyAsync(sl.s_id, t->id, 8 * n, cudaMemcpyHostToDevice, ctx->copy_stream));
+    CU(cudaMemcpyAsync(sl.s_frame, t->frame_id, 4 * n, cudaMemcpyHostToDevice, ctx->copy_stream));
+    CU(cudaMemcpyAsync(sl.s_bbox, t->bbox, 8 * n, cudaMemcpyHostToDevice, ctx->copy_stream));
+    CU(cudaMemcpyAsync(sl.s_label, t->label, 2 * n, cudaMemcpyHostToDevice, ctx->copy_stream));
+    CU(cudaEventRecord(sl.uploaded, ctx->copy_stream));
+    CU(cudaStreamWaitEvent(ctx->stream, sl.uploaded, 0));
     id = sl.s_id;
     fr = sl.s_frame;
     bb = sl.s_bbox;
@@ -714,10 +721,12 @@ hydro_status hydro_collect_results(hydro_ctx* ctx, int64_t batch_id, uint64_t* i
   if (capacity < c) return set_err(HYDRO_ERANGE, "capacity < result count");
   if (c > 0) {
     if (!ids || !bboxes) return set_err(HYDRO_EINVAL, "NULL output buffer");
+    // copy on the copy stream after this batch only (the compute stream may already run later batches)
     const cudaMemcpyKind k = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    CU(cudaMemcpyAsync(ids, sl->out_ids, 8 * c, k, ctx->stream));
-    CU(cudaMemcpyAsync(bboxes, sl->out_bbox, 8 * c, k, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->copy_stream, sl->done, 0));
+    CU(cudaMemcpyAsync(ids, sl->out_ids, 8 * c, k, ctx->copy_stream));
+    CU(cudaMemcpyAsync(bboxes, sl->out_bbox, 8 * c, k, ctx->copy_stream));
+    CU(cudaStreamSynchronize(ctx->copy_stream));
   }
   sl->busy = false;
   return HYDRO_OK;
@@ -862,6 +871,7 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slot& s : ctx->slots) {
     if (s.done) cudaEventDestroy(s.done);
+    if (s.uploaded) cudaEventDestroy(s.uploaded);
     cudaFree(s.out_ids);
     cudaFree(s.out_bbox);
     cudaFree(s.rec);
@@ -889,6 +899,10 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
   cudaFree(ctx->warm_and);
   cudaFree(ctx->zero_word);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return HYDRO_OK;
