@@ -98,7 +98,9 @@ typedef struct {
   int32_t sync_every;        /* world > 1: fold (after an NCCL all-reduce of the statistics
                                 deltas) every sync_every batches (default 1)                  */
   const void* nccl_unique_id;/* world > 1: the 128-byte ncclUniqueId from
-                                hydro_nccl_unique_id() on rank 0, broadcast by the caller    */
+                                hydro_nccl_unique_id() on rank 0, broadcast by the caller.
+                                Also accepted with world == 1 (a 1-rank communicator: the fold
+                                then runs the same NCCL all-reduce path as a multi-GPU run)  */
   const uint8_t* frames;     /* DEVICE frame pool, HWC uint8 [n_frames][frame_h][frame_w][3],
                                 BORROWED for the context's lifetime (R11); may be NULL when no
                                 LINEAR predicate is used                                      */

@@ -242,7 +242,7 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   CU(cudaMalloc(&ctx->preds_dev, sizeof(PredDev) * kMaxPred));
   CU(cudaMalloc(&ctx->zero_word, 16));
   CU(cudaMemset(ctx->zero_word, 0, 16));
-  if (cfg->world > 1) {
+  if (cfg->nccl_unique_id) {  // world > 1, or world == 1 with an id: exercise the NCCL merge path
     ncclUniqueId id;
     std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank);
@@ -531,7 +531,7 @@ static hydro_status launch_fold(hydro_ctx* ctx, BatchRec* rec, int mode) {
 
 static hydro_status fold_and_sync(hydro_ctx* ctx, BatchRec* rec, int record, bool force_sync) {
   hydro_status s;
-  if (ctx->cfg.world == 1) return launch_fold(ctx, rec, 1 | 2 | (record ? 4 : 0));
+  if (!ctx->comm) return launch_fold(ctx, rec, 1 | 2 | (record ? 4 : 0));
   if ((s = launch_fold(ctx, rec, 1 | (record ? 4 : 0))) != HYDRO_OK) return s;
   ctx->since_sync += record ? 1 : 0;
   if (force_sync || ctx->since_sync >= ctx->cfg.sync_every) {

@@ -320,3 +320,24 @@ def test_cfg4_small_end_to_end():
         n_in, n_pass = expected_batch_counters(Vb, info["order_used"], 1024 if b == 0 else 0)
         assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist()
     e.close()
+
+
+def test_nccl_statistics_path_single_rank_matches():
+    """The multi-GPU fold path (NCCL all-reduce of the pending deltas, then fold) on a 1-rank
+    communicator gives the same rows, orders and statistics as the plain path."""
+    from paper_2403_14902_b200 import hydro as H
+
+    w = workload("cfg2", small=True, n=12000)
+    frames = w.frames()
+    t = w.tuples().to("cuda")
+    runs = []
+    for uid in (None, H.hydro_nccl_unique_id()):
+        e = H.Eddy(frames=frames.cuda(), policy="score", cost_source="declared", warmup_tuples=1024,
+                   max_batch_tuples=3000, world=1, rank=0, nccl_unique_id=uid)
+        for p in w.preds:
+            e.add_predicate(p)
+        ids, bbs, infos = run_stream(e, t, 3000)
+        runs.append((ids, bbs, [i["order_used"] for i in infos], [e.stats(k)["selectivity"] for k in range(3)]))
+        e.close()
+    (i0, b0, o0, s0), (i1, b1, o1, s1) = runs
+    assert np.array_equal(i0, i1) and np.array_equal(b0, b1) and o0 == o1 and s0 == s1
