@@ -313,8 +313,8 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
 // kernels (defined in k_route.cu / k_classifier.cu), launched by runtime.cu
 __global__ void hydro_route_kernel(hydro::RouteParams p);
 __global__ void hydro_compact_kernel(hydro::CompactParams p);
-template <bool kDbg, bool kArea>
-__global__ void hydro_classifier_kernel(hydro::ClsParams p);
+cudaError_t hydro_classifier_configure();
+void hydro_classifier_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug, bool area);
 __global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode);
 __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,
                                           int32_t to_fp16, int32_t* inexact);

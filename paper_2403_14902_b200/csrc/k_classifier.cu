@@ -62,6 +62,7 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
+#ifdef HYDRO_PRED_LDS
 // predicated load: lanes with !pred issue no shared-memory access
 __device__ __forceinline__ uint32_t lds32_if(uint32_t addr, bool pred) {
   uint32_t v = 0;
@@ -69,9 +70,7 @@ __device__ __forceinline__ uint32_t lds32_if(uint32_t addr, bool pred) {
                : "+r"(v) : "r"(addr), "r"(static_cast<uint32_t>(pred)));
   return v;
 }
-__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
-  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
+#endif
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -117,11 +116,13 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+#ifdef HYDRO_L2_PREFETCH
 // per-thread L2 prefetch of one line (a regular LSU op: unlike the uniform-datapath
 // cp.async.bulk.prefetch it does not serialise across the lanes of a warp)
 __device__ __forceinline__ void prefetch_line_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+#endif
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -554,7 +555,28 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   }
 }
 
-template __global__ void hydro_classifier_kernel<false, false>(ClsParams p);
-template __global__ void hydro_classifier_kernel<true, false>(ClsParams p);
-template __global__ void hydro_classifier_kernel<false, true>(ClsParams p);
-template __global__ void hydro_classifier_kernel<true, true>(ClsParams p);
+// Host-side entry points (the kernel template stays inside this translation unit).
+cudaError_t hydro_classifier_configure() {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(hydro_classifier_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kClsSmemBytes)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(hydro_classifier_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kClsSmemBytes)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(hydro_classifier_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kClsSmemBytes)) != cudaSuccess)
+    return e;
+  return cudaFuncSetAttribute(hydro_classifier_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kClsSmemBytes);
+}
+
+void hydro_classifier_launch(const ClsParams& c, int grid, cudaStream_t stream, bool debug, bool area) {
+  if (area) {
+    if (debug) hydro_classifier_kernel<true, true><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
+    else hydro_classifier_kernel<false, true><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
+  } else {
+    if (debug) hydro_classifier_kernel<true, false><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
+    else hydro_classifier_kernel<false, false><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
+  }
+}

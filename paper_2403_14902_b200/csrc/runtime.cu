@@ -233,10 +233,7 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->k1_occ, hydro_route_kernel, kRouteThreads, 0));
   if (ctx->k1_occ < 1) ctx->k1_occ = 1;
-  CU(cudaFuncSetAttribute(hydro_classifier_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
-  CU(cudaFuncSetAttribute(hydro_classifier_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
-  CU(cudaFuncSetAttribute(hydro_classifier_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
-  CU(cudaFuncSetAttribute(hydro_classifier_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes));
+  CU(hydro_classifier_configure());
   CU(cudaMalloc(&ctx->st, sizeof(DevState)));
   CU(cudaMemset(ctx->st, 0, sizeof(DevState)));
   CU(cudaMalloc(&ctx->preds_dev, sizeof(PredDev) * kMaxPred));
@@ -515,13 +512,7 @@ static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_
   return timed_launch(ctx, 1, [&] {
     // kernel instantiation by context capability: AREA support only when an AREA head exists
     const bool dbg = c.dbg_crops || c.dbg_logits || c.dbg_verdict;
-    if (ctx->has_area) {
-      if (dbg) hydro_classifier_kernel<true, true><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
-      else hydro_classifier_kernel<false, true><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
-    } else {
-      if (dbg) hydro_classifier_kernel<true, false><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
-      else hydro_classifier_kernel<false, false><<<grid, kClsThreads, kClsSmemBytes, ctx->stream>>>(c);
-    }
+    hydro_classifier_launch(c, grid, ctx->stream, dbg, ctx->has_area);
   });
 }
 
