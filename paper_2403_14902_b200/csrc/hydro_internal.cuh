@@ -71,6 +71,7 @@ struct DevState {
   int32_t kind[kMaxPred];
   int32_t order[kMaxPred];
   int32_t position[kMaxPred];
+  int32_t sched[kMaxPred];            // hop slot -> first order position of that hop (-1: none)
   double declared_cost[kMaxPred];
   double declared_sel[kMaxPred];
   double cost_norm[kMaxPred];         // raw cycles -> SM-cycles
@@ -82,6 +83,17 @@ struct DevState {
   double sel[kMaxPred], cost[kMaxPred], key[kMaxPred];
   unsigned int pad1, pad2;
 };
+
+// Hop schedule: the evaluator hops of an order are its LINEAR positions and the starts of its
+// maximal runs of cheap predicates; slot i of the per-batch chain runs hop sched[i].  The host
+// launches only as many slots as any order of the context can need.
+__host__ __device__ inline void build_sched(const int32_t* kind, const int32_t* order, int P, int32_t* sched) {
+  int n = 0;
+  if (P == 0) sched[n++] = 0;
+  for (int h = 0; h < P; ++h)
+    if (kind[order[h]] == kLinear || h == 0 || kind[order[h - 1]] == kLinear) sched[n++] = h;
+  for (; n < kMaxPred; ++n) sched[n] = -1;
+}
 
 struct BatchRec {
   unsigned int warm_count;    // survivors of the warmup slice (written first in the output)
@@ -149,7 +161,7 @@ struct CompactParams {
   const uint64_t* bbox;
   DevState* st;
 };
-constexpr int kCompactSegs = 16;  // 2048-position segments per K2 CTA
+constexpr int kCompactSegs = 4;  // 2048-position segments per K2 CTA (multiple of 4: vector prefix loads)
 
 struct ClsParams {
   int32_t dispatch;       // 1: hop from device order; 0: explicit_pred

@@ -17,6 +17,10 @@
 //              exact u8 -> fp16 (PRMT 0x64vv = 1024+v, HSUB2 1024) or bf16, st.shared into the
 //              128B-swizzled K-major A ring (conflict-free), fence.proxy.async, arrive.
 // The A operand never touches HBM: only the crop-row segments of the frames are read.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -26,9 +30,16 @@ using namespace hydro;
 
 namespace {
 
+#ifdef HYDRO_2CTA
+constexpr int kPair = 2;  // CTA pairs (cta_group::2, M=256): each CTA holds half of every weight K-block
+#else
+constexpr int kPair = 1;
+#endif
+constexpr int kBStages = kBRing * kPair;  // same B-ring bytes; half-size stages in pair mode
+
 struct ClsCtrl {
   uint64_t full_a[kARing], empty_a[kARing];
-  uint64_t full_b[kBRing], empty_b[kBRing];
+  uint64_t full_b[kBStages], empty_b[kBStages];
   uint64_t tfull[2], tempty[2];
   uint32_t tmem_base;
   uint32_t pad;
@@ -62,15 +73,16 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
-#ifdef HYDRO_PRED_LDS
-// predicated load: lanes with !pred issue no shared-memory access
+// predicated load: lanes with !pred issue no shared-memory access (and cause no bank conflict)
 __device__ __forceinline__ uint32_t lds32_if(uint32_t addr, bool pred) {
   uint32_t v = 0;
   asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.b32 %0, [%1];\n}"
                : "+r"(v) : "r"(addr), "r"(static_cast<uint32_t>(pred)));
   return v;
 }
-#endif
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t a) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(a) : "memory");
+}
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -137,6 +149,47 @@ __device__ __forceinline__ void bulk_g2s_hint(void* smem_dst, const void* gsrc, 
       : "memory");
 }
 
+// ---- CTA-pair (cta_group::2) helpers: the two CTAs of a cluster share one M=256 MMA stream
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+#ifdef HYDRO_SLEEPWAIT
+#define HYDRO_PIPE_WAIT mbar_wait_sleep  // producer/MMA waits suspend instead of spinning
+#else
+#define HYDRO_PIPE_WAIT mbar_wait
+#endif
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same shared-memory offset in the leader CTA (rank 0)
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit to the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
 }  // namespace
 
 // One quad (4 crop rows x 8 lanes) of output pixels: lane (r, j) produces pixels 8j .. 8j+7 of
@@ -192,6 +245,57 @@ __device__ __forceinline__ void convert_quad(uint32_t seg, const uint32_t (&po)[
     }
   }
 }
+
+#ifdef HYDRO_ROWWISE
+// One crop row per warp instruction: lane l produces output pixels 2l, 2l+1 of a row (6 fp16 =
+// 3 words, words 3l .. 3l+2 of the row's 96).  The 32 lanes read one row's staged segment at
+// increasing offsets, so a load touches a contiguous word range (few bank conflicts); the second
+// word is read only when the pixel's 3 bytes straddle two words.  Stores are 32-bit: lane l's
+// words land in pairwise different banks for every swizzle phase (conflict-free).
+// Four rows at a time: all 16 loads are issued before any store so their latencies overlap.
+__device__ __forceinline__ uint32_t fetch_px(uint32_t seg, uint32_t o) {
+  const uint32_t a = seg + (o & ~3u);
+  const uint32_t w0 = lds32(a);
+  const uint32_t w1 = lds32_if(a + 4, (o & 2u) != 0u);
+  return __funnelshift_r(w0, w1, o << 3);
+}
+template <bool kFp16, bool kDbg>
+__device__ __forceinline__ void convert_rows4(const uint32_t (&seg)[4], const uint32_t (&po)[4],
+                                              const uint32_t (&rbase)[4], const uint32_t (&sw)[4],
+                                              const uint32_t (&bt)[3], uint16_t* const (&dbg)[4]) {
+  uint32_t px[4][2];
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    px[rr][0] = fetch_px(seg[rr], po[rr] & 0xFFFFu);
+    px[rr][1] = fetch_px(seg[rr], po[rr] >> 16);
+  }
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const uint32_t p0 = px[rr][0], p1 = px[rr][1];
+    uint32_t e[3];
+    if (kFp16) {
+      const uint32_t K = 0x64646464u;
+      e[0] = f16x2_sub(__byte_perm(p0, K, 0x4140), 0x64006400u);
+      e[1] = f16x2_sub(__byte_perm(__byte_perm(p0, p1, 0x0042), K, 0x4140), 0x64006400u);
+      e[2] = f16x2_sub(__byte_perm(p1, K, 0x4241), 0x64006400u);
+    } else {
+      e[0] = bf16x2_of_bytes(p0 & 0xFF, (p0 >> 8) & 0xFF);
+      e[1] = bf16x2_of_bytes((p0 >> 16) & 0xFF, p1 & 0xFF);
+      e[2] = bf16x2_of_bytes((p1 >> 8) & 0xFF, (p1 >> 16) & 0xFF);
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t) sts32(rbase[rr] + (bt[t] ^ sw[rr]), e[t]);
+    if (kDbg && dbg[rr]) {
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        dbg[rr][3 * kk + 0] = static_cast<uint16_t>(bf16_bits_of_byte(px[rr][kk] & 0xFF));
+        dbg[rr][3 * kk + 1] = static_cast<uint16_t>(bf16_bits_of_byte((px[rr][kk] >> 8) & 0xFF));
+        dbg[rr][3 * kk + 2] = static_cast<uint16_t>(bf16_bits_of_byte((px[rr][kk] >> 16) & 0xFF));
+      }
+    }
+  }
+}
+#endif
 
 // AREA crop (R10, cfg4): output pixel (dy, dx) is the mean over the bin
 // [y0 + dy*h//64, y0 + ceil((dy+1)h/64)) x [x0 + dx*w//64, x0 + ceil((dx+1)w/64)), one IEEE f32
@@ -250,17 +354,18 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   uint32_t count, base = p.range_base;
   uint32_t* bits_out;
   if (p.dispatch) {
-    if (p.hop >= st->n_pred) return;
-    pred = st->order[p.hop];
+    const int h = st->sched[p.hop];  // p.hop is the chain slot
+    if (h < 0 || h >= st->n_pred) return;
+    pred = st->order[h];
     if (st->kind[pred] != kLinear) return;
-    if (p.hop == 0) {
+    if (h == 0) {
       list_in = nullptr;
       count = p.range_n;
     } else {
-      list_in = p.lists + static_cast<uint64_t>(p.hop) * p.list_stride;
-      count = p.counts[p.hop];
+      list_in = p.lists + static_cast<uint64_t>(h) * p.list_stride;
+      count = p.counts[h];
     }
-    bits_out = p.bits + static_cast<uint64_t>(p.hop) * p.bits_stride;
+    bits_out = p.bits + static_cast<uint64_t>(h) * p.bits_stride;
   } else {
     pred = p.explicit_pred;
     list_in = p.list_in;
@@ -268,7 +373,12 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     bits_out = p.bits_out;
   }
   const uint32_t num_tiles = (count + kTileM - 1) / kTileM;
-  if (blockIdx.x >= num_tiles) return;
+  // work unit = kPair consecutive M-tiles (one per CTA of the cluster); both CTAs of a pair walk
+  // the same units, so a pair's last unit may hold a tile past num_tiles (all rows invalid)
+  const uint32_t crank = kPair == 2 ? cluster_ctarank() : 0u;
+  const uint32_t unit0 = blockIdx.x / kPair, unit_stride = gridDim.x / kPair;
+  const uint32_t num_units = (num_tiles + kPair - 1) / kPair;
+  if (unit0 >= num_units) return;
 
   const long long t_start = clock64();
   const PredDev& pdg = p.preds[pred];
@@ -279,6 +389,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   const int n_alloc = n_pad <= 32 ? 32 : (n_pad <= 64 ? 64 : 128);
   const uint32_t tmem_cols = 2u * n_alloc;
   const uint32_t b_stage_bytes = static_cast<uint32_t>(n_pad) * 128u;
+  const uint32_t b_load_bytes = b_stage_bytes / kPair;  // pair: CTA r holds weight rows [r*N/2, (r+1)*N/2)
   const uint32_t row_pitch = static_cast<uint32_t>(p.frame_w * 3);
 
   // ---- shared memory carve-up: [A ring][B ring][ctrl][staging ring]
@@ -295,28 +406,38 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < kARing; ++s) {
-      mbar_init(&ctrl->full_a[s], kConvWarps);
+      mbar_init(&ctrl->full_a[s], kConvWarps * kPair);
       mbar_init(&ctrl->empty_a[s], 1);
     }
-    for (int s = 0; s < kBRing; ++s) {
-      mbar_init(&ctrl->full_b[s], 1);
+    for (int s = 0; s < kBStages; ++s) {
+      mbar_init(&ctrl->full_b[s], crank == 0 ? kPair : 1);  // pair: + the peer's relay
       mbar_init(&ctrl->empty_b[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&ctrl->tfull[a], 1);
-      mbar_init(&ctrl->tempty[a], kEpiWarps);
+      mbar_init(&ctrl->tempty[a], kEpiWarps * kPair);
     }
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&ctrl->tmem_base)),
-                 "r"(tmem_cols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (kPair == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&ctrl->tmem_base)),
+                   "r"(tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&ctrl->tmem_base)),
+                   "r"(tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   if (tid < HYDRO_MAX_CLASSES) ctrl->bias[tid] = tid < n_classes ? pdg.bias[tid] : 0.0f;
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair == 2) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = ctrl->tmem_base;
 
@@ -328,7 +449,8 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     constexpr int kPrefetchGroups = HYDRO_PF_GROUPS;
     const uint64_t pol_w = policy_evict_last();  // weights are re-read by every tile: keep them in L2
     uint32_t itb = 0;
-    for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
+      const uint32_t tile = unit * kPair + crank;
       RowMeta mr[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) mr[r] = load_meta(p, list_in, base, tile * kTileM + lane * 4 + r, count);
@@ -352,21 +474,35 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
           if (g < kGroups) prefetch_group(g);
         }
         if (lane == 0) {
-          const uint32_t s = itb % kBRing, ph = (itb / kBRing) & 1u;
-          mbar_wait(&ctrl->empty_b[s], ph ^ 1u);
-          mbar_arrive_expect_tx(&ctrl->full_b[s], b_stage_bytes);
-          bulk_g2s_hint(smem + (b_ring - a_ring) + s * b_stage_bytes, w_tiled + static_cast<uint64_t>(kb) * b_stage_bytes,
-                        b_stage_bytes, &ctrl->full_b[s], pol_w);
+          const uint32_t s = itb % kBStages, ph = (itb / kBStages) & 1u;
+          HYDRO_PIPE_WAIT(&ctrl->empty_b[s], ph ^ 1u);
+          mbar_arrive_expect_tx(&ctrl->full_b[s], b_load_bytes);
+          bulk_g2s_hint(smem + (b_ring - a_ring) + s * b_load_bytes,
+                        w_tiled + static_cast<uint64_t>(kb) * b_stage_bytes + crank * b_load_bytes, b_load_bytes,
+                        &ctrl->full_b[s], pol_w);
         }
         __syncwarp();
       }
     }
+    if (kPair == 2 && lane == 0) {  // drain: every B stage released (the leader's commits land here)
+      for (int e = 0; e < kBStages; ++e, ++itb) mbar_wait(&ctrl->empty_b[itb % kBStages], ((itb / kBStages) & 1u) ^ 1u);
+    }
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (single thread)
-    if (lane == 0) {
-      const uint32_t idesc = idesc_f16_f32(kTileM, static_cast<uint32_t>(n_pad), !fp16);
+    if (kPair == 2 && crank != 0 && lane == 0) {
+      // peer: relay "my half of B landed" to the leader's full_b (the bulk copy completes locally)
+      uint32_t itb = 0;
+      for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
+        for (int kb = 0; kb < kNumKBlocks; ++kb, ++itb) {
+          const uint32_t s = itb % kBStages;
+          mbar_wait(&ctrl->full_b[s], (itb / kBStages) & 1u);
+          mbar_arrive_leader(&ctrl->full_b[s]);
+        }
+      }
+    } else if (lane == 0) {
+      const uint32_t idesc = idesc_f16_f32(kTileM * kPair, static_cast<uint32_t>(n_pad), !fp16);
       uint32_t itb = 0, gg = 0, tl = 0;
-      for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl) {
+      for (uint32_t unit = unit0; unit < num_units; unit += unit_stride, ++tl) {
         const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
         mbar_wait_sleep(&ctrl->tempty[acc], aph ^ 1u);
         tc_fence_after();
@@ -376,22 +512,33 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
 #pragma unroll
           for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr, ++itb) {
             const uint32_t sa = set + kbr;
-            const uint32_t sb = itb % kBRing, bph = (itb / kBRing) & 1u;
-            mbar_wait(&ctrl->full_a[sa], aph2);
-            mbar_wait(&ctrl->full_b[sb], bph);
+            const uint32_t sb = itb % kBStages, bph = (itb / kBStages) & 1u;
+            // (pair: the leader's barriers also count the peer's remote arrivals)
+            HYDRO_PIPE_WAIT(&ctrl->full_a[sa], aph2);
+            HYDRO_PIPE_WAIT(&ctrl->full_b[sb], bph);
             tc_fence_after();
             const uint32_t a_addr = a_ring + sa * kAKBlockBytes;
-            const uint32_t b_addr = b_ring + sb * b_stage_bytes;
+            const uint32_t b_addr = b_ring + sb * b_load_bytes;
 #pragma unroll
             for (int kk = 0; kk < kKBlock / 16; ++kk) {
-              tc_mma_bf16(d_tmem, desc_sw128(a_addr + kk * 32), desc_sw128(b_addr + kk * 32), idesc,
-                          (g | kbr | kk) != 0 ? 1u : 0u);
+              if constexpr (kPair == 2)
+                tc_mma_pair(d_tmem, desc_sw128(a_addr + kk * 32), desc_sw128(b_addr + kk * 32), idesc,
+                            (g | kbr | kk) != 0 ? 1u : 0u);
+              else
+                tc_mma_bf16(d_tmem, desc_sw128(a_addr + kk * 32), desc_sw128(b_addr + kk * 32), idesc,
+                            (g | kbr | kk) != 0 ? 1u : 0u);
             }
-            tc_commit(&ctrl->empty_a[sa]);
-            tc_commit(&ctrl->empty_b[sb]);
+            if constexpr (kPair == 2) {
+              tc_commit_pair(&ctrl->empty_a[sa]);
+              tc_commit_pair(&ctrl->empty_b[sb]);
+            } else {
+              tc_commit(&ctrl->empty_a[sa]);
+              tc_commit(&ctrl->empty_b[sb]);
+            }
           }
         }
-        tc_commit(&ctrl->tfull[acc]);
+        if constexpr (kPair == 2) tc_commit_pair(&ctrl->tfull[acc]);
+        else tc_commit(&ctrl->tfull[acc]);
       }
     }
     __syncwarp();
@@ -404,14 +551,28 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     const int r = lane >> 3, j = lane & 7;  // row-in-quad and 8-pixel block (pixels 8j .. 8j+7)
     const uint32_t slots = staging_addr + static_cast<uint32_t>(cu) * (kQuadSlots * kQuadSlotBytes);
     const uint8_t* frames = p.frames;
+#ifdef HYDRO_ROWWISE
+    uint32_t bt[3];  // lane's words 3*lane+t of a crop row: K-block, 16-byte chunk (pre-swizzle), word
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const uint32_t W = 3u * static_cast<uint32_t>(lane) + t;
+      bt[t] = (W >> 5) * kAKBlockBytes + (((W >> 2) & 7u) << 4) + (W & 3u) * 4u;
+    }
+#endif
     uint32_t gg = 0;
-    for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
+      const uint32_t tile = unit * kPair + crank;
       // rows' metadata: lane l < 16 holds row 16*cu + l
       const RowMeta mm = load_meta(p, list_in, base, tile * kTileM + cu * kConvRows + (lane & 15),
                                    lane < 16 ? count : 0u);
       const uint32_t my_src = mm.row0 + mm.seg_lo;                 // + sy * pitch per crop row
       const uint32_t my_len = (lane < 16 && mm.valid) ? mm.seg_len : 0u;
       const uint32_t my_h = static_cast<uint32_t>(mm.h);
+#ifdef HYDRO_ROWWISE
+      // lane i < 16 holds row i's (x0, w); each row's pixel offsets are recomputed where used
+      const uint32_t xw = static_cast<uint32_t>(mm.x0) | (static_cast<uint32_t>(mm.w) << 16);
+      const uint32_t k0 = 4u * static_cast<uint32_t>(lane) + 1u;  // (2*dx + 1) for dx = 2*lane
+#else
       uint32_t po[4][4];
 #pragma unroll
       for (int it = 0; it < 4; ++it) {
@@ -427,6 +588,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
           po[it][q] = o0 | (o1 << 16);
         }
       }
+#endif
       // Stage quad k = 4*g + it (rows 4*it .. 4*it+3 of this warp, crop row g) into slot k % kQuadSlots:
       // lanes 8r .. 8r+7 copy row r's segment in 16-byte chunks j + 8c (c < 7: segments <= 784 B).
       auto stage_quad = [&](int k, uint32_t slot) {
@@ -477,10 +639,31 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
             const uint32_t aw = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
             if (fp16) convert_quad_area<true, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
             else convert_quad_area<false, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
-          } else if (fp16) {
-            convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
           } else {
-            convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
+#ifdef HYDRO_ROWWISE
+            (void)seg;
+            uint32_t seg4[4], po4[4], rb4[4], sw4[4];
+            uint16_t* dbg4[4];
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+              const uint32_t mr = static_cast<uint32_t>(cu * kConvRows + 4 * it + rr);
+              seg4[rr] = slots + slot_use * kQuadSlotBytes + rr * kMaxSegBytes;
+              rb4[rr] = a_set + (mr >> 3) * 1024u + (mr & 7u) * 128u;
+              sw4[rr] = static_cast<uint32_t>((4 * it + rr) & 7) << 4;  // == (mr & 7) << 4
+              dbg4[rr] = (kDbg && p.dbg_crops && tile * kTileM + mr < count)
+                             ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + mr) * kFeatures + g * 192 + 6 * lane
+                             : nullptr;
+              const uint32_t rxw = __shfl_sync(0xFFFFFFFFu, xw, 4 * it + rr);
+              const uint32_t x0 = rxw & 0xFFFFu, w = rxw >> 16;
+              const uint32_t base_o = 3u * x0 - ((3u * x0) & ~15u);  // 3*x0 - seg_lo
+              po4[rr] = (base_o + 3u * ((k0 * w) >> 7)) | ((base_o + 3u * (((k0 + 2u) * w) >> 7)) << 16);
+            }
+            if (fp16) convert_rows4<true, kDbg>(seg4, po4, rb4, sw4, bt, dbg4);
+            else convert_rows4<false, kDbg>(seg4, po4, rb4, sw4, bt, dbg4);
+#else
+            if (fp16) convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
+            else convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
+#endif
           }
           slot_use = slot_use + 1 == kQuadSlots ? 0 : slot_use + 1;
           __syncwarp();  // the slot is refilled kQuadDepth quads later
@@ -489,16 +672,26 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
         __syncwarp();
         if (lane == 0) {
 #pragma unroll
-          for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_arrive(&ctrl->full_a[set + kbr]);
+          for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) {
+            if (kPair == 2 && crank != 0) mbar_arrive_leader(&ctrl->full_a[set + kbr]);
+            else mbar_arrive(&ctrl->full_a[set + kbr]);
+          }
         }
       }
       cp_async_wait<0>();
+    }
+    if (kPair == 2) {  // drain: both A sets released (the leader's commits land here)
+      for (int e = 0; e < 2; ++e, ++gg) {
+        const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph = (gg >> 1) & 1u;
+        for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_wait(&ctrl->empty_a[set + kbr], aph ^ 1u);
+      }
     }
   } else {
     // ===================== epilogue warps 0..3 (TMEM lane quadrant = warp)
     const int q = warp;
     uint32_t n_in = 0, n_pass = 0, tl = 0;
-    for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl) {
+    for (uint32_t unit = unit0; unit < num_units; unit += unit_stride, ++tl) {
+      const uint32_t tile = unit * kPair + crank;
       const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
       mbar_wait_sleep(&ctrl->tfull[acc], aph);
       tc_fence_after();
@@ -527,7 +720,10 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ctrl->tempty[acc]);
+      if (lane == 0) {
+        if (kPair == 2 && crank != 0) mbar_arrive_leader(&ctrl->tempty[acc]);
+        else mbar_arrive(&ctrl->tempty[acc]);
+      }
       const bool verdict = valid && (bi == target);
       const uint32_t bv = __ballot_sync(0xFFFFFFFFu, verdict);
       const uint32_t bvalid = __ballot_sync(0xFFFFFFFFu, valid);
@@ -545,10 +741,17 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     }
   }
 
-  __syncthreads();
+  tc_fence_before();
+  if constexpr (kPair == 2) cluster_sync_all();  // no CTA leaves while its peer may still touch it
+  else __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols) : "memory");
+    if constexpr (kPair == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols)
+                   : "memory");
   }
   if (tid == 0 && p.collect_stats) {
     atomicAdd(&st->d_cost[pred], static_cast<unsigned long long>(clock64() - t_start));
@@ -572,11 +775,31 @@ cudaError_t hydro_classifier_configure() {
 }
 
 void hydro_classifier_launch(const ClsParams& c, int grid, cudaStream_t stream, bool debug, bool area) {
-  if (area) {
-    if (debug) hydro_classifier_kernel<true, true><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
-    else hydro_classifier_kernel<false, true><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
+  void (*k)(ClsParams) = area ? (debug ? hydro_classifier_kernel<true, true> : hydro_classifier_kernel<false, true>)
+                              : (debug ? hydro_classifier_kernel<true, false> : hydro_classifier_kernel<false, false>);
+  if constexpr (kPair == 2) {
+    // CTA pairs: grid = 2 x min(pairs of tiles, co-resident clusters)
+    static int max_clusters = 0;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(kClsThreads);
+    cfg.dynamicSmemBytes = kClsSmemBytes;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (max_clusters == 0) {
+      cfg.gridDim = dim3(2 * 74);
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, k, &cfg) != cudaSuccess || max_clusters < 1) max_clusters = 1;
+      if (getenv("HYDRO_DEBUG_LAUNCH")) fprintf(stderr, "hydro: K4 CTA pairs, %d co-resident clusters\n", max_clusters);
+    }
+    const int pairs = std::min((grid + 1) / 2, max_clusters);
+    cfg.gridDim = dim3(2 * pairs);
+    cudaLaunchKernelEx(&cfg, k, c);
   } else {
-    if (debug) hydro_classifier_kernel<true, false><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
-    else hydro_classifier_kernel<false, false><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
+    k<<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
   }
 }

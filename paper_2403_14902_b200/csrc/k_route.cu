@@ -57,13 +57,16 @@ __device__ __forceinline__ bool k1_runs(const DevState* st, int h, int* run) {
 __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams p) {
   __shared__ PredDev s_pred[kMaxPred];
   __shared__ int32_t s_run_id[kMaxPred];
-  __shared__ unsigned long long s_in[kMaxPred], s_pass[kMaxPred], s_cost[kMaxPred];
-  __shared__ uint32_t s_warp_cnt[kRouteThreads / 32];
+  // per-warp statistic slots (lane 0 of each warp owns its row: plain adds, no shared atomics)
+  __shared__ uint32_t s_in[kRouteThreads / 32][kMaxPred], s_pass[kRouteThreads / 32][kMaxPred];
+  __shared__ unsigned long long s_cost[kRouteThreads / 32][kMaxPred];
+  __shared__ uint32_t s_warp_cnt[2][kRouteThreads / 32];  // double-buffered: one barrier per tile
   __shared__ int32_t s_work, s_nrun, s_n_and, s_need_id, s_need_bbox, s_need_label;
   __shared__ const uint32_t* s_list_in;
   __shared__ const uint32_t* s_and[kMaxPred];
   __shared__ uint32_t* s_bits_out;
   __shared__ uint32_t s_count, s_range_base;
+  __shared__ int32_t s_hop;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   DevState* st = p.st;
@@ -73,10 +76,12 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
     const uint32_t* list_in = p.list_in;
     uint32_t count = 0;
     uint32_t* bits_out = p.bitmap_out;
+    int32_t hop = -1;
     if (p.dispatch) {
-      const int h = p.hop;
+      const int h = st->sched[p.hop];  // p.hop is the chain slot
+      hop = h;
       int run = 0;
-      work = k1_runs(st, h, &run);
+      work = h >= 0 && k1_runs(st, h, &run);
       if (work) {
         if (h == 0) {
           list_in = nullptr;
@@ -118,23 +123,25 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
     s_need_id = need_id;
     s_need_bbox = need_bbox;
     s_need_label = need_label;
+    s_hop = hop;
   }
   __syncthreads();
   if (!s_work) {
     // hop h is a classifier hop: clear the segment counts its K4 accumulates into
-    if (p.dispatch && p.hop < st->n_pred && st->kind[st->order[p.hop]] == kLinear) {
-      const uint32_t n = p.hop == 0 ? p.range_n : p.counts[p.hop];
+    const int h = s_hop;
+    if (p.dispatch && h >= 0 && h < st->n_pred && st->kind[st->order[h]] == kLinear) {
+      const uint32_t n = h == 0 ? p.range_n : p.counts[h];
       const uint32_t nseg = (n + kRouteTile - 1) / kRouteTile;
       for (uint32_t i = blockIdx.x * kRouteThreads + tid; i < nseg; i += gridDim.x * kRouteThreads) p.seg_counts[i] = 0;
     }
     return;
   }
   const int nrun = s_nrun;
-  if (tid < nrun) {
-    s_pred[tid] = p.preds[s_run_id[tid]];
-    s_in[tid] = 0;
-    s_pass[tid] = 0;
-    s_cost[tid] = 0;
+  if (tid < nrun) s_pred[tid] = p.preds[s_run_id[tid]];
+  if (lane < kMaxPred) {
+    s_in[warp][lane] = 0;
+    s_pass[warp][lane] = 0;
+    s_cost[warp][lane] = 0;
   }
   __syncthreads();
   const uint32_t count = s_count;
@@ -145,7 +152,8 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
   uint32_t* bits_out = s_bits_out;
   const bool need_id = s_need_id, need_bbox = s_need_bbox, need_label = s_need_label;
 
-  for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+  uint32_t buf = 0;
+  for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x, buf ^= 1u) {
     const uint32_t p0 = t * kRouteTile + tid * kRouteItems;
     uint32_t idx[kRouteItems];
     uint32_t mask = 0;
@@ -226,13 +234,28 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
 #pragma unroll
           for (int j = 0; j < kRouteItems; ++j)
             if (((labs[j >> 1] >> (16 * (j & 1))) & 0xFFFFu) != want) mask &= ~(1u << j);
-        } else {  // kHash
+        } else if (pd.units_per_area > 0) {  // HASH with per-tuple units (cfg4): per-item loop
 #pragma unroll
           for (int j = 0; j < kRouteItems; ++j) {
             if ((mask >> j) & 1u) {
-              if (!hash_pass(pd, ids[j], pd.units_per_area > 0 ? bbs[j] : 0ull)) mask &= ~(1u << j);
+              if (!hash_pass(pd, ids[j], bbs[j])) mask &= ~(1u << j);
             }
           }
+        } else {  // HASH, uniform units: the 8 items branch-free (independent chains, no divergence)
+          uint32_t hv[kRouteItems];
+#pragma unroll
+          for (int j = 0; j < kRouteItems; ++j) hv[j] = static_cast<uint32_t>(splitmix64(ids[j] ^ pd.seed) >> 32);
+          for (int r = 0; r < pd.units; ++r) {
+#pragma unroll
+            for (int j = 0; j < kRouteItems; ++j) hv[j] = fmix32(hv[j] + static_cast<uint32_t>(r));
+          }
+          uint32_t fail = 0;
+#pragma unroll
+          for (int j = 0; j < kRouteItems; ++j) {
+            const uint64_t T = (ids[j] >= pd.drift_id) ? pd.thr1 : pd.thr0;
+            fail |= (static_cast<uint64_t>(hv[j]) < T ? 0u : 1u) << j;
+          }
+          mask &= ~fail;
         }
       }
       const long long t1 = clock64();
@@ -240,11 +263,11 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
         const uint32_t ci = __reduce_add_sync(kFull, __popc(in_mask));
         const uint32_t cp = __reduce_add_sync(kFull, __popc(mask));
         if (lane == 0) {
-          atomicAdd(&s_in[r], static_cast<unsigned long long>(ci));
-          atomicAdd(&s_pass[r], static_cast<unsigned long long>(cp));
+          s_in[warp][r] += ci;
+          s_pass[warp][r] += cp;
           // dense-equivalent cost: SIMT lanes without an alive item idle, so the warp's cycles are
           // charged in proportion to its occupancy (ci of 256 items); SM-cycles = raw / (256 * warps/SM)
-          atomicAdd(&s_cost[r], static_cast<unsigned long long>(t1 - t0) * ci);
+          s_cost[warp][r] += static_cast<unsigned long long>(t1 - t0) * ci;
         }
       }
     }
@@ -255,22 +278,29 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
     wbits |= __shfl_xor_sync(kFull, wbits, 2);
     if ((lane & 3) == 0 && p0 < count) bits_out[p0 >> 5] = wbits;
     const uint32_t wc = __reduce_add_sync(kFull, __popc(mask));
-    if (lane == 0) s_warp_cnt[warp] = wc;
-    __syncthreads();
+    if (lane == 0) s_warp_cnt[buf][warp] = wc;
+    __syncthreads();  // the other buffer is rewritten only after the next tile's barrier
     if (tid == 0) {
       uint32_t tot = 0;
 #pragma unroll
-      for (int w = 0; w < kRouteThreads / 32; ++w) tot += s_warp_cnt[w];
+      for (int w = 0; w < kRouteThreads / 32; ++w) tot += s_warp_cnt[buf][w];
       p.seg_counts[t] = tot;
     }
-    __syncthreads();
   }
 
+  __syncthreads();
   if (p.collect_stats && tid < nrun) {
     const int k = s_run_id[tid];
-    atomicAdd(&st->d_in[k], s_in[tid]);
-    atomicAdd(&st->d_pass[k], s_pass[tid]);
-    atomicAdd(&st->d_cost[k], s_cost[tid]);
+    unsigned long long in = 0, pass = 0, cost = 0;
+#pragma unroll
+    for (int w = 0; w < kRouteThreads / 32; ++w) {
+      in += s_in[w][tid];
+      pass += s_pass[w][tid];
+      cost += s_cost[w][tid];
+    }
+    atomicAdd(&st->d_in[k], in);
+    atomicAdd(&st->d_pass[k], pass);
+    atomicAdd(&st->d_cost[k], cost);
   }
 }
 
@@ -299,10 +329,13 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactPar
     uint32_t count = 0;
     if (p.dispatch) {
       const DevState* st = p.st;
-      const int h = p.hop, P = st->n_pred;
+      const int h = st->sched[p.hop], P = st->n_pred;  // p.hop is the chain slot
       int run = 0;
       int next;
-      if (k1_runs(st, h, &run)) {
+      if (h < 0) {
+        work = 0;
+        next = 0;
+      } else if (k1_runs(st, h, &run)) {
         next = h + run;
       } else if (h < P && st->kind[st->order[h]] == kLinear) {
         next = h + 1;
@@ -350,7 +383,14 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactPar
 
   // output offset of this CTA: survivors of every earlier segment
   uint32_t part = 0;
-  for (uint32_t s = tid; s < seg0; s += kRouteThreads) part += __ldg(p.seg_counts + s);
+  {  // seg0 is a multiple of 4 (kCompactSegs): 16-byte loads, independent so they overlap
+    const uint4* sc4 = reinterpret_cast<const uint4*>(p.seg_counts);
+#pragma unroll 4
+    for (uint32_t s = tid; s < seg0 / 4; s += kRouteThreads) {
+      const uint4 v = __ldg(sc4 + s);
+      part += v.x + v.y + v.z + v.w;
+    }
+  }
   part = __reduce_add_sync(kFull, part);
   if (lane == 0) s_red[warp] = part;
   __syncthreads();
@@ -366,6 +406,22 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactPar
     if (p0 < count) {
       mask = (__ldg(bits + (p0 >> 5)) >> (p0 & 31)) & 0xFFu;
       if (p0 + kRouteItems > count) mask &= (1u << (count - p0)) - 1u;
+    }
+    // gather the survivors' payload before the scan so its latency overlaps the scan and barriers
+    uint32_t sidx[kRouteItems];
+    uint64_t sid[kRouteItems], sbb[kRouteItems];
+#pragma unroll
+    for (int j = 0; j < kRouteItems; ++j) {
+      sidx[j] = 0;
+      sid[j] = 0;
+      sbb[j] = 0;
+      if ((mask >> j) & 1u) {
+        sidx[j] = list_in ? __ldg(list_in + p0 + j) : base + p0 + j;
+        if (emit) {
+          sid[j] = __ldg(p.id + sidx[j]);
+          sbb[j] = __ldg(p.bbox + sidx[j]);
+        }
+      }
     }
     const uint32_t c = __popc(mask);
     uint32_t x = c;
@@ -394,14 +450,13 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactPar
       if (!emit) {
 #pragma unroll
         for (int j = 0; j < kRouteItems; ++j)
-          if ((mask >> j) & 1u) s_list_out[pos++] = list_in ? __ldg(list_in + p0 + j) : base + p0 + j;
+          if ((mask >> j) & 1u) s_list_out[pos++] = sidx[j];
       } else {
 #pragma unroll
         for (int j = 0; j < kRouteItems; ++j) {
           if ((mask >> j) & 1u) {
-            const uint32_t idx = list_in ? __ldg(list_in + p0 + j) : base + p0 + j;
-            p.out_ids[pos] = __ldg(p.id + idx);
-            p.out_bbox[pos] = __ldg(p.bbox + idx);
+            p.out_ids[pos] = sid[j];
+            p.out_bbox[pos] = sbb[j];
             ++pos;
           }
         }
@@ -491,6 +546,7 @@ __global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode) {
       for (int i = 0; i < P; ++i) st->order[i] = ord[i];
     }
     for (int i = 0; i < P; ++i) st->position[st->order[i]] = i;
+    build_sched(st->kind, st->order, P, st->sched);
   }
 }
 

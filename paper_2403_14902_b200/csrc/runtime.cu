@@ -332,6 +332,10 @@ hydro_status hydro_set_fixed_order(hydro_ctx* ctx, const int32_t* order, int32_t
     for (int i = 0; i < P; ++i) pos[order[i]] = i;
     CU(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, order), ctx->fixed_order, sizeof(int32_t) * P, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, position), pos, sizeof(int32_t) * P, cudaMemcpyHostToDevice, ctx->stream));
+    int32_t kind[kMaxPred], sched[kMaxPred];
+    for (int i = 0; i < P; ++i) kind[i] = ctx->preds[i].desc.kind;
+    build_sched(kind, ctx->fixed_order, P, sched);
+    CU(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, sched), sched, sizeof(sched), cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
   }
   return HYDRO_OK;
@@ -392,6 +396,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
     std::stable_sort(h.order, h.order + P, [&](int a, int b) { return h.key[a] < h.key[b]; });
   }
   for (int i = 0; i < P; ++i) h.position[h.order[i]] = i;
+  build_sched(h.kind, h.order, P, h.sched);
   CU(cudaMemcpy(ctx->st, &h, sizeof(h), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(ctx->preds_dev, pd.data(), sizeof(PredDev) * kMaxPred, cudaMemcpyHostToDevice));
   // workspace
@@ -638,14 +643,19 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
   // predicates, or K4 for a classifier) then K2 compaction into the next hop's alive list / emit
   const uint32_t rest_base = static_cast<uint32_t>(warm);
   const uint32_t rest_n = static_cast<uint32_t>(n - warm);
-  for (int h = 0; h < std::max(P, 1); ++h) {
+  // chain slots: any order has at most L classifier hops and min(C, L + 1) cheap runs
+  int n_lin = 0;
+  for (int k = 0; k < P; ++k) n_lin += ctx->preds[k].desc.kind == HYDRO_PRED_LINEAR ? 1 : 0;
+  const int n_cheap = P - n_lin;
+  const int slots = (P == 0 || n_lin == 0) ? 1 : std::min(P, n_lin + std::min(n_cheap, n_lin + 1));
+  for (int h = 0; h < slots; ++h) {
     RouteParams r = route_base(ctx, id, fr, bb, lab);
     r.dispatch = 1;
     r.hop = h;
     r.range_base = rest_base;
     r.range_n = rest_n;
     if ((s = launch_route(ctx, r, rest_n)) != HYDRO_OK) return s;
-    if (h < P) {
+    if (n_lin > 0) {
       ClsParams c = cls_base(ctx, fr, bb);
       c.dispatch = 1;
       c.hop = h;
