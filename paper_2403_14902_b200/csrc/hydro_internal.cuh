@@ -126,6 +126,7 @@ struct RouteParams {
   // ---- outputs
   uint32_t* bitmap_out;   // explicit mode
   uint32_t* seg_counts;   // survivors per 2048-position segment
+  uint32_t* warp_counts;  // survivors per 256-position warp segment (8 per 2048-position segment)
   // ---- columns
   const uint64_t* id;
   const uint32_t* frame_id;
@@ -145,6 +146,7 @@ struct CompactParams {
   uint32_t range_base, range_n;
   const uint32_t* bits_in;  // explicit
   const uint32_t* seg_counts;
+  const uint32_t* warp_counts;
   uint32_t* lists;
   uint64_t list_stride;
   uint32_t* counts;
@@ -161,6 +163,7 @@ struct CompactParams {
   const uint64_t* bbox;
   DevState* st;
 };
+constexpr int kWarpSeg = 256;  // positions per K1 warp per tile (= kRouteTile / 8)
 constexpr int kCompactSegs = 4;  // 2048-position segments per K2 CTA (multiple of 4: vector prefix loads)
 
 struct ClsParams {
@@ -176,7 +179,8 @@ struct ClsParams {
   uint32_t* bits;
   uint64_t bits_stride;
   uint32_t* bits_out;         // explicit mode output bitmap
-  uint32_t* seg_counts;       // survivors per 2048-position segment (atomically accumulated; zeroed by the host)
+  uint32_t* seg_counts;       // survivors per 2048-position segment (atomically accumulated; zeroed by K1)
+  uint32_t* warp_counts;      // survivors per 256-position warp segment (likewise)
   const uint32_t* frame_id;
   const uint64_t* bbox;
   const uint8_t* frames;

@@ -729,7 +729,10 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       const uint32_t bvalid = __ballot_sync(0xFFFFFFFFu, valid);
       if (lane == 0 && bvalid) {
         bits_out[tile * (kTileM / 32) + q] = bv;
-        if (bv) atomicAdd(p.seg_counts + ((tile * kTileM + q * 32) / kRouteTile), static_cast<uint32_t>(__popc(bv)));
+        if (bv) {
+          atomicAdd(p.seg_counts + ((tile * kTileM + q * 32) / kRouteTile), static_cast<uint32_t>(__popc(bv)));
+          atomicAdd(p.warp_counts + ((tile * kTileM + q * 32) / kWarpSeg), static_cast<uint32_t>(__popc(bv)));
+        }
       }
       if (kDbg && p.dbg_verdict && valid) p.dbg_verdict[pos] = verdict ? 1 : 0;
       n_in += __popc(bvalid);

@@ -54,13 +54,17 @@ __device__ __forceinline__ bool k1_runs(const DevState* st, int h, int* run) {
 
 // ------------------------------------------------------------------------------------------
 // K1: evaluate.  Persistent grid, tile t = positions [2048 t, 2048 t + 2048); thread = 8 positions.
-__global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams p) {
+#ifndef HYDRO_K1_MINB
+#define HYDRO_K1_MINB 1
+#endif
+__global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kernel(RouteParams p) {
   __shared__ PredDev s_pred[kMaxPred];
   __shared__ int32_t s_run_id[kMaxPred];
   // per-warp statistic slots (lane 0 of each warp owns its row: plain adds, no shared atomics)
   __shared__ uint32_t s_in[kRouteThreads / 32][kMaxPred], s_pass[kRouteThreads / 32][kMaxPred];
   __shared__ unsigned long long s_cost[kRouteThreads / 32][kMaxPred];
   __shared__ uint32_t s_warp_cnt[2][kRouteThreads / 32];  // double-buffered: one barrier per tile
+  __shared__ uint64_t s_cids[kRouteThreads / 32][kWarpSeg];  // per-warp compacted ids (sparse HASH hops)
   __shared__ int32_t s_work, s_nrun, s_n_and, s_need_id, s_need_bbox, s_need_label;
   __shared__ const uint32_t* s_list_in;
   __shared__ const uint32_t* s_and[kMaxPred];
@@ -133,6 +137,8 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
       const uint32_t n = h == 0 ? p.range_n : p.counts[h];
       const uint32_t nseg = (n + kRouteTile - 1) / kRouteTile;
       for (uint32_t i = blockIdx.x * kRouteThreads + tid; i < nseg; i += gridDim.x * kRouteThreads) p.seg_counts[i] = 0;
+      for (uint32_t i = blockIdx.x * kRouteThreads + tid; i < nseg * (kRouteTile / kWarpSeg); i += gridDim.x * kRouteThreads)
+        p.warp_counts[i] = 0;
     }
     return;
   }
@@ -228,7 +234,60 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
       const PredDev& pd = s_pred[r];
       const long long t0 = clock64();
       const uint32_t in_mask = mask;
-      if (mask) {
+      const uint32_t warp_alive = __reduce_add_sync(kFull, __popc(mask));
+#ifdef HYDRO_K1_COMPACT
+      constexpr bool kCompactHash = true;
+#else
+      constexpr bool kCompactHash = false;  // measured slower on B200 (the dense chains overlap better)
+#endif
+      if (kCompactHash && pd.kind == kHash && pd.units_per_area <= 0 && warp_alive > 0 &&
+          warp_alive * 2u <= static_cast<uint32_t>(kWarpSeg)) {
+        // HASH, uniform units, at most half of the warp's 256 positions alive (all lanes take
+        // this branch): compact the alive ids into a warp buffer, hash 32 per step (one per
+        // lane), ballot the verdicts back
+        const uint32_t c = __popc(mask);
+        uint32_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, x, o);
+          if (lane >= o) x += y;
+        }
+        const uint32_t off = x - c, n_alive = __shfl_sync(kFull, x, 31);
+        uint64_t* buf = s_cids[warp];
+        uint32_t k = off;
+#pragma unroll
+        for (int j = 0; j < kRouteItems; ++j)
+          if ((mask >> j) & 1u) buf[k++] = ids[j];
+        __syncwarp();
+        uint32_t vw = 0;  // lane i: fail bits of compact entries 32i .. 32i+31
+        const bool one_thr = pd.thr0 == pd.thr1;
+        for (uint32_t i = 0; i * 32u < n_alive; ++i) {
+          const uint32_t e = i * 32u + lane;
+          bool f = false;
+          if (e < n_alive) {
+            const uint64_t id = buf[e];
+            uint32_t h = static_cast<uint32_t>(splitmix64(id ^ pd.seed) >> 32);
+            for (int u = 0; u < pd.units; ++u) h = fmix32(h + static_cast<uint32_t>(u));
+            const uint64_t T = (one_thr || id < pd.drift_id) ? pd.thr0 : pd.thr1;
+            f = static_cast<uint64_t>(h) >= T;
+          }
+          const uint32_t b = __ballot_sync(kFull, f);
+          if (lane == static_cast<int>(i)) vw = b;
+        }
+        const uint32_t w0 = __shfl_sync(kFull, vw, off >> 5);
+        const uint32_t w1 = __shfl_sync(kFull, vw, min((off >> 5) + 1u, 7u));
+        const uint32_t fb = __funnelshift_r(w0, w1, off & 31u) & ((1u << c) - 1u);  // this thread's entries
+        uint32_t fail = 0, t = 0;
+#pragma unroll
+        for (int j = 0; j < kRouteItems; ++j) {
+          if ((mask >> j) & 1u) {
+            fail |= ((fb >> t) & 1u) << j;
+            ++t;
+          }
+        }
+        mask &= ~fail;
+        __syncwarp();  // the buffer is rewritten by the next predicate of the run
+      } else if (mask) {
         if (pd.kind == kLabelEq) {
           const uint32_t want = static_cast<uint32_t>(pd.label_value) & 0xFFFFu;
 #pragma unroll
@@ -250,10 +309,18 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
             for (int j = 0; j < kRouteItems; ++j) hv[j] = fmix32(hv[j] + static_cast<uint32_t>(r));
           }
           uint32_t fail = 0;
+          if (pd.thr0 == pd.thr1) {  // no drift: one threshold; T >= 2^32 passes everything
+            if (pd.thr0 <= 0xFFFFFFFFull) {
+              const uint32_t T32 = static_cast<uint32_t>(pd.thr0);
 #pragma unroll
-          for (int j = 0; j < kRouteItems; ++j) {
-            const uint64_t T = (ids[j] >= pd.drift_id) ? pd.thr1 : pd.thr0;
-            fail |= (static_cast<uint64_t>(hv[j]) < T ? 0u : 1u) << j;
+              for (int j = 0; j < kRouteItems; ++j) fail |= (hv[j] >= T32 ? 1u : 0u) << j;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < kRouteItems; ++j) {
+              const uint64_t T = (ids[j] >= pd.drift_id) ? pd.thr1 : pd.thr0;
+              fail |= (static_cast<uint64_t>(hv[j]) < T ? 0u : 1u) << j;
+            }
           }
           mask &= ~fail;
         }
@@ -278,7 +345,10 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
     wbits |= __shfl_xor_sync(kFull, wbits, 2);
     if ((lane & 3) == 0 && p0 < count) bits_out[p0 >> 5] = wbits;
     const uint32_t wc = __reduce_add_sync(kFull, __popc(mask));
-    if (lane == 0) s_warp_cnt[buf][warp] = wc;
+    if (lane == 0) {
+      s_warp_cnt[buf][warp] = wc;
+      p.warp_counts[t * (kRouteTile / kWarpSeg) + warp] = wc;
+    }
     __syncthreads();  // the other buffer is rewritten only after the next tile's barrier
     if (tid == 0) {
       uint32_t tot = 0;
@@ -306,11 +376,11 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_route_kernel(RouteParams 
 
 // ------------------------------------------------------------------------------------------
 // K2: order-preserving compaction (eager materialization).  CTA c owns
-// segments [16c, 16c + 16); its output offset is the sum of all earlier segments' counts (<= a few
-// thousand L2-resident words), so no CTA ever waits for another.  Within a segment: warp ballot /
-// popc + block scan; survivors are written in input order.
+// segments [4c, 4c + 4); its output offset is the sum of all earlier segments' counts (<= a few
+// thousand L2-resident words), so no CTA ever waits for another.  Within a segment each warp owns
+// a 256-position slice whose offset comes from the evaluator's per-warp counts: warp scan only,
+// no block barrier; survivors are written in input order.
 __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactParams p) {
-  __shared__ uint32_t s_warp_tot[kRouteThreads / 32], s_warp_excl[kRouteThreads / 32];
   __shared__ uint32_t s_red[kRouteThreads / 32];
   __shared__ int32_t s_work, s_emit;
   __shared__ const uint32_t* s_list_in;
@@ -400,26 +470,54 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactPar
   prefix += s_emit_off;
 
   const uint32_t seg1 = min(seg0 + kCompactSegs, nseg);
+  // Each warp walks its own 256-position slice of every segment, independently of the other
+  // warps: its output offset is the segment's offset plus the survivors of the earlier warp
+  // slices of the same segment (warp counts written by the evaluator), so there is no barrier.
+  constexpr uint32_t kWarpsPerSeg = kRouteTile / kWarpSeg;
   for (uint32_t sgi = seg0; sgi < seg1; ++sgi) {
+    const uint32_t wcv = lane < kWarpsPerSeg ? __ldg(p.warp_counts + sgi * kWarpsPerSeg + lane) : 0u;
+    const uint32_t wexcl = __reduce_add_sync(kFull, lane < static_cast<uint32_t>(warp) ? wcv : 0u);
+    const uint32_t seg_total = __reduce_add_sync(kFull, wcv);
     const uint32_t p0 = sgi * kRouteTile + tid * kRouteItems;
     uint32_t mask = 0;
     if (p0 < count) {
       mask = (__ldg(bits + (p0 >> 5)) >> (p0 & 31)) & 0xFFu;
       if (p0 + kRouteItems > count) mask &= (1u << (count - p0)) - 1u;
     }
-    // gather the survivors' payload before the scan so its latency overlaps the scan and barriers
     uint32_t sidx[kRouteItems];
     uint64_t sid[kRouteItems], sbb[kRouteItems];
+    // emit from a dense range segment (>= 1 in 10 positions survive): the scattered gathers would
+    // touch most DRAM bursts of the id / bbox columns anyway, so read the thread's 8 rows
+    // contiguously (16-byte loads, fully coalesced) and keep the survivors
+    const bool dense = emit && !list_in && seg_total * 10u >= static_cast<uint32_t>(kRouteTile) &&
+                       p0 + kRouteItems <= count &&
+                       ((reinterpret_cast<uintptr_t>(p.id + base + p0) | reinterpret_cast<uintptr_t>(p.bbox + base + p0)) &
+                        15u) == 0u;
+    if (dense) {
+      const ulonglong2* qi = reinterpret_cast<const ulonglong2*>(p.id + base + p0);
+      const ulonglong2* qb = reinterpret_cast<const ulonglong2*>(p.bbox + base + p0);
 #pragma unroll
-    for (int j = 0; j < kRouteItems; ++j) {
-      sidx[j] = 0;
-      sid[j] = 0;
-      sbb[j] = 0;
-      if ((mask >> j) & 1u) {
-        sidx[j] = list_in ? __ldg(list_in + p0 + j) : base + p0 + j;
-        if (emit) {
-          sid[j] = __ldg(p.id + sidx[j]);
-          sbb[j] = __ldg(p.bbox + sidx[j]);
+      for (int j = 0; j < kRouteItems / 2; ++j) {
+        const ulonglong2 a = __ldg(qi + j), b = __ldg(qb + j);
+        sid[2 * j] = a.x;
+        sid[2 * j + 1] = a.y;
+        sbb[2 * j] = b.x;
+        sbb[2 * j + 1] = b.y;
+      }
+#pragma unroll
+      for (int j = 0; j < kRouteItems; ++j) sidx[j] = base + p0 + j;
+    } else {
+#pragma unroll
+      for (int j = 0; j < kRouteItems; ++j) {
+        sidx[j] = 0;
+        sid[j] = 0;
+        sbb[j] = 0;
+        if ((mask >> j) & 1u) {
+          sidx[j] = list_in ? __ldg(list_in + p0 + j) : base + p0 + j;
+          if (emit) {
+            sid[j] = __ldg(p.id + sidx[j]);
+            sbb[j] = __ldg(p.bbox + sidx[j]);
+          }
         }
       }
     }
@@ -430,22 +528,7 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactPar
       const uint32_t y = __shfl_up_sync(kFull, x, o);
       if (lane >= o) x += y;
     }
-    if (lane == 31) s_warp_tot[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t v = lane < kRouteThreads / 32 ? s_warp_tot[lane] : 0u;
-      uint32_t sc = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, sc, o);
-        if (lane >= o) sc += y;
-      }
-      if (lane < kRouteThreads / 32) s_warp_excl[lane] = sc - v;
-      if (lane == kRouteThreads / 32 - 1) s_warp_tot[0] = sc;  // segment total (read after the barrier)
-    }
-    __syncthreads();
-    uint32_t pos = prefix + s_warp_excl[warp] + (x - c);
-    const uint32_t seg_total = s_warp_tot[0];
+    uint32_t pos = prefix + wexcl + (x - c);
     if (mask) {
       if (!emit) {
 #pragma unroll
@@ -463,7 +546,6 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactPar
       }
     }
     prefix += seg_total;
-    __syncthreads();  // s_warp_* reuse
   }
   // the CTA holding the last segment publishes the count
   const bool last = (nseg == 0) ? (blockIdx.x == 0) : (seg1 == nseg);

@@ -96,7 +96,8 @@ struct hydro_ctx {
   uint32_t* bits = nullptr;
   uint64_t bits_stride = 0;
   uint32_t* warm_bits = nullptr;
-  uint32_t* seg_counts = nullptr;
+  uint32_t* seg_counts = nullptr;  // [max_segs] segment counts, then [8 * max_segs] warp counts
+  uint64_t max_segs = 0;
   uint32_t* warm_and = nullptr;
   uint32_t* zero_word = nullptr;
   std::vector<Slot> slots;
@@ -408,8 +409,9 @@ static hydro_status freeze(hydro_ctx* ctx) {
   CU(cudaMalloc(&ctx->bits, sizeof(uint32_t) * ctx->bits_stride * std::max(P, 1)));
   CU(cudaMalloc(&ctx->warm_bits, sizeof(uint32_t) * ctx->bits_stride * std::max(P, 1)));
   const uint64_t max_segs = (maxb + kRouteTile - 1) / kRouteTile + 1;
-  CU(cudaMalloc(&ctx->seg_counts, sizeof(uint32_t) * max_segs));
-  CU(cudaMemset(ctx->seg_counts, 0, sizeof(uint32_t) * max_segs));
+  ctx->max_segs = (max_segs + 3) & ~3ull;  // warp counts follow, 16-byte aligned
+  CU(cudaMalloc(&ctx->seg_counts, sizeof(uint32_t) * ctx->max_segs * 9));
+  CU(cudaMemset(ctx->seg_counts, 0, sizeof(uint32_t) * ctx->max_segs * 9));
   CU(cudaMalloc(&ctx->warm_and, sizeof(uint32_t) * ctx->bits_stride));
   ctx->slots.resize(ctx->cfg.max_inflight);
   for (Slot& s : ctx->slots) {
@@ -442,6 +444,7 @@ static RouteParams route_base(hydro_ctx* ctx, const uint64_t* id, const uint32_t
   r.bits = ctx->bits;
   r.bits_stride = ctx->bits_stride;
   r.seg_counts = ctx->seg_counts;
+  r.warp_counts = ctx->seg_counts + ctx->max_segs;
   r.id = id;
   r.frame_id = fr;
   r.bbox = bb;
@@ -456,6 +459,7 @@ static RouteParams route_base(hydro_ctx* ctx, const uint64_t* id, const uint32_t
 static CompactParams compact_base(hydro_ctx* ctx, const uint64_t* id, const uint64_t* bb, Slot& sl) {
   CompactParams c{};
   c.seg_counts = ctx->seg_counts;
+  c.warp_counts = ctx->seg_counts + ctx->max_segs;
   c.lists = ctx->lists;
   c.list_stride = ctx->list_stride;
   c.counts = ctx->counts;
@@ -485,6 +489,7 @@ static ClsParams cls_base(hydro_ctx* ctx, const uint32_t* fr, const uint64_t* bb
   c.st = ctx->st;
   c.preds = ctx->preds_dev;
   c.seg_counts = ctx->seg_counts;
+  c.warp_counts = ctx->seg_counts + ctx->max_segs;
   c.collect_stats = 1;
   c.explicit_pred = -1;
   return c;
