@@ -69,7 +69,10 @@ enum {
 enum {
   HYDRO_PRED_LABEL_EQ = 0, /* label == label_value                                          */
   HYDRO_PRED_HASH = 1,     /* synthetic predicate with set selectivity and per-tuple cost (R5) */
-  HYDRO_PRED_LINEAR = 2    /* argmax(W . Crop(frame, bbox) + b) == target (R10-R14, R19)     */
+  HYDRO_PRED_LINEAR = 2,   /* argmax(W . Crop(frame, bbox) + b) == target (R10-R14, R19)     */
+  HYDRO_PRED_MLP = 3       /* argmax(W2 . bf16(relu(W1 . Crop + b1)) + b2) == target: the
+                              "small MLP classifier" of the north star (
+                              stand-in for the ViT breed model; R25)  */
 };
 
 enum { HYDRO_CROP_NEAREST = 0, HYDRO_CROP_AREA = 1 }; /* R10 */
@@ -78,6 +81,7 @@ enum { HYDRO_CROP_NEAREST = 0, HYDRO_CROP_AREA = 1 }; /* R10 */
 #define HYDRO_CROP 64
 #define HYDRO_FEATURES 12288 /* 64 * 64 * 3, feature k = (dy*64 + dx)*3 + ch (R10) */
 #define HYDRO_MAX_CLASSES 128
+#define HYDRO_MLP_HIDDEN_MAX 512 /* MLP hidden width: 256 or 512 */
 
 typedef struct hydro_ctx hydro_ctx; /* opaque */
 
@@ -125,7 +129,13 @@ typedef struct {
   int32_t weights_on_device;  /* 1: weight_bf16 / bias are device pointers, 0: host pointers  */
   int32_t n_classes;          /* 2 .. HYDRO_MAX_CLASSES                                        */
   int32_t target;             /* 0 .. n_classes-1                                              */
-  int32_t crop_mode;          /* HYDRO_CROP_*                                                  */
+  int32_t crop_mode;          /* HYDRO_CROP_* (MLP: NEAREST only)                              */
+  /* MLP (R25): h = bf16_rne(relu(W1 x + b1)) with fp32 accumulation; z = W2 h + b2.  For an MLP
+     weight_bf16 / bias are W1 [hidden][HYDRO_FEATURES] / b1 [hidden]; the second layer is below
+     (same residency flag, COPIED at add time).                                                */
+  int32_t hidden;             /* 256 or 512                                                    */
+  const uint16_t* weight2_bf16;/* bf16 bits, row-major [n_classes][hidden]                     */
+  const float* bias2;         /* [n_classes]                                                   */
   /* statistics priors (STATIC policy values; DECLARED cost source; used before any fold)    */
   double declared_cost;       /* > 0, same unit as the measured cost for a mixed SCORE policy  */
   double declared_selectivity;/* in [0, 1]                                                     */
@@ -189,7 +199,8 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out);
 /* Registers predicate number *pred_id = 0, 1, 2 ... (call order = the conjunction's textual
    order = the FIXED_ORDER default).  At most HYDRO_MAX_PREDICATES.  ESTATE after the first
    submit.  EINVAL: n_classes out of range, target outside [0, n_classes), threshold > 2^32,
-   negative units, LINEAR without a frame pool, declared values out of range. */
+   negative units, LINEAR / MLP without a frame pool, MLP with hidden not in {256, 512} or an
+   AREA crop, declared values out of range. */
 hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* desc, int32_t* pred_id);
 
 /* FIXED_ORDER policy: sets the order (a permutation of 0..P-1).  EINVAL if not a permutation. */

@@ -14,7 +14,7 @@ What it computes (PAPER.md citations; "R<n>" = numbered reading in DESIGN.md §2
 * per-predicate verdicts, each a pure function of the tuple:
   LABEL_EQ, HASH (R5, stand-in for the synthetic 10/20 ms predicates,
   PAPER.md:550-552), LINEAR = argmax(W . Crop(frame, bbox) + b) == target (PAPER.md:47-48,
-  286-288; R9-R14, R19);
+  286-288; R9-R14, R19), MLP = argmax(W2 . bf16(relu(W1 . Crop + b1)) + b2) == target (R25);
 * eddy statistics: count-based selectivity, measured cost,
   the score ``cost / (1 - selectivity)`` and its lowest-first order,
   the decayed fold (R4), the closed-form expected cost (R20);
@@ -171,6 +171,26 @@ def linear_logits(pred: Dict, x: np.ndarray) -> np.ndarray:
     return x @ W.T + b[None, :]
 
 
+def _f64(t) -> np.ndarray:
+    if hasattr(t, "float"):
+        return t.float().cpu().numpy().astype(np.float64)
+    return np.asarray(t, dtype=np.float64)
+
+
+def mlp_logits(pred: Dict, x: np.ndarray) -> np.ndarray:
+    """MLP head (R25, the north star's "small ... MLP classifier"):
+
+    a = W1 x + b1                       (float64; the method accumulates in fp32)
+    h = bf16_rne(f32(max(a, 0)))        (the hidden layer is bf16, as the second GEMM's operand)
+    z = W2 h + b2                       (float64 from the exact bf16 h, W2 and f32 b2)
+    """
+    W1, b1 = _f64(pred["weight"]), _f64(pred["bias"])
+    W2, b2 = _f64(pred["weight2"]), _f64(pred["bias2"])
+    a = x @ W1.T + b1[None, :]
+    h = f32_to_bf16_rne(np.maximum(a, 0.0).astype(np.float32)).astype(np.float64)
+    return h @ W2.T + b2[None, :]
+
+
 def argmax_first(z: np.ndarray) -> np.ndarray:
     """argmax over classes, lowest index on ties (R12)."""
     best = np.zeros(z.shape[0], dtype=np.int64)
@@ -186,10 +206,12 @@ def margin(z: np.ndarray, target: int) -> np.ndarray:
 
 
 def linear_verdict(pred: Dict, frames, frame_id, bbox, chunk=512, return_logits=False):
+    """LINEAR and MLP classifier predicates: argmax(logits(Crop(frame, bbox))) == target."""
+    head = mlp_logits if pred["kind"] == "mlp" else linear_logits
     out, logits = [], []
     for a in range(0, len(bbox), chunk):
         x = crop_features(pred, frames, frame_id[a:a + chunk], bbox[a:a + chunk])
-        z = linear_logits(pred, x)
+        z = head(pred, x)
         out.append(argmax_first(z) == int(pred["target"]))
         if return_logits:
             logits.append(z)
@@ -217,7 +239,7 @@ def predicate_verdict(pred: Dict, tup: Dict[str, np.ndarray], frames=None) -> np
         return label_verdict(pred, tup["label"])
     if kind == "hash":
         return hash_verdict(pred, tup["id"], tup["bbox"])
-    if kind == "linear":
+    if kind in ("linear", "mlp"):
         return linear_verdict(pred, frames, tup["frame_id"], tup["bbox"])
     raise ValueError(kind)
 

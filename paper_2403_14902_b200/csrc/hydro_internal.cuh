@@ -38,12 +38,22 @@ constexpr int kAKBlockBytes = kTileM * 128;                 // one 128 x 64 fp16
 constexpr int kARing = 6;                                   // A K-block stages (2 crop rows)
 constexpr int kBRing = 3;                                   // B K-block stages
 constexpr int kMaxSegBytes = 784;                           // 3*255 + 16-byte alignment slack
-constexpr int kQuadDepth = 2;                               // quads staged ahead per converter warp
+#ifndef HYDRO_QUAD_DEPTH
+#define HYDRO_QUAD_DEPTH 2
+#endif
+constexpr int kQuadDepth = HYDRO_QUAD_DEPTH;                // quads staged ahead per converter warp
 constexpr int kQuadSlots = kQuadDepth + 1;
 constexpr int kQuadSlotBytes = 4 * kMaxSegBytes;            // 4 rows x worst-case segment
 constexpr int kClsSmemBytes = 232448;                       // 227 KB opt-in maximum
 
-enum PredKind : int32_t { kLabelEq = HYDRO_PRED_LABEL_EQ, kHash = HYDRO_PRED_HASH, kLinear = HYDRO_PRED_LINEAR };
+enum PredKind : int32_t {
+  kLabelEq = HYDRO_PRED_LABEL_EQ,
+  kHash = HYDRO_PRED_HASH,
+  kLinear = HYDRO_PRED_LINEAR,
+  kMlp = HYDRO_PRED_MLP
+};
+// classifier hops run in K4 (linear or MLP head); cheap hops run in K1
+__host__ __device__ inline bool is_classifier(int32_t kind) { return kind == kLinear || kind == kMlp; }
 
 struct PredDev {
   int32_t kind;
@@ -56,7 +66,9 @@ struct PredDev {
   const float* bias;        // [n_pad] (padding rows: -inf never wins; they are skipped anyway)
   int32_t n_classes, n_pad, target, crop_mode;
   int32_t a_fp16;           // 1: operands staged as fp16 (weights exactly representable), 0: bf16
-  int32_t pad_;
+  int32_t hidden;           // MLP: hidden width (256 / 512); w_tiled = W1 (n_pad rows = hidden), bias = b2
+  const uint8_t* w2_tiled;  // MLP: W2 [hidden/64 kblk][n_pad rows][128 B SW128], bf16
+  const float* bias1;       // MLP: b1 [hidden]
 };
 
 // Device-resident eddy state (one per context).  d_* are the atomically accumulated deltas of
@@ -91,7 +103,7 @@ __host__ __device__ inline void build_sched(const int32_t* kind, const int32_t* 
   int n = 0;
   if (P == 0) sched[n++] = 0;
   for (int h = 0; h < P; ++h)
-    if (kind[order[h]] == kLinear || h == 0 || kind[order[h - 1]] == kLinear) sched[n++] = h;
+    if (is_classifier(kind[order[h]]) || h == 0 || is_classifier(kind[order[h - 1]])) sched[n++] = h;
   for (; n < kMaxPred; ++n) sched[n] = -1;
 }
 
@@ -331,6 +343,7 @@ __global__ void hydro_route_kernel(hydro::RouteParams p);
 __global__ void hydro_compact_kernel(hydro::CompactParams p);
 cudaError_t hydro_classifier_configure();
 void hydro_classifier_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug, bool area);
+void hydro_mlp_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug);
 __global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode);
 __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,
-                                          int32_t to_fp16, int32_t* inexact);
+                                          int32_t k_features, int32_t to_fp16, int32_t* inexact);

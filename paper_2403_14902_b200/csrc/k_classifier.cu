@@ -35,15 +35,22 @@ constexpr int kPair = 2;  // CTA pairs (cta_group::2, M=256): each CTA holds hal
 #else
 constexpr int kPair = 1;
 #endif
+#ifdef HYDRO_PAIR_SMALL_B
+static_assert(kPair == 2, "HYDRO_PAIR_SMALL_B needs HYDRO_2CTA");
+constexpr int kBStages = kBRing;  // pair mode: half-size stages, half the B-ring bytes (freed for staging)
+#else
 constexpr int kBStages = kBRing * kPair;  // same B-ring bytes; half-size stages in pair mode
+#endif
 
 struct ClsCtrl {
   uint64_t full_a[kARing], empty_a[kARing];
   uint64_t full_b[kBStages], empty_b[kBStages];
   uint64_t tfull[2], tempty[2];
+  uint64_t hready, tfull2;  // MLP: hidden layer written back to TMEM / second GEMM done
   uint32_t tmem_base;
   uint32_t pad;
   float bias[HYDRO_MAX_CLASSES];
+  float bias1[HYDRO_MLP_HIDDEN_MAX];  // MLP: b1
 };
 
 __device__ __forceinline__ uint32_t bf16_bits_of_byte(uint32_t b) {
@@ -190,6 +197,31 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
+// D[tmem] (+)= A[tmem] . B[smem]^T, CTA pair (the MLP's second layer reads the bf16 hidden
+// activations straight from tensor memory: lane = tuple, 32-bit column j = elements 2j, 2j+1)
+__device__ __forceinline__ void tc_mma_pair_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_st_32x32b_x8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
 }  // namespace
 
 // One quad (4 crop rows x 8 lanes) of output pixels: lane (r, j) produces pixels 8j .. 8j+7 of
@@ -246,56 +278,6 @@ __device__ __forceinline__ void convert_quad(uint32_t seg, const uint32_t (&po)[
   }
 }
 
-#ifdef HYDRO_ROWWISE
-// One crop row per warp instruction: lane l produces output pixels 2l, 2l+1 of a row (6 fp16 =
-// 3 words, words 3l .. 3l+2 of the row's 96).  The 32 lanes read one row's staged segment at
-// increasing offsets, so a load touches a contiguous word range (few bank conflicts); the second
-// word is read only when the pixel's 3 bytes straddle two words.  Stores are 32-bit: lane l's
-// words land in pairwise different banks for every swizzle phase (conflict-free).
-// Four rows at a time: all 16 loads are issued before any store so their latencies overlap.
-__device__ __forceinline__ uint32_t fetch_px(uint32_t seg, uint32_t o) {
-  const uint32_t a = seg + (o & ~3u);
-  const uint32_t w0 = lds32(a);
-  const uint32_t w1 = lds32_if(a + 4, (o & 2u) != 0u);
-  return __funnelshift_r(w0, w1, o << 3);
-}
-template <bool kFp16, bool kDbg>
-__device__ __forceinline__ void convert_rows4(const uint32_t (&seg)[4], const uint32_t (&po)[4],
-                                              const uint32_t (&rbase)[4], const uint32_t (&sw)[4],
-                                              const uint32_t (&bt)[3], uint16_t* const (&dbg)[4]) {
-  uint32_t px[4][2];
-#pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
-    px[rr][0] = fetch_px(seg[rr], po[rr] & 0xFFFFu);
-    px[rr][1] = fetch_px(seg[rr], po[rr] >> 16);
-  }
-#pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
-    const uint32_t p0 = px[rr][0], p1 = px[rr][1];
-    uint32_t e[3];
-    if (kFp16) {
-      const uint32_t K = 0x64646464u;
-      e[0] = f16x2_sub(__byte_perm(p0, K, 0x4140), 0x64006400u);
-      e[1] = f16x2_sub(__byte_perm(__byte_perm(p0, p1, 0x0042), K, 0x4140), 0x64006400u);
-      e[2] = f16x2_sub(__byte_perm(p1, K, 0x4241), 0x64006400u);
-    } else {
-      e[0] = bf16x2_of_bytes(p0 & 0xFF, (p0 >> 8) & 0xFF);
-      e[1] = bf16x2_of_bytes((p0 >> 16) & 0xFF, p1 & 0xFF);
-      e[2] = bf16x2_of_bytes((p1 >> 8) & 0xFF, (p1 >> 16) & 0xFF);
-    }
-#pragma unroll
-    for (int t = 0; t < 3; ++t) sts32(rbase[rr] + (bt[t] ^ sw[rr]), e[t]);
-    if (kDbg && dbg[rr]) {
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {
-        dbg[rr][3 * kk + 0] = static_cast<uint16_t>(bf16_bits_of_byte(px[rr][kk] & 0xFF));
-        dbg[rr][3 * kk + 1] = static_cast<uint16_t>(bf16_bits_of_byte((px[rr][kk] >> 8) & 0xFF));
-        dbg[rr][3 * kk + 2] = static_cast<uint16_t>(bf16_bits_of_byte((px[rr][kk] >> 16) & 0xFF));
-      }
-    }
-  }
-}
-#endif
 
 // AREA crop (R10, cfg4): output pixel (dy, dx) is the mean over the bin
 // [y0 + dy*h//64, y0 + ceil((dy+1)h/64)) x [x0 + dx*w//64, x0 + ceil((dx+1)w/64)), one IEEE f32
@@ -343,6 +325,125 @@ __device__ __forceinline__ void convert_quad_area(const uint8_t* frames, uint32_
   }
 }
 
+// Converter warps (shared by the linear and the MLP classifier kernels): cp.async-staged crop-row
+// segments -> pixels -> the swizzled K-major A ring, one K-group (crop row g of all 128 tuples of
+// the CTA's M-tile) at a time, full_a / empty_a handshake with the MMA issuer.
+template <bool kDbg, bool kArea, int kP, int kQD>
+__device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl, const uint32_t* list_in,
+                                               uint32_t base, uint32_t count, uint32_t unit0, uint32_t unit_stride,
+                                               uint32_t num_units, uint32_t crank, int warp, int lane,
+                                               uint32_t staging_addr, uint32_t a_ring, uint32_t row_pitch, bool area,
+                                               bool fp16) {
+  constexpr int kQS = kQD + 1;
+  // ===================== converters: cp.async-staged segments -> pixels -> swizzled A ring
+  // Warp cu owns rows 16*cu .. 16*cu+15; it walks them as "quads" of 4 rows (one warp
+  // instruction = 4 rows x 8 lanes x 8 output pixels).  Quad k's source segments are
+  // copied (16-byte cp.async, coalesced per row) kQD quads ahead into fixed slots.
+  const int cu = warp - kConvWarp0;
+  const int r = lane >> 3, j = lane & 7;  // row-in-quad and 8-pixel block (pixels 8j .. 8j+7)
+  const uint32_t slots = staging_addr + static_cast<uint32_t>(cu) * (kQS * kQuadSlotBytes);
+  const uint8_t* frames = p.frames;
+  uint32_t gg = 0;
+  for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
+    const uint32_t tile = unit * kP + crank;
+    // rows' metadata: lane l < 16 holds row 16*cu + l
+    const RowMeta mm = load_meta(p, list_in, base, tile * kTileM + cu * kConvRows + (lane & 15),
+                                 lane < 16 ? count : 0u);
+    const uint32_t my_src = mm.row0 + mm.seg_lo;                 // + sy * pitch per crop row
+    const uint32_t my_len = (lane < 16 && mm.valid) ? mm.seg_len : 0u;
+    const uint32_t my_h = static_cast<uint32_t>(mm.h);
+    uint32_t po[4][4];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int src = 4 * it + r;
+      const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src);
+      const uint32_t w = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src);
+      const uint32_t slo = __shfl_sync(0xFFFFFFFFu, mm.seg_lo, src);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t dx0 = 8u * j + 2u * q;
+        const uint32_t o0 = 3u * (x0 + (((2u * dx0 + 1u) * w) >> 7)) - slo;
+        const uint32_t o1 = 3u * (x0 + (((2u * dx0 + 3u) * w) >> 7)) - slo;
+        po[it][q] = o0 | (o1 << 16);
+      }
+    }
+    // Stage quad k = 4*g + it (rows 4*it .. 4*it+3 of this warp, crop row g) into slot k % kQS:
+    // lanes 8r .. 8r+7 copy row r's segment in 16-byte chunks j + 8c (c < 7: segments <= 784 B).
+    auto stage_quad = [&](int k, uint32_t slot) {
+      if (!area && k < kGroups * 4) {
+        const int g = k >> 2, it = k & 3;
+        const int src_lane = 4 * it + r;
+        const uint32_t len = __shfl_sync(0xFFFFFFFFu, my_len, src_lane);
+        const uint32_t off = __shfl_sync(0xFFFFFFFFu, my_src, src_lane);
+        const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
+        const uint8_t* src = frames + (off + (((2u * g + 1u) * h) >> 7) * row_pitch + 16u * j);
+        const uint32_t dst = slots + slot * kQuadSlotBytes + r * kMaxSegBytes + 16u * j;
+        const uint32_t nch = len >> 4;
+#pragma unroll
+        for (int c = 0; c < 7; ++c)
+          if (j + 8u * c < nch) cp_async16(dst + 128u * c, src + 128u * c);
+      }
+      cp_async_commit();  // one group per quad (possibly empty) keeps wait_group counting uniform
+    };
+    uint32_t slot_stage = 0, slot_use = 0;
+#pragma unroll
+    for (int k = 0; k < kQD; ++k) {
+      stage_quad(k, slot_stage);
+      slot_stage = slot_stage + 1 == kQS ? 0 : slot_stage + 1;
+    }
+    for (int g = 0; g < kGroups; ++g, ++gg) {
+      const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph = (gg >> 1) & 1u;
+#pragma unroll
+      for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_wait(&ctrl->empty_a[set + kbr], aph ^ 1u);
+      const uint32_t a_set = a_ring + set * kAKBlockBytes;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        stage_quad(4 * g + it + kQD, slot_stage);
+        slot_stage = slot_stage + 1 == kQS ? 0 : slot_stage + 1;
+        cp_async_wait<kQD>();  // this thread's copies of quad k have landed
+        __syncwarp();                 // ... and every lane's
+        // rows past the tile's count convert stale bytes into A rows whose results are masked
+        const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * it + r);
+        const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kMaxSegBytes;
+        const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
+        uint16_t* dbg = (kDbg && p.dbg_crops && tile * kTileM + m < count)
+                            ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + m) * kFeatures + g * 192 + 24 * j
+                            : nullptr;
+        if (kArea && area) {
+          const int src_lane = 4 * it + r;
+          const uint32_t ar0 = __shfl_sync(0xFFFFFFFFu, mm.row0, src_lane);
+          const uint32_t ah = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.h), src_lane);
+          const uint32_t ax0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src_lane);
+          const uint32_t aw = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
+          if (fp16) convert_quad_area<true, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
+          else convert_quad_area<false, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
+        } else {
+          if (fp16) convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
+          else convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
+        }
+        slot_use = slot_use + 1 == kQS ? 0 : slot_use + 1;
+        __syncwarp();  // the slot is refilled kQD quads later
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) {
+          if (kP == 2 && crank != 0) mbar_arrive_leader(&ctrl->full_a[set + kbr]);
+          else mbar_arrive(&ctrl->full_a[set + kbr]);
+        }
+      }
+    }
+    cp_async_wait<0>();
+  }
+  if (kP == 2) {  // drain: both A sets released (the leader's commits land here)
+    for (int e = 0; e < 2; ++e, ++gg) {
+      const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph = (gg >> 1) & 1u;
+      for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_wait(&ctrl->empty_a[set + kbr], aph ^ 1u);
+    }
+  }
+}
+
 extern __shared__ __align__(1024) uint8_t hydro_cls_smem[];
 
 template <bool kDbg, bool kArea>
@@ -357,7 +458,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     const int h = st->sched[p.hop];  // p.hop is the chain slot
     if (h < 0 || h >= st->n_pred) return;
     pred = st->order[h];
-    if (st->kind[pred] != kLinear) return;
+    if (st->kind[pred] != kLinear) return;  // (an MLP hop runs in hydro_mlp_kernel)
     if (h == 0) {
       list_in = nullptr;
       count = p.range_n;
@@ -397,7 +498,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   uint8_t* smem = hydro_cls_smem + (((raw + 1023u) & ~1023u) - raw);
   const uint32_t a_ring = smem_u32(smem);
   const uint32_t b_ring = a_ring + kARing * kAKBlockBytes;
-  const uint32_t ctrl_off = kARing * kAKBlockBytes + kBRing * b_stage_bytes;
+  const uint32_t ctrl_off = kARing * kAKBlockBytes + kBStages * b_load_bytes;
   ClsCtrl* ctrl = reinterpret_cast<ClsCtrl*>(smem + ctrl_off);
   const uint32_t stg_off = (ctrl_off + static_cast<uint32_t>(sizeof(ClsCtrl)) + 15u) & ~15u;
   uint8_t* staging = smem + stg_off;
@@ -543,149 +644,8 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     }
     __syncwarp();
   } else if (warp >= kConvWarp0) {
-    // ===================== converters: cp.async-staged segments -> pixels -> swizzled A ring
-    // Warp cu owns rows 16*cu .. 16*cu+15; it walks them as "quads" of 4 rows (one warp
-    // instruction = 4 rows x 8 lanes x 8 output pixels).  Quad k's source segments are
-    // copied (16-byte cp.async, coalesced per row) kQuadDepth quads ahead into fixed slots.
-    const int cu = warp - kConvWarp0;
-    const int r = lane >> 3, j = lane & 7;  // row-in-quad and 8-pixel block (pixels 8j .. 8j+7)
-    const uint32_t slots = staging_addr + static_cast<uint32_t>(cu) * (kQuadSlots * kQuadSlotBytes);
-    const uint8_t* frames = p.frames;
-#ifdef HYDRO_ROWWISE
-    uint32_t bt[3];  // lane's words 3*lane+t of a crop row: K-block, 16-byte chunk (pre-swizzle), word
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      const uint32_t W = 3u * static_cast<uint32_t>(lane) + t;
-      bt[t] = (W >> 5) * kAKBlockBytes + (((W >> 2) & 7u) << 4) + (W & 3u) * 4u;
-    }
-#endif
-    uint32_t gg = 0;
-    for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
-      const uint32_t tile = unit * kPair + crank;
-      // rows' metadata: lane l < 16 holds row 16*cu + l
-      const RowMeta mm = load_meta(p, list_in, base, tile * kTileM + cu * kConvRows + (lane & 15),
-                                   lane < 16 ? count : 0u);
-      const uint32_t my_src = mm.row0 + mm.seg_lo;                 // + sy * pitch per crop row
-      const uint32_t my_len = (lane < 16 && mm.valid) ? mm.seg_len : 0u;
-      const uint32_t my_h = static_cast<uint32_t>(mm.h);
-#ifdef HYDRO_ROWWISE
-      // lane i < 16 holds row i's (x0, w); each row's pixel offsets are recomputed where used
-      const uint32_t xw = static_cast<uint32_t>(mm.x0) | (static_cast<uint32_t>(mm.w) << 16);
-      const uint32_t k0 = 4u * static_cast<uint32_t>(lane) + 1u;  // (2*dx + 1) for dx = 2*lane
-#else
-      uint32_t po[4][4];
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const int src = 4 * it + r;
-        const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src);
-        const uint32_t w = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src);
-        const uint32_t slo = __shfl_sync(0xFFFFFFFFu, mm.seg_lo, src);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t dx0 = 8u * j + 2u * q;
-          const uint32_t o0 = 3u * (x0 + (((2u * dx0 + 1u) * w) >> 7)) - slo;
-          const uint32_t o1 = 3u * (x0 + (((2u * dx0 + 3u) * w) >> 7)) - slo;
-          po[it][q] = o0 | (o1 << 16);
-        }
-      }
-#endif
-      // Stage quad k = 4*g + it (rows 4*it .. 4*it+3 of this warp, crop row g) into slot k % kQuadSlots:
-      // lanes 8r .. 8r+7 copy row r's segment in 16-byte chunks j + 8c (c < 7: segments <= 784 B).
-      auto stage_quad = [&](int k, uint32_t slot) {
-        if (!area && k < kGroups * 4) {
-          const int g = k >> 2, it = k & 3;
-          const int src_lane = 4 * it + r;
-          const uint32_t len = __shfl_sync(0xFFFFFFFFu, my_len, src_lane);
-          const uint32_t off = __shfl_sync(0xFFFFFFFFu, my_src, src_lane);
-          const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
-          const uint8_t* src = frames + (off + (((2u * g + 1u) * h) >> 7) * row_pitch + 16u * j);
-          const uint32_t dst = slots + slot * kQuadSlotBytes + r * kMaxSegBytes + 16u * j;
-          const uint32_t nch = len >> 4;
-#pragma unroll
-          for (int c = 0; c < 7; ++c)
-            if (j + 8u * c < nch) cp_async16(dst + 128u * c, src + 128u * c);
-        }
-        cp_async_commit();  // one group per quad (possibly empty) keeps wait_group counting uniform
-      };
-      uint32_t slot_stage = 0, slot_use = 0;
-#pragma unroll
-      for (int k = 0; k < kQuadDepth; ++k) {
-        stage_quad(k, slot_stage);
-        slot_stage = slot_stage + 1 == kQuadSlots ? 0 : slot_stage + 1;
-      }
-      for (int g = 0; g < kGroups; ++g, ++gg) {
-        const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph = (gg >> 1) & 1u;
-#pragma unroll
-        for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_wait(&ctrl->empty_a[set + kbr], aph ^ 1u);
-        const uint32_t a_set = a_ring + set * kAKBlockBytes;
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          stage_quad(4 * g + it + kQuadDepth, slot_stage);
-          slot_stage = slot_stage + 1 == kQuadSlots ? 0 : slot_stage + 1;
-          cp_async_wait<kQuadDepth>();  // this thread's copies of quad k have landed
-          __syncwarp();                 // ... and every lane's
-          // rows past the tile's count convert stale bytes into A rows whose results are masked
-          const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * it + r);
-          const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kMaxSegBytes;
-          const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
-          uint16_t* dbg = (kDbg && p.dbg_crops && tile * kTileM + m < count)
-                              ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + m) * kFeatures + g * 192 + 24 * j
-                              : nullptr;
-          if (kArea && area) {
-            const int src_lane = 4 * it + r;
-            const uint32_t ar0 = __shfl_sync(0xFFFFFFFFu, mm.row0, src_lane);
-            const uint32_t ah = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.h), src_lane);
-            const uint32_t ax0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src_lane);
-            const uint32_t aw = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
-            if (fp16) convert_quad_area<true, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
-            else convert_quad_area<false, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
-          } else {
-#ifdef HYDRO_ROWWISE
-            (void)seg;
-            uint32_t seg4[4], po4[4], rb4[4], sw4[4];
-            uint16_t* dbg4[4];
-#pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-              const uint32_t mr = static_cast<uint32_t>(cu * kConvRows + 4 * it + rr);
-              seg4[rr] = slots + slot_use * kQuadSlotBytes + rr * kMaxSegBytes;
-              rb4[rr] = a_set + (mr >> 3) * 1024u + (mr & 7u) * 128u;
-              sw4[rr] = static_cast<uint32_t>((4 * it + rr) & 7) << 4;  // == (mr & 7) << 4
-              dbg4[rr] = (kDbg && p.dbg_crops && tile * kTileM + mr < count)
-                             ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + mr) * kFeatures + g * 192 + 6 * lane
-                             : nullptr;
-              const uint32_t rxw = __shfl_sync(0xFFFFFFFFu, xw, 4 * it + rr);
-              const uint32_t x0 = rxw & 0xFFFFu, w = rxw >> 16;
-              const uint32_t base_o = 3u * x0 - ((3u * x0) & ~15u);  // 3*x0 - seg_lo
-              po4[rr] = (base_o + 3u * ((k0 * w) >> 7)) | ((base_o + 3u * (((k0 + 2u) * w) >> 7)) << 16);
-            }
-            if (fp16) convert_rows4<true, kDbg>(seg4, po4, rb4, sw4, bt, dbg4);
-            else convert_rows4<false, kDbg>(seg4, po4, rb4, sw4, bt, dbg4);
-#else
-            if (fp16) convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
-            else convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
-#endif
-          }
-          slot_use = slot_use + 1 == kQuadSlots ? 0 : slot_use + 1;
-          __syncwarp();  // the slot is refilled kQuadDepth quads later
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-#pragma unroll
-          for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) {
-            if (kPair == 2 && crank != 0) mbar_arrive_leader(&ctrl->full_a[set + kbr]);
-            else mbar_arrive(&ctrl->full_a[set + kbr]);
-          }
-        }
-      }
-      cp_async_wait<0>();
-    }
-    if (kPair == 2) {  // drain: both A sets released (the leader's commits land here)
-      for (int e = 0; e < 2; ++e, ++gg) {
-        const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph = (gg >> 1) & 1u;
-        for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_wait(&ctrl->empty_a[set + kbr], aph ^ 1u);
-      }
-    }
+    converter_role<kDbg, kArea, kPair, kQuadDepth>(p, ctrl, list_in, base, count, unit0, unit_stride, num_units, crank,
+                                                   warp, lane, staging_addr, a_ring, row_pitch, area, fp16);
   } else {
     // ===================== epilogue warps 0..3 (TMEM lane quadrant = warp)
     const int q = warp;
@@ -761,48 +721,326 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   }
 }
 
-// Host-side entry points (the kernel template stays inside this translation unit).
-cudaError_t hydro_classifier_configure() {
-  cudaError_t e;
-  if ((e = cudaFuncSetAttribute(hydro_classifier_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kClsSmemBytes)) != cudaSuccess)
-    return e;
-  if ((e = cudaFuncSetAttribute(hydro_classifier_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kClsSmemBytes)) != cudaSuccess)
-    return e;
-  if ((e = cudaFuncSetAttribute(hydro_classifier_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kClsSmemBytes)) != cudaSuccess)
-    return e;
-  return cudaFuncSetAttribute(hydro_classifier_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kClsSmemBytes);
+// ------------------------------------------------------------------------------------------
+// K4-MLP (R25): z = W2 . bf16(relu(W1 . Crop(frame, bbox) + b1)) + b2, verdict
+// argmax z == target.  CTA pairs (cta_group::2, M = 256 tuples per unit): the first layer is
+// 12288 x hidden (hidden = 256 / 512), N = 256 per MMA, its fp32 accumulator fills the CTA's whole
+// TMEM (512 columns).  The epilogue adds b1, applies ReLU, rounds to bf16 and writes the packed
+// activations back into TMEM columns [0, hidden/2); the second layer then runs with A read from
+// TMEM (no shared-memory round trip) into columns [256, 256 + n_pad).  W1 K-blocks (each CTA
+// loads its half of every N=256 slice) and W2 K-blocks stream through a 2 x 32 KB ring; the
+// converters are the linear kernel's, with a one-quad staging lookahead (shared memory).
+template <bool kDbg>
+__global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) {
+  constexpr int kP = 2, kQD = 1, kMB = 2;
+  constexpr uint32_t kMlpBStage = 32768;
+  DevState* st = p.st;
+  int pred;
+  const uint32_t* list_in;
+  uint32_t count, base = p.range_base;
+  uint32_t* bits_out;
+  if (p.dispatch) {
+    const int h = st->sched[p.hop];
+    if (h < 0 || h >= st->n_pred) return;
+    pred = st->order[h];
+    if (st->kind[pred] != kMlp) return;
+    if (h == 0) {
+      list_in = nullptr;
+      count = p.range_n;
+    } else {
+      list_in = p.lists + static_cast<uint64_t>(h) * p.list_stride;
+      count = p.counts[h];
+    }
+    bits_out = p.bits + static_cast<uint64_t>(h) * p.bits_stride;
+  } else {
+    pred = p.explicit_pred;
+    list_in = p.list_in;
+    count = list_in ? *p.count_in : p.range_n;
+    bits_out = p.bits_out;
+  }
+  const uint32_t num_tiles = (count + kTileM - 1) / kTileM;
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t unit0 = blockIdx.x / kP, unit_stride = gridDim.x / kP;
+  const uint32_t num_units = (num_tiles + kP - 1) / kP;
+  if (unit0 >= num_units) return;
+
+  const long long t_start = clock64();
+  const PredDev& pdg = p.preds[pred];
+  const int n_classes = pdg.n_classes, n_pad = pdg.n_pad, target = pdg.target, hidden = pdg.hidden;
+  const bool fp16 = pdg.a_fp16 != 0;
+  const int n_mma1 = hidden / 256;                                     // N=256 slices of layer 1
+  const uint32_t w1_stage = static_cast<uint32_t>(n_mma1) * 16384u;     // this CTA's half of each slice
+  const uint32_t w1_kb = static_cast<uint32_t>(hidden) * 128u;          // one tiled W1 K-block
+  const uint32_t w2_load = static_cast<uint32_t>(n_pad / 2) * 128u;     // this CTA's half of a W2 K-block
+  const uint32_t w2_kb = static_cast<uint32_t>(n_pad) * 128u;
+  const int n_kb2 = hidden / kKBlock;
+  const uint32_t tmem_cols = 512;
+  const uint32_t row_pitch = static_cast<uint32_t>(p.frame_w * 3);
+
+  const uint32_t raw = smem_u32(hydro_cls_smem);
+  uint8_t* smem = hydro_cls_smem + (((raw + 1023u) & ~1023u) - raw);
+  const uint32_t a_ring = smem_u32(smem);
+  const uint32_t b_ring = a_ring + kARing * kAKBlockBytes;
+  const uint32_t ctrl_off = kARing * kAKBlockBytes + kMB * kMlpBStage;
+  ClsCtrl* ctrl = reinterpret_cast<ClsCtrl*>(smem + ctrl_off);
+  const uint32_t stg_off = (ctrl_off + static_cast<uint32_t>(sizeof(ClsCtrl)) + 15u) & ~15u;
+  const uint32_t staging_addr = smem_u32(smem + stg_off);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kARing; ++s) {
+      mbar_init(&ctrl->full_a[s], kConvWarps * kP);
+      mbar_init(&ctrl->empty_a[s], 1);
+    }
+    for (int s = 0; s < kMB; ++s) {
+      mbar_init(&ctrl->full_b[s], crank == 0 ? 2 : 1);
+      mbar_init(&ctrl->empty_b[s], 1);
+    }
+    mbar_init(&ctrl->tfull[0], 1);
+    mbar_init(&ctrl->tempty[0], kEpiWarps * kP);
+    mbar_init(&ctrl->hready, kEpiWarps * kP);
+    mbar_init(&ctrl->tfull2, 1);
+    fence_mbar_init();
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&ctrl->tmem_base)),
+                 "r"(tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (tid < HYDRO_MAX_CLASSES) ctrl->bias[tid] = tid < n_classes ? pdg.bias[tid] : 0.0f;
+  for (int i = tid; i < hidden; i += kClsThreads) ctrl->bias1[i] = pdg.bias1[i];
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = ctrl->tmem_base;
+  const int kb_per_tile = kNumKBlocks + n_kb2;
+
+  if (warp == kLoaderWarp) {
+    // ===================== loader: W1 K-blocks (this CTA's half of each N=256 slice), then W2
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_last();
+      uint32_t itb = 0;
+      for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
+        for (int kb = 0; kb < kb_per_tile; ++kb, ++itb) {
+          const uint32_t s = itb % kMB, ph = (itb / kMB) & 1u;
+          HYDRO_PIPE_WAIT(&ctrl->empty_b[s], ph ^ 1u);
+          uint8_t* dst = smem + (b_ring - a_ring) + s * kMlpBStage;
+          if (kb < kNumKBlocks) {
+            mbar_arrive_expect_tx(&ctrl->full_b[s], w1_stage);
+            for (int m = 0; m < n_mma1; ++m)
+              bulk_g2s_hint(dst + m * 16384, pdg.w_tiled + static_cast<uint64_t>(kb) * w1_kb + (m * 256 + crank * 128) * 128u,
+                            16384u, &ctrl->full_b[s], pol_w);
+          } else {
+            mbar_arrive_expect_tx(&ctrl->full_b[s], w2_load);
+            bulk_g2s_hint(dst, pdg.w2_tiled + static_cast<uint64_t>(kb - kNumKBlocks) * w2_kb + crank * w2_load, w2_load,
+                          &ctrl->full_b[s], pol_w);
+          }
+        }
+      }
+      for (int e = 0; e < kMB; ++e, ++itb) mbar_wait(&ctrl->empty_b[itb % kMB], ((itb / kMB) & 1u) ^ 1u);
+    }
+    __syncwarp();
+  } else if (warp == kMmaWarp) {
+    if (crank != 0 && lane == 0) {
+      // peer: relay "my half of the B stage landed" to the leader
+      uint32_t itb = 0;
+      for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
+        for (int kb = 0; kb < kb_per_tile; ++kb, ++itb) {
+          const uint32_t s = itb % kMB;
+          mbar_wait(&ctrl->full_b[s], (itb / kMB) & 1u);
+          mbar_arrive_leader(&ctrl->full_b[s]);
+        }
+      }
+    } else if (lane == 0) {
+      // ===================== leader MMA issuer
+      const uint32_t idesc1 = idesc_f16_f32(kTileM * kP, 256u, !fp16);
+      const uint32_t idesc2 = idesc_f16_f32(kTileM * kP, static_cast<uint32_t>(n_pad), true);
+      uint32_t itb = 0, gg = 0, tl = 0;
+      for (uint32_t unit = unit0; unit < num_units; unit += unit_stride, ++tl) {
+        mbar_wait_sleep(&ctrl->tempty[0], (tl & 1u) ^ 1u);  // previous unit's logits read out
+        tc_fence_after();
+        for (int g = 0; g < kGroups; ++g, ++gg) {
+          const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph2 = (gg >> 1) & 1u;
+#pragma unroll
+          for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr, ++itb) {
+            const uint32_t sa = set + kbr;
+            const uint32_t sb = itb % kMB, bph = (itb / kMB) & 1u;
+            HYDRO_PIPE_WAIT(&ctrl->full_a[sa], aph2);
+            HYDRO_PIPE_WAIT(&ctrl->full_b[sb], bph);
+            tc_fence_after();
+            const uint32_t a_addr = a_ring + sa * kAKBlockBytes;
+            const uint32_t b_addr = b_ring + sb * kMlpBStage;
+#pragma unroll
+            for (int kk = 0; kk < kKBlock / 16; ++kk) {
+              for (int m = 0; m < n_mma1; ++m)
+                tc_mma_pair(tmem_base + m * 256, desc_sw128(a_addr + kk * 32), desc_sw128(b_addr + m * 16384 + kk * 32),
+                            idesc1, (g | kbr | kk) != 0 ? 1u : 0u);
+            }
+            tc_commit_pair(&ctrl->empty_a[sa]);
+            tc_commit_pair(&ctrl->empty_b[sb]);
+          }
+        }
+        tc_commit_pair(&ctrl->tfull[0]);
+        mbar_wait_sleep(&ctrl->hready, tl & 1u);  // bf16 hidden activations back in TMEM (both CTAs)
+        tc_fence_after();
+        for (int kb2 = 0; kb2 < n_kb2; ++kb2, ++itb) {
+          const uint32_t sb = itb % kMB, bph = (itb / kMB) & 1u;
+          HYDRO_PIPE_WAIT(&ctrl->full_b[sb], bph);
+          tc_fence_after();
+          const uint32_t b_addr = b_ring + sb * kMlpBStage;
+#pragma unroll
+          for (int kk = 0; kk < kKBlock / 16; ++kk)
+            tc_mma_pair_ts(tmem_base + 256, tmem_base + kb2 * (kKBlock / 2) + kk * 8, desc_sw128(b_addr + kk * 32), idesc2,
+                           (kb2 | kk) != 0 ? 1u : 0u);
+          tc_commit_pair(&ctrl->empty_b[sb]);
+        }
+        tc_commit_pair(&ctrl->tfull2);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kConvWarp0) {
+    converter_role<kDbg, false, kP, kQD>(p, ctrl, list_in, base, count, unit0, unit_stride, num_units, crank, warp, lane,
+                                         staging_addr, a_ring, row_pitch, false, fp16);
+  } else {
+    // ===================== epilogue warps 0..3 (TMEM lane quadrant = warp)
+    const int q = warp;
+    uint32_t n_in = 0, n_pass = 0, tl = 0;
+    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+    for (uint32_t unit = unit0; unit < num_units; unit += unit_stride, ++tl) {
+      const uint32_t tile = unit * kP + crank;
+      mbar_wait_sleep(&ctrl->tfull[0], tl & 1u);
+      tc_fence_after();
+      // hidden: + b1, ReLU, bf16 RNE, packed pairs written back over the consumed fp32 columns
+      for (int c0 = 0; c0 < hidden; c0 += 16) {
+        uint32_t v[16], w[8];
+        tc_ld_32x32b_x16(taddr + c0, v);
+        tc_wait_ld();
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const float lo = fmaxf(__uint_as_float(v[2 * t]) + ctrl->bias1[c0 + 2 * t], 0.0f);
+          const float hi = fmaxf(__uint_as_float(v[2 * t + 1]) + ctrl->bias1[c0 + 2 * t + 1], 0.0f);
+          w[t] = bf16x2_rn(lo, hi);
+        }
+        tc_st_32x32b_x8(taddr + c0 / 2, w);
+      }
+      tc_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (crank != 0) mbar_arrive_leader(&ctrl->hready);
+        else mbar_arrive(&ctrl->hready);
+      }
+      mbar_wait_sleep(&ctrl->tfull2, tl & 1u);
+      tc_fence_after();
+      const int m = q * 32 + lane;
+      const uint32_t pos = tile * kTileM + m;
+      const bool valid = pos < count;
+      float best = -3.402823466e38f;
+      int bi = 0;
+      for (int c0 = 0; c0 < n_pad; c0 += 16) {
+        uint32_t v[16];
+        tc_ld_32x32b_x16(taddr + 256 + c0, v);
+        tc_wait_ld();
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int c = c0 + jj;
+          if (c < n_classes) {
+            const float z = __uint_as_float(v[jj]) + ctrl->bias[c];
+            if (z > best) {  // strict: lowest index wins ties (R12)
+              best = z;
+              bi = c;
+            }
+            if (kDbg && p.dbg_logits && valid) p.dbg_logits[static_cast<uint64_t>(pos) * n_classes + c] = z;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (crank != 0) mbar_arrive_leader(&ctrl->tempty[0]);
+        else mbar_arrive(&ctrl->tempty[0]);
+      }
+      const bool verdict = valid && (bi == target);
+      const uint32_t bv = __ballot_sync(0xFFFFFFFFu, verdict);
+      const uint32_t bvalid = __ballot_sync(0xFFFFFFFFu, valid);
+      if (lane == 0 && bvalid) {
+        bits_out[tile * (kTileM / 32) + q] = bv;
+        if (bv) {
+          atomicAdd(p.seg_counts + ((tile * kTileM + q * 32) / kRouteTile), static_cast<uint32_t>(__popc(bv)));
+          atomicAdd(p.warp_counts + ((tile * kTileM + q * 32) / kWarpSeg), static_cast<uint32_t>(__popc(bv)));
+        }
+      }
+      if (kDbg && p.dbg_verdict && valid) p.dbg_verdict[pos] = verdict ? 1 : 0;
+      n_in += __popc(bvalid);
+      n_pass += __popc(bv);
+    }
+    if (p.collect_stats && lane == 0) {
+      atomicAdd(&st->d_in[pred], static_cast<unsigned long long>(n_in));
+      atomicAdd(&st->d_pass[pred], static_cast<unsigned long long>(n_pass));
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols) : "memory");
+  }
+  if (tid == 0 && p.collect_stats) {
+    atomicAdd(&st->d_cost[pred], static_cast<unsigned long long>(clock64() - t_start));
+  }
 }
+
+// Host-side entry points (the kernel templates stay inside this translation unit).
+cudaError_t hydro_classifier_configure() {
+  void (*ks[])(ClsParams) = {hydro_classifier_kernel<false, false>, hydro_classifier_kernel<true, false>,
+                             hydro_classifier_kernel<false, true>, hydro_classifier_kernel<true, true>,
+                             hydro_mlp_kernel<false>, hydro_mlp_kernel<true>};
+  for (auto k : ks) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+namespace {
+// CTA-pair launch: grid = 2 x min(pairs of tiles, co-resident clusters of this kernel)
+void launch_pairs(void (*k)(ClsParams), int* max_clusters, const ClsParams& c, int grid, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kClsThreads);
+  cfg.dynamicSmemBytes = kClsSmemBytes;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (*max_clusters == 0) {
+    cfg.gridDim = dim3(2 * 74);
+    if (cudaOccupancyMaxActiveClusters(max_clusters, k, &cfg) != cudaSuccess || *max_clusters < 1) *max_clusters = 1;
+    if (getenv("HYDRO_DEBUG_LAUNCH")) fprintf(stderr, "hydro: K4 CTA pairs, %d co-resident clusters\n", *max_clusters);
+  }
+  const int pairs = std::min((grid + 1) / 2, *max_clusters);
+  cfg.gridDim = dim3(2 * pairs);
+  cudaLaunchKernelEx(&cfg, k, c);
+}
+}  // namespace
 
 void hydro_classifier_launch(const ClsParams& c, int grid, cudaStream_t stream, bool debug, bool area) {
   void (*k)(ClsParams) = area ? (debug ? hydro_classifier_kernel<true, true> : hydro_classifier_kernel<false, true>)
                               : (debug ? hydro_classifier_kernel<true, false> : hydro_classifier_kernel<false, false>);
   if constexpr (kPair == 2) {
-    // CTA pairs: grid = 2 x min(pairs of tiles, co-resident clusters)
     static int max_clusters = 0;
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(kClsThreads);
-    cfg.dynamicSmemBytes = kClsSmemBytes;
-    cfg.stream = stream;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (max_clusters == 0) {
-      cfg.gridDim = dim3(2 * 74);
-      if (cudaOccupancyMaxActiveClusters(&max_clusters, k, &cfg) != cudaSuccess || max_clusters < 1) max_clusters = 1;
-      if (getenv("HYDRO_DEBUG_LAUNCH")) fprintf(stderr, "hydro: K4 CTA pairs, %d co-resident clusters\n", max_clusters);
-    }
-    const int pairs = std::min((grid + 1) / 2, max_clusters);
-    cfg.gridDim = dim3(2 * pairs);
-    cudaLaunchKernelEx(&cfg, k, c);
+    launch_pairs(k, &max_clusters, c, grid, stream);
   } else {
     k<<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
   }
+}
+
+void hydro_mlp_launch(const ClsParams& c, int grid, cudaStream_t stream, bool debug) {
+  static int max_clusters = 0;
+  launch_pairs(debug ? hydro_mlp_kernel<true> : hydro_mlp_kernel<false>, &max_clusters, c, grid, stream);
 }

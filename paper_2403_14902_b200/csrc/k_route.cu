@@ -42,10 +42,10 @@ __device__ __forceinline__ bool k1_runs(const DevState* st, int h, int* run) {
   const int P = st->n_pred;
   *run = 0;
   if (P == 0) return h == 0;
-  if (h >= P || st->kind[st->order[h]] == kLinear) return false;
-  if (h > 0 && st->kind[st->order[h - 1]] != kLinear) return false;  // inside a run started earlier
+  if (h >= P || is_classifier(st->kind[st->order[h]])) return false;
+  if (h > 0 && !is_classifier(st->kind[st->order[h - 1]])) return false;  // inside a run started earlier
   int r = 0;
-  while (h + r < P && st->kind[st->order[h + r]] != kLinear) ++r;
+  while (h + r < P && !is_classifier(st->kind[st->order[h + r]])) ++r;
   *run = r;
   return true;
 }
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kern
   if (!s_work) {
     // hop h is a classifier hop: clear the segment counts its K4 accumulates into
     const int h = s_hop;
-    if (p.dispatch && h >= 0 && h < st->n_pred && st->kind[st->order[h]] == kLinear) {
+    if (p.dispatch && h >= 0 && h < st->n_pred && is_classifier(st->kind[st->order[h]])) {
       const uint32_t n = h == 0 ? p.range_n : p.counts[h];
       const uint32_t nseg = (n + kRouteTile - 1) / kRouteTile;
       for (uint32_t i = blockIdx.x * kRouteThreads + tid; i < nseg; i += gridDim.x * kRouteThreads) p.seg_counts[i] = 0;
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactPar
         next = 0;
       } else if (k1_runs(st, h, &run)) {
         next = h + run;
-      } else if (h < P && st->kind[st->order[h]] == kLinear) {
+      } else if (h < P && is_classifier(st->kind[st->order[h]])) {
         next = h + 1;
       } else {
         work = 0;
@@ -633,14 +633,15 @@ __global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Weight re-layout: W[C][12288] bf16 row-major -> [192 K-blocks][n_pad rows][128 B] with the
+// Weight re-layout: W[rows][K] bf16 row-major (K = 12288: a linear head or MLP layer 1; K = hidden:
+// MLP layer 2) -> [K/64 K-blocks][n_pad rows][128 B] with the
 // 128-byte swizzle applied (16-byte chunk c of row n stored at chunk c ^ (n & 7)), i.e. the exact
 // shared-memory image UMMA reads, so one 1-D bulk copy per stage lands it.  Rows >= C are 0.
 // to_fp16 = 1 re-encodes every weight as fp16 (identical value) and raises *inexact if any bf16
 // weight is not exactly representable in fp16 (the runtime then re-tiles as bf16).
 __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,
-                                          int32_t to_fp16, int32_t* inexact) {
-  const uint64_t total = static_cast<uint64_t>(kNumKBlocks) * n_pad * 8;
+                                          int32_t k_features, int32_t to_fp16, int32_t* inexact) {
+  const uint64_t total = static_cast<uint64_t>(k_features / kKBlock) * n_pad * 8;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t c = static_cast<uint32_t>(i & 7);
@@ -649,7 +650,7 @@ __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, i
     const uint32_t kb = static_cast<uint32_t>(rowi / n_pad);
     uint4 v = make_uint4(0, 0, 0, 0);
     if (static_cast<int32_t>(n) < n_classes) {
-      v = *reinterpret_cast<const uint4*>(w + static_cast<uint64_t>(n) * kFeatures + kb * kKBlock + c * 8);
+      v = *reinterpret_cast<const uint4*>(w + static_cast<uint64_t>(n) * k_features + kb * kKBlock + c * 8);
       if (to_fp16) {
         uint32_t* u = reinterpret_cast<uint32_t*>(&v);
         int bad = 0;

@@ -47,6 +47,8 @@ struct PredHost {
   float* bias = nullptr;
   int n_pad = 0;
   int a_fp16 = 0;
+  uint8_t* w2_tiled = nullptr;  // MLP layer 2
+  float* bias1 = nullptr;       // MLP layer 1 bias
 };
 
 struct Slot {
@@ -108,6 +110,7 @@ struct hydro_ctx {
   int32_t fixed_order[kMaxPred];
   bool fixed_order_set = false;
   bool has_area = false;
+  bool has_linear = false, has_mlp = false;
   // timing
   bool timing = false;
   std::vector<TimedLaunch> timed;
@@ -163,6 +166,12 @@ static hydro_status timed_launch(hydro_ctx* ctx, int kind, F&& launch) {
 static int next_pow2_pad(int c) {  // n_pad: multiple of 16 >= c
   return ((c + 15) / 16) * 16;
 }
+
+// Copies W [rows][k_features] (bf16; host or device) and re-lays it out as the swizzled K-block
+// image the classifier kernels bulk-copy (n_pad rows per K-block).  try_fp16: re-encode as fp16
+// when every weight is exactly representable (*fp16 = 1), else keep bf16 (*fp16 = 0).
+static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_device, int rows, int n_pad,
+                                 int k_features, bool try_fp16, uint8_t** out, int* fp16);
 
 // ------------------------------------------------------------------------------------------
 
@@ -271,6 +280,30 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
     if (d->threshold[0] > (1ull << 32) || d->threshold[1] > (1ull << 32))
       return set_err(HYDRO_EINVAL, "threshold must be <= 2^32");
     if (d->units < 0 || d->units_per_area < 0) return set_err(HYDRO_EINVAL, "units must be >= 0");
+  } else if (d->kind == HYDRO_PRED_MLP) {
+    if (!ctx->cfg.frames) return set_err(HYDRO_EINVAL, "MLP predicate needs the frame pool in hydro_config");
+    if (d->n_classes < 2 || d->n_classes > HYDRO_MAX_CLASSES) return set_err(HYDRO_EINVAL, "n_classes in [2, 128]");
+    if (d->target < 0 || d->target >= d->n_classes) return set_err(HYDRO_EINVAL, "target outside [0, n_classes)");
+    if (d->hidden != 256 && d->hidden != 512) return set_err(HYDRO_EINVAL, "MLP hidden must be 256 or 512");
+    if (!d->weight_bf16 || !d->bias || !d->weight2_bf16 || !d->bias2)
+      return set_err(HYDRO_EINVAL, "MLP needs weight_bf16, bias, weight2_bf16 and bias2");
+    if (d->crop_mode != HYDRO_CROP_NEAREST) return set_err(HYDRO_EINVAL, "MLP supports HYDRO_CROP_NEAREST only");
+    const int C = d->n_classes, H = d->hidden;
+    ph.n_pad = next_pow2_pad(C);
+    const cudaMemcpyKind kind = d->weights_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    hydro_status st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, H, H, kFeatures, true, &ph.w_tiled,
+                                   &ph.a_fp16);
+    if (st != HYDRO_OK) return st;
+    int w2_fp16 = 0;
+    st = tile_weights(ctx, d->weight2_bf16, d->weights_on_device != 0, C, ph.n_pad, H, false, &ph.w2_tiled, &w2_fp16);
+    if (st != HYDRO_OK) return st;
+    CU(cudaMalloc(&ph.bias, sizeof(float) * HYDRO_MAX_CLASSES));
+    CU(cudaMemsetAsync(ph.bias, 0, sizeof(float) * HYDRO_MAX_CLASSES, ctx->stream));
+    CU(cudaMemcpyAsync(ph.bias, d->bias2, sizeof(float) * C, kind, ctx->stream));
+    CU(cudaMalloc(&ph.bias1, sizeof(float) * H));
+    CU(cudaMemcpyAsync(ph.bias1, d->bias, sizeof(float) * H, kind, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    ctx->has_mlp = true;
   } else if (d->kind == HYDRO_PRED_LINEAR) {
     if (!ctx->cfg.frames) return set_err(HYDRO_EINVAL, "LINEAR predicate needs the frame pool in hydro_config");
     if (d->n_classes < 2 || d->n_classes > HYDRO_MAX_CLASSES) return set_err(HYDRO_EINVAL, "n_classes in [2, 128]");
@@ -280,34 +313,17 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
       return set_err(HYDRO_EINVAL, "crop_mode must be HYDRO_CROP_NEAREST or HYDRO_CROP_AREA");
     const int C = d->n_classes;
     ph.n_pad = next_pow2_pad(C);
-    const size_t wbytes = static_cast<size_t>(C) * kFeatures * 2;
-    uint16_t* wdev = nullptr;
-    CU(cudaMalloc(&wdev, wbytes));
-    CU(cudaMemcpyAsync(wdev, d->weight_bf16, wbytes, d->weights_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                       ctx->stream));
-    CU(cudaMalloc(&ph.w_tiled, static_cast<size_t>(kNumKBlocks) * ph.n_pad * 128));
+    // stage operands as fp16 when every weight is exactly representable (u8 pixels always are):
+    // same products, cheaper u8 -> fp16 operand construction in K4 (DESIGN.md §4)
+    hydro_status st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, C, ph.n_pad, kFeatures, true,
+                                   &ph.w_tiled, &ph.a_fp16);
+    if (st != HYDRO_OK) return st;
     CU(cudaMalloc(&ph.bias, sizeof(float) * HYDRO_MAX_CLASSES));
     CU(cudaMemsetAsync(ph.bias, 0, sizeof(float) * HYDRO_MAX_CLASSES, ctx->stream));
     CU(cudaMemcpyAsync(ph.bias, d->bias, sizeof(float) * C,
                        d->weights_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
-    // stage operands as fp16 when every weight is exactly representable (u8 pixels always are):
-    // same products, cheaper u8 -> fp16 operand construction in K4 (DESIGN.md §4)
-    CU(cudaMemsetAsync(ctx->zero_word + 1, 0, sizeof(int32_t), ctx->stream));
-    int32_t* inexact = reinterpret_cast<int32_t*>(ctx->zero_word + 1);
-    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, ph.w_tiled, C, ph.n_pad, 1, inexact);
-    ctx->launches += 1;
-    CU(cudaGetLastError());
-    int32_t bad = 0;
-    CU(cudaMemcpyAsync(&bad, inexact, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
-    ph.a_fp16 = bad ? 0 : 1;
-    if (bad) {
-      hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, ph.w_tiled, C, ph.n_pad, 0, inexact);
-      ctx->launches += 1;
-      CU(cudaGetLastError());
-      CU(cudaStreamSynchronize(ctx->stream));
-    }
-    CU(cudaFree(wdev));
+    ctx->has_linear = true;
   } else {
     return set_err(HYDRO_EINVAL, "unknown predicate kind");
   }
@@ -316,6 +332,38 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
   if (pred_id) *pred_id = static_cast<int32_t>(ctx->preds.size() - 1);
   return HYDRO_OK;
 }
+
+}  // extern "C"
+
+static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_device, int rows, int n_pad,
+                                 int k_features, bool try_fp16, uint8_t** out, int* fp16) {
+  const size_t wbytes = static_cast<size_t>(rows) * k_features * 2;
+  uint16_t* wdev = nullptr;
+  CU(cudaMalloc(&wdev, wbytes));
+  CU(cudaMemcpyAsync(wdev, w, wbytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMalloc(out, static_cast<size_t>(k_features / kKBlock) * n_pad * 128));
+  CU(cudaMemsetAsync(ctx->zero_word + 1, 0, sizeof(int32_t), ctx->stream));
+  int32_t* inexact = reinterpret_cast<int32_t*>(ctx->zero_word + 1);
+  int32_t bad = 1;
+  if (try_fp16) {
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 1, inexact);
+    ctx->launches += 1;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(&bad, inexact, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  *fp16 = bad ? 0 : 1;
+  if (bad) {
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 0, inexact);
+    ctx->launches += 1;
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  CU(cudaFree(wdev));
+  return HYDRO_OK;
+}
+
+extern "C" {
 
 hydro_status hydro_set_fixed_order(hydro_ctx* ctx, const int32_t* order, int32_t n) {
   if (!ctx || !order) return set_err(HYDRO_EINVAL, "NULL argument");
@@ -360,7 +408,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
     h.kind[k] = d.kind;
     h.declared_cost[k] = d.declared_cost;
     h.declared_sel[k] = d.declared_selectivity;
-    h.cost_norm[k] = d.kind == HYDRO_PRED_LINEAR ? 1.0 : k1_norm;
+    h.cost_norm[k] = is_classifier(d.kind) ? 1.0 : k1_norm;
     PredDev& q = pd[k];
     q.kind = d.kind;
     q.label_value = d.label_value;
@@ -377,6 +425,9 @@ static hydro_status freeze(hydro_ctx* ctx) {
     q.target = d.target;
     q.crop_mode = d.crop_mode;
     q.a_fp16 = ctx->preds[k].a_fp16;
+    q.hidden = d.hidden;
+    q.w2_tiled = ctx->preds[k].w2_tiled;
+    q.bias1 = ctx->preds[k].bias1;
   }
   // initial order: declared statistics (SCORE/COST/SEL before warmup; STATIC), or add order
   for (int k = 0; k < P; ++k) {
@@ -516,13 +567,14 @@ static hydro_status launch_compact(hydro_ctx* ctx, const CompactParams& c, uint6
   return timed_launch(ctx, 3, [&] { hydro_compact_kernel<<<grid, kRouteThreads, 0, ctx->stream>>>(c); });
 }
 
-static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_positions) {
+static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_positions, bool mlp = false) {
   const uint64_t tiles = (max_positions + kTileM - 1) / kTileM;
   const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctx->num_sms)));
   return timed_launch(ctx, 1, [&] {
-    // kernel instantiation by context capability: AREA support only when an AREA head exists
     const bool dbg = c.dbg_crops || c.dbg_logits || c.dbg_verdict;
-    hydro_classifier_launch(c, grid, ctx->stream, dbg, ctx->has_area);
+    if (mlp) hydro_mlp_launch(c, grid, ctx->stream, dbg);
+    // kernel instantiation by context capability: AREA support only when an AREA head exists
+    else hydro_classifier_launch(c, grid, ctx->stream, dbg, ctx->has_area);
   });
 }
 
@@ -603,7 +655,7 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
     warm = std::min<uint64_t>(n, static_cast<uint64_t>(ctx->cfg.warmup_tuples));
     for (int k = 0; k < P; ++k) {
       uint32_t* wb = ctx->warm_bits + static_cast<uint64_t>(k) * ctx->bits_stride;
-      if (ctx->preds[k].desc.kind == HYDRO_PRED_LINEAR) {
+      if (is_classifier(ctx->preds[k].desc.kind)) {
         ClsParams c = cls_base(ctx, fr, bb);
         c.dispatch = 0;
         c.explicit_pred = k;
@@ -611,7 +663,7 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
         c.range_base = 0;
         c.range_n = static_cast<uint32_t>(warm);
         c.bits_out = wb;
-        if ((s = launch_cls(ctx, c, warm)) != HYDRO_OK) return s;
+        if ((s = launch_cls(ctx, c, warm, ctx->preds[k].desc.kind == HYDRO_PRED_MLP)) != HYDRO_OK) return s;
       } else {
         RouteParams r = route_base(ctx, id, fr, bb, lab);
         r.dispatch = 0;
@@ -650,7 +702,7 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
   const uint32_t rest_n = static_cast<uint32_t>(n - warm);
   // chain slots: any order has at most L classifier hops and min(C, L + 1) cheap runs
   int n_lin = 0;
-  for (int k = 0; k < P; ++k) n_lin += ctx->preds[k].desc.kind == HYDRO_PRED_LINEAR ? 1 : 0;
+  for (int k = 0; k < P; ++k) n_lin += is_classifier(ctx->preds[k].desc.kind) ? 1 : 0;
   const int n_cheap = P - n_lin;
   const int slots = (P == 0 || n_lin == 0) ? 1 : std::min(P, n_lin + std::min(n_cheap, n_lin + 1));
   for (int h = 0; h < slots; ++h) {
@@ -660,13 +712,14 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
     r.range_base = rest_base;
     r.range_n = rest_n;
     if ((s = launch_route(ctx, r, rest_n)) != HYDRO_OK) return s;
-    if (n_lin > 0) {
+    if (n_lin > 0) {  // the classifier kernel(s) the context needs; each exits unless its kind is the hop's
       ClsParams c = cls_base(ctx, fr, bb);
       c.dispatch = 1;
       c.hop = h;
       c.range_base = rest_base;
       c.range_n = rest_n;
-      if ((s = launch_cls(ctx, c, rest_n)) != HYDRO_OK) return s;
+      if (ctx->has_linear && (s = launch_cls(ctx, c, rest_n, false)) != HYDRO_OK) return s;
+      if (ctx->has_mlp && (s = launch_cls(ctx, c, rest_n, true)) != HYDRO_OK) return s;
     }
     CompactParams k2 = compact_base(ctx, id, bb, sl);
     k2.dispatch = 1;
@@ -850,8 +903,8 @@ hydro_status hydro_kernel_time(hydro_ctx* ctx, int32_t kind, double* total_ms, i
 hydro_status hydro_debug_linear(hydro_ctx* ctx, int32_t k, const hydro_tuples* t, float* logits_out,
                                 uint16_t* crops_out, uint8_t* verdict_out) {
   if (!ctx || !t) return set_err(HYDRO_EINVAL, "NULL argument");
-  if (k < 0 || k >= static_cast<int32_t>(ctx->preds.size()) || ctx->preds[k].desc.kind != HYDRO_PRED_LINEAR)
-    return set_err(HYDRO_EINVAL, "pred_id is not a LINEAR predicate");
+  if (k < 0 || k >= static_cast<int32_t>(ctx->preds.size()) || !is_classifier(ctx->preds[k].desc.kind))
+    return set_err(HYDRO_EINVAL, "pred_id is not a LINEAR or MLP predicate");
   if (!t->on_device) return set_err(HYDRO_EINVAL, "debug_linear needs device tuples");
   if (t->n < 0 || t->n > ctx->cfg.max_batch_tuples) return set_err(HYDRO_EINVAL, "bad n");
   hydro_status s = freeze(ctx);
@@ -866,7 +919,8 @@ hydro_status hydro_debug_linear(hydro_ctx* ctx, int32_t k, const hydro_tuples* t
   c.dbg_crops = crops_out;
   c.dbg_verdict = verdict_out;
   c.collect_stats = 0;
-  if ((s = launch_cls(ctx, c, static_cast<uint64_t>(t->n))) != HYDRO_OK) return s;
+  if ((s = launch_cls(ctx, c, static_cast<uint64_t>(t->n), ctx->preds[k].desc.kind == HYDRO_PRED_MLP)) != HYDRO_OK)
+    return s;
   CU(cudaStreamSynchronize(ctx->stream));
   return check_sticky(ctx);
 }
@@ -889,6 +943,8 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
   for (PredHost& p : ctx->preds) {
     cudaFree(p.w_tiled);
     cudaFree(p.bias);
+    cudaFree(p.w2_tiled);
+    cudaFree(p.bias1);
   }
   for (TimedLaunch& t : ctx->timed) {
     cudaEventDestroy(t.a);

@@ -21,7 +21,7 @@ HYDRO_OK, HYDRO_EINVAL, HYDRO_ENOMEM, HYDRO_ECUDA, HYDRO_ENCCL, HYDRO_ESTATE, HY
     0, -1, -2, -3, -4, -5, -6, -7)
 POLICY = {"score": 0, "static": 1, "fixed": 2, "cost": 3, "selectivity": 4}
 COST_SOURCE = {"measured": 0, "declared": 1}
-PRED_KIND = {"label_eq": 0, "hash": 1, "linear": 2}
+PRED_KIND = {"label_eq": 0, "hash": 1, "linear": 2, "mlp": 3}
 CROP_MODE = {"nearest": 0, "area": 1}
 MAX_PRED = 8
 FEATURES = 12288
@@ -46,7 +46,8 @@ class hydro_predicate_desc(C.Structure):
                 ("threshold", C.c_uint64 * 2), ("drift_id", C.c_uint64), ("units", C.c_int32),
                 ("units_per_area", C.c_int32), ("weight_bf16", C.c_void_p), ("bias", C.c_void_p),
                 ("weights_on_device", C.c_int32), ("n_classes", C.c_int32), ("target", C.c_int32),
-                ("crop_mode", C.c_int32), ("declared_cost", C.c_double), ("declared_selectivity", C.c_double)]
+                ("crop_mode", C.c_int32), ("hidden", C.c_int32), ("weight2_bf16", C.c_void_p), ("bias2", C.c_void_p),
+                ("declared_cost", C.c_double), ("declared_selectivity", C.c_double)]
 
 
 class hydro_tuples(C.Structure):
@@ -286,11 +287,11 @@ class Eddy:
             d.drift_id = int(p["drift_id"])
             d.units = int(p.get("units", 1))
             d.units_per_area = int(p.get("units_per_area", 0))
-        elif p["kind"] == "linear":
+        elif p["kind"] in ("linear", "mlp"):
             w = p["weight"].contiguous()
             b = p["bias"].to(torch.float32).contiguous()
             if w.dtype != torch.bfloat16 or w.shape[1] != FEATURES:
-                raise ValueError("weight must be bf16 [C, 12288]")
+                raise ValueError("weight must be bf16 [rows, 12288]")
             w = w.view(torch.int16)
             d.weights_on_device = 1 if w.is_cuda else 0
             if b.is_cuda != w.is_cuda:
@@ -301,6 +302,17 @@ class Eddy:
             d.n_classes = int(p["n_classes"])
             d.target = int(p["target"])
             d.crop_mode = CROP_MODE[p.get("crop_mode", "nearest")]
+            if p["kind"] == "mlp":
+                w2 = p["weight2"].contiguous()
+                b2 = p["bias2"].to(torch.float32).contiguous()
+                if w2.dtype != torch.bfloat16 or w2.shape[1] != w.shape[0]:
+                    raise ValueError("weight2 must be bf16 [C, hidden]")
+                w2 = w2.view(torch.int16).to(w.device)
+                b2 = b2.to(w.device)
+                self._keep += [w2, b2]
+                d.hidden = int(w.shape[0])
+                d.weight2_bf16 = w2.data_ptr()
+                d.bias2 = b2.data_ptr()
         pid = hydro_add_predicate(self.ctx, d)
         self.n_pred += 1
         return pid

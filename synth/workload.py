@@ -38,6 +38,7 @@ _MULT = 0x45D9F3B  # < 2**27, so (x < 2**32) * _MULT < 2**59 fits int64
 
 # stream ids
 S_LABEL, S_LABEL2, S_WOCT, S_WOFF, S_HOCT, S_HOFF, S_X, S_Y, S_FRAME, S_WEIGHT = range(1, 11)
+S_W1, S_W2 = 11, 12
 
 CROP = 64
 K_FEATURES = CROP * CROP * 3  # 12288
@@ -204,6 +205,35 @@ def make_linear_head(seed: int, n_classes: int, target: int, selectivity: float,
             {"kappa": kappa, "sigma": sigma * WEIGHT_SCALE, "scale": WEIGHT_SCALE})
 
 
+def make_mlp_head(seed: int, hidden: int, n_classes: int, target: int, selectivity: float,
+                  k_features: int = K_FEATURES):
+    """Two-layer head (R25): W1 = s*{-2..2} [hidden][K], b1 = -s*floor(127.5*rowsum)
+    (centres every hidden pre-activation), W2 = s*{-2..2} [C][hidden], b2 centring the logits on
+    the half-normal mean of the hidden units plus the target offset kappa*sigma_z (s = 2^-8).
+
+    With integer (nearest-crop) inputs every hidden pre-activation is s * integer, exact in fp32,
+    so its bf16 rounding is the same for any accumulation order.  Only the logits' f32 sums differ
+    from float64 (tolerance 1e-2).  These are draws, not method arithmetic.
+    """
+    h = torch.arange(hidden, dtype=torch.int64)[:, None]
+    k = torch.arange(k_features, dtype=torch.int64)[None, :]
+    w1 = gen_u32(seed, S_W1, h * k_features + k) % 5 - 2
+    b1 = torch.floor(-127.5 * w1.sum(dim=1).to(torch.float64))
+    sigma1 = math.sqrt(_PIX_VAR * float((w1 * w1).sum(dim=1).to(torch.float64).mean())) * WEIGHT_SCALE
+    c = torch.arange(n_classes, dtype=torch.int64)[:, None]
+    hh = torch.arange(hidden, dtype=torch.int64)[None, :]
+    w2 = gen_u32(seed, S_W2, c * hidden + hh) % 5 - 2
+    w2f = w2.to(torch.float64) * WEIGHT_SCALE
+    mean_h = sigma1 / math.sqrt(2.0 * math.pi)            # E[relu(N(0, sigma1))]
+    var_h = sigma1 ** 2 * (0.5 - 1.0 / (2.0 * math.pi))   # Var[relu(N(0, sigma1))]
+    sigma_z = math.sqrt(var_h * float((w2f * w2f).sum(dim=1).mean()))
+    b2 = -mean_h * w2f.sum(dim=1)
+    b2[target] += target_offset_sigmas(n_classes, selectivity) * sigma_z
+    return ((w1.to(torch.float64) * WEIGHT_SCALE).to(torch.bfloat16), (b1 * WEIGHT_SCALE).to(torch.float32),
+            w2f.to(torch.bfloat16), b2.to(torch.float32),
+            {"sigma1": sigma1, "sigma_z": sigma_z, "scale": WEIGHT_SCALE})
+
+
 # ----------------------------------------------------------------------------------------------
 # predicate / workload descriptions (plain data)
 
@@ -233,6 +263,13 @@ def linear_pred(seed, n_classes, target, selectivity, crop_mode="nearest", decla
                 calib=meta)
 
 
+def mlp_pred(seed, n_classes, target, selectivity, hidden=512, declared_cost=1000.0, name=None):
+    w1, b1, w2, b2, meta = make_mlp_head(seed, hidden, n_classes, target, selectivity)
+    return dict(kind="mlp", weight=w1, bias=b1, weight2=w2, bias2=b2, hidden=hidden, target=target,
+                n_classes=n_classes, crop_mode="nearest", declared_cost=declared_cost,
+                declared_selectivity=float(selectivity), name=name or f"mlp{hidden}x{n_classes}", calib=meta)
+
+
 @dataclass
 class Workload:
     name: str
@@ -260,7 +297,7 @@ class Workload:
 
     @property
     def needs_frames(self) -> bool:
-        return any(p["kind"] == "linear" for p in self.preds)
+        return any(p["kind"] in ("linear", "mlp") for p in self.preds)
 
 
 SEED = 20240321
@@ -297,6 +334,12 @@ def workload(name: str, *, n: Optional[int] = None, small: bool = False) -> Work
         return Workload("cfg4", SEED, n or 10_000_000, nf, fh, fw, preds, w_min=wmin,
                         batch_tuples=1 << 20,
                         notes="area-correlated classifier cost, 4 predicates")
+    if name == "mlp":  # the dog query with the breed classifier as an MLP head
+        preds = [label_pred(),
+                 mlp_pred(SEED + 3, 120, 57, 0.254, name="breed=great dane (mlp)"),
+                 linear_pred(SEED + 2, 10, 1, 0.633, name="colour=black")]
+        return Workload("mlp", SEED, n or 1_000_000, nf, fh, fw, preds, w_min=wmin,
+                        notes="cfg2 with a 12288-512-120 MLP breed head")
     if name == "cfg5":
         w = workload("cfg2", n=n or 100_000_000, small=small)
         w.name = "cfg5"

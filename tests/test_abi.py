@@ -62,6 +62,7 @@ int main(void) {
          sizeof(hydro_batch_report));
   O(hydro_config, frames); O(hydro_config, frame_w); O(hydro_config, nccl_unique_id);
   O(hydro_predicate_desc, threshold); O(hydro_predicate_desc, weight_bf16); O(hydro_predicate_desc, declared_selectivity);
+  O(hydro_predicate_desc, hidden); O(hydro_predicate_desc, weight2_bf16); O(hydro_predicate_desc, bias2);
   O(hydro_tuples, on_device); O(hydro_pred_stats, cost_raw_total); O(hydro_batch_report, cost_raw);
   O(hydro_batch_report, n_pred);
   return 0;

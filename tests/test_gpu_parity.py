@@ -341,3 +341,62 @@ def test_nccl_statistics_path_single_rank_matches():
         e.close()
     (i0, b0, o0, s0), (i1, b1, o1, s1) = runs
     assert np.array_equal(i0, i1) and np.array_equal(b0, b1) and o0 == o1 and s0 == s1
+
+
+# ------------------------------------------------------------------------------- MLP head (f1)
+
+def test_mlp_crops_logits_verdicts():
+    """MLP breed head (12288-512-120, R25) in the CTA-pair kernel: crops bit-exact, logits within
+    1e-2 of the f64 oracle (hidden layer rounded to bf16 on both sides), verdicts equal away from
+    the decision boundary.  700 tuples = 3 CTA-pair units with a ragged, odd tile count."""
+    w = workload("mlp", small=True, n=4000)
+    frames = w.frames()
+    n = 700
+    t = w.tuples(n=n)
+    k = 1
+    p = w.preds[k]
+    e = make_eddy(w, frames.cuda(), policy="fixed", warmup=0, max_batch=4096)
+    C = p["n_classes"]
+    logits = torch.full((n, C), float("nan"), device="cuda")
+    crops = torch.zeros((n, O.K_FEATURES), dtype=torch.int16, device="cuda")
+    verdict = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    e.debug_linear(k, t.to("cuda"), logits, crops, verdict)
+    tup = O.as_numpy_tuples(t)
+    fr = frames.numpy()
+    ref_crop = O.crop_nearest(fr, tup["frame_id"], tup["bbox"]).reshape(n, -1)
+    assert np.array_equal(crops.view(torch.bfloat16).float().cpu().numpy(), ref_crop.astype(np.float32))
+    v_ref, z_ref = O.linear_verdict(p, fr, tup["frame_id"], tup["bbox"], return_logits=True)
+    err = np.abs(logits.double().cpu().numpy() - z_ref).max()
+    assert err <= LOGIT_TOL, err
+    m = np.abs(O.margin(z_ref, p["target"]))
+    v = verdict.cpu().numpy().astype(bool)
+    assert np.all((v == v_ref) | (m < 2 * LOGIT_TOL))
+    e.close()
+
+
+@pytest.mark.parametrize("hidden", [256, 512])
+def test_mlp_query_end_to_end(hidden):
+    """The dog query with the MLP breed head through the eddy (score policy, warmup, several
+    batches): rows and per-batch counters equal the oracle's; near-threshold tuples (MLP margin
+    within 4x the logit tolerance) are removed from the input (excluded by construction)."""
+    from synth import mlp_pred
+
+    w = workload("mlp", small=True, n=6000)
+    if hidden != 512:
+        w.preds[1] = mlp_pred(20240324, 120, 57, 0.254, hidden=hidden, name="breed (mlp256)")
+    frames = w.frames()
+    t = w.tuples()
+    tup = O.as_numpy_tuples(t)
+    fr = frames.numpy()
+    _, z = O.linear_verdict(w.preds[1], fr, tup["frame_id"], tup["bbox"], return_logits=True)
+    keep_in = np.abs(O.margin(z, w.preds[1]["target"])) >= 4 * LOGIT_TOL
+    t = t.select(torch.from_numpy(np.where(keep_in)[0]))
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, fr)
+    e = make_eddy(w, frames.cuda(), policy="score", warmup=1024, max_batch=2048)
+    ids, bbs, infos = run_stream(e, t.to("cuda"), 2048)
+    _assert_rows(ids, bbs, ref_ids, ref_bbox)
+    for b, info in enumerate(infos):
+        Vb = V[:, b * 2048:(b + 1) * 2048]
+        n_in, n_pass = expected_batch_counters(Vb, info["order_used"], 1024 if b == 0 else 0)
+        assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist()
+    e.close()

@@ -179,6 +179,78 @@ def test_generator_makes_half_integer_target_margins():
         assert np.all(np.mod(z[:, p["target"]] / p["calib"]["scale"], 1.0) == 0.5)
 
 
+# ----------------------------------------------------------------------------- MLP head (R25)
+
+
+def _mlp_pred(W1, b1, W2, b2, target=0):
+    return dict(kind="mlp", weight=torch.as_tensor(W1).to(torch.bfloat16), bias=torch.as_tensor(b1, dtype=torch.float32),
+                weight2=torch.as_tensor(W2).to(torch.bfloat16), bias2=torch.as_tensor(b2, dtype=torch.float32),
+                hidden=len(b1), n_classes=len(b2), target=target, crop_mode="nearest")
+
+
+def test_mlp_one_hot_first_layer_selects_pixels():
+    """W1 rows = e_{k_h}, b1 = 0 -> h = crop pixel x[k_h] (integers <= 255 are exact in bf16), so
+    z = W2 x_sel + b2 with x from torch nearest-exact (a closed form through the whole head)."""
+    F = make_frames(7, 2, 96, 128).numpy()
+    t = make_tuples(7, 0, 30, n_frames=2, frame_h=96, frame_w=128, w_min=8, n_octaves=4)
+    tup = O.as_numpy_tuples(t)
+    picks = [(0, 0, 0), (5, 9, 1), (63, 63, 2), (40, 2, 0)]
+    W1 = np.zeros((len(picks), O.K_FEATURES), np.float32)
+    for h, (dy, dx, ch) in enumerate(picks):
+        W1[h, (dy * 64 + dx) * 3 + ch] = 1.0
+    W2 = np.array([[1.0, -2.0, 0.5, 0.0], [0.25, 0.0, 1.0, -1.0], [0.0, 0.0, 0.0, 0.0]], np.float32)
+    b2 = np.array([0.5, -1.0, 3.0], np.float32)
+    pred = _mlp_pred(W1, np.zeros(len(picks), np.float32), W2, b2)
+    z = O.mlp_logits(pred, O.crop_features(pred, F, tup["frame_id"], tup["bbox"]))
+    for i in range(len(tup["id"])):
+        ref = torch.nn.functional.interpolate(_torch_crop(F[tup["frame_id"][i]], tup["bbox"][i]),
+                                              size=(64, 64), mode="nearest-exact")[0]
+        xs = np.array([float(ref[ch, dy, dx]) for (dy, dx, ch) in picks])
+        assert np.allclose(z[i], W2.astype(np.float64) @ xs + b2, rtol=0, atol=1e-12)
+
+
+def test_mlp_hidden_is_relu_then_bf16_round_to_nearest_even():
+    """Single hidden unit a = x0 * w + b1 with hand-picked values: ReLU clips negatives, 257 ties to
+    even (256), 258 is exact, 259 rounds up to 260 (bf16 has 8 significant bits)."""
+    W1 = np.zeros((1, O.K_FEATURES), np.float32)
+    W1[0, 0] = 1.0
+    W2 = np.ones((1, 1), np.float32)
+    for x0, b1, expect in [(10, -20.0, 0.0), (200, 57.0, 256.0), (200, 58.0, 258.0), (200, 59.0, 260.0),
+                           (3, 0.25, 3.25)]:
+        x = np.zeros((1, O.K_FEATURES))
+        x[0, 0] = x0
+        z = O.mlp_logits(_mlp_pred(W1, np.array([b1], np.float32), W2, np.zeros(1, np.float32)), x)
+        assert z[0, 0] == expect, (x0, b1, z[0, 0], expect)
+
+
+def test_mlp_matches_torch_bf16_pipeline_on_generated_head():
+    """The generated head on real crops against torch's own ops (f64 matmul, relu, .to(bfloat16))."""
+    w = workload("mlp", small=True)
+    p = w.preds[1]
+    F = w.frames().numpy()
+    tup = O.as_numpy_tuples(w.tuples(n=64))
+    x = O.crop_features(p, F, tup["frame_id"], tup["bbox"])
+    xt = torch.from_numpy(x)
+    a = xt @ p["weight"].double().T + p["bias"].double()
+    h = torch.relu(a).to(torch.float32).to(torch.bfloat16).double()
+    ref = h @ p["weight2"].double().T + p["bias2"].double()
+    assert torch.allclose(torch.from_numpy(O.mlp_logits(p, x)), ref, rtol=0, atol=1e-9)
+    # every hidden pre-activation of the generated head is s * integer (exact in fp32, R25)
+    assert torch.all(torch.frac(a / p["calib"]["scale"]) == 0)
+
+
+def test_mlp_all_negative_hidden_gives_bias_and_generated_selectivity():
+    W1 = np.ones((2, O.K_FEATURES), np.float32)
+    pred = _mlp_pred(W1, np.array([-1e9, -1e9], np.float32), np.ones((3, 2), np.float32),
+                     np.array([1.0, 2.0, 3.0], np.float32), target=2)
+    z = O.mlp_logits(pred, np.full((4, O.K_FEATURES), 255.0))
+    assert np.array_equal(z, np.tile([1.0, 2.0, 3.0], (4, 1)))
+    w = workload("mlp", small=True)
+    tup = O.as_numpy_tuples(w.tuples(n=3000))
+    v = O.linear_verdict(w.preds[1], w.frames().numpy(), tup["frame_id"], tup["bbox"])
+    assert abs(v.mean() - 0.254) < 0.04
+
+
 # ----------------------------------------------------------------------------- AND / order
 
 def test_and_is_order_independent_brute_force():
