@@ -35,9 +35,12 @@ METRIC = "tuples/sec through 3-predicate UDF conjunction at 1/2/4/8 B200; % HBM/
 UNIT = "tuples/s"
 TUPLES_PER_STEP = 1_000_000
 ROTATING_BATCHES = 6          # 6 x 22 MB of tuple columns + 2.83 GB frames: inputs larger than L2
-K4_BYTES_PER_TUPLE = 12288 + 16
+K4_FEATURES = 12288
+K4_BYTES_PER_TUPLE = K4_FEATURES + 16
 WORKLOAD = ("cfg2: 1M dog-query detections per GPU per step; label='dog' AND breed(C=120) AND "
             "colour(C=10) linear heads on 64x64 nearest crops; 1024 x 720x1280x3 u8 frame pool")
+WORKLOAD_MLP = ("mlp (SURVEY.md §8(f) f1): cfg2 with the breed classifier as a 12288-512-120 MLP head "
+                "(bf16 hidden), colour linear C=10; 1M detections per GPU per step; 1024 x 720x1280x3 frames")
 
 
 def _peaks():
@@ -188,7 +191,8 @@ def run_gpu(args):
         B.build()
     if dist:
         dist.barrier()
-    w = workload("cfg2")
+    mlp = args.workload == "mlp"
+    w = workload("mlp" if mlp else "cfg2")
     frames = w.frames(device="cuda")
     uid = broadcast_unique_id(dist, rank, H.hydro_nccl_unique_id) if world > 1 else None
     stream = torch.cuda.current_stream()
@@ -217,9 +221,13 @@ def run_gpu(args):
             collect_dev(bid)
 
     lin = [k for k, p in enumerate(w.preds) if p["kind"] == "linear"]
+    mlps = [k for k, p in enumerate(w.preds) if p["kind"] == "mlp"]
 
     def lin_in():
         return sum(e.stats(k)["tuples_in"] for k in lin)
+
+    def mlp_in():
+        return sum(e.stats(k)["tuples_in"] for k in mlps)
 
     run_steps(max(args.warmup, 3), 0)
     torch.cuda.synchronize()
@@ -243,10 +251,12 @@ def run_gpu(args):
     value = world * TUPLES_PER_STEP * args.steps / (ms / 1000.0)
 
     # ---- kernel timing pass (separate, untimed for `value`): K4 share + achieved bandwidth
-    in0 = lin_in()
+    in0, min0 = lin_in(), mlp_in()
     e.set_kernel_timing(True)
     run_steps(args.steps, 2)
     k4_ms, k4_n = e.kernel_time(1)
+    km_ms, km_n = e.kernel_time(4)
+    km_tuples = mlp_in() - min0
     k1_ms, k1_n = e.kernel_time(0)
     k5_ms, k5_n = e.kernel_time(2)
     k2c_ms, k2c_n = e.kernel_time(3)
@@ -306,24 +316,44 @@ def run_gpu(args):
                "sample": f"first {done} tuples of the step's 1M-tuple batch ({secs:.1f} s of CPU work), every "
                          f"predicate on every tuple, f64 numpy/OpenBLAS"}
     e.close()
+    if mlp:
+        # MLP hop: tensor-bound; algorithmic flops per input tuple 2*12288*H + 2*H*C
+        pm = w.preds[mlps[0]]
+        flops_t = 2 * K4_FEATURES * pm["hidden"] + 2 * pm["hidden"] * pm["n_classes"]
+        peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        ach_tf = km_tuples * flops_t / (km_ms / 1000.0) / 1e12 if km_ms > 0 else 0.0
+        mtp = os.path.join(ROOT, "profiles", "mlp_dram_traffic.json")
+        mtraffic = json.load(open(mtp)).get("bytes_per_launch") if os.path.exists(mtp) else None
+        roofline = {"kernel": "hydro_mlp_kernel (K4-MLP: crop gather + two chained tcgen05 GEMMs, CTA pairs)",
+                    "bound": "tensor", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach_tf / peak_tf,
+                    "frac_vs_burst_peak": ach_tf / peaks["bf16_tflops"],
+                    "traffic": mtraffic, "algorithmic_flops_per_launch": km_tuples * flops_t / max(km_n, 1),
+                    "avg_launch_ms": km_ms / max(km_n, 1), "launches": km_n,
+                    "share_of_step": km_ms / max(km_ms + k4_ms + k1_ms + k5_ms + k2c_ms, 1e-9),
+                    "mlp_ms_per_step": km_ms / args.steps, "linear_k4_ms_per_step": k4_ms / args.steps,
+                    "k1_ms_per_step": k1_ms / args.steps, "k2_ms_per_step": k2c_ms / args.steps,
+                    "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside the step; fp16 "
+                                   "operands of layer 1 run at the bf16 rate)"}
+    else:
+        roofline = {"kernel": "hydro_classifier_kernel (K4: crop gather + tcgen05 linear head)",
+                    "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                    "algorithmic_bytes_per_launch": k4_bytes / max(k4_n, 1),
+                    "avg_launch_ms": k4_ms / max(k4_n, 1), "launches": k4_n,
+                    "share_of_step": k4_ms / max(k4_ms + k1_ms + k5_ms + k2c_ms, 1e-9),
+                    "k2_ms_per_step": k2c_ms / args.steps,
+                    "k1_ms_per_step": k1_ms / args.steps, "k4_ms_per_step": k4_ms / args.steps,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"}
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-               "config": {"workload": WORKLOAD, "tuples_per_step": world * TUPLES_PER_STEP,
+               "config": {"workload": WORKLOAD_MLP if mlp else WORKLOAD, "tuples_per_step": world * TUPLES_PER_STEP,
                           "batch_tuples": TUPLES_PER_STEP, "policy": "score (cost/(1-sel)), measured costs",
                           "l2": "inputs larger than L2: 2.83 GB frame pool + 6 rotating 22 MB tuple batches",
                           "parallelism": f"dp{world}", "final_order": [w.preds[k]["name"] for k in order],
                           "selectivity": sel, "cost_sm_cycles_per_tuple": cost},
-               "roofline": {"kernel": "hydro_classifier_kernel (K4: crop gather + tcgen05 linear head)",
-                            "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                            "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                            "algorithmic_bytes_per_launch": k4_bytes / max(k4_n, 1),
-                            "avg_launch_ms": k4_ms / max(k4_n, 1), "launches": k4_n,
-                            "share_of_step": k4_ms / max(k4_ms + k1_ms + k5_ms + k2c_ms, 1e-9),
-                            "k2_ms_per_step": k2c_ms / args.steps,
-                            "k1_ms_per_step": k1_ms / args.steps, "k4_ms_per_step": k4_ms / args.steps,
-                            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"},
+               "roofline": roofline,
                "cpu_baseline": cpu,
                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": int(sum(d2h) / max(len(d2h), 1))},
@@ -415,8 +445,9 @@ def main():
     ap.add_argument("--impl", default="hydro", choices=["hydro", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute"],
-                    help="cfg2 = the BASELINE metric (default); rroute = K1 HBM evidence run")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute", "mlp"],
+                    help="cfg2 = the BASELINE metric (default); rroute = K1 HBM evidence run; "
+                         "mlp = cfg2 with the 12288-512-120 MLP breed head (SURVEY.md §8(f) f1, tensor roofline)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -242,7 +242,8 @@ hydro_status hydro_launch_count(hydro_ctx* ctx, int64_t* launches);
 
 /* Kernel timing (CUDA events on the context stream around every launch of the kind):
    enable = 1 starts recording (and clears), 0 stops.  kind: 0 = route kernel (K1, cheap
-   predicates), 1 = classifier kernel (K4), 2 = fold (K5), 3 = compaction / emit kernel (K2).  hydro_kernel_time synchronises and returns the
+   predicates), 1 = linear classifier kernel (K4), 2 = fold (K5), 3 = compaction / emit kernel
+   (K2), 4 = MLP classifier kernel (K4-MLP).  hydro_kernel_time synchronises and returns the
    summed milliseconds and the number of launches recorded since the last enable. */
 hydro_status hydro_set_kernel_timing(hydro_ctx* ctx, int32_t enable);
 hydro_status hydro_kernel_time(hydro_ctx* ctx, int32_t kind, double* total_ms, int64_t* launches);
@@ -252,7 +253,7 @@ hydro_status hydro_destroy(hydro_ctx* ctx);
 
 /* ---- debug hooks (tests) ---------------------------------------------------------------- */
 
-/* Runs predicate pred_id's LINEAR kernel on every tuple of the DEVICE batch `tuples`
+/* Runs predicate pred_id's classifier kernel (LINEAR or MLP) on every tuple of the DEVICE batch `tuples`
    (no short-circuit, statistics untouched) and writes, when non-NULL, the f32 logits
    logits_out[n][n_classes] (device) and the bf16 crop features crops_out[n][HYDRO_FEATURES]
    (device, bf16 bits) plus the verdicts verdict_out[n] (device, uint8 0/1).  Synchronises. */

@@ -732,8 +732,10 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
 // converters are the linear kernel's, with a one-quad staging lookahead (shared memory).
 template <bool kDbg>
 __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) {
-  constexpr int kP = 2, kQD = 1, kMB = 2;
-  constexpr uint32_t kMlpBStage = 32768;
+  // B stage = this CTA's half of one N=256 slice of a W1 K-block (16 KB) or of a W2 K-block;
+  // 3 stages leave room for the linear kernel's two-quad staging lookahead
+  constexpr int kP = 2, kQD = kQuadDepth, kMB = 3;
+  constexpr uint32_t kMlpBStage = 16384;
   DevState* st = p.st;
   int pred;
   const uint32_t* list_in;
@@ -769,7 +771,6 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
   const int n_classes = pdg.n_classes, n_pad = pdg.n_pad, target = pdg.target, hidden = pdg.hidden;
   const bool fp16 = pdg.a_fp16 != 0;
   const int n_mma1 = hidden / 256;                                     // N=256 slices of layer 1
-  const uint32_t w1_stage = static_cast<uint32_t>(n_mma1) * 16384u;     // this CTA's half of each slice
   const uint32_t w1_kb = static_cast<uint32_t>(hidden) * 128u;          // one tiled W1 K-block
   const uint32_t w2_load = static_cast<uint32_t>(n_pad / 2) * 128u;     // this CTA's half of a W2 K-block
   const uint32_t w2_kb = static_cast<uint32_t>(n_pad) * 128u;
@@ -814,7 +815,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = ctrl->tmem_base;
-  const int kb_per_tile = kNumKBlocks + n_kb2;
+  const int kb_per_tile = kNumKBlocks * n_mma1 + n_kb2;  // B stages per unit
 
   if (warp == kLoaderWarp) {
     // ===================== loader: W1 K-blocks (this CTA's half of each N=256 slice), then W2
@@ -826,15 +827,15 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
           const uint32_t s = itb % kMB, ph = (itb / kMB) & 1u;
           HYDRO_PIPE_WAIT(&ctrl->empty_b[s], ph ^ 1u);
           uint8_t* dst = smem + (b_ring - a_ring) + s * kMlpBStage;
-          if (kb < kNumKBlocks) {
-            mbar_arrive_expect_tx(&ctrl->full_b[s], w1_stage);
-            for (int m = 0; m < n_mma1; ++m)
-              bulk_g2s_hint(dst + m * 16384, pdg.w_tiled + static_cast<uint64_t>(kb) * w1_kb + (m * 256 + crank * 128) * 128u,
-                            16384u, &ctrl->full_b[s], pol_w);
+          if (kb < kNumKBlocks * n_mma1) {  // W1 K-block kb / n_mma1, N slice kb % n_mma1
+            const int k1 = kb / n_mma1, m = kb % n_mma1;
+            mbar_arrive_expect_tx(&ctrl->full_b[s], 16384u);
+            bulk_g2s_hint(dst, pdg.w_tiled + static_cast<uint64_t>(k1) * w1_kb + (m * 256 + crank * 128) * 128u, 16384u,
+                          &ctrl->full_b[s], pol_w);
           } else {
             mbar_arrive_expect_tx(&ctrl->full_b[s], w2_load);
-            bulk_g2s_hint(dst, pdg.w2_tiled + static_cast<uint64_t>(kb - kNumKBlocks) * w2_kb + crank * w2_load, w2_load,
-                          &ctrl->full_b[s], pol_w);
+            bulk_g2s_hint(dst, pdg.w2_tiled + static_cast<uint64_t>(kb - kNumKBlocks * n_mma1) * w2_kb + crank * w2_load,
+                          w2_load, &ctrl->full_b[s], pol_w);
           }
         }
       }
@@ -863,22 +864,22 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
         for (int g = 0; g < kGroups; ++g, ++gg) {
           const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph2 = (gg >> 1) & 1u;
 #pragma unroll
-          for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr, ++itb) {
+          for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) {
             const uint32_t sa = set + kbr;
-            const uint32_t sb = itb % kMB, bph = (itb / kMB) & 1u;
             HYDRO_PIPE_WAIT(&ctrl->full_a[sa], aph2);
-            HYDRO_PIPE_WAIT(&ctrl->full_b[sb], bph);
-            tc_fence_after();
             const uint32_t a_addr = a_ring + sa * kAKBlockBytes;
-            const uint32_t b_addr = b_ring + sb * kMlpBStage;
+            for (int m = 0; m < n_mma1; ++m, ++itb) {
+              const uint32_t sb = itb % kMB, bph = (itb / kMB) & 1u;
+              HYDRO_PIPE_WAIT(&ctrl->full_b[sb], bph);
+              tc_fence_after();
+              const uint32_t b_addr = b_ring + sb * kMlpBStage;
 #pragma unroll
-            for (int kk = 0; kk < kKBlock / 16; ++kk) {
-              for (int m = 0; m < n_mma1; ++m)
-                tc_mma_pair(tmem_base + m * 256, desc_sw128(a_addr + kk * 32), desc_sw128(b_addr + m * 16384 + kk * 32),
-                            idesc1, (g | kbr | kk) != 0 ? 1u : 0u);
+              for (int kk = 0; kk < kKBlock / 16; ++kk)
+                tc_mma_pair(tmem_base + m * 256, desc_sw128(a_addr + kk * 32), desc_sw128(b_addr + kk * 32), idesc1,
+                            (g | kbr | kk) != 0 ? 1u : 0u);
+              tc_commit_pair(&ctrl->empty_b[sb]);
             }
             tc_commit_pair(&ctrl->empty_a[sa]);
-            tc_commit_pair(&ctrl->empty_b[sb]);
           }
         }
         tc_commit_pair(&ctrl->tfull[0]);

@@ -570,7 +570,7 @@ static hydro_status launch_compact(hydro_ctx* ctx, const CompactParams& c, uint6
 static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_positions, bool mlp = false) {
   const uint64_t tiles = (max_positions + kTileM - 1) / kTileM;
   const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctx->num_sms)));
-  return timed_launch(ctx, 1, [&] {
+  return timed_launch(ctx, mlp ? 4 : 1, [&] {
     const bool dbg = c.dbg_crops || c.dbg_logits || c.dbg_verdict;
     if (mlp) hydro_mlp_launch(c, grid, ctx->stream, dbg);
     // kernel instantiation by context capability: AREA support only when an AREA head exists
