@@ -56,7 +56,10 @@ enum {
   HYDRO_POLICY_FIXED_ORDER = 2, /* "No Reordering" / test hook: the order set by
                                    hydro_set_fixed_order (default: add order) */
   HYDRO_POLICY_COST = 3,        /* cost only */
-  HYDRO_POLICY_SELECTIVITY = 4  /* selectivity only */
+  HYDRO_POLICY_SELECTIVITY = 4, /* selectivity only */
+  HYDRO_POLICY_REUSE = 5        /* reuse-aware: per batch, estimated cost
+                                   (1 - cache hit rate of the batch) * cost of computing the UDF,
+                                   lowest first; needs verdict caches (hydro_cache_enable) */
 };
 
 /* Where the per-tuple cost of a predicate comes from (R6). */
@@ -166,6 +169,9 @@ typedef struct {
   int32_t position;           /* position in the current order (0 = first)                     */
   double s_in, s_pass, s_cost;/* decayed counters S (R4)                                       */
   double cost_raw_total;      /* cumulative measured raw cycles                                */
+  int64_t tuples_computed;    /* cumulative tuples actually evaluated (not served by the verdict
+                                 cache); == tuples_in without a cache                           */
+  double cache_hit_rate;      /* REUSE policy: the last batch's cache hit rate (0 otherwise)   */
 } hydro_pred_stats;
 
 /* Per-batch record, available after the batch completed (hydro_batch_info). */
@@ -177,6 +183,7 @@ typedef struct {
   int64_t tuples_in[HYDRO_MAX_PREDICATES];  /* this batch's counters (warmup included)         */
   int64_t tuples_passed[HYDRO_MAX_PREDICATES];
   double cost_raw[HYDRO_MAX_PREDICATES];
+  int64_t tuples_computed[HYDRO_MAX_PREDICATES]; /* evaluated, not served by the verdict cache  */
   int32_t n_pred;
 } hydro_batch_report;
 
@@ -202,6 +209,23 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out);
    negative units, LINEAR / MLP without a frame pool, MLP with hidden not in {256, 512} or an
    AREA crop, declared values out of range. */
 hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* desc, int32_t* pred_id);
+
+/* Verdict cache for reuse-aware routing: predicate
+   pred_id (LABEL_EQ or HASH) keeps a device bitmap of known verdicts over tuple ids
+   [0, id_capacity) (2 bits per id, library-owned).  A cached verdict is used instead of
+   evaluating the predicate (the result is unchanged: the cache holds the predicate's verdicts);
+   cost statistics count only evaluated tuples (the cost of computing the UDF).  fill = 1 also
+   records every verdict the predicate computes.  Before the first submit (ESTATE after);
+   EINVAL for classifier predicates, id_capacity 0 or > 2^34, or a second call. */
+hydro_status hydro_cache_enable(hydro_ctx* ctx, int32_t pred_id, uint64_t id_capacity, int32_t fill);
+
+/* Records verdicts[i] (0 / 1) of predicate pred_id for tuple ids[i], i < n (e.g. the results of
+   an earlier query that evaluated the same UDF).  Ordered on the context stream; ids and
+   verdicts are host arrays (copied before return) or device arrays (on_device = 1, borrowed
+   until the next synchronising call).  ids >= id_capacity are ignored.  The caller vouches
+   that the verdicts are the predicate's.  EINVAL without an enabled cache. */
+hydro_status hydro_cache_put(hydro_ctx* ctx, int32_t pred_id, const uint64_t* ids, const uint8_t* verdicts,
+                             int64_t n, int32_t on_device);
 
 /* FIXED_ORDER policy: sets the order (a permutation of 0..P-1).  EINVAL if not a permutation. */
 hydro_status hydro_set_fixed_order(hydro_ctx* ctx, const int32_t* order, int32_t n);

@@ -313,6 +313,29 @@ def policy_key(policy: str, c: float, s: float) -> float:
     raise ValueError(policy)
 
 
+def reuse_estimated_cost(c: float, hit: float) -> float:
+    """Reuse-aware routing: estimated cost = (1 - cache hit rate) * cost of
+    computing the UDF; the cache lookup is assumed free."""
+    return (1.0 - hit) * c
+
+
+def cache_hit_rate(ids: np.ndarray, cached: Sequence[tuple]) -> float:
+    """Fraction of a batch's tuple ids whose verdict is cached; ``cached`` = open id intervals
+    (lo, hi) as in UC2's ``WHERE id > lo AND id < hi``."""
+    ids = np.asarray(ids, dtype=np.int64)
+    if len(ids) == 0:
+        return 0.0
+    hit = np.zeros(len(ids), dtype=bool)
+    for lo, hi in cached:
+        hit |= (ids > lo) & (ids < hi)
+    return float(hit.mean())
+
+
+def reuse_order(costs: Sequence[float], hits: Sequence[float]) -> List[int]:
+    """Lowest estimated cost first, ties -> lowest predicate id (R2)."""
+    return order_by_key([reuse_estimated_cost(c, h) for c, h in zip(costs, hits)])
+
+
 def order_by_key(keys: Sequence[float]) -> List[int]:
     """Lowest key first; ties -> lowest predicate id (R2)."""
     return sorted(range(len(keys)), key=lambda k: (keys[k], k))

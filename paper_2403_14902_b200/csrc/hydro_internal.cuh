@@ -69,6 +69,11 @@ struct PredDev {
   int32_t hidden;           // MLP: hidden width (256 / 512); w_tiled = W1 (n_pad rows = hidden), bias = b2
   const uint8_t* w2_tiled;  // MLP: W2 [hidden/64 kblk][n_pad rows][128 B SW128], bf16
   const float* bias1;       // MLP: b1 [hidden]
+  uint32_t* cache_known;    // verdict cache (reuse-aware routing): bit id = verdict known
+  uint32_t* cache_pass;     //   bit id = cached verdict
+  uint64_t cache_cap;       //   ids [0, cache_cap)
+  int32_t cache_fill;       //   record computed verdicts
+  int32_t pad2_;
 };
 
 // Device-resident eddy state (one per context).  d_* are the atomically accumulated deltas of
@@ -88,7 +93,12 @@ struct DevState {
   double declared_sel[kMaxPred];
   double cost_norm[kMaxPred];         // raw cycles -> SM-cycles
   unsigned long long d_in[kMaxPred], d_pass[kMaxPred], d_cost[kMaxPred];
-  unsigned long long pend[3 * kMaxPred];   // in[8], pass[8], cost[8]  (NCCL all-reduce buffer)
+  unsigned long long d_comp[kMaxPred];     // tuples evaluated (not served by the verdict cache)
+  unsigned long long d_hit[kMaxPred];      // REUSE probe: cached ids of the batch
+  unsigned long long pend[4 * kMaxPred];   // in[8], pass[8], cost[8], comp[8]  (NCCL all-reduce buffer)
+  unsigned long long tot_comp[kMaxPred];
+  double s_comp[kMaxPred];
+  double hit[kMaxPred];                    // REUSE: the batch's cache hit rate
   unsigned long long tot_in[kMaxPred], tot_pass[kMaxPred];
   double tot_cost[kMaxPred];
   double s_in[kMaxPred], s_pass[kMaxPred], s_cost[kMaxPred];
@@ -111,7 +121,7 @@ struct BatchRec {
   unsigned int warm_count;    // survivors of the warmup slice (written first in the output)
   unsigned int total_count;   // all survivors of the batch
   int32_t order_used[kMaxPred];
-  unsigned long long d_in[kMaxPred], d_pass[kMaxPred], d_cost[kMaxPred];
+  unsigned long long d_in[kMaxPred], d_pass[kMaxPred], d_cost[kMaxPred], d_comp[kMaxPred];
 };
 
 // K1: evaluate a run of cheap predicates -> verdict bitmap (bit per input position) + survivors
@@ -344,6 +354,10 @@ __global__ void hydro_compact_kernel(hydro::CompactParams p);
 cudaError_t hydro_classifier_configure();
 void hydro_classifier_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug, bool area);
 void hydro_mlp_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug);
-__global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode);
+__global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode, uint32_t n_batch);
+__global__ void hydro_probe_kernel(hydro::DevState* st, const hydro::PredDev* preds, const uint64_t* id, uint32_t base,
+                                   uint32_t n);
+__global__ void hydro_cache_put_kernel(uint32_t* known, uint32_t* pass, uint64_t cap, const uint64_t* ids,
+                                       const uint8_t* verdicts, uint64_t n);
 __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,
                                           int32_t k_features, int32_t to_fp16, int32_t* inexact);

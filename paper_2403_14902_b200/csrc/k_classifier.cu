@@ -701,6 +701,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     if (p.collect_stats && lane == 0) {
       atomicAdd(&st->d_in[pred], static_cast<unsigned long long>(n_in));
       atomicAdd(&st->d_pass[pred], static_cast<unsigned long long>(n_pass));
+      atomicAdd(&st->d_comp[pred], static_cast<unsigned long long>(n_in));  // no verdict cache here
     }
   }
 
@@ -979,6 +980,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
     if (p.collect_stats && lane == 0) {
       atomicAdd(&st->d_in[pred], static_cast<unsigned long long>(n_in));
       atomicAdd(&st->d_pass[pred], static_cast<unsigned long long>(n_pass));
+      atomicAdd(&st->d_comp[pred], static_cast<unsigned long long>(n_in));  // no verdict cache here
     }
   }
 

@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kern
   __shared__ int32_t s_run_id[kMaxPred];
   // per-warp statistic slots (lane 0 of each warp owns its row: plain adds, no shared atomics)
   __shared__ uint32_t s_in[kRouteThreads / 32][kMaxPred], s_pass[kRouteThreads / 32][kMaxPred];
+  __shared__ uint32_t s_comp[kRouteThreads / 32][kMaxPred];
   __shared__ unsigned long long s_cost[kRouteThreads / 32][kMaxPred];
   __shared__ uint32_t s_warp_cnt[2][kRouteThreads / 32];  // double-buffered: one barrier per tile
   __shared__ uint64_t s_cids[kRouteThreads / 32][kWarpSeg];  // per-warp compacted ids (sparse HASH hops)
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kern
       } else {
         need_label = 1;
       }
+      if (q.cache_known) need_id = 1;  // the verdict cache is keyed by tuple id
     }
     s_work = work;
     s_nrun = nrun;
@@ -147,6 +149,7 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kern
   if (lane < kMaxPred) {
     s_in[warp][lane] = 0;
     s_pass[warp][lane] = 0;
+    s_comp[warp][lane] = 0;
     s_cost[warp][lane] = 0;
   }
   __syncthreads();
@@ -234,6 +237,22 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kern
       const PredDev& pd = s_pred[r];
       const long long t0 = clock64();
       const uint32_t in_mask = mask;
+      // verdict cache: alive items whose verdict is known are not evaluated
+      uint32_t cm = 0, cpass = 0;
+      if (pd.cache_known && mask) {
+#pragma unroll
+        for (int j = 0; j < kRouteItems; ++j) {
+          if (((mask >> j) & 1u) && ids[j] < pd.cache_cap) {
+            const uint64_t v = ids[j];
+            const uint32_t kw = __ldg(pd.cache_known + (v >> 5)), pw = __ldg(pd.cache_pass + (v >> 5));
+            cm |= ((kw >> (v & 31)) & 1u) << j;
+            cpass |= ((pw >> (v & 31)) & 1u) << j;
+          }
+        }
+        cpass &= cm;
+        mask &= ~cm;  // evaluate the rest (mask = the items this predicate computes)
+      }
+      const uint32_t todo = mask;
       const uint32_t warp_alive = __reduce_add_sync(kFull, __popc(mask));
 #ifdef HYDRO_K1_COMPACT
       constexpr bool kCompactHash = true;
@@ -326,15 +345,32 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kern
         }
       }
       const long long t1 = clock64();
+      if (pd.cache_known) {
+        if (pd.cache_fill && todo) {  // record the verdicts this predicate computed
+#pragma unroll
+          for (int j = 0; j < kRouteItems; ++j) {
+            if (((todo >> j) & 1u) && ids[j] < pd.cache_cap) {
+              const uint64_t v = ids[j];
+              const uint32_t bit = 1u << (v & 31);
+              if ((mask >> j) & 1u) atomicOr(pd.cache_pass + (v >> 5), bit);
+              atomicOr(pd.cache_known + (v >> 5), bit);
+            }
+          }
+        }
+        mask |= cpass;  // cached passes rejoin the alive set
+      }
       if (p.collect_stats) {
         const uint32_t ci = __reduce_add_sync(kFull, __popc(in_mask));
         const uint32_t cp = __reduce_add_sync(kFull, __popc(mask));
+        const uint32_t cc = pd.cache_known ? __reduce_add_sync(kFull, __popc(todo)) : ci;
         if (lane == 0) {
           s_in[warp][r] += ci;
           s_pass[warp][r] += cp;
-          // dense-equivalent cost: SIMT lanes without an alive item idle, so the warp's cycles are
-          // charged in proportion to its occupancy (ci of 256 items); SM-cycles = raw / (256 * warps/SM)
-          s_cost[warp][r] += static_cast<unsigned long long>(t1 - t0) * ci;
+          s_comp[warp][r] += cc;
+          // dense-equivalent cost: SIMT lanes without an item to evaluate idle, so the warp's cycles
+          // are charged in proportion to the items it evaluated (cc of 256); SM-cycles = raw / (256 *
+          // warps/SM).  Cache hits cost nothing (PAPER.md:604 assumes the lookup overhead negligible)
+          s_cost[warp][r] += static_cast<unsigned long long>(t1 - t0) * cc;
         }
       }
     }
@@ -361,16 +397,18 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kern
   __syncthreads();
   if (p.collect_stats && tid < nrun) {
     const int k = s_run_id[tid];
-    unsigned long long in = 0, pass = 0, cost = 0;
+    unsigned long long in = 0, pass = 0, cost = 0, comp = 0;
 #pragma unroll
     for (int w = 0; w < kRouteThreads / 32; ++w) {
       in += s_in[w][tid];
       pass += s_pass[w][tid];
       cost += s_cost[w][tid];
+      comp += s_comp[w][tid];
     }
     atomicAdd(&st->d_in[k], in);
     atomicAdd(&st->d_pass[k], pass);
     atomicAdd(&st->d_cost[k], cost);
+    atomicAdd(&st->d_comp[k], comp);
   }
 }
 
@@ -556,36 +594,111 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactPar
 }
 
 // ------------------------------------------------------------------------------------------
-// K5: fold.  mode bit 0 = PREP (deltas -> batch record + pending), bit 1 = APPLY (pending ->
-// decayed statistics -> keys -> order), bit 2 = RECORD (order used by this batch's chain).
+// Verdict cache (reuse-aware routing).  K0 probe: for every predicate with a
+// cache, the number of the batch's tuple ids whose verdict is cached ("the router algorithms first
+// check the potential cache hit rate for a batch") -> d_hit; K5 mode 8 turns it
+// into the batch's hit rates and the order by estimated cost.  put: records given verdicts.
+__global__ void __launch_bounds__(kRouteThreads) hydro_probe_kernel(DevState* st, const PredDev* preds,
+                                                                    const uint64_t* id, uint32_t base, uint32_t n) {
+  __shared__ unsigned long long s_hit[kMaxPred];
+  const int P = st->n_pred;
+  if (threadIdx.x < kMaxPred) s_hit[threadIdx.x] = 0;
+  __syncthreads();
+  for (int k = 0; k < P; ++k) {
+    const uint32_t* known = preds[k].cache_known;
+    if (!known) continue;
+    const uint64_t cap = preds[k].cache_cap;
+    uint32_t c = 0;
+    for (uint32_t i = blockIdx.x * kRouteThreads + threadIdx.x; i < n; i += gridDim.x * kRouteThreads) {
+      const uint64_t v = __ldg(id + base + i);
+      if (v < cap) c += (__ldg(known + (v >> 5)) >> (v & 31)) & 1u;
+    }
+    c = __reduce_add_sync(kFull, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_hit[k], static_cast<unsigned long long>(c));
+  }
+  __syncthreads();
+  if (threadIdx.x < P && s_hit[threadIdx.x]) atomicAdd(&st->d_hit[threadIdx.x], s_hit[threadIdx.x]);
+}
 
-__device__ __forceinline__ double policy_key(int policy, double c, double s) {
+__global__ void hydro_cache_put_kernel(uint32_t* known, uint32_t* pass, uint64_t cap, const uint64_t* ids,
+                                       const uint8_t* verdicts, uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t v = ids[i];
+    if (v >= cap) continue;
+    const uint32_t bit = 1u << (v & 31);
+    if (verdicts[i]) atomicOr(pass + (v >> 5), bit);
+    else atomicAnd(pass + (v >> 5), ~bit);
+    atomicOr(known + (v >> 5), bit);  // after the verdict bit: readers in later kernels see both
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K5: fold.
+
+__device__ __forceinline__ double policy_key(int policy, double c, double s, double hit) {
   if (policy == HYDRO_POLICY_COST) return c;
   if (policy == HYDRO_POLICY_SELECTIVITY) return s;
+  if (policy == HYDRO_POLICY_REUSE) return (1.0 - hit) * c;  // estimated cost
   if (c == 0.0) return 0.0;                      // R1
   if (s >= 1.0) return __longlong_as_double(0x7FF0000000000000ll);  // +inf (R1)
   return c / (1.0 - s);
 }
 
-__global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode) {
+// keys from st->cost / sel / hit, stable order by (key, id) (R2), positions, hop slots
+__device__ void order_by_keys(DevState* st) {
+  const int P = st->n_pred;
+  for (int k = 0; k < P; ++k) st->key[k] = policy_key(st->policy, st->cost[k], st->sel[k], st->hit[k]);
+  if (st->policy != HYDRO_POLICY_FIXED_ORDER) {
+    int ord[kMaxPred];
+    for (int k = 0; k < P; ++k) ord[k] = k;
+    for (int i = 1; i < P; ++i) {  // stable insertion sort by (key, id): R2
+      const int v = ord[i];
+      int j = i - 1;
+      while (j >= 0 && st->key[ord[j]] > st->key[v]) {
+        ord[j + 1] = ord[j];
+        --j;
+      }
+      ord[j + 1] = v;
+    }
+    for (int i = 0; i < P; ++i) st->order[i] = ord[i];
+  }
+  for (int i = 0; i < P; ++i) st->position[st->order[i]] = i;
+  build_sched(st->kind, st->order, P, st->sched);
+}
+
+// mode: bit 0 = PREP (batch deltas -> batch record + pending), bit 1 = APPLY (pending -> decayed
+// statistics -> keys -> order), bit 2 = RECORD (order used by this batch's chain), bit 3 = REUSE
+// (the batch's cache hit rates from the probe counts over n_batch tuples -> keys -> order).
+__global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode, uint32_t n_batch) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const int P = st->n_pred;
+  if (mode & 8) {
+    for (int k = 0; k < P; ++k) {
+      st->hit[k] = n_batch > 0 ? static_cast<double>(st->d_hit[k]) / static_cast<double>(n_batch) : 0.0;
+      st->d_hit[k] = 0;
+    }
+    order_by_keys(st);
+  }
   if (mode & 4) {
     for (int k = 0; k < kMaxPred; ++k) rec->order_used[k] = k < P ? st->order[k] : -1;
   }
   if (mode & 1) {
     for (int k = 0; k < P; ++k) {
-      const unsigned long long di = st->d_in[k], dp = st->d_pass[k], dc = st->d_cost[k];
+      const unsigned long long di = st->d_in[k], dp = st->d_pass[k], dc = st->d_cost[k], dm = st->d_comp[k];
       rec->d_in[k] += di;
       rec->d_pass[k] += dp;
       rec->d_cost[k] += dc;
+      rec->d_comp[k] += dm;
       st->pend[k] += di;
       st->pend[kMaxPred + k] += dp;
       st->pend[2 * kMaxPred + k] += dc;
+      st->pend[3 * kMaxPred + k] += dm;
       st->tot_in[k] += di;
       st->tot_pass[k] += dp;
       st->tot_cost[k] += static_cast<double>(dc);
-      st->d_in[k] = st->d_pass[k] = st->d_cost[k] = 0;
+      st->tot_comp[k] += dm;
+      st->d_in[k] = st->d_pass[k] = st->d_cost[k] = st->d_comp[k] = 0;
     }
   }
   if (mode & 2) {
@@ -596,8 +709,9 @@ __global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode) {
         st->s_in[k] = g * st->s_in[k] + static_cast<double>(di);
         st->s_pass[k] = g * st->s_pass[k] + static_cast<double>(st->pend[kMaxPred + k]);
         st->s_cost[k] = g * st->s_cost[k] + static_cast<double>(st->pend[2 * kMaxPred + k]) * st->cost_norm[k];
+        st->s_comp[k] = g * st->s_comp[k] + static_cast<double>(st->pend[3 * kMaxPred + k]);
       }
-      st->pend[k] = st->pend[kMaxPred + k] = st->pend[2 * kMaxPred + k] = 0;
+      st->pend[k] = st->pend[kMaxPred + k] = st->pend[2 * kMaxPred + k] = st->pend[3 * kMaxPred + k] = 0;
     }
     for (int k = 0; k < P; ++k) {
       double s, c;
@@ -606,29 +720,15 @@ __global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode) {
         c = st->declared_cost[k];
       } else {
         s = st->s_in[k] > 0.0 ? st->s_pass[k] / st->s_in[k] : st->prior;  // PAPER.md:416, R3
-        c = (st->cost_source == HYDRO_COST_DECLARED || st->s_in[k] <= 0.0) ? st->declared_cost[k]
-                                                                             : st->s_cost[k] / st->s_in[k];
+        // cost of computing the predicate per evaluated tuple (cache hits excluded,
+        // PAPER.md:600); without a cache every routed tuple is evaluated (s_comp == s_in)
+        c = (st->cost_source == HYDRO_COST_DECLARED || st->s_comp[k] <= 0.0) ? st->declared_cost[k]
+                                                                               : st->s_cost[k] / st->s_comp[k];
       }
       st->sel[k] = s;
       st->cost[k] = c;
-      st->key[k] = policy_key(st->policy, c, s);
     }
-    if (st->policy != HYDRO_POLICY_FIXED_ORDER) {
-      int ord[kMaxPred];
-      for (int k = 0; k < P; ++k) ord[k] = k;
-      for (int i = 1; i < P; ++i) {  // stable insertion sort by (key, id): R2
-        const int v = ord[i];
-        int j = i - 1;
-        while (j >= 0 && st->key[ord[j]] > st->key[v]) {
-          ord[j + 1] = ord[j];
-          --j;
-        }
-        ord[j + 1] = v;
-      }
-      for (int i = 0; i < P; ++i) st->order[i] = ord[i];
-    }
-    for (int i = 0; i < P; ++i) st->position[st->order[i]] = i;
-    build_sched(st->kind, st->order, P, st->sched);
+    order_by_keys(st);
   }
 }
 

@@ -49,6 +49,10 @@ struct PredHost {
   int a_fp16 = 0;
   uint8_t* w2_tiled = nullptr;  // MLP layer 2
   float* bias1 = nullptr;       // MLP layer 1 bias
+  uint32_t* cache_known = nullptr;  // verdict cache (reuse-aware routing)
+  uint32_t* cache_pass = nullptr;
+  uint64_t cache_cap = 0;
+  int cache_fill = 0;
 };
 
 struct Slot {
@@ -217,7 +221,7 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   if (!(cfg->decay_gamma > 0.0 && cfg->decay_gamma <= 1.0)) return set_err(HYDRO_EINVAL, "decay_gamma in (0, 1]");
   if (!(cfg->prior_selectivity >= 0.0 && cfg->prior_selectivity <= 1.0))
     return set_err(HYDRO_EINVAL, "prior_selectivity in [0, 1]");
-  if (cfg->policy < 0 || cfg->policy > 4) return set_err(HYDRO_EINVAL, "unknown policy");
+  if (cfg->policy < 0 || cfg->policy > HYDRO_POLICY_REUSE) return set_err(HYDRO_EINVAL, "unknown policy");
   if (cfg->cost_source < 0 || cfg->cost_source > 1) return set_err(HYDRO_EINVAL, "unknown cost_source");
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return set_err(HYDRO_EINVAL, "bad rank/world");
   if (cfg->world > 1 && !cfg->nccl_unique_id) return set_err(HYDRO_EINVAL, "world > 1 needs nccl_unique_id");
@@ -261,7 +265,8 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   }
   ctx->warmup_pending = (cfg->warmup_tuples > 0) && (cfg->policy == HYDRO_POLICY_SCORE ||
                                                      cfg->policy == HYDRO_POLICY_COST ||
-                                                     cfg->policy == HYDRO_POLICY_SELECTIVITY);
+                                                     cfg->policy == HYDRO_POLICY_SELECTIVITY ||
+                                                     cfg->policy == HYDRO_POLICY_REUSE);
   *out = ctx;
   return HYDRO_OK;
 }
@@ -365,6 +370,57 @@ static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_devi
 
 extern "C" {
 
+hydro_status hydro_cache_enable(hydro_ctx* ctx, int32_t k, uint64_t id_capacity, int32_t fill) {
+  if (!ctx) return set_err(HYDRO_EINVAL, "NULL argument");
+  if (ctx->frozen) return set_err(HYDRO_ESTATE, "cache_enable after the first submit");
+  if (k < 0 || k >= static_cast<int32_t>(ctx->preds.size())) return set_err(HYDRO_EINVAL, "bad pred id");
+  PredHost& ph = ctx->preds[k];
+  if (is_classifier(ph.desc.kind)) return set_err(HYDRO_EINVAL, "verdict caches are for LABEL_EQ / HASH predicates");
+  if (ph.cache_known) return set_err(HYDRO_EINVAL, "cache already enabled");
+  if (id_capacity == 0 || id_capacity > (1ull << 34)) return set_err(HYDRO_EINVAL, "id_capacity in [1, 2^34]");
+  const size_t words = static_cast<size_t>((id_capacity + 31) / 32);
+  CU(cudaMalloc(&ph.cache_known, words * 4));
+  CU(cudaMalloc(&ph.cache_pass, words * 4));
+  CU(cudaMemsetAsync(ph.cache_known, 0, words * 4, ctx->stream));
+  CU(cudaMemsetAsync(ph.cache_pass, 0, words * 4, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ph.cache_cap = id_capacity;
+  ph.cache_fill = fill ? 1 : 0;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_cache_put(hydro_ctx* ctx, int32_t k, const uint64_t* ids, const uint8_t* verdicts, int64_t n,
+                             int32_t on_device) {
+  if (!ctx) return set_err(HYDRO_EINVAL, "NULL argument");
+  if (k < 0 || k >= static_cast<int32_t>(ctx->preds.size())) return set_err(HYDRO_EINVAL, "bad pred id");
+  PredHost& ph = ctx->preds[k];
+  if (!ph.cache_known) return set_err(HYDRO_EINVAL, "no verdict cache on this predicate (hydro_cache_enable)");
+  if (n < 0 || (n > 0 && (!ids || !verdicts))) return set_err(HYDRO_EINVAL, "bad ids / verdicts");
+  if (n == 0) return HYDRO_OK;
+  const uint64_t* d_ids = ids;
+  const uint8_t* d_v = verdicts;
+  uint64_t* tmp_ids = nullptr;
+  uint8_t* tmp_v = nullptr;
+  if (!on_device) {
+    CU(cudaMalloc(&tmp_ids, sizeof(uint64_t) * n));
+    CU(cudaMalloc(&tmp_v, static_cast<size_t>(n)));
+    CU(cudaMemcpyAsync(tmp_ids, ids, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(tmp_v, verdicts, static_cast<size_t>(n), cudaMemcpyHostToDevice, ctx->stream));
+    d_ids = tmp_ids;
+    d_v = tmp_v;
+  }
+  hydro_cache_put_kernel<<<256, 256, 0, ctx->stream>>>(ph.cache_known, ph.cache_pass, ph.cache_cap, d_ids, d_v,
+                                                        static_cast<uint64_t>(n));
+  ctx->launches += 1;
+  CU(cudaGetLastError());
+  if (!on_device) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaFree(tmp_ids));
+    CU(cudaFree(tmp_v));
+  }
+  return HYDRO_OK;
+}
+
 hydro_status hydro_set_fixed_order(hydro_ctx* ctx, const int32_t* order, int32_t n) {
   if (!ctx || !order) return set_err(HYDRO_EINVAL, "NULL argument");
   const int P = static_cast<int>(ctx->preds.size());
@@ -428,12 +484,16 @@ static hydro_status freeze(hydro_ctx* ctx) {
     q.hidden = d.hidden;
     q.w2_tiled = ctx->preds[k].w2_tiled;
     q.bias1 = ctx->preds[k].bias1;
+    q.cache_known = ctx->preds[k].cache_known;
+    q.cache_pass = ctx->preds[k].cache_pass;
+    q.cache_cap = ctx->preds[k].cache_cap;
+    q.cache_fill = ctx->preds[k].cache_fill;
   }
   // initial order: declared statistics (SCORE/COST/SEL before warmup; STATIC), or add order
   for (int k = 0; k < P; ++k) {
     double c = h.declared_cost[k], s = h.declared_sel[k];
     double key;
-    if (h.policy == HYDRO_POLICY_COST) key = c;
+    if (h.policy == HYDRO_POLICY_COST || h.policy == HYDRO_POLICY_REUSE) key = c;  // REUSE: hit rates per batch
     else if (h.policy == HYDRO_POLICY_SELECTIVITY) key = s;
     else key = (c == 0.0) ? 0.0 : (s >= 1.0 ? INFINITY : c / (1.0 - s));
     h.key[k] = key;
@@ -579,7 +639,7 @@ static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_
 }
 
 static hydro_status launch_fold(hydro_ctx* ctx, BatchRec* rec, int mode) {
-  return timed_launch(ctx, 2, [&] { hydro_fold_kernel<<<1, 32, 0, ctx->stream>>>(ctx->st, rec, mode); });
+  return timed_launch(ctx, 2, [&] { hydro_fold_kernel<<<1, 32, 0, ctx->stream>>>(ctx->st, rec, mode, 0u); });
 }
 
 static hydro_status fold_and_sync(hydro_ctx* ctx, BatchRec* rec, int record, bool force_sync) {
@@ -589,7 +649,7 @@ static hydro_status fold_and_sync(hydro_ctx* ctx, BatchRec* rec, int record, boo
   ctx->since_sync += record ? 1 : 0;
   if (force_sync || ctx->since_sync >= ctx->cfg.sync_every) {
     void* pend = reinterpret_cast<char*>(ctx->st) + offsetof(DevState, pend);
-    ncclResult_t r = ncclAllReduce(pend, pend, 3 * kMaxPred, ncclUint64, ncclSum, ctx->comm,
+    ncclResult_t r = ncclAllReduce(pend, pend, 4 * kMaxPred, ncclUint64, ncclSum, ctx->comm,
                                    ctx->stream);
     if (r != ncclSuccess) return ctx_fail(ctx, HYDRO_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
     ctx->since_sync = 0;
@@ -700,6 +760,18 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
   // predicates, or K4 for a classifier) then K2 compaction into the next hop's alive list / emit
   const uint32_t rest_base = static_cast<uint32_t>(warm);
   const uint32_t rest_n = static_cast<uint32_t>(n - warm);
+  if (ctx->cfg.policy == HYDRO_POLICY_REUSE && rest_n > 0) {
+    // reuse-aware routing: this batch's cache hit rates -> order by estimated cost
+    const int pgrid = static_cast<int>(std::min<uint64_t>((rest_n + 2047) / 2048, static_cast<uint64_t>(ctx->num_sms) * 4));
+    if ((s = timed_launch(ctx, 0, [&] {
+           hydro_probe_kernel<<<pgrid, kRouteThreads, 0, ctx->stream>>>(ctx->st, ctx->preds_dev, id, rest_base, rest_n);
+         })) != HYDRO_OK)
+      return s;
+    if ((s = timed_launch(ctx, 2, [&] {
+           hydro_fold_kernel<<<1, 32, 0, ctx->stream>>>(ctx->st, sl.rec, 8, rest_n);
+         })) != HYDRO_OK)
+      return s;
+  }
   // chain slots: any order has at most L classifier hops and min(C, L + 1) cheap runs
   int n_lin = 0;
   for (int k = 0; k < P; ++k) n_lin += is_classifier(ctx->preds[k].desc.kind) ? 1 : 0;
@@ -817,6 +889,7 @@ hydro_status hydro_batch_info(hydro_ctx* ctx, int64_t batch_id, hydro_batch_repo
     out->tuples_in[k] = static_cast<int64_t>(r.d_in[k]);
     out->tuples_passed[k] = static_cast<int64_t>(r.d_pass[k]);
     out->cost_raw[k] = static_cast<double>(r.d_cost[k]);
+    out->tuples_computed[k] = static_cast<int64_t>(r.d_comp[k]);
   }
   return HYDRO_OK;
 }
@@ -846,6 +919,8 @@ hydro_status hydro_get_stats(hydro_ctx* ctx, int32_t k, hydro_pred_stats* out) {
   out->s_pass = h.s_pass[k];
   out->s_cost = h.s_cost[k];
   out->cost_raw_total = h.tot_cost[k];
+  out->tuples_computed = static_cast<int64_t>(h.tot_comp[k]);
+  out->cache_hit_rate = h.hit[k];
   return HYDRO_OK;
 }
 
@@ -945,6 +1020,8 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
     cudaFree(p.bias);
     cudaFree(p.w2_tiled);
     cudaFree(p.bias1);
+    cudaFree(p.cache_known);
+    cudaFree(p.cache_pass);
   }
   for (TimedLaunch& t : ctx->timed) {
     cudaEventDestroy(t.a);

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("HYDRO_LIB_PATH") or os.path.join(HERE, "libhydro.so")
 
 HYDRO_OK, HYDRO_EINVAL, HYDRO_ENOMEM, HYDRO_ECUDA, HYDRO_ENCCL, HYDRO_ESTATE, HYDRO_ERANGE, HYDRO_EBUSY = (
     0, -1, -2, -3, -4, -5, -6, -7)
-POLICY = {"score": 0, "static": 1, "fixed": 2, "cost": 3, "selectivity": 4}
+POLICY = {"score": 0, "static": 1, "fixed": 2, "cost": 3, "selectivity": 4, "reuse": 5}
 COST_SOURCE = {"measured": 0, "declared": 1}
 PRED_KIND = {"label_eq": 0, "hash": 1, "linear": 2, "mlp": 3}
 CROP_MODE = {"nearest": 0, "area": 1}
@@ -59,14 +59,14 @@ class hydro_pred_stats(C.Structure):
     _fields_ = [("tuples_in", C.c_int64), ("tuples_passed", C.c_int64), ("cost_per_tuple", C.c_double),
                 ("selectivity", C.c_double), ("rank", C.c_double), ("position", C.c_int32),
                 ("s_in", C.c_double), ("s_pass", C.c_double), ("s_cost", C.c_double),
-                ("cost_raw_total", C.c_double)]
+                ("cost_raw_total", C.c_double), ("tuples_computed", C.c_int64), ("cache_hit_rate", C.c_double)]
 
 
 class hydro_batch_report(C.Structure):
     _fields_ = [("n_tuples", C.c_int64), ("n_results", C.c_int64), ("warmup_tuples", C.c_int64),
                 ("order_used", C.c_int32 * MAX_PRED), ("tuples_in", C.c_int64 * MAX_PRED),
                 ("tuples_passed", C.c_int64 * MAX_PRED), ("cost_raw", C.c_double * MAX_PRED),
-                ("n_pred", C.c_int32)]
+                ("tuples_computed", C.c_int64 * MAX_PRED), ("n_pred", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -78,6 +78,8 @@ _SIGS = {
     "hydro_create": ([C.POINTER(hydro_config), C.POINTER(_P)], C.c_int32),
     "hydro_add_predicate": ([_P, C.POINTER(hydro_predicate_desc), C.POINTER(C.c_int32)], C.c_int32),
     "hydro_set_fixed_order": ([_P, C.POINTER(C.c_int32), C.c_int32], C.c_int32),
+    "hydro_cache_enable": ([_P, C.c_int32, C.c_uint64, C.c_int32], C.c_int32),
+    "hydro_cache_put": ([_P, C.c_int32, _P, _P, C.c_int64, C.c_int32], C.c_int32),
     "hydro_submit_batch": ([_P, C.POINTER(hydro_tuples), C.POINTER(C.c_int64)], C.c_int32),
     "hydro_batch_count": ([_P, C.c_int64, C.POINTER(C.c_int64)], C.c_int32),
     "hydro_collect_results": ([_P, C.c_int64, _P, _P, C.c_int64, C.POINTER(C.c_int64), C.c_int32], C.c_int32),
@@ -148,6 +150,16 @@ def hydro_add_predicate(ctx, desc: hydro_predicate_desc) -> int:
     pid = C.c_int32()
     _check(lib().hydro_add_predicate(ctx, C.byref(desc), C.byref(pid)))
     return pid.value
+
+
+def hydro_cache_enable(ctx, pred_id: int, id_capacity: int, fill: bool = False):
+    _check(lib().hydro_cache_enable(ctx, pred_id, id_capacity, 1 if fill else 0))
+
+
+def hydro_cache_put(ctx, pred_id: int, ids, verdicts, on_device: bool):
+    """ids: uint64-compatible (torch int64) 1-D, verdicts: uint8/bool 1-D, same length."""
+    _check(lib().hydro_cache_put(ctx, pred_id, ids.data_ptr(), verdicts.data_ptr(), int(ids.numel()),
+                                 1 if on_device else 0))
 
 
 def hydro_set_fixed_order(ctx, order: Sequence[int]):
@@ -343,7 +355,8 @@ class Eddy:
         P = r.n_pred
         return dict(n_tuples=r.n_tuples, n_results=r.n_results, warmup_tuples=r.warmup_tuples,
                     order_used=list(r.order_used[:P]), tuples_in=list(r.tuples_in[:P]),
-                    tuples_passed=list(r.tuples_passed[:P]), cost_raw=list(r.cost_raw[:P]))
+                    tuples_passed=list(r.tuples_passed[:P]), cost_raw=list(r.cost_raw[:P]),
+                    tuples_computed=list(r.tuples_computed[:P]))
 
     def stats(self, pred_id: int) -> Dict:
         s = hydro_get_stats(self.ctx, pred_id)
@@ -351,6 +364,19 @@ class Eddy:
 
     def order(self) -> List[int]:
         return hydro_get_order(self.ctx)
+
+    def cache_enable(self, pred_id: int, id_capacity: int, fill: bool = False):
+        hydro_cache_enable(self.ctx, pred_id, id_capacity, fill)
+
+    def cache_put(self, pred_id: int, ids, verdicts):
+        """Records verdicts of pred_id for tuple ids (torch tensors on the host or the GPU)."""
+        v = verdicts.to(torch.uint8).contiguous()
+        i = ids.to(torch.int64).contiguous()
+        if i.is_cuda:
+            v = v.to(i.device)
+        hydro_cache_put(self.ctx, pred_id, i, v, i.is_cuda)
+        if i.is_cuda:
+            self.synchronize()  # device arrays are borrowed until the put ran
 
     def synchronize(self):
         hydro_synchronize(self.ctx)

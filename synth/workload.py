@@ -340,12 +340,21 @@ def workload(name: str, *, n: Optional[int] = None, small: bool = False) -> Work
                  linear_pred(SEED + 2, 10, 1, 0.633, name="colour=black")]
         return Workload("mlp", SEED, n or 1_000_000, nf, fh, fw, preds, w_min=wmin,
                         notes="cfg2 with a 12288-512-120 MLP breed head")
+    if name == "uc2":  # PAPER.md:562-605 reuse-aware routing, HASH stand-ins for the two detectors
+        preds = [hash_pred(SEED + 11, 0.5, units=64, declared_cost=64.0, name="ObjectDetector 'person'"),
+                 hash_pred(SEED + 12, 0.5, units=64, declared_cost=64.0, name="HardHatDetector 'no hardhat'")]
+        return Workload("uc2", SEED, n or 15_000, 4, 96, 128, preds, policy="reuse", w_min=8,
+                        batch_tuples=1000, warmup_tuples=0,
+                        notes="verdicts cached for ids in (1000, 7000) (predicate 0) and (8000, 14000) (predicate 1)")
     if name == "cfg5":
         w = workload("cfg2", n=n or 100_000_000, small=small)
         w.name = "cfg5"
         w.notes = "cfg2 query, 100M tuples sharded over ranks"
         return w
     raise KeyError(name)
+
+
+UC2_CACHED = ([(1000, 7000)], [(8000, 14000)])  # per predicate, cached id ranges
 
 
 def shard_range(n: int, rank: int, world: int):

@@ -64,6 +64,7 @@ int main(void) {
   O(hydro_predicate_desc, threshold); O(hydro_predicate_desc, weight_bf16); O(hydro_predicate_desc, declared_selectivity);
   O(hydro_predicate_desc, hidden); O(hydro_predicate_desc, weight2_bf16); O(hydro_predicate_desc, bias2);
   O(hydro_tuples, on_device); O(hydro_pred_stats, cost_raw_total); O(hydro_batch_report, cost_raw);
+  O(hydro_pred_stats, tuples_computed); O(hydro_pred_stats, cache_hit_rate); O(hydro_batch_report, tuples_computed);
   O(hydro_batch_report, n_pred);
   return 0;
 }

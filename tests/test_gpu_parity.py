@@ -400,3 +400,65 @@ def test_mlp_query_end_to_end(hidden):
         n_in, n_pass = expected_batch_counters(Vb, info["order_used"], 1024 if b == 0 else 0)
         assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist()
     e.close()
+
+
+# ------------------------------------------------------------------------ reuse-aware routing (f2)
+
+def _uc2_cached_verdicts(w, t, V):
+    """The verdicts an earlier query would have cached: predicate k's oracle
+    verdicts for the ids inside its UC2 range."""
+    from synth import UC2_CACHED
+
+    ids = t.id.numpy()
+    out = []
+    for k in range(len(w.preds)):
+        m = np.zeros(len(ids), dtype=bool)
+        for lo, hi in UC2_CACHED[k]:
+            m |= (ids > lo) & (ids < hi)
+        out.append((torch.from_numpy(ids[m].astype(np.int64)), torch.from_numpy(V[k][m].astype(np.uint8))))
+    return out
+
+
+@pytest.mark.parametrize("fill", [False, True])
+def test_uc2_reuse_aware_routing(fill):
+    """UC2: two expensive HASH stand-ins with verdicts cached for ids in
+    (1000, 7000) and (8000, 14000); REUSE policy with declared (equal) costs orders every
+    1000-tuple batch by (1 - hit rate) * cost exactly as the oracle predicts; rows and counters
+    equal the oracle's; cached tuples are not evaluated (tuples_computed).  fill = 1 also records
+    computed verdicts, so a second pass over the same ids computes nothing."""
+    from synth import UC2_CACHED
+
+    w = workload("uc2")
+    t = w.tuples()
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, None)
+    e = make_eddy(w, None, policy="reuse", cost_source="declared", warmup=0, max_batch=1000)
+    for k in range(2):
+        e.cache_enable(k, 1 << 15, fill=fill)
+    for k, (ids, ver) in enumerate(_uc2_cached_verdicts(w, t, V)):
+        e.cache_put(k, ids, ver)
+    ids, bbs, infos = run_stream(e, t.to("cuda"), 1000)
+    _assert_rows(ids, bbs, ref_ids, ref_bbox)
+    tid = t.id.numpy()
+    for b, info in enumerate(infos):
+        bid = tid[b * 1000:(b + 1) * 1000]
+        hits = [O.cache_hit_rate(bid, UC2_CACHED[k]) for k in range(2)]
+        order = O.reuse_order([64.0, 64.0], hits)
+        assert info["order_used"] == order, (b, hits, info["order_used"])
+        Vb = V[:, b * 1000:(b + 1) * 1000]
+        n_in, n_pass = expected_batch_counters(Vb, order, 0)
+        assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist()
+        # evaluated = routed to the predicate and not cached
+        alive = np.ones(len(bid), dtype=bool)
+        for k in order:
+            cached = np.zeros(len(bid), dtype=bool)
+            for lo, hi in UC2_CACHED[k]:
+                cached |= (bid > lo) & (bid < hi)
+            assert info["tuples_computed"][k] == int((alive & ~cached).sum()), (b, k)
+            alive &= Vb[k]
+    if fill:  # every verdict any predicate computed is now cached: a rerun evaluates nothing new
+        ids2, bbs2, infos2 = run_stream(e, t.to("cuda"), 1000)
+        _assert_rows(ids2, bbs2, ref_ids, ref_bbox)
+        computed = sum(sum(i["tuples_computed"]) for i in infos2)
+        # tuples a predicate never saw in pass 1 (dropped earlier under that batch's order) may run now
+        assert computed < 0.5 * sum(sum(i["tuples_computed"]) for i in infos), computed
+    e.close()

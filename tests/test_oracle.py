@@ -251,6 +251,52 @@ def test_mlp_all_negative_hidden_gives_bias_and_generated_selectivity():
     assert abs(v.mean() - 0.254) < 0.04
 
 
+# ----------------------------------------------------------------------------- reuse-aware routing (f2)
+
+
+def test_reuse_paper_example_orders_by_cached_range():
+    """UC2: inside (1000, 7000) ObjectDetector's results are cached, so it goes
+    first; inside (8000, 14000) HardHatDetector goes first; equal costs elsewhere keep the id order."""
+    from synth import UC2_CACHED
+
+    c = [64.0, 64.0]
+    for lo, expect in [(2000, [0, 1]), (9000, [1, 0]), (0, [0, 1]), (14500, [0, 1]), (7200, [0, 1])]:
+        ids = np.arange(lo, lo + 500)
+        hits = [O.cache_hit_rate(ids, UC2_CACHED[k]) for k in range(2)]
+        assert O.reuse_order(c, hits) == expect, (lo, hits)
+    # a batch straddling the (8000, 14000) boundary: 60% cached -> estimated 0.4 * 64 < 64
+    ids = np.arange(7600, 8601)
+    hits = [O.cache_hit_rate(ids, UC2_CACHED[k]) for k in range(2)]
+    assert abs(hits[1] - 600 / 1001) < 1e-12 and O.reuse_order(c, hits) == [1, 0]
+
+
+def test_reuse_estimated_cost_equals_realized_compute_cost():
+    """(1 - hit) * c is the compute cost per tuple when every uncached tuple costs c and cache hits
+    cost nothing: brute-force count over random batches and cached ranges."""
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        ids = rng.integers(0, 10_000, size=rng.integers(1, 400))
+        lo = int(rng.integers(0, 9000))
+        cached = [(lo, lo + int(rng.integers(1, 3000)))]
+        c = float(rng.uniform(0.1, 100))
+        realized = sum(c for v in ids if not (cached[0][0] < v < cached[0][1])) / len(ids)
+        assert abs(O.reuse_estimated_cost(c, O.cache_hit_rate(ids, cached)) - realized) < 1e-9 * c
+
+
+def test_reuse_order_minimises_compute_cost_for_equal_selectivity():
+    """With equal selectivities (so the order does not change which tuples reach the second
+    predicate) the lowest-estimated-cost-first order minimises the expected compute cost
+    e_1 + s * e_2 (brute force over both orders, E of R20 with estimated costs)."""
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        c = rng.uniform(1, 50, size=2)
+        h = rng.uniform(0, 1, size=2)
+        s = float(rng.uniform(0.05, 0.95))
+        e = [O.reuse_estimated_cost(c[k], h[k]) for k in range(2)]
+        best = min(itertools.permutations(range(2)), key=lambda p: O.expected_cost(p, e, [s, s]))
+        assert O.expected_cost(O.reuse_order(c, h), e, [s, s]) <= O.expected_cost(best, e, [s, s]) + 1e-12
+
+
 # ----------------------------------------------------------------------------- AND / order
 
 def test_and_is_order_independent_brute_force():
