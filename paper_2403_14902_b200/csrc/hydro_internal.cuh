@@ -158,6 +158,7 @@ struct RouteParams {
   DevState* st;
   const PredDev* preds;
   int32_t collect_stats;
+  int32_t force_fill;     // record every computed verdict in the predicate's cache (hydro_cache_fill)
 };
 
 struct CompactParams {
@@ -185,6 +186,7 @@ struct CompactParams {
   const uint64_t* bbox;
   DevState* st;
 };
+constexpr int kCompactUnits = 16;  // HASH rounds from which K1 compacts the alive ids before hashing
 constexpr int kWarpSeg = 256;  // positions per K1 warp per tile (= kRouteTile / 8)
 constexpr int kCompactSegs = 4;  // 2048-position segments per K2 CTA (multiple of 4: vector prefix loads)
 
@@ -349,7 +351,8 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
 }  // namespace hydro
 
 // kernels (defined in k_route.cu / k_classifier.cu), launched by runtime.cu
-__global__ void hydro_route_kernel(hydro::RouteParams p);
+void hydro_route_launch(const hydro::RouteParams& r, int grid, cudaStream_t stream, bool compact);
+int hydro_route_occupancy(bool compact);
 __global__ void hydro_compact_kernel(hydro::CompactParams p);
 cudaError_t hydro_classifier_configure();
 void hydro_classifier_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug, bool area);

@@ -36,6 +36,34 @@ __device__ __forceinline__ bool hash_pass(const PredDev& pd, uint64_t id, uint64
   return static_cast<uint64_t>(h) < T;
 }
 
+// Compacted HASH evaluation: thread tid hashes compact entries tid + 256 q, q < M (M independent
+// chains); the fail bits come back as one ballot word per 32 entries in s_vw.
+template <int M>
+__device__ __forceinline__ void hash_compacted(const PredDev& pd, const uint64_t* buf, uint32_t n, int tid, int lane,
+                                               int warp, uint32_t* s_vw) {
+  const bool one_thr = pd.thr0 == pd.thr1;
+  const int units = pd.units;
+  uint32_t hq[M];
+  uint64_t iq[M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    const uint32_t e = q * kRouteThreads + tid;
+    iq[q] = e < n ? buf[e] : 0ull;
+    hq[q] = static_cast<uint32_t>(splitmix64(iq[q] ^ pd.seed) >> 32);
+  }
+  for (int u = 0; u < units; ++u) {
+#pragma unroll
+    for (int q = 0; q < M; ++q) hq[q] = fmix32(hq[q] + static_cast<uint32_t>(u));
+  }
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    const uint32_t e = q * kRouteThreads + tid;
+    const uint64_t T = (one_thr || iq[q] < pd.drift_id) ? pd.thr0 : pd.thr1;
+    const uint32_t bw = __ballot_sync(kFull, e < n && static_cast<uint64_t>(hq[q]) >= T);
+    if (lane == 0 && q * kRouteThreads < n) s_vw[q * (kRouteThreads / 32) + warp] = bw;
+  }
+}
+
 // Which hop-h evaluator ran (device order): returns the first predicate's kind, and the cheap run
 // length in *run (0 when hop h is LINEAR or K1 has nothing to do).
 __device__ __forceinline__ bool k1_runs(const DevState* st, int h, int* run) {
@@ -54,10 +82,13 @@ __device__ __forceinline__ bool k1_runs(const DevState* st, int h, int* run) {
 
 // ------------------------------------------------------------------------------------------
 // K1: evaluate.  Persistent grid, tile t = positions [2048 t, 2048 t + 2048); thread = 8 positions.
+// kCompact: the context has an expensive HASH predicate (units >= kCompactUnits), so the kernel
+// carries the CTA-wide compaction path (more registers and 16 KB of shared memory)
+template <bool kCompact>
 #ifndef HYDRO_K1_MINB
-#define HYDRO_K1_MINB 1
+#define HYDRO_K1_MINB 3
 #endif
-__global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kernel(RouteParams p) {
+__global__ void __launch_bounds__(kRouteThreads, kCompact ? 2 : HYDRO_K1_MINB) hydro_route_kernel(RouteParams p) {
   __shared__ PredDev s_pred[kMaxPred];
   __shared__ int32_t s_run_id[kMaxPred];
   // per-warp statistic slots (lane 0 of each warp owns its row: plain adds, no shared atomics)
@@ -65,7 +96,9 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kern
   __shared__ uint32_t s_comp[kRouteThreads / 32][kMaxPred];
   __shared__ unsigned long long s_cost[kRouteThreads / 32][kMaxPred];
   __shared__ uint32_t s_warp_cnt[2][kRouteThreads / 32];  // double-buffered: one barrier per tile
-  __shared__ uint64_t s_cids[kRouteThreads / 32][kWarpSeg];  // per-warp compacted ids (sparse HASH hops)
+  __shared__ uint64_t s_cids[kCompact ? kRouteThreads / 32 : 1][kWarpSeg];  // compacted alive ids
+  __shared__ uint32_t s_vw[kRouteTile / 32];                 // their fail bits, one word per 32 entries
+  __shared__ uint32_t s_cw[kRouteThreads / 32];              // warp alive counts
   __shared__ int32_t s_work, s_nrun, s_n_and, s_need_id, s_need_bbox, s_need_label;
   __shared__ const uint32_t* s_list_in;
   __shared__ const uint32_t* s_and[kMaxPred];
@@ -253,17 +286,11 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kern
         mask &= ~cm;  // evaluate the rest (mask = the items this predicate computes)
       }
       const uint32_t todo = mask;
-      const uint32_t warp_alive = __reduce_add_sync(kFull, __popc(mask));
-#ifdef HYDRO_K1_COMPACT
-      constexpr bool kCompactHash = true;
-#else
-      constexpr bool kCompactHash = false;  // measured slower on B200 (the dense chains overlap better)
-#endif
-      if (kCompactHash && pd.kind == kHash && pd.units_per_area <= 0 && warp_alive > 0 &&
-          warp_alive * 2u <= static_cast<uint32_t>(kWarpSeg)) {
-        // HASH, uniform units, at most half of the warp's 256 positions alive (all lanes take
-        // this branch): compact the alive ids into a warp buffer, hash 32 per step (one per
-        // lane), ballot the verdicts back
+      // compact only expensive HASH predicates: at 1 round the dense chains overlap better (measured),
+      // but SIMT evaluates every position of a warp with any alive one, so without compaction an
+      // expensive predicate costs the same whatever its input selectivity (the eddy's saving is lost)
+      bool compacted = false;
+      if (kCompact && pd.kind == kHash && pd.units >= kCompactUnits && pd.units_per_area <= 0) {  // CTA-uniform
         const uint32_t c = __popc(mask);
         uint32_t x = c;
 #pragma unroll
@@ -271,42 +298,53 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kern
           const uint32_t y = __shfl_up_sync(kFull, x, o);
           if (lane >= o) x += y;
         }
-        const uint32_t off = x - c, n_alive = __shfl_sync(kFull, x, 31);
-        uint64_t* buf = s_cids[warp];
-        uint32_t k = off;
+        if (lane == 31) s_cw[warp] = x;
+        __syncthreads();
+        uint32_t wo = 0, n_cta = 0;
 #pragma unroll
-        for (int j = 0; j < kRouteItems; ++j)
-          if ((mask >> j) & 1u) buf[k++] = ids[j];
-        __syncwarp();
-        uint32_t vw = 0;  // lane i: fail bits of compact entries 32i .. 32i+31
-        const bool one_thr = pd.thr0 == pd.thr1;
-        for (uint32_t i = 0; i * 32u < n_alive; ++i) {
-          const uint32_t e = i * 32u + lane;
-          bool f = false;
-          if (e < n_alive) {
-            const uint64_t id = buf[e];
-            uint32_t h = static_cast<uint32_t>(splitmix64(id ^ pd.seed) >> 32);
-            for (int u = 0; u < pd.units; ++u) h = fmix32(h + static_cast<uint32_t>(u));
-            const uint64_t T = (one_thr || id < pd.drift_id) ? pd.thr0 : pd.thr1;
-            f = static_cast<uint64_t>(h) >= T;
-          }
-          const uint32_t b = __ballot_sync(kFull, f);
-          if (lane == static_cast<int>(i)) vw = b;
+        for (int w2 = 0; w2 < kRouteThreads / 32; ++w2) {
+          const uint32_t v = s_cw[w2];
+          wo += w2 < warp ? v : 0u;
+          n_cta += v;
         }
-        const uint32_t w0 = __shfl_sync(kFull, vw, off >> 5);
-        const uint32_t w1 = __shfl_sync(kFull, vw, min((off >> 5) + 1u, 7u));
-        const uint32_t fb = __funnelshift_r(w0, w1, off & 31u) & ((1u << c) - 1u);  // this thread's entries
-        uint32_t fail = 0, t = 0;
+        if (n_cta > 0 && 4u * n_cta <= 3u * static_cast<uint32_t>(kRouteTile)) {
+          // CTA-wide compaction: the tile's alive ids -> s_cids in position order, every thread then
+          // hashes 4 entries at a time (independent chains), verdicts come back as ballot words
+          compacted = true;
+          const uint32_t off = wo + x - c;
+          uint64_t* buf = &s_cids[0][0];
+          uint32_t k = off;
 #pragma unroll
-        for (int j = 0; j < kRouteItems; ++j) {
-          if ((mask >> j) & 1u) {
-            fail |= ((fb >> t) & 1u) << j;
-            ++t;
+          for (int j = 0; j < kRouteItems; ++j)
+            if ((mask >> j) & 1u) buf[k++] = ids[j];
+          __syncthreads();
+          // ceil(n / 256) entries per thread (1..6 at <= 75% alive), as independent chains
+          const uint32_t m = (n_cta + kRouteThreads - 1) / kRouteThreads;
+          switch (m) {
+            case 1: hash_compacted<1>(pd, buf, n_cta, tid, lane, warp, s_vw); break;
+            case 2: hash_compacted<2>(pd, buf, n_cta, tid, lane, warp, s_vw); break;
+            case 3: hash_compacted<3>(pd, buf, n_cta, tid, lane, warp, s_vw); break;
+            case 4: hash_compacted<4>(pd, buf, n_cta, tid, lane, warp, s_vw); break;
+            case 5: hash_compacted<5>(pd, buf, n_cta, tid, lane, warp, s_vw); break;
+            default: hash_compacted<6>(pd, buf, n_cta, tid, lane, warp, s_vw); break;
           }
+          __syncthreads();
+          const uint32_t w0 = c ? s_vw[off >> 5] : 0u;
+          const uint32_t w1 = (c && ((off & 31u) + c > 32u)) ? s_vw[(off >> 5) + 1] : 0u;
+          const uint32_t fb = __funnelshift_r(w0, w1, off & 31u) & ((1u << c) - 1u);  // this thread's entries
+          uint32_t fail = 0, t = 0;
+#pragma unroll
+          for (int j = 0; j < kRouteItems; ++j) {
+            if ((mask >> j) & 1u) {
+              fail |= ((fb >> t) & 1u) << j;
+              ++t;
+            }
+          }
+          mask &= ~fail;
         }
-        mask &= ~fail;
-        __syncwarp();  // the buffer is rewritten by the next predicate of the run
-      } else if (mask) {
+        __syncthreads();  // s_cw / s_cids / s_vw are reused by the next predicate or tile
+      }
+      if (!compacted && mask) {
         if (pd.kind == kLabelEq) {
           const uint32_t want = static_cast<uint32_t>(pd.label_value) & 0xFFFFu;
 #pragma unroll
@@ -346,7 +384,7 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K1_MINB) hydro_route_kern
       }
       const long long t1 = clock64();
       if (pd.cache_known) {
-        if (pd.cache_fill && todo) {  // record the verdicts this predicate computed
+        if ((pd.cache_fill || p.force_fill) && todo) {  // record the verdicts this predicate computed
 #pragma unroll
           for (int j = 0; j < kRouteItems; ++j) {
             if (((todo >> j) & 1u) && ids[j] < pd.cache_cap) {
@@ -767,4 +805,17 @@ __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, i
     uint8_t* dst = w_tiled + (static_cast<uint64_t>(kb) * n_pad + n) * 128 + ((c ^ (n & 7)) << 4);
     *reinterpret_cast<uint4*>(dst) = v;
   }
+}
+
+// Host-side entry points (the kernel template stays inside this translation unit).
+void hydro_route_launch(const RouteParams& r, int grid, cudaStream_t stream, bool compact) {
+  if (compact) hydro_route_kernel<true><<<grid, kRouteThreads, 0, stream>>>(r);
+  else hydro_route_kernel<false><<<grid, kRouteThreads, 0, stream>>>(r);
+}
+
+int hydro_route_occupancy(bool compact) {
+  int occ = 1;
+  if (compact) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hydro_route_kernel<true>, kRouteThreads, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hydro_route_kernel<false>, kRouteThreads, 0);
+  return occ < 1 ? 1 : occ;
 }

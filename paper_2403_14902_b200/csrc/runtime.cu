@@ -88,6 +88,7 @@ struct hydro_ctx {
   bool own_stream = false;
   int num_sms = 0;
   int k1_occ = 1;
+  bool k1_compact = false;  // a HASH predicate expensive enough for K1's compaction path
   std::vector<PredHost> preds;
   bool frozen = false;
   bool warmup_pending = true;
@@ -115,6 +116,7 @@ struct hydro_ctx {
   bool fixed_order_set = false;
   bool has_area = false;
   bool has_linear = false, has_mlp = false;
+  std::vector<PredDev> pd_host;  // the device predicate table as uploaded at freeze
   // timing
   bool timing = false;
   std::vector<TimedLaunch> timed;
@@ -245,8 +247,7 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
     ctx->own_stream = true;
   }
   CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->k1_occ, hydro_route_kernel, kRouteThreads, 0));
-  if (ctx->k1_occ < 1) ctx->k1_occ = 1;
+  ctx->k1_occ = hydro_route_occupancy(false);
   CU(hydro_classifier_configure());
   CU(cudaMalloc(&ctx->st, sizeof(DevState)));
   CU(cudaMemset(ctx->st, 0, sizeof(DevState)));
@@ -372,7 +373,10 @@ extern "C" {
 
 hydro_status hydro_cache_enable(hydro_ctx* ctx, int32_t k, uint64_t id_capacity, int32_t fill) {
   if (!ctx) return set_err(HYDRO_EINVAL, "NULL argument");
-  if (ctx->frozen) return set_err(HYDRO_ESTATE, "cache_enable after the first submit");
+  if (ctx->frozen) {  // allowed between batches once nothing is in flight
+    for (const Slot& sl : ctx->slots)
+      if (sl.busy) return set_err(HYDRO_ESTATE, "cache_enable with uncollected batches in flight");
+  }
   if (k < 0 || k >= static_cast<int32_t>(ctx->preds.size())) return set_err(HYDRO_EINVAL, "bad pred id");
   PredHost& ph = ctx->preds[k];
   if (is_classifier(ph.desc.kind)) return set_err(HYDRO_EINVAL, "verdict caches are for LABEL_EQ / HASH predicates");
@@ -386,6 +390,14 @@ hydro_status hydro_cache_enable(hydro_ctx* ctx, int32_t k, uint64_t id_capacity,
   CU(cudaStreamSynchronize(ctx->stream));
   ph.cache_cap = id_capacity;
   ph.cache_fill = fill ? 1 : 0;
+  if (ctx->frozen) {  // refresh the device predicate table entry
+    PredDev& q = ctx->pd_host[k];
+    q.cache_known = ph.cache_known;
+    q.cache_pass = ph.cache_pass;
+    q.cache_cap = ph.cache_cap;
+    q.cache_fill = ph.cache_fill;
+    CU(cudaMemcpy(ctx->preds_dev + k, &q, sizeof(PredDev), cudaMemcpyHostToDevice));
+  }
   return HYDRO_OK;
 }
 
@@ -457,6 +469,10 @@ static hydro_status freeze(hydro_ctx* ctx) {
   h.cost_source = ctx->cfg.cost_source;
   h.gamma = ctx->cfg.decay_gamma;
   h.prior = ctx->cfg.prior_selectivity;
+  for (const PredHost& ph : ctx->preds)
+    if (ph.desc.kind == HYDRO_PRED_HASH && ph.desc.units >= kCompactUnits && ph.desc.units_per_area <= 0)
+      ctx->k1_compact = true;
+  ctx->k1_occ = hydro_route_occupancy(ctx->k1_compact);
   const double k1_norm = 1.0 / (256.0 * static_cast<double>(ctx->k1_occ) * (kRouteThreads / 32));
   std::vector<PredDev> pd(kMaxPred);
   for (int k = 0; k < P; ++k) {
@@ -511,6 +527,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
   build_sched(h.kind, h.order, P, h.sched);
   CU(cudaMemcpy(ctx->st, &h, sizeof(h), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(ctx->preds_dev, pd.data(), sizeof(PredDev) * kMaxPred, cudaMemcpyHostToDevice));
+  ctx->pd_host = pd;
   // workspace
   ctx->list_stride = (maxb + 7) & ~7ull;
   CU(cudaMalloc(&ctx->lists, sizeof(uint32_t) * ctx->list_stride * (P + 1)));
@@ -618,7 +635,7 @@ static int route_grid(hydro_ctx* ctx, uint64_t positions) {
 
 static hydro_status launch_route(hydro_ctx* ctx, const RouteParams& r, uint64_t max_positions) {
   const int grid = route_grid(ctx, max_positions);
-  return timed_launch(ctx, 0, [&] { hydro_route_kernel<<<grid, kRouteThreads, 0, ctx->stream>>>(r); });
+  return timed_launch(ctx, 0, [&] { hydro_route_launch(r, grid, ctx->stream, ctx->k1_compact); });
 }
 
 static hydro_status launch_compact(hydro_ctx* ctx, const CompactParams& c, uint64_t max_positions) {
@@ -996,6 +1013,28 @@ hydro_status hydro_debug_linear(hydro_ctx* ctx, int32_t k, const hydro_tuples* t
   c.collect_stats = 0;
   if ((s = launch_cls(ctx, c, static_cast<uint64_t>(t->n), ctx->preds[k].desc.kind == HYDRO_PRED_MLP)) != HYDRO_OK)
     return s;
+  CU(cudaStreamSynchronize(ctx->stream));
+  return check_sticky(ctx);
+}
+
+hydro_status hydro_cache_fill(hydro_ctx* ctx, int32_t k, const hydro_tuples* t) {
+  if (!ctx || !t) return set_err(HYDRO_EINVAL, "NULL argument");
+  if (k < 0 || k >= static_cast<int32_t>(ctx->preds.size())) return set_err(HYDRO_EINVAL, "bad pred id");
+  if (!ctx->preds[k].cache_known) return set_err(HYDRO_EINVAL, "no verdict cache on this predicate (hydro_cache_enable)");
+  if (!t->on_device) return set_err(HYDRO_EINVAL, "cache_fill needs device tuples");
+  if (t->n < 0 || t->n > ctx->cfg.max_batch_tuples) return set_err(HYDRO_EINVAL, "bad n");
+  hydro_status s = freeze(ctx);
+  if (s != HYDRO_OK) return s;
+  if (t->n == 0) return HYDRO_OK;
+  RouteParams r = route_base(ctx, t->id, t->frame_id, reinterpret_cast<const uint64_t*>(t->bbox), t->label);
+  r.dispatch = 0;
+  r.explicit_pred = k;
+  r.range_base = 0;
+  r.range_n = static_cast<uint32_t>(t->n);
+  r.bitmap_out = ctx->warm_bits;
+  r.collect_stats = 0;
+  r.force_fill = 1;
+  if ((s = launch_route(ctx, r, static_cast<uint64_t>(t->n))) != HYDRO_OK) return s;
   CU(cudaStreamSynchronize(ctx->stream));
   return check_sticky(ctx);
 }

@@ -80,6 +80,7 @@ _SIGS = {
     "hydro_set_fixed_order": ([_P, C.POINTER(C.c_int32), C.c_int32], C.c_int32),
     "hydro_cache_enable": ([_P, C.c_int32, C.c_uint64, C.c_int32], C.c_int32),
     "hydro_cache_put": ([_P, C.c_int32, _P, _P, C.c_int64, C.c_int32], C.c_int32),
+    "hydro_cache_fill": ([_P, C.c_int32, C.POINTER(hydro_tuples)], C.c_int32),
     "hydro_submit_batch": ([_P, C.POINTER(hydro_tuples), C.POINTER(C.c_int64)], C.c_int32),
     "hydro_batch_count": ([_P, C.c_int64, C.POINTER(C.c_int64)], C.c_int32),
     "hydro_collect_results": ([_P, C.c_int64, _P, _P, C.c_int64, C.POINTER(C.c_int64), C.c_int32], C.c_int32),
@@ -160,6 +161,10 @@ def hydro_cache_put(ctx, pred_id: int, ids, verdicts, on_device: bool):
     """ids: uint64-compatible (torch int64) 1-D, verdicts: uint8/bool 1-D, same length."""
     _check(lib().hydro_cache_put(ctx, pred_id, ids.data_ptr(), verdicts.data_ptr(), int(ids.numel()),
                                  1 if on_device else 0))
+
+
+def hydro_cache_fill(ctx, pred_id: int, tup: hydro_tuples):
+    _check(lib().hydro_cache_fill(ctx, pred_id, C.byref(tup)))
 
 
 def hydro_set_fixed_order(ctx, order: Sequence[int]):
@@ -367,6 +372,10 @@ class Eddy:
 
     def cache_enable(self, pred_id: int, id_capacity: int, fill: bool = False):
         hydro_cache_enable(self.ctx, pred_id, id_capacity, fill)
+
+    def cache_fill(self, pred_id: int, tuples):
+        """Evaluates pred_id alone on a device batch and caches its verdicts (UC2's Q1 / Q2)."""
+        hydro_cache_fill(self.ctx, pred_id, make_tuples_struct(tuples.id, tuples.frame_id, tuples.bbox, tuples.label))
 
     def cache_put(self, pred_id: int, ids, verdicts):
         """Records verdicts of pred_id for tuple ids (torch tensors on the host or the GPU)."""

@@ -462,3 +462,32 @@ def test_uc2_reuse_aware_routing(fill):
         # tuples a predicate never saw in pass 1 (dropped earlier under that batch's order) may run now
         assert computed < 0.5 * sum(sum(i["tuples_computed"]) for i in infos), computed
     e.close()
+
+
+def test_uc2_cache_fill_by_exploratory_queries():
+    """The caches filled the way UC2 fills them: each detector stand-in is
+    evaluated alone on its id range (hydro_cache_fill), then the recurrent query reuses them:
+    rows exact, orders and evaluated counts as with oracle-provided verdicts."""
+    from synth import UC2_CACHED
+
+    w = workload("uc2")
+    t = w.tuples()
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, None)
+    e = make_eddy(w, None, policy="reuse", cost_source="declared", warmup=0, max_batch=1000)
+    tid = t.id.numpy()
+    for k in range(2):
+        e.cache_enable(k, 1 << 15)
+        lo, hi = UC2_CACHED[k][0]
+        sel = np.where((tid > lo) & (tid < hi))[0]
+        for a in range(0, len(sel), 1000):
+            e.cache_fill(k, t.select(torch.from_numpy(sel[a:a + 1000])).to("cuda"))
+    ids, bbs, infos = run_stream(e, t.to("cuda"), 1000)
+    _assert_rows(ids, bbs, ref_ids, ref_bbox)
+    for b, info in enumerate(infos):
+        bid = tid[b * 1000:(b + 1) * 1000]
+        hits = [O.cache_hit_rate(bid, UC2_CACHED[k]) for k in range(2)]
+        assert info["order_used"] == O.reuse_order([64.0, 64.0], hits)
+    total_in = sum(sum(i["tuples_in"]) for i in infos)
+    total_comp = sum(sum(i["tuples_computed"]) for i in infos)
+    assert total_comp < total_in
+    e.close()
