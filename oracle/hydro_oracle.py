@@ -191,6 +191,70 @@ def mlp_logits(pred: Dict, x: np.ndarray) -> np.ndarray:
     return h @ W2.T + b2[None, :]
 
 
+# --------------------------------------------------------------------------------------
+# HSV colour heuristic (DogColorClassifier; R27)
+
+# inclusive (H, S, V) boxes in OpenCV's 8-bit convention (H in [0, 180), S, V in [0, 255]);
+# class c is the union of its boxes; only red's range is printed in the paper
+HSV_COLOURS = ["red", "black", "gray", "yellow", "green", "blue", "purple", "pink", "white", "other"]
+HSV_BOXES = [
+    [((0, 50, 70), (9, 255, 255)), ((170, 50, 70), (179, 255, 255))],  # red (PAPER.md:395 + hue wrap)
+    [((0, 0, 0), (179, 255, 30))],                                     # black
+    [((0, 0, 31), (179, 18, 230))],                                    # gray
+    [((20, 50, 70), (34, 255, 255))],                                  # yellow
+    [((35, 50, 70), (89, 255, 255))],                                  # green
+    [((90, 50, 70), (128, 255, 255))],                                 # blue
+    [((129, 50, 70), (158, 255, 255))],                                # purple
+    [((159, 50, 70), (169, 255, 255))],                                # pink
+    [((0, 0, 231), (179, 18, 255))],                                   # white
+]
+
+
+def _div_round_half_up(num: np.ndarray, den: np.ndarray) -> np.ndarray:
+    """floor(num / den + 1/2) for integer arrays, den > 0 (exact integer arithmetic)."""
+    return np.floor_divide(2 * num + den, 2 * den)
+
+
+def rgb_to_hsv_u8(rgb: np.ndarray) -> np.ndarray:
+    """8-bit RGB -> 8-bit HSV (R27, OpenCV's convention): V = max, S = round(255 (V - min) / V),
+    H = round(30 (G - B) / d), 60 + round-arg ..., i.e. hue in degrees / 2, tested R then G then B."""
+    c = np.asarray(rgb, dtype=np.int64)
+    R, G, B = c[..., 0], c[..., 1], c[..., 2]
+    V = np.maximum(np.maximum(R, G), B)
+    m = np.minimum(np.minimum(R, G), B)
+    d = V - m
+    S = np.where(V == 0, 0, _div_round_half_up(255 * d, np.maximum(V, 1)))
+    num = np.where(V == R, 30 * (G - B), np.where(V == G, 60 * d + 30 * (B - R), 120 * d + 30 * (R - G)))
+    H = np.where(d == 0, 0, _div_round_half_up(num, np.maximum(d, 1)))
+    H = np.mod(H, 180)
+    return np.stack([H, S, V], axis=-1)
+
+
+def hsv_class(hsv: np.ndarray) -> np.ndarray:
+    """Colour class per pixel: the first box containing it, else 9 ('other')."""
+    out = np.full(hsv.shape[:-1], 9, dtype=np.int64)
+    for c in range(len(HSV_BOXES) - 1, -1, -1):  # reverse so the lowest class index wins overlaps
+        inside = np.zeros(hsv.shape[:-1], dtype=bool)
+        for lo, hi in HSV_BOXES[c]:
+            inside |= np.all((hsv >= np.array(lo)) & (hsv <= np.array(hi)), axis=-1)
+        out = np.where(inside, c, out)
+    return out
+
+
+def hsv_counts(crops_u8: np.ndarray) -> np.ndarray:
+    """Per crop the number of pixels of each of the 10 classes (crops [n, 64, 64, 3] u8)."""
+    cls = hsv_class(rgb_to_hsv_u8(crops_u8)).reshape(len(crops_u8), -1)
+    return np.stack([(cls == c).sum(axis=1) for c in range(10)], axis=1)
+
+
+def hsv_verdict(pred: Dict, frames, frame_id, bbox, return_counts=False):
+    """DogColorClassifier(Crop(frame, bbox)) = colour: the class with most pixels of the 64x64
+    nearest crop (lowest index on ties) equals the target (R27)."""
+    counts = hsv_counts(crop_nearest(frames, frame_id, bbox))
+    v = argmax_first(counts.astype(np.float64)) == int(pred["target"])
+    return (v, counts) if return_counts else v
+
+
 def argmax_first(z: np.ndarray) -> np.ndarray:
     """argmax over classes, lowest index on ties (R12)."""
     best = np.zeros(z.shape[0], dtype=np.int64)
@@ -241,6 +305,8 @@ def predicate_verdict(pred: Dict, tup: Dict[str, np.ndarray], frames=None) -> np
         return hash_verdict(pred, tup["id"], tup["bbox"])
     if kind in ("linear", "mlp"):
         return linear_verdict(pred, frames, tup["frame_id"], tup["bbox"])
+    if kind == "hsv":
+        return hsv_verdict(pred, frames, tup["frame_id"], tup["bbox"])
     raise ValueError(kind)
 
 

@@ -39,6 +39,10 @@ _MULT = 0x45D9F3B  # < 2**27, so (x < 2**32) * _MULT < 2**59 fits int64
 # stream ids
 S_LABEL, S_LABEL2, S_WOCT, S_WOFF, S_HOCT, S_HOFF, S_X, S_Y, S_FRAME, S_WEIGHT = range(1, 11)
 S_W1, S_W2 = 11, 12
+S_BLOCK, S_NOISE = 13, 14
+# palette of the coloured frame pool (RGB; one per HSV class of DESIGN.md R27, plus orange)
+PALETTE = [(200, 30, 30), (15, 15, 15), (128, 128, 128), (220, 200, 40), (40, 160, 40), (40, 60, 200),
+           (130, 40, 160), (230, 120, 170), (240, 240, 240), (200, 120, 40)]
 
 CROP = 64
 K_FEATURES = CROP * CROP * 3  # 12288
@@ -263,6 +267,26 @@ def linear_pred(seed, n_classes, target, selectivity, crop_mode="nearest", decla
                 calib=meta)
 
 
+def make_color_frames(seed: int, n_frames: int, h: int, w: int, device="cpu", block: int = 16) -> torch.Tensor:
+    """Frames of 16x16 blocks, each a palette colour (drawn per block) plus uniform noise in
+    [-8, 8] per channel: crops cover a few blocks, so the HSV heuristic has a dominant colour."""
+    f = torch.arange(n_frames, dtype=torch.int64, device=device)[:, None, None]
+    y = torch.arange(h, dtype=torch.int64, device=device)[None, :, None]
+    x = torch.arange(w, dtype=torch.int64, device=device)[None, None, :]
+    blk = (f * ((h + block - 1) // block) + y // block) * ((w + block - 1) // block) + x // block
+    pal = torch.tensor(PALETTE, dtype=torch.int64, device=device)
+    base = pal[gen_u32(seed, S_BLOCK, blk) % len(PALETTE)]                      # [F, H, W, 3]
+    pix = (f * h + y) * w + x
+    ch = torch.arange(3, dtype=torch.int64, device=device)
+    noise = gen_u32(seed, S_NOISE, pix[..., None] * 3 + ch) % 17 - 8
+    return (base + noise).clamp(0, 255).to(torch.uint8)
+
+
+def hsv_pred(target: int, selectivity: float, declared_cost=50.0, name=None):
+    return dict(kind="hsv", target=target, n_classes=10, crop_mode="nearest", declared_cost=declared_cost,
+                declared_selectivity=float(selectivity), name=name or f"hsv={target}")
+
+
 def mlp_pred(seed, n_classes, target, selectivity, hidden=512, declared_cost=1000.0, name=None):
     w1, b1, w2, b2, meta = make_mlp_head(seed, hidden, n_classes, target, selectivity)
     return dict(kind="mlp", weight=w1, bias=b1, weight2=w2, bias2=b2, hidden=hidden, target=target,
@@ -285,6 +309,7 @@ class Workload:
     batch_tuples: int = 1 << 20
     warmup_tuples: int = 65536
     notes: str = ""
+    frame_kind: str = "noise"  # "noise" (uniform u8) or "color" (palette blocks, make_color_frames)
 
     def tuples(self, id_start=0, n=None, device="cpu") -> Tuples:
         return make_tuples(self.seed, id_start, self.n if n is None else n, n_frames=self.n_frames,
@@ -292,12 +317,15 @@ class Workload:
                            n_octaves=self.n_octaves, device=device)
 
     def frames(self, device="cpu", frame_ids=None) -> torch.Tensor:
+        if self.frame_kind == "color":
+            f = make_color_frames(self.seed, self.n_frames, self.frame_h, self.frame_w, device=device)
+            return f if frame_ids is None else f[frame_ids]
         return make_frames(self.seed, self.n_frames, self.frame_h, self.frame_w, device=device,
                            frame_ids=frame_ids)
 
     @property
     def needs_frames(self) -> bool:
-        return any(p["kind"] in ("linear", "mlp") for p in self.preds)
+        return any(p["kind"] in ("linear", "mlp", "hsv") for p in self.preds)
 
 
 SEED = 20240321
@@ -340,6 +368,12 @@ def workload(name: str, *, n: Optional[int] = None, small: bool = False) -> Work
                  linear_pred(SEED + 2, 10, 1, 0.633, name="colour=black")]
         return Workload("mlp", SEED, n or 1_000_000, nf, fh, fw, preds, w_min=wmin,
                         notes="cfg2 with a 12288-512-120 MLP breed head")
+    if name == "hsv":  # the dog query with DogColorClassifier as the HSV heuristic
+        preds = [label_pred(),
+                 linear_pred(SEED + 1, 120, 57, 0.254, name="breed=great dane"),
+                 hsv_pred(1, 0.1, name="colour=black (hsv)")]
+        return Workload("hsv", SEED, n or 1_000_000, nf, fh, fw, preds, w_min=wmin, frame_kind="color",
+                        notes="cfg2 with the HSV colour heuristic on a coloured-block frame pool")
     if name == "uc2":  # PAPER.md:562-605 reuse-aware routing, HASH stand-ins for the two detectors
         preds = [hash_pred(SEED + 11, 0.5, units=64, declared_cost=64.0, name="ObjectDetector 'person'"),
                  hash_pred(SEED + 12, 0.5, units=64, declared_cost=64.0, name="HardHatDetector 'no hardhat'")]

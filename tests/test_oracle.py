@@ -251,6 +251,62 @@ def test_mlp_all_negative_hidden_gives_bias_and_generated_selectivity():
     assert abs(v.mean() - 0.254) < 0.04
 
 
+# ----------------------------------------------------------------------------- HSV colour heuristic (f4, R27)
+
+
+def test_rgb_to_hsv_matches_colorsys():
+    """Against Python's colorsys (float HSV): V exact, S and H within one unit of
+    round(255 s) / round(180 h) (they differ only where the float rounding sees a .5 tie), and
+    exact on the primaries, the secondaries and greys."""
+    import colorsys
+
+    rng = np.random.default_rng(11)
+    rgb = rng.integers(0, 256, size=(20000, 3))
+    got = O.rgb_to_hsv_u8(rgb)
+    for (r, g, b), (H, S, V) in zip(rgb.tolist(), got.tolist()):
+        h, s_, v = colorsys.rgb_to_hsv(r / 255, g / 255, b / 255)
+        assert V == round(v * 255)
+        assert abs(S - s_ * 255) <= 0.5 + 1e-9
+        dh = abs(H - h * 180)
+        assert min(dh, 180 - dh) <= 0.5 + 1e-9, ((r, g, b), H, h * 180)
+    fixed = {(255, 0, 0): (0, 255, 255), (0, 255, 0): (60, 255, 255), (0, 0, 255): (120, 255, 255),
+             (255, 255, 0): (30, 255, 255), (0, 255, 255): (90, 255, 255), (255, 0, 255): (150, 255, 255),
+             (0, 0, 0): (0, 0, 0), (128, 128, 128): (0, 0, 128), (255, 255, 255): (0, 0, 255)}
+    for k, v in fixed.items():
+        assert tuple(O.rgb_to_hsv_u8(np.array(k)).tolist()) == v
+
+
+def test_hsv_boxes_disjoint_over_all_colours_and_paper_red():
+    """Every 8-bit RGB colour falls in at most one class box (so 'first box' = 'the box'), and the
+    paper's red range (0, 50, 70)-(9, 255, 255) classifies as red."""
+    v = np.arange(0, 256, 3)
+    rgb = np.stack(np.meshgrid(v, v, v, indexing="ij"), -1).reshape(-1, 3)
+    hsv = O.rgb_to_hsv_u8(rgb)
+    hits = np.zeros(len(rgb), dtype=np.int64)
+    for boxes in O.HSV_BOXES:
+        inside = np.zeros(len(rgb), dtype=bool)
+        for lo, hi in boxes:
+            inside |= np.all((hsv >= np.array(lo)) & (hsv <= np.array(hi)), axis=-1)
+        hits += inside
+    assert hits.max() == 1
+    assert O.hsv_class(np.array([[0, 50, 70], [9, 255, 255], [5, 200, 200]])).tolist() == [0, 0, 0]
+    assert O.hsv_class(np.array([[10, 200, 200], [0, 49, 200], [0, 200, 69]])).tolist() == [9, 9, 9]
+
+
+def test_hsv_counts_and_verdict_closed_forms():
+    """A crop of a constant-colour frame has all 4096 pixels in that colour's class; ties in the
+    counts go to the lowest class index."""
+    for rgb, cls in [((200, 30, 30), 0), ((15, 15, 15), 1), ((40, 60, 200), 5), ((240, 240, 240), 8),
+                     ((200, 120, 40), 9)]:
+        F = np.zeros((1, 96, 128, 3), np.uint8)
+        F[:] = rgb
+        t = make_tuples(4, 0, 5, n_frames=1, frame_h=96, frame_w=128, w_min=8)
+        tup = O.as_numpy_tuples(t)
+        v, c = O.hsv_verdict(dict(kind="hsv", target=cls), F, tup["frame_id"], tup["bbox"], return_counts=True)
+        assert np.all(c[:, cls] == 4096) and np.all(c.sum(1) == 4096) and v.all()
+    assert O.argmax_first(np.array([[3.0, 5.0, 5.0, 1.0]])).tolist() == [1]
+
+
 # ----------------------------------------------------------------------------- reuse-aware routing (f2)
 
 
