@@ -73,9 +73,13 @@ enum {
   HYDRO_PRED_LABEL_EQ = 0, /* label == label_value                                          */
   HYDRO_PRED_HASH = 1,     /* synthetic predicate with set selectivity and per-tuple cost (R5) */
   HYDRO_PRED_LINEAR = 2,   /* argmax(W . Crop(frame, bbox) + b) == target (R10-R14, R19)     */
-  HYDRO_PRED_MLP = 3       /* argmax(W2 . bf16(relu(W1 . Crop + b1)) + b2) == target: the
+  HYDRO_PRED_MLP = 3,      /* argmax(W2 . bf16(relu(W1 . Crop + b1)) + b2) == target: the
                               "small MLP classifier" of the north star (
                               stand-in for the ViT breed model; R25)  */
+  HYDRO_PRED_HSV = 4       /* DogColorClassifier as the paper implements it (
+                              R27): the HSV colour class with most pixels of the 64x64 nearest
+                              crop == target (0 red, 1 black, 2 gray, 3 yellow, 4 green, 5 blue,
+                              6 purple, 7 pink, 8 white, 9 other); no weights                */
 };
 
 enum { HYDRO_CROP_NEAREST = 0, HYDRO_CROP_AREA = 1 }; /* R10 */
@@ -283,7 +287,8 @@ hydro_status hydro_destroy(hydro_ctx* ctx);
 
 /* ---- debug hooks (tests) ---------------------------------------------------------------- */
 
-/* Runs predicate pred_id's classifier kernel (LINEAR or MLP) on every tuple of the DEVICE batch `tuples`
+/* Runs predicate pred_id's classifier kernel (LINEAR, MLP or HSV; for HSV the "logits" are the
+   10 colour-class pixel counts) on every tuple of the DEVICE batch `tuples`
    (no short-circuit, statistics untouched) and writes, when non-NULL, the f32 logits
    logits_out[n][n_classes] (device) and the bf16 crop features crops_out[n][HYDRO_FEATURES]
    (device, bf16 bits) plus the verdicts verdict_out[n] (device, uint8 0/1).  Synchronises. */

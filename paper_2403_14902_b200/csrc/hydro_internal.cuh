@@ -50,10 +50,11 @@ enum PredKind : int32_t {
   kLabelEq = HYDRO_PRED_LABEL_EQ,
   kHash = HYDRO_PRED_HASH,
   kLinear = HYDRO_PRED_LINEAR,
-  kMlp = HYDRO_PRED_MLP
+  kMlp = HYDRO_PRED_MLP,
+  kHsv = HYDRO_PRED_HSV
 };
 // classifier hops run in K4 (linear or MLP head); cheap hops run in K1
-__host__ __device__ inline bool is_classifier(int32_t kind) { return kind == kLinear || kind == kMlp; }
+__host__ __device__ inline bool is_classifier(int32_t kind) { return kind == kLinear || kind == kMlp || kind == kHsv; }
 
 struct PredDev {
   int32_t kind;
@@ -357,6 +358,8 @@ __global__ void hydro_compact_kernel(hydro::CompactParams p);
 cudaError_t hydro_classifier_configure();
 void hydro_classifier_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug, bool area);
 void hydro_mlp_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug);
+void hydro_hsv_launch(const hydro::ClsParams& c, uint64_t max_positions, int num_sms, cudaStream_t stream);
+int hydro_hsv_warps_per_sm();
 __global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode, uint32_t n_batch);
 __global__ void hydro_probe_kernel(hydro::DevState* st, const hydro::PredDev* preds, const uint64_t* id, uint32_t base,
                                    uint32_t n);

@@ -115,7 +115,7 @@ struct hydro_ctx {
   int32_t fixed_order[kMaxPred];
   bool fixed_order_set = false;
   bool has_area = false;
-  bool has_linear = false, has_mlp = false;
+  bool has_linear = false, has_mlp = false, has_hsv = false;
   std::vector<PredDev> pd_host;  // the device predicate table as uploaded at freeze
   // timing
   bool timing = false;
@@ -286,6 +286,12 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
     if (d->threshold[0] > (1ull << 32) || d->threshold[1] > (1ull << 32))
       return set_err(HYDRO_EINVAL, "threshold must be <= 2^32");
     if (d->units < 0 || d->units_per_area < 0) return set_err(HYDRO_EINVAL, "units must be >= 0");
+  } else if (d->kind == HYDRO_PRED_HSV) {
+    if (!ctx->cfg.frames) return set_err(HYDRO_EINVAL, "HSV predicate needs the frame pool in hydro_config");
+    if (d->target < 0 || d->target > 9) return set_err(HYDRO_EINVAL, "HSV target is a colour class in [0, 9]");
+    if (d->crop_mode != HYDRO_CROP_NEAREST) return set_err(HYDRO_EINVAL, "HSV supports HYDRO_CROP_NEAREST only");
+    ph.desc.n_classes = 10;
+    ctx->has_hsv = true;
   } else if (d->kind == HYDRO_PRED_MLP) {
     if (!ctx->cfg.frames) return set_err(HYDRO_EINVAL, "MLP predicate needs the frame pool in hydro_config");
     if (d->n_classes < 2 || d->n_classes > HYDRO_MAX_CLASSES) return set_err(HYDRO_EINVAL, "n_classes in [2, 128]");
@@ -480,7 +486,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
     h.kind[k] = d.kind;
     h.declared_cost[k] = d.declared_cost;
     h.declared_sel[k] = d.declared_selectivity;
-    h.cost_norm[k] = is_classifier(d.kind) ? 1.0 : k1_norm;
+    h.cost_norm[k] = d.kind == HYDRO_PRED_HSV ? 1.0 / hydro_hsv_warps_per_sm() : (is_classifier(d.kind) ? 1.0 : k1_norm);
     PredDev& q = pd[k];
     q.kind = d.kind;
     q.label_value = d.label_value;
@@ -644,12 +650,19 @@ static hydro_status launch_compact(hydro_ctx* ctx, const CompactParams& c, uint6
   return timed_launch(ctx, 3, [&] { hydro_compact_kernel<<<grid, kRouteThreads, 0, ctx->stream>>>(c); });
 }
 
-static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_positions, bool mlp = false) {
+// classifier kernel kinds: the linear head (K4), the MLP head (K4-MLP), the HSV heuristic (K4-HSV)
+enum ClsKind { kClsLinear = 0, kClsMlp = 1, kClsHsv = 2 };
+static ClsKind cls_kind_of(int32_t pred_kind) {
+  return pred_kind == HYDRO_PRED_MLP ? kClsMlp : (pred_kind == HYDRO_PRED_HSV ? kClsHsv : kClsLinear);
+}
+
+static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_positions, ClsKind kind = kClsLinear) {
   const uint64_t tiles = (max_positions + kTileM - 1) / kTileM;
   const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctx->num_sms)));
-  return timed_launch(ctx, mlp ? 4 : 1, [&] {
+  return timed_launch(ctx, kind == kClsMlp ? 4 : (kind == kClsHsv ? 5 : 1), [&] {
     const bool dbg = c.dbg_crops || c.dbg_logits || c.dbg_verdict;
-    if (mlp) hydro_mlp_launch(c, grid, ctx->stream, dbg);
+    if (kind == kClsMlp) hydro_mlp_launch(c, grid, ctx->stream, dbg);
+    else if (kind == kClsHsv) hydro_hsv_launch(c, max_positions, ctx->num_sms, ctx->stream);
     // kernel instantiation by context capability: AREA support only when an AREA head exists
     else hydro_classifier_launch(c, grid, ctx->stream, dbg, ctx->has_area);
   });
@@ -740,7 +753,7 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
         c.range_base = 0;
         c.range_n = static_cast<uint32_t>(warm);
         c.bits_out = wb;
-        if ((s = launch_cls(ctx, c, warm, ctx->preds[k].desc.kind == HYDRO_PRED_MLP)) != HYDRO_OK) return s;
+        if ((s = launch_cls(ctx, c, warm, cls_kind_of(ctx->preds[k].desc.kind))) != HYDRO_OK) return s;
       } else {
         RouteParams r = route_base(ctx, id, fr, bb, lab);
         r.dispatch = 0;
@@ -807,8 +820,9 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
       c.hop = h;
       c.range_base = rest_base;
       c.range_n = rest_n;
-      if (ctx->has_linear && (s = launch_cls(ctx, c, rest_n, false)) != HYDRO_OK) return s;
-      if (ctx->has_mlp && (s = launch_cls(ctx, c, rest_n, true)) != HYDRO_OK) return s;
+      if (ctx->has_linear && (s = launch_cls(ctx, c, rest_n, kClsLinear)) != HYDRO_OK) return s;
+      if (ctx->has_mlp && (s = launch_cls(ctx, c, rest_n, kClsMlp)) != HYDRO_OK) return s;
+      if (ctx->has_hsv && (s = launch_cls(ctx, c, rest_n, kClsHsv)) != HYDRO_OK) return s;
     }
     CompactParams k2 = compact_base(ctx, id, bb, sl);
     k2.dispatch = 1;
@@ -996,7 +1010,7 @@ hydro_status hydro_debug_linear(hydro_ctx* ctx, int32_t k, const hydro_tuples* t
                                 uint16_t* crops_out, uint8_t* verdict_out) {
   if (!ctx || !t) return set_err(HYDRO_EINVAL, "NULL argument");
   if (k < 0 || k >= static_cast<int32_t>(ctx->preds.size()) || !is_classifier(ctx->preds[k].desc.kind))
-    return set_err(HYDRO_EINVAL, "pred_id is not a LINEAR or MLP predicate");
+    return set_err(HYDRO_EINVAL, "pred_id is not a classifier (LINEAR, MLP or HSV) predicate");
   if (!t->on_device) return set_err(HYDRO_EINVAL, "debug_linear needs device tuples");
   if (t->n < 0 || t->n > ctx->cfg.max_batch_tuples) return set_err(HYDRO_EINVAL, "bad n");
   hydro_status s = freeze(ctx);
@@ -1011,7 +1025,7 @@ hydro_status hydro_debug_linear(hydro_ctx* ctx, int32_t k, const hydro_tuples* t
   c.dbg_crops = crops_out;
   c.dbg_verdict = verdict_out;
   c.collect_stats = 0;
-  if ((s = launch_cls(ctx, c, static_cast<uint64_t>(t->n), ctx->preds[k].desc.kind == HYDRO_PRED_MLP)) != HYDRO_OK)
+  if ((s = launch_cls(ctx, c, static_cast<uint64_t>(t->n), cls_kind_of(ctx->preds[k].desc.kind))) != HYDRO_OK)
     return s;
   CU(cudaStreamSynchronize(ctx->stream));
   return check_sticky(ctx);

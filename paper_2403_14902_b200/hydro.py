@@ -21,7 +21,7 @@ HYDRO_OK, HYDRO_EINVAL, HYDRO_ENOMEM, HYDRO_ECUDA, HYDRO_ENCCL, HYDRO_ESTATE, HY
     0, -1, -2, -3, -4, -5, -6, -7)
 POLICY = {"score": 0, "static": 1, "fixed": 2, "cost": 3, "selectivity": 4, "reuse": 5}
 COST_SOURCE = {"measured": 0, "declared": 1}
-PRED_KIND = {"label_eq": 0, "hash": 1, "linear": 2, "mlp": 3}
+PRED_KIND = {"label_eq": 0, "hash": 1, "linear": 2, "mlp": 3, "hsv": 4}
 CROP_MODE = {"nearest": 0, "area": 1}
 MAX_PRED = 8
 FEATURES = 12288
@@ -304,6 +304,10 @@ class Eddy:
             d.drift_id = int(p["drift_id"])
             d.units = int(p.get("units", 1))
             d.units_per_area = int(p.get("units_per_area", 0))
+        elif p["kind"] == "hsv":
+            d.n_classes = 10
+            d.target = int(p["target"])
+            d.crop_mode = CROP_MODE[p.get("crop_mode", "nearest")]
         elif p["kind"] in ("linear", "mlp"):
             w = p["weight"].contiguous()
             b = p["bias"].to(torch.float32).contiguous()

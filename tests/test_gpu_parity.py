@@ -491,3 +491,41 @@ def test_uc2_cache_fill_by_exploratory_queries():
     total_comp = sum(sum(i["tuples_computed"]) for i in infos)
     assert total_comp < total_in
     e.close()
+
+
+# ------------------------------------------------------------------- HSV colour heuristic (f4)
+
+def test_hsv_counts_and_verdicts():
+    """K4-HSV against the oracle (R27): the 10 colour-class pixel counts of every crop exact, and
+    so the verdicts (integer decisions on both sides).  1000 tuples = 32 bitmap words, ragged."""
+    w = workload("hsv", small=True, n=4000)
+    frames = w.frames()
+    n = 1000
+    t = w.tuples(n=n)
+    k = 2
+    e = make_eddy(w, frames.cuda(), policy="fixed", warmup=0, max_batch=4096)
+    counts = torch.full((n, 10), -1.0, device="cuda")
+    verdict = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    e.debug_linear(k, t.to("cuda"), counts, None, verdict)
+    tup = O.as_numpy_tuples(t)
+    v_ref, c_ref = O.hsv_verdict(w.preds[k], frames.numpy(), tup["frame_id"], tup["bbox"], return_counts=True)
+    assert np.array_equal(counts.cpu().numpy().astype(np.int64), c_ref)
+    assert np.array_equal(verdict.cpu().numpy().astype(bool), v_ref)
+    e.close()
+
+
+def test_hsv_query_end_to_end():
+    """The dog query with the HSV colour heuristic through the eddy (score policy, warmup,
+    several batches): rows and per-batch counters equal the oracle's exactly."""
+    w = workload("hsv", small=True, n=6000)
+    frames = w.frames()
+    t = w.tuples()
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, frames.numpy())
+    e = make_eddy(w, frames.cuda(), policy="score", warmup=1024, max_batch=2048)
+    ids, bbs, infos = run_stream(e, t.to("cuda"), 2048)
+    _assert_rows(ids, bbs, ref_ids, ref_bbox)
+    for b, info in enumerate(infos):
+        Vb = V[:, b * 2048:(b + 1) * 2048]
+        n_in, n_pass = expected_batch_counters(Vb, info["order_used"], 1024 if b == 0 else 0)
+        assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist()
+    e.close()
