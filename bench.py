@@ -39,6 +39,8 @@ K4_FEATURES = 12288
 K4_BYTES_PER_TUPLE = K4_FEATURES + 16
 WORKLOAD = ("cfg2: 1M dog-query detections per GPU per step; label='dog' AND breed(C=120) AND "
             "colour(C=10) linear heads on 64x64 nearest crops; 1024 x 720x1280x3 u8 frame pool")
+WORKLOAD_HSV = ("hsv (SURVEY.md §8(f) f4): cfg2 with DogColorClassifier as the paper's HSV heuristic on a "
+                "coloured-block frame pool (1024 x 720x1280x3), breed linear C=120; 1M detections per GPU per step")
 WORKLOAD_MLP = ("mlp (SURVEY.md §8(f) f1): cfg2 with the breed classifier as a 12288-512-120 MLP head "
                 "(bf16 hidden), colour linear C=10; 1M detections per GPU per step; 1024 x 720x1280x3 frames")
 
@@ -192,7 +194,8 @@ def run_gpu(args):
     if dist:
         dist.barrier()
     mlp = args.workload == "mlp"
-    w = workload("mlp" if mlp else "cfg2")
+    hsv = args.workload == "hsv"
+    w = workload("mlp" if mlp else ("hsv" if hsv else "cfg2"))
     frames = w.frames(device="cuda")
     uid = broadcast_unique_id(dist, rank, H.hydro_nccl_unique_id) if world > 1 else None
     stream = torch.cuda.current_stream()
@@ -222,6 +225,10 @@ def run_gpu(args):
 
     lin = [k for k, p in enumerate(w.preds) if p["kind"] == "linear"]
     mlps = [k for k, p in enumerate(w.preds) if p["kind"] == "mlp"]
+    hsvs = [k for k, p in enumerate(w.preds) if p["kind"] == "hsv"]
+
+    def hsv_in():
+        return sum(e.stats(k)["tuples_in"] for k in hsvs)
 
     def lin_in():
         return sum(e.stats(k)["tuples_in"] for k in lin)
@@ -251,11 +258,13 @@ def run_gpu(args):
     value = world * TUPLES_PER_STEP * args.steps / (ms / 1000.0)
 
     # ---- kernel timing pass (separate, untimed for `value`): K4 share + achieved bandwidth
-    in0, min0 = lin_in(), mlp_in()
+    in0, min0, hin0 = lin_in(), mlp_in(), hsv_in()
     e.set_kernel_timing(True)
     run_steps(args.steps, 2)
     k4_ms, k4_n = e.kernel_time(1)
     km_ms, km_n = e.kernel_time(4)
+    kh_ms, kh_n = e.kernel_time(5)
+    kh_tuples = hsv_in() - hin0
     km_tuples = mlp_in() - min0
     k1_ms, k1_n = e.kernel_time(0)
     k5_ms, k5_n = e.kernel_time(2)
@@ -344,11 +353,16 @@ def run_gpu(args):
                     "k2_ms_per_step": k2c_ms / args.steps,
                     "k1_ms_per_step": k1_ms / args.steps, "k4_ms_per_step": k4_ms / args.steps,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"}
+        if hsv:  # the HSV colour hop (K4-HSV) is ALU work: its own time and rate next to the linear hop
+            roofline.update({"hsv_ms_per_step": kh_ms / args.steps, "hsv_launches": kh_n,
+                             "hsv_kernel_tuples_per_s": kh_tuples / (kh_ms / 1000.0) if kh_ms > 0 else None,
+                             "share_of_step": (k4_ms) / max(k4_ms + kh_ms + k1_ms + k5_ms + k2c_ms, 1e-9)})
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-               "config": {"workload": WORKLOAD_MLP if mlp else WORKLOAD, "tuples_per_step": world * TUPLES_PER_STEP,
+               "config": {"workload": WORKLOAD_MLP if mlp else (WORKLOAD_HSV if hsv else WORKLOAD),
+                          "tuples_per_step": world * TUPLES_PER_STEP,
                           "batch_tuples": TUPLES_PER_STEP, "policy": "score (cost/(1-sel)), measured costs",
                           "l2": "inputs larger than L2: 2.83 GB frame pool + 6 rotating 22 MB tuple batches",
                           "parallelism": f"dp{world}", "final_order": [w.preds[k]["name"] for k in order],
@@ -521,7 +535,7 @@ def main():
     ap.add_argument("--impl", default="hydro", choices=["hydro", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute", "mlp", "uc2"],
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute", "mlp", "uc2", "hsv"],
                     help="cfg2 = the BASELINE metric (default); rroute = K1 HBM evidence run; "
                          "mlp = cfg2 with the 12288-512-120 MLP breed head (SURVEY.md §8(f) f1, tensor roofline)")
     args = ap.parse_args()

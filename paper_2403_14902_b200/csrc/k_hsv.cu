@@ -19,33 +19,35 @@ namespace {
 constexpr int kHsvThreads = 256;
 constexpr uint32_t kFullMask = 0xFFFFFFFFu;
 
-// round-half-up integer quotient floor(num / den + 1/2), den > 0, |2 num + den| < 2^24: exact
-// through one fp32 division (the rounded quotient cannot cross an integer boundary)
-__device__ __forceinline__ int div_round_half_up(int num, int den) {
-  return static_cast<int>(floorf(__fdiv_rn(static_cast<float>(2 * num + den), static_cast<float>(2 * den))));
+// floor(a / b) for b > 0, |a| < 2^22: an approximate reciprocal puts the quotient within 1 of the
+// floor, one remainder test corrects it (exact integer result)
+__device__ __forceinline__ int floor_div(int a, int b) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(static_cast<float>(b)));
+  int q = static_cast<int>(floorf(static_cast<float>(a) * r));
+  const int rem = a - q * b;
+  q += rem < 0 ? -1 : (rem >= b ? 1 : 0);
+  return q;
 }
+// round-half-up integer quotient floor(num / den + 1/2), den > 0
+__device__ __forceinline__ int div_round_half_up(int num, int den) { return floor_div(2 * num + den, 2 * den); }
 
-// 8-bit HSV class of one RGB pixel (R27): boxes are disjoint (pinned in tests/test_oracle.py)
+// 8-bit HSV class of one RGB pixel (R27); boxes are disjoint (pinned in tests/test_oracle.py).
+// Branch-free (selects only): neighbouring lanes' pixels take different paths.
 __device__ __forceinline__ uint32_t hsv_class_of(uint32_t R, uint32_t G, uint32_t B) {
   const int r = static_cast<int>(R), g = static_cast<int>(G), b = static_cast<int>(B);
   const int V = max(max(r, g), b), m = min(min(r, g), b), d = V - m;
-  const int S = V == 0 ? 0 : div_round_half_up(255 * d, V);
-  int H = 0;
-  if (d != 0) {
-    const int num = (V == r) ? 30 * (g - b) : (V == g) ? 60 * d + 30 * (b - r) : 120 * d + 30 * (r - g);
-    H = div_round_half_up(num, d);
-    H = H < 0 ? H + 180 : (H >= 180 ? H - 180 : H);
-  }
-  if (V <= 30) return 1;                                // black: (0,0,0)-(179,255,30)
-  if (S <= 18) return V <= 230 ? 2u : 8u;               // gray (V 31..230) / white (V 231..255)
-  if (S < 50 || V < 70) return 9;                       // other
-  if (H <= 9 || H >= 170) return 0;                     // red (with the hue wrap)
-  if (H < 20) return 9;                                 // orange -> other
-  if (H <= 34) return 3;                                // yellow
-  if (H <= 89) return 4;                                // green
-  if (H <= 128) return 5;                               // blue
-  if (H <= 158) return 6;                               // purple
-  return 7;                                             // pink (159..169)
+  const int S = V == 0 ? 0 : div_round_half_up(255 * d, max(V, 1));
+  const int num = (V == r) ? 30 * (g - b) : (V == g) ? 60 * d + 30 * (b - r) : 120 * d + 30 * (r - g);
+  int H = div_round_half_up(num, max(d, 1));
+  H = H < 0 ? H + 180 : (H >= 180 ? H - 180 : H);
+  H = d == 0 ? 0 : H;
+  // hue classes of chromatic pixels (S >= 50, V >= 70): red (with the hue wrap),
+  // orange -> other, yellow, green, blue, purple, pink
+  uint32_t hc = H <= 9 ? 0u : (H < 20 ? 9u : (H <= 34 ? 3u : (H <= 89 ? 4u : (H <= 128 ? 5u : (H <= 158 ? 6u : (H <= 169 ? 7u : 0u))))));
+  uint32_t cls = (S >= 50 && V >= 70) ? hc : 9u;
+  cls = S <= 18 ? (V <= 230 ? 2u : 8u) : cls;  // gray (V 31..230) / white (V 231..255)
+  return V <= 30 ? 1u : cls;                   // black: (0,0,0)-(179,255,30)
 }
 
 __device__ __forceinline__ uint32_t ldg32(const uint8_t* p) { return __ldg(reinterpret_cast<const uint32_t*>(p)); }
@@ -117,19 +119,31 @@ __global__ void __launch_bounds__(kHsvThreads) hydro_hsv_kernel(ClsParams p) {
       const uint32_t o0 = 3u * (tx + (((2u * lane + 1u) * tw) >> 7));
       const uint32_t o1 = 3u * (tx + (((2u * (lane + 32u) + 1u) * tw) >> 7));
       uint32_t c0 = 0, c1 = 0, c2 = 0;  // class counters, 4 x 8 bits per register
-      for (int dy = 0; dy < 64; ++dy) {
-        const uint8_t* row = frame + (ty + (((2u * dy + 1u) * th) >> 7)) * pitch;
+      constexpr int kRows = 8;           // crop rows in flight per step (16 pixel loads issued first)
+      for (int dy0 = 0; dy0 < 64; dy0 += kRows) {
+        uint32_t px[kRows][2];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const uint32_t o = k ? o1 : o0;
-          const uint32_t a = o & ~3u;
-          const uint32_t hi = (o & 3u) > 1u ? ldg32(row + a + 4) : 0u;  // only if the pixel straddles
-          const uint32_t px = __funnelshift_r(ldg32(row + a), hi, o << 3);
-          const uint32_t cls = hsv_class_of(px & 0xFF, (px >> 8) & 0xFF, (px >> 16) & 0xFF);
-          const uint32_t inc = 1u << ((cls & 3u) * 8u);
-          c0 += cls < 4 ? inc : 0u;
-          c1 += (cls >= 4 && cls < 8) ? inc : 0u;
-          c2 += cls >= 8 ? inc : 0u;
+        for (int rr = 0; rr < kRows; ++rr) {
+          const uint8_t* row = frame + (ty + (((2u * (dy0 + rr) + 1u) * th) >> 7)) * pitch;
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const uint32_t o = k ? o1 : o0;
+            const uint32_t a = o & ~3u;
+            const uint32_t hi = (o & 3u) > 1u ? ldg32(row + a + 4) : 0u;  // only if the pixel straddles
+            px[rr][k] = __funnelshift_r(ldg32(row + a), hi, o << 3);
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < kRows; ++rr) {
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const uint32_t q = px[rr][k];
+            const uint32_t cls = hsv_class_of(q & 0xFF, (q >> 8) & 0xFF, (q >> 16) & 0xFF);
+            const uint32_t inc = 1u << ((cls & 3u) * 8u);
+            c0 += cls < 4 ? inc : 0u;
+            c1 += (cls >= 4 && cls < 8) ? inc : 0u;
+            c2 += cls >= 8 ? inc : 0u;
+          }
         }
       }
       int best = -1, bc = 0;
