@@ -142,6 +142,7 @@ __device__ __forceinline__ void prefetch_line_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 #endif
+
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -561,7 +562,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
           if (!mr[r].valid) continue;
           const uint32_t sy = static_cast<uint32_t>(((2 * g + 1) * mr[r].h) >> 7);
           const uint8_t* a = p.frames + mr[r].row0 + sy * row_pitch + mr[r].seg_lo;
-#ifdef HYDRO_L2_PREFETCH  // measured slightly slower on B200 (line-granular overfetch, L2 pressure)
+#if defined(HYDRO_L2_PREFETCH)  // measured slightly slower on B200 (line-granular overfetch, L2 pressure)
           for (uint32_t c = 0; c < mr[r].seg_len; c += 128u) prefetch_line_l2(a + c);
 #else
           (void)a;
