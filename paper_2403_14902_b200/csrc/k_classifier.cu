@@ -131,6 +131,9 @@ __device__ __forceinline__ RowMeta load_meta(const ClsParams& p, const uint32_t*
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -326,6 +329,132 @@ __device__ __forceinline__ void convert_quad_area(const uint8_t* frames, uint32_
   }
 }
 
+// Wide-crop staging: lane j of a row copies the words around its 8 sampled pixels k = 8j .. 8j+7
+// to slot bytes [8k, 8k + 8) (the second word only when the pixel straddles it, so nothing past the
+// crop row is read).  Out of line: it must not cost the common path registers.
+__device__ __noinline__ void stage_wide_row(uint32_t dst, const uint8_t* row, uint32_t xw, uint32_t j) {
+  const uint32_t x0 = xw & 0xFFFFu, w = xw >> 16;
+  const uint8_t* base_row = row - ((3u * x0) & ~15u);  // frame row start (row = start + seg_lo)
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const uint32_t dx = 8u * j + t;
+    const uint32_t b = 3u * (x0 + (((2u * dx + 1u) * w) >> 7));
+    cp_async4(dst + 8u * dx, base_row + (b & ~3u));
+    if ((b & 3u) > 1u) cp_async4(dst + 8u * dx + 4u, base_row + (b & ~3u) + 4u);
+  }
+}
+
+// One M-tile of a converter warp: 64 K-groups (crop rows) of its 16 tuples (see converter_role).
+// A crop wider than a staging slot (w > 255 px) is staged as a gather instead of its contiguous
+// segment: for each of the 64 sampled pixels the two words around it (2 x 4-byte cp.async) go to
+// slot bytes [8k, 8k + 8), and its pixel offsets become 8k + (byte-in-word), so the conversion
+// itself is unchanged.
+template <bool kDbg, bool kArea, int kP, int kQD, bool kWide>
+__device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, const uint32_t* list_in, uint32_t count,
+                                             uint32_t tile, uint32_t crank, int cu, int lane, uint32_t slots, uint32_t a_ring,
+                                             uint32_t row_pitch, bool area, bool fp16, const RowMeta& mm,
+                                             uint32_t& gg) {
+  constexpr int kQS = kQD + 1;
+  const int r = lane >> 3, j = lane & 7;
+  const uint8_t* frames = p.frames;
+  const uint32_t my_src = mm.row0 + mm.seg_lo;                 // + sy * pitch per crop row
+  const bool my_wide = kWide && lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes);
+  // staged bytes per crop row: the segment, or (wide rows) a negative marker for the gather
+  const uint32_t my_len = (lane < 16 && mm.valid) ? (my_wide ? 0xFFFFFFFFu : mm.seg_len) : 0u;
+  const uint32_t my_h = static_cast<uint32_t>(mm.h);
+  const uint32_t my_xw = kWide ? static_cast<uint32_t>(mm.x0) | (static_cast<uint32_t>(mm.w) << 16) : 0u;
+  uint32_t po[4][4];
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int src = 4 * it + r;
+    const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src);
+    const uint32_t w = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src);
+    const uint32_t slo = __shfl_sync(0xFFFFFFFFu, mm.seg_lo, src);
+    const bool wide = kWide && __shfl_sync(0xFFFFFFFFu, my_wide, src);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t dx0 = 8u * j + 2u * q;
+      const uint32_t b0 = 3u * (x0 + (((2u * dx0 + 1u) * w) >> 7)), b1 = 3u * (x0 + (((2u * dx0 + 3u) * w) >> 7));
+      const uint32_t o0 = wide ? 8u * dx0 + (b0 & 3u) : b0 - slo;
+      const uint32_t o1 = wide ? 8u * (dx0 + 1u) + (b1 & 3u) : b1 - slo;
+      po[it][q] = o0 | (o1 << 16);
+    }
+  }
+  // Stage quad k = 4*g + it (rows 4*it .. 4*it+3 of this warp, crop row g) into slot k % kQS:
+  // lanes 8r .. 8r+7 copy row r's segment in 16-byte chunks j + 8c (c < 7: segments <= 784 B).
+  auto stage_quad = [&](int k, uint32_t slot) {
+    if (!area && k < kGroups * 4) {
+      const int g = k >> 2, it = k & 3;
+      const int src_lane = 4 * it + r;
+      const uint32_t len = __shfl_sync(0xFFFFFFFFu, my_len, src_lane);
+      const uint32_t off = __shfl_sync(0xFFFFFFFFu, my_src, src_lane);
+      const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
+      const uint32_t xw = kWide ? __shfl_sync(0xFFFFFFFFu, my_xw, src_lane) : 0u;  // (all lanes: before the branch)
+      const uint8_t* row = frames + (off + (((2u * g + 1u) * h) >> 7) * row_pitch);
+      const uint32_t dst = slots + slot * kQuadSlotBytes + r * kMaxSegBytes;
+      if (!kWide || len != 0xFFFFFFFFu) {
+        const uint32_t nch = len >> 4;
+#pragma unroll
+        for (int c = 0; c < 7; ++c)
+          if (j + 8u * c < nch) cp_async16(dst + 16u * j + 128u * c, row + 16u * j + 128u * c);
+      } else {  // wide crop (rare): gather this lane's 8 sampled pixels
+        stage_wide_row(dst, row, xw, j);
+      }
+    }
+    cp_async_commit();  // one group per quad (possibly empty) keeps wait_group counting uniform
+  };
+  uint32_t slot_stage = 0, slot_use = 0;
+#pragma unroll
+  for (int k = 0; k < kQD; ++k) {
+    stage_quad(k, slot_stage);
+    slot_stage = slot_stage + 1 == kQS ? 0 : slot_stage + 1;
+  }
+  for (int g = 0; g < kGroups; ++g, ++gg) {
+    const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph = (gg >> 1) & 1u;
+#pragma unroll
+    for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_wait(&ctrl->empty_a[set + kbr], aph ^ 1u);
+    const uint32_t a_set = a_ring + set * kAKBlockBytes;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      stage_quad(4 * g + it + kQD, slot_stage);
+      slot_stage = slot_stage + 1 == kQS ? 0 : slot_stage + 1;
+      cp_async_wait<kQD>();  // this thread's copies of quad k have landed
+      __syncwarp();                 // ... and every lane's
+      // rows past the tile's count convert stale bytes into A rows whose results are masked
+      const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * it + r);
+      const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kMaxSegBytes;
+      const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
+      uint16_t* dbg = (kDbg && p.dbg_crops && tile * kTileM + m < count)
+                          ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + m) * kFeatures + g * 192 + 24 * j
+                          : nullptr;
+      if (kArea && area) {
+        const int src_lane = 4 * it + r;
+        const uint32_t ar0 = __shfl_sync(0xFFFFFFFFu, mm.row0, src_lane);
+        const uint32_t ah = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.h), src_lane);
+        const uint32_t ax0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src_lane);
+        const uint32_t aw = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
+        if (fp16) convert_quad_area<true, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
+        else convert_quad_area<false, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
+      } else {
+        if (fp16) convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
+        else convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
+      }
+      slot_use = slot_use + 1 == kQS ? 0 : slot_use + 1;
+      __syncwarp();  // the slot is refilled kQD quads later
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) {
+        if (kP == 2 && crank != 0) mbar_arrive_leader(&ctrl->full_a[set + kbr]);
+        else mbar_arrive(&ctrl->full_a[set + kbr]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
 // Converter warps (shared by the linear and the MLP classifier kernels): cp.async-staged crop-row
 // segments -> pixels -> the swizzled K-major A ring, one K-group (crop row g of all 128 tuples of
 // the CTA's M-tile) at a time, full_a / empty_a handshake with the MMA issuer.
@@ -341,101 +470,20 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
   // instruction = 4 rows x 8 lanes x 8 output pixels).  Quad k's source segments are
   // copied (16-byte cp.async, coalesced per row) kQD quads ahead into fixed slots.
   const int cu = warp - kConvWarp0;
-  const int r = lane >> 3, j = lane & 7;  // row-in-quad and 8-pixel block (pixels 8j .. 8j+7)
   const uint32_t slots = staging_addr + static_cast<uint32_t>(cu) * (kQS * kQuadSlotBytes);
-  const uint8_t* frames = p.frames;
   uint32_t gg = 0;
   for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
     const uint32_t tile = unit * kP + crank;
     // rows' metadata: lane l < 16 holds row 16*cu + l
     const RowMeta mm = load_meta(p, list_in, base, tile * kTileM + cu * kConvRows + (lane & 15),
                                  lane < 16 ? count : 0u);
-    const uint32_t my_src = mm.row0 + mm.seg_lo;                 // + sy * pitch per crop row
-    const uint32_t my_len = (lane < 16 && mm.valid) ? mm.seg_len : 0u;
-    const uint32_t my_h = static_cast<uint32_t>(mm.h);
-    uint32_t po[4][4];
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int src = 4 * it + r;
-      const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src);
-      const uint32_t w = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src);
-      const uint32_t slo = __shfl_sync(0xFFFFFFFFu, mm.seg_lo, src);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t dx0 = 8u * j + 2u * q;
-        const uint32_t o0 = 3u * (x0 + (((2u * dx0 + 1u) * w) >> 7)) - slo;
-        const uint32_t o1 = 3u * (x0 + (((2u * dx0 + 3u) * w) >> 7)) - slo;
-        po[it][q] = o0 | (o1 << 16);
-      }
-    }
-    // Stage quad k = 4*g + it (rows 4*it .. 4*it+3 of this warp, crop row g) into slot k % kQS:
-    // lanes 8r .. 8r+7 copy row r's segment in 16-byte chunks j + 8c (c < 7: segments <= 784 B).
-    auto stage_quad = [&](int k, uint32_t slot) {
-      if (!area && k < kGroups * 4) {
-        const int g = k >> 2, it = k & 3;
-        const int src_lane = 4 * it + r;
-        const uint32_t len = __shfl_sync(0xFFFFFFFFu, my_len, src_lane);
-        const uint32_t off = __shfl_sync(0xFFFFFFFFu, my_src, src_lane);
-        const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
-        const uint8_t* src = frames + (off + (((2u * g + 1u) * h) >> 7) * row_pitch + 16u * j);
-        const uint32_t dst = slots + slot * kQuadSlotBytes + r * kMaxSegBytes + 16u * j;
-        const uint32_t nch = len >> 4;
-#pragma unroll
-        for (int c = 0; c < 7; ++c)
-          if (j + 8u * c < nch) cp_async16(dst + 128u * c, src + 128u * c);
-      }
-      cp_async_commit();  // one group per quad (possibly empty) keeps wait_group counting uniform
-    };
-    uint32_t slot_stage = 0, slot_use = 0;
-#pragma unroll
-    for (int k = 0; k < kQD; ++k) {
-      stage_quad(k, slot_stage);
-      slot_stage = slot_stage + 1 == kQS ? 0 : slot_stage + 1;
-    }
-    for (int g = 0; g < kGroups; ++g, ++gg) {
-      const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph = (gg >> 1) & 1u;
-#pragma unroll
-      for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_wait(&ctrl->empty_a[set + kbr], aph ^ 1u);
-      const uint32_t a_set = a_ring + set * kAKBlockBytes;
-#pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        stage_quad(4 * g + it + kQD, slot_stage);
-        slot_stage = slot_stage + 1 == kQS ? 0 : slot_stage + 1;
-        cp_async_wait<kQD>();  // this thread's copies of quad k have landed
-        __syncwarp();                 // ... and every lane's
-        // rows past the tile's count convert stale bytes into A rows whose results are masked
-        const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * it + r);
-        const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kMaxSegBytes;
-        const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
-        uint16_t* dbg = (kDbg && p.dbg_crops && tile * kTileM + m < count)
-                            ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + m) * kFeatures + g * 192 + 24 * j
-                            : nullptr;
-        if (kArea && area) {
-          const int src_lane = 4 * it + r;
-          const uint32_t ar0 = __shfl_sync(0xFFFFFFFFu, mm.row0, src_lane);
-          const uint32_t ah = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.h), src_lane);
-          const uint32_t ax0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src_lane);
-          const uint32_t aw = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
-          if (fp16) convert_quad_area<true, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
-          else convert_quad_area<false, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
-        } else {
-          if (fp16) convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
-          else convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
-        }
-        slot_use = slot_use + 1 == kQS ? 0 : slot_use + 1;
-        __syncwarp();  // the slot is refilled kQD quads later
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-#pragma unroll
-        for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) {
-          if (kP == 2 && crank != 0) mbar_arrive_leader(&ctrl->full_a[set + kbr]);
-          else mbar_arrive(&ctrl->full_a[set + kbr]);
-        }
-      }
-    }
-    cp_async_wait<0>();
+    // a tile with a crop wider than a staging slot (rare) runs the gather-staging variant
+    if (__any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes)))
+      convert_tile<kDbg, kArea, kP, kQD, true>(p, ctrl, list_in, count, tile, crank, cu, lane, slots, a_ring, row_pitch,
+                                               area, fp16, mm, gg);
+    else
+      convert_tile<kDbg, kArea, kP, kQD, false>(p, ctrl, list_in, count, tile, crank, cu, lane, slots, a_ring,
+                                                row_pitch, area, fp16, mm, gg);
   }
   if (kP == 2) {  // drain: both A sets released (the leader's commits land here)
     for (int e = 0; e < 2; ++e, ++gg) {

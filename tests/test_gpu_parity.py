@@ -529,3 +529,38 @@ def test_hsv_query_end_to_end():
         n_in, n_pass = expected_batch_counters(Vb, info["order_used"], 1024 if b == 0 else 0)
         assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist()
     e.close()
+
+
+def test_wide_crops_nearest_linear_and_mlp():
+    """Crops wider than a staging slot (w > 255 px, up to the full 1280-px frame width) on 720p
+    frames, mixed with ordinary ones in the same tiles: crops bit-exact and logits within 1e-2
+    for the linear breed head and the MLP head (their lanes read global memory, R10)."""
+    from synth import Tuples, make_frames, mlp_pred
+
+    F = make_frames(9, 4, 720, 1280)
+    n = 300
+    g = torch.Generator().manual_seed(5)
+    w = torch.randint(8, 256, (n,), generator=g)
+    w[::3] = torch.tensor([300, 700, 1000, 1280])[torch.arange(0, n, 3) % 4]
+    h = torch.randint(8, 720, (n,), generator=g)
+    x0 = (torch.rand(n, generator=g) * (1280 - w + 1).double()).long().clamp(min=0)
+    y0 = (torch.rand(n, generator=g) * (720 - h + 1).double()).long().clamp(min=0)
+    bbox = torch.stack([x0, y0, x0 + w, y0 + h], 1).to(torch.int16)
+    t = Tuples(torch.arange(n, dtype=torch.int64), torch.arange(n, dtype=torch.int32) % 4, bbox,
+               torch.full((n,), 16, dtype=torch.int16))
+    tup = O.as_numpy_tuples(t)
+    fr = F.numpy()
+    ref_crop = O.crop_nearest(fr, tup["frame_id"], tup["bbox"]).reshape(n, -1)
+    wl = workload("cfg2", small=True, n=100)
+    for p in (wl.preds[1], mlp_pred(20240330, 120, 57, 0.254)):
+        from paper_2403_14902_b200.hydro import Eddy
+
+        e = Eddy(frames=F.cuda(), policy="fixed", warmup_tuples=0, max_batch_tuples=4096)
+        k = e.add_predicate(p)
+        logits = torch.full((n, 120), float("nan"), device="cuda")
+        crops = torch.zeros((n, O.K_FEATURES), dtype=torch.int16, device="cuda")
+        e.debug_linear(k, t.to("cuda"), logits, crops, None)
+        assert np.array_equal(crops.view(torch.bfloat16).float().cpu().numpy(), ref_crop.astype(np.float32))
+        _, z_ref = O.linear_verdict(p, fr, tup["frame_id"], tup["bbox"], return_logits=True)
+        assert np.abs(logits.double().cpu().numpy() - z_ref).max() <= LOGIT_TOL
+        e.close()
