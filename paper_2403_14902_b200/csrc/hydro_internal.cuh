@@ -38,13 +38,29 @@ constexpr int kAKBlockBytes = kTileM * 128;                 // one 128 x 64 fp16
 constexpr int kARing = 6;                                   // A K-block stages (2 crop rows)
 constexpr int kBRing = 3;                                   // B K-block stages
 constexpr int kMaxSegBytes = 784;                           // 3*255 + 16-byte alignment slack
+// staging pitch of the 4 rows of a quad: 800 B = 200 words puts row r's segment 8r banks after
+// row 0's, which spreads the 4 rows' read windows (measured by simulation: 41.4 -> 40.0 LDS
+// wavefronts per quad with the interleaved pixel order below)
+constexpr int kSegPitch = 800;
 #ifndef HYDRO_QUAD_DEPTH
 #define HYDRO_QUAD_DEPTH 2
 #endif
 constexpr int kQuadDepth = HYDRO_QUAD_DEPTH;                // quads staged ahead per converter warp
 constexpr int kQuadSlots = kQuadDepth + 1;
-constexpr int kQuadSlotBytes = 4 * kMaxSegBytes;            // 4 rows x worst-case segment
+constexpr int kQuadSlotBytes = 4 * kSegPitch;               // 4 rows x worst-case segment
 constexpr int kClsSmemBytes = 232448;                       // 227 KB opt-in maximum
+
+// K order of the A operand inside one crop row (192 = 64 px x 3 ch elements):
+// converter lane j of a row produces output pixels dx = j + 8k (k = 0..7, interleaved so that the
+// 8 lanes of a row read 8 neighbouring pixels in every load instruction: one short shared-memory
+// window per row instead of 8 windows spread over the whole segment) and stores them as three
+// 16-byte chunks 3j .. 3j+2.  Position p of the crop row therefore holds feature
+//   (g*64 + dx) * 3 + ch  with  j = p / 24, k = (p % 24) / 3, ch = p % 3, dx = j + 8k.
+// The weight tiling applies the same permutation, so the contraction sum_k x_k W[c][k] is unchanged.
+__host__ __device__ __forceinline__ uint32_t crop_pos_feature(uint32_t g, uint32_t p) {
+  const uint32_t j = p / 24u, rem = p % 24u;
+  return (g * 64u + j + 8u * (rem / 3u)) * 3u + rem % 3u;
+}
 
 enum PredKind : int32_t {
   kLabelEq = HYDRO_PRED_LABEL_EQ,
@@ -366,4 +382,4 @@ __global__ void hydro_probe_kernel(hydro::DevState* st, const hydro::PredDev* pr
 __global__ void hydro_cache_put_kernel(uint32_t* known, uint32_t* pass, uint64_t cap, const uint64_t* ids,
                                        const uint8_t* verdicts, uint64_t n);
 __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,
-                                          int32_t k_features, int32_t to_fp16, int32_t* inexact);
+                                          int32_t k_features, int32_t to_fp16, int32_t crop_order, int32_t* inexact);

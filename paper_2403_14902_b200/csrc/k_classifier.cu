@@ -12,8 +12,9 @@
 //              K-block, tcgen05.commit releases A / B stages and publishes finished tiles
 //   warps 6-13 converters: stage each tuple's source row segment [3*x0 & ~15, roundup16(3*x1))
 //              of frame row sy = y0 + ((2dy+1)h)>>7 into shared memory with coalesced 16-byte
-//              cp.async (two 4-row quads ahead); then 8 lanes x 8 output pixels per crop row,
-//              4 rows per warp instruction; nearest-exact pixel selection sx = x0 + ((2dx+1)w)>>7,
+//              cp.async (two 4-row quads ahead); then 8 lanes x 8 output pixels per crop row
+//              (lane j: pixels j + 8k, the interleaved K order of crop_pos_feature), 4 rows per
+//              warp instruction; nearest-exact pixel selection sx = x0 + ((2dx+1)w)>>7,
 //              exact u8 -> fp16 (PRMT 0x64vv = 1024+v, HSUB2 1024) or bf16, st.shared into the
 //              128B-swizzled K-major A ring (conflict-free), fence.proxy.async, arrive.
 // The A operand never touches HBM: only the crop-row segments of the frames are read.
@@ -228,9 +229,9 @@ __device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
 
 }  // namespace
 
-// One quad (4 crop rows x 8 lanes) of output pixels: lane (r, j) produces pixels 8j .. 8j+7 of
-// row m from its staged segment `seg` (smem address).  po[q] packs the byte offsets (relative to
-// the segment) of pixels 8j+2q and 8j+2q+1.  Branch-free: both words around a pixel are always
+// One quad (4 crop rows x 8 lanes) of output pixels: lane (r, j) produces pixels j + 8k (k = 0..7,
+// the interleaved K order of crop_pos_feature) of row m from its staged segment `seg` (smem
+// address).  po[q] packs the byte offsets (relative to the segment) of pixels j+16q and j+16q+8.  Branch-free: both words around a pixel are always
 // read (the slots carry slack), the funnel shift uses the wrap mode (shift = 8*o mod 32).
 template <bool kFp16, bool kDbg>
 __device__ __forceinline__ void convert_quad(uint32_t seg, const uint32_t (&po)[4], uint32_t row_base, uint32_t j,
@@ -275,9 +276,9 @@ __device__ __forceinline__ void convert_quad(uint32_t seg, const uint32_t (&po)[
   if (kDbg && dbg) {
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      dbg[3 * kk + 0] = static_cast<uint16_t>(bf16_bits_of_byte(px[kk] & 0xFF));
-      dbg[3 * kk + 1] = static_cast<uint16_t>(bf16_bits_of_byte((px[kk] >> 8) & 0xFF));
-      dbg[3 * kk + 2] = static_cast<uint16_t>(bf16_bits_of_byte((px[kk] >> 16) & 0xFF));
+      dbg[24 * kk + 0] = static_cast<uint16_t>(bf16_bits_of_byte(px[kk] & 0xFF));  // pixel j + 8kk
+      dbg[24 * kk + 1] = static_cast<uint16_t>(bf16_bits_of_byte((px[kk] >> 8) & 0xFF));
+      dbg[24 * kk + 2] = static_cast<uint16_t>(bf16_bits_of_byte((px[kk] >> 16) & 0xFF));
     }
   }
 }
@@ -286,7 +287,7 @@ __device__ __forceinline__ void convert_quad(uint32_t seg, const uint32_t (&po)[
 // AREA crop (R10, cfg4): output pixel (dy, dx) is the mean over the bin
 // [y0 + dy*h//64, y0 + ceil((dy+1)h/64)) x [x0 + dx*w//64, x0 + ceil((dx+1)w/64)), one IEEE f32
 // division then bf16 round-to-nearest-even; the bf16 value is staged exactly (fp16 or bf16).
-// Bins are read straight from global memory (L1-cached); lane (r, j) makes pixels 8j .. 8j+7.
+// Bins are read straight from global memory (L1-cached); lane (r, j) makes pixels j + 8k, k = 0..7.
 template <bool kFp16, bool kDbg>
 __device__ __forceinline__ void convert_quad_area(const uint8_t* frames, uint32_t row0, uint32_t h, uint32_t x0,
                                                   uint32_t w, uint32_t pitch, uint32_t g, uint32_t row_base,
@@ -295,7 +296,7 @@ __device__ __forceinline__ void convert_quad_area(const uint8_t* frames, uint32_
   uint32_t half[24];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const uint32_t dx = 8u * j + k;
+    const uint32_t dx = j + 8u * k;
     const uint32_t xs = x0 + ((dx * w) >> 6), xe = x0 + (((dx + 1u) * w + 63u) >> 6);
     uint32_t s0 = 0, s1 = 0, s2 = 0;
     for (uint32_t y = ys; y < ye; ++y) {
@@ -317,7 +318,7 @@ __device__ __forceinline__ void convert_quad_area(const uint8_t* frames, uint32_
       const __nv_bfloat16 b = __float2bfloat16_rn(__fdiv_rn(static_cast<float>(sums[ch]), cnt));
       const uint32_t bbits = __bfloat16_as_ushort(b);
       half[3 * k + ch] = kFp16 ? static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__bfloat162float(b)))) : bbits;
-      if (kDbg && dbg) dbg[3 * k + ch] = static_cast<uint16_t>(bbits);
+      if (kDbg && dbg) dbg[24 * k + ch] = static_cast<uint16_t>(bbits);
     }
   }
 #pragma unroll
@@ -373,10 +374,10 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
     const bool wide = kWide && __shfl_sync(0xFFFFFFFFu, my_wide, src);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint32_t dx0 = 8u * j + 2u * q;
-      const uint32_t b0 = 3u * (x0 + (((2u * dx0 + 1u) * w) >> 7)), b1 = 3u * (x0 + (((2u * dx0 + 3u) * w) >> 7));
+      const uint32_t dx0 = j + 16u * q, dx1 = dx0 + 8u;  // pixels k = 2q, 2q+1 of lane j
+      const uint32_t b0 = 3u * (x0 + (((2u * dx0 + 1u) * w) >> 7)), b1 = 3u * (x0 + (((2u * dx1 + 1u) * w) >> 7));
       const uint32_t o0 = wide ? 8u * dx0 + (b0 & 3u) : b0 - slo;
-      const uint32_t o1 = wide ? 8u * (dx0 + 1u) + (b1 & 3u) : b1 - slo;
+      const uint32_t o1 = wide ? 8u * dx1 + (b1 & 3u) : b1 - slo;
       po[it][q] = o0 | (o1 << 16);
     }
   }
@@ -391,7 +392,7 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
       const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
       const uint32_t xw = kWide ? __shfl_sync(0xFFFFFFFFu, my_xw, src_lane) : 0u;  // (all lanes: before the branch)
       const uint8_t* row = frames + (off + (((2u * g + 1u) * h) >> 7) * row_pitch);
-      const uint32_t dst = slots + slot * kQuadSlotBytes + r * kMaxSegBytes;
+      const uint32_t dst = slots + slot * kQuadSlotBytes + r * kSegPitch;
       if (!kWide || len != 0xFFFFFFFFu) {
         const uint32_t nch = len >> 4;
 #pragma unroll
@@ -422,10 +423,10 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
       __syncwarp();                 // ... and every lane's
       // rows past the tile's count convert stale bytes into A rows whose results are masked
       const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * it + r);
-      const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kMaxSegBytes;
+      const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kSegPitch;
       const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
       uint16_t* dbg = (kDbg && p.dbg_crops && tile * kTileM + m < count)
-                          ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + m) * kFeatures + g * 192 + 24 * j
+                          ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + m) * kFeatures + g * 192 + 3 * j
                           : nullptr;
       if (kArea && area) {
         const int src_lane = 4 * it + r;

@@ -777,8 +777,10 @@ __global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode, uin
 // shared-memory image UMMA reads, so one 1-D bulk copy per stage lands it.  Rows >= C are 0.
 // to_fp16 = 1 re-encodes every weight as fp16 (identical value) and raises *inexact if any bf16
 // weight is not exactly representable in fp16 (the runtime then re-tiles as bf16).
+// crop_order = 1 (matrices over the 12288 crop features: linear heads, MLP W1) places feature
+// crop_pos_feature(g, p) at position p of crop row g, the order K4's converters produce.
 __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,
-                                          int32_t k_features, int32_t to_fp16, int32_t* inexact) {
+                                          int32_t k_features, int32_t to_fp16, int32_t crop_order, int32_t* inexact) {
   const uint64_t total = static_cast<uint64_t>(k_features / kKBlock) * n_pad * 8;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -788,7 +790,17 @@ __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, i
     const uint32_t kb = static_cast<uint32_t>(rowi / n_pad);
     uint4 v = make_uint4(0, 0, 0, 0);
     if (static_cast<int32_t>(n) < n_classes) {
-      v = *reinterpret_cast<const uint4*>(w + static_cast<uint64_t>(n) * k_features + kb * kKBlock + c * 8);
+      const uint16_t* wrow = w + static_cast<uint64_t>(n) * k_features;
+      if (crop_order) {
+        uint16_t e[8];
+        const uint32_t g = kb / kKBlocksPerGroup, p0 = (kb % kKBlocksPerGroup) * kKBlock + c * 8;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) e[t] = wrow[crop_pos_feature(g, p0 + t)];
+        v = make_uint4(e[0] | (static_cast<uint32_t>(e[1]) << 16), e[2] | (static_cast<uint32_t>(e[3]) << 16),
+                       e[4] | (static_cast<uint32_t>(e[5]) << 16), e[6] | (static_cast<uint32_t>(e[7]) << 16));
+      } else {
+        v = *reinterpret_cast<const uint4*>(wrow + kb * kKBlock + c * 8);
+      }
       if (to_fp16) {
         uint32_t* u = reinterpret_cast<uint32_t*>(&v);
         int bad = 0;

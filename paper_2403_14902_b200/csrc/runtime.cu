@@ -358,7 +358,7 @@ static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_devi
   int32_t* inexact = reinterpret_cast<int32_t*>(ctx->zero_word + 1);
   int32_t bad = 1;
   if (try_fp16) {
-    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 1, inexact);
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 1, k_features == kFeatures ? 1 : 0, inexact);
     ctx->launches += 1;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(&bad, inexact, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -366,7 +366,7 @@ static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_devi
   }
   *fp16 = bad ? 0 : 1;
   if (bad) {
-    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 0, inexact);
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 0, k_features == kFeatures ? 1 : 0, inexact);
     ctx->launches += 1;
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(ctx->stream));
