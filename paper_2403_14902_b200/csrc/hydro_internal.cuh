@@ -37,11 +37,17 @@ constexpr int kClsThreads = kClsWarps * 32;                 // 448
 constexpr int kAKBlockBytes = kTileM * 128;                 // one 128 x 64 fp16 K-block: 16 KB
 constexpr int kARing = 6;                                   // A K-block stages (2 crop rows)
 constexpr int kBRing = 3;                                   // B K-block stages
-constexpr int kMaxSegBytes = 784;                           // 3*255 + 16-byte alignment slack
 // staging pitch of the 4 rows of a quad: 800 B = 200 words puts row r's segment 8r banks after
 // row 0's, which spreads the 4 rows' read windows (measured by simulation: 41.4 -> 40.0 LDS
 // wavefronts per quad with the interleaved pixel order below)
-constexpr int kSegPitch = 800;
+#ifndef HYDRO_SEG_PITCH
+#define HYDRO_SEG_PITCH 800
+#endif
+constexpr int kSegPitch = HYDRO_SEG_PITCH;
+// longest crop-row segment staged contiguously (3*255 + 16-byte alignment slack when the pitch
+// allows); wider segments are staged as a 64-pixel gather (8 B per sampled pixel)
+constexpr int kMaxSegBytes = kSegPitch < 784 ? kSegPitch : 784;
+static_assert(kSegPitch % 16 == 0 && kMaxSegBytes >= 512, "staging pitch");
 #ifndef HYDRO_QUAD_DEPTH
 #define HYDRO_QUAD_DEPTH 2
 #endif

@@ -54,6 +54,11 @@ struct ClsCtrl {
   float bias1[HYDRO_MLP_HIDDEN_MAX];  // MLP: b1
 };
 
+// worst-case carve-up of both classifier kernels: [A ring][B ring (3 x 16 KB)][ctrl][staging]
+static_assert(1023 + kARing * kAKBlockBytes + 3 * 16384 + sizeof(ClsCtrl) + 15 +
+                      kConvWarps * kQuadSlots * kQuadSlotBytes <= kClsSmemBytes,
+              "classifier shared memory exceeds 227 KB");
+
 __device__ __forceinline__ uint32_t bf16_bits_of_byte(uint32_t b) {
   // exact: the float 2^23 + b minus 2^23 is b; its top 16 bits are the bf16 of b (b < 256)
   const float f = __uint_as_float(0x4B000000u | b) - 8388608.0f;
