@@ -62,6 +62,16 @@ enum {
                                    lowest first; needs verdict caches (hydro_cache_enable) */
 };
 
+/* Work distribution of a classifier hop over the persistent K4 CTAs (the hop's "workers";
+   SURVEY.md §8(f) f4). */
+enum {
+  HYDRO_BALANCE_ROUND_ROBIN = 0, /* tile i -> CTA i mod G, the paper's default     */
+  HYDRO_BALANCE_DATA_AWARE = 1   /* AREA heads: contiguous position ranges of equal estimated cost,
+                                    the input size w*h of each tuple being the cost proxy
+                                    (PAPER.md:863-882); NEAREST heads keep round-robin (every
+                                    tuple samples 64 rows: its cost does not follow w*h)       */
+};
+
 /* Where the per-tuple cost of a predicate comes from (R6). */
 enum {
   HYDRO_COST_MEASURED = 0, /* SM-cycles per tuple measured in the kernels (clock64) */
@@ -116,6 +126,8 @@ typedef struct {
                                 BORROWED for the context's lifetime (R11); may be NULL when no
                                 LINEAR predicate is used                                      */
   int32_t n_frames, frame_h, frame_w; /* frame_w % 16 == 0, frames 16-byte aligned, pool < 4 GiB */
+  int32_t balance;           /* HYDRO_BALANCE_*: how a classifier hop's tiles are spread over the
+                                SMs (default ROUND_ROBIN)                                     */
 } hydro_config;
 
 typedef struct {
@@ -277,9 +289,18 @@ hydro_status hydro_launch_count(hydro_ctx* ctx, int64_t* launches);
 /* Kernel timing (CUDA events on the context stream around every launch of the kind):
    enable = 1 starts recording (and clears), 0 stops.  kind: 0 = route kernel (K1, cheap
    predicates), 1 = linear classifier kernel (K4), 2 = fold (K5), 3 = compaction / emit kernel
-   (K2), 4 = MLP classifier kernel (K4-MLP).  hydro_kernel_time synchronises and returns the
+   (K2), 4 = MLP classifier kernel (K4-MLP), 5 = HSV classifier kernel (K4-HSV), 6 = data-aware
+   balance kernels (K6, 2 kernels per launch).  hydro_kernel_time synchronises and returns the
    summed milliseconds and the number of launches recorded since the last enable. */
 hydro_status hydro_set_kernel_timing(hydro_ctx* ctx, int32_t enable);
+
+/* Debug (tests): the position bounds K6 computed for the most recent launch of a data-aware
+   classifier hop (HYDRO_BALANCE_DATA_AWARE with an AREA head):
+   out[c], c = 0..G, CTA c of that K4 launch owned hop-input positions [out[c], out[c+1]).  The
+   bounds are only meaningful if that hop was an AREA hop (K6 exits on other hops).  Writes
+   *n = G + 1; HYDRO_ERANGE (with *n set) when capacity < G + 1; HYDRO_ESTATE when the context
+   has no data-aware AREA head or no hop ran yet.  Synchronises the context stream.           */
+hydro_status hydro_debug_balance_bounds(hydro_ctx* ctx, uint32_t* out, int32_t capacity, int32_t* n);
 hydro_status hydro_kernel_time(hydro_ctx* ctx, int32_t kind, double* total_ms, int64_t* launches);
 
 /* Destroys the context (synchronises first).  Safe on NULL. */

@@ -467,3 +467,58 @@ def brute_force_best_orders(c: Sequence[float], s: Sequence[float]):
         elif abs(e - best) <= 1e-12 * max(1.0, abs(best)):
             arg.append(perm)
     return best, arg
+
+
+# ------------------------------------------------------------------------------------------
+# Data-aware load balancing (R28).
+# The Laminar router gives work to the least-loaded worker, the load being estimated
+# proactively from the input size ("input size as a reasonable proxy for execution cost ...
+# for vision models, it is the input image/frame size").  For a classifier
+# hop the workers are the G persistent CTAs; the hop's input (positions 0..count-1) is cut into
+# G contiguous ranges of equal estimated cost, at 32-position granularity (R28).
+
+def input_size_costs(bbox: np.ndarray) -> np.ndarray:
+    """Estimated cost of each tuple = its input size w * h."""
+    w, h = bbox_wh(bbox)
+    return (w * h).astype(np.int64)
+
+
+def chunk_costs(costs: np.ndarray, chunk: int = 32) -> np.ndarray:
+    """Sum of the estimated costs over consecutive `chunk`-position chunks (last one ragged)."""
+    n = len(costs)
+    out = np.zeros((n + chunk - 1) // chunk, np.int64)
+    for k in range(len(out)):
+        out[k] = int(costs[k * chunk:(k + 1) * chunk].sum())
+    return out
+
+
+def balanced_bounds(chunk_cost: np.ndarray, G: int, count: int, chunk: int = 32) -> List[int]:
+    """R28: worker c (0 <= c < G) starts at chunk min{k : X_k * G >= c * A}, X_k the cost of the
+    chunks before k and A the total; bounds[0] = 0, bounds[G] = count, positions clipped to
+    count.  Each worker's load is at most A / G plus one chunk.  Plain loops, exact integers."""
+    A = int(sum(int(x) for x in chunk_cost))
+    bounds = [0] * (G + 1)
+    bounds[G] = count
+    if A == 0:
+        return bounds
+    X = [0]
+    for x in chunk_cost:
+        X.append(X[-1] + int(x))  # X[k] = exclusive prefix of chunk k; X[n] = A
+    for c in range(1, G):
+        k = next(k for k in range(len(X)) if X[k] * G >= c * A)
+        bounds[c] = min(chunk * k, count)
+    return bounds
+
+
+def range_loads(costs: np.ndarray, bounds: Sequence[int]) -> List[int]:
+    """Estimated load of every worker for position ranges [bounds[c], bounds[c+1])."""
+    return [int(costs[bounds[c]:bounds[c + 1]].sum()) for c in range(len(bounds) - 1)]
+
+
+def round_robin_loads(costs: np.ndarray, G: int, tile: int = 128) -> List[int]:
+    """Estimated load of every worker when tile i (128 positions) goes to worker i mod G, the
+    default round-robin routing."""
+    loads = [0] * G
+    for i in range((len(costs) + tile - 1) // tile):
+        loads[i % G] += int(costs[i * tile:(i + 1) * tile].sum())
+    return loads

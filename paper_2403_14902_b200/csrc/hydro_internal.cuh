@@ -238,6 +238,11 @@ struct ClsParams {
   uint16_t* dbg_crops;    // [pos][12288]
   uint8_t* dbg_verdict;   // [pos]
   int32_t collect_stats;
+  // data-aware tile scheduling (HYDRO_BALANCE_DATA_AWARE, AREA heads)
+  const uint32_t* bounds;  // K4: CTA c owns positions [bounds[c], bounds[c+1]) when the hop is AREA
+  uint32_t* bal_chunks;    // K6: estimated cost (sum of w*h) per 32-position chunk of the hop input
+  uint32_t* bal_bounds;    // K6: output bounds, bal_ctas + 1 entries
+  int32_t bal_ctas;        // CTAs of the K4 launch the bounds are for
 };
 
 // ------------------------------------------------------------------------------------------
@@ -379,6 +384,8 @@ int hydro_route_occupancy(bool compact);
 __global__ void hydro_compact_kernel(hydro::CompactParams p);
 cudaError_t hydro_classifier_configure();
 void hydro_classifier_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug, bool area);
+// K6 data-aware balance: per-chunk input-size estimates, then the bounds
+void hydro_balance_launch(const hydro::ClsParams& c, uint64_t max_positions, int num_sms, cudaStream_t stream);
 void hydro_mlp_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug);
 void hydro_hsv_launch(const hydro::ClsParams& c, uint64_t max_positions, int num_sms, cudaStream_t stream);
 int hydro_hsv_warps_per_sm();

@@ -134,6 +134,22 @@ __device__ __forceinline__ RowMeta load_meta(const ClsParams& p, const uint32_t*
   return m;
 }
 
+// Which M-tiles of the hop a CTA walks.  Round-robin (the default): unit u of the
+// CTA is tile u * kP + crank, units first, first + step, ...  Data-aware (
+// HYDRO_BALANCE_DATA_AWARE, AREA heads): the CTA owns the contiguous position range [lo, lim)
+// whose estimated cost (sum of input sizes w*h) K6 made equal across CTAs; its units are the
+// 128-position tiles lo + 128u (the last one ragged).  Every position range start is a multiple
+// of 32, so each verdict word has exactly one writer.
+struct TileWalk {
+  uint32_t first, step, end;  // units
+  uint32_t lo, lim;           // positions >= lim are invalid
+  uint32_t kp, crank;
+  bool bal;
+  __device__ __forceinline__ uint32_t pos0(uint32_t unit) const {
+    return bal ? lo + unit * static_cast<uint32_t>(kTileM) : (unit * kp + crank) * static_cast<uint32_t>(kTileM);
+  }
+};
+
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -144,13 +160,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-#ifdef HYDRO_L2_PREFETCH
 // per-thread L2 prefetch of one line (a regular LSU op: unlike the uniform-datapath
 // cp.async.bulk.prefetch it does not serialise across the lanes of a warp)
 __device__ __forceinline__ void prefetch_line_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
-#endif
 
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
@@ -298,29 +312,47 @@ __device__ __forceinline__ void convert_quad_area(const uint8_t* frames, uint32_
                                                   uint32_t w, uint32_t pitch, uint32_t g, uint32_t row_base,
                                                   uint32_t j, uint32_t m, uint16_t* dbg) {
   const uint32_t ys = (g * h) >> 6, ye = ((g + 1u) * h + 63u) >> 6;
-  uint32_t half[24];
+  uint32_t xs[8], bw[8], bwmax = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint32_t dx = j + 8u * k;
-    const uint32_t xs = x0 + ((dx * w) >> 6), xe = x0 + (((dx + 1u) * w + 63u) >> 6);
-    uint32_t s0 = 0, s1 = 0, s2 = 0;
-    for (uint32_t y = ys; y < ye; ++y) {
-      const uint8_t* rp = frames + row0 + y * pitch;
-      for (uint32_t x = xs; x < xe; ++x) {
-        const uint32_t o = 3u * x;
-        const uint32_t w0 = ldg32(rp + (o & ~3u));
-        const uint32_t w1 = (o & 3u) > 1u ? ldg32(rp + (o & ~3u) + 4) : 0u;
-        const uint32_t pxl = __funnelshift_r(w0, w1, o << 3);
-        s0 += pxl & 0xFFu;
-        s1 += (pxl >> 8) & 0xFFu;
-        s2 += (pxl >> 16) & 0xFFu;
+    xs[k] = x0 + ((dx * w) >> 6);
+    bw[k] = x0 + (((dx + 1u) * w + 63u) >> 6) - xs[k];
+    bwmax = max(bwmax, bw[k]);
+  }
+  uint32_t s[8][3];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s[k][0] = s[k][1] = s[k][2] = 0u;
+  // Bin row y, bin column t: the loads of all 8 bins are issued before any is summed (16
+  // independent L1/L2 requests in flight per lane instead of one dependent chain per pixel).
+  for (uint32_t y = ys; y < ye; ++y) {
+    const uint8_t* rp = frames + row0 + y * pitch;
+    for (uint32_t t = 0; t < bwmax; ++t) {
+      uint32_t w0[8], w1[8], sh[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const bool on = t < bw[k];
+        const uint32_t o = 3u * (xs[k] + t);
+        sh[k] = on ? o << 3 : 0u;
+        w0[k] = on ? ldg32(rp + (o & ~3u)) : 0u;
+        w1[k] = (on && (o & 3u) > 1u) ? ldg32(rp + (o & ~3u) + 4) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t pxl = __funnelshift_r(w0[k], w1[k], sh[k]);
+        s[k][0] += pxl & 0xFFu;
+        s[k][1] += (pxl >> 8) & 0xFFu;
+        s[k][2] += (pxl >> 16) & 0xFFu;
       }
     }
-    const float cnt = static_cast<float>((ye - ys) * (xe - xs));
-    const uint32_t sums[3] = {s0, s1, s2};
+  }
+  uint32_t half[24];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float cnt = static_cast<float>((ye - ys) * bw[k]);
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      const __nv_bfloat16 b = __float2bfloat16_rn(__fdiv_rn(static_cast<float>(sums[ch]), cnt));
+      const __nv_bfloat16 b = __float2bfloat16_rn(__fdiv_rn(static_cast<float>(s[k][ch]), cnt));
       const uint32_t bbits = __bfloat16_as_ushort(b);
       half[3 * k + ch] = kFp16 ? static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__bfloat162float(b)))) : bbits;
       if (kDbg && dbg) dbg[24 * k + ch] = static_cast<uint16_t>(bbits);
@@ -356,8 +388,8 @@ __device__ __noinline__ void stage_wide_row(uint32_t dst, const uint8_t* row, ui
 // slot bytes [8k, 8k + 8), and its pixel offsets become 8k + (byte-in-word), so the conversion
 // itself is unchanged.
 template <bool kDbg, bool kArea, int kP, int kQD, bool kWide>
-__device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, const uint32_t* list_in, uint32_t count,
-                                             uint32_t tile, uint32_t crank, int cu, int lane, uint32_t slots, uint32_t a_ring,
+__device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, const uint32_t* list_in, uint32_t lim,
+                                             uint32_t pos0, uint32_t crank, int cu, int lane, uint32_t slots, uint32_t a_ring,
                                              uint32_t row_pitch, bool area, bool fp16, const RowMeta& mm,
                                              uint32_t& gg) {
   constexpr int kQS = kQD + 1;
@@ -430,8 +462,8 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
       const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * it + r);
       const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kSegPitch;
       const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
-      uint16_t* dbg = (kDbg && p.dbg_crops && tile * kTileM + m < count)
-                          ? p.dbg_crops + static_cast<uint64_t>(tile * kTileM + m) * kFeatures + g * 192 + 3 * j
+      uint16_t* dbg = (kDbg && p.dbg_crops && pos0 + m < lim)
+                          ? p.dbg_crops + static_cast<uint64_t>(pos0 + m) * kFeatures + g * 192 + 3 * j
                           : nullptr;
       if (kArea && area) {
         const int src_lane = 4 * it + r;
@@ -466,8 +498,7 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
 // the CTA's M-tile) at a time, full_a / empty_a handshake with the MMA issuer.
 template <bool kDbg, bool kArea, int kP, int kQD>
 __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl, const uint32_t* list_in,
-                                               uint32_t base, uint32_t count, uint32_t unit0, uint32_t unit_stride,
-                                               uint32_t num_units, uint32_t crank, int warp, int lane,
+                                               uint32_t base, const TileWalk& tw, uint32_t crank, int warp, int lane,
                                                uint32_t staging_addr, uint32_t a_ring, uint32_t row_pitch, bool area,
                                                bool fp16) {
   constexpr int kQS = kQD + 1;
@@ -478,17 +509,16 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
   const int cu = warp - kConvWarp0;
   const uint32_t slots = staging_addr + static_cast<uint32_t>(cu) * (kQS * kQuadSlotBytes);
   uint32_t gg = 0;
-  for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
-    const uint32_t tile = unit * kP + crank;
+  for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
+    const uint32_t pos0 = tw.pos0(unit);
     // rows' metadata: lane l < 16 holds row 16*cu + l
-    const RowMeta mm = load_meta(p, list_in, base, tile * kTileM + cu * kConvRows + (lane & 15),
-                                 lane < 16 ? count : 0u);
+    const RowMeta mm = load_meta(p, list_in, base, pos0 + cu * kConvRows + (lane & 15), lane < 16 ? tw.lim : 0u);
     // a tile with a crop wider than a staging slot (rare) runs the gather-staging variant
     if (__any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes)))
-      convert_tile<kDbg, kArea, kP, kQD, true>(p, ctrl, list_in, count, tile, crank, cu, lane, slots, a_ring, row_pitch,
+      convert_tile<kDbg, kArea, kP, kQD, true>(p, ctrl, list_in, tw.lim, pos0, crank, cu, lane, slots, a_ring, row_pitch,
                                                area, fp16, mm, gg);
     else
-      convert_tile<kDbg, kArea, kP, kQD, false>(p, ctrl, list_in, count, tile, crank, cu, lane, slots, a_ring,
+      convert_tile<kDbg, kArea, kP, kQD, false>(p, ctrl, list_in, tw.lim, pos0, crank, cu, lane, slots, a_ring,
                                                 row_pitch, area, fp16, mm, gg);
   }
   if (kP == 2) {  // drain: both A sets released (the leader's commits land here)
@@ -529,18 +559,25 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     bits_out = p.bits_out;
   }
   const uint32_t num_tiles = (count + kTileM - 1) / kTileM;
+  const PredDev& pdg = p.preds[pred];
+  const bool area = kArea && pdg.crop_mode == HYDRO_CROP_AREA;  // kArea: the context has an AREA head
   // work unit = kPair consecutive M-tiles (one per CTA of the cluster); both CTAs of a pair walk
   // the same units, so a pair's last unit may hold a tile past num_tiles (all rows invalid)
   const uint32_t crank = kPair == 2 ? cluster_ctarank() : 0u;
-  const uint32_t unit0 = blockIdx.x / kPair, unit_stride = gridDim.x / kPair;
-  const uint32_t num_units = (num_tiles + kPair - 1) / kPair;
-  if (unit0 >= num_units) return;
+  TileWalk tw{blockIdx.x / kPair, gridDim.x / kPair, (num_tiles + kPair - 1) / kPair, 0u, count, kPair, crank, false};
+  if (kPair == 1 && area && p.bounds) {  // data-aware: this CTA's balanced position range
+    tw.bal = true;
+    tw.lo = min(p.bounds[blockIdx.x], count);
+    tw.lim = min(p.bounds[blockIdx.x + 1], count);
+    tw.first = 0;
+    tw.step = 1;
+    tw.end = tw.lim > tw.lo ? (tw.lim - tw.lo + kTileM - 1) / kTileM : 0u;
+  }
+  if (tw.first >= tw.end) return;
 
   const long long t_start = clock64();
-  const PredDev& pdg = p.preds[pred];
   const int n_classes = pdg.n_classes, n_pad = pdg.n_pad, target = pdg.target;
   const bool fp16 = pdg.a_fp16 != 0;
-  const bool area = kArea && pdg.crop_mode == HYDRO_CROP_AREA;  // kArea: the context has an AREA head
   const uint8_t* w_tiled = pdg.w_tiled;
   const int n_alloc = n_pad <= 32 ? 32 : (n_pad <= 64 ? 64 : 128);
   const uint32_t tmem_cols = 2u * n_alloc;
@@ -605,15 +642,24 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     constexpr int kPrefetchGroups = HYDRO_PF_GROUPS;
     const uint64_t pol_w = policy_evict_last();  // weights are re-read by every tile: keep them in L2
     uint32_t itb = 0;
-    for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
-      const uint32_t tile = unit * kPair + crank;
+    for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
+      const uint32_t pos0 = tw.pos0(unit);
       RowMeta mr[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) mr[r] = load_meta(p, list_in, base, tile * kTileM + lane * 4 + r, count);
+      for (int r = 0; r < 4; ++r) mr[r] = load_meta(p, list_in, base, pos0 + lane * 4 + r, tw.lim);
       auto prefetch_group = [&](int g) {
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           if (!mr[r].valid) continue;
+          if (area) {  // AREA: every source row of the crop row's bins, whole lines (all bytes are used)
+            const uint32_t h = static_cast<uint32_t>(mr[r].h);
+            const uint32_t ys = (static_cast<uint32_t>(g) * h) >> 6, ye = ((static_cast<uint32_t>(g) + 1u) * h + 63u) >> 6;
+            for (uint32_t y = ys; y < ye; ++y) {
+              const uint8_t* a = p.frames + mr[r].row0 + y * row_pitch + mr[r].seg_lo;
+              for (uint32_t c = 0; c < mr[r].seg_len; c += 128u) prefetch_line_l2(a + c);
+            }
+            continue;
+          }
           const uint32_t sy = static_cast<uint32_t>(((2 * g + 1) * mr[r].h) >> 7);
           const uint8_t* a = p.frames + mr[r].row0 + sy * row_pitch + mr[r].seg_lo;
 #if defined(HYDRO_L2_PREFETCH)  // measured slightly slower on B200 (line-granular overfetch, L2 pressure)
@@ -648,7 +694,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     if (kPair == 2 && crank != 0 && lane == 0) {
       // peer: relay "my half of B landed" to the leader's full_b (the bulk copy completes locally)
       uint32_t itb = 0;
-      for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
+      for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
         for (int kb = 0; kb < kNumKBlocks; ++kb, ++itb) {
           const uint32_t s = itb % kBStages;
           mbar_wait(&ctrl->full_b[s], (itb / kBStages) & 1u);
@@ -658,7 +704,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     } else if (lane == 0) {
       const uint32_t idesc = idesc_f16_f32(kTileM * kPair, static_cast<uint32_t>(n_pad), !fp16);
       uint32_t itb = 0, gg = 0, tl = 0;
-      for (uint32_t unit = unit0; unit < num_units; unit += unit_stride, ++tl) {
+      for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
         const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
         mbar_wait_sleep(&ctrl->tempty[acc], aph ^ 1u);
         tc_fence_after();
@@ -699,20 +745,20 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     }
     __syncwarp();
   } else if (warp >= kConvWarp0) {
-    converter_role<kDbg, kArea, kPair, kQuadDepth>(p, ctrl, list_in, base, count, unit0, unit_stride, num_units, crank,
+    converter_role<kDbg, kArea, kPair, kQuadDepth>(p, ctrl, list_in, base, tw, crank,
                                                    warp, lane, staging_addr, a_ring, row_pitch, area, fp16);
   } else {
     // ===================== epilogue warps 0..3 (TMEM lane quadrant = warp)
     const int q = warp;
     uint32_t n_in = 0, n_pass = 0, tl = 0;
-    for (uint32_t unit = unit0; unit < num_units; unit += unit_stride, ++tl) {
-      const uint32_t tile = unit * kPair + crank;
+    for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
+      const uint32_t pos0 = tw.pos0(unit);
       const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
       mbar_wait_sleep(&ctrl->tfull[acc], aph);
       tc_fence_after();
       const int m = q * 32 + lane;
-      const uint32_t pos = tile * kTileM + m;
-      const bool valid = pos < count;
+      const uint32_t pos = pos0 + m;
+      const bool valid = pos < tw.lim;
       float best = -3.402823466e38f;
       int bi = 0;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * static_cast<uint32_t>(n_alloc);
@@ -743,10 +789,10 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       const uint32_t bv = __ballot_sync(0xFFFFFFFFu, verdict);
       const uint32_t bvalid = __ballot_sync(0xFFFFFFFFu, valid);
       if (lane == 0 && bvalid) {
-        bits_out[tile * (kTileM / 32) + q] = bv;
+        bits_out[(pos0 >> 5) + q] = bv;
         if (bv) {
-          atomicAdd(p.seg_counts + ((tile * kTileM + q * 32) / kRouteTile), static_cast<uint32_t>(__popc(bv)));
-          atomicAdd(p.warp_counts + ((tile * kTileM + q * 32) / kWarpSeg), static_cast<uint32_t>(__popc(bv)));
+          atomicAdd(p.seg_counts + ((pos0 + q * 32) / kRouteTile), static_cast<uint32_t>(__popc(bv)));
+          atomicAdd(p.warp_counts + ((pos0 + q * 32) / kWarpSeg), static_cast<uint32_t>(__popc(bv)));
         }
       }
       if (kDbg && p.dbg_verdict && valid) p.dbg_verdict[pos] = verdict ? 1 : 0;
@@ -818,9 +864,8 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
   }
   const uint32_t num_tiles = (count + kTileM - 1) / kTileM;
   const uint32_t crank = cluster_ctarank();
-  const uint32_t unit0 = blockIdx.x / kP, unit_stride = gridDim.x / kP;
-  const uint32_t num_units = (num_tiles + kP - 1) / kP;
-  if (unit0 >= num_units) return;
+  const TileWalk tw{blockIdx.x / kP, gridDim.x / kP, (num_tiles + kP - 1) / kP, 0u, count, kP, crank, false};
+  if (tw.first >= tw.end) return;
 
   const long long t_start = clock64();
   const PredDev& pdg = p.preds[pred];
@@ -878,7 +923,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_last();
       uint32_t itb = 0;
-      for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
+      for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
         for (int kb = 0; kb < kb_per_tile; ++kb, ++itb) {
           const uint32_t s = itb % kMB, ph = (itb / kMB) & 1u;
           HYDRO_PIPE_WAIT(&ctrl->empty_b[s], ph ^ 1u);
@@ -902,7 +947,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
     if (crank != 0 && lane == 0) {
       // peer: relay "my half of the B stage landed" to the leader
       uint32_t itb = 0;
-      for (uint32_t unit = unit0; unit < num_units; unit += unit_stride) {
+      for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
         for (int kb = 0; kb < kb_per_tile; ++kb, ++itb) {
           const uint32_t s = itb % kMB;
           mbar_wait(&ctrl->full_b[s], (itb / kMB) & 1u);
@@ -914,7 +959,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
       const uint32_t idesc1 = idesc_f16_f32(kTileM * kP, 256u, !fp16);
       const uint32_t idesc2 = idesc_f16_f32(kTileM * kP, static_cast<uint32_t>(n_pad), true);
       uint32_t itb = 0, gg = 0, tl = 0;
-      for (uint32_t unit = unit0; unit < num_units; unit += unit_stride, ++tl) {
+      for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
         mbar_wait_sleep(&ctrl->tempty[0], (tl & 1u) ^ 1u);  // previous unit's logits read out
         tc_fence_after();
         for (int g = 0; g < kGroups; ++g, ++gg) {
@@ -957,15 +1002,15 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
     }
     __syncwarp();
   } else if (warp >= kConvWarp0) {
-    converter_role<kDbg, false, kP, kQD>(p, ctrl, list_in, base, count, unit0, unit_stride, num_units, crank, warp, lane,
+    converter_role<kDbg, false, kP, kQD>(p, ctrl, list_in, base, tw, crank, warp, lane,
                                          staging_addr, a_ring, row_pitch, false, fp16);
   } else {
     // ===================== epilogue warps 0..3 (TMEM lane quadrant = warp)
     const int q = warp;
     uint32_t n_in = 0, n_pass = 0, tl = 0;
     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-    for (uint32_t unit = unit0; unit < num_units; unit += unit_stride, ++tl) {
-      const uint32_t tile = unit * kP + crank;
+    for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
+      const uint32_t pos0 = tw.pos0(unit);
       mbar_wait_sleep(&ctrl->tfull[0], tl & 1u);
       tc_fence_after();
       // hidden: + b1, ReLU, bf16 RNE, packed pairs written back over the consumed fp32 columns
@@ -991,8 +1036,8 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
       mbar_wait_sleep(&ctrl->tfull2, tl & 1u);
       tc_fence_after();
       const int m = q * 32 + lane;
-      const uint32_t pos = tile * kTileM + m;
-      const bool valid = pos < count;
+      const uint32_t pos = pos0 + m;
+      const bool valid = pos < tw.lim;
       float best = -3.402823466e38f;
       int bi = 0;
       for (int c0 = 0; c0 < n_pad; c0 += 16) {
@@ -1022,10 +1067,10 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
       const uint32_t bv = __ballot_sync(0xFFFFFFFFu, verdict);
       const uint32_t bvalid = __ballot_sync(0xFFFFFFFFu, valid);
       if (lane == 0 && bvalid) {
-        bits_out[tile * (kTileM / 32) + q] = bv;
+        bits_out[(pos0 >> 5) + q] = bv;
         if (bv) {
-          atomicAdd(p.seg_counts + ((tile * kTileM + q * 32) / kRouteTile), static_cast<uint32_t>(__popc(bv)));
-          atomicAdd(p.warp_counts + ((tile * kTileM + q * 32) / kWarpSeg), static_cast<uint32_t>(__popc(bv)));
+          atomicAdd(p.seg_counts + ((pos0 + q * 32) / kRouteTile), static_cast<uint32_t>(__popc(bv)));
+          atomicAdd(p.warp_counts + ((pos0 + q * 32) / kWarpSeg), static_cast<uint32_t>(__popc(bv)));
         }
       }
       if (kDbg && p.dbg_verdict && valid) p.dbg_verdict[pos] = verdict ? 1 : 0;

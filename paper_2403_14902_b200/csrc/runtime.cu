@@ -106,6 +106,9 @@ struct hydro_ctx {
   uint32_t* seg_counts = nullptr;  // [max_segs] segment counts, then [8 * max_segs] warp counts
   uint64_t max_segs = 0;
   uint32_t* warm_and = nullptr;
+  uint32_t* bal_chunks = nullptr;  // K6 (data-aware balance): chunk cost estimates
+  uint32_t* bal_bounds = nullptr;  // K6: per-CTA position bounds of the current AREA hop
+  int bal_last_ctas = 0;           // CTAs of the last data-aware K4 launch
   uint32_t* zero_word = nullptr;
   std::vector<Slot> slots;
   int64_t next_batch = 0;
@@ -228,6 +231,8 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return set_err(HYDRO_EINVAL, "bad rank/world");
   if (cfg->world > 1 && !cfg->nccl_unique_id) return set_err(HYDRO_EINVAL, "world > 1 needs nccl_unique_id");
   if (cfg->sync_every < 1) return set_err(HYDRO_EINVAL, "sync_every >= 1");
+  if (cfg->balance != HYDRO_BALANCE_ROUND_ROBIN && cfg->balance != HYDRO_BALANCE_DATA_AWARE)
+    return set_err(HYDRO_EINVAL, "unknown balance mode");
   if (cfg->frames) {
     if (cfg->n_frames < 1 || cfg->frame_h < 1 || cfg->frame_w < 1 || (cfg->frame_w % 16) != 0 ||
         cfg->frame_h > 65535 || cfg->frame_w > 65535)
@@ -547,6 +552,10 @@ static hydro_status freeze(hydro_ctx* ctx) {
   CU(cudaMalloc(&ctx->seg_counts, sizeof(uint32_t) * ctx->max_segs * 9));
   CU(cudaMemset(ctx->seg_counts, 0, sizeof(uint32_t) * ctx->max_segs * 9));
   CU(cudaMalloc(&ctx->warm_and, sizeof(uint32_t) * ctx->bits_stride));
+  if (ctx->cfg.balance == HYDRO_BALANCE_DATA_AWARE && ctx->has_area) {
+    CU(cudaMalloc(&ctx->bal_chunks, sizeof(uint32_t) * ((maxb + 31) / 32 + 1)));
+    CU(cudaMalloc(&ctx->bal_bounds, sizeof(uint32_t) * (ctx->num_sms + 1)));
+  }
   ctx->slots.resize(ctx->cfg.max_inflight);
   for (Slot& s : ctx->slots) {
     CU(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
@@ -656,9 +665,22 @@ static ClsKind cls_kind_of(int32_t pred_kind) {
   return pred_kind == HYDRO_PRED_MLP ? kClsMlp : (pred_kind == HYDRO_PRED_HSV ? kClsHsv : kClsLinear);
 }
 
-static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c, uint64_t max_positions, ClsKind kind = kClsLinear) {
+static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c0, uint64_t max_positions, ClsKind kind = kClsLinear) {
   const uint64_t tiles = (max_positions + kTileM - 1) / kTileM;
   const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(tiles, ctx->num_sms)));
+  ClsParams c = c0;
+  if (kind == kClsLinear && ctx->bal_bounds && !(c.dbg_crops || c.dbg_logits || c.dbg_verdict)) {
+    // data-aware: K6 cuts an AREA hop's input into `grid` ranges of equal estimated cost (it exits
+    // on other hops, and K4 then ignores the bounds)
+    c.bal_chunks = ctx->bal_chunks;
+    c.bal_bounds = ctx->bal_bounds;
+    c.bal_ctas = grid;
+    c.bounds = ctx->bal_bounds;
+    ctx->bal_last_ctas = grid;
+    hydro_status s = timed_launch(ctx, 6, [&] { hydro_balance_launch(c, max_positions, ctx->num_sms, ctx->stream); });
+    if (s != HYDRO_OK) return s;
+    ctx->launches += 1;  // two kernels per K6 launch
+  }
   return timed_launch(ctx, kind == kClsMlp ? 4 : (kind == kClsHsv ? 5 : 1), [&] {
     const bool dbg = c.dbg_crops || c.dbg_logits || c.dbg_verdict;
     if (kind == kClsMlp) hydro_mlp_launch(c, grid, ctx->stream, dbg);
@@ -989,6 +1011,18 @@ hydro_status hydro_set_kernel_timing(hydro_ctx* ctx, int32_t enable) {
   return HYDRO_OK;
 }
 
+hydro_status hydro_debug_balance_bounds(hydro_ctx* ctx, uint32_t* out, int32_t capacity, int32_t* n) {
+  if (!ctx || !n) return set_err(HYDRO_EINVAL, "NULL argument");
+  if (!ctx->bal_bounds || ctx->bal_last_ctas == 0) return set_err(HYDRO_ESTATE, "no data-aware AREA hop ran");
+  *n = ctx->bal_last_ctas + 1;
+  if (capacity < *n || !out) return set_err(HYDRO_ERANGE, "capacity < G + 1");
+  CU(cudaStreamSynchronize(ctx->stream));
+  hydro_status s = check_sticky(ctx);
+  if (s != HYDRO_OK) return s;
+  CU(cudaMemcpy(out, ctx->bal_bounds, sizeof(uint32_t) * (*n), cudaMemcpyDeviceToHost));
+  return HYDRO_OK;
+}
+
 hydro_status hydro_kernel_time(hydro_ctx* ctx, int32_t kind, double* total_ms, int64_t* launches) {
   if (!ctx || !total_ms || !launches) return set_err(HYDRO_EINVAL, "NULL argument");
   CU(cudaStreamSynchronize(ctx->stream));
@@ -1089,6 +1123,8 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
   cudaFree(ctx->warm_bits);
   cudaFree(ctx->seg_counts);
   cudaFree(ctx->warm_and);
+  cudaFree(ctx->bal_chunks);
+  cudaFree(ctx->bal_bounds);
   cudaFree(ctx->zero_word);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->copy_stream) {

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("HYDRO_LIB_PATH") or os.path.join(HERE, "libhydro.so")
 
 HYDRO_OK, HYDRO_EINVAL, HYDRO_ENOMEM, HYDRO_ECUDA, HYDRO_ENCCL, HYDRO_ESTATE, HYDRO_ERANGE, HYDRO_EBUSY = (
     0, -1, -2, -3, -4, -5, -6, -7)
+BALANCE = {"round_robin": 0, "data_aware": 1}  # HYDRO_BALANCE_* (hydro.h)
 POLICY = {"score": 0, "static": 1, "fixed": 2, "cost": 3, "selectivity": 4, "reuse": 5}
 COST_SOURCE = {"measured": 0, "declared": 1}
 PRED_KIND = {"label_eq": 0, "hash": 1, "linear": 2, "mlp": 3, "hsv": 4}
@@ -38,7 +39,8 @@ class hydro_config(C.Structure):
                 ("decay_gamma", C.c_double), ("prior_selectivity", C.c_double), ("warmup_tuples", C.c_int64),
                 ("max_batch_tuples", C.c_int64), ("max_inflight", C.c_int32), ("rank", C.c_int32),
                 ("world", C.c_int32), ("sync_every", C.c_int32), ("nccl_unique_id", C.c_void_p),
-                ("frames", C.c_void_p), ("n_frames", C.c_int32), ("frame_h", C.c_int32), ("frame_w", C.c_int32)]
+                ("frames", C.c_void_p), ("n_frames", C.c_int32), ("frame_h", C.c_int32), ("frame_w", C.c_int32),
+                ("balance", C.c_int32)]
 
 
 class hydro_predicate_desc(C.Structure):
@@ -92,6 +94,7 @@ _SIGS = {
     "hydro_launch_count": ([_P, C.POINTER(C.c_int64)], C.c_int32),
     "hydro_set_kernel_timing": ([_P, C.c_int32], C.c_int32),
     "hydro_kernel_time": ([_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int32),
+    "hydro_debug_balance_bounds": ([_P, C.POINTER(C.c_uint32), C.c_int32, C.POINTER(C.c_int32)], C.c_int32),
     "hydro_destroy": ([_P], C.c_int32),
     "hydro_debug_linear": ([_P, C.c_int32, C.POINTER(hydro_tuples), _P, _P, _P], C.c_int32),
 }
@@ -234,6 +237,13 @@ def hydro_kernel_time(ctx, kind: int):
     return ms.value, n.value
 
 
+def hydro_debug_balance_bounds(ctx, capacity: int = 1024) -> List[int]:
+    buf = (C.c_uint32 * capacity)()
+    n = C.c_int32()
+    _check(lib().hydro_debug_balance_bounds(ctx, buf, capacity, C.byref(n)))
+    return list(buf[:n.value])
+
+
 def hydro_destroy(ctx):
     _check(lib().hydro_destroy(ctx))
 
@@ -264,7 +274,7 @@ class Eddy:
                  cost_source: str = "measured", decay_gamma: float = 0.5, prior_selectivity: float = 0.5,
                  warmup_tuples: int = 65536, max_batch_tuples: int = 1 << 20, max_inflight: int = 4,
                  rank: int = 0, world: int = 1, sync_every: int = 1, nccl_unique_id: Optional[bytes] = None,
-                 stream: Optional[torch.cuda.Stream] = None):
+                 stream: Optional[torch.cuda.Stream] = None, balance: str = "round_robin"):
         cfg = hydro_config_default()
         cfg.device = device
         cfg.stream = (stream or torch.cuda.current_stream(device)).cuda_stream
@@ -276,6 +286,7 @@ class Eddy:
         cfg.max_batch_tuples = max_batch_tuples
         cfg.max_inflight = max_inflight
         cfg.rank, cfg.world, cfg.sync_every = rank, world, sync_every
+        cfg.balance = BALANCE[balance]
         self._uid = None
         if nccl_unique_id is not None:
             self._uid = C.create_string_buffer(nccl_unique_id, 128)
@@ -402,6 +413,9 @@ class Eddy:
 
     def kernel_time(self, kind: int):
         return hydro_kernel_time(self.ctx, kind)
+
+    def debug_balance_bounds(self) -> List[int]:
+        return hydro_debug_balance_bounds(self.ctx)
 
     def debug_linear(self, pred_id: int, tuples, logits=None, crops=None, verdict=None):
         t = make_tuples_struct(tuples.id, tuples.frame_id, tuples.bbox, tuples.label)

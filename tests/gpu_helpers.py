@@ -12,8 +12,8 @@ def ensure_built():
 
 
 def make_eddy(w, frames_dev=None, *, policy=None, cost_source="measured", warmup=None, max_batch=None,
-              gamma=0.5, max_inflight=4):
-    e = Eddy(frames=frames_dev, policy=policy or w.policy, cost_source=cost_source,
+              gamma=0.5, max_inflight=4, balance="round_robin"):
+    e = Eddy(frames=frames_dev, policy=policy or w.policy, cost_source=cost_source, balance=balance,
              warmup_tuples=w.warmup_tuples if warmup is None else warmup,
              max_batch_tuples=max_batch or w.batch_tuples, decay_gamma=gamma, max_inflight=max_inflight)
     for p in w.preds:

@@ -299,10 +299,12 @@ def test_linear_area_crops_logits_verdicts():
     e.close()
 
 
-def test_cfg4_small_end_to_end():
+@pytest.mark.parametrize("balance", ["round_robin", "data_aware"])
+def test_cfg4_small_end_to_end(balance):
     """cfg4 (label, area-weighted HASH, colour nearest, breed AREA) through the eddy; tuples whose
     AREA-head margin is within 4x the logit tolerance are removed from the input (excluded by
-    construction), the rest must match the oracle row for row."""
+    construction), the rest must match the oracle row for row -- with round-robin and with
+    data-aware (R28) tile scheduling of the AREA hop."""
     w = workload("cfg4", small=True, n=6000)
     frames = w.frames()
     t = w.tuples()
@@ -312,7 +314,7 @@ def test_cfg4_small_end_to_end():
     keep_in = np.abs(O.margin(z, w.preds[3]["target"])) >= 4 * LOGIT_TOL
     t = t.select(torch.from_numpy(np.where(keep_in)[0]))
     V, ref_ids, ref_bbox, _ = oracle_result(w, t, fr)
-    e = make_eddy(w, frames.cuda(), policy="score", warmup=1024, max_batch=2048)
+    e = make_eddy(w, frames.cuda(), policy="score", warmup=1024, max_batch=2048, balance=balance)
     ids, bbs, infos = run_stream(e, t.to("cuda"), 2048)
     _assert_rows(ids, bbs, ref_ids, ref_bbox)
     for b, info in enumerate(infos):
@@ -564,3 +566,44 @@ def test_wide_crops_nearest_linear_and_mlp():
         _, z_ref = O.linear_verdict(p, fr, tup["frame_id"], tup["bbox"], return_logits=True)
         assert np.abs(logits.double().cpu().numpy() - z_ref).max() <= LOGIT_TOL
         e.close()
+
+
+# ------------------------------------------------------------- data-aware tile scheduling (f4, R28)
+
+@pytest.mark.parametrize("n", [700, 9000, 20000])
+def test_data_aware_bounds_match_oracle_and_rows_unchanged(n):
+    """An AREA head alone over one range batch: K6's per-CTA position bounds equal the oracle's
+    input-size partition (R28) exactly, and the result rows equal the oracle's (and the
+    round-robin run's).  Sizes: fewer tiles than SMs, a few tiles per CTA, a ragged tail."""
+    from paper_2403_14902_b200.hydro import Eddy
+    w = workload("cfg4", small=True, n=n)
+    frames = w.frames()
+    p = w.preds[3]
+    assert p["crop_mode"] == "area"
+    t = w.tuples()
+    tup = O.as_numpy_tuples(t)
+    fr = frames.numpy()
+    v_ref, z = O.linear_verdict(p, fr, tup["frame_id"], tup["bbox"], return_logits=True)
+    keep_in = np.abs(O.margin(z, p["target"])) >= 4 * LOGIT_TOL
+    t = t.select(torch.from_numpy(np.where(keep_in)[0]))
+    tup = O.as_numpy_tuples(t)
+    v_ref = v_ref[keep_in]
+    m = len(t)
+    rows = {}
+    for balance in ("round_robin", "data_aware"):
+        e = Eddy(frames=frames.cuda(), policy="fixed", warmup_tuples=0, max_batch_tuples=m, balance=balance)
+        e.add_predicate(p)
+        bid = e.submit(t.to("cuda"))
+        ids, bb = e.collect(bid)
+        rows[balance] = (ids.numpy().astype(np.uint64), bb.numpy().astype(np.int64))
+        if balance == "data_aware":
+            bounds = e.debug_balance_bounds()
+            G = len(bounds) - 1
+            assert G == min((m + 127) // 128, torch.cuda.get_device_properties(0).multi_processor_count)
+            ref = O.balanced_bounds(O.chunk_costs(O.input_size_costs(tup["bbox"])), G, m)
+            assert bounds == ref
+        e.close()
+    ref_ids = tup["id"][v_ref].astype(np.uint64)
+    ref_bb = tup["bbox"][v_ref].astype(np.int64)
+    for balance, (ids, bb) in rows.items():
+        _assert_rows(ids, bb, ref_ids, ref_bb)

@@ -466,3 +466,59 @@ def test_fold_gamma_one_is_plain_counts_and_priors():
     g.fold([100], [10], [100.0])
     g.fold([100], [90], [300.0])
     assert g.s_in == [150.0] and g.s_pass == [95.0] and g.s_cost == [350.0]
+
+
+# ------------------------------------------------------------------ data-aware balance (f4, R28)
+
+def _best_contiguous_max_load(chunk_cost, G):
+    """Brute force: the smallest possible max load over all cuts of the chunks into G
+    contiguous (possibly empty) ranges."""
+    n = len(chunk_cost)
+    best = None
+    for cuts in itertools.combinations_with_replacement(range(n + 1), G - 1):
+        b = (0,) + cuts + (n,)
+        m = max(int(sum(chunk_cost[b[i]:b[i + 1]])) for i in range(G))
+        best = m if best is None else min(best, m)
+    return best
+
+
+def test_balanced_bounds_load_bound_and_near_optimal_brute_force():
+    """PAPER.md:863-882 balance the estimated loads: every worker's load is at most A/G plus one
+    chunk, and the max load is within one chunk of the best contiguous cut (brute force)."""
+    rng = np.random.default_rng(7)
+    for _ in range(300):
+        n = int(rng.integers(1, 8))
+        G = int(rng.integers(1, 5))
+        cc = rng.integers(0, 50, n).astype(np.int64)
+        count = 32 * n - int(rng.integers(0, 32))
+        b = O.balanced_bounds(cc, G, count)
+        assert b[0] == 0 and b[-1] == count and all(b[i] <= b[i + 1] for i in range(G))
+        assert all(x % 32 == 0 or x == count for x in b)
+        loads = [int(cc[b[i] // 32:(b[i + 1] + 31) // 32].sum()) if b[i + 1] > b[i] else 0 for i in range(G)]
+        A = int(cc.sum())
+        assert sum(loads) == A
+        assert max(loads) <= A / G + cc.max() + 1e-9
+        assert max(loads) <= _best_contiguous_max_load(cc, G) + cc.max()
+
+
+def test_balanced_bounds_uniform_cost_closed_form():
+    """Equal chunk costs: worker c starts at chunk ceil(c * n / G) (closed form)."""
+    for n in (1, 5, 37, 148, 1000):
+        for G in (1, 3, 148):
+            b = O.balanced_bounds(np.full(n, 7, np.int64), G, 32 * n)
+            assert b == [min(32 * (-(-c * n // G)), 32 * n) for c in range(G)] + [32 * n]
+
+
+def test_input_size_costs_and_loads_conserve_the_total():
+    t = workload("cfg4", small=True, n=3000).tuples()
+    tup = O.as_numpy_tuples(t)
+    cost = O.input_size_costs(tup["bbox"])
+    w = tup["bbox"][:, 2].astype(np.int64) - tup["bbox"][:, 0]
+    h = tup["bbox"][:, 3].astype(np.int64) - tup["bbox"][:, 1]
+    assert np.array_equal(cost, w * h)
+    cc = O.chunk_costs(cost)
+    assert int(cc.sum()) == int(cost.sum()) and len(cc) == (3000 + 31) // 32
+    b = O.balanced_bounds(cc, 16, 3000)
+    assert sum(O.range_loads(cost, b)) == int(cost.sum()) == sum(O.round_robin_loads(cost, 16))
+    # on this heavy-tailed input size the data-aware cut beats round-robin's worst worker
+    assert max(O.range_loads(cost, b)) < max(O.round_robin_loads(cost, 16))
