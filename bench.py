@@ -607,6 +607,111 @@ def run_area(args):
     print(json.dumps(out))
 
 
+def _flow_shop(rows):
+    """Makespan of batches through serial workers in a fixed order (the model the bench compares
+    the measured times with): C[b][i] = max(C[b][i-1], C[b-1][i]) + t[b][i]."""
+    prev = None
+    for row in rows:
+        cur = []
+        for i, t in enumerate(row):
+            cur.append(max(cur[i - 1] if i else 0.0, prev[i] if prev else 0.0) + t)
+        prev = cur
+    return prev[-1] if prev else 0.0
+
+
+def run_concurrent(args):
+    """--workload concurrent: cost-driven routing over concurrent workers (SURVEY.md §8(f) f3;
+    PAPER.md:320-365; R29).  The paper's example (colour: cost 1, selectivity 0.6; breed:
+    cost 2, selectivity 0.1) as HASH stand-ins with 512 / 1024 rounds, 16M tuples
+    in 1M-tuple routing batches.  Each predicate is a worker on half of the SMs (own context, stream,
+    SM budget); batches flow through the workers in the order of the policy, consecutive batches
+    overlapping.  Timed: cost-driven, score-driven and selectivity-driven routing, plus the
+    sequential eddy on all SMs (one context, score policy) for reference, and the flow-shop model's
+    prediction from the warmup's measured costs and selectivities."""
+    import torch
+
+    from paper_2403_14902_b200 import build as B
+    from paper_2403_14902_b200 import hydro as H
+    from paper_2403_14902_b200.pipeline import ConcurrentEddy
+    from synth import hash_pred, workload
+
+    torch.cuda.set_device(0)
+    B.build()
+    n, batch, units = 16_000_000, 1 << 20, 512
+    preds = [hash_pred(31, 0.6, units=units, name="colour (cost 1, sel 0.6)"),
+             hash_pred(32, 0.1, units=2 * units, name="breed (cost 2, sel 0.1)")]
+    t = workload("cfg1", n=n).tuples(device="cuda")
+    batches = [t.slice(a, min(a + batch, n)) for a in range(0, n, batch)]
+    main = torch.cuda.current_stream()
+    res_ids = torch.empty(batch, dtype=torch.int64, device="cuda")
+    res_bb = torch.empty((batch, 4), dtype=torch.int16, device="cuda")
+
+    def timed(fn, streams):
+        fn()  # warm-up pass
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(args.steps):
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(main)
+            out = fn()
+            for st in streams:
+                main.wait_stream(st)
+            ev1.record(main)
+            torch.cuda.synchronize()
+            ms.append(ev0.elapsed_time(ev1))
+        return sorted(ms)[len(ms) // 2], out
+
+    modes = {}
+    for policy in ("cost", "score", "selectivity"):
+        ce = ConcurrentEddy(preds, policy=policy, max_batch_tuples=batch)
+        order = ce.warmup(batches[0])
+        c, sel = list(ce.cost_per_tuple), list(ce.selectivity)
+        ms, out = timed(lambda: sum(r[0] for r in ce.run(batches, res_ids, res_bb)), ce.streams)
+        # flow-shop model: per batch, stage i sees the fraction that passed the earlier stages
+        rows = []
+        for b in batches:
+            alive, row = float(len(b)), []
+            for k in order:
+                row.append(alive * c[k])
+                alive *= sel[k]
+            rows.append(row)
+        modes[policy] = {"ms_per_pass": ms, "order": [preds[k]["name"] for k in order], "results": out,
+                         "cycles_per_tuple_per_worker": [round(x, 2) for x in c], "selectivity": [round(x, 4) for x in sel],
+                         "model_cycles": _flow_shop(rows), "sms": ce.sms}
+        ce.close()
+    seq = H.Eddy(policy="score", warmup_tuples=65536, max_batch_tuples=batch, max_inflight=4, stream=main)
+    for p in preds:
+        seq.add_predicate(p)
+
+    def seq_pass():
+        pend, tot = [], 0
+        for b in batches:
+            pend.append(seq.submit(b))
+            if len(pend) >= 3:
+                tot += H.hydro_collect_results(seq.ctx, pend.pop(0), res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
+        for bid in pend:
+            tot += H.hydro_collect_results(seq.ctx, bid, res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
+        return tot
+
+    ms_seq, tot_seq = timed(seq_pass, [])
+    modes["sequential_all_sms_score"] = {"ms_per_pass": ms_seq, "order": [preds[k]["name"] for k in seq.order()],
+                                         "results": tot_seq}
+    seq.close()
+    assert len({m["results"] for m in modes.values()}) == 1, modes  # the routing never changes the result
+    cost, score = modes["cost"], modes["score"]
+    out = {"metric": "tuples/s through the paper's two-predicate example on concurrent workers (SURVEY.md §8(f) f3)",
+           "value": n / (cost["ms_per_pass"] / 1000.0), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+           "warmup": 1, "ms_per_step": cost["ms_per_pass"], "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+           "config": {"workload": "concurrent: colour HASH (512 rounds, sel 0.6) and breed HASH (1024 rounds, sel "
+                                  "0.1), one worker per predicate on 74 SMs each, 16M tuples in 1M batches"},
+           "modes": modes,
+           "speedup_cost_vs_score": score["ms_per_pass"] / cost["ms_per_pass"],
+           "model_speedup_cost_vs_score": score["model_cycles"] / cost["model_cycles"],
+           "paper_context": "PAPER.md:357-359: 20 (score/selectivity-driven) vs 14 (cost-driven) time units for 10 items"}
+    print(json.dumps(out))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -615,7 +720,7 @@ def main():
     ap.add_argument("--impl", default="hydro", choices=["hydro", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute", "mlp", "uc2", "hsv", "area"],
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute", "mlp", "uc2", "hsv", "area", "concurrent"],
                     help="cfg2 = the BASELINE metric (default); rroute = K1 HBM evidence run; "
                          "mlp = cfg2 with the 12288-512-120 MLP breed head (SURVEY.md §8(f) f1, tensor roofline)")
     args = ap.parse_args()
@@ -629,6 +734,8 @@ def main():
         run_uc2(args)
     elif args.workload == "area":
         run_area(args)
+    elif args.workload == "concurrent":
+        run_concurrent(args)
     else:
         run_gpu(args)
 

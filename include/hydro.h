@@ -128,6 +128,10 @@ typedef struct {
   int32_t n_frames, frame_h, frame_w; /* frame_w % 16 == 0, frames 16-byte aligned, pool < 4 GiB */
   int32_t balance;           /* HYDRO_BALANCE_*: how a classifier hop's tiles are spread over the
                                 SMs (default ROUND_ROBIN)                                     */
+  int32_t max_sms;           /* SM budget of the context's persistent kernels (grids capped at
+                                this many SMs; 0 = all).  Two contexts with budgets summing to
+                                the SM count on two streams run as concurrent workers on
+                                (approximately) disjoint SM partitions   */
 } hydro_config;
 
 typedef struct {
@@ -174,6 +178,15 @@ typedef struct {
                                    host, then uploaded asynchronously on the context's copy
                                    stream so batch k+1's upload overlaps batch k's kernels:
                                    BORROWED until the batch is collected                       */
+  const uint32_t* sel;        /* optional DEVICE selection (NULL: all n positions): the batch is
+                                 the positions sel[0 .. *sel_count) of the columns, in that order
+                                 (each < the columns' length, ascending for input-order output);
+                                 n is then an upper bound of *sel_count.  Device columns only; no
+                                 warmup slice runs on a selection batch; not with REUSE.  Used to
+                                 chain workers (hydro_batch_output of another context)          */
+  const uint32_t* sel_count;  /* DEVICE count of sel (read by the kernels, never by the host)   */
+  void* wait_event;           /* optional cudaEvent_t the context stream waits on before the
+                                 batch's kernels (e.g. the producer batch's done_event)         */
 } hydro_tuples;
 
 typedef struct {
@@ -265,6 +278,14 @@ hydro_status hydro_batch_count(hydro_ctx* ctx, int64_t batch_id, int64_t* count)
 /* Blocks until batch_id finished, then copies its rows: ids[count] (u64) and bboxes[count][4]
    (u16), in input order, to HOST (out_on_device = 0) or DEVICE (1) buffers, and releases the
    batch slot.  capacity < count: ERANGE with *count set and the batch kept. */
+/* The survivors of an uncollected batch as DEVICE data, for chaining a second context (worker)
+   without a host round trip: *positions = their input positions (u32, input
+   order), *count = device pointer to their number, *done_event = the cudaEvent_t recorded when
+   the batch completes (pass it as the consumer's hydro_tuples.wait_event).  The pointers stay
+   valid until the batch is collected or released.  Non-blocking.                                */
+hydro_status hydro_batch_output(hydro_ctx* ctx, int64_t batch_id, const uint32_t** positions,
+                                const uint32_t** count, void** done_event);
+
 hydro_status hydro_collect_results(hydro_ctx* ctx, int64_t batch_id, uint64_t* ids, uint16_t* bboxes,
                                    int64_t capacity, int64_t* count, int32_t out_on_device);
 

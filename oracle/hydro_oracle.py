@@ -522,3 +522,53 @@ def round_robin_loads(costs: np.ndarray, G: int, tile: int = 128) -> List[int]:
     for i in range((len(costs) + tile - 1) // tile):
         loads[i % G] += int(costs[i * tile:(i + 1) * tile].sum())
     return loads
+
+
+# ------------------------------------------------------------------------------------------
+# Concurrent workers and cost-driven routing (
+# DESIGN.md R29).  Each predicate runs on its own resource ("worker"), serially FIFO; an item
+# enters predicate i+1 when predicate i passed it (eager materialization).
+
+def two_stage_completion(n_items: int, cost_first: float, cost_second: float, pass_mask) -> float:
+    """The timeline of Fig. cost_route: item i (1-indexed) leaves stage 1 at
+    i * cost_first; a passing item queues for stage 2, which serves one item at a time for
+    cost_second each.  Returns the completion instant of the last event of either stage."""
+    t1 = 0.0
+    t2 = 0.0
+    for i in range(n_items):
+        t1 += cost_first
+        if pass_mask[i]:
+            t2 = max(t2, t1) + cost_second
+    return max(t1, t2)
+
+
+def flow_shop_makespan(stage_times) -> float:
+    """Batches through P serial workers in a fixed order (a permutation flow shop): batch b's
+    stage i starts when its stage i-1 and batch b-1's stage i are done,
+    C[b][i] = max(C[b][i-1], C[b-1][i]) + t[b][i]; returns C[last][last].  With one item per
+    batch and P = 2 it is two_stage_completion."""
+    prev = None
+    for row in stage_times:
+        cur = []
+        for i, t in enumerate(row):
+            start = max(cur[i - 1] if i else 0.0, prev[i] if prev is not None else 0.0)
+            cur.append(start + float(t))
+        prev = cur
+    return prev[-1] if prev else 0.0
+
+
+def pipeline_stage_times(V: np.ndarray, order: Sequence[int], batch: int, time_per_tuple: Sequence[float]):
+    """Stage times of every routing batch when the batch visits the workers in `order`: stage i
+    sees the tuples that passed the earlier stages (oracle verdicts V[k, t]) and costs
+    time_per_tuple[order[i]] per tuple."""
+    out = []
+    n = V.shape[1]
+    for a in range(0, n, batch):
+        Vb = V[:, a:a + batch]
+        alive = np.ones(Vb.shape[1], dtype=bool)
+        row = []
+        for k in order:
+            row.append(int(alive.sum()) * float(time_per_tuple[k]))
+            alive &= Vb[k]
+        out.append(row)
+    return out

@@ -156,6 +156,8 @@ struct RouteParams {
   const uint32_t* list_in;
   const uint32_t* count_in;
   uint32_t range_base, range_n;
+  const uint32_t* sel0;        // dispatch: hop 0 reads these positions (nullptr: the range)
+  const uint32_t* sel0_count;  // device count of sel0
   const uint32_t* and_bits[kMaxPred];  // verdict bitmaps (bit p) ANDed into the alive mask
   int32_t n_and;
   // ---- which predicates: dispatch (device order) or explicit
@@ -190,6 +192,8 @@ struct CompactParams {
   const uint32_t* list_in;  // explicit: nullptr = range
   const uint32_t* count_in;
   uint32_t range_base, range_n;
+  const uint32_t* sel0;        // dispatch: hop 0 reads these positions (nullptr: the range)
+  const uint32_t* sel0_count;  // device count of sel0
   const uint32_t* bits_in;  // explicit
   const uint32_t* seg_counts;
   const uint32_t* warp_counts;
@@ -203,6 +207,7 @@ struct CompactParams {
   uint32_t* count_out;
   uint64_t* out_ids;
   uint64_t* out_bbox;
+  uint32_t* out_pos;           // emit: the survivors' input positions too (nullable)
   uint32_t* emit_count;        // *emit_count = *emit_offset + survivors
   const uint32_t* emit_offset; // nullable
   const uint64_t* id;
@@ -220,6 +225,8 @@ struct ClsParams {
   const uint32_t* list_in;    // explicit mode input (nullptr: range)
   const uint32_t* count_in;
   uint32_t range_base, range_n;
+  const uint32_t* sel0;        // dispatch: hop 0 reads these positions (nullptr: the range)
+  const uint32_t* sel0_count;  // device count of sel0
   uint32_t* lists;
   uint64_t list_stride;
   uint32_t* counts;

@@ -40,7 +40,8 @@ __device__ __forceinline__ HopIn resolve_hop(const ClsParams& p) {
     if (h < 0 || h >= st->n_pred) return r;
     pred = st->order[h];
     if (h == 0) {
-      r.count = p.range_n;
+      r.list_in = p.sel0;
+      r.count = p.sel0 ? *p.sel0_count : p.range_n;
     } else {
       r.list_in = p.lists + static_cast<uint64_t>(h) * p.list_stride;
       r.count = p.counts[h];

@@ -544,9 +544,9 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     if (h < 0 || h >= st->n_pred) return;
     pred = st->order[h];
     if (st->kind[pred] != kLinear) return;  // (an MLP hop runs in hydro_mlp_kernel)
-    if (h == 0) {
-      list_in = nullptr;
-      count = p.range_n;
+    if (h == 0) {  // the batch: its position range, or the caller's selection
+      list_in = p.sel0;
+      count = p.sel0 ? *p.sel0_count : p.range_n;
     } else {
       list_in = p.lists + static_cast<uint64_t>(h) * p.list_stride;
       count = p.counts[h];
@@ -848,9 +848,9 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
     if (h < 0 || h >= st->n_pred) return;
     pred = st->order[h];
     if (st->kind[pred] != kMlp) return;
-    if (h == 0) {
-      list_in = nullptr;
-      count = p.range_n;
+    if (h == 0) {  // the batch: its position range, or the caller's selection
+      list_in = p.sel0;
+      count = p.sel0 ? *p.sel0_count : p.range_n;
     } else {
       list_in = p.lists + static_cast<uint64_t>(h) * p.list_stride;
       count = p.counts[h];

@@ -121,9 +121,9 @@ __global__ void __launch_bounds__(kRouteThreads, kCompact ? 2 : HYDRO_K1_MINB) h
       int run = 0;
       work = h >= 0 && k1_runs(st, h, &run);
       if (work) {
-        if (h == 0) {
-          list_in = nullptr;
-          count = p.range_n;
+        if (h == 0) {  // the batch: its position range, or the caller's selection
+          list_in = p.sel0;
+          count = p.sel0 ? *p.sel0_count : p.range_n;
         } else {
           list_in = p.lists + static_cast<uint64_t>(h) * p.list_stride;
           count = p.counts[h];
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kRouteThreads, kCompact ? 2 : HYDRO_K1_MINB) h
     // hop h is a classifier hop: clear the segment counts its K4 accumulates into
     const int h = s_hop;
     if (p.dispatch && h >= 0 && h < st->n_pred && is_classifier(st->kind[st->order[h]])) {
-      const uint32_t n = h == 0 ? p.range_n : p.counts[h];
+      const uint32_t n = h == 0 ? (p.sel0 ? *p.sel0_count : p.range_n) : p.counts[h];
       const uint32_t nseg = (n + kRouteTile - 1) / kRouteTile;
       for (uint32_t i = blockIdx.x * kRouteThreads + tid; i < nseg; i += gridDim.x * kRouteThreads) p.seg_counts[i] = 0;
       for (uint32_t i = blockIdx.x * kRouteThreads + tid; i < nseg * (kRouteTile / kWarpSeg); i += gridDim.x * kRouteThreads)
@@ -490,9 +490,9 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactPar
         next = 0;
       }
       if (work) {
-        if (h == 0) {
-          list_in = nullptr;
-          count = p.range_n;
+        if (h == 0) {  // the batch: its position range, or the caller's selection
+          list_in = p.sel0;
+          count = p.sel0 ? *p.sel0_count : p.range_n;
         } else {
           list_in = p.lists + static_cast<uint64_t>(h) * p.list_stride;
           count = p.counts[h];
@@ -616,6 +616,7 @@ __global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactPar
           if ((mask >> j) & 1u) {
             p.out_ids[pos] = sid[j];
             p.out_bbox[pos] = sbb[j];
+            if (p.out_pos) p.out_pos[pos] = sidx[j];
             ++pos;
           }
         }

@@ -64,6 +64,7 @@ struct Slot {
   cudaEvent_t uploaded = nullptr;
   uint64_t* out_ids = nullptr;
   uint64_t* out_bbox = nullptr;
+  uint32_t* out_pos = nullptr;  // the survivors' input positions (hydro_batch_output)
   BatchRec* rec = nullptr;
   BatchRec rec_host{};
   bool rec_valid = false;
@@ -233,6 +234,7 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   if (cfg->sync_every < 1) return set_err(HYDRO_EINVAL, "sync_every >= 1");
   if (cfg->balance != HYDRO_BALANCE_ROUND_ROBIN && cfg->balance != HYDRO_BALANCE_DATA_AWARE)
     return set_err(HYDRO_EINVAL, "unknown balance mode");
+  if (cfg->max_sms < 0) return set_err(HYDRO_EINVAL, "max_sms >= 0");
   if (cfg->frames) {
     if (cfg->n_frames < 1 || cfg->frame_h < 1 || cfg->frame_w < 1 || (cfg->frame_w % 16) != 0 ||
         cfg->frame_h > 65535 || cfg->frame_w > 65535)
@@ -245,6 +247,7 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   ctx->cfg = *cfg;
   CU(cudaSetDevice(cfg->device));
   CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+  if (cfg->max_sms > 0) ctx->num_sms = std::min(ctx->num_sms, static_cast<int>(cfg->max_sms));  // SM budget
   if (cfg->stream) {
     ctx->stream = static_cast<cudaStream_t>(cfg->stream);
   } else {
@@ -562,6 +565,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
     CU(cudaEventCreateWithFlags(&s.uploaded, cudaEventDisableTiming));
     CU(cudaMalloc(&s.out_ids, sizeof(uint64_t) * maxb));
     CU(cudaMalloc(&s.out_bbox, sizeof(uint64_t) * maxb));
+    CU(cudaMalloc(&s.out_pos, sizeof(uint32_t) * maxb));
     CU(cudaMalloc(&s.rec, sizeof(BatchRec)));
   }
   ctx->frozen = true;
@@ -610,6 +614,7 @@ static CompactParams compact_base(hydro_ctx* ctx, const uint64_t* id, const uint
   c.bits_stride = ctx->bits_stride;
   c.out_ids = sl.out_ids;
   c.out_bbox = sl.out_bbox;
+  c.out_pos = sl.out_pos;
   c.id = id;
   c.bbox = bb;
   c.st = ctx->st;
@@ -730,6 +735,10 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
   if (s != HYDRO_OK) return s;
   if (t->n < 0 || t->n > ctx->cfg.max_batch_tuples) return set_err(HYDRO_EINVAL, "n must be in [0, max_batch_tuples]");
   if (t->n > 0 && (!t->id || !t->frame_id || !t->bbox || !t->label)) return set_err(HYDRO_EINVAL, "NULL column");
+  const bool has_sel = t->sel != nullptr;
+  if (has_sel && (!t->sel_count || !t->on_device))
+    return set_err(HYDRO_EINVAL, "a selection needs sel_count and device columns");
+  if (has_sel && ctx->cfg.policy == HYDRO_POLICY_REUSE) return set_err(HYDRO_EINVAL, "REUSE does not take selections");
   if ((s = freeze(ctx)) != HYDRO_OK) return s;
   int si = -1;
   for (int i = 0; i < static_cast<int>(ctx->slots.size()); ++i)
@@ -759,10 +768,11 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
     bb = sl.s_bbox;
     lab = sl.s_label;
   }
+  if (t->wait_event) CU(cudaStreamWaitEvent(ctx->stream, static_cast<cudaEvent_t>(t->wait_event), 0));
   CU(cudaMemsetAsync(sl.rec, 0, sizeof(BatchRec), ctx->stream));
   const int P = static_cast<int>(ctx->preds.size());
   uint64_t warm = 0;
-  if (ctx->warmup_pending) {
+  if (ctx->warmup_pending && !has_sel) {  // a selection batch never runs the warmup slice
     // ---- warmup slice (R8): every predicate on the slice, no short-circuit
     warm = std::min<uint64_t>(n, static_cast<uint64_t>(ctx->cfg.warmup_tuples));
     for (int k = 0; k < P; ++k) {
@@ -835,6 +845,8 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
     r.hop = h;
     r.range_base = rest_base;
     r.range_n = rest_n;
+    r.sel0 = t->sel;
+    r.sel0_count = t->sel_count;
     if ((s = launch_route(ctx, r, rest_n)) != HYDRO_OK) return s;
     if (n_lin > 0) {  // the classifier kernel(s) the context needs; each exits unless its kind is the hop's
       ClsParams c = cls_base(ctx, fr, bb);
@@ -842,6 +854,8 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
       c.hop = h;
       c.range_base = rest_base;
       c.range_n = rest_n;
+      c.sel0 = t->sel;
+      c.sel0_count = t->sel_count;
       if (ctx->has_linear && (s = launch_cls(ctx, c, rest_n, kClsLinear)) != HYDRO_OK) return s;
       if (ctx->has_mlp && (s = launch_cls(ctx, c, rest_n, kClsMlp)) != HYDRO_OK) return s;
       if (ctx->has_hsv && (s = launch_cls(ctx, c, rest_n, kClsHsv)) != HYDRO_OK) return s;
@@ -851,6 +865,8 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
     k2.hop = h;
     k2.range_base = rest_base;
     k2.range_n = rest_n;
+    k2.sel0 = t->sel;
+    k2.sel0_count = t->sel_count;
     k2.emit_count = &sl.rec->total_count;
     k2.emit_offset = &sl.rec->warm_count;
     if ((s = launch_compact(ctx, k2, rest_n)) != HYDRO_OK) return s;
@@ -890,6 +906,17 @@ hydro_status hydro_batch_count(hydro_ctx* ctx, int64_t batch_id, int64_t* count)
   hydro_status s = wait_slot(ctx, sl);
   if (s != HYDRO_OK) return s;
   *count = sl->rec_host.total_count;
+  return HYDRO_OK;
+}
+
+hydro_status hydro_batch_output(hydro_ctx* ctx, int64_t batch_id, const uint32_t** positions,
+                                const uint32_t** count, void** done_event) {
+  if (!ctx || !positions || !count || !done_event) return set_err(HYDRO_EINVAL, "NULL argument");
+  Slot* sl = find_slot(ctx, batch_id);
+  if (!sl) return set_err(HYDRO_EINVAL, "unknown or already collected batch_id");
+  *positions = sl->out_pos;
+  *count = &sl->rec->total_count;
+  *done_event = static_cast<void*>(sl->done);
   return HYDRO_OK;
 }
 
@@ -1096,6 +1123,7 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
     if (s.uploaded) cudaEventDestroy(s.uploaded);
     cudaFree(s.out_ids);
     cudaFree(s.out_bbox);
+    cudaFree(s.out_pos);
     cudaFree(s.rec);
     cudaFree(s.s_id);
     cudaFree(s.s_frame);

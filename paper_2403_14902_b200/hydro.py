@@ -40,7 +40,7 @@ class hydro_config(C.Structure):
                 ("max_batch_tuples", C.c_int64), ("max_inflight", C.c_int32), ("rank", C.c_int32),
                 ("world", C.c_int32), ("sync_every", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("frames", C.c_void_p), ("n_frames", C.c_int32), ("frame_h", C.c_int32), ("frame_w", C.c_int32),
-                ("balance", C.c_int32)]
+                ("balance", C.c_int32), ("max_sms", C.c_int32)]
 
 
 class hydro_predicate_desc(C.Structure):
@@ -54,7 +54,8 @@ class hydro_predicate_desc(C.Structure):
 
 class hydro_tuples(C.Structure):
     _fields_ = [("id", C.c_void_p), ("frame_id", C.c_void_p), ("bbox", C.c_void_p), ("label", C.c_void_p),
-                ("n", C.c_int64), ("on_device", C.c_int32)]
+                ("n", C.c_int64), ("on_device", C.c_int32), ("sel", C.c_void_p), ("sel_count", C.c_void_p),
+                ("wait_event", C.c_void_p)]
 
 
 class hydro_pred_stats(C.Structure):
@@ -87,6 +88,8 @@ _SIGS = {
     "hydro_batch_count": ([_P, C.c_int64, C.POINTER(C.c_int64)], C.c_int32),
     "hydro_collect_results": ([_P, C.c_int64, _P, _P, C.c_int64, C.POINTER(C.c_int64), C.c_int32], C.c_int32),
     "hydro_release_batch": ([_P, C.c_int64], C.c_int32),
+    "hydro_batch_output": ([_P, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)],
+                           C.c_int32),
     "hydro_batch_info": ([_P, C.c_int64, C.POINTER(hydro_batch_report)], C.c_int32),
     "hydro_get_stats": ([_P, C.c_int32, C.POINTER(hydro_pred_stats)], C.c_int32),
     "hydro_get_order": ([_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int32),
@@ -197,6 +200,13 @@ def hydro_release_batch(ctx, batch_id: int):
     _check(lib().hydro_release_batch(ctx, batch_id))
 
 
+def hydro_batch_output(ctx, batch_id: int):
+    """(positions, count, done_event) device pointers of an uncollected batch's survivors."""
+    pos, cnt, ev = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    _check(lib().hydro_batch_output(ctx, batch_id, C.byref(pos), C.byref(cnt), C.byref(ev)))
+    return pos.value, cnt.value, ev.value
+
+
 def hydro_batch_info(ctx, batch_id: int) -> hydro_batch_report:
     r = hydro_batch_report()
     _check(lib().hydro_batch_info(ctx, batch_id, C.byref(r)))
@@ -274,7 +284,7 @@ class Eddy:
                  cost_source: str = "measured", decay_gamma: float = 0.5, prior_selectivity: float = 0.5,
                  warmup_tuples: int = 65536, max_batch_tuples: int = 1 << 20, max_inflight: int = 4,
                  rank: int = 0, world: int = 1, sync_every: int = 1, nccl_unique_id: Optional[bytes] = None,
-                 stream: Optional[torch.cuda.Stream] = None, balance: str = "round_robin"):
+                 stream: Optional[torch.cuda.Stream] = None, balance: str = "round_robin", max_sms: int = 0):
         cfg = hydro_config_default()
         cfg.device = device
         cfg.stream = (stream or torch.cuda.current_stream(device)).cuda_stream
@@ -287,6 +297,7 @@ class Eddy:
         cfg.max_inflight = max_inflight
         cfg.rank, cfg.world, cfg.sync_every = rank, world, sync_every
         cfg.balance = BALANCE[balance]
+        cfg.max_sms = max_sms
         self._uid = None
         if nccl_unique_id is not None:
             self._uid = C.create_string_buffer(nccl_unique_id, 128)
@@ -352,9 +363,17 @@ class Eddy:
     def set_fixed_order(self, order: Sequence[int]):
         hydro_set_fixed_order(self.ctx, list(order))
 
-    def submit(self, tuples) -> int:
+    def submit(self, tuples, sel=None, wait_event=None) -> int:
+        """sel = (positions_ptr, count_ptr, capacity): device selection of the columns (R29)."""
         t = make_tuples_struct(tuples.id, tuples.frame_id, tuples.bbox, tuples.label)
+        if sel is not None:
+            t.sel, t.sel_count, t.n = sel[0], sel[1], int(sel[2])
+        if wait_event is not None:
+            t.wait_event = wait_event
         return hydro_submit_batch(self.ctx, t)
+
+    def batch_output(self, batch_id: int):
+        return hydro_batch_output(self.ctx, batch_id)
 
     def count(self, batch_id: int) -> int:
         return hydro_batch_count(self.ctx, batch_id)

@@ -607,3 +607,74 @@ def test_data_aware_bounds_match_oracle_and_rows_unchanged(n):
     ref_bb = tup["bbox"][v_ref].astype(np.int64)
     for balance, (ids, bb) in rows.items():
         _assert_rows(ids, bb, ref_ids, ref_bb)
+
+
+# ------------------------------------------------------------- concurrent workers (f3, R29)
+
+def _paper_example_preds(units=256):
+    """DogColorClassifier cost 1 / selectivity 0.6, DogBreedClassifier cost 2 /
+    selectivity 0.1, as HASH stand-ins with 1 : 2 rounds."""
+    return [hash_pred(31, 0.6, units=units, name="colour (cost 1, sel 0.6)"),
+            hash_pred(32, 0.1, units=2 * units, name="breed (cost 2, sel 0.1)")]
+
+
+def test_selection_chain_between_contexts_on_two_streams():
+    """Context B evaluates only the survivors of context A (hydro_batch_output -> selection batch,
+    B's stream waiting on A's done event): B's rows and A's survivor positions equal the oracle's."""
+    from paper_2403_14902_b200.hydro import Eddy
+    preds = _paper_example_preds(32)
+    t = workload("cfg1", n=50_000).tuples()
+    V = O.evaluate_all(preds, t)
+    tup = O.as_numpy_tuples(t)
+    td = t.to("cuda")
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    ea = Eddy(policy="fixed", warmup_tuples=0, max_batch_tuples=len(t), stream=sa, max_sms=74)
+    eb = Eddy(policy="fixed", warmup_tuples=0, max_batch_tuples=len(t), stream=sb, max_sms=74)
+    ea.add_predicate(preds[0])
+    eb.add_predicate(preds[1])
+    ba = ea.submit(td)
+    pos, cnt, ev = ea.batch_output(ba)
+    bb_ = eb.submit(td, sel=(pos, cnt, len(t)), wait_event=ev)
+    info = eb.batch_info(bb_)
+    ids, bbox = eb.collect(bb_)
+    keep = V[0] & V[1]
+    _assert_rows(ids.numpy().astype(np.uint64), bbox.numpy().astype(np.int64), tup["id"][keep], tup["bbox"][keep])
+    n_a = int(V[0].sum())
+    pos_t = torch.empty(n_a, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    import ctypes
+    import os
+
+    import nvidia.cuda_runtime as ncr
+    cudart = ctypes.CDLL(os.path.join(list(ncr.__path__)[0], "lib", "libcudart.so.12"))
+    assert cudart.cudaMemcpy(ctypes.c_void_p(pos_t.data_ptr()), ctypes.c_void_p(pos), ctypes.c_size_t(4 * n_a), 3) == 0
+    assert np.array_equal(pos_t.cpu().numpy(), np.where(V[0])[0])
+    assert info["tuples_in"] == [n_a] and info["tuples_passed"] == [int(keep.sum())]
+    ea.release(ba)
+    ea.close()
+    eb.close()
+
+
+@pytest.mark.parametrize("policy,expected", [("cost", [0, 1]), ("score", [1, 0]), ("selectivity", [1, 0])])
+def test_concurrent_eddy_orders_and_rows(policy, expected):
+    """The paper's example on two concurrent workers (one SM partition each): the warmup measures
+    costs and selectivities, cost-driven routing puts the cheap predicate first and score /
+    selectivity-driven routing the selective one; whatever the order, the
+    streamed batches return exactly the oracle's rows."""
+    from paper_2403_14902_b200.pipeline import ConcurrentEddy
+    preds = _paper_example_preds()
+    t = workload("cfg1", n=160_000).tuples()
+    V = O.evaluate_all(preds, t)
+    tup = O.as_numpy_tuples(t)
+    td = t.to("cuda")
+    ce = ConcurrentEddy(preds, policy=policy, max_batch_tuples=1 << 16)
+    order = ce.warmup(td.slice(0, 1 << 16))
+    assert order == expected, (order, ce.cost_per_tuple, ce.selectivity)
+    assert abs(ce.selectivity[0] - 0.6) < 0.02 and abs(ce.selectivity[1] - 0.1) < 0.02
+    batches = [td.slice(a, min(a + 40_000, len(t))) for a in range(0, len(t), 40_000)]
+    rows = ce.run(batches)
+    ids = np.concatenate([r[0].numpy().astype(np.uint64) for r in rows])
+    bbs = np.concatenate([r[1].numpy().astype(np.int64) for r in rows])
+    keep = V[0] & V[1]
+    _assert_rows(ids, bbs, tup["id"][keep], tup["bbox"][keep])
+    ce.close()

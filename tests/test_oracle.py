@@ -522,3 +522,62 @@ def test_input_size_costs_and_loads_conserve_the_total():
     assert sum(O.range_loads(cost, b)) == int(cost.sum()) == sum(O.round_robin_loads(cost, 16))
     # on this heavy-tailed input size the data-aware cut beats round-robin's worst worker
     assert max(O.range_loads(cost, b)) < max(O.round_robin_loads(cost, 16))
+
+
+# ------------------------------------------------------------- concurrent workers (f3, R29)
+
+def _masks(n, k):
+    for c in itertools.combinations(range(n), k):
+        yield [i in c for i in range(n)]
+
+
+def test_cost_route_timeline_paper_numbers():
+    """PAPER.md:349-359 (Fig. cost_route): 10 items, DogColorClassifier cost 1 / selectivity 0.6,
+    DogBreedClassifier cost 2 / selectivity 0.1, the two predicates on concurrent workers.
+    Breed first: 20 time units (stage 1 is the bottleneck); colour first: 14 for the paper's
+    arrival pattern, and 13..17 over every pattern of 6 passing items -- always below 20."""
+    breed_first = [O.two_stage_completion(10, 2, 1, m) for m in _masks(10, 1)]
+    assert breed_first[:-1] == [20.0] * 9 and breed_first[-1] == 21.0  # the last item passing adds its cost
+    colour_first = [O.two_stage_completion(10, 1, 2, m) for m in _masks(10, 6)]
+    assert O.two_stage_completion(10, 1, 2, [i + 1 in (2, 4, 6, 8, 9, 10) for i in range(10)]) == 14.0
+    assert min(colour_first) == 13.0 and max(colour_first) == 17.0
+    assert max(colour_first) < min(breed_first)
+    # the routing decisions the paper derives: score picks breed (2/0.9 < 1/0.4), cost picks colour
+    assert O.score(2, 0.1) < O.score(1, 0.6)
+
+
+def test_fig7_cost_driven_never_worse_all_masks():
+    """PAPER.md:548-556 (Fig. 7): A = 10 ms, B = 20 ms, sel_B in {0.1, 0.5, 0.9}, sel_A 0.1..0.9;
+    cost-driven routing (A first) is never slower than selectivity- or score-driven routing:
+    over every arrival pattern, A-first's worst completion <= the other order's best."""
+    n = 10
+    for sB in (0.1, 0.5, 0.9):
+        for sA in [x / 10 for x in range(1, 10)]:
+            kA, kB = round(sA * n), round(sB * n)
+            a_first = [O.two_stage_completion(n, 10, 20, m) for m in _masks(n, kA)]
+            b_first = [O.two_stage_completion(n, 20, 10, m) for m in _masks(n, kB)]
+            assert max(a_first) <= min(b_first)
+
+
+def test_flow_shop_closed_form_and_item_reduction():
+    """Identical batches (a, b): makespan = a + b + (B - 1) * max(a, b) (closed form); one item per
+    batch reduces the flow shop to the item timeline."""
+    for a, b, B in ((1.0, 2.0, 10), (3.0, 1.0, 7), (2.5, 2.5, 4)):
+        assert O.flow_shop_makespan([[a, b]] * B) == a + b + (B - 1) * max(a, b)
+    rng = np.random.default_rng(3)
+    for _ in range(50):
+        m = rng.random(12) < 0.4
+        rows = [[1.0, 2.0 if x else 0.0] for x in m]
+        fs = O.flow_shop_makespan(rows)
+        assert fs == O.two_stage_completion(12, 1.0, 2.0, m)
+
+
+def test_pipeline_stage_times_counts_follow_eager_materialization():
+    """Stage i of a batch is charged for exactly the tuples its predecessors passed (the counts of
+    sequential_eval), times the worker's time per tuple."""
+    rng = np.random.default_rng(5)
+    V = rng.random((3, 1000)) < np.array([[0.6], [0.1], [0.5]])
+    rows = O.pipeline_stage_times(V, [1, 0, 2], 250, [1.0, 2.0, 3.0])
+    for b, row in enumerate(rows):
+        n_in, _, _ = O.sequential_eval(V[:, 250 * b:250 * (b + 1)], [1, 0, 2])
+        assert row == [n_in[1] * 2.0, n_in[0] * 1.0, n_in[2] * 3.0]
