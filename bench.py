@@ -662,8 +662,9 @@ def run_concurrent(args):
         return sorted(ms)[len(ms) // 2], out
 
     modes = {}
-    for policy in ("cost", "score", "selectivity"):
-        ce = ConcurrentEddy(preds, policy=policy, max_batch_tuples=batch)
+    for policy in ("cost", "score", "selectivity", "cost@grid", "score@grid"):
+        pol, part = (policy.split("@") + ["green"])[:2]
+        ce = ConcurrentEddy(preds, policy=pol, max_batch_tuples=batch, partition=part)
         order = ce.warmup(batches[0])
         c, sel = list(ce.cost_per_tuple), list(ce.selectivity)
         ms, out = timed(lambda: sum(r[0] for r in ce.run(batches, res_ids, res_bb)), ce.streams)
@@ -677,7 +678,7 @@ def run_concurrent(args):
             rows.append(row)
         modes[policy] = {"ms_per_pass": ms, "order": [preds[k]["name"] for k in order], "results": out,
                          "cycles_per_tuple_per_worker": [round(x, 2) for x in c], "selectivity": [round(x, 4) for x in sel],
-                         "model_cycles": _flow_shop(rows), "sms": ce.sms}
+                         "model_cycles": _flow_shop(rows), "sms": ce.sms, "partition": part}
         ce.close()
     seq = H.Eddy(policy="score", warmup_tuples=65536, max_batch_tuples=batch, max_inflight=4, stream=main)
     for p in preds:
@@ -704,7 +705,8 @@ def run_concurrent(args):
            "warmup": 1, "ms_per_step": cost["ms_per_pass"], "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
            "config": {"workload": "concurrent: colour HASH (512 rounds, sel 0.6) and breed HASH (1024 rounds, sel "
-                                  "0.1), one worker per predicate on 74 SMs each, 16M tuples in 1M batches"},
+                                  "0.1), one worker per predicate on its own half of the SMs (green-context "
+                                  "partitions; @grid = grid caps only), 16M tuples in 1M batches"},
            "modes": modes,
            "speedup_cost_vs_score": score["ms_per_pass"] / cost["ms_per_pass"],
            "model_speedup_cost_vs_score": score["model_cycles"] / cost["model_cycles"],

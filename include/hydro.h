@@ -130,8 +130,15 @@ typedef struct {
                                 SMs (default ROUND_ROBIN)                                     */
   int32_t max_sms;           /* SM budget of the context's persistent kernels (grids capped at
                                 this many SMs; 0 = all).  Two contexts with budgets summing to
-                                the SM count on two streams run as concurrent workers on
-                                (approximately) disjoint SM partitions   */
+                                the SM count on two streams run side by side, but the
+                                hardware may place their CTAs on any SM                       */
+  int32_t sm_groups, sm_group; /* sm_groups >= 2: the context is a worker on its own SM
+                                partition -- group sm_group of an even split of the device's
+                                SMs into sm_groups CUDA green-context partitions; the context
+                                then runs on a library-owned stream of that partition (stream
+                                above is ignored) and its grids fit the partition.  Contexts
+                                with distinct sm_group values run on disjoint SMs (SURVEY.md
+                                §8(f) f3, R29).  0 or 1: the whole device                      */
 } hydro_config;
 
 typedef struct {

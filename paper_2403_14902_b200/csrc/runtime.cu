@@ -8,6 +8,7 @@
 //                           K4(h)  classifier hop (exits unless order[h] is LINEAR)
 //   K1(P)   final compaction + emit of (id, bbox) in input order
 //   K5      fold (+ NCCL all-reduce of the deltas when world > 1)
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -25,6 +26,42 @@
 using namespace hydro;
 
 static thread_local std::string g_last_error;
+
+// Driver-API entry points for green contexts, resolved through the runtime (cudaGetDriverEntryPoint)
+// so the library keeps no link-time dependency on libcuda (it still loads on a machine without a
+// driver; only sm_groups > 1 needs them).
+struct GreenApi {
+  decltype(&cuDeviceGet) deviceGet = nullptr;
+  decltype(&cuDeviceGetDevResource) getDevResource = nullptr;
+  decltype(&cuDevSmResourceSplitByCount) splitByCount = nullptr;
+  decltype(&cuDevResourceGenerateDesc) generateDesc = nullptr;
+  decltype(&cuGreenCtxCreate) ctxCreate = nullptr;
+  decltype(&cuGreenCtxStreamCreate) streamCreate = nullptr;
+  decltype(&cuGreenCtxDestroy) ctxDestroy = nullptr;
+  decltype(&cuGetErrorString) errorString = nullptr;
+  bool ok = false;
+};
+static const GreenApi& green_api() {
+  static GreenApi g = [] {
+    GreenApi a;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      // the ABI version of the prototypes in the cuda.h this file is compiled against
+      return cudaGetDriverEntryPointByVersion(name, fn, CUDA_VERSION, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess;
+    };
+    a.ok = get("cuDeviceGet", reinterpret_cast<void**>(&a.deviceGet)) &&
+           get("cuDeviceGetDevResource", reinterpret_cast<void**>(&a.getDevResource)) &&
+           get("cuDevSmResourceSplitByCount", reinterpret_cast<void**>(&a.splitByCount)) &&
+           get("cuDevResourceGenerateDesc", reinterpret_cast<void**>(&a.generateDesc)) &&
+           get("cuGreenCtxCreate", reinterpret_cast<void**>(&a.ctxCreate)) &&
+           get("cuGreenCtxStreamCreate", reinterpret_cast<void**>(&a.streamCreate)) &&
+           get("cuGreenCtxDestroy", reinterpret_cast<void**>(&a.ctxDestroy)) &&
+           get("cuGetErrorString", reinterpret_cast<void**>(&a.errorString));
+    return a;
+  }();
+  return g;
+}
 
 static hydro_status set_err(hydro_status s, const std::string& msg) {
   g_last_error = msg;
@@ -87,6 +124,7 @@ struct hydro_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // host -> device uploads of batch k+1 overlap batch k
   bool own_stream = false;
+  CUgreenCtx green = nullptr;  // sm_groups > 1: the SM partition the context's stream runs on
   int num_sms = 0;
   int k1_occ = 1;
   bool k1_compact = false;  // a HASH predicate expensive enough for K1's compaction path
@@ -235,6 +273,8 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   if (cfg->balance != HYDRO_BALANCE_ROUND_ROBIN && cfg->balance != HYDRO_BALANCE_DATA_AWARE)
     return set_err(HYDRO_EINVAL, "unknown balance mode");
   if (cfg->max_sms < 0) return set_err(HYDRO_EINVAL, "max_sms >= 0");
+  if (cfg->sm_groups < 0 || (cfg->sm_groups > 1 && (cfg->sm_group < 0 || cfg->sm_group >= cfg->sm_groups)))
+    return set_err(HYDRO_EINVAL, "sm_group must be in [0, sm_groups)");
   if (cfg->frames) {
     if (cfg->n_frames < 1 || cfg->frame_h < 1 || cfg->frame_w < 1 || (cfg->frame_w % 16) != 0 ||
         cfg->frame_h > 65535 || cfg->frame_w > 65535)
@@ -248,7 +288,38 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   CU(cudaSetDevice(cfg->device));
   CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
   if (cfg->max_sms > 0) ctx->num_sms = std::min(ctx->num_sms, static_cast<int>(cfg->max_sms));  // SM budget
-  if (cfg->stream) {
+  if (cfg->sm_groups > 1) {
+    // a worker on its own SM partition (CUDA green context): group sm_group of an even split
+    const GreenApi& G = green_api();
+    CUdevice dev;
+    CUdevResource all, rem;
+    std::vector<CUdevResource> groups(static_cast<size_t>(cfg->sm_groups));
+    unsigned int ng = static_cast<unsigned int>(cfg->sm_groups);
+    CUdevResourceDesc desc;
+    CUstream gs = nullptr;
+    CUresult r = G.ok ? CUDA_SUCCESS : CUDA_ERROR_NOT_SUPPORTED;
+    const char* step = "driver entry points";
+    if (r == CUDA_SUCCESS) r = G.deviceGet(&dev, cfg->device), step = "cuDeviceGet";
+    if (r == CUDA_SUCCESS) r = G.getDevResource(dev, &all, CU_DEV_RESOURCE_TYPE_SM), step = "cuDeviceGetDevResource";
+    // even split; the SM count of a group a multiple of 8 (the co-scheduling granularity)
+    const unsigned int per = r == CUDA_SUCCESS ? (all.sm.smCount / static_cast<unsigned int>(cfg->sm_groups)) & ~7u : 0u;
+    if (r == CUDA_SUCCESS) r = G.splitByCount(groups.data(), &ng, &all, &rem, 0, per), step = "cuDevSmResourceSplitByCount";
+    if (r == CUDA_SUCCESS && ng <= static_cast<unsigned int>(cfg->sm_group)) r = CUDA_ERROR_INVALID_VALUE, step = "group count";
+    if (r == CUDA_SUCCESS) r = G.generateDesc(&desc, &groups[cfg->sm_group], 1), step = "cuDevResourceGenerateDesc";
+    if (r == CUDA_SUCCESS) r = G.ctxCreate(&ctx->green, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM), step = "cuGreenCtxCreate";
+    if (r == CUDA_SUCCESS) r = G.streamCreate(&gs, ctx->green, CU_STREAM_NON_BLOCKING, 0), step = "cuGreenCtxStreamCreate";
+    if (r != CUDA_SUCCESS) {
+      const char* msg = nullptr;
+      if (G.errorString) G.errorString(r, &msg);
+      hydro_status s = set_err(HYDRO_ECUDA, std::string("green context SM partition (") + step + "): " +
+                                                (msg ? msg : "driver API unavailable"));
+      hydro_destroy(ctx);
+      return s;
+    }
+    ctx->stream = reinterpret_cast<cudaStream_t>(gs);
+    ctx->own_stream = true;
+    ctx->num_sms = std::min(ctx->num_sms, static_cast<int>(groups[cfg->sm_group].sm.smCount));
+  } else if (cfg->stream) {
     ctx->stream = static_cast<cudaStream_t>(cfg->stream);
   } else {
     CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
@@ -1160,6 +1231,7 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
     cudaStreamDestroy(ctx->copy_stream);
   }
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->green) green_api().ctxDestroy(ctx->green);
   delete ctx;
   return HYDRO_OK;
 }

@@ -40,7 +40,7 @@ class hydro_config(C.Structure):
                 ("max_batch_tuples", C.c_int64), ("max_inflight", C.c_int32), ("rank", C.c_int32),
                 ("world", C.c_int32), ("sync_every", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("frames", C.c_void_p), ("n_frames", C.c_int32), ("frame_h", C.c_int32), ("frame_w", C.c_int32),
-                ("balance", C.c_int32), ("max_sms", C.c_int32)]
+                ("balance", C.c_int32), ("max_sms", C.c_int32), ("sm_groups", C.c_int32), ("sm_group", C.c_int32)]
 
 
 class hydro_predicate_desc(C.Structure):
@@ -284,7 +284,8 @@ class Eddy:
                  cost_source: str = "measured", decay_gamma: float = 0.5, prior_selectivity: float = 0.5,
                  warmup_tuples: int = 65536, max_batch_tuples: int = 1 << 20, max_inflight: int = 4,
                  rank: int = 0, world: int = 1, sync_every: int = 1, nccl_unique_id: Optional[bytes] = None,
-                 stream: Optional[torch.cuda.Stream] = None, balance: str = "round_robin", max_sms: int = 0):
+                 stream: Optional[torch.cuda.Stream] = None, balance: str = "round_robin", max_sms: int = 0,
+                 sm_groups: int = 0, sm_group: int = 0):
         cfg = hydro_config_default()
         cfg.device = device
         cfg.stream = (stream or torch.cuda.current_stream(device)).cuda_stream
@@ -298,6 +299,7 @@ class Eddy:
         cfg.rank, cfg.world, cfg.sync_every = rank, world, sync_every
         cfg.balance = BALANCE[balance]
         cfg.max_sms = max_sms
+        cfg.sm_groups, cfg.sm_group = sm_groups, sm_group
         self._uid = None
         if nccl_unique_id is not None:
             self._uid = C.create_string_buffer(nccl_unique_id, 128)

@@ -5,8 +5,9 @@ cost/(1-selectivity) score) when "workers associated with these predicates can r
 (PAPER.md:327-330): the cheaper stage first keeps the expensive stage -- the bottleneck of the
 pipeline -- fed with fewer tuples per unit of time.
 
-On one B200 the workers are hydro contexts, one per predicate, each with its own CUDA stream and an
-SM budget (``max_sms``) so their persistent kernels run side by side on disjoint SM partitions.  A
+On one B200 the workers are hydro contexts, one per predicate, each on its own SM partition (a CUDA
+green context: ``sm_groups`` / ``sm_group``) with its own stream, so their kernels run side by side on
+disjoint SMs.  A
 routing batch visits the workers in the order the policy picks; worker ``order[i+1]`` reads the
 survivors of worker ``order[i]`` straight from device memory (``hydro_batch_output`` -> a selection
 batch), its stream waiting on the producer batch's done event, so batch b+1's first stage overlaps
@@ -47,7 +48,8 @@ class ConcurrentEddy:
     workers in the policy's order, consecutive batches overlapping on different workers."""
 
     def __init__(self, preds: Sequence[Dict], *, frames: Optional[torch.Tensor] = None, policy: str = "cost",
-                 max_batch_tuples: int = 1 << 20, sms: Optional[Sequence[int]] = None, depth: int = 3):
+                 max_batch_tuples: int = 1 << 20, sms: Optional[Sequence[int]] = None, depth: int = 3,
+                 partition: str = "green"):
         if policy not in POLICIES:
             raise ValueError(f"policy must be one of {POLICIES}")
         n_sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
@@ -60,9 +62,12 @@ class ConcurrentEddy:
         self.streams = [torch.cuda.Stream() for _ in range(P)]
         self.workers = []
         for k, p in enumerate(preds):
+            # "green": worker k owns SM group k of an even split (CUDA green contexts: disjoint SMs);
+            # "grid": the grids are only capped at the budget (the CTAs may land on any SM)
+            green = partition == "green"
             e = Eddy(frames=frames, policy="fixed", cost_source="measured", warmup_tuples=0,
                      max_batch_tuples=max_batch_tuples, max_inflight=depth + 2, stream=self.streams[k],
-                     max_sms=int(sms[k]))
+                     max_sms=0 if green else int(sms[k]), sm_groups=P if green else 0, sm_group=k if green else 0)
             e.add_predicate(p)
             self.workers.append(e)
         self.sms = sms
