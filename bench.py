@@ -448,6 +448,28 @@ def run_route(args):
                         "k1_launches": k1_n, "k2_launches": k2_n},
            "clocks": clk.summary()}
     e.close()
+    # routing + compaction alone (no UDF arithmetic): label='dog' then emit; K1 reads the label
+    # column (2 B/tuple), K2 reads the survivors' id + bbox and writes the (id, bbox) rows
+    e = H.Eddy(policy="score", warmup_tuples=65536, max_batch_tuples=batch, max_inflight=4, stream=stream)
+    e.add_predicate(label_pred())
+    run_steps(2)
+    torch.cuda.synchronize()
+    e.set_kernel_timing(True)
+    outs.clear()
+    run_steps(args.steps)
+    l1_ms, l1_n = e.kernel_time(0)
+    l2_ms, l2_n = e.kernel_time(3)
+    e.set_kernel_timing(False)
+    e.close()
+    lbytes = tuples * 2 + 32 * sum(outs)
+    lach = lbytes / ((l1_ms + l2_ms) / 1000.0) / 1e9
+    out["roofline_label_only"] = {
+        "kernel": "hydro_route_kernel + hydro_compact_kernel on label='dog' alone (routing + compaction, no UDF "
+                  "arithmetic)", "bound": "hbm", "achieved": lach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+        "frac": lach / peaks["hbm_gbs"], "algorithmic_bytes_per_tuple": lbytes / tuples,
+        "k1_ms_per_step": l1_ms / args.steps, "k2_ms_per_step": l2_ms / args.steps,
+        "k1_gbs": tuples * 2 / (l1_ms / 1000.0) / 1e9, "k2_gbs": 32 * sum(outs) / (l2_ms / 1000.0) / 1e9,
+        "launches": l1_n + l2_n}
     print(json.dumps(out))
 
 
