@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kRouteThreads, kCompact ? 2 : HYDRO_K1_MINB) h
   __shared__ uint64_t s_cids[kCompact ? kRouteThreads / 32 : 1][kWarpSeg];  // compacted alive ids
   __shared__ uint32_t s_vw[kRouteTile / 32];                 // their fail bits, one word per 32 entries
   __shared__ uint32_t s_cw[kRouteThreads / 32];              // warp alive counts
-  __shared__ int32_t s_work, s_nrun, s_n_and, s_need_id, s_need_bbox, s_need_label;
+  __shared__ int32_t s_work, s_nrun, s_n_and, s_need_id, s_need_bbox, s_need_label, s_lean;
   __shared__ const uint32_t* s_list_in;
   __shared__ const uint32_t* s_and[kMaxPred];
   __shared__ uint32_t* s_bits_out;
@@ -162,6 +162,9 @@ __global__ void __launch_bounds__(kRouteThreads, kCompact ? 2 : HYDRO_K1_MINB) h
     s_need_id = need_id;
     s_need_bbox = need_bbox;
     s_need_label = need_label;
+    // lean path: one LABEL_EQ predicate over a position range (the usual first hop): no id / bbox
+    // columns, no verdict cache, no AND inputs
+    s_lean = (nrun == 1 && need_label && !need_id && !need_bbox && n_and == 0 && list_in == nullptr) ? 1 : 0;
     s_hop = hop;
   }
   __syncthreads();
@@ -195,6 +198,84 @@ __global__ void __launch_bounds__(kRouteThreads, kCompact ? 2 : HYDRO_K1_MINB) h
   const bool need_id = s_need_id, need_bbox = s_need_bbox, need_label = s_need_label;
 
   uint32_t buf = 0;
+  if (s_lean) {
+    // ---- lean path (label test only): one 16-byte label load, 8 compares, the bitmap and the
+    // counts per thread per tile; statistics kept in registers and reduced once at the end.  The
+    // cost charged is the same quantity as the generic path's, sum over warp-tiles of
+    // cycles x items evaluated (t0 / t1 are the warp's clock, so summing per thread gives it).
+    const uint32_t want = static_cast<uint32_t>(s_pred[0].label_value) & 0xFFFFu;
+    const bool lab_aligned = ((reinterpret_cast<uintptr_t>(p.label + base)) & 15u) == 0;
+    uint32_t n_in = 0, n_pass = 0;
+    unsigned long long cost = 0;
+    // the labels of kLeanTiles tiles are loaded before any is evaluated: 64 bytes in flight per
+    // thread (one 16-byte load per tile left the kernel latency-bound at ~1 TB/s)
+    constexpr int kLeanTiles = 4;
+    for (uint32_t t0i = blockIdx.x; t0i < num_tiles; t0i += kLeanTiles * gridDim.x) {
+      uint32_t labs[kLeanTiles][kRouteItems / 2];
+      uint32_t avail[kLeanTiles];
+#pragma unroll
+      for (int u = 0; u < kLeanTiles; ++u) {
+        const uint32_t t = t0i + u * gridDim.x;
+        const uint32_t p0 = t * kRouteTile + tid * kRouteItems;
+        avail[u] = (t < num_tiles && p0 < count) ? min(count - p0, static_cast<uint32_t>(kRouteItems)) : 0u;
+        labs[u][0] = labs[u][1] = labs[u][2] = labs[u][3] = 0u;
+        if (avail[u] == static_cast<uint32_t>(kRouteItems) && lab_aligned) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.label + base + p0));
+          labs[u][0] = v.x; labs[u][1] = v.y; labs[u][2] = v.z; labs[u][3] = v.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < kRouteItems; ++j)
+            if (static_cast<uint32_t>(j) < avail[u])
+              labs[u][j >> 1] |= static_cast<uint32_t>(__ldg(p.label + base + p0 + j)) << (16 * (j & 1));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kLeanTiles; ++u) {
+        const uint32_t t = t0i + u * gridDim.x;
+        if (t >= num_tiles) break;  // CTA-uniform
+        const uint32_t p0 = t * kRouteTile + tid * kRouteItems;
+        const uint32_t in_mask = avail[u] >= static_cast<uint32_t>(kRouteItems) ? 0xFFu : ((1u << avail[u]) - 1u);
+        const long long c0 = clock64();
+        uint32_t mask = in_mask;
+#pragma unroll
+        for (int j = 0; j < kRouteItems; ++j)
+          if (((labs[u][j >> 1] >> (16 * (j & 1))) & 0xFFFFu) != want) mask &= ~(1u << j);
+        const long long c1 = clock64();
+        n_in += __popc(in_mask);
+        n_pass += __popc(mask);
+        cost += static_cast<unsigned long long>(c1 - c0) * __popc(in_mask);
+        uint32_t wbits = mask << (8 * (lane & 3));
+        wbits |= __shfl_xor_sync(kFull, wbits, 1);
+        wbits |= __shfl_xor_sync(kFull, wbits, 2);
+        if ((lane & 3) == 0 && p0 < count) bits_out[p0 >> 5] = wbits;
+        const uint32_t wc = __reduce_add_sync(kFull, __popc(mask));
+        if (lane == 0) {
+          s_warp_cnt[buf][warp] = wc;
+          p.warp_counts[t * (kRouteTile / kWarpSeg) + warp] = wc;
+        }
+        __syncthreads();  // the other buffer is rewritten only after the next tile's barrier
+        if (tid == 0) {
+          uint32_t tot = 0;
+#pragma unroll
+          for (int w = 0; w < kRouteThreads / 32; ++w) tot += s_warp_cnt[buf][w];
+          p.seg_counts[t] = tot;
+        }
+        buf ^= 1u;
+      }
+    }
+    if (p.collect_stats) {
+      n_in = __reduce_add_sync(kFull, n_in);
+      n_pass = __reduce_add_sync(kFull, n_pass);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cost += __shfl_xor_sync(kFull, cost, o);
+      if (lane == 0) {
+        s_in[warp][0] = n_in;
+        s_pass[warp][0] = n_pass;
+        s_comp[warp][0] = n_in;
+        s_cost[warp][0] = cost;
+      }
+    }
+  } else  // ---- generic path: any run of cheap predicates, range or list input, caches, AND inputs
   for (uint32_t t = blockIdx.x; t < num_tiles; t += gridDim.x, buf ^= 1u) {
     const uint32_t p0 = t * kRouteTile + tid * kRouteItems;
     uint32_t idx[kRouteItems];
@@ -456,7 +537,10 @@ __global__ void __launch_bounds__(kRouteThreads, kCompact ? 2 : HYDRO_K1_MINB) h
 // thousand L2-resident words), so no CTA ever waits for another.  Within a segment each warp owns
 // a 256-position slice whose offset comes from the evaluator's per-warp counts: warp scan only,
 // no block barrier; survivors are written in input order.
-__global__ void __launch_bounds__(kRouteThreads) hydro_compact_kernel(CompactParams p) {
+#ifndef HYDRO_K2_MINB
+#define HYDRO_K2_MINB 1
+#endif
+__global__ void __launch_bounds__(kRouteThreads, HYDRO_K2_MINB) hydro_compact_kernel(CompactParams p) {
   __shared__ uint32_t s_red[kRouteThreads / 32];
   __shared__ int32_t s_work, s_emit;
   __shared__ const uint32_t* s_list_in;
