@@ -493,6 +493,171 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
   cp_async_wait<0>();
 }
 
+// AREA crops, staged (R10, cfg4): the bins of crop row g of a tuple cover its source rows
+// ys .. ye-1 (ys = g*h/64, ye = ceil((g+1)h/64)).  The converter walks "items" (g, quad it, source
+// row i < hbq = the quad's largest bin height): each item's 4 row segments are copied with
+// coalesced 16-byte cp.async into a staging slot kQD items ahead (the nearest path's ring); lane
+// (r, j) adds the pixels of its 8 bins (output pixels j + 8k) found in that row, and after the
+// quad's last row divides by the bin sizes (one f32 division, bf16 RNE) and stores the A row.
+template <bool kDbg, int kP, int kQD>
+__device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* ctrl, uint32_t lim, uint32_t pos0,
+                                                  uint32_t crank, int cu, int lane, uint32_t slots, uint32_t a_ring,
+                                                  uint32_t row_pitch, bool fp16, const RowMeta& mm, uint32_t& gg) {
+  constexpr int kQS = kQD + 1;
+  const int r = lane >> 3, j = lane & 7;
+  const uint8_t* frames = p.frames;
+  const uint32_t my_src = mm.row0 + mm.seg_lo;
+  const uint32_t my_len = (lane < 16 && mm.valid) ? mm.seg_len : 0u;
+  const uint32_t my_h = (lane < 16 && mm.valid) ? static_cast<uint32_t>(mm.h) : 0u;
+  // bin height of crop row g for the tuple of row r of quad it, and the quad's largest
+  auto bin_h = [&](uint32_t g, int it) {
+    const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, 4 * it + r);
+    return ((g + 1u) * h + 63u) / 64u - (g * h) / 64u;
+  };
+  // (at least 1: a quad of rows past the tile's count still stores its (masked) A rows)
+  auto quad_rows = [&](uint32_t g, int it) { return max(__reduce_max_sync(0xFFFFFFFFu, bin_h(g, it)), 1u); };
+  struct Cursor {
+    uint32_t g, i, hbq;
+    int it;
+  };
+  auto advance = [&](Cursor& c) {
+    if (++c.i < c.hbq) return;
+    c.i = 0;
+    if (++c.it == 4) {
+      c.it = 0;
+      ++c.g;
+    }
+    c.hbq = c.g < static_cast<uint32_t>(kGroups) ? quad_rows(c.g, c.it) : 1u;
+  };
+  // stage item c into a slot: row r's segment of source row ys(g) + i (nothing when i >= its bins)
+  auto stage_item = [&](const Cursor& c, uint32_t slot) {
+    if (c.g < static_cast<uint32_t>(kGroups)) {
+      const int src_lane = 4 * c.it + r;
+      const uint32_t len = __shfl_sync(0xFFFFFFFFu, my_len, src_lane);
+      const uint32_t off = __shfl_sync(0xFFFFFFFFu, my_src, src_lane);
+      const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
+      const uint32_t ys = (c.g * h) / 64u, hb = ((c.g + 1u) * h + 63u) / 64u - ys;
+      if (c.i < hb) {
+        const uint8_t* row = frames + (off + (ys + c.i) * row_pitch);
+        const uint32_t dst = slots + slot * kQuadSlotBytes + r * kSegPitch;
+        const uint32_t nch = len >> 4;
+#pragma unroll
+        for (int cc = 0; cc < 7; ++cc)
+          if (j + 8u * cc < nch) cp_async16(dst + 16u * j + 128u * cc, row + 16u * j + 128u * cc);
+      }
+    }
+    cp_async_commit();  // one group per item (possibly empty): uniform wait_group counting
+  };
+  Cursor cs{0u, 0u, quad_rows(0u, 0), 0};
+  Cursor cc = cs;
+  uint32_t slot_stage = 0, slot_use = 0;
+#pragma unroll
+  for (int k = 0; k < kQD; ++k) {
+    stage_item(cs, slot_stage);
+    advance(cs);
+    slot_stage = slot_stage + 1 == kQS ? 0 : slot_stage + 1;
+  }
+  uint32_t sum[8][3];
+  uint32_t set = 0, a_set = 0;
+  while (cc.g < static_cast<uint32_t>(kGroups)) {
+    if (cc.it == 0 && cc.i == 0) {  // first item of group g: its A stages must be free
+      set = (gg & 1u) * kKBlocksPerGroup;
+      const uint32_t aph = (gg >> 1) & 1u;
+#pragma unroll
+      for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_wait(&ctrl->empty_a[set + kbr], aph ^ 1u);
+      a_set = a_ring + set * kAKBlockBytes;
+    }
+    if (cc.i == 0) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum[k][0] = sum[k][1] = sum[k][2] = 0u;
+    }
+    stage_item(cs, slot_stage);
+    advance(cs);
+    slot_stage = slot_stage + 1 == kQS ? 0 : slot_stage + 1;
+    cp_async_wait<kQD>();  // this thread's copies of item cc have landed
+    __syncwarp();          // ... and every lane's
+    const int src_lane = 4 * cc.it + r;
+    const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src_lane);
+    const uint32_t w = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
+    const uint32_t slo = __shfl_sync(0xFFFFFFFFu, mm.seg_lo, src_lane);
+    const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
+    const uint32_t ys = (cc.g * h) / 64u, hb = ((cc.g + 1u) * h + 63u) / 64u - ys;
+    uint32_t xs[8], bw[8], bwmax = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t dx = static_cast<uint32_t>(j) + 8u * k;
+      xs[k] = x0 + ((dx * w) >> 6);
+      bw[k] = x0 + (((dx + 1u) * w + 63u) >> 6) - xs[k];
+      bwmax = max(bwmax, bw[k]);
+    }
+    if (cc.i < hb) {  // this row belongs to the tuple's bins: add it
+      const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kSegPitch;
+      for (uint32_t t = 0; t < bwmax; ++t) {
+        uint32_t w0[8], w1[8], sh[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const bool on = t < bw[k];
+          const uint32_t o = 3u * (xs[k] + t) - slo;
+          const uint32_t a = (seg + o) & ~3u;
+          sh[k] = o << 3;
+          w0[k] = on ? lds32(a) : 0u;
+          w1[k] = on ? lds32(a + 4) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t pxl = __funnelshift_r(w0[k], w1[k], sh[k]);
+          sum[k][0] += pxl & 0xFFu;
+          sum[k][1] += (pxl >> 8) & 0xFFu;
+          sum[k][2] += (pxl >> 16) & 0xFFu;
+        }
+      }
+    }
+    slot_use = slot_use + 1 == kQS ? 0 : slot_use + 1;
+    __syncwarp();  // the slot is refilled kQD items later
+    if (cc.i + 1 == cc.hbq) {  // the quad's last row: bin means -> A row m
+      const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * cc.it + r);
+      const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
+      uint16_t* dbg = (kDbg && p.dbg_crops && pos0 + m < lim)
+                          ? p.dbg_crops + static_cast<uint64_t>(pos0 + m) * kFeatures + cc.g * 192 + 3 * j
+                          : nullptr;
+      uint32_t half[24];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float cnt = static_cast<float>(max(hb * bw[k], 1u));
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const __nv_bfloat16 b = __float2bfloat16_rn(__fdiv_rn(static_cast<float>(sum[k][ch]), cnt));
+          const uint32_t bbits = __bfloat16_as_ushort(b);
+          half[3 * k + ch] =
+              fp16 ? static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__bfloat162float(b)))) : bbits;
+          if (kDbg && dbg) dbg[24 * k + ch] = static_cast<uint16_t>(bbits);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const uint32_t c = 3u * j + t;
+        const uint32_t addr = row_base + (c >> 3) * kAKBlockBytes + (((c & 7u) ^ (m & 7u)) << 4);
+        sts128(addr, half[8 * t] | (half[8 * t + 1] << 16), half[8 * t + 2] | (half[8 * t + 3] << 16),
+               half[8 * t + 4] | (half[8 * t + 5] << 16), half[8 * t + 6] | (half[8 * t + 7] << 16));
+      }
+      if (cc.it == 3) {  // group g complete: publish its A stages
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) {
+            if (kP == 2 && crank != 0) mbar_arrive_leader(&ctrl->full_a[set + kbr]);
+            else mbar_arrive(&ctrl->full_a[set + kbr]);
+          }
+        }
+        ++gg;
+      }
+    }
+    advance(cc);
+  }
+  cp_async_wait<0>();
+}
+
 // Converter warps (shared by the linear and the MLP classifier kernels): cp.async-staged crop-row
 // segments -> pixels -> the swizzled K-major A ring, one K-group (crop row g of all 128 tuples of
 // the CTA's M-tile) at a time, full_a / empty_a handshake with the MMA issuer.
@@ -514,7 +679,11 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
     // rows' metadata: lane l < 16 holds row 16*cu + l
     const RowMeta mm = load_meta(p, list_in, base, pos0 + cu * kConvRows + (lane & 15), lane < 16 ? tw.lim : 0u);
     // a tile with a crop wider than a staging slot (rare) runs the gather-staging variant
-    if (__any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes)))
+    const bool any_wide =
+        __any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes));
+    if (kArea && area && !any_wide)
+      convert_tile_area<kDbg, kP, kQD>(p, ctrl, tw.lim, pos0, crank, cu, lane, slots, a_ring, row_pitch, fp16, mm, gg);
+    else if (any_wide)
       convert_tile<kDbg, kArea, kP, kQD, true>(p, ctrl, list_in, tw.lim, pos0, crank, cu, lane, slots, a_ring, row_pitch,
                                                area, fp16, mm, gg);
     else
