@@ -678,3 +678,33 @@ def test_concurrent_eddy_orders_and_rows(policy, expected):
     keep = V[0] & V[1]
     _assert_rows(ids, bbs, tup["id"][keep], tup["bbox"][keep])
     ce.close()
+
+
+def test_concurrent_eddy_classifier_workers_and_empty_stage():
+    """Concurrent workers whose predicates are the dog query's two linear heads (K4 reading a
+    selection at hop 0), on two SM partitions: the streamed rows equal the oracle's for both
+    orders; a first stage that passes nothing hands an empty selection to the second."""
+    from paper_2403_14902_b200.pipeline import ConcurrentEddy
+    w = workload("cfg2", small=True, n=6000)
+    frames = w.frames()
+    preds = [w.preds[2], w.preds[1]]  # colour (C=10), breed (C=120)
+    t = w.tuples()
+    V = O.evaluate_all(preds, t, frames.numpy())
+    tup = O.as_numpy_tuples(t)
+    keep = V[0] & V[1]
+    td = t.to("cuda")
+    batches = [td.slice(a, min(a + 1500, len(t))) for a in range(0, len(t), 1500)]
+    for policy in ("cost", "selectivity"):
+        ce = ConcurrentEddy(preds, frames=frames.cuda(), policy=policy, max_batch_tuples=2048)
+        ce.warmup(batches[0])
+        rows = ce.run(batches)
+        ids = np.concatenate([r[0].numpy().astype(np.uint64) for r in rows])
+        bbs = np.concatenate([r[1].numpy().astype(np.int64) for r in rows])
+        _assert_rows(ids, bbs, tup["id"][keep], tup["bbox"][keep])
+        ce.close()
+    none = [hash_pred(41, 0.0, units=4, name="nothing passes"), hash_pred(42, 0.5, units=4)]
+    ce = ConcurrentEddy(none, policy="cost", max_batch_tuples=4096)
+    ce.order = [0, 1]  # the empty stage first
+    rows = ce.run([workload("cfg1", n=4000).tuples().to("cuda")])
+    assert len(rows) == 1 and len(rows[0][0]) == 0
+    ce.close()
