@@ -643,13 +643,18 @@ def _flow_shop(rows):
 
 def run_concurrent(args):
     """--workload concurrent: cost-driven routing over concurrent workers (SURVEY.md §8(f) f3;
-    PAPER.md:320-365; R29).  The paper's example (colour: cost 1, selectivity 0.6; breed:
-    cost 2, selectivity 0.1) as HASH stand-ins with 512 / 1024 rounds, 16M tuples
-    in 1M-tuple routing batches.  Each predicate is a worker on half of the SMs (own context, stream,
-    SM budget); batches flow through the workers in the order of the policy, consecutive batches
-    overlapping.  Timed: cost-driven, score-driven and selectivity-driven routing, plus the
-    sequential eddy on all SMs (one context, score policy) for reference, and the flow-shop model's
-    prediction from the warmup's measured costs and selectivities."""
+    PAPER.md:320-365; R29).  Two scenarios, each predicate a worker on its own half of the
+    SMs (own context, stream and green-context SM partition); batches flow through the workers in
+    the policy's order, consecutive batches overlapping:
+      example: the paper's example (colour: cost 1, selectivity 0.6; breed: cost 2, selectivity
+               0.1) as HASH stand-ins with 512 / 1024 rounds, 16M tuples in 1M
+               batches (the headline line);
+      dog:     the UC1 classifiers themselves -- DogColorClassifier as the HSV heuristic and the
+               breed linear head (C=120) on 64x64 crops of a coloured-block frame pool, 2M dog
+               detections in 256K batches.
+    Timed per scenario: cost-, score- and selectivity-driven routing, and the sequential eddy on all
+    SMs (one context, score policy) for reference; plus the flow-shop model's prediction from the
+    warmup's measured costs and selectivities."""
     import torch
 
     from paper_2403_14902_b200 import build as B
@@ -659,69 +664,78 @@ def run_concurrent(args):
 
     torch.cuda.set_device(0)
     B.build()
-    n, batch, units = 16_000_000, 1 << 20, 512
-    preds = [hash_pred(31, 0.6, units=units, name="colour (cost 1, sel 0.6)"),
-             hash_pred(32, 0.1, units=2 * units, name="breed (cost 2, sel 0.1)")]
-    t = workload("cfg1", n=n).tuples(device="cuda")
-    batches = [t.slice(a, min(a + batch, n)) for a in range(0, n, batch)]
     main = torch.cuda.current_stream()
-    res_ids = torch.empty(batch, dtype=torch.int64, device="cuda")
-    res_bb = torch.empty((batch, 4), dtype=torch.int16, device="cuda")
 
-    def timed(fn, streams):
+    def timed(fn):
         fn()  # warm-up pass
         torch.cuda.synchronize()
         ms = []
         for _ in range(args.steps):
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ev0.record(main)
-            out = fn()
-            for st in streams:
-                main.wait_stream(st)
+            out = fn()  # returns after the last batch's results were collected (all work done)
             ev1.record(main)
             torch.cuda.synchronize()
             ms.append(ev0.elapsed_time(ev1))
         return sorted(ms)[len(ms) // 2], out
 
-    modes = {}
-    for policy in ("cost", "score", "selectivity", "cost@grid", "score@grid"):
-        pol, part = (policy.split("@") + ["green"])[:2]
-        ce = ConcurrentEddy(preds, policy=pol, max_batch_tuples=batch, partition=part)
-        order = ce.warmup(batches[0])
-        c, sel = list(ce.cost_per_tuple), list(ce.selectivity)
-        ms, out = timed(lambda: sum(r[0] for r in ce.run(batches, res_ids, res_bb)), ce.streams)
-        # flow-shop model: per batch, stage i sees the fraction that passed the earlier stages
-        rows = []
-        for b in batches:
-            alive, row = float(len(b)), []
-            for k in order:
-                row.append(alive * c[k])
-                alive *= sel[k]
-            rows.append(row)
-        modes[policy] = {"ms_per_pass": ms, "order": [preds[k]["name"] for k in order], "results": out,
-                         "cycles_per_tuple_per_worker": [round(x, 2) for x in c], "selectivity": [round(x, 4) for x in sel],
-                         "model_cycles": _flow_shop(rows), "sms": ce.sms, "partition": part}
-        ce.close()
-    seq = H.Eddy(policy="score", warmup_tuples=65536, max_batch_tuples=batch, max_inflight=4, stream=main)
-    for p in preds:
-        seq.add_predicate(p)
+    def scenario(preds, t, n, batch, frames=None, policies=("cost", "score", "selectivity")):
+        batches = [t.slice(a, min(a + batch, n)) for a in range(0, n, batch)]
+        res_ids = torch.empty(batch, dtype=torch.int64, device="cuda")
+        res_bb = torch.empty((batch, 4), dtype=torch.int16, device="cuda")
+        modes = {}
+        for policy in policies:
+            pol, part = (policy.split("@") + ["green"])[:2]
+            ce = ConcurrentEddy(preds, frames=frames, policy=pol, max_batch_tuples=batch, partition=part)
+            order = ce.warmup(batches[0])
+            c, sel = list(ce.cost_per_tuple), list(ce.selectivity)
+            ms, out = timed(lambda: sum(r[0] for r in ce.run(batches, res_ids, res_bb)))
+            rows = []  # flow-shop model: stage i sees the fraction the earlier stages passed
+            for b in batches:
+                alive, row = float(len(b)), []
+                for k in order:
+                    row.append(alive * c[k])
+                    alive *= sel[k]
+                rows.append(row)
+            modes[policy] = {"ms_per_pass": ms, "order": [preds[k]["name"] for k in order], "results": out,
+                             "cycles_per_tuple_per_worker": [round(x, 2) for x in c],
+                             "selectivity": [round(x, 4) for x in sel], "model_cycles": _flow_shop(rows),
+                             "sms": ce.sms, "partition": part}
+            ce.close()
+        seq = H.Eddy(frames=frames, policy="score", warmup_tuples=65536, max_batch_tuples=batch, max_inflight=4,
+                     stream=main)
+        for p in preds:
+            seq.add_predicate(p)
 
-    def seq_pass():
-        pend, tot = [], 0
-        for b in batches:
-            pend.append(seq.submit(b))
-            if len(pend) >= 3:
-                tot += H.hydro_collect_results(seq.ctx, pend.pop(0), res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
-        for bid in pend:
-            tot += H.hydro_collect_results(seq.ctx, bid, res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
-        return tot
+        def seq_pass():
+            pend, tot = [], 0
+            for b in batches:
+                pend.append(seq.submit(b))
+                if len(pend) >= 3:
+                    tot += H.hydro_collect_results(seq.ctx, pend.pop(0), res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
+            for bid in pend:
+                tot += H.hydro_collect_results(seq.ctx, bid, res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
+            return tot
 
-    ms_seq, tot_seq = timed(seq_pass, [])
-    modes["sequential_all_sms_score"] = {"ms_per_pass": ms_seq, "order": [preds[k]["name"] for k in seq.order()],
-                                         "results": tot_seq}
-    seq.close()
-    assert len({m["results"] for m in modes.values()}) == 1, modes  # the routing never changes the result
-    cost, score = modes["cost"], modes["score"]
+        ms_seq, tot_seq = timed(seq_pass)
+        modes["sequential_all_sms_score"] = {"ms_per_pass": ms_seq, "order": [preds[k]["name"] for k in seq.order()],
+                                             "results": tot_seq}
+        seq.close()
+        assert len({m["results"] for m in modes.values()}) == 1, modes  # routing never changes the result
+        return modes
+
+    n, batch, units = 16_000_000, 1 << 20, 512
+    ex_preds = [hash_pred(31, 0.6, units=units, name="colour (cost 1, sel 0.6)"),
+                hash_pred(32, 0.1, units=2 * units, name="breed (cost 2, sel 0.1)")]
+    ex = scenario(ex_preds, workload("cfg1", n=n).tuples(device="cuda"), n, batch,
+                  policies=("cost", "score", "selectivity", "cost@grid", "score@grid"))
+    wd = workload("hsv")
+    frames = wd.frames(device="cuda")
+    nd, bd = 2_000_000, 1 << 18
+    td = wd.tuples(n=nd, device="cuda")
+    dog_preds = [wd.preds[2], wd.preds[1]]  # colour (HSV heuristic), breed (linear C=120)
+    dog = scenario(dog_preds, td, nd, bd, frames=frames)
+    cost, score = ex["cost"], ex["score"]
     out = {"metric": "tuples/s through the paper's two-predicate example on concurrent workers (SURVEY.md §8(f) f3)",
            "value": n / (cost["ms_per_pass"] / 1000.0), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
            "warmup": 1, "ms_per_step": cost["ms_per_pass"], "higher_is_better": True, "scaling": "weak",
@@ -729,9 +743,13 @@ def run_concurrent(args):
            "config": {"workload": "concurrent: colour HASH (512 rounds, sel 0.6) and breed HASH (1024 rounds, sel "
                                   "0.1), one worker per predicate on its own half of the SMs (green-context "
                                   "partitions; @grid = grid caps only), 16M tuples in 1M batches"},
-           "modes": modes,
+           "modes": ex,
            "speedup_cost_vs_score": score["ms_per_pass"] / cost["ms_per_pass"],
            "model_speedup_cost_vs_score": score["model_cycles"] / cost["model_cycles"],
+           "dog_query_workers": {"workload": "DogColorClassifier (HSV heuristic) and DogBreedClassifier (linear "
+                                             "C=120) as two workers, 2M detections in 256K batches, coloured-block frames",
+                                 "modes": dog,
+                                 "tuples_per_s": {k: nd / (v["ms_per_pass"] / 1000.0) for k, v in dog.items()}},
            "paper_context": "PAPER.md:357-359: 20 (score/selectivity-driven) vs 14 (cost-driven) time units for 10 items"}
     print(json.dumps(out))
 
