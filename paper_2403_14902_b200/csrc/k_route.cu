@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kRouteThreads, kCompact ? 2 : HYDRO_K1_MINB) h
 // a 256-position slice whose offset comes from the evaluator's per-warp counts: warp scan only,
 // no block barrier; survivors are written in input order.
 #ifndef HYDRO_K2_MINB
-#define HYDRO_K2_MINB 1
+#define HYDRO_K2_MINB 4  // 64 registers: 4 CTAs per SM with the first segment preloaded (measured best of 1, 3, 4, 5, 6)
 #endif
 __global__ void __launch_bounds__(kRouteThreads, HYDRO_K2_MINB) hydro_compact_kernel(CompactParams p) {
   __shared__ uint32_t s_red[kRouteThreads / 32];
@@ -611,6 +611,32 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K2_MINB) hydro_compact_ke
   const uint32_t base = p.range_base;
   if (seg0 >= nseg && !(nseg == 0 && blockIdx.x == 0)) return;
 
+  // The first segment's rows are loaded before the prefix sum (they do not depend on it), so
+  // their DRAM latency overlaps the prefix's L2 loads.  Dense = the emit reads the thread's 8 rows
+  // contiguously (see below); the segment total comes from the evaluator's seg_counts.
+  uint32_t sidx[kRouteItems];
+  uint64_t sid[kRouteItems], sbb[kRouteItems];
+  auto dense_seg = [&](uint32_t sg, uint32_t total) {
+    const uint32_t q0 = sg * kRouteTile + tid * kRouteItems;
+    return emit && !list_in && total * 10u >= static_cast<uint32_t>(kRouteTile) && q0 + kRouteItems <= count &&
+           ((reinterpret_cast<uintptr_t>(p.id + base + q0) | reinterpret_cast<uintptr_t>(p.bbox + base + q0)) & 15u) == 0u;
+  };
+  auto load_dense = [&](uint32_t sg) {
+    const uint32_t q0 = sg * kRouteTile + tid * kRouteItems;
+    const ulonglong2* qi = reinterpret_cast<const ulonglong2*>(p.id + base + q0);
+    const ulonglong2* qb = reinterpret_cast<const ulonglong2*>(p.bbox + base + q0);
+#pragma unroll
+    for (int j = 0; j < kRouteItems / 2; ++j) {
+      const ulonglong2 a = __ldg(qi + j), b = __ldg(qb + j);
+      sid[2 * j] = a.x;
+      sid[2 * j + 1] = a.y;
+      sbb[2 * j] = b.x;
+      sbb[2 * j + 1] = b.y;
+    }
+  };
+  const bool pre = seg0 < nseg && dense_seg(seg0, __ldg(p.seg_counts + seg0));
+  if (pre) load_dense(seg0);
+
   // output offset of this CTA: survivors of every earlier segment
   uint32_t part = 0;
   {  // seg0 is a multiple of 4 (kCompactSegs): 16-byte loads, independent so they overlap
@@ -644,26 +670,12 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K2_MINB) hydro_compact_ke
       mask = (__ldg(bits + (p0 >> 5)) >> (p0 & 31)) & 0xFFu;
       if (p0 + kRouteItems > count) mask &= (1u << (count - p0)) - 1u;
     }
-    uint32_t sidx[kRouteItems];
-    uint64_t sid[kRouteItems], sbb[kRouteItems];
     // emit from a dense range segment (>= 1 in 10 positions survive): the scattered gathers would
     // touch most DRAM bursts of the id / bbox columns anyway, so read the thread's 8 rows
     // contiguously (16-byte loads, fully coalesced) and keep the survivors
-    const bool dense = emit && !list_in && seg_total * 10u >= static_cast<uint32_t>(kRouteTile) &&
-                       p0 + kRouteItems <= count &&
-                       ((reinterpret_cast<uintptr_t>(p.id + base + p0) | reinterpret_cast<uintptr_t>(p.bbox + base + p0)) &
-                        15u) == 0u;
+    const bool dense = dense_seg(sgi, seg_total);
     if (dense) {
-      const ulonglong2* qi = reinterpret_cast<const ulonglong2*>(p.id + base + p0);
-      const ulonglong2* qb = reinterpret_cast<const ulonglong2*>(p.bbox + base + p0);
-#pragma unroll
-      for (int j = 0; j < kRouteItems / 2; ++j) {
-        const ulonglong2 a = __ldg(qi + j), b = __ldg(qb + j);
-        sid[2 * j] = a.x;
-        sid[2 * j + 1] = a.y;
-        sbb[2 * j] = b.x;
-        sbb[2 * j + 1] = b.y;
-      }
+      if (!(pre && sgi == seg0)) load_dense(sgi);
 #pragma unroll
       for (int j = 0; j < kRouteItems; ++j) sidx[j] = base + p0 + j;
     } else {
