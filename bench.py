@@ -353,6 +353,12 @@ def run_gpu(args):
                     "k2_ms_per_step": k2c_ms / args.steps,
                     "k1_ms_per_step": k1_ms / args.steps, "k4_ms_per_step": k4_ms / args.steps,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"}
+        if traffic and k4_n and k4_ms > 0:
+            # the bytes K4 actually moves (ncu dram__bytes per launch, profiles/k4_dram_traffic.json)
+            # over this run's live launch time: nearest sampling touches whole DRAM bursts around
+            # the 64 sampled pixels of a row, so this exceeds the algorithmic rate above
+            tgbs = traffic / (k4_ms / k4_n / 1000.0) / 1e9
+            roofline.update({"traffic_gbs": tgbs, "traffic_frac": tgbs / peaks["hbm_gbs"]})
         if hsv:  # the HSV colour hop (K4-HSV) is ALU work: its own time and rate next to the linear hop
             roofline.update({"hsv_ms_per_step": kh_ms / args.steps, "hsv_launches": kh_n,
                              "hsv_kernel_tuples_per_s": kh_tuples / (kh_ms / 1000.0) if kh_ms > 0 else None,
