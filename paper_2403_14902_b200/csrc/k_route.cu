@@ -14,6 +14,8 @@
 // (R1, R2).
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "hydro_internal.cuh"
 
 using namespace hydro;
@@ -84,6 +86,8 @@ __device__ __forceinline__ bool k1_runs(const DevState* st, int h, int* run) {
 // K1: evaluate.  Persistent grid, tile t = positions [2048 t, 2048 t + 2048); thread = 8 positions.
 // kCompact: the context has an expensive HASH predicate (units >= kCompactUnits), so the kernel
 // carries the CTA-wide compaction path (more registers and 16 KB of shared memory)
+constexpr int kLeanMaxRun = 4;  // K1 lean path: predicates per run
+
 template <bool kCompact>
 #ifndef HYDRO_K1_MINB
 #define HYDRO_K1_MINB 3
@@ -162,9 +166,14 @@ __global__ void __launch_bounds__(kRouteThreads, kCompact ? 2 : HYDRO_K1_MINB) h
     s_need_id = need_id;
     s_need_bbox = need_bbox;
     s_need_label = need_label;
-    // lean path: one LABEL_EQ predicate over a position range (the usual first hop): no id / bbox
-    // columns, no verdict cache, no AND inputs
-    s_lean = (nrun == 1 && need_label && !need_id && !need_bbox && n_and == 0 && list_in == nullptr) ? 1 : 0;
+    // lean path: a run of at most 4 LABEL_EQ / uniform-units HASH predicates over a position range
+    // (the usual first hop), no verdict cache, no AND inputs, no per-area units, no compacted HASH
+    int lean = (nrun >= 1 && nrun <= kLeanMaxRun && !need_bbox && n_and == 0 && list_in == nullptr) ? 1 : 0;
+    for (int r = 0; r < nrun && lean; ++r) {
+      const PredDev& q = p.preds[s_run_id[r]];
+      if (q.cache_known || (q.kind == kHash && q.units >= kCompactUnits)) lean = 0;
+    }
+    s_lean = lean;
     s_hop = hop;
   }
   __syncthreads();
@@ -199,80 +208,158 @@ __global__ void __launch_bounds__(kRouteThreads, kCompact ? 2 : HYDRO_K1_MINB) h
 
   uint32_t buf = 0;
   if (s_lean) {
-    // ---- lean path (label test only): one 16-byte label load, 8 compares, the bitmap and the
-    // counts per thread per tile; statistics kept in registers and reduced once at the end.  The
-    // cost charged is the same quantity as the generic path's, sum over warp-tiles of
-    // cycles x items evaluated (t0 / t1 are the warp's clock, so summing per thread gives it).
-    const uint32_t want = static_cast<uint32_t>(s_pred[0].label_value) & 0xFFFFu;
+    // ---- lean path: the columns of kTiles tiles are loaded before any is evaluated (labels 16 B,
+    // ids 64 B per thread and tile), then each tile runs the predicates in order on 8 positions
+    // per thread (HASH branch-free: 8 independent chains), writes the bitmap and the counts.
+    // Statistics stay in registers (at most kLeanMaxRun predicates, unrolled) and are reduced
+    // once; the cost charged is the generic path's quantity, sum over warp-tiles of cycles x
+    // items evaluated (t0 / t1 are the warp's clock, so summing per thread gives it).
     const bool lab_aligned = ((reinterpret_cast<uintptr_t>(p.label + base)) & 15u) == 0;
-    uint32_t n_in = 0, n_pass = 0;
-    unsigned long long cost = 0;
-    // the labels of kLeanTiles tiles are loaded before any is evaluated: 64 bytes in flight per
-    // thread (one 16-byte load per tile left the kernel latency-bound at ~1 TB/s)
-    constexpr int kLeanTiles = 4;
-    for (uint32_t t0i = blockIdx.x; t0i < num_tiles; t0i += kLeanTiles * gridDim.x) {
-      uint32_t labs[kLeanTiles][kRouteItems / 2];
-      uint32_t avail[kLeanTiles];
+    const bool id_aligned = ((reinterpret_cast<uintptr_t>(p.id + base)) & 15u) == 0;
+    uint32_t n_in[kLeanMaxRun], n_pass[kLeanMaxRun];
+    unsigned long long cost[kLeanMaxRun];
 #pragma unroll
-      for (int u = 0; u < kLeanTiles; ++u) {
-        const uint32_t t = t0i + u * gridDim.x;
-        const uint32_t p0 = t * kRouteTile + tid * kRouteItems;
-        avail[u] = (t < num_tiles && p0 < count) ? min(count - p0, static_cast<uint32_t>(kRouteItems)) : 0u;
-        labs[u][0] = labs[u][1] = labs[u][2] = labs[u][3] = 0u;
-        if (avail[u] == static_cast<uint32_t>(kRouteItems) && lab_aligned) {
-          const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.label + base + p0));
-          labs[u][0] = v.x; labs[u][1] = v.y; labs[u][2] = v.z; labs[u][3] = v.w;
-        } else {
+    for (int r = 0; r < kLeanMaxRun; ++r) n_in[r] = n_pass[r] = 0, cost[r] = 0;
+    const uint32_t want0 = static_cast<uint32_t>(s_pred[0].label_value) & 0xFFFFu;
+    auto lean_loop = [&](auto tiles_c, auto ids_c, auto one_label_c) {
+      constexpr int kTiles = decltype(tiles_c)::value;
+      constexpr bool kIds = decltype(ids_c)::value;
+      constexpr bool kOneLabel = decltype(one_label_c)::value;  // the run is a single LABEL_EQ
+      for (uint32_t t0i = blockIdx.x; t0i < num_tiles; t0i += kTiles * gridDim.x) {
+        uint32_t labs[kTiles][kRouteItems / 2];
+        uint64_t ids[kTiles][kIds ? kRouteItems : 1];
+        uint32_t avail[kTiles];
 #pragma unroll
-          for (int j = 0; j < kRouteItems; ++j)
-            if (static_cast<uint32_t>(j) < avail[u])
-              labs[u][j >> 1] |= static_cast<uint32_t>(__ldg(p.label + base + p0 + j)) << (16 * (j & 1));
+        for (int u = 0; u < kTiles; ++u) {
+          const uint32_t t = t0i + u * gridDim.x;
+          const uint32_t p0 = t * kRouteTile + tid * kRouteItems;
+          avail[u] = (t < num_tiles && p0 < count) ? min(count - p0, static_cast<uint32_t>(kRouteItems)) : 0u;
+          const bool full = avail[u] == static_cast<uint32_t>(kRouteItems);
+          labs[u][0] = labs[u][1] = labs[u][2] = labs[u][3] = 0u;
+          if (need_label) {
+            if (full && lab_aligned) {
+              const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.label + base + p0));
+              labs[u][0] = v.x; labs[u][1] = v.y; labs[u][2] = v.z; labs[u][3] = v.w;
+            } else {
+#pragma unroll
+              for (int j = 0; j < kRouteItems; ++j)
+                if (static_cast<uint32_t>(j) < avail[u])
+                  labs[u][j >> 1] |= static_cast<uint32_t>(__ldg(p.label + base + p0 + j)) << (16 * (j & 1));
+            }
+          }
+          if constexpr (kIds) {
+            if (full && id_aligned) {
+              const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p.id + base + p0);
+#pragma unroll
+              for (int j = 0; j < kRouteItems / 2; ++j) {
+                const ulonglong2 v = __ldg(q + j);
+                ids[u][2 * j] = v.x;
+                ids[u][2 * j + 1] = v.y;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < kRouteItems; ++j)
+                ids[u][j] = static_cast<uint32_t>(j) < avail[u] ? __ldg(p.id + base + p0 + j) : 0ull;
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kTiles; ++u) {
+          const uint32_t t = t0i + u * gridDim.x;
+          if (t >= num_tiles) break;  // CTA-uniform
+          const uint32_t p0 = t * kRouteTile + tid * kRouteItems;
+          uint32_t mask = avail[u] >= static_cast<uint32_t>(kRouteItems) ? 0xFFu : ((1u << avail[u]) - 1u);
+          if constexpr (kOneLabel) {
+            const uint32_t in_mask = mask;
+            const long long c0 = clock64();
+#pragma unroll
+            for (int j = 0; j < kRouteItems; ++j)
+              if (((labs[u][j >> 1] >> (16 * (j & 1))) & 0xFFFFu) != want0) mask &= ~(1u << j);
+            const long long c1 = clock64();
+            n_in[0] += __popc(in_mask);
+            n_pass[0] += __popc(mask);
+            cost[0] += static_cast<unsigned long long>(c1 - c0) * __popc(in_mask);
+          }
+#pragma unroll
+          for (int r = 0; r < kLeanMaxRun; ++r) {
+            if (kOneLabel || r >= nrun) break;
+            const PredDev& pd = s_pred[r];
+            const uint32_t in_mask = mask;
+            const long long c0 = clock64();
+            if (pd.kind == kLabelEq) {
+              const uint32_t want = static_cast<uint32_t>(pd.label_value) & 0xFFFFu;
+#pragma unroll
+              for (int j = 0; j < kRouteItems; ++j)
+                if (((labs[u][j >> 1] >> (16 * (j & 1))) & 0xFFFFu) != want) mask &= ~(1u << j);
+            } else if constexpr (kIds) {  // HASH, uniform units, all 8 positions branch-free
+              uint32_t hv[kRouteItems];
+#pragma unroll
+              for (int j = 0; j < kRouteItems; ++j) hv[j] = static_cast<uint32_t>(splitmix64(ids[u][j] ^ pd.seed) >> 32);
+              for (int rr = 0; rr < pd.units; ++rr) {
+#pragma unroll
+                for (int j = 0; j < kRouteItems; ++j) hv[j] = fmix32(hv[j] + static_cast<uint32_t>(rr));
+              }
+              uint32_t fail = 0;
+              if (pd.thr0 == pd.thr1) {
+                if (pd.thr0 <= 0xFFFFFFFFull) {
+                  const uint32_t T32 = static_cast<uint32_t>(pd.thr0);
+#pragma unroll
+                  for (int j = 0; j < kRouteItems; ++j) fail |= (hv[j] >= T32 ? 1u : 0u) << j;
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < kRouteItems; ++j) {
+                  const uint64_t T = (ids[u][j] >= pd.drift_id) ? pd.thr1 : pd.thr0;
+                  fail |= (static_cast<uint64_t>(hv[j]) < T ? 0u : 1u) << j;
+                }
+              }
+              mask &= ~fail;
+            }
+            const long long c1 = clock64();
+            n_in[r] += __popc(in_mask);
+            n_pass[r] += __popc(mask);
+            cost[r] += static_cast<unsigned long long>(c1 - c0) * __popc(in_mask);
+          }
+          uint32_t wbits = mask << (8 * (lane & 3));
+          wbits |= __shfl_xor_sync(kFull, wbits, 1);
+          wbits |= __shfl_xor_sync(kFull, wbits, 2);
+          if ((lane & 3) == 0 && p0 < count) bits_out[p0 >> 5] = wbits;
+          const uint32_t wc = __reduce_add_sync(kFull, __popc(mask));
+          if (lane == 0) {
+            s_warp_cnt[buf][warp] = wc;
+            p.warp_counts[t * (kRouteTile / kWarpSeg) + warp] = wc;
+          }
+          __syncthreads();  // the other buffer is rewritten only after the next tile's barrier
+          if (tid == 0) {
+            uint32_t tot = 0;
+#pragma unroll
+            for (int w = 0; w < kRouteThreads / 32; ++w) tot += s_warp_cnt[buf][w];
+            p.seg_counts[t] = tot;
+          }
+          buf ^= 1u;
         }
       }
-#pragma unroll
-      for (int u = 0; u < kLeanTiles; ++u) {
-        const uint32_t t = t0i + u * gridDim.x;
-        if (t >= num_tiles) break;  // CTA-uniform
-        const uint32_t p0 = t * kRouteTile + tid * kRouteItems;
-        const uint32_t in_mask = avail[u] >= static_cast<uint32_t>(kRouteItems) ? 0xFFu : ((1u << avail[u]) - 1u);
-        const long long c0 = clock64();
-        uint32_t mask = in_mask;
-#pragma unroll
-        for (int j = 0; j < kRouteItems; ++j)
-          if (((labs[u][j >> 1] >> (16 * (j & 1))) & 0xFFFFu) != want) mask &= ~(1u << j);
-        const long long c1 = clock64();
-        n_in += __popc(in_mask);
-        n_pass += __popc(mask);
-        cost += static_cast<unsigned long long>(c1 - c0) * __popc(in_mask);
-        uint32_t wbits = mask << (8 * (lane & 3));
-        wbits |= __shfl_xor_sync(kFull, wbits, 1);
-        wbits |= __shfl_xor_sync(kFull, wbits, 2);
-        if ((lane & 3) == 0 && p0 < count) bits_out[p0 >> 5] = wbits;
-        const uint32_t wc = __reduce_add_sync(kFull, __popc(mask));
-        if (lane == 0) {
-          s_warp_cnt[buf][warp] = wc;
-          p.warp_counts[t * (kRouteTile / kWarpSeg) + warp] = wc;
-        }
-        __syncthreads();  // the other buffer is rewritten only after the next tile's barrier
-        if (tid == 0) {
-          uint32_t tot = 0;
-#pragma unroll
-          for (int w = 0; w < kRouteThreads / 32; ++w) tot += s_warp_cnt[buf][w];
-          p.seg_counts[t] = tot;
-        }
-        buf ^= 1u;
-      }
-    }
+    };
+    if (need_id)
+      lean_loop(std::integral_constant<int, 2>{}, std::true_type{}, std::false_type{});
+    else if (nrun == 1)
+      lean_loop(std::integral_constant<int, 4>{}, std::false_type{}, std::true_type{});
+    else
+      lean_loop(std::integral_constant<int, 4>{}, std::false_type{}, std::false_type{});
     if (p.collect_stats) {
-      n_in = __reduce_add_sync(kFull, n_in);
-      n_pass = __reduce_add_sync(kFull, n_pass);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) cost += __shfl_xor_sync(kFull, cost, o);
-      if (lane == 0) {
-        s_in[warp][0] = n_in;
-        s_pass[warp][0] = n_pass;
-        s_comp[warp][0] = n_in;
-        s_cost[warp][0] = cost;
+      for (int r = 0; r < kLeanMaxRun; ++r) {
+        const uint32_t a = __reduce_add_sync(kFull, n_in[r]);
+        const uint32_t b = __reduce_add_sync(kFull, n_pass[r]);
+        unsigned long long c = cost[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+        if (lane == 0 && r < nrun) {
+          s_in[warp][r] = a;
+          s_pass[warp][r] = b;
+          s_comp[warp][r] = a;
+          s_cost[warp][r] = c;
+        }
       }
     }
   } else  // ---- generic path: any run of cheap predicates, range or list input, caches, AND inputs
