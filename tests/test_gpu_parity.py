@@ -708,3 +708,41 @@ def test_concurrent_eddy_classifier_workers_and_empty_stage():
     rows = ce.run([workload("cfg1", n=4000).tuples().to("cuda")])
     assert len(rows) == 1 and len(rows[0][0]) == 0
     ce.close()
+
+
+def test_new_abi_error_paths():
+    """Selections, batch outputs, balance and SM partitions reject invalid use with EINVAL and
+    leave the context usable (hydro.h conventions)."""
+    from paper_2403_14902_b200.hydro import Eddy, HydroError, hydro_batch_output
+    t = workload("cfg1", n=1000).tuples().to("cuda")
+    with pytest.raises(HydroError) as ex:
+        Eddy(policy="fixed", warmup_tuples=0, max_batch_tuples=1024, sm_groups=2, sm_group=2)
+    assert ex.value.status == -1
+    with pytest.raises(HydroError) as ex:
+        Eddy(policy="fixed", warmup_tuples=0, max_batch_tuples=1024, balance="data_aware", max_sms=-1)
+    assert ex.value.status == -1
+    e = Eddy(policy="fixed", warmup_tuples=0, max_batch_tuples=1024)
+    e.add_predicate(hash_pred(1, 0.5))
+    with pytest.raises(HydroError) as ex:
+        hydro_batch_output(e.ctx, 12345)
+    assert ex.value.status == -1
+    b = e.submit(t)
+    pos, cnt, ev = e.batch_output(b)
+    with pytest.raises(HydroError) as ex:  # a selection needs its device count
+        e.submit(t, sel=(pos, 0, len(t)))
+    assert ex.value.status == -1
+    b2 = e.submit(t, sel=(pos, cnt, len(t)), wait_event=ev)  # a selection of the context's own output
+    V = O.evaluate_all([hash_pred(1, 0.5)], O.as_numpy_tuples(workload("cfg1", n=1000).tuples()))
+    ids, _ = e.collect(b2)
+    assert np.array_equal(ids.numpy().astype(np.uint64), O.as_numpy_tuples(workload("cfg1", n=1000).tuples())["id"][V[0]])
+    e.collect(b)
+    e.close()
+    r = Eddy(policy="reuse", warmup_tuples=0, max_batch_tuples=1024)
+    r.add_predicate(hash_pred(1, 0.5))
+    rb = r.submit(t)
+    rpos, rcnt, rev = r.batch_output(rb)
+    with pytest.raises(HydroError) as ex:  # REUSE probes a position range: no selections
+        r.submit(t, sel=(rpos, rcnt, len(t)))
+    assert ex.value.status == -1
+    r.collect(rb)
+    r.close()
