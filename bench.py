@@ -760,6 +760,102 @@ def run_concurrent(args):
     print(json.dumps(out))
 
 
+def run_small(args):
+    """--workload small: the latency- and adaptation-bound configs.
+    cfg1: 10k tuples, two HASH predicates (sel 0.5 / 0.1, 1 / 10 units), STATIC statistics, one batch:
+          microseconds per batch (submit -> rows on the host), median over repetitions.
+    cfg3: 1M tuples in 64K batches, three HASH predicates (2 / 4 / 8 units) whose selectivities swap
+          at id 500,000 (0.9, 0.5, 0.1 -> 0.1, 0.5, 0.9): tuples/s, the batches the score policy takes
+          to reach the post-drift optimal order, and the realized cost (units x tuples evaluated,
+          from the per-batch counters) against each half's optimum E(pi*) = sum_i c_i prod_{j<i} s_j."""
+    import itertools
+
+    import torch
+
+    from paper_2403_14902_b200 import build as B
+    from paper_2403_14902_b200 import hydro as H
+    from synth import workload
+
+    torch.cuda.set_device(0)
+    B.build()
+    stream = torch.cuda.current_stream()
+    # ---- cfg1 latency
+    w1 = workload("cfg1")
+    t1 = w1.tuples(device="cuda")
+    e = H.Eddy(policy="static", warmup_tuples=0, max_batch_tuples=len(t1), stream=stream)
+    for p in w1.preds:
+        e.add_predicate(p)
+    for _ in range(20):
+        e.collect(e.submit(t1))
+    lat, dev = [], []
+    for _ in range(200):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        h0 = time.perf_counter()
+        ev0.record(stream)
+        b = e.submit(t1)
+        ev1.record(stream)
+        ids, _ = e.collect(b)
+        lat.append((time.perf_counter() - h0) * 1e6)
+        dev.append(ev0.elapsed_time(ev1) * 1e3)
+    n1 = len(ids)
+    launches = e.launch_count()
+    e.close()
+    # ---- cfg3 adaptation
+    w3 = workload("cfg3")
+    n3, b3 = w3.n, w3.batch_tuples
+    t3 = w3.tuples(device="cuda")
+    units = [p["units"] for p in w3.preds]
+    sel_before, sel_after = [0.9, 0.5, 0.1], [0.1, 0.5, 0.9]
+
+    def e_cost(order, sel):
+        tot, alive = 0.0, 1.0
+        for k in order:
+            tot += units[k] * alive
+            alive *= sel[k]
+        return tot
+
+    best_before = min(itertools.permutations(range(3)), key=lambda o: e_cost(o, sel_before))
+    best_after = min(itertools.permutations(range(3)), key=lambda o: e_cost(o, sel_after))
+    res = {}
+    for policy in ("score", "static"):
+        e = H.Eddy(policy=policy, warmup_tuples=w3.warmup_tuples, max_batch_tuples=b3, stream=stream)
+        for p in w3.preds:
+            e.add_predicate(p)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        infos, total = [], 0
+        for a in range(0, n3, b3):
+            bid = e.submit(t3.slice(a, min(a + b3, n3)))
+            infos.append(e.batch_info(bid))
+            total += len(e.collect(bid)[0])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        e.close()
+        drift_batch = (n3 // 2) // b3
+        lag = next((i - drift_batch for i in range(drift_batch, len(infos))
+                    if tuple(infos[i]["order_used"]) == tuple(best_after)), None)
+        realized = sum(sum(u * x for u, x in zip(units, inf["tuples_in"])) for inf in infos)
+        optimal = sum(e_cost(best_before if (i * b3) < n3 // 2 else best_after, sel_before if (i * b3) < n3 // 2 else sel_after)
+                      * min(b3, n3 - i * b3) for i in range(len(infos)))
+        res[policy] = {"tuples_per_s": n3 / (ms / 1000.0), "ms": ms, "results": total,
+                       "orders": [inf["order_used"] for inf in infos], "adaptation_lag_batches": lag,
+                       "realized_cost_units": realized, "optimal_cost_units": optimal,
+                       "regret": realized / optimal}
+    out = {"metric": "latency (cfg1) and adaptation (cfg3) of the eddy (SURVEY.md §8(d))",
+           "value": statistics.median(lat), "unit": "us/batch", "n_gpus": 1, "steps": 200, "warmup": 20,
+           "ms_per_step": statistics.median(lat) / 1000.0, "higher_is_better": False, "scaling": "weak",
+           "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+           "config": {"workload": "cfg1: 10k tuples, HASH 0.5/0.1 (1/10 units), STATIC, one batch; cfg3: 1M tuples, "
+                                  "64K batches, selectivity drift at id 500k"},
+           "cfg1": {"us_per_batch_host": statistics.median(lat), "us_per_batch_device": statistics.median(dev),
+                    "results": n1, "launches_total": launches},
+           "cfg3": {"best_order_before": list(best_before), "best_order_after": list(best_after), **res}}
+    print(json.dumps(out))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -768,7 +864,7 @@ def main():
     ap.add_argument("--impl", default="hydro", choices=["hydro", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute", "mlp", "uc2", "hsv", "area", "concurrent"],
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute", "mlp", "uc2", "hsv", "area", "concurrent", "small"],
                     help="cfg2 = the BASELINE metric (default); rroute = K1 HBM evidence run; "
                          "mlp = cfg2 with the 12288-512-120 MLP breed head (SURVEY.md §8(f) f1, tensor roofline)")
     args = ap.parse_args()
@@ -784,6 +880,8 @@ def main():
         run_area(args)
     elif args.workload == "concurrent":
         run_concurrent(args)
+    elif args.workload == "small":
+        run_small(args)
     else:
         run_gpu(args)
 
