@@ -86,6 +86,7 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
+#ifdef HYDRO_PRED_LDS
 // predicated load: lanes with !pred issue no shared-memory access (and cause no bank conflict)
 __device__ __forceinline__ uint32_t lds32_if(uint32_t addr, bool pred) {
   uint32_t v = 0;
@@ -93,9 +94,7 @@ __device__ __forceinline__ uint32_t lds32_if(uint32_t addr, bool pred) {
                : "+r"(v) : "r"(addr), "r"(static_cast<uint32_t>(pred)));
   return v;
 }
-__device__ __forceinline__ void sts32(uint32_t addr, uint32_t a) {
-  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(a) : "memory");
-}
+#endif
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
