@@ -140,10 +140,13 @@ def test_score_policy_multi_batch_counters_and_fold_replay(small_dog):
 
 
 def test_cfg3_selectivity_drift_reorders():
+    """Selectivities swap at id 500k: rows exact, and the score order follows the drift.  Costs are
+    the declared 2 / 4 / 8 units so the order depends only on the counted selectivities
+    (deterministic; with measured cycle costs the same test is timing-dependent, R6)."""
     w = workload("cfg3", n=1_000_000)
     t = w.tuples()
     V, ref_ids, ref_bbox, _ = oracle_result(w, t, None)
-    e = make_eddy(w, None, policy="score", warmup=65536, max_batch=w.batch_tuples)
+    e = make_eddy(w, None, policy="score", cost_source="declared", warmup=65536, max_batch=w.batch_tuples)
     ids, bbs, infos = run_stream(e, t.to("cuda"), w.batch_tuples)
     _assert_rows(ids, bbs, ref_ids, ref_bbox)
     drift_batch = 500_000 // w.batch_tuples
