@@ -665,7 +665,9 @@ def test_concurrent_eddy_orders_and_rows(policy, expected):
     selectivity-driven routing the selective one; whatever the order, the
     streamed batches return exactly the oracle's rows."""
     from paper_2403_14902_b200.pipeline import ConcurrentEddy
-    preds = _paper_example_preds()
+    # the paper's selectivities with a 1 : 1.5 cost ratio: the policies' choices keep a wide margin
+    # against cycle-count noise (score: 1.5/0.9 = 1.67 vs 1/0.4 = 2.5; the paper's 1 : 2 is 2.22 vs 2.5)
+    preds = [hash_pred(31, 0.6, units=256, name="colour (sel 0.6)"), hash_pred(32, 0.1, units=384, name="breed (sel 0.1)")]
     t = workload("cfg1", n=160_000).tuples()
     V = O.evaluate_all(preds, t)
     tup = O.as_numpy_tuples(t)
