@@ -7,7 +7,7 @@
 // 32 tuples of one verdict-bitmap word, one tuple at a time: lane l takes output pixels l and
 // l + 32 of every crop row (two aligned 32-bit loads from the L1-cached frame row, funnel shift),
 // keeps 10 per-lane class counters packed 4 x 8 bits per register (a lane sees <= 128 pixels of a
-// tuple), then one warp reduction per class.  Divisions are exact in fp32 (numerators < 2^24).
+// tuple), then one warp reduction per class.  The HSV thresholds are evaluated without divisions.
 #include <algorithm>
 
 #include "hydro_internal.cuh"
@@ -19,42 +19,43 @@ namespace {
 constexpr int kHsvThreads = 256;
 constexpr uint32_t kFullMask = 0xFFFFFFFFu;
 
-// floor(a / b) for b > 0, |a| < 2^22: an approximate reciprocal puts the quotient within 1 of the
-// floor, one remainder test corrects it (exact integer result)
-__device__ __forceinline__ int floor_div(int a, int b) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(static_cast<float>(b)));
-  int q = static_cast<int>(floorf(static_cast<float>(a) * r));
-  const int rem = a - q * b;
-  q += rem < 0 ? -1 : (rem >= b ? 1 : 0);
-  return q;
-}
-// round-half-up integer quotient floor(num / den + 1/2), den > 0
-__device__ __forceinline__ int div_round_half_up(int num, int den) { return floor_div(2 * num + den, 2 * den); }
-
 // 8-bit HSV class of one RGB pixel (R27); boxes are disjoint (pinned in tests/test_oracle.py).
-// Branch-free (selects only): neighbouring lanes' pixels take different paths.
+// Division-free and branch-free: every threshold on the rounded quotients
+//   S = floor((510 d + V) / 2V)   and   H_raw = floor((2 num + d) / 2d)   (round half up)
+// is an exact integer comparison of the numerator against a multiple of the denominator:
+//   S <= 18  <=>  510 d < 37 V,        S >= 50  <=>  510 d >= 99 V,
+//   H_raw <= T  <=>  2 num < (2T + 1) d   (d > 0),   H = H_raw mod 180 (H_raw in [-30, 150]).
+// (|2 num| < 2^17 and (2T+1) d < 2^17: no overflow.)  Checked against the oracle on all 2^24
+// colours (tests/test_gpu_parity.py::test_hsv_every_rgb_colour).
 __device__ __forceinline__ uint32_t hsv_class_of(uint32_t R, uint32_t G, uint32_t B) {
   const int r = static_cast<int>(R), g = static_cast<int>(G), b = static_cast<int>(B);
   const int V = max(max(r, g), b), m = min(min(r, g), b), d = V - m;
-  const int S = V == 0 ? 0 : div_round_half_up(255 * d, max(V, 1));
-  const int num = (V == r) ? 30 * (g - b) : (V == g) ? 60 * d + 30 * (b - r) : 120 * d + 30 * (r - g);
-  int H = div_round_half_up(num, max(d, 1));
-  H = H < 0 ? H + 180 : (H >= 180 ? H - 180 : H);
-  H = d == 0 ? 0 : H;
+  const int num2 = 2 * ((V == r) ? 30 * (g - b) : (V == g) ? 60 * d + 30 * (b - r) : 120 * d + 30 * (r - g));
   // hue classes of chromatic pixels (S >= 50, V >= 70): red (with the hue wrap),
   // orange -> other, yellow, green, blue, purple, pink
-  uint32_t hc = H <= 9 ? 0u : (H < 20 ? 9u : (H <= 34 ? 3u : (H <= 89 ? 4u : (H <= 128 ? 5u : (H <= 158 ? 6u : (H <= 169 ? 7u : 0u))))));
-  uint32_t cls = (S >= 50 && V >= 70) ? hc : 9u;
-  cls = S <= 18 ? (V <= 230 ? 2u : 8u) : cls;  // gray (V 31..230) / white (V 231..255)
-  return V <= 30 ? 1u : cls;                   // black: (0,0,0)-(179,255,30)
+  uint32_t hc;
+  if (num2 < -d) {  // H_raw < 0: H = H_raw + 180 in [150, 179]
+    hc = num2 < -43 * d ? 6u : (num2 < -21 * d ? 7u : 0u);  // purple <= 158, pink <= 169, red
+  } else {
+    hc = num2 < 19 * d    ? 0u    // H <= 9: red
+         : num2 < 39 * d  ? 9u    // H <= 19: orange -> other
+         : num2 < 69 * d  ? 3u    // H <= 34: yellow
+         : num2 < 179 * d ? 4u    // H <= 89: green
+         : num2 < 257 * d ? 5u    // H <= 128: blue
+         : num2 < 317 * d ? 6u    // H <= 158: purple
+         : num2 < 339 * d ? 7u    // H <= 169: pink
+                          : 0u;   // H 170..179: red (unreachable for H_raw >= 0)
+  }
+  uint32_t cls = (510 * d >= 99 * V && V >= 70) ? hc : 9u;
+  cls = 510 * d < 37 * V ? (V <= 230 ? 2u : 8u) : cls;  // S <= 18: gray (V 31..230) / white (V 231..255)
+  return V <= 30 ? 1u : cls;                             // black: (0,0,0)-(179,255,30)
 }
 
 __device__ __forceinline__ uint32_t ldg32(const uint8_t* p) { return __ldg(reinterpret_cast<const uint32_t*>(p)); }
 
 }  // namespace
 
-__global__ void __launch_bounds__(kHsvThreads) hydro_hsv_kernel(ClsParams p) {
+__global__ void __launch_bounds__(kHsvThreads, 3) hydro_hsv_kernel(ClsParams p) {
   DevState* st = p.st;
   int pred;
   const uint32_t* list_in;

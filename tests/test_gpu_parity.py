@@ -751,3 +751,33 @@ def test_new_abi_error_paths():
     assert ex.value.status == -1
     r.collect(rb)
     r.close()
+
+
+def test_hsv_every_rgb_colour():
+    """K4-HSV's division-free classifier against the oracle's HSV (R27) on all 2^24 RGB colours:
+    16 frames of 1024 x 1024 hold every colour once, 4096 crops of 64 x 64 (nearest-exact at w = h
+    = 64 samples every pixel) tile them, and each crop's 10 class counts must equal the oracle's."""
+    from paper_2403_14902_b200.hydro import Eddy
+    from synth import Tuples, hsv_pred
+
+    i = torch.arange(1 << 24, dtype=torch.int64)
+    rgb = torch.stack([i & 255, (i >> 8) & 255, i >> 16], dim=1).to(torch.uint8)
+    frames = rgb.view(16, 1024, 1024, 3).contiguous()
+    n = 16 * 16 * 16
+    k = torch.arange(n, dtype=torch.int64)
+    fid = (k // 256).to(torch.int32)
+    x0 = ((k % 16) * 64).to(torch.int16)
+    y0 = (((k // 16) % 16) * 64).to(torch.int16)
+    bbox = torch.stack([x0, y0, x0 + 64, y0 + 64], dim=1).to(torch.int16).contiguous()
+    t = Tuples(id=k.clone(), frame_id=fid, bbox=bbox, label=torch.zeros(n, dtype=torch.int16))
+    p = hsv_pred(1, 0.1)
+    e = Eddy(frames=frames.cuda(), policy="fixed", warmup_tuples=0, max_batch_tuples=n)
+    e.add_predicate(p)
+    counts = torch.full((n, 10), -1.0, device="cuda")
+    e.debug_linear(0, t.to("cuda"), counts, None, None)
+    got = counts.cpu().numpy().astype(np.int64)
+    e.close()
+    fr = frames.numpy()
+    for a in range(0, n, 512):
+        crops = np.stack([fr[int(fid[j]), int(y0[j]):int(y0[j]) + 64, int(x0[j]):int(x0[j]) + 64] for j in range(a, a + 512)])
+        assert np.array_equal(got[a:a + 512], O.hsv_counts(crops)), a
