@@ -33,19 +33,15 @@ __device__ __forceinline__ uint32_t hsv_class_of(uint32_t R, uint32_t G, uint32_
   const int num2 = 2 * ((V == r) ? 30 * (g - b) : (V == g) ? 60 * d + 30 * (b - r) : 120 * d + 30 * (r - g));
   // hue classes of chromatic pixels (S >= 50, V >= 70): red (with the hue wrap),
   // orange -> other, yellow, green, blue, purple, pink
-  uint32_t hc;
-  if (num2 < -d) {  // H_raw < 0: H = H_raw + 180 in [150, 179]
-    hc = num2 < -43 * d ? 6u : (num2 < -21 * d ? 7u : 0u);  // purple <= 158, pink <= 169, red
-  } else {
-    hc = num2 < 19 * d    ? 0u    // H <= 9: red
-         : num2 < 39 * d  ? 9u    // H <= 19: orange -> other
-         : num2 < 69 * d  ? 3u    // H <= 34: yellow
-         : num2 < 179 * d ? 4u    // H <= 89: green
-         : num2 < 257 * d ? 5u    // H <= 128: blue
-         : num2 < 317 * d ? 6u    // H <= 158: purple
-         : num2 < 339 * d ? 7u    // H <= 169: pink
-                          : 0u;   // H 170..179: red (unreachable for H_raw >= 0)
-  }
+  // the class is picked from a nibble table by the number of hue bounds at or below H (no branches):
+  // H_raw >= 0: red <= 9 < other <= 19 < yellow <= 34 < green <= 89 < blue <= 128 < purple <= 158
+  //             < pink <= 169 < red;  H_raw < 0 (H = H_raw + 180): purple <= 158 < pink <= 169 < red
+  const uint32_t ipos = static_cast<uint32_t>(num2 >= 19 * d) + static_cast<uint32_t>(num2 >= 39 * d) +
+                        static_cast<uint32_t>(num2 >= 69 * d) + static_cast<uint32_t>(num2 >= 179 * d) +
+                        static_cast<uint32_t>(num2 >= 257 * d) + static_cast<uint32_t>(num2 >= 317 * d) +
+                        static_cast<uint32_t>(num2 >= 339 * d);
+  const uint32_t ineg = static_cast<uint32_t>(num2 >= -43 * d) + static_cast<uint32_t>(num2 >= -21 * d);
+  const uint32_t hc = num2 < -d ? (0x076u >> (4u * ineg)) & 15u : (0x07654390u >> (4u * ipos)) & 15u;
   uint32_t cls = (510 * d >= 99 * V && V >= 70) ? hc : 9u;
   cls = 510 * d < 37 * V ? (V <= 230 ? 2u : 8u) : cls;  // S <= 18: gray (V 31..230) / white (V 231..255)
   return V <= 30 ? 1u : cls;                             // black: (0,0,0)-(179,255,30)
