@@ -274,6 +274,39 @@ def test_cfg2_full_size_sampled_parity():
 
 # ------------------------------------------------------------------------ AREA crop / cfg4
 
+def test_cfg4_full_size_sampled_parity():
+    """cfg4 at BASELINE size (10M tuples, 1024 x 720p frames, 1M-tuple batches, data-aware tiles for
+    the AREA hop) in the area bench's launch configuration: rows checked against the oracle one by
+    one on samples of survivors and non-survivors; sampled tuples whose AREA-head margin is within
+    4x the logit tolerance are not compared (near-threshold, excluded by construction, R12)."""
+    w = workload("cfg4")
+    frames_dev = w.frames(device="cuda")
+    t = w.tuples()
+    e = make_eddy(w, frames_dev, policy="score", warmup=65536, max_batch=1 << 20, balance="data_aware")
+    ids, bbs, infos = run_stream(e, t.to("cuda"), 1 << 20)
+    e.close()
+    assert np.all(np.diff(ids.astype(np.int64)) > 0)  # input order, no duplicates
+    all_ids = t.id.numpy()
+    pos = np.searchsorted(all_ids, ids.astype(np.int64))
+    assert np.array_equal(t.bbox.numpy()[pos].astype(np.int64), bbs)
+    rng = np.random.default_rng(1)
+    in_res = np.zeros(len(all_ids), bool)
+    in_res[pos] = True
+    samp = np.concatenate([rng.choice(np.where(in_res)[0], 1000, replace=False),
+                           rng.choice(np.where(~in_res)[0], 1000, replace=False)])
+    samp.sort()
+    sub = t.select(torch.from_numpy(samp))
+    fids = np.unique(sub.frame_id.numpy())
+    fr = np.zeros((w.n_frames, w.frame_h, w.frame_w, 3), np.uint8)
+    fr[fids] = w.frames(frame_ids=fids).numpy()
+    tup = O.as_numpy_tuples(sub)
+    _, z = O.linear_verdict(w.preds[3], fr, tup["frame_id"], tup["bbox"], return_logits=True)
+    clear = np.abs(O.margin(z, w.preds[3]["target"])) >= 4 * LOGIT_TOL
+    V = O.evaluate_all(w.preds, sub, fr)
+    assert clear.mean() > 0.95
+    assert np.array_equal(V.all(0)[clear], in_res[samp][clear])
+
+
 def test_linear_area_crops_logits_verdicts():
     """cfg4's breed head on AREA crops: crops bit-exact (bf16 bin means), logits <= 1e-2 of f64."""
     w = workload("cfg4", small=True, n=4000)
