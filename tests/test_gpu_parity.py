@@ -272,6 +272,36 @@ def test_cfg2_full_size_sampled_parity():
     e.close()
 
 
+def test_cfg5_last_shard_sampled_parity():
+    """cfg5 (the dog query on 100M tuples sharded over 8 GPUs): the last rank's contiguous shard,
+    ids [87.5M, 100M), through one context in 1M-tuple batches; rows checked against the oracle one
+    by one on samples (the union over ranks in rank order is the global result)."""
+    from synth import shard_range
+    w = workload("cfg5")
+    a, b = shard_range(w.n, 7, 8)
+    frames_dev = w.frames(device="cuda")
+    t = w.tuples(id_start=a, n=b - a)
+    e = make_eddy(w, frames_dev, policy="score", warmup=65536, max_batch=1 << 20)
+    ids, bbs, _ = run_stream(e, t.to("cuda"), 1 << 20)
+    e.close()
+    assert ids.min() >= a and ids.max() < b and np.all(np.diff(ids.astype(np.int64)) > 0)
+    all_ids = t.id.numpy()
+    pos = np.searchsorted(all_ids, ids.astype(np.int64))
+    assert np.array_equal(t.bbox.numpy()[pos].astype(np.int64), bbs)
+    rng = np.random.default_rng(2)
+    in_res = np.zeros(len(all_ids), bool)
+    in_res[pos] = True
+    samp = np.concatenate([rng.choice(np.where(in_res)[0], 1000, replace=False),
+                           rng.choice(np.where(~in_res)[0], 1000, replace=False)])
+    samp.sort()
+    sub = t.select(torch.from_numpy(samp))
+    fids = np.unique(sub.frame_id.numpy())
+    fr = np.zeros((w.n_frames, w.frame_h, w.frame_w, 3), np.uint8)
+    fr[fids] = w.frames(frame_ids=fids).numpy()
+    V = O.evaluate_all(w.preds, sub, fr)
+    assert np.array_equal(V.all(0), in_res[samp])
+
+
 # ------------------------------------------------------------------------ AREA crop / cfg4
 
 def test_cfg4_full_size_sampled_parity():
