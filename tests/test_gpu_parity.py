@@ -302,6 +302,61 @@ def test_cfg5_last_shard_sampled_parity():
     assert np.array_equal(V.all(0), in_res[samp])
 
 
+def test_mlp_workload_full_size_sampled_parity():
+    """The MLP dog query (breed as the 12288-512-120 head, bench --workload mlp) at full size (1M
+    tuples, 1024 x 720p frames) in the bench's launch configuration; sampled rows against the
+    oracle, near-threshold MLP margins (within 4x the logit tolerance) not compared (R25)."""
+    w = workload("mlp")
+    frames_dev = w.frames(device="cuda")
+    t = w.tuples()
+    e = make_eddy(w, frames_dev, policy="score", warmup=65536, max_batch=1 << 20)
+    ids, bbs, _ = run_stream(e, t.to("cuda"), 1 << 20)
+    e.close()
+    all_ids = t.id.numpy()
+    pos = np.searchsorted(all_ids, ids.astype(np.int64))
+    assert np.array_equal(t.bbox.numpy()[pos].astype(np.int64), bbs)
+    rng = np.random.default_rng(3)
+    in_res = np.zeros(len(all_ids), bool)
+    in_res[pos] = True
+    samp = np.concatenate([rng.choice(np.where(in_res)[0], 400, replace=False),
+                           rng.choice(np.where(~in_res)[0], 400, replace=False)])
+    samp.sort()
+    sub = t.select(torch.from_numpy(samp))
+    fids = np.unique(sub.frame_id.numpy())
+    fr = np.zeros((w.n_frames, w.frame_h, w.frame_w, 3), np.uint8)
+    fr[fids] = w.frames(frame_ids=fids).numpy()
+    tup = O.as_numpy_tuples(sub)
+    _, z = O.linear_verdict(w.preds[1], fr, tup["frame_id"], tup["bbox"], return_logits=True)
+    clear = np.abs(O.margin(z, w.preds[1]["target"])) >= 4 * LOGIT_TOL
+    V = O.evaluate_all(w.preds, sub, fr)
+    assert clear.mean() > 0.9
+    assert np.array_equal(V.all(0)[clear], in_res[samp][clear])
+
+
+def test_hsv_workload_full_size_sampled_parity():
+    """The HSV dog query (bench --workload hsv: coloured-block 720p frames, 1M tuples) at full size;
+    sampled rows against the oracle one by one (all integer decisions: exact)."""
+    w = workload("hsv")
+    frames_dev = w.frames(device="cuda")
+    t = w.tuples()
+    e = make_eddy(w, frames_dev, policy="score", warmup=65536, max_batch=1 << 20)
+    ids, bbs, _ = run_stream(e, t.to("cuda"), 1 << 20)
+    e.close()
+    all_ids = t.id.numpy()
+    pos = np.searchsorted(all_ids, ids.astype(np.int64))
+    assert np.array_equal(t.bbox.numpy()[pos].astype(np.int64), bbs)
+    rng = np.random.default_rng(4)
+    in_res = np.zeros(len(all_ids), bool)
+    in_res[pos] = True
+    samp = np.concatenate([rng.choice(np.where(in_res)[0], 500, replace=False),
+                           rng.choice(np.where(~in_res)[0], 500, replace=False)])
+    samp.sort()
+    sub = t.select(torch.from_numpy(samp))
+    fr = frames_dev.cpu().numpy()
+    V = O.evaluate_all(w.preds, sub, fr)
+    assert np.array_equal(V.all(0), in_res[samp])
+
+
 # ------------------------------------------------------------------------ AREA crop / cfg4
 
 def test_cfg4_full_size_sampled_parity():
