@@ -210,23 +210,39 @@ HSV_BOXES = [
 ]
 
 
-def _div_round_half_up(num: np.ndarray, den: np.ndarray) -> np.ndarray:
-    """floor(num / den + 1/2) for integer arrays, den > 0 (exact integer arithmetic)."""
-    return np.floor_divide(2 * num + den, 2 * den)
+HSV_SHIFT = 12  # OpenCV's fixed-point shift for 8-bit RGB -> HSV
+
+
+def _hsv_tables():
+    """OpenCV's 8-bit reciprocal tables (R27): sdiv[i] = round(255 * 2^12 / i),
+    hdiv[i] = round(180 * 2^12 / (6 i)) for i = 1..255, both 0 at i = 0 (no exact .5 occurs:
+    2 * 255 * 2^12 / i and 2 * 180 * 2^12 / (6 i) are never odd integers for i < 2^13)."""
+    i = np.arange(256, dtype=np.float64)
+    sdiv = np.zeros(256, np.int64)
+    hdiv = np.zeros(256, np.int64)
+    sdiv[1:] = np.rint((255 << HSV_SHIFT) / i[1:])
+    hdiv[1:] = np.rint((180 << HSV_SHIFT) / (6.0 * i[1:]))
+    return sdiv, hdiv
 
 
 def rgb_to_hsv_u8(rgb: np.ndarray) -> np.ndarray:
-    """8-bit RGB -> 8-bit HSV (R27, OpenCV's convention): V = max, S = round(255 (V - min) / V),
-    H = round(30 (G - B) / d), 60 + round-arg ..., i.e. hue in degrees / 2, tested R then G then B."""
+    """8-bit RGB -> 8-bit HSV exactly as OpenCV's cvtColor(COLOR_RGB2HSV) (R27; the paper's red
+    range, is in OpenCV's H in [0, 180) scale), plain fixed-point steps:
+      V = max(R, G, B), d = V - min(R, G, B)
+      S = (d * sdiv[V] + 2^11) >> 12
+      h = G - B if V == R, else B - R + 2d if V == G, else R - G + 4d
+      H = (h * hdiv[d] + 2^11) >> 12 (floor shift), + 180 if negative.
+    Pinned bit for bit against cv2.cvtColor on all 2^24 colours (tests/test_oracle.py)."""
+    sdiv, hdiv = _hsv_tables()
     c = np.asarray(rgb, dtype=np.int64)
     R, G, B = c[..., 0], c[..., 1], c[..., 2]
     V = np.maximum(np.maximum(R, G), B)
-    m = np.minimum(np.minimum(R, G), B)
-    d = V - m
-    S = np.where(V == 0, 0, _div_round_half_up(255 * d, np.maximum(V, 1)))
-    num = np.where(V == R, 30 * (G - B), np.where(V == G, 60 * d + 30 * (B - R), 120 * d + 30 * (R - G)))
-    H = np.where(d == 0, 0, _div_round_half_up(num, np.maximum(d, 1)))
-    H = np.mod(H, 180)
+    d = V - np.minimum(np.minimum(R, G), B)
+    half = 1 << (HSV_SHIFT - 1)
+    S = (d * sdiv[V] + half) >> HSV_SHIFT
+    h = np.where(V == R, G - B, np.where(V == G, B - R + 2 * d, R - G + 4 * d))
+    H = (h * hdiv[d] + half) >> HSV_SHIFT
+    H = np.where(H < 0, H + 180, H)
     return np.stack([H, S, V], axis=-1)
 
 

@@ -7,7 +7,8 @@
 // 32 tuples of one verdict-bitmap word, one tuple at a time: lane l takes output pixels l and
 // l + 32 of every crop row (two aligned 32-bit loads from the L1-cached frame row, funnel shift),
 // keeps 10 per-lane class counters packed 4 x 8 bits per register (a lane sees <= 128 pixels of a
-// tuple), then one warp reduction per class.  The HSV thresholds are evaluated without divisions.
+// tuple), then one warp reduction per class.  HSV is OpenCV's fixed-point conversion (two table
+// lookups in shared memory per pixel, no divisions).
 #include <algorithm>
 
 #include "hydro_internal.cuh"
@@ -19,32 +20,32 @@ namespace {
 constexpr int kHsvThreads = 256;
 constexpr uint32_t kFullMask = 0xFFFFFFFFu;
 
-// 8-bit HSV class of one RGB pixel (R27); boxes are disjoint (pinned in tests/test_oracle.py).
-// Division-free and branch-free: every threshold on the rounded quotients
-//   S = floor((510 d + V) / 2V)   and   H_raw = floor((2 num + d) / 2d)   (round half up)
-// is an exact integer comparison of the numerator against a multiple of the denominator:
-//   S <= 18  <=>  510 d < 37 V,        S >= 50  <=>  510 d >= 99 V,
-//   H_raw <= T  <=>  2 num < (2T + 1) d   (d > 0),   H = H_raw mod 180 (H_raw in [-30, 150]).
-// (|2 num| < 2^17 and (2T+1) d < 2^17: no overflow.)  Checked against the oracle on all 2^24
-// colours (tests/test_gpu_parity.py::test_hsv_every_rgb_colour).
-__device__ __forceinline__ uint32_t hsv_class_of(uint32_t R, uint32_t G, uint32_t B) {
+// 8-bit HSV class of one RGB pixel (R27): OpenCV's cvtColor(RGB2HSV) fixed-point arithmetic with
+// its reciprocal tables (hsv_shift 12; sdiv = round(255 * 2^12 / V), hdiv = round(30 * 2^12 / d),
+// in shared memory), then the disjoint class boxes (pinned in tests/test_oracle.py):
+//   S = (d sdiv[V] + 2^11) >> 12,  H = (h hdiv[d] + 2^11) >> 12 (+180 if < 0),
+//   h = G - B (V = R), B - R + 2d (V = G), R - G + 4d (V = B).
+// Branch-free; checked against the oracle (= cv2) on all 2^24 colours
+// (tests/test_gpu_parity.py::test_hsv_every_rgb_colour).
+__device__ __forceinline__ uint32_t hsv_class_of(uint32_t R, uint32_t G, uint32_t B, const int* sdiv,
+                                                 const int* hdiv) {
   const int r = static_cast<int>(R), g = static_cast<int>(G), b = static_cast<int>(B);
-  const int V = max(max(r, g), b), m = min(min(r, g), b), d = V - m;
-  const int num2 = 2 * ((V == r) ? 30 * (g - b) : (V == g) ? 60 * d + 30 * (b - r) : 120 * d + 30 * (r - g));
-  // hue classes of chromatic pixels (S >= 50, V >= 70): red (with the hue wrap),
-  // orange -> other, yellow, green, blue, purple, pink
-  // the class is picked from a nibble table by the number of hue bounds at or below H (no branches):
-  // H_raw >= 0: red <= 9 < other <= 19 < yellow <= 34 < green <= 89 < blue <= 128 < purple <= 158
-  //             < pink <= 169 < red;  H_raw < 0 (H = H_raw + 180): purple <= 158 < pink <= 169 < red
-  const uint32_t ipos = static_cast<uint32_t>(num2 >= 19 * d) + static_cast<uint32_t>(num2 >= 39 * d) +
-                        static_cast<uint32_t>(num2 >= 69 * d) + static_cast<uint32_t>(num2 >= 179 * d) +
-                        static_cast<uint32_t>(num2 >= 257 * d) + static_cast<uint32_t>(num2 >= 317 * d) +
-                        static_cast<uint32_t>(num2 >= 339 * d);
-  const uint32_t ineg = static_cast<uint32_t>(num2 >= -43 * d) + static_cast<uint32_t>(num2 >= -21 * d);
-  const uint32_t hc = num2 < -d ? (0x076u >> (4u * ineg)) & 15u : (0x07654390u >> (4u * ipos)) & 15u;
-  uint32_t cls = (510 * d >= 99 * V && V >= 70) ? hc : 9u;
-  cls = 510 * d < 37 * V ? (V <= 230 ? 2u : 8u) : cls;  // S <= 18: gray (V 31..230) / white (V 231..255)
-  return V <= 30 ? 1u : cls;                             // black: (0,0,0)-(179,255,30)
+  const int V = max(max(r, g), b), d = V - min(min(r, g), b);
+  const int sd = d * sdiv[V];  // S <= 18 <=> sd < 19 * 4096 - 2048;  S >= 50 <=> sd >= 50 * 4096 - 2048
+  const int hn = (V == r) ? g - b : ((V == g) ? b - r + 2 * d : r - g + 4 * d);
+  int H = (hn * hdiv[d] + 2048) >> 12;
+  H += H < 0 ? 180 : 0;
+  // hue classes of chromatic pixels (S >= 50, V >= 70), picked from a nibble table by the number of
+  // hue bounds at or below H: red <= 9 < other <= 19 < yellow <= 34 < green <= 89 < blue <= 128
+  // < purple <= 158 < pink <= 169 < red (PAPER.md:395 with the hue wrap)
+  const uint32_t ipos = static_cast<uint32_t>(H >= 10) + static_cast<uint32_t>(H >= 20) +
+                        static_cast<uint32_t>(H >= 35) + static_cast<uint32_t>(H >= 90) +
+                        static_cast<uint32_t>(H >= 129) + static_cast<uint32_t>(H >= 159) +
+                        static_cast<uint32_t>(H >= 170);
+  const uint32_t hc = (0x07654390u >> (4u * ipos)) & 15u;
+  uint32_t cls = (sd >= 50 * 4096 - 2048 && V >= 70) ? hc : 9u;
+  cls = sd < 19 * 4096 - 2048 ? (V <= 230 ? 2u : 8u) : cls;  // S <= 18: gray (V 31..230) / white (V 231..255)
+  return V <= 30 ? 1u : cls;                                // black: (0,0,0)-(179,255,30)
 }
 
 __device__ __forceinline__ uint32_t ldg32(const uint8_t* p) { return __ldg(reinterpret_cast<const uint32_t*>(p)); }
@@ -76,6 +77,13 @@ __global__ void __launch_bounds__(kHsvThreads, 3) hydro_hsv_kernel(ClsParams p) 
     count = list_in ? *p.count_in : p.range_n;
     bits_out = p.bits_out;
   }
+  // OpenCV's reciprocal tables (exact integer rounding; no .5 ties occur for i < 2^13)
+  __shared__ int s_sdiv[256], s_hdiv[256];
+  for (int i = threadIdx.x; i < 256; i += kHsvThreads) {
+    s_sdiv[i] = i ? (2 * (255 << 12) + i) / (2 * i) : 0;
+    s_hdiv[i] = i ? (2 * (30 << 12) + i) / (2 * i) : 0;
+  }
+  __syncthreads();
   const int target = p.preds[pred].target;
   const int lane = threadIdx.x & 31;
   const uint32_t words = (count + 31) / 32;
@@ -135,7 +143,7 @@ __global__ void __launch_bounds__(kHsvThreads, 3) hydro_hsv_kernel(ClsParams p) 
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
             const uint32_t q = px[rr][k];
-            const uint32_t cls = hsv_class_of(q & 0xFF, (q >> 8) & 0xFF, (q >> 16) & 0xFF);
+            const uint32_t cls = hsv_class_of(q & 0xFF, (q >> 8) & 0xFF, (q >> 16) & 0xFF, s_sdiv, s_hdiv);
             const uint32_t inc = 1u << ((cls & 3u) * 8u);
             c0 += cls < 4 ? inc : 0u;
             c1 += (cls >= 4 && cls < 8) ? inc : 0u;

@@ -86,6 +86,25 @@ def test_cfg1_counts():
     assert V[0].sum() == g["A_pass"] and V[1].sum() == g["B_pass"] and V.all(0).sum() == g["A_and_B"]
     n_in, n_pass, _ = O.sequential_eval(V, [0, 1])
     assert n_in.tolist() == [10000, g["A_pass"]] and n_pass.tolist() == [g["A_pass"], g["A_and_B"]]
+    # realized cost of the run = 10000 * 1 + 5039 * 10 units (SURVEY.md §8(c) "realized 60,390")
+    assert O.realized_cost(n_in, [1.0, 10.0]) == 60390.0
+
+
+def test_realized_cost_equals_per_tuple_short_circuit_brute_force():
+    """sum_k c_k in_k equals the cost summed tuple by tuple over a plain short-circuit AND (each
+    tuple pays c_k for every predicate it reaches), for every order of random verdicts."""
+    rng = np.random.default_rng(5)
+    V = rng.random((4, 300)) < np.array([0.2, 0.5, 0.7, 0.9])[:, None]
+    c = [3.0, 1.5, 7.0, 0.25]
+    for order in itertools.permutations(range(4)):
+        n_in, _, _ = O.sequential_eval(V, order)
+        brute = 0.0
+        for t in range(V.shape[1]):
+            for k in order:
+                brute += c[k]
+                if not V[k, t]:
+                    break
+        assert O.realized_cost(n_in, c) == pytest.approx(brute, rel=1e-12)
 
 
 # ----------------------------------------------------------------------------- crops (R10)
@@ -254,10 +273,27 @@ def test_mlp_all_negative_hidden_gives_bias_and_generated_selectivity():
 # ----------------------------------------------------------------------------- HSV colour heuristic (f4, R27)
 
 
-def test_rgb_to_hsv_matches_colorsys():
-    """Against Python's colorsys (float HSV): V exact, S and H within one unit of
-    round(255 s) / round(180 h) (they differ only where the float rounding sees a .5 tie), and
-    exact on the primaries, the secondaries and greys."""
+def _all_rgb():
+    v = np.arange(1 << 24, dtype=np.int64)
+    return np.stack([(v >> 16) & 255, (v >> 8) & 255, v & 255], axis=-1)
+
+
+def test_rgb_to_hsv_equals_opencv_on_every_colour():
+    """R27 reads DogColorClassifier's HSV as OpenCV's 8-bit cvtColor: the oracle's
+    fixed-point steps equal cv2.cvtColor(COLOR_RGB2HSV) bit for bit on all 2^24 RGB colours, and so
+    does the resulting colour class."""
+    cv2 = pytest.importorskip("cv2")
+    rgb = _all_rgb()
+    ref = cv2.cvtColor(rgb.astype(np.uint8).reshape(4096, 4096, 3), cv2.COLOR_RGB2HSV).reshape(-1, 3)
+    got = O.rgb_to_hsv_u8(rgb)
+    assert np.array_equal(got, ref.astype(np.int64))
+    assert np.array_equal(O.hsv_class(got), O.hsv_class(ref.astype(np.int64)))
+
+
+def test_rgb_to_hsv_near_colorsys():
+    """Against Python's colorsys (float HSV): V exact, S and H within one unit of 255 s / 180 h
+    (the fixed-point reciprocals round once more than the float formula), and exact on the
+    primaries, the secondaries and greys."""
     import colorsys
 
     rng = np.random.default_rng(11)
@@ -266,9 +302,9 @@ def test_rgb_to_hsv_matches_colorsys():
     for (r, g, b), (H, S, V) in zip(rgb.tolist(), got.tolist()):
         h, s_, v = colorsys.rgb_to_hsv(r / 255, g / 255, b / 255)
         assert V == round(v * 255)
-        assert abs(S - s_ * 255) <= 0.5 + 1e-9
+        assert abs(S - s_ * 255) <= 1.0
         dh = abs(H - h * 180)
-        assert min(dh, 180 - dh) <= 0.5 + 1e-9, ((r, g, b), H, h * 180)
+        assert min(dh, 180 - dh) <= 1.0, ((r, g, b), H, h * 180)
     fixed = {(255, 0, 0): (0, 255, 255), (0, 255, 0): (60, 255, 255), (0, 0, 255): (120, 255, 255),
              (255, 255, 0): (30, 255, 255), (0, 255, 255): (90, 255, 255), (255, 0, 255): (150, 255, 255),
              (0, 0, 0): (0, 0, 0), (128, 128, 128): (0, 0, 128), (255, 255, 255): (0, 0, 255)}
@@ -279,12 +315,10 @@ def test_rgb_to_hsv_matches_colorsys():
 def test_hsv_boxes_disjoint_over_all_colours_and_paper_red():
     """Every 8-bit RGB colour falls in at most one class box (so 'first box' = 'the box'), and the
     paper's red range (0, 50, 70)-(9, 255, 255) classifies as red."""
-    v = np.arange(0, 256, 3)
-    rgb = np.stack(np.meshgrid(v, v, v, indexing="ij"), -1).reshape(-1, 3)
-    hsv = O.rgb_to_hsv_u8(rgb)
-    hits = np.zeros(len(rgb), dtype=np.int64)
+    hsv = O.rgb_to_hsv_u8(_all_rgb())
+    hits = np.zeros(len(hsv), dtype=np.int64)
     for boxes in O.HSV_BOXES:
-        inside = np.zeros(len(rgb), dtype=bool)
+        inside = np.zeros(len(hsv), dtype=bool)
         for lo, hi in boxes:
             inside |= np.all((hsv >= np.array(lo)) & (hsv <= np.array(hi)), axis=-1)
         hits += inside
