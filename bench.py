@@ -107,6 +107,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def _profile_traffic(name: str):
+    """bytes_per_launch of a committed ncu capture (profiles/<name>), only if it was captured on the
+    current library sources (csrc_sha16 stamp); else (None, why)."""
+    path = os.path.join(ROOT, "profiles", name)
+    if not os.path.exists(path):
+        return None, "no capture"
+    try:
+        d = json.load(open(path))
+    except Exception as ex:
+        return None, f"unreadable: {ex}"
+    if d.get("csrc_sha16") != csrc_sha16():
+        return None, f"stale: profiles/{name} was captured on sources {d.get('csrc_sha16')}, not {csrc_sha16()}"
+    return d.get("bytes_per_launch"), f"profiles/{name} ({d.get('source', 'ncu')}), same sources"
+
+
 def _dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -114,23 +129,71 @@ def _dist_env():
     return world, rank, local
 
 
-def cpu_oracle_rate(w, tuples_cpu, frames_host, seconds: float = 15.0, min_tuples: int = 256):
-    """Oracle (as it stands) on host cores over a bounded contiguous sample of the workload."""
-    import numpy as np
+PAPER_CONTEXT = {"speedup": "up to 11.52x over the EvaDB baseline (UC3, long video, Eddy + Laminar on 2 GPUs)",
+                 "hardware": "2 x NVIDIA A40 (48 GB) on an AMD EPYC 7452 32-core server, CUDA 12.0",
+                 "cite": "PAPER.md:16, 383-385, 785 (§4.2 setup, §5.2 UC3)",
+                 "note": "context only: another system, machine and workload"}
+
+
+def csrc_sha16() -> str:
+    """Hash of the library sources (csrc/*, include/hydro.h): stamps profile-derived numbers."""
+    import hashlib
+
+    from paper_2403_14902_b200 import build as B
+
+    h = hashlib.sha256()
+    for f in B.sources():
+        h.update(os.path.basename(f).encode())
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:16]
+
+
+def cpu_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+_ORC = {}
+
+
+def _oracle_chunk(bounds):
+    from threadpoolctl import threadpool_limits
 
     import oracle as O
-    from threadpoolctl import threadpool_info
 
-    cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    chunk, done, t0 = 512, 0, time.perf_counter()
-    while True:
-        sub = tuples_cpu.slice(done, done + chunk)
-        O.evaluate_all(w.preds, sub, frames_host)
-        done += len(sub)
+    a, b = bounds
+    with threadpool_limits(1):
+        O.evaluate_all(_ORC["w"].preds, _ORC["t"].slice(a, b), _ORC["frames"])
+    return b - a
+
+
+def cpu_oracle_rate(w, tuples_cpu, frames_host, seconds: float = 15.0, chunk: int = 256):
+    """The oracle as it stands (every predicate on every tuple, f64 numpy) on the host: first one
+    thread (BLAS limited to 1) on one chunk, then every core -- one single-threaded worker process
+    per core over consecutive chunks of the same sample -- for about `seconds`.  Returns both rates
+    and the sample sizes; `cores` = the worker processes that ran."""
+    import multiprocessing as mp
+
+    _ORC.update(w=w, t=tuples_cpu, frames=frames_host)
+    t0 = time.perf_counter()
+    one = _oracle_chunk((0, chunk))
+    r1 = one / (time.perf_counter() - t0)
+    procs = os.cpu_count() or 1
+    n_target = int(min(len(tuples_cpu), max(procs * chunk, r1 * procs * seconds)))
+    spans = [(a, min(a + chunk, n_target)) for a in range(0, n_target, chunk)]
+    with mp.get_context("fork").Pool(procs) as pool:
+        t0 = time.perf_counter()
+        done = sum(pool.map(_oracle_chunk, spans, chunksize=1))
         el = time.perf_counter() - t0
-        if (el >= seconds and done >= min_tuples) or done >= len(tuples_cpu):
-            break
-    return done / el, done, el, cores
+    return {"value": done / el, "cores": procs, "tuples": done, "seconds": el, "one_thread_value": r1,
+            "one_thread_tuples": one, **cpu_info()}
 
 
 def run_reference(args):
@@ -144,29 +207,35 @@ def run_reference(args):
     from synth import workload
     from threadpoolctl import threadpool_info
 
-    w = workload("cfg2")
-    per_step = 4096
+    import multiprocessing as mp
+
+    w = workload("cfg2", weights=args.weights)
+    procs = os.cpu_count() or 1
+    per_step = 16 * procs  # one 16-tuple chunk per core per step: a bounded sample of the workload
     t = w.tuples(n=per_step * 4)
     fids = np.unique(t.frame_id.numpy())
     frames = np.zeros((w.n_frames, w.frame_h, w.frame_w, 3), np.uint8)
     frames[fids] = w.frames(frame_ids=fids).numpy()
-    cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    _ORC.update(w=w, t=t, frames=frames)
+    cores = procs
     times = []
-    for s in range(args.warmup + args.steps):
-        sub = t.slice((s % 4) * per_step, (s % 4 + 1) * per_step)
-        t0 = time.perf_counter()
-        O.evaluate_all(w.preds, sub, frames)
-        if s >= args.warmup:
-            times.append(time.perf_counter() - t0)
+    with mp.get_context("fork").Pool(procs) as pool:
+        for s in range(args.warmup + args.steps):
+            a = (s % 4) * per_step
+            t0 = time.perf_counter()
+            pool.map(_oracle_chunk, [(a + 16 * i, a + 16 * (i + 1)) for i in range(procs)], chunksize=1)
+            if s >= args.warmup:
+                times.append(time.perf_counter() - t0)
     el = sum(times)
     value = per_step * len(times) / el
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * el / len(times),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": WORKLOAD, "tuples_per_step": per_step,
-                                           "parallelism": "host cores (numpy/OpenBLAS)"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                            "sample": f"{per_step} tuples per step of the cfg2 workload, every predicate on every tuple"},
+           "data": "synthetic", "config": {"workload": WORKLOAD, "weights": args.weights, "tuples_per_step": per_step,
+                                           "parallelism": f"{procs} single-threaded oracle processes (one per host core)"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", **cpu_info(),
+                            "sample": f"{per_step} tuples per step of the cfg2 workload ({procs} chunks of 16 in "
+                                      f"parallel), every predicate on every tuple"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
@@ -195,7 +264,7 @@ def run_gpu(args):
         dist.barrier()
     mlp = args.workload == "mlp"
     hsv = args.workload == "hsv"
-    w = workload("mlp" if mlp else ("hsv" if hsv else "cfg2"))
+    w = workload("mlp" if mlp else ("hsv" if hsv else "cfg2"), weights=args.weights)
     frames = w.frames(device="cuda")
     uid = broadcast_unique_id(dist, rank, H.hydro_nccl_unique_id) if world > 1 else None
     stream = torch.cuda.current_stream()
@@ -212,7 +281,7 @@ def run_gpu(args):
     res_bb = torch.empty((1 << 20, 4), dtype=torch.int16, device="cuda")
 
     def collect_dev(bid):
-        return H.hydro_collect_results(e.ctx, bid, res_ids.data_ptr(), res_bb.data_ptr(), 1 << 20, 1)
+        return e.collect_into(bid, res_ids, res_bb)
 
     def run_steps(k, offset):
         pend = []
@@ -240,6 +309,10 @@ def run_gpu(args):
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
+    # classifier tuples in and the device launch timers, read around the timed region (outside it)
+    in_t0, min_t0, hin_t0 = lin_in(), mlp_in(), hsv_in()
+    for kind in (1, 4, 5):
+        e.device_time(kind, reset=True)
     launches0 = e.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -256,31 +329,26 @@ def run_gpu(args):
         ms = max_over_ranks(ms, dist, "cuda")
         dist.barrier()
     value = world * TUPLES_PER_STEP * args.steps / (ms / 1000.0)
-
-    # ---- kernel timing pass (separate, untimed for `value`): K4 share + achieved bandwidth
-    in0, min0, hin0 = lin_in(), mlp_in(), hsv_in()
+    # ---- the classifier kernels' share of THIS timed run: device launch timers (%globaltimer of the
+    # first CTA start / last CTA end of every launch that evaluated a hop; no host events)
+    k4_ms, k4_n = e.device_time(1)
+    km_ms, km_n = e.device_time(4)
+    kh_ms, kh_n = e.device_time(5)
+    k4_tuples = lin_in() - in_t0
+    km_tuples = mlp_in() - min_t0
+    kh_tuples = hsv_in() - hin_t0
+    op_fp16 = [e.stats(k)["operand_fp16"] for k in lin + mlps]
+    # ---- breakdown of the rest of the step (separate pass, CUDA events around every launch)
     e.set_kernel_timing(True)
     run_steps(args.steps, 2)
-    k4_ms, k4_n = e.kernel_time(1)
-    km_ms, km_n = e.kernel_time(4)
-    kh_ms, kh_n = e.kernel_time(5)
-    kh_tuples = hsv_in() - hin0
-    km_tuples = mlp_in() - min0
     k1_ms, k1_n = e.kernel_time(0)
     k5_ms, k5_n = e.kernel_time(2)
     k2c_ms, k2c_n = e.kernel_time(3)
     e.set_kernel_timing(False)
-    k4_tuples = lin_in() - in0
     k4_bytes = k4_tuples * K4_BYTES_PER_TUPLE
     peaks = _peaks()
     achieved = k4_bytes / (k4_ms / 1000.0) / 1e9 if k4_ms > 0 else 0.0
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "k4_dram_traffic.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic, traffic_note = _profile_traffic("k4_dram_traffic.json")
 
     # ---- e2e through the C ABI with pinned host buffers
     host_batches = [batches[b].to("cpu", pin=True) for b in range(2)]
@@ -294,10 +362,10 @@ def run_gpu(args):
         for s in range(k):
             pend.append(e.submit(host_batches[s % 2]))
             if len(pend) >= 2:
-                n = H.hydro_collect_results(e.ctx, pend.pop(0), out_ids.data_ptr(), out_bb.data_ptr(), 1 << 20, 0)
+                n = e.collect_into(pend.pop(0), out_ids, out_bb)
                 d2h.append(16 * n)
         for bid in pend:
-            n = H.hydro_collect_results(e.ctx, bid, out_ids.data_ptr(), out_bb.data_ptr(), 1 << 20, 0)
+            n = e.collect_into(bid, out_ids, out_bb)
             d2h.append(16 * n)
 
     e2e_steps(2)
@@ -320,10 +388,12 @@ def run_gpu(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         fr_host = frames.cpu().numpy()
         tc = batches[0].slice(0, 200_000).to("cpu")
-        rate, done, secs, cores = cpu_oracle_rate(w, tc, fr_host, seconds=args.cpu_seconds)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"first {done} tuples of the step's 1M-tuple batch ({secs:.1f} s of CPU work), every "
-                         f"predicate on every tuple, f64 numpy/OpenBLAS"}
+        r = cpu_oracle_rate(w, tc, fr_host, seconds=args.cpu_seconds)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
+               "nproc": r["nproc"], "cpu_model": r["cpu_model"],
+               "one_thread": {"value": r["one_thread_value"], "tuples": r["one_thread_tuples"]},
+               "sample": f"first {r['tuples']} tuples of the step's 1M-tuple batch ({r['seconds']:.1f} s wall on "
+                         f"{r['cores']} single-threaded oracle processes), every predicate on every tuple, f64 numpy"}
     e.close()
     if mlp:
         # MLP hop: tensor-bound; algorithmic flops per input tuple 2*12288*H + 2*H*C
@@ -331,14 +401,14 @@ def run_gpu(args):
         flops_t = 2 * K4_FEATURES * pm["hidden"] + 2 * pm["hidden"] * pm["n_classes"]
         peak_tf = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
         ach_tf = km_tuples * flops_t / (km_ms / 1000.0) / 1e12 if km_ms > 0 else 0.0
-        mtp = os.path.join(ROOT, "profiles", "mlp_dram_traffic.json")
-        mtraffic = json.load(open(mtp)).get("bytes_per_launch") if os.path.exists(mtp) else None
+        mtraffic, mtraffic_note = _profile_traffic("mlp_dram_traffic.json")
         roofline = {"kernel": "hydro_mlp_kernel (K4-MLP: crop gather + two chained tcgen05 GEMMs, CTA pairs)",
                     "bound": "tensor", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach_tf / peak_tf,
                     "frac_vs_burst_peak": ach_tf / peaks["bf16_tflops"],
-                    "traffic": mtraffic, "algorithmic_flops_per_launch": km_tuples * flops_t / max(km_n, 1),
+                    "traffic": mtraffic, "traffic_source": mtraffic_note,
+                    "algorithmic_flops_per_launch": km_tuples * flops_t / max(km_n, 1),
                     "avg_launch_ms": km_ms / max(km_n, 1), "launches": km_n,
-                    "share_of_step": km_ms / max(km_ms + k4_ms + k1_ms + k5_ms + k2c_ms, 1e-9),
+                    "share_of_step": km_ms / ms, "time_source": "device launch timers inside the timed run",
                     "mlp_ms_per_step": km_ms / args.steps, "linear_k4_ms_per_step": k4_ms / args.steps,
                     "k1_ms_per_step": k1_ms / args.steps, "k2_ms_per_step": k2c_ms / args.steps,
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside the step; fp16 "
@@ -346,10 +416,11 @@ def run_gpu(args):
     else:
         roofline = {"kernel": "hydro_classifier_kernel (K4: crop gather + tcgen05 linear head)",
                     "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_note,
                     "algorithmic_bytes_per_launch": k4_bytes / max(k4_n, 1),
+                    "algorithmic_bytes_per_tuple": K4_BYTES_PER_TUPLE, "classifier_tuples_per_step": k4_tuples / args.steps,
                     "avg_launch_ms": k4_ms / max(k4_n, 1), "launches": k4_n,
-                    "share_of_step": k4_ms / max(k4_ms + k1_ms + k5_ms + k2c_ms, 1e-9),
+                    "share_of_step": k4_ms / ms, "time_source": "device launch timers inside the timed run",
                     "k2_ms_per_step": k2c_ms / args.steps,
                     "k1_ms_per_step": k1_ms / args.steps, "k4_ms_per_step": k4_ms / args.steps,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "_fallback" not in peaks else "fallback"}
@@ -361,13 +432,14 @@ def run_gpu(args):
             roofline.update({"traffic_gbs": tgbs, "traffic_frac": tgbs / peaks["hbm_gbs"]})
         if hsv:  # the HSV colour hop (K4-HSV) is ALU work: its own time and rate next to the linear hop
             roofline.update({"hsv_ms_per_step": kh_ms / args.steps, "hsv_launches": kh_n,
-                             "hsv_kernel_tuples_per_s": kh_tuples / (kh_ms / 1000.0) if kh_ms > 0 else None,
-                             "share_of_step": (k4_ms) / max(k4_ms + kh_ms + k1_ms + k5_ms + k2c_ms, 1e-9)})
+                             "hsv_kernel_tuples_per_s": kh_tuples / (kh_ms / 1000.0) if kh_ms > 0 else None})
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-               "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+               "vs_baseline": None, "dtype": "fp16" if all(op_fp16) else "bf16", "data": "synthetic",
                "config": {"workload": WORKLOAD_MLP if mlp else (WORKLOAD_HSV if hsv else WORKLOAD),
+                          "weights": args.weights + (" (every weight fp16-exact: fp16 operands, the same products)"
+                                                     if all(op_fp16) else " (bf16 operands)"),
                           "tuples_per_step": world * TUPLES_PER_STEP,
                           "batch_tuples": TUPLES_PER_STEP, "policy": "score (cost/(1-sel)), measured costs",
                           "l2": "inputs larger than L2: 2.83 GB frame pool + 6 rotating 22 MB tuple batches",
@@ -377,7 +449,7 @@ def run_gpu(args):
                "cpu_baseline": cpu,
                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": int(sum(d2h) / max(len(d2h), 1))},
-               "clocks": clk.summary(), "gpu_launches": launches}
+               "clocks": clk.summary(), "gpu_launches": launches, "paper_context": PAPER_CONTEXT}
         print(json.dumps(out))
     if dist:
         dist.barrier()
@@ -415,9 +487,9 @@ def run_route(args):
         for s in range(k * nb):
             pend.append(e.submit(batches[s % nb]))
             if len(pend) >= 3:
-                outs.append(H.hydro_collect_results(e.ctx, pend.pop(0), res_ids.data_ptr(), res_bb.data_ptr(), batch, 1))
+                outs.append(e.collect_into(pend.pop(0), res_ids, res_bb))
         for bid in pend:
-            outs.append(H.hydro_collect_results(e.ctx, bid, res_ids.data_ptr(), res_bb.data_ptr(), batch, 1))
+            outs.append(e.collect_into(bid, res_ids, res_bb))
 
     run_steps(max(args.warmup, 3))
     torch.cuda.synchronize()
@@ -437,9 +509,12 @@ def run_route(args):
     k2_ms, k2_n = e.kernel_time(3)
     e.set_kernel_timing(False)
     tuples = args.steps * nb * batch
-    alg_bytes = tuples * (2 + 8) + 16 * sum(outs)
+    # SURVEY.md §8(d) R-route: 2 (label) + 4 (id of the 1/2 label-passing tuples) + 2 (id of the 1/4
+    # passing the first HASH) = 8 algorithmic bytes per input tuple
+    alg_bytes = tuples * 8
     peaks = _peaks()
     achieved = alg_bytes / ((k1_ms + k2_ms) / 1000.0) / 1e9
+    achieved_step = alg_bytes / (ms / 1000.0) / 1e9
     out = {"metric": "tuples/s through the 3-predicate cheap conjunction (R-route evidence for K1+K2)",
            "value": tuples / (ms / 1000.0), "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -449,7 +524,10 @@ def run_route(args):
            "roofline": {"kernel": "hydro_route_kernel + hydro_compact_kernel (K1 evaluate + K2 compact/emit)",
                         "bound": "hbm", "achieved": achieved,
                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                        "traffic": None, "algorithmic_bytes_per_tuple": 10 + 16 * sum(outs) / tuples,
+                        "achieved_over_step": achieved_step, "frac_over_step": achieved_step / peaks["hbm_gbs"],
+                        "traffic": None, "algorithmic_bytes_per_tuple": 8,
+                        "bytes_note": "SURVEY.md §8(d): 2 B label + 8 B id x 1/2 + 8 B id x 1/4; the emitted "
+                                      "(id, bbox) rows (16 B x 1/8 read + written) are not counted",
                         "k1_ms_per_step": k1_ms / args.steps, "k2_ms_per_step": k2_ms / args.steps,
                         "k1_launches": k1_n, "k2_launches": k2_n},
            "clocks": clk.summary()}
@@ -520,9 +598,9 @@ def run_uc2(args):
             for a in range(0, n, batch):
                 pend.append(e.submit(t.slice(a, a + batch)))
                 if len(pend) >= 3:
-                    total += H.hydro_collect_results(e.ctx, pend.pop(0), res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
+                    total += e.collect_into(pend.pop(0), res_ids, res_bb)
             for bid in pend:
-                total += H.hydro_collect_results(e.ctx, bid, res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
+                total += e.collect_into(bid, res_ids, res_bb)
             return total
 
         for _ in range(max(args.warmup, 1)):
@@ -590,9 +668,9 @@ def run_area(args):
                 for a in range(0, n, batch):
                     pend.append(e.submit(t.slice(a, min(a + batch, n))))
                     if len(pend) >= 3:
-                        total += H.hydro_collect_results(e.ctx, pend.pop(0), res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
+                        total += e.collect_into(pend.pop(0), res_ids, res_bb)
                 for bid in pend:
-                    total += H.hydro_collect_results(e.ctx, bid, res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
+                    total += e.collect_into(bid, res_ids, res_bb)
                 return total
 
             for _ in range(max(args.warmup, 1)):
@@ -718,9 +796,9 @@ def run_concurrent(args):
             for b in batches:
                 pend.append(seq.submit(b))
                 if len(pend) >= 3:
-                    tot += H.hydro_collect_results(seq.ctx, pend.pop(0), res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
+                    tot += seq.collect_into(pend.pop(0), res_ids, res_bb)
             for bid in pend:
-                tot += H.hydro_collect_results(seq.ctx, bid, res_ids.data_ptr(), res_bb.data_ptr(), batch, 1)
+                tot += seq.collect_into(bid, res_ids, res_bb)
             return tot
 
         ms_seq, tot_seq = timed(seq_pass)
@@ -863,6 +941,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hydro", choices=["hydro", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--weights", default="grid", choices=["grid", "bf16"],
+                    help="classifier heads: fp16-exact 'grid' weights or general bf16 weights (bf16 operands)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute", "mlp", "uc2", "hsv", "area", "concurrent", "small"],
                     help="cfg2 = the BASELINE metric (default); rroute = K1 HBM evidence run; "

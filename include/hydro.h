@@ -102,6 +102,16 @@ enum { HYDRO_CROP_NEAREST = 0, HYDRO_CROP_AREA = 1 }; /* R10 */
 
 typedef struct hydro_ctx hydro_ctx; /* opaque */
 
+/* How the ranks of a data-parallel run exchange their statistics deltas. */
+enum {
+  HYDRO_TRANSPORT_NCCL = 0, /* ncclAllReduce(sum) on a library side stream (default)             */
+  HYDRO_TRANSPORT_HOST = 1  /* the caller's host callback (e.g. a gloo all-reduce): synchronous   */
+};
+/* HOST transport: sums `count` u64 values in place over all ranks (every rank calls it with the
+   same count at the same point); returns 0 on success, anything else is reported as HYDRO_ENCCL.
+   Called on the thread that called hydro_submit_batch / hydro_flush_stats. */
+typedef int32_t (*hydro_allreduce_fn)(void* user, uint64_t* data, int32_t count);
+
 typedef struct {
   int32_t device;            /* CUDA device ordinal                                           */
   void* stream;              /* cudaStream_t to run on (e.g. torch.cuda.current_stream());
@@ -116,8 +126,16 @@ typedef struct {
   int64_t max_batch_tuples;  /* largest batch accepted (default 1<<20, max 1<<30)             */
   int32_t max_inflight;      /* uncollected batches held at once (default 4)                 */
   int32_t rank, world;       /* data-parallel rank / world size (default 0 / 1)              */
-  int32_t sync_every;        /* world > 1: fold (after an NCCL all-reduce of the statistics
-                                deltas) every sync_every batches (default 1)                  */
+  int32_t sync_every;        /* world > 1: the statistics exchange (a11) every sync_every batches
+                                (default 1).  At each sync point the window of the last
+                                sync_every batches' deltas is snapshot and summed over the ranks
+                                (NCCL on a side stream, or the HOST callback) and the window of
+                                the PREVIOUS sync point is folded: every rank folds identical
+                                integers at the same batch, so every rank holds the same order
+                                (routing converges by construction), and the exchange is never
+                                waited on by the batch that starts it.  The warmup slice's
+                                statistics are exchanged and folded at once.  Every rank must
+                                submit the same number of batches (empty batches are legal).  */
   const void* nccl_unique_id;/* world > 1: the 128-byte ncclUniqueId from
                                 hydro_nccl_unique_id() on rank 0, broadcast by the caller.
                                 Also accepted with world == 1 (a 1-rank communicator: the fold
@@ -138,7 +156,12 @@ typedef struct {
                                 then runs on a library-owned stream of that partition (stream
                                 above is ignored) and its grids fit the partition.  Contexts
                                 with distinct sm_group values run on disjoint SMs (SURVEY.md
-                                §8(f) f3, R29).  0 or 1: the whole device                      */
+                                §8(f) f3, R29).  0 or 1: the whole device.  The batch's kernels
+                                still run after the work enqueued on `stream` (when non-NULL)
+                                before the submit (the library stream waits on an event)       */
+  int32_t transport;         /* HYDRO_TRANSPORT_* (world > 1, or world == 1 with a HOST callback) */
+  hydro_allreduce_fn allreduce_fn; /* HOST transport callback (required for it)                 */
+  void* allreduce_user;      /* passed to allreduce_fn                                         */
 } hydro_config;
 
 typedef struct {
@@ -208,6 +231,9 @@ typedef struct {
   int64_t tuples_computed;    /* cumulative tuples actually evaluated (not served by the verdict
                                  cache); == tuples_in without a cache                           */
   double cache_hit_rate;      /* REUSE policy: the last batch's cache hit rate (0 otherwise)   */
+  int32_t operand_fp16;       /* LINEAR / MLP: 1 when the contraction runs on fp16 operands (every
+                                 weight exactly representable in fp16: the same products as bf16),
+                                 0 on bf16 operands; 0 for other kinds                            */
 } hydro_pred_stats;
 
 /* Per-batch record, available after the batch completed (hydro_batch_info). */
@@ -236,7 +262,9 @@ hydro_status hydro_config_default(hydro_config* cfg);
 hydro_status hydro_nccl_unique_id(void* out128);
 
 /* Creates a context on cfg->device.  EINVAL on bad sizes; ENOMEM; ENCCL when the communicator
-   cannot be formed (world > 1; collective over all ranks). */
+   cannot be formed (world > 1; collective over all ranks).  EINVAL: REUSE policy with world > 1
+   (its order is per batch, from that batch's own cache hit rates, which differ between ranks),
+   HOST transport without a callback. */
 hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out);
 
 /* Registers predicate number *pred_id = 0, 1, 2 ... (call order = the conjunction's textual
@@ -308,6 +336,24 @@ hydro_status hydro_get_stats(hydro_ctx* ctx, int32_t pred_id, hydro_pred_stats* 
 /* Current order (synchronises): order[0..P-1]; *n = P. */
 hydro_status hydro_get_order(hydro_ctx* ctx, int32_t* order, int32_t* n);
 
+/* Router of concurrent workers ("cost-driven routing" when
+   the predicates' workers run concurrently; R29).  workers[i] (i < n <= 8) is a context holding ONE
+   predicate (worker i), normally on its own SM partition (sm_groups / sm_group), that has folded
+   statistics (e.g. after a warmup batch every worker evaluated).  A device kernel
+   takes, per worker, its time per tuple c_i = (SM-cycles per tuple, R6) / (the worker's SM count)
+   and its selectivity s_i, and writes order[0..n) = the workers sorted by the policy key, lowest
+   first, ties by index (R2): HYDRO_POLICY_COST c, HYDRO_POLICY_SCORE c / (1 - s)
+   (R1), HYDRO_POLICY_SELECTIVITY s.  cost / sel (host, nullable) receive c_i and
+   s_i.  Synchronises every worker's stream.  EINVAL: n outside [1, 8], a NULL worker, a worker
+   with a predicate count != 1 or no batch yet, workers on different devices, other policies. */
+hydro_status hydro_route_workers(hydro_ctx* const* workers, int32_t n, int32_t policy, int32_t* order, double* cost,
+                                 double* sel);
+
+/* Multi-rank only (a no-op otherwise): folds the outstanding exchanged window, then exchanges and
+   folds the deltas of the batches since the last sync point, so every rank's statistics and order
+   cover every batch.  Collective: every rank calls it at the same point.  Synchronises. */
+hydro_status hydro_flush_stats(hydro_ctx* ctx);
+
 /* Waits for all enqueued work of the context. */
 hydro_status hydro_synchronize(hydro_ctx* ctx);
 
@@ -330,6 +376,12 @@ hydro_status hydro_set_kernel_timing(hydro_ctx* ctx, int32_t enable);
    has no data-aware AREA head or no hop ran yet.  Synchronises the context stream.           */
 hydro_status hydro_debug_balance_bounds(hydro_ctx* ctx, uint32_t* out, int32_t capacity, int32_t* n);
 hydro_status hydro_kernel_time(hydro_ctx* ctx, int32_t kind, double* total_ms, int64_t* launches);
+
+/* Device launch timers of the classifier kernels (kind 1 = K4 linear, 4 = K4-MLP, 5 = K4-HSV),
+   always on and free of host events: every launch that evaluates a hop adds (%globaltimer at its
+   last CTA's end - at its first CTA's start) to the kind's total.  Returns the summed
+   milliseconds and the launch count (synchronises the context stream); reset = 1 then zeroes them. */
+hydro_status hydro_device_time(hydro_ctx* ctx, int32_t kind, int32_t reset, double* total_ms, int64_t* launches);
 
 /* Destroys the context (synchronises first).  Safe on NULL. */
 hydro_status hydro_destroy(hydro_ctx* ctx);

@@ -118,7 +118,8 @@ struct DevState {
   unsigned long long d_in[kMaxPred], d_pass[kMaxPred], d_cost[kMaxPred];
   unsigned long long d_comp[kMaxPred];     // tuples evaluated (not served by the verdict cache)
   unsigned long long d_hit[kMaxPred];      // REUSE probe: cached ids of the batch
-  unsigned long long pend[4 * kMaxPred];   // in[8], pass[8], cost[8], comp[8]  (NCCL all-reduce buffer)
+  unsigned long long pend[4 * kMaxPred];   // in[8], pass[8], cost[8], comp[8]: the local window
+  unsigned long long xfer[2][4 * kMaxPred];  // exchanged windows (multi-rank): summed over the ranks in place
   unsigned long long tot_comp[kMaxPred];
   double s_comp[kMaxPred];
   double hit[kMaxPred];                    // REUSE: the batch's cache hit rate
@@ -127,6 +128,10 @@ struct DevState {
   double s_in[kMaxPred], s_pass[kMaxPred], s_cost[kMaxPred];
   double sel[kMaxPred], cost[kMaxPred], key[kMaxPred];
   unsigned int pad1, pad2;
+  // device launch timers (bench evidence, hydro_device_time): per kernel kind, %globaltimer of the
+  // first CTA's start and the last CTA's end of every launch that did work, summed
+  unsigned long long kt_start[8], kt_end[8], kt_total[8], kt_count[8];
+  unsigned int kt_done[8];
 };
 
 // Hop schedule: the evaluator hops of an order are its LINEAR positions and the starts of its
@@ -214,6 +219,14 @@ struct CompactParams {
   const uint64_t* bbox;
   DevState* st;
 };
+// concurrent-worker router (hydro_route_workers): each worker's device state and SM count
+struct WorkerRoute {
+  const DevState* st[kMaxPred];
+  double sms[kMaxPred];
+  int32_t n;
+  int32_t policy;
+};
+
 constexpr int kCompactUnits = 16;  // HASH rounds from which K1 compacts the alive ids before hashing
 constexpr int kWarpSeg = 256;  // positions per K1 warp per tile (= kRouteTile / 8)
 constexpr int kCompactSegs = 4;  // 2048-position segments per K2 CTA (multiple of 4: vector prefix loads)
@@ -368,6 +381,29 @@ __device__ __forceinline__ void tc_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[1
 }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// ---- device launch timer: thread 0 of every CTA of a launch calls begin after the dispatch check
+// and end after the CTA's work; the last CTA to end adds (last end - first start) to the kind's total
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ktimer_begin(DevState* st, int kind) { atomicMin(&st->kt_start[kind], gtimer_ns()); }
+__device__ __forceinline__ void ktimer_end(DevState* st, int kind) {
+  atomicMax(&st->kt_end[kind], gtimer_ns());
+  __threadfence();
+  const unsigned int n = gridDim.x * gridDim.y * gridDim.z;
+  if (atomicAdd(&st->kt_done[kind], 1u) == n - 1) {
+    __threadfence();
+    const unsigned long long e = atomicAdd(&st->kt_end[kind], 0ull), s = atomicAdd(&st->kt_start[kind], 0ull);
+    st->kt_total[kind] += e > s ? e - s : 0ull;
+    st->kt_count[kind] += 1;
+    st->kt_start[kind] = ~0ull;
+    st->kt_end[kind] = 0ull;
+    st->kt_done[kind] = 0u;
+  }
+}
+
 // ---- method arithmetic on device (independent of oracle/, written from DESIGN.md R5)
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
@@ -396,7 +432,9 @@ void hydro_balance_launch(const hydro::ClsParams& c, uint64_t max_positions, int
 void hydro_mlp_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug);
 void hydro_hsv_launch(const hydro::ClsParams& c, uint64_t max_positions, int num_sms, cudaStream_t stream);
 int hydro_hsv_warps_per_sm();
-__global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode, uint32_t n_batch);
+__global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode, uint32_t n_batch,
+                                  int32_t snap_slot, int32_t apply_slot);
+__global__ void hydro_route_workers_kernel(hydro::WorkerRoute w, int32_t* order, double* cost, double* sel);
 __global__ void hydro_probe_kernel(hydro::DevState* st, const hydro::PredDev* preds, const uint64_t* id, uint32_t base,
                                    uint32_t n);
 __global__ void hydro_cache_put_kernel(uint32_t* known, uint32_t* pass, uint64_t cap, const uint64_t* ids,

@@ -741,7 +741,11 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     tw.step = 1;
     tw.end = tw.lim > tw.lo ? (tw.lim - tw.lo + kTileM - 1) / kTileM : 0u;
   }
-  if (tw.first >= tw.end) return;
+  if (threadIdx.x == 0) ktimer_begin(st, 1);
+  if (tw.first >= tw.end) {
+    if (threadIdx.x == 0) ktimer_end(st, 1);
+    return;
+  }
 
   const long long t_start = clock64();
   const int n_classes = pdg.n_classes, n_pad = pdg.n_pad, target = pdg.target;
@@ -989,6 +993,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   if (tid == 0 && p.collect_stats) {
     atomicAdd(&st->d_cost[pred], static_cast<unsigned long long>(clock64() - t_start));
   }
+  if (tid == 0) ktimer_end(st, 1);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1033,7 +1038,11 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
   const uint32_t num_tiles = (count + kTileM - 1) / kTileM;
   const uint32_t crank = cluster_ctarank();
   const TileWalk tw{blockIdx.x / kP, gridDim.x / kP, (num_tiles + kP - 1) / kP, 0u, count, kP, crank, false};
-  if (tw.first >= tw.end) return;
+  if (threadIdx.x == 0) ktimer_begin(st, 4);
+  if (tw.first >= tw.end) {
+    if (threadIdx.x == 0) ktimer_end(st, 4);
+    return;
+  }
 
   const long long t_start = clock64();
   const PredDev& pdg = p.preds[pred];
@@ -1261,6 +1270,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
   if (tid == 0 && p.collect_stats) {
     atomicAdd(&st->d_cost[pred], static_cast<unsigned long long>(clock64() - t_start));
   }
+  if (tid == 0) ktimer_end(st, 4);
 }
 
 // Host-side entry points (the kernel templates stay inside this translation unit).

@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kHsvThreads, 3) hydro_hsv_kernel(ClsParams p) 
     s_sdiv[i] = i ? (2 * (255 << 12) + i) / (2 * i) : 0;
     s_hdiv[i] = i ? (2 * (30 << 12) + i) / (2 * i) : 0;
   }
+  if (threadIdx.x == 0) ktimer_begin(st, 5);
   __syncthreads();
   const int target = p.preds[pred].target;
   const int lane = threadIdx.x & 31;
@@ -183,6 +184,8 @@ __global__ void __launch_bounds__(kHsvThreads, 3) hydro_hsv_kernel(ClsParams p) 
     atomicAdd(&st->d_comp[pred], static_cast<unsigned long long>(n_in));
     atomicAdd(&st->d_cost[pred], cyc);
   }
+  __syncthreads();
+  if (threadIdx.x == 0) ktimer_end(st, 5);
 }
 
 void hydro_hsv_launch(const ClsParams& c, uint64_t max_positions, int num_sms, cudaStream_t stream) {

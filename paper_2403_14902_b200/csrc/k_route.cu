@@ -889,10 +889,14 @@ __device__ void order_by_keys(DevState* st) {
   build_sched(st->kind, st->order, P, st->sched);
 }
 
-// mode: bit 0 = PREP (batch deltas -> batch record + pending), bit 1 = APPLY (pending -> decayed
-// statistics -> keys -> order), bit 2 = RECORD (order used by this batch's chain), bit 3 = REUSE
-// (the batch's cache hit rates from the probe counts over n_batch tuples -> keys -> order).
-__global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode, uint32_t n_batch) {
+// mode: bit 0 = PREP (batch deltas -> batch record + pending), bit 1 = APPLY (deltas -> decayed
+// statistics -> keys -> order; from `pending`, or with bit 5 from the exchanged window
+// xfer[apply_slot]), bit 2 = RECORD (order used by this batch's chain), bit 3 = REUSE (the batch's
+// cache hit rates from the probe counts over n_batch tuples -> keys -> order), bit 4 = SNAPSHOT
+// (pending -> xfer[snap_slot], pending cleared: the window the ranks' exchange sums).
+// Order inside one launch: REUSE, RECORD, PREP, SNAPSHOT, APPLY.
+__global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode, uint32_t n_batch, int32_t snap_slot,
+                                  int32_t apply_slot) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const int P = st->n_pred;
   if (mode & 8) {
@@ -923,17 +927,24 @@ __global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode, uin
       st->d_in[k] = st->d_pass[k] = st->d_cost[k] = st->d_comp[k] = 0;
     }
   }
+  if (mode & 16) {
+    for (int i = 0; i < 4 * kMaxPred; ++i) {
+      st->xfer[snap_slot][i] = st->pend[i];
+      st->pend[i] = 0;
+    }
+  }
   if (mode & 2) {
     const double g = st->gamma;
+    unsigned long long* src = (mode & 32) ? st->xfer[apply_slot] : st->pend;
     for (int k = 0; k < P; ++k) {
-      const unsigned long long di = st->pend[k];
+      const unsigned long long di = src[k];
       if (di > 0) {  // R4: fold only observed predicates
         st->s_in[k] = g * st->s_in[k] + static_cast<double>(di);
-        st->s_pass[k] = g * st->s_pass[k] + static_cast<double>(st->pend[kMaxPred + k]);
-        st->s_cost[k] = g * st->s_cost[k] + static_cast<double>(st->pend[2 * kMaxPred + k]) * st->cost_norm[k];
-        st->s_comp[k] = g * st->s_comp[k] + static_cast<double>(st->pend[3 * kMaxPred + k]);
+        st->s_pass[k] = g * st->s_pass[k] + static_cast<double>(src[kMaxPred + k]);
+        st->s_cost[k] = g * st->s_cost[k] + static_cast<double>(src[2 * kMaxPred + k]) * st->cost_norm[k];
+        st->s_comp[k] = g * st->s_comp[k] + static_cast<double>(src[3 * kMaxPred + k]);
       }
-      st->pend[k] = st->pend[kMaxPred + k] = st->pend[2 * kMaxPred + k] = st->pend[3 * kMaxPred + k] = 0;
+      src[k] = src[kMaxPred + k] = src[2 * kMaxPred + k] = src[3 * kMaxPred + k] = 0;
     }
     for (int k = 0; k < P; ++k) {
       double s, c;
@@ -952,6 +963,33 @@ __global__ void hydro_fold_kernel(DevState* st, BatchRec* rec, int32_t mode, uin
     }
     order_by_keys(st);
   }
+}
+
+// Router of concurrent workers: worker i is a context
+// holding one predicate on its own SM partition.  Its time per tuple is its folded cost (SM-cycles
+// per tuple, R6) spread over its SMs, its selectivity the folded one; the workers are ordered by
+// the policy key, lowest first, ties by index (R2).  One thread: at most 8 workers.
+__global__ void hydro_route_workers_kernel(WorkerRoute w, int32_t* order, double* cost, double* sel) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double key[kMaxPred];
+  int ord[kMaxPred];
+  for (int k = 0; k < w.n; ++k) {
+    const double c = w.st[k]->cost[0] / w.sms[k], s = w.st[k]->sel[0];
+    key[k] = policy_key(w.policy, c, s, 0.0);
+    cost[k] = c;
+    sel[k] = s;
+    ord[k] = k;
+  }
+  for (int i = 1; i < w.n; ++i) {  // stable insertion sort by (key, index)
+    const int v = ord[i];
+    int j = i - 1;
+    while (j >= 0 && key[ord[j]] > key[v]) {
+      ord[j + 1] = ord[j];
+      --j;
+    }
+    ord[j + 1] = v;
+  }
+  for (int i = 0; i < w.n; ++i) order[i] = ord[i];
 }
 
 // ------------------------------------------------------------------------------------------

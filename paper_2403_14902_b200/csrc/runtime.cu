@@ -154,6 +154,16 @@ struct hydro_ctx {
   int64_t launches = 0;
   int64_t since_sync = 0;
   ncclComm_t comm = nullptr;
+  // statistics exchange between ranks (a11): NCCL on a side stream or the HOST callback
+  bool exchange = false;
+  cudaStream_t xchg_stream = nullptr;
+  cudaEvent_t xchg_ready[2] = {nullptr, nullptr}, xchg_done[2] = {nullptr, nullptr};
+  uint64_t* host_xfer = nullptr;  // pinned, HOST transport
+  int xchg_next = 0;              // slot of the next snapshot
+  int xchg_outstanding = -1;      // slot exchanged at the last sync point, not folded yet
+  // green-context workers run on a library stream: it waits on the caller's stream per submit
+  cudaStream_t user_stream = nullptr;
+  cudaEvent_t user_ev = nullptr;
   int32_t fixed_order[kMaxPred];
   bool fixed_order_set = false;
   bool has_area = false;
@@ -268,7 +278,14 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   if (cfg->policy < 0 || cfg->policy > HYDRO_POLICY_REUSE) return set_err(HYDRO_EINVAL, "unknown policy");
   if (cfg->cost_source < 0 || cfg->cost_source > 1) return set_err(HYDRO_EINVAL, "unknown cost_source");
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return set_err(HYDRO_EINVAL, "bad rank/world");
-  if (cfg->world > 1 && !cfg->nccl_unique_id) return set_err(HYDRO_EINVAL, "world > 1 needs nccl_unique_id");
+  if (cfg->transport != HYDRO_TRANSPORT_NCCL && cfg->transport != HYDRO_TRANSPORT_HOST)
+    return set_err(HYDRO_EINVAL, "unknown transport");
+  if (cfg->transport == HYDRO_TRANSPORT_HOST && !cfg->allreduce_fn)
+    return set_err(HYDRO_EINVAL, "HOST transport needs allreduce_fn");
+  if (cfg->world > 1 && cfg->transport == HYDRO_TRANSPORT_NCCL && !cfg->nccl_unique_id)
+    return set_err(HYDRO_EINVAL, "world > 1 needs nccl_unique_id (NCCL transport)");
+  if (cfg->world > 1 && cfg->policy == HYDRO_POLICY_REUSE)
+    return set_err(HYDRO_EINVAL, "REUSE orders each batch by its own cache hit rate: single rank only");
   if (cfg->sync_every < 1) return set_err(HYDRO_EINVAL, "sync_every >= 1");
   if (cfg->balance != HYDRO_BALANCE_ROUND_ROBIN && cfg->balance != HYDRO_BALANCE_DATA_AWARE)
     return set_err(HYDRO_EINVAL, "unknown balance mode");
@@ -318,6 +335,10 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
     }
     ctx->stream = reinterpret_cast<cudaStream_t>(gs);
     ctx->own_stream = true;
+    if (cfg->stream) {  // keep the caller's stream order: every submit waits on it
+      ctx->user_stream = static_cast<cudaStream_t>(cfg->stream);
+      CU(cudaEventCreateWithFlags(&ctx->user_ev, cudaEventDisableTiming));
+    }
     ctx->num_sms = std::min(ctx->num_sms, static_cast<int>(groups[cfg->sm_group].sm.smCount));
   } else if (cfg->stream) {
     ctx->stream = static_cast<cudaStream_t>(cfg->stream);
@@ -333,7 +354,16 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   CU(cudaMalloc(&ctx->preds_dev, sizeof(PredDev) * kMaxPred));
   CU(cudaMalloc(&ctx->zero_word, 16));
   CU(cudaMemset(ctx->zero_word, 0, 16));
-  if (cfg->nccl_unique_id) {  // world > 1, or world == 1 with an id: exercise the NCCL merge path
+  if (cfg->transport == HYDRO_TRANSPORT_HOST) {
+    ctx->exchange = true;
+    CU(cudaMallocHost(&ctx->host_xfer, sizeof(uint64_t) * 4 * kMaxPred));
+  } else if (cfg->nccl_unique_id) {  // world > 1, or world == 1 with an id: exercise the NCCL merge path
+    ctx->exchange = true;
+    CU(cudaStreamCreateWithFlags(&ctx->xchg_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CU(cudaEventCreateWithFlags(&ctx->xchg_ready[i], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&ctx->xchg_done[i], cudaEventDisableTiming));
+    }
     ncclUniqueId id;
     std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank);
@@ -610,6 +640,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
   }
   for (int i = 0; i < P; ++i) h.position[h.order[i]] = i;
   build_sched(h.kind, h.order, P, h.sched);
+  for (int i = 0; i < 8; ++i) h.kt_start[i] = ~0ull;
   CU(cudaMemcpy(ctx->st, &h, sizeof(h), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(ctx->preds_dev, pd.data(), sizeof(PredDev) * kMaxPred, cudaMemcpyHostToDevice));
   ctx->pd_host = pd;
@@ -766,22 +797,65 @@ static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c0, uint64_t max
   });
 }
 
-static hydro_status launch_fold(hydro_ctx* ctx, BatchRec* rec, int mode) {
-  return timed_launch(ctx, 2, [&] { hydro_fold_kernel<<<1, 32, 0, ctx->stream>>>(ctx->st, rec, mode, 0u); });
+static hydro_status launch_fold(hydro_ctx* ctx, BatchRec* rec, int mode, int snap_slot = 0, int apply_slot = 0) {
+  return timed_launch(ctx, 2, [&] {
+    hydro_fold_kernel<<<1, 32, 0, ctx->stream>>>(ctx->st, rec, mode, 0u, snap_slot, apply_slot);
+  });
 }
 
-static hydro_status fold_and_sync(hydro_ctx* ctx, BatchRec* rec, int record, bool force_sync) {
-  hydro_status s;
-  if (!ctx->comm) return launch_fold(ctx, rec, 1 | 2 | (record ? 4 : 0));
-  if ((s = launch_fold(ctx, rec, 1 | (record ? 4 : 0))) != HYDRO_OK) return s;
-  ctx->since_sync += record ? 1 : 0;
-  if (force_sync || ctx->since_sync >= ctx->cfg.sync_every) {
-    void* pend = reinterpret_cast<char*>(ctx->st) + offsetof(DevState, pend);
-    ncclResult_t r = ncclAllReduce(pend, pend, 4 * kMaxPred, ncclUint64, ncclSum, ctx->comm,
-                                   ctx->stream);
+// Sums the window snapshot in xfer[slot] over the ranks, in place.  NCCL:
+// an all-reduce on the side stream after the snapshot, completion recorded in xchg_done[slot]
+// (the compute stream never waits for it until the window is folded, one sync point later).
+// HOST: the caller's callback on a pinned copy (synchronous), written back in stream order.
+static hydro_status exchange_slot(hydro_ctx* ctx, int slot) {
+  void* buf = reinterpret_cast<char*>(ctx->st) + offsetof(DevState, xfer) + sizeof(uint64_t) * 4 * kMaxPred * slot;
+  const size_t bytes = sizeof(uint64_t) * 4 * kMaxPred;
+  if (ctx->comm) {
+    CU(cudaEventRecord(ctx->xchg_ready[slot], ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->xchg_stream, ctx->xchg_ready[slot], 0));
+    ncclResult_t r = ncclAllReduce(buf, buf, 4 * kMaxPred, ncclUint64, ncclSum, ctx->comm, ctx->xchg_stream);
     if (r != ncclSuccess) return ctx_fail(ctx, HYDRO_ENCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
-    ctx->since_sync = 0;
-    return launch_fold(ctx, rec, 2);
+    CU(cudaEventRecord(ctx->xchg_done[slot], ctx->xchg_stream));
+    return HYDRO_OK;
+  }
+  CU(cudaMemcpyAsync(ctx->host_xfer, buf, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  const int32_t rc = ctx->cfg.allreduce_fn(ctx->cfg.allreduce_user, ctx->host_xfer, 4 * kMaxPred);
+  if (rc != 0) return ctx_fail(ctx, HYDRO_ENCCL, "HOST transport all-reduce callback failed (" + std::to_string(rc) + ")");
+  CU(cudaMemcpyAsync(buf, ctx->host_xfer, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return HYDRO_OK;
+}
+
+// The compute stream may fold xfer[slot] once its exchange completed.
+static hydro_status wait_exchange(hydro_ctx* ctx, int slot) {
+  if (ctx->comm) CU(cudaStreamWaitEvent(ctx->stream, ctx->xchg_done[slot], 0));
+  return HYDRO_OK;
+}
+
+// End-of-batch (record = 1) or warmup-slice (force = true) statistics step.  Single rank: the
+// deltas are folded at once.  Multi-rank: the deltas join the local window; at a sync point
+// (every sync_every batches) ONE launch records, snapshots the window into a slot and folds the
+// window exchanged at the previous sync point, then the new slot's exchange is started.  force:
+// the window is exchanged and folded immediately (the warmup slice, hydro_flush_stats).
+static hydro_status fold_and_sync(hydro_ctx* ctx, BatchRec* rec, int record, bool force) {
+  hydro_status s;
+  const int rec_bits = rec ? (1 | (record ? 4 : 0)) : 0;
+  if (!ctx->exchange) return launch_fold(ctx, rec, rec_bits | 2);
+  ctx->since_sync += record ? 1 : 0;
+  if (!force && ctx->since_sync < ctx->cfg.sync_every) return launch_fold(ctx, rec, rec_bits);
+  const int snap = ctx->xchg_next;
+  ctx->xchg_next ^= 1;
+  const int prev = ctx->xchg_outstanding;
+  if (prev >= 0 && (s = wait_exchange(ctx, prev)) != HYDRO_OK) return s;
+  if ((s = launch_fold(ctx, rec, rec_bits | 16 | (prev >= 0 ? (2 | 32) : 0), snap, prev >= 0 ? prev : 0)) != HYDRO_OK)
+    return s;
+  if ((s = exchange_slot(ctx, snap)) != HYDRO_OK) return s;
+  ctx->since_sync = 0;
+  ctx->xchg_outstanding = snap;
+  if (force) {
+    if ((s = wait_exchange(ctx, snap)) != HYDRO_OK) return s;
+    if ((s = launch_fold(ctx, nullptr, 2 | 32, 0, snap)) != HYDRO_OK) return s;
+    ctx->xchg_outstanding = -1;
   }
   return HYDRO_OK;
 }
@@ -840,6 +914,10 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
     lab = sl.s_label;
   }
   if (t->wait_event) CU(cudaStreamWaitEvent(ctx->stream, static_cast<cudaEvent_t>(t->wait_event), 0));
+  if (ctx->user_stream) {  // a green-context worker: after the caller's stream's earlier work
+    CU(cudaEventRecord(ctx->user_ev, ctx->user_stream));
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->user_ev, 0));
+  }
   CU(cudaMemsetAsync(sl.rec, 0, sizeof(BatchRec), ctx->stream));
   const int P = static_cast<int>(ctx->preds.size());
   uint64_t warm = 0;
@@ -901,7 +979,7 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
          })) != HYDRO_OK)
       return s;
     if ((s = timed_launch(ctx, 2, [&] {
-           hydro_fold_kernel<<<1, 32, 0, ctx->stream>>>(ctx->st, sl.rec, 8, rest_n);
+           hydro_fold_kernel<<<1, 32, 0, ctx->stream>>>(ctx->st, sl.rec, 8, rest_n, 0, 0);
          })) != HYDRO_OK)
       return s;
   }
@@ -1072,6 +1150,7 @@ hydro_status hydro_get_stats(hydro_ctx* ctx, int32_t k, hydro_pred_stats* out) {
   out->cost_raw_total = h.tot_cost[k];
   out->tuples_computed = static_cast<int64_t>(h.tot_comp[k]);
   out->cache_hit_rate = h.hit[k];
+  out->operand_fp16 = ctx->preds[k].a_fp16;
   return HYDRO_OK;
 }
 
@@ -1083,6 +1162,58 @@ hydro_status hydro_get_order(hydro_ctx* ctx, int32_t* order, int32_t* n) {
   *n = h.n_pred;
   for (int i = 0; i < h.n_pred; ++i) order[i] = h.order[i];
   return HYDRO_OK;
+}
+
+hydro_status hydro_route_workers(hydro_ctx* const* workers, int32_t n, int32_t policy, int32_t* order, double* cost,
+                                 double* sel) {
+  if (!workers || !order) return set_err(HYDRO_EINVAL, "NULL argument");
+  if (n < 1 || n > kMaxPred) return set_err(HYDRO_EINVAL, "n must be in [1, 8]");
+  if (policy != HYDRO_POLICY_COST && policy != HYDRO_POLICY_SCORE && policy != HYDRO_POLICY_SELECTIVITY)
+    return set_err(HYDRO_EINVAL, "policy must be COST, SCORE or SELECTIVITY");
+  WorkerRoute wr{};
+  wr.n = n;
+  wr.policy = policy;
+  for (int i = 0; i < n; ++i) {
+    hydro_ctx* w = workers[i];
+    if (!w) return set_err(HYDRO_EINVAL, "NULL worker");
+    if (w->preds.size() != 1 || !w->frozen) return set_err(HYDRO_EINVAL, "a worker holds one predicate and has run a batch");
+    if (w->cfg.device != workers[0]->cfg.device) return set_err(HYDRO_EINVAL, "workers on different devices");
+    hydro_status s = hydro_synchronize(w);
+    if (s != HYDRO_OK) return s;
+    wr.st[i] = w->st;
+    wr.sms[i] = static_cast<double>(std::max(w->num_sms, 1));
+  }
+  hydro_ctx* ctx = workers[0];
+  void* buf = nullptr;
+  CU(cudaMalloc(&buf, 256));
+  int32_t* d_order = static_cast<int32_t*>(buf);
+  double* d_cost = reinterpret_cast<double*>(static_cast<char*>(buf) + 64);
+  double* d_sel = reinterpret_cast<double*>(static_cast<char*>(buf) + 128);
+  hydro_route_workers_kernel<<<1, 32, 0, ctx->stream>>>(wr, d_order, d_cost, d_sel);
+  ctx->launches += 1;
+  cudaError_t e = cudaGetLastError();
+  double h_cost[kMaxPred], h_sel[kMaxPred];
+  if (e == cudaSuccess) e = cudaMemcpyAsync(order, d_order, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_cost, d_cost, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h_sel, d_sel, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(buf);
+  if (e != cudaSuccess) return ctx_fail(ctx, HYDRO_ECUDA, std::string("hydro_route_workers: ") + cudaGetErrorString(e));
+  for (int i = 0; i < n; ++i) {
+    if (cost) cost[i] = h_cost[i];
+    if (sel) sel[i] = h_sel[i];
+  }
+  return HYDRO_OK;
+}
+
+hydro_status hydro_flush_stats(hydro_ctx* ctx) {
+  if (!ctx) return set_err(HYDRO_EINVAL, "NULL argument");
+  hydro_status s = check_sticky(ctx);
+  if (s != HYDRO_OK) return s;
+  if (!ctx->exchange || !ctx->frozen) return HYDRO_OK;
+  if ((s = fold_and_sync(ctx, nullptr, 0, true)) != HYDRO_OK) return s;
+  CU(cudaStreamSynchronize(ctx->stream));
+  return check_sticky(ctx);
 }
 
 hydro_status hydro_synchronize(hydro_ctx* ctx) {
@@ -1118,6 +1249,22 @@ hydro_status hydro_debug_balance_bounds(hydro_ctx* ctx, uint32_t* out, int32_t c
   hydro_status s = check_sticky(ctx);
   if (s != HYDRO_OK) return s;
   CU(cudaMemcpy(out, ctx->bal_bounds, sizeof(uint32_t) * (*n), cudaMemcpyDeviceToHost));
+  return HYDRO_OK;
+}
+
+hydro_status hydro_device_time(hydro_ctx* ctx, int32_t kind, int32_t reset, double* total_ms, int64_t* launches) {
+  if (!ctx || !total_ms || !launches) return set_err(HYDRO_EINVAL, "NULL argument");
+  if (kind != 1 && kind != 4 && kind != 5) return set_err(HYDRO_EINVAL, "device timers exist for kinds 1, 4, 5");
+  DevState h;
+  hydro_status s = read_state(ctx, &h);
+  if (s != HYDRO_OK) return s;
+  *total_ms = static_cast<double>(h.kt_total[kind]) * 1e-6;
+  *launches = static_cast<int64_t>(h.kt_count[kind]);
+  if (reset) {
+    const unsigned long long z[2] = {0ull, 0ull};
+    CU(cudaMemcpy(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, kt_total) + 8 * kind, z, 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, kt_count) + 8 * kind, z, 8, cudaMemcpyHostToDevice));
+  }
   return HYDRO_OK;
 }
 
@@ -1225,7 +1372,15 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
   cudaFree(ctx->bal_chunks);
   cudaFree(ctx->bal_bounds);
   cudaFree(ctx->zero_word);
+  if (ctx->xchg_stream) cudaStreamSynchronize(ctx->xchg_stream);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->xchg_stream) cudaStreamDestroy(ctx->xchg_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->xchg_ready[i]) cudaEventDestroy(ctx->xchg_ready[i]);
+    if (ctx->xchg_done[i]) cudaEventDestroy(ctx->xchg_done[i]);
+  }
+  if (ctx->host_xfer) cudaFreeHost(ctx->host_xfer);
+  if (ctx->user_ev) cudaEventDestroy(ctx->user_ev);
   if (ctx->copy_stream) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);

@@ -40,7 +40,13 @@ class hydro_config(C.Structure):
                 ("max_batch_tuples", C.c_int64), ("max_inflight", C.c_int32), ("rank", C.c_int32),
                 ("world", C.c_int32), ("sync_every", C.c_int32), ("nccl_unique_id", C.c_void_p),
                 ("frames", C.c_void_p), ("n_frames", C.c_int32), ("frame_h", C.c_int32), ("frame_w", C.c_int32),
-                ("balance", C.c_int32), ("max_sms", C.c_int32), ("sm_groups", C.c_int32), ("sm_group", C.c_int32)]
+                ("balance", C.c_int32), ("max_sms", C.c_int32), ("sm_groups", C.c_int32), ("sm_group", C.c_int32),
+                ("transport", C.c_int32), ("allreduce_fn", C.c_void_p), ("allreduce_user", C.c_void_p)]
+
+
+# int32_t (*hydro_allreduce_fn)(void* user, uint64_t* data, int32_t count)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.POINTER(C.c_uint64), C.c_int32)
+TRANSPORT = {"nccl": 0, "host": 1}
 
 
 class hydro_predicate_desc(C.Structure):
@@ -62,7 +68,8 @@ class hydro_pred_stats(C.Structure):
     _fields_ = [("tuples_in", C.c_int64), ("tuples_passed", C.c_int64), ("cost_per_tuple", C.c_double),
                 ("selectivity", C.c_double), ("rank", C.c_double), ("position", C.c_int32),
                 ("s_in", C.c_double), ("s_pass", C.c_double), ("s_cost", C.c_double),
-                ("cost_raw_total", C.c_double), ("tuples_computed", C.c_int64), ("cache_hit_rate", C.c_double)]
+                ("cost_raw_total", C.c_double), ("tuples_computed", C.c_int64), ("cache_hit_rate", C.c_double),
+                ("operand_fp16", C.c_int32)]
 
 
 class hydro_batch_report(C.Structure):
@@ -94,9 +101,13 @@ _SIGS = {
     "hydro_get_stats": ([_P, C.c_int32, C.POINTER(hydro_pred_stats)], C.c_int32),
     "hydro_get_order": ([_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)], C.c_int32),
     "hydro_synchronize": ([_P], C.c_int32),
+    "hydro_flush_stats": ([_P], C.c_int32),
+    "hydro_route_workers": ([C.POINTER(_P), C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                             C.POINTER(C.c_double)], C.c_int32),
     "hydro_launch_count": ([_P, C.POINTER(C.c_int64)], C.c_int32),
     "hydro_set_kernel_timing": ([_P, C.c_int32], C.c_int32),
     "hydro_kernel_time": ([_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int32),
+    "hydro_device_time": ([_P, C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int32),
     "hydro_debug_balance_bounds": ([_P, C.POINTER(C.c_uint32), C.c_int32, C.POINTER(C.c_int32)], C.c_int32),
     "hydro_destroy": ([_P], C.c_int32),
     "hydro_debug_linear": ([_P, C.c_int32, C.POINTER(hydro_tuples), _P, _P, _P], C.c_int32),
@@ -230,6 +241,21 @@ def hydro_synchronize(ctx):
     _check(lib().hydro_synchronize(ctx))
 
 
+def hydro_route_workers(ctxs: Sequence, policy: str):
+    """(order, cost per tuple per worker, selectivity) from the workers' folded statistics (f3)."""
+    n = len(ctxs)
+    arr = (_P * n)(*[c.value if isinstance(c, C.c_void_p) else c for c in ctxs])
+    order = (C.c_int32 * n)()
+    cost = (C.c_double * n)()
+    sel = (C.c_double * n)()
+    _check(lib().hydro_route_workers(arr, n, POLICY[policy], order, cost, sel))
+    return list(order), list(cost), list(sel)
+
+
+def hydro_flush_stats(ctx):
+    _check(lib().hydro_flush_stats(ctx))
+
+
 def hydro_launch_count(ctx) -> int:
     n = C.c_int64()
     _check(lib().hydro_launch_count(ctx, C.byref(n)))
@@ -244,6 +270,13 @@ def hydro_kernel_time(ctx, kind: int):
     ms = C.c_double()
     n = C.c_int64()
     _check(lib().hydro_kernel_time(ctx, kind, C.byref(ms), C.byref(n)))
+    return ms.value, n.value
+
+
+def hydro_device_time(ctx, kind: int, reset: bool = False):
+    ms = C.c_double()
+    n = C.c_int64()
+    _check(lib().hydro_device_time(ctx, kind, 1 if reset else 0, C.byref(ms), C.byref(n)))
     return ms.value, n.value
 
 
@@ -285,7 +318,10 @@ class Eddy:
                  warmup_tuples: int = 65536, max_batch_tuples: int = 1 << 20, max_inflight: int = 4,
                  rank: int = 0, world: int = 1, sync_every: int = 1, nccl_unique_id: Optional[bytes] = None,
                  stream: Optional[torch.cuda.Stream] = None, balance: str = "round_robin", max_sms: int = 0,
-                 sm_groups: int = 0, sm_group: int = 0):
+                 sm_groups: int = 0, sm_group: int = 0, allreduce=None):
+        """allreduce: HOST statistics transport (hydro.h HYDRO_TRANSPORT_HOST) -- a callable summing
+        an int64 CPU tensor in place over the ranks, e.g. ``lambda t: dist.all_reduce(t)`` on a
+        gloo group; None = NCCL (world > 1 needs nccl_unique_id)."""
         cfg = hydro_config_default()
         cfg.device = device
         cfg.stream = (stream or torch.cuda.current_stream(device)).cuda_stream
@@ -301,6 +337,19 @@ class Eddy:
         cfg.max_sms = max_sms
         cfg.sm_groups, cfg.sm_group = sm_groups, sm_group
         self._uid = None
+        self._allreduce = None
+        if allreduce is not None:
+            def _cb(user, data, count, _f=allreduce):
+                try:
+                    t = torch.frombuffer(C.cast(data, C.POINTER(C.c_uint8 * (8 * count))).contents,
+                                         dtype=torch.int64)
+                    _f(t)
+                    return 0
+                except Exception:  # reported as HYDRO_ENCCL by the library
+                    return 1
+            self._allreduce = ALLREDUCE_FN(_cb)  # kept alive for the context's lifetime
+            cfg.transport = TRANSPORT["host"]
+            cfg.allreduce_fn = C.cast(self._allreduce, C.c_void_p)
         if nccl_unique_id is not None:
             self._uid = C.create_string_buffer(nccl_unique_id, 128)
             cfg.nccl_unique_id = C.cast(self._uid, C.c_void_p)
@@ -314,6 +363,7 @@ class Eddy:
         self.ctx = hydro_create(cfg)
         self.n_pred = 0
         self._keep: List[object] = []
+        self._inflight: Dict[int, tuple] = {}  # batch id -> borrowed tensors (kept alive until collect)
 
     def add_predicate(self, p: Dict) -> int:
         d = hydro_predicate_desc()
@@ -372,7 +422,10 @@ class Eddy:
             t.sel, t.sel_count, t.n = sel[0], sel[1], int(sel[2])
         if wait_event is not None:
             t.wait_event = wait_event
-        return hydro_submit_batch(self.ctx, t)
+        bid = hydro_submit_batch(self.ctx, t)
+        # the C ABI borrows the columns until the batch is collected or released
+        self._inflight[bid] = (tuples.id, tuples.frame_id, tuples.bbox, tuples.label)
+        return bid
 
     def batch_output(self, batch_id: int):
         return hydro_batch_output(self.ctx, batch_id)
@@ -386,10 +439,23 @@ class Eddy:
         ids = torch.empty(max(n, 1), dtype=torch.int64, device=device, pin_memory=pin and not on_dev)
         bbox = torch.empty((max(n, 1), 4), dtype=torch.int16, device=device, pin_memory=pin and not on_dev)
         got = hydro_collect_results(self.ctx, batch_id, ids.data_ptr(), bbox.data_ptr(), n, 1 if on_dev else 0)
+        self._inflight.pop(batch_id, None)
         return ids[:got], bbox[:got]
+
+    def collect_into(self, batch_id: int, ids: torch.Tensor, bbox: torch.Tensor) -> int:
+        """Copies the rows into caller buffers (host or device); returns the count."""
+        got = hydro_collect_results(self.ctx, batch_id, ids.data_ptr(), bbox.data_ptr(), int(ids.shape[0]),
+                                    1 if ids.is_cuda else 0)
+        self._inflight.pop(batch_id, None)
+        return got
 
     def release(self, batch_id: int):
         hydro_release_batch(self.ctx, batch_id)
+        self._inflight.pop(batch_id, None)
+
+    def flush_stats(self):
+        """Multi-rank: fold every outstanding statistics window (collective over the ranks)."""
+        hydro_flush_stats(self.ctx)
 
     def batch_info(self, batch_id: int) -> Dict:
         r = hydro_batch_info(self.ctx, batch_id)
@@ -435,6 +501,10 @@ class Eddy:
     def kernel_time(self, kind: int):
         return hydro_kernel_time(self.ctx, kind)
 
+    def device_time(self, kind: int, reset: bool = False):
+        """(ms, launches) summed by the classifier kernels' device timers (kind 1 / 4 / 5)."""
+        return hydro_device_time(self.ctx, kind, reset)
+
     def debug_balance_bounds(self) -> List[int]:
         return hydro_debug_balance_bounds(self.ctx)
 
@@ -446,6 +516,7 @@ class Eddy:
         if getattr(self, "ctx", None) is not None:
             hydro_destroy(self.ctx)
             self.ctx = None
+            self._inflight = {}
 
     def __del__(self):
         try:

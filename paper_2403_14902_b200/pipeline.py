@@ -12,8 +12,9 @@ routing batch visits the workers in the order the policy picks; worker ``order[i
 survivors of worker ``order[i]`` straight from device memory (``hydro_batch_output`` -> a selection
 batch), its stream waiting on the producer batch's done event, so batch b+1's first stage overlaps
 batch b's later stages.  Every step runs in libhydro's kernels; this module only sequences the
-calls and decides the order (the paper's router), from statistics measured in a warmup phase in
-which every worker evaluates the same batch.
+calls; the order (the paper's router) is decided inside libhydro (``hydro_route_workers``, a device
+kernel over the workers' folded statistics) after a warmup phase in which every worker evaluates the
+same batch.
 """
 from __future__ import annotations
 
@@ -22,25 +23,9 @@ from typing import Dict, List, Optional, Sequence
 
 import torch
 
-from .hydro import Eddy, hydro_collect_results
+from .hydro import Eddy, hydro_route_workers
 
 POLICIES = ("cost", "score", "selectivity")
-
-
-def order_by_policy(policy: str, cost: Sequence[float], sel: Sequence[float]) -> List[int]:
-    """Lowest key first, ties by predicate id (R2): cost, cost/(1-sel) (PAPER.md:324,
-    R1 for s >= 1 / c = 0), selectivity (PAPER.md:355)."""
-    def key(k):
-        c, s = cost[k], sel[k]
-        if policy == "cost":
-            return c
-        if policy == "selectivity":
-            return s
-        if c == 0.0:
-            return 0.0
-        return float("inf") if s >= 1.0 else c / (1.0 - s)
-
-    return sorted(range(len(cost)), key=lambda k: (key(k), k))
 
 
 class ConcurrentEddy:
@@ -72,28 +57,34 @@ class ConcurrentEddy:
             self.workers.append(e)
         self.sms = sms
         self.order: List[int] = list(range(P))
-        self.cost_per_tuple = [1.0] * P   # SM-cycles per tuple (R6) / SMs of the worker
+        self.cost_per_tuple = [1.0] * P   # reported by the router: SM-cycles per tuple (R6) / worker SMs
         self.selectivity = [0.5] * P
 
     # ---- warmup: every worker evaluates the same batch; unconditional statistics
+    @staticmethod
+    def _producer_event():
+        """Event on the caller's current stream: the workers' first kernels wait for the work that
+        produced the tuples (the workers run on their own streams)."""
+        ev = torch.cuda.Event()
+        ev.record()
+        return ev
+
     def warmup(self, tuples) -> List[int]:
-        bids = [w.submit(tuples) for w in self.workers]
+        ev = self._producer_event()
+        bids = [w.submit(tuples, wait_event=ev.cuda_event) for w in self.workers]
         for w, b in zip(self.workers, bids):
             w.collect(b)
-        for k, w in enumerate(self.workers):
-            st = w.stats(0)
-            # a worker's time per tuple: its cycles per tuple spread over its SM budget
-            self.cost_per_tuple[k] = st["cost_per_tuple"] / max(self.sms[k], 1)
-            self.selectivity[k] = st["selectivity"]
-        self.order = order_by_policy(self.policy, self.cost_per_tuple, self.selectivity)
+        self.order, self.cost_per_tuple, self.selectivity = hydro_route_workers([w.ctx for w in self.workers],
+                                                                                self.policy)
         return self.order
 
     # ---- streaming: batch b's stage i on worker order[i] after stage i-1 (device-side chaining)
     def _submit(self, tuples) -> List[int]:
         chain = []
+        ev = self._producer_event()
         for i, k in enumerate(self.order):
             if i == 0:
-                chain.append(self.workers[k].submit(tuples))
+                chain.append(self.workers[k].submit(tuples, wait_event=ev.cuda_event))
             else:
                 prev = self.order[i - 1]
                 pos, cnt, ev = self.workers[prev].batch_output(chain[-1])
@@ -105,7 +96,7 @@ class ConcurrentEddy:
         if ids_out is None:
             ids, bb = last.collect(chain[-1])
         else:  # device outputs (bench): no host copy
-            n = hydro_collect_results(last.ctx, chain[-1], ids_out.data_ptr(), bb_out.data_ptr(), ids_out.shape[0], 1)
+            n = last.collect_into(chain[-1], ids_out, bb_out)
             ids, bb = n, None
         for i in range(len(chain) - 1):  # the earlier stages' survivors were consumed on the device
             self.workers[self.order[i]].release(chain[i])

@@ -18,21 +18,26 @@ Recipe (DESIGN.md §3 "Input recipe"):
   log-uniformly by octave in ``[w_min, w_min * 2**n_octaves)`` and clipped to
   the frame; the position is uniform inside the frame;
 * frames: HWC uint8 noise, ``n_frames`` x H x W x 3;
-* linear heads: weights 2^-8 * {-2..2} stored as bf16 (exact), biases 2^-8 * (integer, +1/2 on
-  the target), so nearest-crop logits are exact multiples of 2^-9 and the target's margin is
-  never 0 (DESIGN.md reading R12);
+* linear heads: ``weights="grid"``: 2^-8 * {-2..2} stored as bf16 (exact, also fp16-exact),
+  biases 2^-8 * (integer, +1/2 on the target); ``weights="bf16"``: N(0, (2.5e-4)^2) rounded to
+  bf16 (SURVEY.md §8(c) Q17; many are not fp16-representable), centring biases in f32;
+* margin guarantee (R12): a tuple's bbox can be redrawn with a
+  retry counter (``retry`` of ``make_tuples``: the draws use index ``id + retry * 2^40``); the
+  counters come from a table written by ``tools/oracle_cache.py`` (which calls only ``oracle/``)
+  so that every classifier margin of the workload is >= 0.05;
 * HASH predicates: threshold ``T = round(sel * 2**32)``.
 """
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence
 
 import numpy as np
 import torch
 
-GEN_VERSION = 1
+GEN_VERSION = 2  # 2: per-tuple bbox redraw counters (margin guarantee, R12) and general bf16 heads
 M32 = 0xFFFFFFFF
 _MULT = 0x45D9F3B  # < 2**27, so (x < 2**32) * _MULT < 2**59 fits int64
 
@@ -40,6 +45,8 @@ _MULT = 0x45D9F3B  # < 2**27, so (x < 2**32) * _MULT < 2**59 fits int64
 S_LABEL, S_LABEL2, S_WOCT, S_WOFF, S_HOCT, S_HOFF, S_X, S_Y, S_FRAME, S_WEIGHT = range(1, 11)
 S_W1, S_W2 = 11, 12
 S_BLOCK, S_NOISE = 13, 14
+S_GAUSS_A, S_GAUSS_B = 15, 16
+REDRAW_STRIDE = 1 << 40  # draw index of a redrawn bbox: id + retry * 2^40 (ids < 2^40)
 # palette of the coloured frame pool (RGB; one per HSV class of DESIGN.md R27, plus orange)
 PALETTE = [(200, 30, 30), (15, 15, 15), (128, 128, 128), (220, 200, 40), (40, 160, 40), (40, 60, 200),
            (130, 40, 160), (230, 120, 170), (240, 240, 240), (200, 120, 40)]
@@ -110,7 +117,8 @@ def _octave_size(seed, s_oct, s_off, ids, lo, n_oct, limit):
 
 def make_tuples(seed: int, id_start: int, n: int, *, n_frames: int, frame_h: int, frame_w: int,
                 dets_per_frame: int = 4, p_dog: float = 0.5, w_min: int = 32, n_octaves: int = 3,
-                device="cpu") -> Tuples:
+                device="cpu", retry: Optional[torch.Tensor] = None) -> Tuples:
+    """``retry`` (int64 [n], optional): per-tuple bbox redraw counter (0 = the first draw)."""
     ids = torch.arange(id_start, id_start + n, dtype=torch.int64, device=device)
     frame_id = torch.div(ids, dets_per_frame, rounding_mode="floor") % n_frames
     dog_cut = int(round(p_dog * 2 ** 32))
@@ -118,10 +126,11 @@ def make_tuples(seed: int, id_start: int, n: int, *, n_frames: int, frame_h: int
     other = gen_u32(seed, S_LABEL2, ids) % 79
     other = other + (other >= DOG_LABEL).to(torch.int64)
     label = torch.where(u < dog_cut, torch.full_like(u, DOG_LABEL), other)
-    w = _octave_size(seed, S_WOCT, S_WOFF, ids, w_min, n_octaves, frame_w)
-    h = _octave_size(seed, S_HOCT, S_HOFF, ids, w_min, n_octaves, frame_h)
-    x0 = gen_u32(seed, S_X, ids) % (frame_w - w + 1)
-    y0 = gen_u32(seed, S_Y, ids) % (frame_h - h + 1)
+    bidx = ids if retry is None else ids + retry.to(device=device, dtype=torch.int64) * REDRAW_STRIDE
+    w = _octave_size(seed, S_WOCT, S_WOFF, bidx, w_min, n_octaves, frame_w)
+    h = _octave_size(seed, S_HOCT, S_HOFF, bidx, w_min, n_octaves, frame_h)
+    x0 = gen_u32(seed, S_X, bidx) % (frame_w - w + 1)
+    y0 = gen_u32(seed, S_Y, bidx) % (frame_h - h + 1)
     bbox = torch.stack([x0, y0, x0 + w, y0 + h], dim=1)
     return Tuples(ids, frame_id.to(torch.int32), bbox.to(torch.int16), label.to(torch.int16))
 
@@ -186,56 +195,77 @@ def target_offset_sigmas(n_classes: int, selectivity: float) -> float:
 
 
 WEIGHT_SCALE = 2.0 ** -8  # keeps AREA-crop logits (non-integer inputs) well inside fp32 (R12)
+BF16_SIGMA = 2.5e-4       # general bf16 heads: W ~ N(0, sigma^2)
+BF16_W2_SIGMA = 0.03      # general bf16 MLP heads: second layer W2 ~ N(0, sigma^2)
+
+
+def gen_normal(seed: int, stream: int, idx: torch.Tensor) -> torch.Tensor:
+    """Counter-based N(0, 1) draw (Box-Muller on two u32 draws), float64 on the CPU."""
+    u1 = (gen_u32(seed, stream, idx).to(torch.float64) + 0.5) / 2.0 ** 32
+    u2 = gen_u32(seed, stream + 100, idx).to(torch.float64) / 2.0 ** 32
+    return torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(2.0 * math.pi * u2)
+
+
+def _draw_weights(seed: int, stream: int, rows: int, cols: int, weights: str, sigma: float) -> torch.Tensor:
+    """[rows][cols] float64 weights holding bf16 values: "grid" = s * {-2..2} (s = 2^-8),
+    "bf16" = bf16(sigma * N(0, 1))."""
+    r = torch.arange(rows, dtype=torch.int64)[:, None]
+    c = torch.arange(cols, dtype=torch.int64)[None, :]
+    idx = r * cols + c
+    if weights == "grid":
+        return (gen_u32(seed, stream, idx) % 5 - 2).to(torch.float64) * WEIGHT_SCALE
+    if weights == "bf16":
+        return (gen_normal(seed, stream, idx) * sigma).to(torch.bfloat16).to(torch.float64)
+    raise ValueError(f"weights must be 'grid' or 'bf16', not {weights!r}")
 
 
 def make_linear_head(seed: int, n_classes: int, target: int, selectivity: float,
-                     k_features: int = K_FEATURES):
-    """Weights s * {-2..2} (s = 2^-8; exact in bf16 and fp16) and half-integer-offset biases.
-
-    b_c = -s * floor(127.5 * sum_k W_ck) centres every logit; the target additionally
-    gets s * (D + 0.5) with D = round(kappa * sigma) so that the (approximate, iid-Gaussian)
-    pass rate is ``selectivity``.  Only the target bias carries the s/2, so with integer
-    (nearest-crop) inputs every logit is an exact multiple of s/2 and the target never ties.
+                     k_features: int = K_FEATURES, weights: str = "grid"):
+    """weights="grid": W = s * {-2..2} (s = 2^-8; exact in bf16 and fp16) and half-integer-offset
+    biases: b_c = -s * floor(127.5 * sum_k W_ck / s) centres every logit; the target additionally
+    gets s * (D + 0.5) with D = round(kappa * sigma / s) so that the (approximate, iid-Gaussian)
+    pass rate is ``selectivity``.  weights="bf16": W = bf16(N(0, 2.5e-4^2)), b_c = f32(-127.5 *
+    sum_k W_ck), target + kappa * sigma.  sigma is the logit spread over uniform-noise pixels.
     """
-    c = torch.arange(n_classes, dtype=torch.int64)[:, None]
-    k = torch.arange(k_features, dtype=torch.int64)[None, :]
-    wi = gen_u32(seed, S_WEIGHT, c * k_features + k) % 5 - 2
-    rowsum = wi.sum(dim=1)
-    bias = torch.floor(-127.5 * rowsum.to(torch.float64))
-    sigma = math.sqrt(_PIX_VAR * float((wi * wi).sum(dim=1).to(torch.float64).mean()))
+    W = _draw_weights(seed, S_WEIGHT, n_classes, k_features, weights, BF16_SIGMA)
+    sigma = math.sqrt(_PIX_VAR * float((W * W).sum(dim=1).mean()))
     kappa = target_offset_sigmas(n_classes, selectivity)
-    bias[target] += round(kappa * sigma) + 0.5
-    return ((wi.to(torch.float64) * WEIGHT_SCALE).to(torch.bfloat16), (bias * WEIGHT_SCALE).to(torch.float32),
-            {"kappa": kappa, "sigma": sigma * WEIGHT_SCALE, "scale": WEIGHT_SCALE})
+    if weights == "grid":
+        wi = torch.round(W / WEIGHT_SCALE)
+        bias = torch.floor(-127.5 * wi.sum(dim=1))
+        bias[target] += round(kappa * sigma / WEIGHT_SCALE) + 0.5
+        bias = bias * WEIGHT_SCALE
+    else:
+        bias = -127.5 * W.sum(dim=1)
+        bias[target] += kappa * sigma
+    return W.to(torch.bfloat16), bias.to(torch.float32), {"kappa": kappa, "sigma": sigma, "weights": weights}
 
 
 def make_mlp_head(seed: int, hidden: int, n_classes: int, target: int, selectivity: float,
-                  k_features: int = K_FEATURES):
-    """Two-layer head (R25): W1 = s*{-2..2} [hidden][K], b1 = -s*floor(127.5*rowsum)
-    (centres every hidden pre-activation), W2 = s*{-2..2} [C][hidden], b2 centring the logits on
-    the half-normal mean of the hidden units plus the target offset kappa*sigma_z (s = 2^-8).
-
-    With integer (nearest-crop) inputs every hidden pre-activation is s * integer, exact in fp32,
-    so its bf16 rounding is the same for any accumulation order.  Only the logits' f32 sums differ
-    from float64 (tolerance 1e-2).  These are draws, not method arithmetic.
+                  k_features: int = K_FEATURES, weights: str = "grid"):
+    """Two-layer head (R25): W1 [hidden][K], b1 = -127.5 * rowsum(W1) (floored to the s
+    grid for "grid") centres every hidden pre-activation; W2 [C][hidden]; b2 centres the logits on
+    the half-normal mean of the hidden units plus the target offset kappa * sigma_z.
+    "grid": W1, W2 = s * {-2..2} (s = 2^-8): with integer (nearest-crop) inputs every hidden
+    pre-activation is s * integer, exact in fp32.  "bf16": W1 = bf16(N(0, 2.5e-4^2)),
+    W2 = bf16(N(0, 0.03^2)).  These are draws, not method arithmetic.
     """
-    h = torch.arange(hidden, dtype=torch.int64)[:, None]
-    k = torch.arange(k_features, dtype=torch.int64)[None, :]
-    w1 = gen_u32(seed, S_W1, h * k_features + k) % 5 - 2
-    b1 = torch.floor(-127.5 * w1.sum(dim=1).to(torch.float64))
-    sigma1 = math.sqrt(_PIX_VAR * float((w1 * w1).sum(dim=1).to(torch.float64).mean())) * WEIGHT_SCALE
-    c = torch.arange(n_classes, dtype=torch.int64)[:, None]
-    hh = torch.arange(hidden, dtype=torch.int64)[None, :]
-    w2 = gen_u32(seed, S_W2, c * hidden + hh) % 5 - 2
-    w2f = w2.to(torch.float64) * WEIGHT_SCALE
+    W1 = _draw_weights(seed, S_W1, hidden, k_features, weights, BF16_SIGMA)
+    if weights == "grid":
+        b1 = torch.floor(-127.5 * torch.round(W1 / WEIGHT_SCALE).sum(dim=1)) * WEIGHT_SCALE
+    else:
+        b1 = -127.5 * W1.sum(dim=1)
+    sigma1 = math.sqrt(_PIX_VAR * float((W1 * W1).sum(dim=1).mean()))
+    # W2 scale for "bf16": a hidden unit whose fp32 pre-activation lands on the other side of a bf16
+    # rounding boundary than the f64 one moves a logit by |W2| * ulp_bf16(h) ~ 0.03 * 2^-7 (R25)
+    w2f = _draw_weights(seed, S_W2, n_classes, hidden, weights, BF16_W2_SIGMA)
     mean_h = sigma1 / math.sqrt(2.0 * math.pi)            # E[relu(N(0, sigma1))]
     var_h = sigma1 ** 2 * (0.5 - 1.0 / (2.0 * math.pi))   # Var[relu(N(0, sigma1))]
     sigma_z = math.sqrt(var_h * float((w2f * w2f).sum(dim=1).mean()))
     b2 = -mean_h * w2f.sum(dim=1)
     b2[target] += target_offset_sigmas(n_classes, selectivity) * sigma_z
-    return ((w1.to(torch.float64) * WEIGHT_SCALE).to(torch.bfloat16), (b1 * WEIGHT_SCALE).to(torch.float32),
-            w2f.to(torch.bfloat16), b2.to(torch.float32),
-            {"sigma1": sigma1, "sigma_z": sigma_z, "scale": WEIGHT_SCALE})
+    return (W1.to(torch.bfloat16), b1.to(torch.float32), w2f.to(torch.bfloat16), b2.to(torch.float32),
+            {"sigma1": sigma1, "sigma_z": sigma_z, "weights": weights})
 
 
 # ----------------------------------------------------------------------------------------------
@@ -259,27 +289,33 @@ def hash_pred(seed, sel, units=1, sel_after=None, drift_id=None, units_per_area=
 
 
 def linear_pred(seed, n_classes, target, selectivity, crop_mode="nearest", declared_cost=100.0,
-                name=None):
-    w, b, meta = make_linear_head(seed, n_classes, target, selectivity)
+                name=None, weights="grid"):
+    w, b, meta = make_linear_head(seed, n_classes, target, selectivity, weights=weights)
     return dict(kind="linear", weight=w, bias=b, target=target, n_classes=n_classes,
                 crop_mode=crop_mode, declared_cost=declared_cost,
                 declared_selectivity=float(selectivity), name=name or f"linear{n_classes}",
                 calib=meta)
 
 
-def make_color_frames(seed: int, n_frames: int, h: int, w: int, device="cpu", block: int = 16) -> torch.Tensor:
+def make_color_frames(seed: int, n_frames: int, h: int, w: int, device="cpu", block: int = 16,
+                      chunk_frames: int = 8) -> torch.Tensor:
     """Frames of 16x16 blocks, each a palette colour (drawn per block) plus uniform noise in
-    [-8, 8] per channel: crops cover a few blocks, so the HSV heuristic has a dominant colour."""
-    f = torch.arange(n_frames, dtype=torch.int64, device=device)[:, None, None]
+    [-8, 8] per channel: crops cover a few blocks, so the HSV heuristic has a dominant colour.
+    Generated `chunk_frames` frames at a time (the int64 intermediates of a whole 720p pool would
+    not fit in host memory); the values do not depend on the chunking."""
+    out = torch.empty((n_frames, h, w, 3), dtype=torch.uint8, device=device)
+    pal = torch.tensor(PALETTE, dtype=torch.int64, device=device)
     y = torch.arange(h, dtype=torch.int64, device=device)[None, :, None]
     x = torch.arange(w, dtype=torch.int64, device=device)[None, None, :]
-    blk = (f * ((h + block - 1) // block) + y // block) * ((w + block - 1) // block) + x // block
-    pal = torch.tensor(PALETTE, dtype=torch.int64, device=device)
-    base = pal[gen_u32(seed, S_BLOCK, blk) % len(PALETTE)]                      # [F, H, W, 3]
-    pix = (f * h + y) * w + x
     ch = torch.arange(3, dtype=torch.int64, device=device)
-    noise = gen_u32(seed, S_NOISE, pix[..., None] * 3 + ch) % 17 - 8
-    return (base + noise).clamp(0, 255).to(torch.uint8)
+    for a in range(0, n_frames, chunk_frames):
+        f = torch.arange(a, min(a + chunk_frames, n_frames), dtype=torch.int64, device=device)[:, None, None]
+        blk = (f * ((h + block - 1) // block) + y // block) * ((w + block - 1) // block) + x // block
+        base = pal[gen_u32(seed, S_BLOCK, blk) % len(PALETTE)]                      # [F, H, W, 3]
+        pix = (f * h + y) * w + x
+        noise = gen_u32(seed, S_NOISE, pix[..., None] * 3 + ch) % 17 - 8
+        out[a:a + f.shape[0]] = (base + noise).clamp(0, 255).to(torch.uint8)
+    return out
 
 
 def hsv_pred(target: int, selectivity: float, declared_cost=50.0, name=None):
@@ -287,8 +323,8 @@ def hsv_pred(target: int, selectivity: float, declared_cost=50.0, name=None):
                 declared_selectivity=float(selectivity), name=name or f"hsv={target}")
 
 
-def mlp_pred(seed, n_classes, target, selectivity, hidden=512, declared_cost=1000.0, name=None):
-    w1, b1, w2, b2, meta = make_mlp_head(seed, hidden, n_classes, target, selectivity)
+def mlp_pred(seed, n_classes, target, selectivity, hidden=512, declared_cost=1000.0, name=None, weights="grid"):
+    w1, b1, w2, b2, meta = make_mlp_head(seed, hidden, n_classes, target, selectivity, weights=weights)
     return dict(kind="mlp", weight=w1, bias=b1, weight2=w2, bias2=b2, hidden=hidden, target=target,
                 n_classes=n_classes, crop_mode="nearest", declared_cost=declared_cost,
                 declared_selectivity=float(selectivity), name=name or f"mlp{hidden}x{n_classes}", calib=meta)
@@ -310,11 +346,40 @@ class Workload:
     warmup_tuples: int = 65536
     notes: str = ""
     frame_kind: str = "noise"  # "noise" (uniform u8) or "color" (palette blocks, make_color_frames)
+    weights: str = "grid"      # classifier weights: "grid" (fp16-exact) or "bf16" (general bf16)
+    small: bool = False
+    # bbox redraw table (R12 margin guarantee): sorted ids and their retry counters
+    redraw: Optional[tuple] = None
+
+    @property
+    def key(self) -> str:
+        """Name of the workload's oracle cache / redraw table (tests/golden/cache/<key>.npz)."""
+        return f"{self.name}-{self.weights}{'-small' if self.small else ''}-g{GEN_VERSION}"
+
+    def retry_for(self, id_start: int, n: int) -> Optional[torch.Tensor]:
+        if self.redraw is None or n == 0:
+            return None
+        ids, retry = self.redraw
+        a, b = np.searchsorted(ids, [id_start, id_start + n])
+        if a == b:
+            return None
+        out = torch.zeros(n, dtype=torch.int64)
+        out[torch.from_numpy(ids[a:b] - id_start)] = torch.from_numpy(retry[a:b].astype(np.int64))
+        return out
 
     def tuples(self, id_start=0, n=None, device="cpu") -> Tuples:
-        return make_tuples(self.seed, id_start, self.n if n is None else n, n_frames=self.n_frames,
+        n = self.n if n is None else n
+        return make_tuples(self.seed, id_start, n, n_frames=self.n_frames,
                            frame_h=self.frame_h, frame_w=self.frame_w, w_min=self.w_min,
-                           n_octaves=self.n_octaves, device=device)
+                           n_octaves=self.n_octaves, device=device, retry=self.retry_for(id_start, n))
+
+    def tuples_at(self, ids: np.ndarray, device="cpu") -> Tuples:
+        """The tuples with the given (sorted, unique) ids, e.g. the 1 % sample id % 100 == 0."""
+        ids = np.asarray(ids, dtype=np.int64)
+        if len(ids) == 0:
+            return self.tuples(0, 0, device)
+        full = self.tuples(int(ids[0]), int(ids[-1]) - int(ids[0]) + 1, device="cpu")
+        return full.select(torch.from_numpy(ids - ids[0])).to(device)
 
     def frames(self, device="cpu", frame_ids=None) -> torch.Tensor:
         if self.frame_kind == "color":
@@ -329,11 +394,34 @@ class Workload:
 
 
 SEED = 20240321
+CACHE_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "cache")
 
 
-def workload(name: str, *, n: Optional[int] = None, small: bool = False) -> Workload:
-    """BASELINE.json configs (cfg1..cfg5).  ``small`` shrinks frames for oracle-speed tests."""
+def load_redraw(key: str):
+    """The bbox redraw table of a workload (written by tests/oracle_cache.py, which calls only
+    oracle/), or None when there is none."""
+    path = os.path.join(CACHE_DIR, key + ".npz")
+    if not os.path.exists(path):
+        return None
+    with np.load(path) as z:
+        return z["redraw_ids"].astype(np.int64), z["redraw_retry"].astype(np.int64)
+
+
+def workload(name: str, *, n: Optional[int] = None, small: bool = False, weights: str = "grid",
+             redraw: bool = True) -> Workload:
+    """BASELINE.json configs (cfg1..cfg5).  ``small`` shrinks frames for oracle-speed tests;
+    ``weights`` picks the classifier heads' weight draw ("grid" or "bf16"); ``redraw`` applies the
+    workload's committed bbox redraw table (margin guarantee) when one exists."""
+    w = _workload(name, n=n, small=small, weights=weights)
+    w.weights, w.small = weights, small
+    if redraw and any(p["kind"] in ("linear", "mlp") for p in w.preds):
+        w.redraw = load_redraw(w.key)
+    return w
+
+
+def _workload(name: str, *, n: Optional[int], small: bool, weights: str) -> Workload:
     fh, fw, nf, wmin = (720, 1280, 1024, 32) if not small else (96, 128, 16, 8)
+    W = weights
     if name == "cfg1":
         preds = [hash_pred(1, 0.5, units=1, name="A"), hash_pred(2, 0.1, units=10, name="B")]
         return Workload("cfg1", SEED, n or 10_000, 4, 96, 128, preds, policy="static", w_min=8,
@@ -341,8 +429,8 @@ def workload(name: str, *, n: Optional[int] = None, small: bool = False) -> Work
                         notes="2 hash predicates sel 0.5/0.1 cost 1/10, static stats, one batch")
     if name == "cfg2":
         preds = [label_pred(),
-                 linear_pred(SEED + 1, 120, 57, 0.254, name="breed=great dane"),
-                 linear_pred(SEED + 2, 10, 1, 0.633, name="colour=black")]
+                 linear_pred(SEED + 1, 120, 57, 0.254, name="breed=great dane", weights=W),
+                 linear_pred(SEED + 2, 10, 1, 0.633, name="colour=black", weights=W)]
         return Workload("cfg2", SEED, n or 1_000_000, nf, fh, fw, preds, w_min=wmin,
                         batch_tuples=1 << 20,
                         notes="dog query: label='dog' AND breed AND colour, linear heads, 64x64 nearest crops")
@@ -357,20 +445,20 @@ def workload(name: str, *, n: Optional[int] = None, small: bool = False) -> Work
     if name == "cfg4":
         preds = [label_pred(),
                  hash_pred(21, 0.5, units=1, units_per_area=4096, name="hash(area)"),
-                 linear_pred(SEED + 2, 10, 1, 0.633, name="colour=black"),
-                 linear_pred(SEED + 1, 120, 57, 0.254, crop_mode="area", name="breed=great dane (area)")]
+                 linear_pred(SEED + 2, 10, 1, 0.633, name="colour=black", weights=W),
+                 linear_pred(SEED + 1, 120, 57, 0.254, crop_mode="area", name="breed=great dane (area)", weights=W)]
         return Workload("cfg4", SEED, n or 10_000_000, nf, fh, fw, preds, w_min=wmin,
                         batch_tuples=1 << 20,
                         notes="area-correlated classifier cost, 4 predicates")
     if name == "mlp":  # the dog query with the breed classifier as an MLP head
         preds = [label_pred(),
-                 mlp_pred(SEED + 3, 120, 57, 0.254, name="breed=great dane (mlp)"),
-                 linear_pred(SEED + 2, 10, 1, 0.633, name="colour=black")]
+                 mlp_pred(SEED + 3, 120, 57, 0.254, name="breed=great dane (mlp)", weights=W),
+                 linear_pred(SEED + 2, 10, 1, 0.633, name="colour=black", weights=W)]
         return Workload("mlp", SEED, n or 1_000_000, nf, fh, fw, preds, w_min=wmin,
                         notes="cfg2 with a 12288-512-120 MLP breed head")
     if name == "hsv":  # the dog query with DogColorClassifier as the HSV heuristic
         preds = [label_pred(),
-                 linear_pred(SEED + 1, 120, 57, 0.254, name="breed=great dane"),
+                 linear_pred(SEED + 1, 120, 57, 0.254, name="breed=great dane", weights=W),
                  hsv_pred(1, 0.1, name="colour=black (hsv)")]
         return Workload("hsv", SEED, n or 1_000_000, nf, fh, fw, preds, w_min=wmin, frame_kind="color",
                         notes="cfg2 with the HSV colour heuristic on a coloured-block frame pool")
@@ -381,7 +469,7 @@ def workload(name: str, *, n: Optional[int] = None, small: bool = False) -> Work
                         batch_tuples=1000, warmup_tuples=0,
                         notes="verdicts cached for ids in (1000, 7000) (predicate 0) and (8000, 14000) (predicate 1)")
     if name == "cfg5":
-        w = workload("cfg2", n=n or 100_000_000, small=small)
+        w = _workload("cfg2", n=n or 100_000_000, small=small, weights=weights)
         w.name = "cfg5"
         w.notes = "cfg2 query, 100M tuples sharded over ranks"
         return w

@@ -1,10 +1,13 @@
 """N > 1 host logic on CPU: world size 2 over gloo (127.0.0.1).
 
 Each rank takes its contiguous shard (paper_2403_14902_b200.dist), evaluates it with the oracle under
-a common order, all-reduces the per-predicate deltas exactly like libhydro's ncclAllReduce of the
-pending statistics, folds them, and must (a) hold the same order as the other rank, (b) hold the
-statistics of a single-process run over all shards, and (c) together with the other rank reproduce
-the 1-process result rows in input order.
+the current order and follows libhydro's exchange schedule (hydro.h sync_every: every sync_every
+batches the window of deltas is all-reduced -- here over gloo, as libhydro's HOST transport does --
+and the window of the previous sync point is folded), and must (a) hold the same order as the other
+rank at every batch, (b) match the single-process replay of the schedule over both shards
+(tests/eddy_replay.py) batch for batch, and (c) together with the other rank reproduce the
+1-process result rows in input order.  The same schedule runs inside libhydro with two contexts in
+tests/test_gpu_parity.py::test_two_rank_libhydro_host_transport.
 """
 import os
 import socket
@@ -20,7 +23,7 @@ from paper_2403_14902_b200.dist import broadcast_unique_id, max_over_ranks, shar
 from synth import workload
 
 N_PER_RANK = 3000
-STEPS = 3
+STEPS = 5
 
 
 def _free_port():
@@ -31,26 +34,39 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, sync_every, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         w = workload("cfg2", small=True)
         frames = w.frames().numpy()
         uid = broadcast_unique_id(dist, rank, lambda: bytes(range(128)))
-        fold = O.FoldState(len(w.preds), 0.5, [p["declared_cost"] for p in w.preds], cost_source="declared")
+        P = len(w.preds)
+        fold = O.FoldState(P, 0.5, [p["declared_cost"] for p in w.preds], cost_source="declared")
         orders, ids = [], []
+        window, since, outstanding = np.zeros(2 * P, np.int64), 0, None
         for s in range(STEPS):
             a, b = shard_ids(N_PER_RANK, rank, world, s)
             t = w.tuples(id_start=a, n=b - a)
             V = O.evaluate_all(w.preds, t, frames)
             order = fold.order("score")
             n_in, n_pass, keep = O.sequential_eval(V, order)
-            d = sum_over_ranks(list(n_in) + list(n_pass), dist)
-            P = len(w.preds)
-            fold.fold(d[:P], d[P:], [0] * P)
+            window += np.concatenate([n_in, n_pass])
+            since += 1
+            if since == sync_every:  # snapshot + exchange this window, fold the previous one
+                d = np.array(sum_over_ranks(window.tolist(), dist), np.int64)
+                window[:] = 0
+                since = 0
+                if outstanding is not None:
+                    fold.fold(outstanding[:P], outstanding[P:], [0] * P)
+                outstanding = d
             orders.append(order)
             ids.append(t.id.numpy()[keep])
+        # flush: fold the outstanding window, then exchange and fold the rest
+        if outstanding is not None:
+            fold.fold(outstanding[:P], outstanding[P:], [0] * P)
+        d = np.array(sum_over_ranks(window.tolist(), dist), np.int64)
+        fold.fold(d[:P], d[P:], [0] * P)
         gathered = [None] * world
         dist.all_gather_object(gathered, [x.tolist() for x in ids])
         tmax = max_over_ranks(float(rank + 1), dist)
@@ -59,32 +75,37 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_two_rank_shards_merge_to_the_single_process_result():
+@pytest.mark.parametrize("sync_every", [1, 2])
+def test_two_rank_shards_merge_to_the_single_process_result(sync_every):
+    from tests.eddy_replay import replay
+
     world = 2
     port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, sync_every, out), nprocs=world, join=True)
     r0, r1 = out[0], out[1]
     assert r0["uid"] == r1["uid"] == bytes(range(128))
     assert r0["orders"] == r1["orders"] and r0["sel"] == r1["sel"]
     assert r0["tmax"] == r1["tmax"] == 2.0
-    # single process over the same ids, in global order
+    # single process over the same ids: the schedule's replay, and the rows in global order
     w = workload("cfg2", small=True)
     frames = w.frames().numpy()
-    fold = O.FoldState(len(w.preds), 0.5, [p["declared_cost"] for p in w.preds], cost_source="declared")
+    Vr = [[], []]
     rows = []
     for s in range(STEPS):
+        for r in range(world):
+            a, b = shard_ids(N_PER_RANK, r, world, s)
+            Vr[r].append(O.evaluate_all(w.preds, w.tuples(id_start=a, n=b - a), frames))
         a, _ = shard_ids(N_PER_RANK, 0, world, s)
         _, b = shard_ids(N_PER_RANK, world - 1, world, s)
         t = w.tuples(id_start=a, n=b - a)
-        V = O.evaluate_all(w.preds, t, frames)
-        order = fold.order("score")
-        assert order == r0["orders"][s]
-        n_in, n_pass, keep = O.sequential_eval(V, order)
-        fold.fold(n_in, n_pass, [0] * len(w.preds))
+        _, _, keep = O.query_result(t, O.evaluate_all(w.preds, t, frames))
         rows.append(t.id.numpy()[keep])
-    assert fold.sel() == pytest.approx(r0["sel"], rel=1e-12)
+    rep = replay([np.concatenate(v, axis=1) for v in Vr], N_PER_RANK, 0, [p["declared_cost"] for p in w.preds],
+                 sync_every=sync_every, exchange=True)
+    assert rep["orders"] == r0["orders"]
+    assert rep["fold"].sel() == pytest.approx(r0["sel"], rel=1e-12)
     merged = [i for s in range(STEPS) for r in range(world) for i in r0["rows"][r][s]]
     assert merged == np.concatenate(rows).tolist()
 

@@ -186,16 +186,43 @@ def test_argmax_lowest_index_on_ties_and_margin():
 
 
 def test_generator_makes_half_integer_target_margins():
-    """R12: logits are multiples of s/2 (s = 2^-8) with the target at an odd multiple -> |margin| >= s/2."""
+    """R12 ("grid" heads): logits are multiples of s/2 (s = 2^-8) with the target at an odd multiple, so
+    |margin| >= s/2 and fp32 accumulation is exact; and the workload's committed redraw table makes
+    every margin of the covered tuples >= 0.05 (tests/oracle_cache.py)."""
+    from synth.workload import WEIGHT_SCALE
+
     w = workload("cfg2", small=True)
+    assert w.redraw is not None
     F = w.frames().numpy()
     t = w.tuples(n=300)
     tup = O.as_numpy_tuples(t)
     for p in w.preds[1:]:
         _, z = O.linear_verdict(p, F, tup["frame_id"], tup["bbox"], return_logits=True)
-        m = O.margin(z, p["target"]) / p["calib"]["scale"]
-        assert np.all(np.abs(m) >= 0.5) and np.all(np.abs(z / p["calib"]["scale"]) < 2 ** 22)
-        assert np.all(np.mod(z[:, p["target"]] / p["calib"]["scale"], 1.0) == 0.5)
+        m = O.margin(z, p["target"]) / WEIGHT_SCALE
+        assert np.all(np.abs(m) >= 0.5) and np.all(np.abs(z / WEIGHT_SCALE) < 2 ** 22)
+        assert np.all(np.mod(z[:, p["target"]] / WEIGHT_SCALE, 1.0) == 0.5)
+        assert np.abs(O.margin(z, p["target"])).min() >= 0.05
+
+
+def test_bf16_heads_redraw_table_guarantees_margins():
+    """General bf16 heads (Q17): many weights are not fp16-representable, and with the committed redraw
+    table every margin of the covered small-workload tuples is >= 0.05 (re-checked here with the
+    oracle); redrawn tuples draw new bboxes, all other tuples are the plain generator's."""
+    w = workload("cfg2", small=True, weights="bf16")
+    plain = workload("cfg2", small=True, weights="bf16", redraw=False)
+    ids, retry = w.redraw
+    assert len(ids) > 0 and retry.min() >= 1
+    F = w.frames().numpy()
+    n = 2000
+    t, t0 = w.tuples(n=n), plain.tuples(n=n)
+    moved = ~(t.bbox == t0.bbox).all(dim=1).numpy()
+    assert np.array_equal(np.where(moved)[0], ids[ids < n])
+    tup = O.as_numpy_tuples(t)
+    for p in w.preds[1:]:
+        wf = p["weight"].float()
+        assert (wf != wf.half().float()).float().mean() > 0.005
+        _, z = O.linear_verdict(p, F, tup["frame_id"], tup["bbox"], return_logits=True)
+        assert np.abs(O.margin(z, p["target"])).min() >= 0.05
 
 
 # ----------------------------------------------------------------------------- MLP head (R25)
