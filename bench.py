@@ -387,7 +387,7 @@ def run_gpu(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         fr_host = frames.cpu().numpy()
-        tc = batches[0].slice(0, 200_000).to("cpu")
+        tc = batches[0].to("cpu")
         r = cpu_oracle_rate(w, tc, fr_host, seconds=args.cpu_seconds)
         cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
                "nproc": r["nproc"], "cpu_model": r["cpu_model"],

@@ -155,6 +155,27 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
+// 16-byte cp.async at [dst + kOff] <- [src + kOff] when p (no branch; the offset is an immediate)
+template <int kOff>
+__device__ __forceinline__ void cp_async16_if(uint32_t dst, const void* src, bool p) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q cp.async.cg.shared.global [%0+%3], [%1+%3], 16;\n}" ::"r"(dst),
+      "l"(src), "r"(static_cast<int>(p)), "n"(kOff)
+      : "memory");
+}
+// one crop-row segment of nch 16-byte chunks: lane j copies chunks j + 8c (c < 7)
+__device__ __forceinline__ void stage_segment(uint32_t dst, const uint8_t* row, uint32_t j, uint32_t nch) {
+  const uint32_t d = dst + 16u * j;
+  const uint8_t* s = row + 16u * j;
+  const int rem = static_cast<int>(nch) - static_cast<int>(j);
+  cp_async16_if<0>(d, s, rem > 0);
+  cp_async16_if<128>(d, s, rem > 8);
+  cp_async16_if<256>(d, s, rem > 16);
+  cp_async16_if<384>(d, s, rem > 24);
+  cp_async16_if<512>(d, s, rem > 32);
+  cp_async16_if<640>(d, s, rem > 40);
+  cp_async16_if<768>(d, s, rem > 48);
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -186,10 +207,10 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-#ifdef HYDRO_SLEEPWAIT
-#define HYDRO_PIPE_WAIT mbar_wait_sleep  // producer/MMA waits suspend instead of spinning
-#else
+#ifdef HYDRO_SPINWAIT
 #define HYDRO_PIPE_WAIT mbar_wait
+#else
+#define HYDRO_PIPE_WAIT mbar_wait_backoff<64>  // producer / MMA waits poll with a short sleep
 #endif
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -430,10 +451,7 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
       const uint8_t* row = frames + (off + (((2u * g + 1u) * h) >> 7) * row_pitch);
       const uint32_t dst = slots + slot * kQuadSlotBytes + r * kSegPitch;
       if (!kWide || len != 0xFFFFFFFFu) {
-        const uint32_t nch = len >> 4;
-#pragma unroll
-        for (int c = 0; c < 7; ++c)
-          if (j + 8u * c < nch) cp_async16(dst + 16u * j + 128u * c, row + 16u * j + 128u * c);
+        stage_segment(dst, row, j, len >> 4);
       } else {  // wide crop (rare): gather this lane's 8 sampled pixels
         stage_wide_row(dst, row, xw, j);
       }
@@ -539,10 +557,7 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
       if (c.i < hb) {
         const uint8_t* row = frames + (off + (ys + c.i) * row_pitch);
         const uint32_t dst = slots + slot * kQuadSlotBytes + r * kSegPitch;
-        const uint32_t nch = len >> 4;
-#pragma unroll
-        for (int cc = 0; cc < 7; ++cc)
-          if (j + 8u * cc < nch) cp_async16(dst + 16u * j + 128u * cc, row + 16u * j + 128u * cc);
+        stage_segment(dst, row, j, len >> 4);
       }
     }
     cp_async_commit();  // one group per item (possibly empty): uniform wait_group counting
@@ -878,7 +893,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       uint32_t itb = 0, gg = 0, tl = 0;
       for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
         const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
-        mbar_wait_sleep(&ctrl->tempty[acc], aph ^ 1u);
+        mbar_wait_backoff<256>(&ctrl->tempty[acc], aph ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * static_cast<uint32_t>(n_alloc);
         for (int g = 0; g < kGroups; ++g, ++gg) {
@@ -926,7 +941,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
       const uint32_t pos0 = tw.pos0(unit);
       const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
-      mbar_wait_sleep(&ctrl->tfull[acc], aph);
+      mbar_wait_backoff<1024>(&ctrl->tfull[acc], aph);
       tc_fence_after();
       const int m = q * 32 + lane;
       const uint32_t pos = pos0 + m;

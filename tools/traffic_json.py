@@ -32,7 +32,7 @@ def main(path, kernel):
         v = float(d["Metric Value"].replace(",", ""))
         unit = d.get("Metric Unit", "")
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                 "msecond": 1e-3, "second": 1}.get(unit, 1)
+                 "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}.get(unit, 1)
         launches.setdefault(key, {})[d["Metric Name"]] = v * scale
     work = [l for l in launches.values()
             if l.get("dram__bytes_read.sum", 0) + l.get("dram__bytes_write.sum", 0) > 1e6]
