@@ -13,6 +13,7 @@ import torch
 
 import oracle as O
 from synth import Tuples, hash_pred, make_frames, make_tuples, workload
+from synth.workload import WEIGHT_SCALE
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_pins.json")))
 
@@ -282,7 +283,8 @@ def test_mlp_matches_torch_bf16_pipeline_on_generated_head():
     ref = h @ p["weight2"].double().T + p["bias2"].double()
     assert torch.allclose(torch.from_numpy(O.mlp_logits(p, x)), ref, rtol=0, atol=1e-9)
     # every hidden pre-activation of the generated head is s * integer (exact in fp32, R25)
-    assert torch.all(torch.frac(a / p["calib"]["scale"]) == 0)
+    assert p["calib"]["weights"] == "grid"
+    assert torch.all(torch.frac(a / WEIGHT_SCALE) == 0)
 
 
 def test_mlp_all_negative_hidden_gives_bias_and_generated_selectivity():
