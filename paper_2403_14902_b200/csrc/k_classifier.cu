@@ -941,7 +941,13 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
       const uint32_t pos0 = tw.pos0(unit);
       const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
+#ifdef HYDRO_EPI_ONEPOLL
+      // one warp polls the accumulator barrier; the other three sleep in a named barrier
+      if (q == 0) mbar_wait_backoff<1024>(&ctrl->tfull[acc], aph);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+#else
       mbar_wait_backoff<1024>(&ctrl->tfull[acc], aph);
+#endif
       tc_fence_after();
       const int m = q * 32 + lane;
       const uint32_t pos = pos0 + m;
@@ -1295,6 +1301,10 @@ cudaError_t hydro_classifier_configure() {
                              hydro_mlp_kernel<false>, hydro_mlp_kernel<true>};
   for (auto k : ks) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes);
+    if (e != cudaSuccess) return e;
+  }
+  if (const char* g = getenv("HYDRO_L2_FETCH")) {  // experiment hook: L2 fetch granularity (bytes)
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(atoi(g)));
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
