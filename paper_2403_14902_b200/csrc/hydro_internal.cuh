@@ -68,6 +68,19 @@ __host__ __device__ __forceinline__ uint32_t crop_pos_feature(uint32_t g, uint32
   return (g * 64u + j + 8u * (rem / 3u)) * 3u + rem % 3u;
 }
 
+// K order of K4-T (hydro_classifier_tm_kernel, A in tensor memory): position
+// p = 2c + e of a crop row is element e of TMEM column c.  Converter thread t0 = t % 4 of a tuple
+// writes columns 8i + 2*t0 + sub (tcgen05.st 16x256b repetition i = 0..11, sub = 0, 1), holding its
+// per-row features f = 4*(i % 6) + 2*sub + e of half hh = i / 6: pixel k = 8*hh + f / 3 (output
+// pixel dx = 4k + t0), channel f % 3.
+__host__ __device__ __forceinline__ uint32_t crop_pos_feature_tm(uint32_t g, uint32_t p) {
+  const uint32_t c = p >> 1, e = p & 1u;
+  const uint32_t i = c >> 3, t0 = (c >> 1) & 3u, sub = c & 1u;
+  const uint32_t f = 4u * (i % 6u) + 2u * sub + e;
+  const uint32_t k = 8u * (i / 6u) + f / 3u;
+  return (g * 64u + 4u * k + t0) * 3u + f % 3u;
+}
+
 enum PredKind : int32_t {
   kLabelEq = HYDRO_PRED_LABEL_EQ,
   kHash = HYDRO_PRED_HASH,
@@ -86,6 +99,7 @@ struct PredDev {
   uint64_t drift_id;
   int32_t units, units_per_area;
   const uint8_t* w_tiled;   // LINEAR: [192 kblk][n_pad rows][128 B SW128-swizzled]
+  const uint8_t* w_tiled_tm;  // LINEAR (nearest): the same in K4-T's K order (crop_pos_feature_tm)
   const float* bias;        // [n_pad] (padding rows: -inf never wins; they are skipped anyway)
   int32_t n_classes, n_pad, target, crop_mode;
   int32_t a_fp16;           // 1: operands staged as fp16 (weights exactly representable), 0: bf16
@@ -451,6 +465,7 @@ void hydro_classifier_launch(const hydro::ClsParams& c, int grid, cudaStream_t s
 // K6 data-aware balance: per-chunk input-size estimates, then the bounds
 void hydro_balance_launch(const hydro::ClsParams& c, uint64_t max_positions, int num_sms, cudaStream_t stream);
 void hydro_mlp_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug);
+void hydro_classifier_tm_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug);
 void hydro_hsv_launch(const hydro::ClsParams& c, uint64_t max_positions, int num_sms, cudaStream_t stream);
 int hydro_hsv_warps_per_sm();
 __global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode, uint32_t n_batch,

@@ -941,13 +941,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
       const uint32_t pos0 = tw.pos0(unit);
       const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
-#ifdef HYDRO_EPI_ONEPOLL
-      // one warp polls the accumulator barrier; the other three sleep in a named barrier
-      if (q == 0) mbar_wait_backoff<1024>(&ctrl->tfull[acc], aph);
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-#else
       mbar_wait_backoff<1024>(&ctrl->tfull[acc], aph);
-#endif
       tc_fence_after();
       const int m = q * 32 + lane;
       const uint32_t pos = pos0 + m;
@@ -1294,17 +1288,439 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
   if (tid == 0) ktimer_end(st, 4);
 }
 
+// ------------------------------------------------------------------------------------------
+// K4-T `hydro_classifier_tm_kernel` (nearest crops): the same warp roles and weight
+// stream as hydro_classifier_kernel, but the A operand lives in TENSOR MEMORY.  Converter warps
+// write their crop pixels with tcgen05.st (16x256b: thread t owns TMEM lanes t/4 and t/4 + 8 of
+// its 16-row band, 2 columns per 8-column repetition) into a 2-group TMEM ring (columns
+// [kTmAcol0, kTmAcol0 + 2 * 96)); the MMA reads A from TMEM (tcgen05.mma ... [d], [a], b_desc),
+// so neither the A stores nor the tensor core's A reads touch shared memory, and the 96 KB the
+// shared-memory A ring took become crop-row staging: each converter warp owns a 22 KB ring of
+// "units" (one crop row of its 16 tuples, segments packed back to back) and stages up to 3 units
+// ahead instead of 2 quads.
+// Converter warp cu owns tile rows [32*((6+cu)%4) + 16*(cu/4), +16) (the TMEM lane quarter of
+// warp 6+cu).  Thread t handles local tuples a = t/4 and a + 8, output pixels dx = 4k + (t%4)
+// (k = 0..15) of every crop row; K order inside a crop row = crop_pos_feature_tm.
+constexpr int kTmAcol0 = 256;      // first TMEM column of the A ring (accumulators: 2 x <= 128 columns)
+constexpr int kTmGroupCols = 96;   // one crop row of A: 192 fp16 = 96 32-bit columns per lane
+constexpr int kTmMaxSlots = 4;     // staging units per converter warp (depth <= 3)
+constexpr int kTmBStages = 3;
+struct TmCtrl {
+  uint64_t full_a[2], empty_a[2];
+  uint64_t full_b[kTmBStages], empty_b[kTmBStages];
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem_base;
+  uint32_t pad;
+  float bias[HYDRO_MAX_CLASSES];
+};
+constexpr int kTmBRingBytes = kTmBStages * 16384;
+constexpr int kTmCtrlBytes = (static_cast<int>(sizeof(TmCtrl)) + 127) & ~127;
+// per-warp staging ring (16-byte multiple) + 64 B of slack at the end of the region (reads of the
+// word after a pixel, and of stale offsets in invalid rows, stay inside the allocation)
+constexpr int kTmWarpStage = ((kClsSmemBytes - 1023 - kTmBRingBytes - kTmCtrlBytes - 64) / kConvWarps) & ~15;
+static_assert(kTmWarpStage >= 16 * 784, "one unit of 16 worst-case segments must fit a converter ring");
+
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_st_16x256b_x4(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tc_st_16x256b_x2(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
+// 8 staged pixels (byte offsets packed 2 per word, relative to `unit`) -> 12 words of fp16x2 (or
+// bf16x2) in feature order f = 3 * pixel + ch
+template <bool kFp16>
+__device__ __forceinline__ void tm_convert8(uint32_t unit, const uint32_t (&po)[4], uint32_t (&e)[12], uint32_t (&px)[8]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const uint32_t o = h2 ? (po[q] >> 16) : (po[q] & 0xFFFFu);
+      const uint32_t a = unit + (o & ~3u);
+      px[2 * q + h2] = __funnelshift_r(lds32(a), lds32(a + 4), o << 3);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t p0 = px[2 * q], p1 = px[2 * q + 1];
+    if (kFp16) {
+      const uint32_t K = 0x64646464u;  // fp16 0x64vv == 1024 + v exactly
+      e[3 * q + 0] = f16x2_sub(__byte_perm(p0, K, 0x4140), 0x64006400u);
+      e[3 * q + 1] = f16x2_sub(__byte_perm(__byte_perm(p0, p1, 0x0042), K, 0x4140), 0x64006400u);
+      e[3 * q + 2] = f16x2_sub(__byte_perm(p1, K, 0x4241), 0x64006400u);
+    } else {
+      e[3 * q + 0] = bf16x2_of_bytes(p0 & 0xFF, (p0 >> 8) & 0xFF);
+      e[3 * q + 1] = bf16x2_of_bytes((p0 >> 16) & 0xFF, p1 & 0xFF);
+      e[3 * q + 2] = bf16x2_of_bytes((p1 >> 8) & 0xFF, (p1 >> 16) & 0xFF);
+    }
+  }
+}
+
+__device__ __forceinline__ void tm_wait_depth(uint32_t d) {
+  // cp.async.wait_group needs an immediate: the runtime depth of this tile picks the case
+  if (d >= 3) cp_async_wait<3>();
+  else if (d == 2) cp_async_wait<2>();
+  else if (d == 1) cp_async_wait<1>();
+  else cp_async_wait<0>();
+}
+
+template <bool kDbg, bool kWide>
+__device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl, uint32_t lim, uint32_t pos0, int cu,
+                                                int lane, uint32_t ring, uint32_t tmem_base, uint32_t row_pitch,
+                                                bool fp16, const RowMeta& mm, uint32_t band, uint32_t& gg) {
+  const uint8_t* frames = p.frames;
+  const int a = lane >> 2, t0 = lane & 3;
+  // unit layout: the segments of local tuples 0..15 back to back (lane l < 16 holds tuple l)
+  const bool my_wide = kWide && lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes);
+  const uint32_t slen = (lane < 16 && mm.valid) ? (my_wide ? 512u : mm.seg_len) : 0u;
+  uint32_t incl = slen;
+#pragma unroll
+  for (int d = 1; d < 16; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  const uint32_t soff = incl - slen;
+  const uint32_t ubytes = max(__shfl_sync(0xFFFFFFFFu, incl, 15), 16u);
+  const uint32_t nslot = min(static_cast<uint32_t>(kTmMaxSlots), static_cast<uint32_t>(kTmWarpStage) / ubytes);
+  const uint32_t depth = nslot - 1u;
+  // this thread's pixel offsets inside a unit: tuples a (tt = 0) and a + 8 (tt = 1), pixels 4k + t0
+  uint32_t po[2][8];
+#pragma unroll
+  for (int tt = 0; tt < 2; ++tt) {
+    const int src = a + 8 * tt;
+    const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src);
+    const uint32_t w = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src);
+    const uint32_t slo = __shfl_sync(0xFFFFFFFFu, mm.seg_lo, src);
+    const uint32_t so = __shfl_sync(0xFFFFFFFFu, soff, src);
+    const bool wide = kWide && __shfl_sync(0xFFFFFFFFu, my_wide, src);
+#pragma unroll
+    for (int k2 = 0; k2 < 8; ++k2) {
+      const uint32_t dx0 = 8u * k2 + t0, dx1 = dx0 + 4u;  // pixels k = 2*k2, 2*k2 + 1
+      const uint32_t b0 = 3u * (x0 + (((2u * dx0 + 1u) * w) >> 7)), b1 = 3u * (x0 + (((2u * dx1 + 1u) * w) >> 7));
+      const uint32_t o0 = so + (wide ? 8u * dx0 + (b0 & 3u) : b0 - slo);
+      const uint32_t o1 = so + (wide ? 8u * dx1 + (b1 & 3u) : b1 - slo);
+      po[tt][k2] = o0 | (o1 << 16);
+    }
+  }
+  // staging: lanes (r = lane/8, j = lane%8) copy segment 4*pass + r in 16-byte chunks j + 8c
+  const int r = lane >> 3, j = lane & 7;
+  const uint32_t my_src = mm.row0 + mm.seg_lo;
+  const uint32_t my_h = static_cast<uint32_t>(mm.h);
+  const uint32_t my_lo = slen | (soff << 16);
+  const uint32_t my_xw =
+      kWide ? static_cast<uint32_t>(mm.x0) | (static_cast<uint32_t>(mm.w) << 16) | (my_wide ? 0x80000000u : 0u) : 0u;
+  auto stage_unit = [&](int g, uint32_t slot) {
+    if (g < kGroups) {
+      const uint32_t dst0 = ring + slot * ubytes;
+#pragma unroll
+      for (int pass = 0; pass < 4; ++pass) {
+        const int L = 4 * pass + r;
+        const uint32_t lo = __shfl_sync(0xFFFFFFFFu, my_lo, L);
+        const uint32_t off = __shfl_sync(0xFFFFFFFFu, my_src, L);
+        const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, L);
+        const uint32_t xw = kWide ? __shfl_sync(0xFFFFFFFFu, my_xw, L) : 0u;
+        const uint32_t len = lo & 0xFFFFu;
+        const uint8_t* row = frames + (off + (((2u * g + 1u) * h) >> 7) * row_pitch);
+        const uint32_t dst = dst0 + (lo >> 16);
+        if (!kWide || !(xw >> 31)) stage_segment(dst, row, j, len >> 4);
+        else stage_wide_row(dst, row, xw & 0x7FFFFFFFu, j);  // wide crop (rare): 64-pixel gather
+      }
+    }
+    cp_async_commit();  // one group per unit (possibly empty) keeps wait_group counting uniform
+  };
+  uint32_t slot_stage = 0, slot_use = 0;
+  for (uint32_t k = 0; k < depth; ++k) {
+    stage_unit(static_cast<int>(k), slot_stage);
+    slot_stage = slot_stage + 1 == nslot ? 0 : slot_stage + 1;
+  }
+  const uint32_t lane_addr = tmem_base + (band << 16) + kTmAcol0;
+  for (int g = 0; g < kGroups; ++g, ++gg) {
+    stage_unit(g + static_cast<int>(depth), slot_stage);
+    slot_stage = slot_stage + 1 == nslot ? 0 : slot_stage + 1;
+    tm_wait_depth(depth);  // this thread's copies of unit g have landed
+    __syncwarp();             // ... and every lane's
+    const uint32_t sa = gg & 1u, aph = (gg >> 1) & 1u;
+    mbar_wait(&ctrl->empty_a[sa], aph ^ 1u);  // the MMA has consumed group gg - 2 from this TMEM slot
+    tc_fence_after();
+    const uint32_t unit = ring + slot_use * ubytes;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      uint32_t ea[12], eb[12], pa[8], pb[8];
+      const uint32_t qa[4] = {po[0][4 * hh], po[0][4 * hh + 1], po[0][4 * hh + 2], po[0][4 * hh + 3]};
+      const uint32_t qb[4] = {po[1][4 * hh], po[1][4 * hh + 1], po[1][4 * hh + 2], po[1][4 * hh + 3]};
+      if (fp16) {
+        tm_convert8<true>(unit, qa, ea, pa);
+        tm_convert8<true>(unit, qb, eb, pb);
+      } else {
+        tm_convert8<false>(unit, qa, ea, pa);
+        tm_convert8<false>(unit, qb, eb, pb);
+      }
+      const uint32_t taddr = lane_addr + sa * kTmGroupCols + 48u * hh;
+      const uint32_t v4[16] = {ea[0], ea[1], eb[0], eb[1], ea[2], ea[3], eb[2], eb[3],
+                               ea[4], ea[5], eb[4], eb[5], ea[6], ea[7], eb[6], eb[7]};
+      const uint32_t v2[8] = {ea[8], ea[9], eb[8], eb[9], ea[10], ea[11], eb[10], eb[11]};
+      tc_st_16x256b_x4(taddr, v4);
+      tc_st_16x256b_x2(taddr + 32u, v2);
+      if (kDbg && p.dbg_crops) {
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          const uint32_t m = band + static_cast<uint32_t>(a + 8 * tt);  // tile row
+          if (pos0 + m < lim) {
+            uint16_t* dbg = p.dbg_crops + static_cast<uint64_t>(pos0 + m) * kFeatures + g * 192;
+            const uint32_t (&px)[8] = tt ? pb : pa;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const uint32_t dx = 4u * (8u * hh + kk) + t0;
+#pragma unroll
+              for (int ch = 0; ch < 3; ++ch)
+                dbg[3 * dx + ch] = static_cast<uint16_t>(bf16_bits_of_byte((px[kk] >> (8 * ch)) & 0xFF));
+            }
+          }
+        }
+      }
+    }
+    slot_use = slot_use + 1 == nslot ? 0 : slot_use + 1;
+    tc_wait_st();  // this thread's TMEM stores have completed
+    tc_fence_before();
+    __syncwarp();  // every lane's stores (and smem reads of the unit) are done
+    if (lane == 0) mbar_arrive(&ctrl->full_a[sa]);
+  }
+  cp_async_wait<0>();
+}
+
+extern __shared__ __align__(1024) uint8_t hydro_tm_smem[];
+
+template <bool kDbg>
+__global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(ClsParams p) {
+  DevState* st = p.st;
+  int pred;
+  const uint32_t* list_in;
+  uint32_t count, base = p.range_base;
+  uint32_t* bits_out;
+  if (p.dispatch) {
+    const int h = st->sched[p.hop];
+    if (h < 0 || h >= st->n_pred) return;
+    pred = st->order[h];
+    if (st->kind[pred] != kLinear) return;
+    if (h == 0) {
+      list_in = p.sel0;
+      count = p.sel0 ? *p.sel0_count : p.range_n;
+    } else {
+      list_in = p.lists + static_cast<uint64_t>(h) * p.list_stride;
+      count = p.counts[h];
+    }
+    bits_out = p.bits + static_cast<uint64_t>(h) * p.bits_stride;
+  } else {
+    pred = p.explicit_pred;
+    list_in = p.list_in;
+    count = list_in ? *p.count_in : p.range_n;
+    bits_out = p.bits_out;
+  }
+  const uint32_t num_tiles = (count + kTileM - 1) / kTileM;
+  const PredDev& pdg = p.preds[pred];
+  TileWalk tw{blockIdx.x, gridDim.x, num_tiles, 0u, count, 1u, 0u, false};
+  if (threadIdx.x == 0) ktimer_begin(st, 1);
+  if (tw.first >= tw.end) {
+    if (threadIdx.x == 0) ktimer_end(st, 1);
+    return;
+  }
+  const long long t_start = clock64();
+  const int n_classes = pdg.n_classes, n_pad = pdg.n_pad, target = pdg.target;
+  const bool fp16 = pdg.a_fp16 != 0;
+  const uint8_t* w_tiled = pdg.w_tiled_tm;
+  const uint32_t n_alloc = n_pad <= 32 ? 32u : (n_pad <= 64 ? 64u : 128u);
+  const uint32_t b_stage_bytes = static_cast<uint32_t>(n_pad) * 128u;
+  const uint32_t row_pitch = static_cast<uint32_t>(p.frame_w * 3);
+
+  // shared memory: [B ring 3 x 16 KB][ctrl][8 converter staging rings]
+  const uint32_t raw = smem_u32(hydro_tm_smem);
+  uint8_t* smem = hydro_tm_smem + (((raw + 1023u) & ~1023u) - raw);
+  const uint32_t b_ring = smem_u32(smem);
+  TmCtrl* ctrl = reinterpret_cast<TmCtrl*>(smem + kTmBRingBytes);
+  const uint32_t stage0 = b_ring + kTmBRingBytes + kTmCtrlBytes;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&ctrl->full_a[s], kConvWarps);
+      mbar_init(&ctrl->empty_a[s], 1);
+      mbar_init(&ctrl->tfull[s], 1);
+      mbar_init(&ctrl->tempty[s], kEpiWarps);
+    }
+    for (int s = 0; s < kTmBStages; ++s) {
+      mbar_init(&ctrl->full_b[s], 1);
+      mbar_init(&ctrl->empty_b[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&ctrl->tmem_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (tid < HYDRO_MAX_CLASSES) ctrl->bias[tid] = tid < n_classes ? pdg.bias[tid] : 0.0f;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = ctrl->tmem_base;
+
+  if (warp == kLoaderWarp) {
+    // ===================== loader: weight K-blocks (1-D bulk copies, L2 evict_last)
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_last();
+      uint32_t itb = 0;
+      for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
+        for (int kb = 0; kb < kNumKBlocks; ++kb, ++itb) {
+          const uint32_t s = itb % kTmBStages, ph = (itb / kTmBStages) & 1u;
+          HYDRO_PIPE_WAIT(&ctrl->empty_b[s], ph ^ 1u);
+          mbar_arrive_expect_tx(&ctrl->full_b[s], b_stage_bytes);
+          bulk_g2s_hint(smem + s * 16384u, w_tiled + static_cast<uint64_t>(kb) * b_stage_bytes, b_stage_bytes,
+                        &ctrl->full_b[s], pol_w);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kMmaWarp) {
+    // ===================== MMA issuer: A from TMEM, B from the shared-memory ring
+    if (lane == 0) {
+      const uint32_t idesc = idesc_f16_f32(kTileM, static_cast<uint32_t>(n_pad), !fp16);
+      uint32_t itb = 0, gg = 0, tl = 0;
+      for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
+        const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
+        mbar_wait_backoff<256>(&ctrl->tempty[acc], aph ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * n_alloc;
+        for (int g = 0; g < kGroups; ++g, ++gg) {
+          const uint32_t sa = gg & 1u;
+          HYDRO_PIPE_WAIT(&ctrl->full_a[sa], (gg >> 1) & 1u);
+          tc_fence_after();
+          const uint32_t a_col = tmem_base + kTmAcol0 + sa * kTmGroupCols;
+#pragma unroll
+          for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr, ++itb) {
+            const uint32_t sb = itb % kTmBStages, bph = (itb / kTmBStages) & 1u;
+            HYDRO_PIPE_WAIT(&ctrl->full_b[sb], bph);
+            tc_fence_after();
+            const uint32_t b_addr = b_ring + sb * 16384u;
+#pragma unroll
+            for (int kk = 0; kk < kKBlock / 16; ++kk)
+              tc_mma_ts(d_tmem, a_col + (kbr * 4 + kk) * 8, desc_sw128(b_addr + kk * 32), idesc,
+                        (g | kbr | kk) != 0 ? 1u : 0u);
+            tc_commit(&ctrl->empty_b[sb]);
+          }
+          tc_commit(&ctrl->empty_a[sa]);
+        }
+        tc_commit(&ctrl->tfull[acc]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kConvWarp0) {
+    // ===================== converters
+    const int cu = warp - kConvWarp0;
+    const uint32_t band = 32u * static_cast<uint32_t>(warp & 3) + 16u * static_cast<uint32_t>(cu >> 2);
+    const uint32_t ring = stage0 + static_cast<uint32_t>(cu) * kTmWarpStage;
+    uint32_t gg = 0;
+    for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
+      const uint32_t pos0 = tw.pos0(unit);
+      const RowMeta mm = load_meta(p, list_in, base, pos0 + band + (lane & 15), lane < 16 ? tw.lim : 0u);
+      const bool any_wide =
+          __any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes));
+      if (any_wide)
+        tm_convert_tile<kDbg, true>(p, ctrl, tw.lim, pos0, cu, lane, ring, tmem_base, row_pitch, fp16, mm, band, gg);
+      else
+        tm_convert_tile<kDbg, false>(p, ctrl, tw.lim, pos0, cu, lane, ring, tmem_base, row_pitch, fp16, mm, band, gg);
+    }
+  } else {
+    // ===================== epilogue warps 0..3 (TMEM lane quadrant = warp)
+    const int q = warp;
+    uint32_t n_in = 0, n_pass = 0, tl = 0;
+    for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
+      const uint32_t pos0 = tw.pos0(unit);
+      const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
+      mbar_wait_backoff<1024>(&ctrl->tfull[acc], aph);
+      tc_fence_after();
+      const int m = q * 32 + lane;
+      const uint32_t pos = pos0 + m;
+      const bool valid = pos < tw.lim;
+      float best = -3.402823466e38f;
+      int bi = 0;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * n_alloc;
+      for (int c0 = 0; c0 < n_pad; c0 += 16) {
+        uint32_t v[16];
+        tc_ld_32x32b_x16(taddr + c0, v);
+        tc_wait_ld();
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int c = c0 + jj;
+          if (c < n_classes) {
+            const float z = __uint_as_float(v[jj]) + ctrl->bias[c];
+            if (z > best) {  // strict: lowest index wins ties (R12)
+              best = z;
+              bi = c;
+            }
+            if (kDbg && p.dbg_logits && valid) p.dbg_logits[static_cast<uint64_t>(pos) * n_classes + c] = z;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctrl->tempty[acc]);
+      const bool verdict = valid && (bi == target);
+      const uint32_t bv = __ballot_sync(0xFFFFFFFFu, verdict);
+      const uint32_t bvalid = __ballot_sync(0xFFFFFFFFu, valid);
+      if (lane == 0 && bvalid) {
+        bits_out[(pos0 >> 5) + q] = bv;
+        if (bv) {
+          atomicAdd(p.seg_counts + ((pos0 + q * 32) / kRouteTile), static_cast<uint32_t>(__popc(bv)));
+          atomicAdd(p.warp_counts + ((pos0 + q * 32) / kWarpSeg), static_cast<uint32_t>(__popc(bv)));
+        }
+      }
+      if (kDbg && p.dbg_verdict && valid) p.dbg_verdict[pos] = verdict ? 1 : 0;
+      n_in += __popc(bvalid);
+      n_pass += __popc(bv);
+    }
+    if (p.collect_stats && lane == 0) {
+      atomicAdd(&st->d_in[pred], static_cast<unsigned long long>(n_in));
+      atomicAdd(&st->d_pass[pred], static_cast<unsigned long long>(n_pass));
+      atomicAdd(&st->d_comp[pred], static_cast<unsigned long long>(n_in));
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+  }
+  if (tid == 0 && p.collect_stats) atomicAdd(&st->d_cost[pred], static_cast<unsigned long long>(clock64() - t_start));
+  if (tid == 0) ktimer_end(st, 1);
+}
+
 // Host-side entry points (the kernel templates stay inside this translation unit).
 cudaError_t hydro_classifier_configure() {
   void (*ks[])(ClsParams) = {hydro_classifier_kernel<false, false>, hydro_classifier_kernel<true, false>,
                              hydro_classifier_kernel<false, true>, hydro_classifier_kernel<true, true>,
-                             hydro_mlp_kernel<false>, hydro_mlp_kernel<true>};
+                             hydro_mlp_kernel<false>, hydro_mlp_kernel<true>,
+                             hydro_classifier_tm_kernel<false>, hydro_classifier_tm_kernel<true>};
   for (auto k : ks) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kClsSmemBytes);
-    if (e != cudaSuccess) return e;
-  }
-  if (const char* g = getenv("HYDRO_L2_FETCH")) {  // experiment hook: L2 fetch granularity (bytes)
-    cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(atoi(g)));
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -1344,6 +1760,11 @@ void hydro_classifier_launch(const ClsParams& c, int grid, cudaStream_t stream, 
   } else {
     k<<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
   }
+}
+
+void hydro_classifier_tm_launch(const ClsParams& c, int grid, cudaStream_t stream, bool debug) {
+  if (debug) hydro_classifier_tm_kernel<true><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
+  else hydro_classifier_tm_kernel<false><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
 }
 
 void hydro_mlp_launch(const ClsParams& c, int grid, cudaStream_t stream, bool debug) {

@@ -81,6 +81,7 @@ namespace {
 struct PredHost {
   hydro_predicate_desc desc;
   uint8_t* w_tiled = nullptr;
+  uint8_t* w_tiled_tm = nullptr;  // nearest LINEAR heads: K4-T's K order
   float* bias = nullptr;
   int n_pad = 0;
   int a_fp16 = 0;
@@ -167,6 +168,7 @@ struct hydro_ctx {
   int32_t fixed_order[kMaxPred];
   bool fixed_order_set = false;
   bool has_area = false;
+  bool k4_legacy = false;  // HYDRO_K4_LEGACY=1: nearest heads on the shared-memory-A kernel (A/B runs)
   bool has_linear = false, has_mlp = false, has_hsv = false;
   std::vector<PredDev> pd_host;  // the device predicate table as uploaded at freeze
   // timing
@@ -229,7 +231,7 @@ static int next_pow2_pad(int c) {  // n_pad: multiple of 16 >= c
 // image the classifier kernels bulk-copy (n_pad rows per K-block).  try_fp16: re-encode as fp16
 // when every weight is exactly representable (*fp16 = 1), else keep bf16 (*fp16 = 0).
 static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_device, int rows, int n_pad,
-                                 int k_features, bool try_fp16, uint8_t** out, int* fp16);
+                                 int k_features, bool try_fp16, uint8_t** out, int* fp16, bool tm_order);
 
 // ------------------------------------------------------------------------------------------
 
@@ -349,6 +351,10 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
   CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   ctx->k1_occ = hydro_route_occupancy(false);
   CU(hydro_classifier_configure());
+  {
+    const char* e = getenv("HYDRO_K4_LEGACY");
+    ctx->k4_legacy = e && e[0] == '1';
+  }
   CU(cudaMalloc(&ctx->st, sizeof(DevState)));
   CU(cudaMemset(ctx->st, 0, sizeof(DevState)));
   CU(cudaMalloc(&ctx->preds_dev, sizeof(PredDev) * kMaxPred));
@@ -413,10 +419,11 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
     ph.n_pad = next_pow2_pad(C);
     const cudaMemcpyKind kind = d->weights_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     hydro_status st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, H, H, kFeatures, true, &ph.w_tiled,
-                                   &ph.a_fp16);
+                                   &ph.a_fp16, false);
     if (st != HYDRO_OK) return st;
     int w2_fp16 = 0;
-    st = tile_weights(ctx, d->weight2_bf16, d->weights_on_device != 0, C, ph.n_pad, H, false, &ph.w2_tiled, &w2_fp16);
+    st = tile_weights(ctx, d->weight2_bf16, d->weights_on_device != 0, C, ph.n_pad, H, false, &ph.w2_tiled, &w2_fp16,
+                      false);
     if (st != HYDRO_OK) return st;
     CU(cudaMalloc(&ph.bias, sizeof(float) * HYDRO_MAX_CLASSES));
     CU(cudaMemsetAsync(ph.bias, 0, sizeof(float) * HYDRO_MAX_CLASSES, ctx->stream));
@@ -437,8 +444,14 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
     // stage operands as fp16 when every weight is exactly representable (u8 pixels always are):
     // same products, cheaper u8 -> fp16 operand construction in K4
     hydro_status st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, C, ph.n_pad, kFeatures, true,
-                                   &ph.w_tiled, &ph.a_fp16);
+                                   &ph.w_tiled, &ph.a_fp16, false);
     if (st != HYDRO_OK) return st;
+    if (d->crop_mode == HYDRO_CROP_NEAREST) {  // K4-T's copy (same operand type: exactness is per weight)
+      int fp16_tm = 0;
+      st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, C, ph.n_pad, kFeatures, ph.a_fp16 != 0,
+                        &ph.w_tiled_tm, &fp16_tm, true);
+      if (st != HYDRO_OK) return st;
+    }
     CU(cudaMalloc(&ph.bias, sizeof(float) * HYDRO_MAX_CLASSES));
     CU(cudaMemsetAsync(ph.bias, 0, sizeof(float) * HYDRO_MAX_CLASSES, ctx->stream));
     CU(cudaMemcpyAsync(ph.bias, d->bias, sizeof(float) * C,
@@ -457,7 +470,7 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
 }  // extern "C"
 
 static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_device, int rows, int n_pad,
-                                 int k_features, bool try_fp16, uint8_t** out, int* fp16) {
+                                 int k_features, bool try_fp16, uint8_t** out, int* fp16, bool tm_order) {
   const size_t wbytes = static_cast<size_t>(rows) * k_features * 2;
   uint16_t* wdev = nullptr;
   CU(cudaMalloc(&wdev, wbytes));
@@ -467,7 +480,7 @@ static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_devi
   int32_t* inexact = reinterpret_cast<int32_t*>(ctx->zero_word + 1);
   int32_t bad = 1;
   if (try_fp16) {
-    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 1, k_features == kFeatures ? 1 : 0, inexact);
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 1, k_features == kFeatures ? (tm_order ? 2 : 1) : 0, inexact);
     ctx->launches += 1;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(&bad, inexact, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -475,7 +488,7 @@ static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_devi
   }
   *fp16 = bad ? 0 : 1;
   if (bad) {
-    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 0, k_features == kFeatures ? 1 : 0, inexact);
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 0, k_features == kFeatures ? (tm_order ? 2 : 1) : 0, inexact);
     ctx->launches += 1;
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(ctx->stream));
@@ -606,6 +619,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
     q.units = d.units;
     q.units_per_area = d.units_per_area;
     q.w_tiled = ctx->preds[k].w_tiled;
+    q.w_tiled_tm = ctx->preds[k].w_tiled_tm;
     q.bias = ctx->preds[k].bias;
     q.n_classes = d.n_classes;
     q.n_pad = ctx->preds[k].n_pad;
@@ -793,6 +807,7 @@ static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c0, uint64_t max
     if (kind == kClsMlp) hydro_mlp_launch(c, grid, ctx->stream, dbg);
     else if (kind == kClsHsv) hydro_hsv_launch(c, max_positions, ctx->num_sms, ctx->stream);
     // kernel instantiation by context capability: AREA support only when an AREA head exists
+    else if (!ctx->has_area && !ctx->k4_legacy) hydro_classifier_tm_launch(c, grid, ctx->stream, dbg);
     else hydro_classifier_launch(c, grid, ctx->stream, dbg, ctx->has_area);
   });
 }
@@ -1350,6 +1365,7 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
   }
   for (PredHost& p : ctx->preds) {
     cudaFree(p.w_tiled);
+    cudaFree(p.w_tiled_tm);
     cudaFree(p.bias);
     cudaFree(p.w2_tiled);
     cudaFree(p.bias1);
