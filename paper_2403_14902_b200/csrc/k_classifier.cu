@@ -1303,9 +1303,18 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
 // (k = 0..15) of every crop row; K order inside a crop row = crop_pos_feature_tm.
 constexpr int kTmAcol0 = 256;      // first TMEM column of the A ring (accumulators: 2 x <= 128 columns)
 constexpr int kTmGroupCols = 96;   // one crop row of A: 192 fp16 = 96 32-bit columns per lane
-constexpr int kTmMaxSlots = 4;     // staging units per converter warp (depth <= 3)
+#ifndef HYDRO_TM_SLOTS
+#define HYDRO_TM_SLOTS 3
+#endif
+constexpr int kTmMaxSlots = HYDRO_TM_SLOTS;
+#ifdef HYDRO_TM_CPASYNC
+constexpr bool kTmBulk = false;  // stage crop rows with per-lane 16-byte cp.async (A/B variant)
+#else
+constexpr bool kTmBulk = true;   // stage crop rows with one 1-D bulk copy per row segment
+#endif  // staging units per converter warp (depth <= slots - 1)
 constexpr int kTmBStages = 3;
 struct TmCtrl {
+  uint64_t stg[kConvWarps][kTmMaxSlots];  // staging units landed (bulk copies, complete_tx)
   uint64_t full_a[2], empty_a[2];
   uint64_t full_b[kTmBStages], empty_b[kTmBStages];
   uint64_t tfull[2], tempty[2];
@@ -1345,6 +1354,12 @@ __device__ __forceinline__ void tc_st_16x256b_x2(uint32_t taddr, const uint32_t 
                : "memory");
 }
 
+__device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // 8 staged pixels (byte offsets packed 2 per word, relative to `unit`) -> 12 words of fp16x2 (or
 // bf16x2) in feature order f = 3 * pixel + ch
 template <bool kFp16>
@@ -1376,7 +1391,9 @@ __device__ __forceinline__ void tm_convert8(uint32_t unit, const uint32_t (&po)[
 
 __device__ __forceinline__ void tm_wait_depth(uint32_t d) {
   // cp.async.wait_group needs an immediate: the runtime depth of this tile picks the case
-  if (d >= 3) cp_async_wait<3>();
+  if (d >= 5) cp_async_wait<5>();
+  else if (d == 4) cp_async_wait<4>();
+  else if (d == 3) cp_async_wait<3>();
   else if (d == 2) cp_async_wait<2>();
   else if (d == 1) cp_async_wait<1>();
   else cp_async_wait<0>();
@@ -1385,7 +1402,8 @@ __device__ __forceinline__ void tm_wait_depth(uint32_t d) {
 template <bool kDbg, bool kWide>
 __device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl, uint32_t lim, uint32_t pos0, int cu,
                                                 int lane, uint32_t ring, uint32_t tmem_base, uint32_t row_pitch,
-                                                bool fp16, const RowMeta& mm, uint32_t band, uint32_t& gg) {
+                                                bool fp16, const RowMeta& mm, uint32_t band, uint32_t& gg,
+                                                uint32_t& stg_par) {
   const uint8_t* frames = p.frames;
   const int a = lane >> 2, t0 = lane & 3;
   // unit layout: the segments of local tuples 0..15 back to back (lane l < 16 holds tuple l)
@@ -1427,7 +1445,22 @@ __device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl
   const uint32_t my_lo = slen | (soff << 16);
   const uint32_t my_xw =
       kWide ? static_cast<uint32_t>(mm.x0) | (static_cast<uint32_t>(mm.w) << 16) | (my_wide ? 0x80000000u : 0u) : 0u;
+  const uint32_t utot = __shfl_sync(0xFFFFFFFFu, incl, 15);  // bytes of one unit (0: no valid tuple)
   auto stage_unit = [&](int g, uint32_t slot) {
+    if (kTmBulk && !kWide) {
+      // one 1-D bulk copy (TMA engine) per row segment, completion counted on the slot's mbarrier:
+      // the shared-memory writes bypass the LSU pipe the pixel loads use
+      if (g < kGroups) {
+        uint64_t* bar = &ctrl->stg[cu][slot];
+        if (lane == 0) mbar_arrive_expect_tx(bar, utot);
+        __syncwarp();
+        if (slen != 0) {
+          const uint8_t* row = frames + (my_src + (((2u * g + 1u) * my_h) >> 7) * row_pitch);
+          bulk_g2s_u32(ring + slot * ubytes + soff, row, slen, bar);
+        }
+      }
+      return;
+    }
     if (g < kGroups) {
       const uint32_t dst0 = ring + slot * ubytes;
 #pragma unroll
@@ -1455,8 +1488,13 @@ __device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl
   for (int g = 0; g < kGroups; ++g, ++gg) {
     stage_unit(g + static_cast<int>(depth), slot_stage);
     slot_stage = slot_stage + 1 == nslot ? 0 : slot_stage + 1;
-    tm_wait_depth(depth);  // this thread's copies of unit g have landed
-    __syncwarp();             // ... and every lane's
+    if (!kTmBulk || kWide) {
+      tm_wait_depth(depth);  // this thread's copies of unit g have landed
+      __syncwarp();          // ... and every lane's
+    } else {
+      mbar_wait(&ctrl->stg[cu][slot_use], (stg_par >> slot_use) & 1u);  // unit g's bulk copies landed
+      stg_par ^= 1u << slot_use;
+    }
     const uint32_t sa = gg & 1u, aph = (gg >> 1) & 1u;
     mbar_wait(&ctrl->empty_a[sa], aph ^ 1u);  // the MMA has consumed group gg - 2 from this TMEM slot
     tc_fence_after();
@@ -1503,7 +1541,7 @@ __device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl
     __syncwarp();  // every lane's stores (and smem reads of the unit) are done
     if (lane == 0) mbar_arrive(&ctrl->full_a[sa]);
   }
-  cp_async_wait<0>();
+  if (!kTmBulk || kWide) cp_async_wait<0>();
 }
 
 extern __shared__ __align__(1024) uint8_t hydro_tm_smem[];
@@ -1569,6 +1607,8 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
       mbar_init(&ctrl->full_b[s], 1);
       mbar_init(&ctrl->empty_b[s], 1);
     }
+    for (int w = 0; w < kConvWarps; ++w)
+      for (int s = 0; s < kTmMaxSlots; ++s) mbar_init(&ctrl->stg[w][s], 1);
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
@@ -1636,16 +1676,18 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
     const int cu = warp - kConvWarp0;
     const uint32_t band = 32u * static_cast<uint32_t>(warp & 3) + 16u * static_cast<uint32_t>(cu >> 2);
     const uint32_t ring = stage0 + static_cast<uint32_t>(cu) * kTmWarpStage;
-    uint32_t gg = 0;
+    uint32_t gg = 0, stg_par = 0;
     for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
       const uint32_t pos0 = tw.pos0(unit);
       const RowMeta mm = load_meta(p, list_in, base, pos0 + band + (lane & 15), lane < 16 ? tw.lim : 0u);
       const bool any_wide =
           __any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes));
       if (any_wide)
-        tm_convert_tile<kDbg, true>(p, ctrl, tw.lim, pos0, cu, lane, ring, tmem_base, row_pitch, fp16, mm, band, gg);
+        tm_convert_tile<kDbg, true>(p, ctrl, tw.lim, pos0, cu, lane, ring, tmem_base, row_pitch, fp16, mm, band, gg,
+                                    stg_par);
       else
-        tm_convert_tile<kDbg, false>(p, ctrl, tw.lim, pos0, cu, lane, ring, tmem_base, row_pitch, fp16, mm, band, gg);
+        tm_convert_tile<kDbg, false>(p, ctrl, tw.lim, pos0, cu, lane, ring, tmem_base, row_pitch, fp16, mm, band, gg,
+                                     stg_par);
     }
   } else {
     // ===================== epilogue warps 0..3 (TMEM lane quadrant = warp)
