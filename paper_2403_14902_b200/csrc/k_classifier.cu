@@ -1301,7 +1301,13 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
 // Converter warp cu owns tile rows [32*((6+cu)%4) + 16*(cu/4), +16) (the TMEM lane quarter of
 // warp 6+cu).  Thread t handles local tuples a = t/4 and a + 8, output pixels dx = 4k + (t%4)
 // (k = 0..15) of every crop row; K order inside a crop row = crop_pos_feature_tm.
-constexpr int kTmAcol0 = 256;      // first TMEM column of the A ring (accumulators: 2 x <= 128 columns)
+#ifndef HYDRO_TM_ASLOTS
+#define HYDRO_TM_ASLOTS 4
+#endif
+constexpr int kTmASlots = HYDRO_TM_ASLOTS;                 // crop rows of A in TMEM (2 or 4)
+constexpr int kTmAcol0 = 512 - kTmASlots * 96;             // first TMEM column of the A ring
+// accumulator buffers below kTmAcol0: two when they fit (N <= 64, or a 2-slot A ring), else one
+// (N = 128 with 4 A slots: the next tile's first MMA waits for the epilogue's tcgen05.ld)
 constexpr int kTmGroupCols = 96;   // one crop row of A: 192 fp16 = 96 32-bit columns per lane
 #ifndef HYDRO_TM_SLOTS
 #define HYDRO_TM_SLOTS 3
@@ -1315,7 +1321,7 @@ constexpr bool kTmBulk = true;   // stage crop rows with one 1-D bulk copy per r
 constexpr int kTmBStages = 3;
 struct TmCtrl {
   uint64_t stg[kConvWarps][kTmMaxSlots];  // staging units landed (bulk copies, complete_tx)
-  uint64_t full_a[2], empty_a[2];
+  uint64_t full_a[kTmASlots], empty_a[kTmASlots];
   uint64_t full_b[kTmBStages], empty_b[kTmBStages];
   uint64_t tfull[2], tempty[2];
   uint32_t tmem_base;
@@ -1495,8 +1501,8 @@ __device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl
       mbar_wait(&ctrl->stg[cu][slot_use], (stg_par >> slot_use) & 1u);  // unit g's bulk copies landed
       stg_par ^= 1u << slot_use;
     }
-    const uint32_t sa = gg & 1u, aph = (gg >> 1) & 1u;
-    mbar_wait(&ctrl->empty_a[sa], aph ^ 1u);  // the MMA has consumed group gg - 2 from this TMEM slot
+    const uint32_t sa = gg % kTmASlots, aph = (gg / kTmASlots) & 1u;
+    mbar_wait(&ctrl->empty_a[sa], aph ^ 1u);  // the MMA has consumed group gg - kTmASlots from this slot
     tc_fence_after();
     const uint32_t unit = ring + slot_use * ubytes;
 #pragma unroll
@@ -1585,6 +1591,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
   const bool fp16 = pdg.a_fp16 != 0;
   const uint8_t* w_tiled = pdg.w_tiled_tm;
   const uint32_t n_alloc = n_pad <= 32 ? 32u : (n_pad <= 64 ? 64u : 128u);
+  const uint32_t n_acc = 2u * n_alloc <= static_cast<uint32_t>(kTmAcol0) ? 2u : 1u;  // accumulator buffers
   const uint32_t b_stage_bytes = static_cast<uint32_t>(n_pad) * 128u;
   const uint32_t row_pitch = static_cast<uint32_t>(p.frame_w * 3);
 
@@ -1597,9 +1604,11 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kTmASlots; ++s) {
       mbar_init(&ctrl->full_a[s], kConvWarps);
       mbar_init(&ctrl->empty_a[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&ctrl->tfull[s], 1);
       mbar_init(&ctrl->tempty[s], kEpiWarps);
     }
@@ -1644,13 +1653,13 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
       const uint32_t idesc = idesc_f16_f32(kTileM, static_cast<uint32_t>(n_pad), !fp16);
       uint32_t itb = 0, gg = 0, tl = 0;
       for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
-        const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
+        const uint32_t acc = tl % n_acc, aph = (tl / n_acc) & 1u;
         mbar_wait_backoff<256>(&ctrl->tempty[acc], aph ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * n_alloc;
         for (int g = 0; g < kGroups; ++g, ++gg) {
-          const uint32_t sa = gg & 1u;
-          HYDRO_PIPE_WAIT(&ctrl->full_a[sa], (gg >> 1) & 1u);
+          const uint32_t sa = gg % kTmASlots;
+          HYDRO_PIPE_WAIT(&ctrl->full_a[sa], (gg / kTmASlots) & 1u);
           tc_fence_after();
           const uint32_t a_col = tmem_base + kTmAcol0 + sa * kTmGroupCols;
 #pragma unroll
@@ -1695,7 +1704,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
     uint32_t n_in = 0, n_pass = 0, tl = 0;
     for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
       const uint32_t pos0 = tw.pos0(unit);
-      const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
+      const uint32_t acc = tl % n_acc, aph = (tl / n_acc) & 1u;
       mbar_wait_backoff<1024>(&ctrl->tfull[acc], aph);
       tc_fence_after();
       const int m = q * 32 + lane;
