@@ -414,7 +414,11 @@ def run_gpu(args):
                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside the step; fp16 "
                                    "operands of layer 1 run at the bf16 rate)"}
     else:
-        roofline = {"kernel": "hydro_classifier_kernel (K4: crop gather + tcgen05 linear head)",
+        k4_name = ("hydro_classifier_kernel (K4: cp.async-staged crop gather, A in shared memory, tcgen05 linear head)"
+                   if os.environ.get("HYDRO_K4_LEGACY") == "1" else
+                   "hydro_classifier_tm_kernel (K4-T: bulk-copy-staged crop gather, A in tensor memory, tcgen05 "
+                   "linear head)")
+        roofline = {"kernel": k4_name,
                     "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_note,
                     "algorithmic_bytes_per_launch": k4_bytes / max(k4_n, 1),
