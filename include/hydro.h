@@ -275,12 +275,16 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out);
 hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* desc, int32_t* pred_id);
 
 /* Verdict cache for reuse-aware routing: predicate
-   pred_id (LABEL_EQ or HASH) keeps a device bitmap of known verdicts over tuple ids
-   [0, id_capacity) (2 bits per id, library-owned).  A cached verdict is used instead of
-   evaluating the predicate (the result is unchanged: the cache holds the predicate's verdicts);
-   cost statistics count only evaluated tuples (the cost of computing the UDF).  fill = 1 also
-   records every verdict the predicate computes.  Any time no batch is in flight (ESTATE
-   otherwise); EINVAL for classifier predicates, id_capacity 0 or > 2^34, or a second call. */
+   pred_id (any kind: LABEL_EQ, HASH, or a classifier -- LINEAR, MLP, HSV, the expensive UDFs
+   UC2 reuses) keeps a device bitmap of known verdicts over tuple ids [0, id_capacity) (2 bits
+   per id, library-owned).  A cached verdict is used instead of evaluating the predicate (the
+   result is unchanged: the cache holds the predicate's verdicts): a cheap predicate looks its
+   alive tuples up inside K1; a classifier hop is first split by K0c into cached verdicts and the
+   uncached tuples, and only those go through the classifier kernel.  Cost statistics count only
+   evaluated tuples (the cost of computing the UDF).  fill = 1 also records every verdict the
+   predicate computes.  Any time no batch is in flight (ESTATE otherwise); EINVAL for
+   id_capacity 0 or > 2^34, or a second call.  The first cache on a classifier allocates two
+   u32 lists of max_batch_tuples (ENOMEM / ECUDA on failure). */
 hydro_status hydro_cache_enable(hydro_ctx* ctx, int32_t pred_id, uint64_t id_capacity, int32_t fill);
 
 /* Records verdicts[i] (0 / 1) of predicate pred_id for tuple ids[i], i < n (e.g. the results of
@@ -291,10 +295,11 @@ hydro_status hydro_cache_enable(hydro_ctx* ctx, int32_t pred_id, uint64_t id_cap
 hydro_status hydro_cache_put(hydro_ctx* ctx, int32_t pred_id, const uint64_t* ids, const uint8_t* verdicts,
                              int64_t n, int32_t on_device);
 
-/* Evaluates predicate pred_id alone on every tuple of the DEVICE batch `tuples` and records
-   its verdicts in its cache -- the exploratory single-UDF queries whose results a later query
-   reuses (Q1 / Q2 of PAPER.md:565-570).  Statistics untouched.  Synchronises.  EINVAL without an
-   enabled cache or with host tuples. */
+/* Evaluates predicate pred_id alone on every tuple of the DEVICE batch `tuples` (K1 for a cheap
+   predicate, its classifier kernel for LINEAR / MLP / HSV) and records its verdicts in its cache
+   -- the exploratory single-UDF queries whose results a later query reuses (Q1 / Q2 of
+   PAPER.md:565-570).  Statistics untouched.  Synchronises.  EINVAL without an enabled cache or
+   with host tuples. */
 hydro_status hydro_cache_fill(hydro_ctx* ctx, int32_t pred_id, const hydro_tuples* tuples);
 
 /* FIXED_ORDER policy: sets the order (a permutation of 0..P-1).  EINVAL if not a permutation. */

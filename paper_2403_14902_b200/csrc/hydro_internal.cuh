@@ -277,6 +277,14 @@ struct ClsParams {
   uint32_t* bal_chunks;    // K6: estimated cost (sum of w*h) per 32-position chunk of the hop input
   uint32_t* bal_bounds;    // K6: output bounds, bal_ctas + 1 entries
   int32_t bal_ctas;        // CTAs of the K4 launch the bounds are for
+  // verdict caches on classifier hops (reuse; R26): K0c splits a cached hop's
+  // input into cached verdicts (written straight into the hop bitmap) and the uncached tuples,
+  // which the classifier kernel then evaluates through this redirection
+  const uint64_t* id;       // tuple ids (cache lookups and fills)
+  uint32_t* cache_idx;      // uncached tuples: batch indices (the classifier's list input) ...
+  uint32_t* cache_pos;      // ... their positions in the hop input (verdict bits) ...
+  uint32_t* cache_count;    // ... and their number; nullptr: the context has no classifier cache
+  int32_t force_fill;       // hydro_cache_fill: record every computed verdict
 };
 
 // ------------------------------------------------------------------------------------------
@@ -439,6 +447,52 @@ __device__ __forceinline__ void ktimer_end(DevState* st, int kind) {
   }
 }
 
+// ---- classifier hop inputs and verdict output (all K4 kernels)
+// A cached classifier hop (its predicate has a verdict cache and K0c ran) evaluates only the
+// uncached tuples: list input = their batch indices, `ind` = their hop-input positions.
+__device__ __forceinline__ const uint32_t* cls_redirect(const ClsParams& p, const PredDev& pd, const uint32_t*& list_in,
+                                                        uint32_t& count) {
+  if (!p.dispatch || !p.cache_count || !pd.cache_known) return nullptr;
+  list_in = p.cache_idx;
+  count = *p.cache_count;
+  return p.cache_pos;
+}
+// Verdict of position `pos` of the kernel's input (one call per lane, the 32 lanes of a warp hold
+// positions wpos0 .. wpos0 + 31): direct mode writes the bitmap word with one ballot; redirected
+// mode sets the bit of the hop-input position (atomicOr: a word's positions are spread over
+// tiles).  Survivor counts per 2048 / 256 positions for K2.  With `fill`, the computed verdict is
+// recorded in the predicate's cache (keyed by tuple id).
+__device__ __forceinline__ void cls_emit(const ClsParams& p, uint32_t* bits_out, const uint32_t* ind,
+                                         const uint32_t* list_in, uint32_t base, uint32_t wpos0, uint32_t pos,
+                                         bool valid, bool verdict, const PredDev& pd, bool fill) {
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  if (!ind) {
+    const uint32_t bv = __ballot_sync(0xFFFFFFFFu, verdict), bvalid = __ballot_sync(0xFFFFFFFFu, valid);
+    if (lane == 0 && bvalid) {
+      bits_out[wpos0 >> 5] = bv;
+      if (bv) {
+        atomicAdd(p.seg_counts + wpos0 / kRouteTile, static_cast<uint32_t>(__popc(bv)));
+        atomicAdd(p.warp_counts + wpos0 / kWarpSeg, static_cast<uint32_t>(__popc(bv)));
+      }
+    }
+  } else if (valid && verdict) {
+    const uint32_t q = __ldg(ind + pos);
+    atomicOr(bits_out + (q >> 5), 1u << (q & 31));
+    atomicAdd(p.seg_counts + q / kRouteTile, 1u);
+    atomicAdd(p.warp_counts + q / kWarpSeg, 1u);
+  }
+  if (fill && valid) {
+    const uint32_t idx = list_in ? __ldg(list_in + pos) : base + pos;
+    const uint64_t id = __ldg(p.id + idx);
+    if (id < pd.cache_cap) {
+      const uint32_t bit = 1u << (id & 31);
+      if (verdict) atomicOr(pd.cache_pass + (id >> 5), bit);
+      else atomicAnd(pd.cache_pass + (id >> 5), ~bit);
+      atomicOr(pd.cache_known + (id >> 5), bit);
+    }
+  }
+}
+
 // ---- method arithmetic on device (independent of oracle/, written from DESIGN.md R5)
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   uint64_t z = x + 0x9E3779B97F4A7C15ull;
@@ -466,6 +520,7 @@ void hydro_classifier_launch(const hydro::ClsParams& c, int grid, cudaStream_t s
 void hydro_balance_launch(const hydro::ClsParams& c, uint64_t max_positions, int num_sms, cudaStream_t stream);
 void hydro_mlp_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug);
 void hydro_classifier_tm_launch(const hydro::ClsParams& c, int grid, cudaStream_t stream, bool debug);
+void hydro_cache_split_launch(const hydro::ClsParams& c, uint64_t max_positions, int num_sms, cudaStream_t stream);
 void hydro_hsv_launch(const hydro::ClsParams& c, uint64_t max_positions, int num_sms, cudaStream_t stream);
 int hydro_hsv_warps_per_sm();
 __global__ void hydro_fold_kernel(hydro::DevState* st, hydro::BatchRec* rec, int32_t mode, uint32_t n_batch,

@@ -741,6 +741,9 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     count = list_in ? *p.count_in : p.range_n;
     bits_out = p.bits_out;
   }
+  // cached classifier hop: only the uncached tuples (K0c's list), verdict bits by hop position
+  const uint32_t* ind = cls_redirect(p, p.preds[pred], list_in, count);
+  const bool fill = p.preds[pred].cache_known && (p.preds[pred].cache_fill || p.force_fill);
   const uint32_t num_tiles = (count + kTileM - 1) / kTileM;
   const PredDev& pdg = p.preds[pred];
   const bool area = kArea && pdg.crop_mode == HYDRO_CROP_AREA;  // kArea: the context has an AREA head
@@ -748,7 +751,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   // the same units, so a pair's last unit may hold a tile past num_tiles (all rows invalid)
   const uint32_t crank = kPair == 2 ? cluster_ctarank() : 0u;
   TileWalk tw{blockIdx.x / kPair, gridDim.x / kPair, (num_tiles + kPair - 1) / kPair, 0u, count, kPair, crank, false};
-  if (kPair == 1 && area && p.bounds) {  // data-aware: this CTA's balanced position range
+  if (kPair == 1 && area && p.bounds && !ind) {  // data-aware: this CTA's balanced position range
     tw.bal = true;
     tw.lo = min(p.bounds[blockIdx.x], count);
     tw.lim = min(p.bounds[blockIdx.x + 1], count);
@@ -975,13 +978,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       const bool verdict = valid && (bi == target);
       const uint32_t bv = __ballot_sync(0xFFFFFFFFu, verdict);
       const uint32_t bvalid = __ballot_sync(0xFFFFFFFFu, valid);
-      if (lane == 0 && bvalid) {
-        bits_out[(pos0 >> 5) + q] = bv;
-        if (bv) {
-          atomicAdd(p.seg_counts + ((pos0 + q * 32) / kRouteTile), static_cast<uint32_t>(__popc(bv)));
-          atomicAdd(p.warp_counts + ((pos0 + q * 32) / kWarpSeg), static_cast<uint32_t>(__popc(bv)));
-        }
-      }
+      cls_emit(p, bits_out, ind, list_in, base, pos0 + q * 32, pos, valid, verdict, pdg, fill);
       if (kDbg && p.dbg_verdict && valid) p.dbg_verdict[pos] = verdict ? 1 : 0;
       n_in += __popc(bvalid);
       n_pass += __popc(bv);
@@ -1050,6 +1047,9 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
     count = list_in ? *p.count_in : p.range_n;
     bits_out = p.bits_out;
   }
+  // cached classifier hop: only the uncached tuples (K0c's list), verdict bits by hop position
+  const uint32_t* ind = cls_redirect(p, p.preds[pred], list_in, count);
+  const bool fill = p.preds[pred].cache_known && (p.preds[pred].cache_fill || p.force_fill);
   const uint32_t num_tiles = (count + kTileM - 1) / kTileM;
   const uint32_t crank = cluster_ctarank();
   const TileWalk tw{blockIdx.x / kP, gridDim.x / kP, (num_tiles + kP - 1) / kP, 0u, count, kP, crank, false};
@@ -1258,13 +1258,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
       const bool verdict = valid && (bi == target);
       const uint32_t bv = __ballot_sync(0xFFFFFFFFu, verdict);
       const uint32_t bvalid = __ballot_sync(0xFFFFFFFFu, valid);
-      if (lane == 0 && bvalid) {
-        bits_out[(pos0 >> 5) + q] = bv;
-        if (bv) {
-          atomicAdd(p.seg_counts + ((pos0 + q * 32) / kRouteTile), static_cast<uint32_t>(__popc(bv)));
-          atomicAdd(p.warp_counts + ((pos0 + q * 32) / kWarpSeg), static_cast<uint32_t>(__popc(bv)));
-        }
-      }
+      cls_emit(p, bits_out, ind, list_in, base, pos0 + q * 32, pos, valid, verdict, pdg, fill);
       if (kDbg && p.dbg_verdict && valid) p.dbg_verdict[pos] = verdict ? 1 : 0;
       n_in += __popc(bvalid);
       n_pass += __popc(bv);
@@ -1578,6 +1572,9 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
     count = list_in ? *p.count_in : p.range_n;
     bits_out = p.bits_out;
   }
+  // cached classifier hop: only the uncached tuples (K0c's list), verdict bits by hop position
+  const uint32_t* ind = cls_redirect(p, p.preds[pred], list_in, count);
+  const bool fill = p.preds[pred].cache_known && (p.preds[pred].cache_fill || p.force_fill);
   const uint32_t num_tiles = (count + kTileM - 1) / kTileM;
   const PredDev& pdg = p.preds[pred];
   TileWalk tw{blockIdx.x, gridDim.x, num_tiles, 0u, count, 1u, 0u, false};
@@ -1736,13 +1733,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
       const bool verdict = valid && (bi == target);
       const uint32_t bv = __ballot_sync(0xFFFFFFFFu, verdict);
       const uint32_t bvalid = __ballot_sync(0xFFFFFFFFu, valid);
-      if (lane == 0 && bvalid) {
-        bits_out[(pos0 >> 5) + q] = bv;
-        if (bv) {
-          atomicAdd(p.seg_counts + ((pos0 + q * 32) / kRouteTile), static_cast<uint32_t>(__popc(bv)));
-          atomicAdd(p.warp_counts + ((pos0 + q * 32) / kWarpSeg), static_cast<uint32_t>(__popc(bv)));
-        }
-      }
+      cls_emit(p, bits_out, ind, list_in, base, pos0 + q * 32, pos, valid, verdict, pdg, fill);
       if (kDbg && p.dbg_verdict && valid) p.dbg_verdict[pos] = verdict ? 1 : 0;
       n_in += __popc(bvalid);
       n_pass += __popc(bv);
@@ -1762,6 +1753,75 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
   }
   if (tid == 0 && p.collect_stats) atomicAdd(&st->d_cost[pred], static_cast<unsigned long long>(clock64() - t_start));
   if (tid == 0) ktimer_end(st, 1);
+}
+
+// ------------------------------------------------------------------------------------------
+// K0c: verdict-cache split of a classifier hop (reuse-aware routing on expensive UDFs, PAPER.md:
+// 589-605; R26).  Exits unless the chain slot's hop is a classifier whose predicate has a cache.
+// One warp per 32 hop-input positions: cached verdicts go straight into the hop's bitmap word
+// (and the survivor counts); the uncached tuples are appended (warp-aggregated atomic) to the
+// list the classifier kernel evaluates next.  Cache hits count as routed and passed, never as
+// computed or charged (R26).
+__global__ void __launch_bounds__(256) hydro_cache_split_kernel(ClsParams p) {
+  DevState* st = p.st;
+  const int h = st->sched[p.hop];
+  if (h < 0 || h >= st->n_pred) return;
+  const int pred = st->order[h];
+  if (!is_classifier(st->kind[pred])) return;
+  const PredDev& pd = p.preds[pred];
+  if (!pd.cache_known) return;
+  const uint32_t* list_in;
+  uint32_t count;
+  const uint32_t base = p.range_base;
+  if (h == 0) {
+    list_in = p.sel0;
+    count = p.sel0 ? *p.sel0_count : p.range_n;
+  } else {
+    list_in = p.lists + static_cast<uint64_t>(h) * p.list_stride;
+    count = p.counts[h];
+  }
+  uint32_t* bits_out = p.bits + static_cast<uint64_t>(h) * p.bits_stride;
+  const int lane = threadIdx.x & 31;
+  const uint32_t words = (count + 31) / 32;
+  uint32_t n_hit = 0, n_hit_pass = 0;
+  for (uint32_t wi = (blockIdx.x * blockDim.x + threadIdx.x) / 32; wi < words; wi += (gridDim.x * blockDim.x) / 32) {
+    const uint32_t pos = wi * 32 + lane;
+    const bool valid = pos < count;
+    uint32_t idx = 0;
+    bool known = false, pass = false;
+    if (valid) {
+      idx = list_in ? __ldg(list_in + pos) : base + pos;
+      const uint64_t id = __ldg(p.id + idx);
+      if (id < pd.cache_cap) {
+        known = (__ldg(pd.cache_known + (id >> 5)) >> (id & 31)) & 1u;
+        pass = known && ((__ldg(pd.cache_pass + (id >> 5)) >> (id & 31)) & 1u);
+      }
+    }
+    const uint32_t vb = __ballot_sync(0xFFFFFFFFu, pass);
+    const uint32_t kb = __ballot_sync(0xFFFFFFFFu, known);
+    const uint32_t ub = __ballot_sync(0xFFFFFFFFu, valid && !known);
+    if (lane == 0) {
+      bits_out[wi] = vb;  // the classifier ORs the computed verdicts in
+      if (vb) {
+        atomicAdd(p.seg_counts + (wi * 32) / kRouteTile, static_cast<uint32_t>(__popc(vb)));
+        atomicAdd(p.warp_counts + (wi * 32) / kWarpSeg, static_cast<uint32_t>(__popc(vb)));
+      }
+    }
+    uint32_t at = 0;
+    if (lane == 0 && ub) at = atomicAdd(p.cache_count, static_cast<uint32_t>(__popc(ub)));
+    at = __shfl_sync(0xFFFFFFFFu, at, 0);
+    if (valid && !known) {
+      const uint32_t r = at + static_cast<uint32_t>(__popc(ub & ((1u << lane) - 1u)));
+      p.cache_idx[r] = idx;
+      p.cache_pos[r] = pos;
+    }
+    n_hit += __popc(kb);
+    n_hit_pass += __popc(vb);
+  }
+  if (p.collect_stats && lane == 0 && n_hit) {
+    atomicAdd(&st->d_in[pred], static_cast<unsigned long long>(n_hit));
+    atomicAdd(&st->d_pass[pred], static_cast<unsigned long long>(n_hit_pass));
+  }
 }
 
 // Host-side entry points (the kernel templates stay inside this translation unit).
@@ -1816,6 +1876,12 @@ void hydro_classifier_launch(const ClsParams& c, int grid, cudaStream_t stream, 
 void hydro_classifier_tm_launch(const ClsParams& c, int grid, cudaStream_t stream, bool debug) {
   if (debug) hydro_classifier_tm_kernel<true><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
   else hydro_classifier_tm_kernel<false><<<grid, kClsThreads, kClsSmemBytes, stream>>>(c);
+}
+
+void hydro_cache_split_launch(const ClsParams& c, uint64_t max_positions, int num_sms, cudaStream_t stream) {
+  const uint64_t warps = (max_positions + 31) / 32;
+  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((warps + 7) / 8, static_cast<uint64_t>(num_sms) * 8));
+  hydro_cache_split_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(c);
 }
 
 void hydro_mlp_launch(const ClsParams& c, int grid, cudaStream_t stream, bool debug) {

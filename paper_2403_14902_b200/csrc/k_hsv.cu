@@ -77,6 +77,8 @@ __global__ void __launch_bounds__(kHsvThreads, 3) hydro_hsv_kernel(ClsParams p) 
     count = list_in ? *p.count_in : p.range_n;
     bits_out = p.bits_out;
   }
+  const uint32_t* ind = cls_redirect(p, p.preds[pred], list_in, count);  // cached hop: uncached tuples
+  const bool fill = p.preds[pred].cache_known && (p.preds[pred].cache_fill || p.force_fill);
   // OpenCV's reciprocal tables (exact integer rounding; no .5 ties occur for i < 2^13)
   __shared__ int s_sdiv[256], s_hdiv[256];
   for (int i = threadIdx.x; i < 256; i += kHsvThreads) {
@@ -165,13 +167,7 @@ __global__ void __launch_bounds__(kHsvThreads, 3) hydro_hsv_kernel(ClsParams p) 
       }
       if (bc == target) vbits |= 1u << i;
     }
-    if (lane == 0 && bvalid) {
-      bits_out[wi] = vbits;
-      if (vbits) {
-        atomicAdd(p.seg_counts + (wi * 32) / kRouteTile, static_cast<uint32_t>(__popc(vbits)));
-        atomicAdd(p.warp_counts + (wi * 32) / kWarpSeg, static_cast<uint32_t>(__popc(vbits)));
-      }
-    }
+    cls_emit(p, bits_out, ind, list_in, base, wi * 32, pos_l, valid_l, (vbits >> lane) & 1u, p.preds[pred], fill);
     if (p.dbg_verdict && valid_l) p.dbg_verdict[pos_l] = (vbits >> lane) & 1u;
     n_in += __popc(bvalid);
     n_pass += __popc(vbits);

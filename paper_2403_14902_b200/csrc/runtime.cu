@@ -168,7 +168,10 @@ struct hydro_ctx {
   int32_t fixed_order[kMaxPred];
   bool fixed_order_set = false;
   bool has_area = false;
-  bool k4_legacy = false;  // HYDRO_K4_LEGACY=1: nearest heads on the shared-memory-A kernel (A/B runs)
+  bool k4_legacy = false;
+  uint32_t* cache_idx = nullptr;    // K0c: uncached tuples of a cached classifier hop (batch indices)
+  uint32_t* cache_pos = nullptr;    //      and their hop-input positions
+  uint32_t* cache_count = nullptr;  //      their number (nullptr: no classifier cache)  // HYDRO_K4_LEGACY=1: nearest heads on the shared-memory-A kernel (A/B runs)
   bool has_linear = false, has_mlp = false, has_hsv = false;
   std::vector<PredDev> pd_host;  // the device predicate table as uploaded at freeze
   // timing
@@ -507,8 +510,13 @@ hydro_status hydro_cache_enable(hydro_ctx* ctx, int32_t k, uint64_t id_capacity,
   }
   if (k < 0 || k >= static_cast<int32_t>(ctx->preds.size())) return set_err(HYDRO_EINVAL, "bad pred id");
   PredHost& ph = ctx->preds[k];
-  if (is_classifier(ph.desc.kind)) return set_err(HYDRO_EINVAL, "verdict caches are for LABEL_EQ / HASH predicates");
   if (ph.cache_known) return set_err(HYDRO_EINVAL, "cache already enabled");
+  if (is_classifier(ph.desc.kind) && !ctx->cache_count) {  // K0c's split lists (one set: hops run in order)
+    const size_t cap = static_cast<size_t>(ctx->cfg.max_batch_tuples) + 64;
+    CU(cudaMalloc(&ctx->cache_idx, cap * sizeof(uint32_t)));
+    CU(cudaMalloc(&ctx->cache_pos, cap * sizeof(uint32_t)));
+    CU(cudaMalloc(&ctx->cache_count, sizeof(uint32_t)));
+  }
   if (id_capacity == 0 || id_capacity > (1ull << 34)) return set_err(HYDRO_EINVAL, "id_capacity in [1, 2^34]");
   const size_t words = static_cast<size_t>((id_capacity + 31) / 32);
   CU(cudaMalloc(&ph.cache_known, words * 4));
@@ -1020,6 +1028,16 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
       c.range_n = rest_n;
       c.sel0 = t->sel;
       c.sel0_count = t->sel_count;
+      c.id = id;
+      if (ctx->cache_count) {  // K0c: cached verdicts of this hop (exits unless it is a cached classifier)
+        c.cache_idx = ctx->cache_idx;
+        c.cache_pos = ctx->cache_pos;
+        c.cache_count = ctx->cache_count;
+        CU(cudaMemsetAsync(ctx->cache_count, 0, sizeof(uint32_t), ctx->stream));
+        if ((s = timed_launch(ctx, 7, [&] { hydro_cache_split_launch(c, rest_n, ctx->num_sms, ctx->stream); })) !=
+            HYDRO_OK)
+          return s;
+      }
       if (ctx->has_linear && (s = launch_cls(ctx, c, rest_n, kClsLinear)) != HYDRO_OK) return s;
       if (ctx->has_mlp && (s = launch_cls(ctx, c, rest_n, kClsMlp)) != HYDRO_OK) return s;
       if (ctx->has_hsv && (s = launch_cls(ctx, c, rest_n, kClsHsv)) != HYDRO_OK) return s;
@@ -1334,6 +1352,22 @@ hydro_status hydro_cache_fill(hydro_ctx* ctx, int32_t k, const hydro_tuples* t) 
   hydro_status s = freeze(ctx);
   if (s != HYDRO_OK) return s;
   if (t->n == 0) return HYDRO_OK;
+  if (is_classifier(ctx->preds[k].desc.kind)) {  // the classifier alone over the batch, verdicts recorded
+    ClsParams c = cls_base(ctx, t->frame_id, reinterpret_cast<const uint64_t*>(t->bbox));
+    c.dispatch = 0;
+    c.explicit_pred = k;
+    c.list_in = nullptr;
+    c.range_base = 0;
+    c.range_n = static_cast<uint32_t>(t->n);
+    c.bits_out = ctx->warm_bits;
+    c.collect_stats = 0;
+    c.id = t->id;
+    c.force_fill = 1;
+    if ((s = launch_cls(ctx, c, static_cast<uint64_t>(t->n), cls_kind_of(ctx->preds[k].desc.kind))) != HYDRO_OK)
+      return s;
+    CU(cudaStreamSynchronize(ctx->stream));
+    return check_sticky(ctx);
+  }
   RouteParams r = route_base(ctx, t->id, t->frame_id, reinterpret_cast<const uint64_t*>(t->bbox), t->label);
   r.dispatch = 0;
   r.explicit_pred = k;
@@ -1383,6 +1417,9 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
   cudaFree(ctx->counts);
   cudaFree(ctx->bits);
   cudaFree(ctx->warm_bits);
+  cudaFree(ctx->cache_idx);
+  cudaFree(ctx->cache_pos);
+  cudaFree(ctx->cache_count);
   cudaFree(ctx->seg_counts);
   cudaFree(ctx->warm_and);
   cudaFree(ctx->bal_chunks);
