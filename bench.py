@@ -338,6 +338,7 @@ def run_gpu(args):
     km_tuples = mlp_in() - min_t0
     kh_tuples = hsv_in() - hin_t0
     op_fp16 = [e.stats(k)["operand_fp16"] for k in lin + mlps]
+    op_scale = [e.stats(k)["operand_scale_log2"] for k in lin]
     # ---- breakdown of the rest of the step (separate pass, CUDA events around every launch)
     e.set_kernel_timing(True)
     run_steps(args.steps, 2)
@@ -442,8 +443,11 @@ def run_gpu(args):
                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "fp16" if all(op_fp16) else "bf16", "data": "synthetic",
                "config": {"workload": WORKLOAD_MLP if mlp else (WORKLOAD_HSV if hsv else WORKLOAD),
-                          "weights": args.weights + (" (every weight fp16-exact: fp16 operands, the same products)"
-                                                     if all(op_fp16) else " (bf16 operands)"),
+                          "weights": args.weights + ((" (every weight fp16-exact: fp16 operands, the same products)"
+                                                      if not any(op_scale) else
+                                                      f" (general bf16 heads tiled as 2^k W, k = {op_scale}: fp16-exact, "
+                                                      "logits scaled back by 2^-k exactly; fp16 operands, the same "
+                                                      "products)") if all(op_fp16) else " (bf16 operands)"),
                           "tuples_per_step": world * TUPLES_PER_STEP,
                           "batch_tuples": TUPLES_PER_STEP, "policy": "score (cost/(1-sel)), measured costs",
                           "l2": "inputs larger than L2: 2.83 GB frame pool + 6 rotating 22 MB tuple batches",
@@ -576,10 +580,22 @@ def run_uc2(args):
 
     torch.cuda.set_device(0)
     B.build()
-    n, batch, scale, units = 15_000_000, 1_000_000, 1000, 1024
-    w = workload("uc2", n=n)
-    for p in w.preds:  # expensive detectors: the UDF cost, not the routing overhead, must dominate
-        p["units"], p["declared_cost"] = units, float(units)
+    frames = None
+    if args.workload == "uc2cls":
+        # the cached detectors are CLASSIFIER hops (K0c split + K4-T on the uncached tuples): the
+        # dog query's breed (C=120) and colour (C=10) linear heads on 64x64 nearest crops
+        n, batch, scale = 3_000_000, 1_000_000, 200
+        wd = workload("cfg2", n=n)
+        w = wd
+        w.preds = [wd.preds[1], wd.preds[2]]
+        frames = wd.frames(device="cuda")
+        detectors = "breed (C=120) + colour (C=10) linear heads on 64x64 nearest crops"
+    else:
+        n, batch, scale, units = 15_000_000, 1_000_000, 1000, 1024
+        w = workload("uc2", n=n)
+        for p in w.preds:  # expensive detectors: the UDF cost, not the routing overhead, must dominate
+            p["units"], p["declared_cost"] = units, float(units)
+        detectors = "2 HASH detectors (1024 rounds, sel 0.5)"
     t = w.tuples(device="cuda")
     ranges = [(1000 * scale, 7000 * scale), (8000 * scale, 14000 * scale)]
     stream = torch.cuda.current_stream()
@@ -587,7 +603,8 @@ def run_uc2(args):
     res_bb = torch.empty((batch, 4), dtype=torch.int16, device="cuda")
     times, results = {}, {}
     for policy in ("fixed", "cost", "reuse"):
-        e = H.Eddy(policy=policy, warmup_tuples=65536, max_batch_tuples=batch, max_inflight=4, stream=stream)
+        e = H.Eddy(frames=frames, policy=policy, warmup_tuples=65536, max_batch_tuples=batch, max_inflight=4,
+                   stream=stream)
         for p in w.preds:
             e.add_predicate(p)
         for k, (lo, hi) in enumerate(ranges):
@@ -626,8 +643,9 @@ def run_uc2(args):
            "value": n / (times["reuse"] / 1000.0), "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": times["reuse"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "u64", "data": "synthetic",
-           "config": {"workload": "uc2 x1000: 15M tuples, 1M-tuple batches, 2 HASH detectors (1024 rounds, sel 0.5), "
-                                  "verdicts cached for ids (1M, 7M) / (8M, 14M)",
+           "config": {"workload": f"uc2 x{scale}: {n // 1_000_000}M tuples, 1M-tuple batches, {detectors}, "
+                                  f"verdicts cached for ids ({ranges[0][0]}, {ranges[0][1]}) / ({ranges[1][0]}, "
+                                  f"{ranges[1][1]}) by hydro_cache_fill (untimed)",
                       "results": results["reuse"]},
            "policies_ms": times,
            "speedup_reuse_vs_fixed": times["fixed"] / times["reuse"],
@@ -946,9 +964,10 @@ def main():
     ap.add_argument("--impl", default="hydro", choices=["hydro", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--weights", default="grid", choices=["grid", "bf16"],
-                    help="classifier heads: fp16-exact 'grid' weights or general bf16 weights (bf16 operands)")
+                    help="classifier heads: fp16-exact 'grid' weights or general bf16 weights (N(0, 2.5e-4^2))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute", "mlp", "uc2", "hsv", "area", "concurrent", "small"],
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute", "mlp", "uc2", "uc2cls", "hsv", "area", "concurrent",
+                                                          "small"],
                     help="cfg2 = the BASELINE metric (default); rroute = K1 HBM evidence run; "
                          "mlp = cfg2 with the 12288-512-120 MLP breed head (SURVEY.md §8(f) f1, tensor roofline)")
     args = ap.parse_args()
@@ -958,7 +977,7 @@ def main():
         run_reference(args)
     elif args.workload == "rroute":
         run_route(args)
-    elif args.workload == "uc2":
+    elif args.workload in ("uc2", "uc2cls"):
         run_uc2(args)
     elif args.workload == "area":
         run_area(args)

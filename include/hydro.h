@@ -232,8 +232,12 @@ typedef struct {
                                  cache); == tuples_in without a cache                           */
   double cache_hit_rate;      /* REUSE policy: the last batch's cache hit rate (0 otherwise)   */
   int32_t operand_fp16;       /* LINEAR / MLP: 1 when the contraction runs on fp16 operands (every
-                                 weight exactly representable in fp16: the same products as bf16),
-                                 0 on bf16 operands; 0 for other kinds                            */
+                                 weight exactly representable in fp16, after the power-of-two
+                                 rescale below: the same products as bf16), 0 on bf16 operands;
+                                 0 for other kinds                                               */
+  int32_t operand_scale_log2; /* LINEAR: k of the exact rescale W' = 2^k W that makes a general
+                                 bf16 head fp16-exact (logits are multiplied by 2^-k, exactly,
+                                 before the bias); 0 when none was needed or possible             */
 } hydro_pred_stats;
 
 /* Per-batch record, available after the batch completed (hydro_batch_info). */

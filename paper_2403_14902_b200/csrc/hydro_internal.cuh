@@ -103,6 +103,7 @@ struct PredDev {
   const float* bias;        // [n_pad] (padding rows: -inf never wins; they are skipped anyway)
   int32_t n_classes, n_pad, target, crop_mode;
   int32_t a_fp16;           // 1: operands staged as fp16 (weights exactly representable), 0: bf16
+  float w_unscale;          // LINEAR: 2^-k for weights tiled as 2^k W (exact fp16 rescale), else 1
   int32_t hidden;           // MLP: hidden width (256 / 512); w_tiled = W1 (n_pad rows = hidden), bias = b2
   const uint8_t* w2_tiled;  // MLP: W2 [hidden/64 kblk][n_pad rows][128 B SW128], bf16
   const float* bias1;       // MLP: b1 [hidden]
@@ -531,4 +532,5 @@ __global__ void hydro_probe_kernel(hydro::DevState* st, const hydro::PredDev* pr
 __global__ void hydro_cache_put_kernel(uint32_t* known, uint32_t* pass, uint64_t cap, const uint64_t* ids,
                                        const uint8_t* verdicts, uint64_t n);
 __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,
-                                          int32_t k_features, int32_t to_fp16, int32_t crop_order, int32_t* inexact);
+                                          int32_t k_features, int32_t to_fp16, int32_t crop_order, int32_t* inexact,
+                                          float scale);

@@ -768,6 +768,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   const long long t_start = clock64();
   const int n_classes = pdg.n_classes, n_pad = pdg.n_pad, target = pdg.target;
   const bool fp16 = pdg.a_fp16 != 0;
+  const float unscale = pdg.w_unscale;
   const uint8_t* w_tiled = pdg.w_tiled;
   const int n_alloc = n_pad <= 32 ? 32 : (n_pad <= 64 ? 64 : 128);
   const uint32_t tmem_cols = 2u * n_alloc;
@@ -960,7 +961,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
         for (int jj = 0; jj < 16; ++jj) {
           const int c = c0 + jj;
           if (c < n_classes) {
-            const float z = __uint_as_float(v[jj]) + ctrl->bias[c];
+            const float z = __uint_as_float(v[jj]) * unscale + ctrl->bias[c];  // 2^-k: exact
             if (z > best) {  // strict: lowest index wins ties (R12)
               best = z;
               bi = c;
@@ -1586,6 +1587,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
   const long long t_start = clock64();
   const int n_classes = pdg.n_classes, n_pad = pdg.n_pad, target = pdg.target;
   const bool fp16 = pdg.a_fp16 != 0;
+  const float unscale = pdg.w_unscale;
   const uint8_t* w_tiled = pdg.w_tiled_tm;
   const uint32_t n_alloc = n_pad <= 32 ? 32u : (n_pad <= 64 ? 64u : 128u);
   const uint32_t n_acc = 2u * n_alloc <= static_cast<uint32_t>(kTmAcol0) ? 2u : 1u;  // accumulator buffers
@@ -1718,7 +1720,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
         for (int jj = 0; jj < 16; ++jj) {
           const int c = c0 + jj;
           if (c < n_classes) {
-            const float z = __uint_as_float(v[jj]) + ctrl->bias[c];
+            const float z = __uint_as_float(v[jj]) * unscale + ctrl->bias[c];  // 2^-k: exact
             if (z > best) {  // strict: lowest index wins ties (R12)
               best = z;
               bi = c;

@@ -997,13 +997,15 @@ __global__ void hydro_route_workers_kernel(WorkerRoute w, int32_t* order, double
 // MLP layer 2) -> [K/64 K-blocks][n_pad rows][128 B] with the
 // 128-byte swizzle applied (16-byte chunk c of row n stored at chunk c ^ (n & 7)), i.e. the exact
 // shared-memory image UMMA reads, so one 1-D bulk copy per stage lands it.  Rows >= C are 0.
-// to_fp16 = 1 re-encodes every weight as fp16 (identical value) and raises *inexact if any bf16
-// weight is not exactly representable in fp16 (the runtime then re-tiles as bf16).
+// to_fp16 = 1 re-encodes every weight times `scale` (a power of two) as fp16 (identical value) and
+// raises *inexact if any scaled weight is not exactly representable in fp16 (the runtime then
+// re-tiles as bf16).
 // crop_order = 1 (matrices over the 12288 crop features: linear heads, MLP W1) places feature
 // crop_pos_feature(g, p) at position p of crop row g, the order K4's converters produce;
 // crop_order = 2 uses crop_pos_feature_tm, the order of K4-T (A in tensor memory).
 __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,
-                                          int32_t k_features, int32_t to_fp16, int32_t crop_order, int32_t* inexact) {
+                                          int32_t k_features, int32_t to_fp16, int32_t crop_order, int32_t* inexact,
+                                          float scale) {
   const uint64_t total = static_cast<uint64_t>(k_features / kKBlock) * n_pad * 8;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -1030,7 +1032,8 @@ __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, i
         int bad = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float lo = __uint_as_float(u[j] << 16), hi = __uint_as_float(u[j] & 0xFFFF0000u);
+          // (scale: a power of two, so lo and hi stay the weights' exact values times 2^k)
+          const float lo = __uint_as_float(u[j] << 16) * scale, hi = __uint_as_float(u[j] & 0xFFFF0000u) * scale;
           const __half hl = __float2half_rn(lo), hh = __float2half_rn(hi);
           bad |= (__half2float(hl) != lo) | (__half2float(hh) != hi);
           u[j] = static_cast<uint32_t>(__half_as_ushort(hl)) | (static_cast<uint32_t>(__half_as_ushort(hh)) << 16);

@@ -85,6 +85,7 @@ struct PredHost {
   float* bias = nullptr;
   int n_pad = 0;
   int a_fp16 = 0;
+  int w_scale_log2 = 0;  // LINEAR: weights tiled as 2^k W (fp16-exact), logits scaled back by 2^-k
   uint8_t* w2_tiled = nullptr;  // MLP layer 2
   float* bias1 = nullptr;       // MLP layer 1 bias
   uint32_t* cache_known = nullptr;  // verdict cache (reuse-aware routing)
@@ -233,8 +234,29 @@ static int next_pow2_pad(int c) {  // n_pad: multiple of 16 >= c
 // Copies W [rows][k_features] (bf16; host or device) and re-lays it out as the swizzled K-block
 // image the classifier kernels bulk-copy (n_pad rows per K-block).  try_fp16: re-encode as fp16
 // when every weight is exactly representable (*fp16 = 1), else keep bf16 (*fp16 = 0).
+// k = 15 - floor(log2 max|w|) over a bf16 weight matrix (host or device; 0 if all zero): the
+// power-of-two rescale that puts the largest weight just below fp16's maximum exponent
+static int fp16_scale_log2(hydro_ctx* ctx, const uint16_t* w, bool on_device, size_t n) {
+  std::vector<uint16_t> h;
+  const uint16_t* src = w;
+  if (on_device) {
+    h.resize(n);
+    if (cudaMemcpy(h.data(), w, n * sizeof(uint16_t), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+    src = h.data();
+  }
+  (void)ctx;
+  int emax = -1000;
+  for (size_t i = 0; i < n; ++i) {
+    const uint32_t e = (src[i] >> 7) & 0xFFu;
+    if ((src[i] & 0x7FFFu) == 0 || e == 0 || e == 0xFFu) continue;  // zeros, subnormals, inf / NaN
+    emax = std::max(emax, static_cast<int>(e) - 127);
+  }
+  return emax == -1000 ? 0 : 15 - emax;
+}
+
 static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_device, int rows, int n_pad,
-                                 int k_features, bool try_fp16, uint8_t** out, int* fp16, bool tm_order);
+                                 int k_features, bool try_fp16, uint8_t** out, int* fp16, bool tm_order,
+                                 float scale = 1.0f);
 
 // ------------------------------------------------------------------------------------------
 
@@ -449,10 +471,32 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
     hydro_status st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, C, ph.n_pad, kFeatures, true,
                                    &ph.w_tiled, &ph.a_fp16, false);
     if (st != HYDRO_OK) return st;
-    if (d->crop_mode == HYDRO_CROP_NEAREST) {  // K4-T's copy (same operand type: exactness is per weight)
+    const char* no_scale = getenv("HYDRO_NO_FP16_SCALE");  // test hook: keep general heads on bf16 operands
+    if (!ph.a_fp16 && !(no_scale && no_scale[0] == '1')) {
+      // a general bf16 head: scaled by 2^k so that its largest weight sits at the top of fp16's
+      // range, every weight is fp16-exact when the head spans <= 32 binades (products and fp32
+      // sums are then exactly 2^k times the bf16 ones; the epilogue multiplies by 2^-k)
+      const int k = fp16_scale_log2(ctx, d->weight_bf16, d->weights_on_device != 0, static_cast<size_t>(C) * kFeatures);
+      if (k != 0 && k > -100 && k < 100) {
+        uint8_t* w2 = nullptr;
+        int ok = 0;
+        st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, C, ph.n_pad, kFeatures, true, &w2, &ok, false,
+                          std::ldexp(1.0f, k));
+        if (st != HYDRO_OK) return st;
+        if (ok) {
+          cudaFree(ph.w_tiled);
+          ph.w_tiled = w2;
+          ph.a_fp16 = 1;
+          ph.w_scale_log2 = k;
+        } else {
+          cudaFree(w2);
+        }
+      }
+    }
+    if (d->crop_mode == HYDRO_CROP_NEAREST) {  // K4-T's copy (same operand type and scale)
       int fp16_tm = 0;
       st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, C, ph.n_pad, kFeatures, ph.a_fp16 != 0,
-                        &ph.w_tiled_tm, &fp16_tm, true);
+                        &ph.w_tiled_tm, &fp16_tm, true, std::ldexp(1.0f, ph.w_scale_log2));
       if (st != HYDRO_OK) return st;
     }
     CU(cudaMalloc(&ph.bias, sizeof(float) * HYDRO_MAX_CLASSES));
@@ -473,7 +517,8 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
 }  // extern "C"
 
 static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_device, int rows, int n_pad,
-                                 int k_features, bool try_fp16, uint8_t** out, int* fp16, bool tm_order) {
+                                 int k_features, bool try_fp16, uint8_t** out, int* fp16, bool tm_order,
+                                 float scale) {
   const size_t wbytes = static_cast<size_t>(rows) * k_features * 2;
   uint16_t* wdev = nullptr;
   CU(cudaMalloc(&wdev, wbytes));
@@ -483,7 +528,7 @@ static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_devi
   int32_t* inexact = reinterpret_cast<int32_t*>(ctx->zero_word + 1);
   int32_t bad = 1;
   if (try_fp16) {
-    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 1, k_features == kFeatures ? (tm_order ? 2 : 1) : 0, inexact);
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 1, k_features == kFeatures ? (tm_order ? 2 : 1) : 0, inexact, scale);
     ctx->launches += 1;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(&bad, inexact, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -491,7 +536,7 @@ static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_devi
   }
   *fp16 = bad ? 0 : 1;
   if (bad) {
-    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 0, k_features == kFeatures ? (tm_order ? 2 : 1) : 0, inexact);
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 0, k_features == kFeatures ? (tm_order ? 2 : 1) : 0, inexact, scale);
     ctx->launches += 1;
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(ctx->stream));
@@ -634,6 +679,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
     q.target = d.target;
     q.crop_mode = d.crop_mode;
     q.a_fp16 = ctx->preds[k].a_fp16;
+    q.w_unscale = std::ldexp(1.0f, -ctx->preds[k].w_scale_log2);
     q.hidden = d.hidden;
     q.w2_tiled = ctx->preds[k].w2_tiled;
     q.bias1 = ctx->preds[k].bias1;
@@ -1184,6 +1230,7 @@ hydro_status hydro_get_stats(hydro_ctx* ctx, int32_t k, hydro_pred_stats* out) {
   out->tuples_computed = static_cast<int64_t>(h.tot_comp[k]);
   out->cache_hit_rate = h.hit[k];
   out->operand_fp16 = ctx->preds[k].a_fp16;
+  out->operand_scale_log2 = ctx->preds[k].w_scale_log2;
   return HYDRO_OK;
 }
 

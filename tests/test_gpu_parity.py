@@ -56,20 +56,24 @@ def test_cfg1_static_two_hash_predicates_exact():
 
 # ------------------------------------------------------------------------------ classifier
 
-@pytest.mark.parametrize("weights", ["grid", "bf16"])
+@pytest.mark.parametrize("weights", ["grid", "bf16", "bf16-operands"])
 @pytest.mark.parametrize("pred_index", [1, 2])
-def test_linear_crops_logits_verdicts(pred_index, weights):
+def test_linear_crops_logits_verdicts(pred_index, weights, monkeypatch):
     """Both linear heads of the dog query, over 700 tuples (6 M-tiles, ragged tail): crops bit-exact,
     logits within 1e-2 of the f64 oracle, every verdict equal (every margin >= 0.05 by construction).
     weights="bf16": general bf16 weights (N(0, 2.5e-4^2)), some not
-    fp16-representable, so K4 runs its bf16-operand path (a_fp16 = 0)."""
-    w = workload("cfg2", small=True, n=6000, weights=weights)
+    fp16-representable: the runtime tiles them as 2^k W (fp16-exact) and K4 scales the logits by
+    2^-k; "bf16-operands": the same heads with that rescale disabled, so K4 runs its bf16-operand
+    path (a_fp16 = 0)."""
+    if weights == "bf16-operands":
+        monkeypatch.setenv("HYDRO_NO_FP16_SCALE", "1")
+    w = workload("cfg2", small=True, n=6000, weights=weights.split("-")[0])
     frames = w.frames()
     n = 700  # 6 M-tiles, ragged tail
     t = w.tuples(n=n)
     p = w.preds[pred_index]
     wf = p["weight"].float()
-    assert (wf != wf.half().float()).any() == (weights == "bf16")  # which operand path K4 must take
+    assert (wf != wf.half().float()).any() == (weights != "grid")  # which operand path K4 must take
     e = make_eddy(w, frames.cuda(), policy="fixed", warmup=0)
     td = t.to("cuda")
     C = p["n_classes"]
@@ -77,7 +81,9 @@ def test_linear_crops_logits_verdicts(pred_index, weights):
     crops = torch.zeros((n, O.K_FEATURES), dtype=torch.int16, device="cuda")
     verdict = torch.zeros(n, dtype=torch.uint8, device="cuda")
     e.debug_linear(pred_index, td, logits, crops, verdict)
-    assert e.stats(pred_index)["operand_fp16"] == (1 if weights == "grid" else 0)
+    st = e.stats(pred_index)
+    assert st["operand_fp16"] == (0 if weights == "bf16-operands" else 1)
+    assert (st["operand_scale_log2"] != 0) == (weights == "bf16"), st["operand_scale_log2"]
     tup = O.as_numpy_tuples(t)
     fr = frames.numpy()
     ref_crop = O.crop_nearest(fr, tup["frame_id"], tup["bbox"]).reshape(n, -1)
