@@ -627,6 +627,9 @@ __global__ void __launch_bounds__(kRouteThreads, kCompact ? 2 : HYDRO_K1_MINB) h
 #ifndef HYDRO_K2_MINB
 #define HYDRO_K2_MINB 4  // 64 registers: 4 CTAs per SM with the first segment preloaded (measured best of 1, 3, 4, 5, 6)
 #endif
+#ifndef HYDRO_K2_DENSE_DIV
+#define HYDRO_K2_DENSE_DIV 10  // emit reads whole row columns once >= 1 in HYDRO_K2_DENSE_DIV positions survive
+#endif
 __global__ void __launch_bounds__(kRouteThreads, HYDRO_K2_MINB) hydro_compact_kernel(CompactParams p) {
   __shared__ uint32_t s_red[kRouteThreads / 32];
   __shared__ int32_t s_work, s_emit;
@@ -705,7 +708,8 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K2_MINB) hydro_compact_ke
   uint64_t sid[kRouteItems], sbb[kRouteItems];
   auto dense_seg = [&](uint32_t sg, uint32_t total) {
     const uint32_t q0 = sg * kRouteTile + tid * kRouteItems;
-    return emit && !list_in && total * 10u >= static_cast<uint32_t>(kRouteTile) && q0 + kRouteItems <= count &&
+    return emit && !list_in && total * static_cast<uint32_t>(HYDRO_K2_DENSE_DIV) >= static_cast<uint32_t>(kRouteTile) &&
+           q0 + kRouteItems <= count &&
            ((reinterpret_cast<uintptr_t>(p.id + base + q0) | reinterpret_cast<uintptr_t>(p.bbox + base + q0)) & 15u) == 0u;
   };
   auto load_dense = [&](uint32_t sg) {
