@@ -234,6 +234,19 @@ struct CompactParams {
   const uint64_t* bbox;
   DevState* st;
 };
+// K1F (fused route + emit for chains without classifiers): K1's inputs, K2's emit outputs and the
+// look-back state (tile_status[ntiles] then tile_counter, zeroed before every launch)
+constexpr int kFusedMaxRun = 4;
+struct FusedParams {
+  RouteParams r;
+  uint64_t* out_ids;
+  uint64_t* out_bbox;
+  uint32_t* out_pos;
+  uint32_t* emit_count;
+  const uint32_t* emit_offset;
+  unsigned long long* tile_status;
+  uint32_t* tile_counter;
+};
 // concurrent-worker router (hydro_route_workers): each worker's device state and SM count
 struct WorkerRoute {
   const DevState* st[kMaxPred];
@@ -513,6 +526,9 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
 
 // kernels (defined in k_route.cu / k_classifier.cu), launched by runtime.cu
 void hydro_route_launch(const hydro::RouteParams& r, int grid, cudaStream_t stream, bool compact);
+void hydro_route_emit_launch(const hydro::FusedParams& f, int grid, cudaStream_t stream);
+int hydro_route_emit_occupancy();
+int hydro_route_emit_tile();
 int hydro_route_occupancy(bool compact);
 __global__ void hydro_compact_kernel(hydro::CompactParams p);
 cudaError_t hydro_classifier_configure();

@@ -820,6 +820,248 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K2_MINB) hydro_compact_ke
 }
 
 // ------------------------------------------------------------------------------------------
+// K1F: the whole chain of a context without classifiers (LABEL_EQ / HASH predicates, range input,
+// no verdict caches) in ONE pass: evaluate the run in the device order, then emit the survivors'
+// (id, bbox) rows directly (eager materialization) at the offset given by a
+// single-pass decoupled look-back over 2048-position tiles taken in increasing order from an
+// atomic counter (a tile publishes its survivor count before it looks back, so it never waits on
+// a tile that has not started).  Replaces K1 + K2 for such chains: the ids are read once (K2 used
+// to re-read the id and bbox columns to emit), and only the survivors' bboxes are gathered.
+// Statistics as K1's lean path (in / pass / computed per predicate, dense-equivalent cycles).
+constexpr unsigned long long kLbAggregate = 1ull << 62, kLbPrefix = 2ull << 62, kLbFlags = 3ull << 62;
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+#ifndef HYDRO_K1F_MINB
+#define HYDRO_K1F_MINB 4
+#endif
+#ifndef HYDRO_K1F_ITEMS
+#define HYDRO_K1F_ITEMS 8
+#endif
+constexpr int kFItems = HYDRO_K1F_ITEMS;           // positions per thread
+constexpr int kFTile = kRouteThreads * kFItems;     // positions per tile
+__global__ void __launch_bounds__(kRouteThreads, HYDRO_K1F_MINB) hydro_route_emit_kernel(FusedParams f) {
+  const RouteParams& p = f.r;
+  __shared__ PredDev s_pred[kMaxPred];
+  __shared__ int32_t s_pid[kMaxPred];
+  __shared__ uint32_t s_wcnt[kRouteThreads / 32];
+  __shared__ uint32_t s_tile, s_excl;
+  __shared__ unsigned long long s_stat[kRouteThreads / 32][kFusedMaxRun][3];  // in, pass, cost per warp
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  DevState* st = p.st;
+  const int P = st->n_pred;
+  if (tid < P) {
+    s_pid[tid] = st->order[tid];
+    s_pred[tid] = p.preds[st->order[tid]];
+  }
+  __syncthreads();
+  bool need_label = false, need_id = false;
+  for (int r = 0; r < P; ++r) {
+    if (s_pred[r].kind == kHash) need_id = true;
+    else need_label = true;
+  }
+  const uint32_t count = p.range_n, base = p.range_base;
+  const uint32_t ntiles = (count + kFTile - 1) / kFTile;
+  const uint32_t emit_off = f.emit_offset ? *f.emit_offset : 0u;
+  const bool lab_aligned = ((reinterpret_cast<uintptr_t>(p.label + base)) & 15u) == 0;
+  const bool id_aligned = ((reinterpret_cast<uintptr_t>(p.id + base)) & 15u) == 0;
+  // statistics: per warp in shared memory (lane 0 adds the warp's sums after each predicate)
+  if (lane == 0)
+    for (int r = 0; r < kFusedMaxRun; ++r) s_stat[warp][r][0] = s_stat[warp][r][1] = s_stat[warp][r][2] = 0;
+
+  uint32_t it_k = 0;
+  while (true) {
+#ifdef HYDRO_K1F_DYNAMIC
+    if (tid == 0) s_tile = atomicAdd(f.tile_counter, 1u);
+    __syncthreads();
+    const uint32_t t = s_tile;
+#else
+    // static round-robin tiles: every CTA is co-resident (grid = occupancy x SMs) and walks its
+    // tiles in increasing order, so a tile's predecessors always make progress
+    const uint32_t t = blockIdx.x + it_k * gridDim.x;
+    ++it_k;
+#endif
+    if (t >= ntiles) break;
+    const uint32_t p0 = t * kFTile + tid * kFItems;
+    const uint32_t avail = p0 < count ? min(count - p0, static_cast<uint32_t>(kFItems)) : 0u;
+    const bool full = avail == static_cast<uint32_t>(kFItems);
+    uint32_t labs[kFItems / 2];
+#pragma unroll
+    for (int j = 0; j < kFItems / 2; ++j) labs[j] = 0u;
+    uint64_t ids[kFItems];
+    if (need_label) {
+      if (full && lab_aligned && kFItems == 8) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.label + base + p0));
+        labs[0] = v.x; labs[1] = v.y; labs[kFItems / 2 - 2] = v.z; labs[kFItems / 2 - 1] = v.w;
+      } else if (full && lab_aligned && kFItems == 4) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p.label + base + p0));
+        labs[0] = v.x; labs[1] = v.y;
+      } else {
+#pragma unroll
+        for (int j = 0; j < kFItems; ++j)
+          if (static_cast<uint32_t>(j) < avail)
+            labs[j >> 1] |= static_cast<uint32_t>(__ldg(p.label + base + p0 + j)) << (16 * (j & 1));
+      }
+    }
+    if (need_id && full && id_aligned) {
+      const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p.id + base + p0);
+#pragma unroll
+      for (int j = 0; j < kFItems / 2; ++j) {
+        const ulonglong2 v = __ldg(q + j);
+        ids[2 * j] = v.x;
+        ids[2 * j + 1] = v.y;
+      }
+    } else if (need_id) {
+#pragma unroll
+      for (int j = 0; j < kFItems; ++j)
+        ids[j] = static_cast<uint32_t>(j) < avail ? __ldg(p.id + base + p0 + j) : 0ull;
+    }
+    uint32_t mask = full ? ((1u << kFItems) - 1u) : ((1u << avail) - 1u);
+    for (int r = 0; r < P; ++r) {
+      const PredDev& pd = s_pred[r];
+      const uint32_t in_mask = mask;
+      const long long c0 = clock64();
+      if (pd.kind == kLabelEq) {
+        const uint32_t want = static_cast<uint32_t>(pd.label_value) & 0xFFFFu;
+#pragma unroll
+        for (int j = 0; j < kFItems; ++j)
+          if (((labs[j >> 1] >> (16 * (j & 1))) & 0xFFFFu) != want) mask &= ~(1u << j);
+      } else {  // HASH, uniform units, all positions branch-free
+        uint32_t hv[kFItems];
+#pragma unroll
+        for (int j = 0; j < kFItems; ++j) hv[j] = static_cast<uint32_t>(splitmix64(ids[j] ^ pd.seed) >> 32);
+        for (int rr = 0; rr < pd.units; ++rr) {
+#pragma unroll
+          for (int j = 0; j < kFItems; ++j) hv[j] = fmix32(hv[j] + static_cast<uint32_t>(rr));
+        }
+        uint32_t fail = 0;
+#pragma unroll
+        for (int j = 0; j < kFItems; ++j) {
+          const uint64_t T = (ids[j] >= pd.drift_id) ? pd.thr1 : pd.thr0;
+          fail |= (static_cast<uint64_t>(hv[j]) < T ? 0u : 1u) << j;
+        }
+        mask &= ~fail;
+      }
+      const long long c1 = clock64();
+      if (p.collect_stats) {
+        const uint32_t a_in = __reduce_add_sync(kFull, __popc(in_mask));
+        const uint32_t a_pass = __reduce_add_sync(kFull, __popc(mask));
+        if (lane == 0) {  // dense-equivalent cost: the warp's cycles x the items it evaluated (as K1)
+          s_stat[warp][r][0] += a_in;
+          s_stat[warp][r][1] += a_pass;
+          s_stat[warp][r][2] += static_cast<unsigned long long>(c1 - c0) * a_in;
+        }
+      }
+    }
+    // the survivors' rows: bbox (and id when no HASH loaded it) gathered now, before the look-back
+    uint64_t bbs[kFItems];
+#pragma unroll
+    for (int j = 0; j < kFItems; ++j) {
+      bbs[j] = 0;
+      if ((mask >> j) & 1u) {
+        bbs[j] = __ldg(p.bbox + base + p0 + j);
+        if (!need_id) ids[j] = __ldg(p.id + base + p0 + j);
+      }
+    }
+    // tile scan: thread -> warp -> tile
+    const uint32_t c = __popc(mask);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wcnt[warp] = x;
+    __syncthreads();
+    uint32_t wexcl = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kRouteThreads / 32; ++w) {
+      const uint32_t v = s_wcnt[w];
+      wexcl += w < warp ? v : 0u;
+      total += v;
+    }
+    if (warp == 0) {  // decoupled look-back
+      if (lane == 0) st_relaxed_u64(f.tile_status + t, (t == 0 ? kLbPrefix : kLbAggregate) | total);
+      uint32_t excl = 0;
+      if (t > 0) {
+        int j = static_cast<int>(t) - 1;
+        while (true) {
+          const int idx = j - lane;
+          unsigned long long v = idx >= 0 ? ld_relaxed_u64(f.tile_status + idx) : kLbPrefix;
+          while (__any_sync(kFull, (v & kLbFlags) == 0)) {
+            if ((v & kLbFlags) == 0) v = ld_relaxed_u64(f.tile_status + idx);
+          }
+          const uint32_t pb = __ballot_sync(kFull, (v & kLbFlags) == kLbPrefix);
+          if (pb) {
+            const int k = __ffs(pb) - 1;  // the nearest predecessor with an inclusive prefix
+            excl += __reduce_add_sync(kFull, lane <= k ? static_cast<uint32_t>(v) : 0u);
+            break;
+          }
+          excl += __reduce_add_sync(kFull, static_cast<uint32_t>(v));
+          j -= 32;
+        }
+        if (lane == 0) st_relaxed_u64(f.tile_status + t, kLbPrefix | (excl + total));
+      }
+      if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    uint32_t pos = emit_off + s_excl + wexcl + (x - c);
+    if (mask) {
+#pragma unroll
+      for (int j = 0; j < kFItems; ++j) {
+        if ((mask >> j) & 1u) {
+          f.out_ids[pos] = ids[j];
+          f.out_bbox[pos] = bbs[j];
+          if (f.out_pos) f.out_pos[pos] = base + p0 + j;
+          ++pos;
+        }
+      }
+    }
+    if (t == ntiles - 1 && tid == 0) *f.emit_count = emit_off + s_excl + total;
+    __syncthreads();  // s_tile / s_wcnt / s_excl are rewritten by the next tile
+  }
+  if (ntiles == 0 && blockIdx.x == 0 && tid == 0) *f.emit_count = emit_off;
+  if (p.collect_stats) {
+    __syncthreads();
+    if (tid < P) {
+      unsigned long long in = 0, pass = 0, cs = 0;
+#pragma unroll
+      for (int w = 0; w < kRouteThreads / 32; ++w) {
+        in += s_stat[w][tid][0];
+        pass += s_stat[w][tid][1];
+        cs += s_stat[w][tid][2];
+      }
+      const int k = s_pid[tid];
+      if (in) {
+        atomicAdd(&st->d_in[k], in);
+        atomicAdd(&st->d_pass[k], pass);
+        atomicAdd(&st->d_cost[k], cs);
+        atomicAdd(&st->d_comp[k], in);
+      }
+    }
+  }
+}
+
+void hydro_route_emit_launch(const FusedParams& f, int grid, cudaStream_t stream) {
+  hydro_route_emit_kernel<<<grid, kRouteThreads, 0, stream>>>(f);
+}
+
+int hydro_route_emit_tile() { return kFTile; }
+
+int hydro_route_emit_occupancy() {
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hydro_route_emit_kernel, kRouteThreads, 0);
+  return occ < 1 ? 1 : occ;
+}
+
+// ------------------------------------------------------------------------------------------
 // Verdict cache (reuse-aware routing).  K0 probe: for every predicate with a
 // cache, the number of the batch's tuple ids whose verdict is cached ("the router algorithms first
 // check the potential cache hit rate for a batch") -> d_hit; K5 mode 8 turns it

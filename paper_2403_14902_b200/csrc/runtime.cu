@@ -63,6 +63,11 @@ static const GreenApi& green_api() {
   return g;
 }
 
+static bool getenv_flag(const char* name) {
+  const char* e = getenv(name);
+  return e && e[0] == '1';
+}
+
 static hydro_status set_err(hydro_status s, const std::string& msg) {
   g_last_error = msg;
   return s;
@@ -145,6 +150,7 @@ struct hydro_ctx {
   uint64_t bits_stride = 0;
   uint32_t* warm_bits = nullptr;
   uint32_t* seg_counts = nullptr;  // [max_segs] segment counts, then [8 * max_segs] warp counts
+  unsigned long long* fused_status = nullptr;  // K1F look-back: [max_segs] tile words, then the tile counter
   uint64_t max_segs = 0;
   uint32_t* warm_and = nullptr;
   uint32_t* bal_chunks = nullptr;  // K6 (data-aware balance): chunk cost estimates
@@ -724,6 +730,7 @@ static hydro_status freeze(hydro_ctx* ctx) {
   ctx->max_segs = (max_segs + 3) & ~3ull;  // warp counts follow, 16-byte aligned
   CU(cudaMalloc(&ctx->seg_counts, sizeof(uint32_t) * ctx->max_segs * 9));
   CU(cudaMemset(ctx->seg_counts, 0, sizeof(uint32_t) * ctx->max_segs * 9));
+  CU(cudaMalloc(&ctx->fused_status, sizeof(unsigned long long) * (8 * ctx->max_segs + 1)));  // tiles >= 256 positions
   CU(cudaMalloc(&ctx->warm_and, sizeof(uint32_t) * ctx->bits_stride));
   if (ctx->cfg.balance == HYDRO_BALANCE_DATA_AWARE && ctx->has_area) {
     CU(cudaMalloc(&ctx->bal_chunks, sizeof(uint32_t) * ((maxb + 31) / 32 + 1)));
@@ -826,6 +833,20 @@ static int route_grid(hydro_ctx* ctx, uint64_t positions) {
 static hydro_status launch_route(hydro_ctx* ctx, const RouteParams& r, uint64_t max_positions) {
   const int grid = route_grid(ctx, max_positions);
   return timed_launch(ctx, 0, [&] { hydro_route_launch(r, grid, ctx->stream, ctx->k1_compact); });
+}
+
+// K1F applies to a chain without classifiers: 1..4 LABEL_EQ / uniform-units HASH predicates
+// (units below the compacted-HASH threshold), no verdict cache, no selection input
+static bool fused_chain_ok(const hydro_ctx* ctx, const hydro_tuples* t) {
+  const int P = static_cast<int>(ctx->preds.size());
+  if (P < 1 || P > kFusedMaxRun || t->sel || getenv_flag("HYDRO_NO_K1F")) return false;
+  for (const PredHost& ph : ctx->preds) {
+    const hydro_predicate_desc& d = ph.desc;
+    if (ph.cache_known) return false;
+    if (d.kind == HYDRO_PRED_LABEL_EQ) continue;
+    if (d.kind != HYDRO_PRED_HASH || d.units_per_area > 0 || d.units >= kCompactUnits) return false;
+  }
+  return true;
 }
 
 static hydro_status launch_compact(hydro_ctx* ctx, const CompactParams& c, uint64_t max_positions) {
@@ -1057,7 +1078,34 @@ hydro_status hydro_submit_batch(hydro_ctx* ctx, const hydro_tuples* t, int64_t* 
   for (int k = 0; k < P; ++k) n_lin += is_classifier(ctx->preds[k].desc.kind) ? 1 : 0;
   const int n_cheap = P - n_lin;
   const int slots = (P == 0 || n_lin == 0) ? 1 : std::min(P, n_lin + std::min(n_cheap, n_lin + 1));
-  for (int h = 0; h < slots; ++h) {
+  // K1F when the batch's tiles fit one wave of co-resident CTAs: each CTA then runs one
+  // load -> evaluate -> gather -> look-back -> write chain (measured faster than K1 + K2 there);
+  // over several waves those chains serialize per CTA and K1 + K2 stream better
+  static const int k1f_occ = hydro_route_emit_occupancy();
+  const bool fused = n_lin == 0 && fused_chain_ok(ctx, t) &&
+                     (static_cast<uint64_t>(rest_n) + hydro_route_emit_tile() - 1) / hydro_route_emit_tile() <=
+                         static_cast<uint64_t>(k1f_occ) * ctx->num_sms;
+  if (fused) {  // K1F: the whole cheap chain and the emit in one pass (decoupled look-back)
+    FusedParams f{};
+    f.r = route_base(ctx, id, fr, bb, lab);
+    f.r.dispatch = 1;
+    f.r.hop = 0;
+    f.r.range_base = rest_base;
+    f.r.range_n = rest_n;
+    f.out_ids = sl.out_ids;
+    f.out_bbox = sl.out_bbox;
+    f.out_pos = sl.out_pos;
+    f.emit_count = &sl.rec->total_count;
+    f.emit_offset = &sl.rec->warm_count;
+    f.tile_status = ctx->fused_status;
+    f.tile_counter = reinterpret_cast<uint32_t*>(ctx->fused_status + 8 * ctx->max_segs);
+    const uint64_t tiles = (static_cast<uint64_t>(rest_n) + hydro_route_emit_tile() - 1) / hydro_route_emit_tile();
+    CU(cudaMemsetAsync(ctx->fused_status, 0, sizeof(unsigned long long) * (tiles + 1), ctx->stream));
+    CU(cudaMemsetAsync(f.tile_counter, 0, sizeof(uint32_t), ctx->stream));
+    const int grid = static_cast<int>(std::max<uint64_t>(1, tiles));  // one tile per CTA, all co-resident
+    if ((s = timed_launch(ctx, 0, [&] { hydro_route_emit_launch(f, grid, ctx->stream); })) != HYDRO_OK) return s;
+  }
+  for (int h = 0; h < (fused ? 0 : slots); ++h) {
     RouteParams r = route_base(ctx, id, fr, bb, lab);
     r.dispatch = 1;
     r.hop = h;
@@ -1468,6 +1516,7 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
   cudaFree(ctx->cache_pos);
   cudaFree(ctx->cache_count);
   cudaFree(ctx->seg_counts);
+  cudaFree(ctx->fused_status);
   cudaFree(ctx->warm_and);
   cudaFree(ctx->bal_chunks);
   cudaFree(ctx->bal_bounds);
