@@ -120,6 +120,7 @@ struct DevState {
   int32_t n_pred;
   int32_t policy;
   int32_t cost_source;
+  int32_t pair_a, pair_b;             // fused linear pair (K4-T, one contraction for both heads); -1: none
   int32_t pad0;
   double gamma;
   double prior;
@@ -149,14 +150,27 @@ struct DevState {
   unsigned int kt_done[8];
 };
 
-// Hop schedule: the evaluator hops of an order are its LINEAR positions and the starts of its
-// maximal runs of cheap predicates; slot i of the per-batch chain runs hop sched[i].  The host
-// launches only as many slots as any order of the context can need.
-__host__ __device__ inline void build_sched(const int32_t* kind, const int32_t* order, int P, int32_t* sched) {
+// Fused pair hop: order positions h and h + 1 hold the context's two pairable linear heads (same
+// nearest crop, one K4-T contraction evaluates both).
+__host__ __device__ inline bool is_pair_hop(const int32_t* order, int P, int h, int pa, int pb) {
+  return pa >= 0 && h >= 0 && h + 1 < P &&
+         ((order[h] == pa && order[h + 1] == pb) || (order[h] == pb && order[h + 1] == pa));
+}
+
+// Hop schedule: the evaluator hops of an order are its classifier positions (a fused pair counts
+// once) and the starts of its maximal runs of cheap predicates; slot i of the per-batch chain runs
+// hop sched[i].  The host launches only as many slots as any order of the context can need.
+__host__ __device__ inline void build_sched(const int32_t* kind, const int32_t* order, int P, int32_t* sched,
+                                            int pa = -1, int pb = -1) {
   int n = 0;
   if (P == 0) sched[n++] = 0;
-  for (int h = 0; h < P; ++h)
-    if (is_classifier(kind[order[h]]) || h == 0 || is_classifier(kind[order[h - 1]])) sched[n++] = h;
+  for (int h = 0; h < P; ++h) {
+    if (is_classifier(kind[order[h]])) {
+      if (h == 0 || !is_pair_hop(order, P, h - 1, pa, pb)) sched[n++] = h;  // (the 2nd of a pair: no hop)
+    } else if (h == 0 || is_classifier(kind[order[h - 1]])) {
+      sched[n++] = h;
+    }
+  }
   for (; n < kMaxPred; ++n) sched[n] = -1;
 }
 
@@ -299,6 +313,12 @@ struct ClsParams {
   uint32_t* cache_pos;      // ... their positions in the hop input (verdict bits) ...
   uint32_t* cache_count;    // ... and their number; nullptr: the context has no classifier cache
   int32_t force_fill;       // hydro_cache_fill: record every computed verdict
+  // fused linear pair (DevState pair_a / pair_b): both heads' weights tiled into one B operand
+  // (pair_a's rows [0, pair_npa), pair_b's after), their biases, per-head logit scales
+  const uint8_t* pair_w_tiled;
+  const float* pair_bias;   // [pair_n_pad]
+  int32_t pair_npa, pair_n_pad;
+  float pair_unscale_a, pair_unscale_b;
 };
 
 // ------------------------------------------------------------------------------------------

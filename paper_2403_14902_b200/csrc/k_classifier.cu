@@ -1288,7 +1288,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
 // stream as hydro_classifier_kernel, but the A operand lives in TENSOR MEMORY.  Converter warps
 // write their crop pixels with tcgen05.st (16x256b: thread t owns TMEM lanes t/4 and t/4 + 8 of
 // its 16-row band, 2 columns per 8-column repetition) into a 2-group TMEM ring (columns
-// [kTmAcol0, kTmAcol0 + 2 * 96)); the MMA reads A from TMEM (tcgen05.mma ... [d], [a], b_desc),
+// [a_col0, 512), 3-4 crop rows of 96 columns); the MMA reads A from TMEM (tcgen05.mma ... [d], [a], b_desc),
 // so neither the A stores nor the tensor core's A reads touch shared memory, and the 96 KB the
 // shared-memory A ring took become crop-row staging: each converter warp owns a 22 KB ring of
 // "units" (one crop row of its 16 tuples, segments packed back to back) and stages up to 3 units
@@ -1296,13 +1296,8 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
 // Converter warp cu owns tile rows [32*((6+cu)%4) + 16*(cu/4), +16) (the TMEM lane quarter of
 // warp 6+cu).  Thread t handles local tuples a = t/4 and a + 8, output pixels dx = 4k + (t%4)
 // (k = 0..15) of every crop row; K order inside a crop row = crop_pos_feature_tm.
-#ifndef HYDRO_TM_ASLOTS
-#define HYDRO_TM_ASLOTS 4
-#endif
-constexpr int kTmASlots = HYDRO_TM_ASLOTS;                 // crop rows of A in TMEM (2 or 4)
-constexpr int kTmAcol0 = 512 - kTmASlots * 96;             // first TMEM column of the A ring
-// accumulator buffers below kTmAcol0: two when they fit (N <= 64, or a 2-slot A ring), else one
-// (N = 128 with 4 A slots: the next tile's first MMA waits for the epilogue's tcgen05.ld)
+constexpr int kTmASlots = 4;  // crop rows of A in TMEM at most: 4 when the accumulators fit in 128
+                               // columns (N <= 128, or two buffers of N <= 64), else 3 (a fused pair)
 constexpr int kTmGroupCols = 96;   // one crop row of A: 192 fp16 = 96 32-bit columns per lane
 #ifndef HYDRO_TM_SLOTS
 #define HYDRO_TM_SLOTS 3
@@ -1321,9 +1316,10 @@ struct TmCtrl {
   uint64_t tfull[2], tempty[2];
   uint32_t tmem_base;
   uint32_t pad;
-  float bias[HYDRO_MAX_CLASSES];
+  float bias[144];
 };
-constexpr int kTmBRingBytes = kTmBStages * 16384;
+constexpr int kTmBStageBytes = 144 * 128;  // one weight K-block of N <= 144 rows (a fused pair: 128 + 16)
+constexpr int kTmBRingBytes = kTmBStages * kTmBStageBytes;
 constexpr int kTmCtrlBytes = (static_cast<int>(sizeof(TmCtrl)) + 127) & ~127;
 // per-warp staging ring (16-byte multiple) + 64 B of slack at the end of the region (reads of the
 // word after a pixel, and of stale offsets in invalid rows, stay inside the allocation)
@@ -1404,7 +1400,7 @@ template <bool kDbg, bool kWide>
 __device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl, uint32_t lim, uint32_t pos0, int cu,
                                                 int lane, uint32_t ring, uint32_t tmem_base, uint32_t row_pitch,
                                                 bool fp16, const RowMeta& mm, uint32_t band, uint32_t& gg,
-                                                uint32_t& stg_par) {
+                                                uint32_t& stg_par, uint32_t a_slots, uint32_t a_col0) {
   const uint8_t* frames = p.frames;
   const int a = lane >> 2, t0 = lane & 3;
   // unit layout: the segments of local tuples 0..15 back to back (lane l < 16 holds tuple l)
@@ -1485,7 +1481,7 @@ __device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl
     stage_unit(static_cast<int>(k), slot_stage);
     slot_stage = slot_stage + 1 == nslot ? 0 : slot_stage + 1;
   }
-  const uint32_t lane_addr = tmem_base + (band << 16) + kTmAcol0;
+  const uint32_t lane_addr = tmem_base + (band << 16) + a_col0;
   for (int g = 0; g < kGroups; ++g, ++gg) {
     stage_unit(g + static_cast<int>(depth), slot_stage);
     slot_stage = slot_stage + 1 == nslot ? 0 : slot_stage + 1;
@@ -1496,8 +1492,8 @@ __device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl
       mbar_wait(&ctrl->stg[cu][slot_use], (stg_par >> slot_use) & 1u);  // unit g's bulk copies landed
       stg_par ^= 1u << slot_use;
     }
-    const uint32_t sa = gg % kTmASlots, aph = (gg / kTmASlots) & 1u;
-    mbar_wait(&ctrl->empty_a[sa], aph ^ 1u);  // the MMA has consumed group gg - kTmASlots from this slot
+    const uint32_t sa = gg % a_slots, aph = (gg / a_slots) & 1u;
+    mbar_wait(&ctrl->empty_a[sa], aph ^ 1u);  // the MMA has consumed group gg - a_slots from this slot
     tc_fence_after();
     const uint32_t unit = ring + slot_use * ubytes;
 #pragma unroll
@@ -1554,11 +1550,13 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
   const uint32_t* list_in;
   uint32_t count, base = p.range_base;
   uint32_t* bits_out;
+  int pred2 = -1;  // fused pair hop: the second head (order position h + 1)
   if (p.dispatch) {
     const int h = st->sched[p.hop];
     if (h < 0 || h >= st->n_pred) return;
     pred = st->order[h];
     if (st->kind[pred] != kLinear) return;
+    if (p.pair_w_tiled && is_pair_hop(st->order, st->n_pred, h, st->pair_a, st->pair_b)) pred2 = st->order[h + 1];
     if (h == 0) {
       list_in = p.sel0;
       count = p.sel0 ? *p.sel0_count : p.range_n;
@@ -1585,12 +1583,19 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
     return;
   }
   const long long t_start = clock64();
-  const int n_classes = pdg.n_classes, n_pad = pdg.n_pad, target = pdg.target;
+  // a fused pair hop contracts with both heads' weights at once: head pair_a in columns
+  // [0, pair_npa), head pair_b after them (one crop gather, N = pair_n_pad)
+  const bool pair = pred2 >= 0;
+  const int n_classes = pdg.n_classes, target = pdg.target;
+  const int n_pad = pair ? p.pair_n_pad : pdg.n_pad;
   const bool fp16 = pdg.a_fp16 != 0;
   const float unscale = pdg.w_unscale;
-  const uint8_t* w_tiled = pdg.w_tiled_tm;
-  const uint32_t n_alloc = n_pad <= 32 ? 32u : (n_pad <= 64 ? 64u : 128u);
-  const uint32_t n_acc = 2u * n_alloc <= static_cast<uint32_t>(kTmAcol0) ? 2u : 1u;  // accumulator buffers
+  const uint8_t* w_tiled = pair ? p.pair_w_tiled : pdg.w_tiled_tm;
+  const uint32_t n_alloc = n_pad <= 32 ? 32u : (n_pad <= 64 ? 64u : (n_pad <= 128 ? 128u : static_cast<uint32_t>(n_pad)));
+  const uint32_t n_acc = 2u * n_alloc <= 128u ? 2u : 1u;  // accumulator buffers below the A ring
+  // A ring: 4 crop rows when the accumulators fit in 128 columns, else 3
+  const uint32_t a_slots = n_acc * n_alloc <= 128u ? 4u : 3u;
+  const uint32_t a_col0 = 512u - a_slots * kTmGroupCols;
   const uint32_t b_stage_bytes = static_cast<uint32_t>(n_pad) * 128u;
   const uint32_t row_pitch = static_cast<uint32_t>(p.frame_w * 3);
 
@@ -1624,7 +1629,11 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (tid < HYDRO_MAX_CLASSES) ctrl->bias[tid] = tid < n_classes ? pdg.bias[tid] : 0.0f;
+  if (pair) {
+    if (tid < n_pad) ctrl->bias[tid] = p.pair_bias[tid];
+  } else if (tid < HYDRO_MAX_CLASSES) {
+    ctrl->bias[tid] = tid < n_classes ? pdg.bias[tid] : 0.0f;
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1640,7 +1649,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
           const uint32_t s = itb % kTmBStages, ph = (itb / kTmBStages) & 1u;
           HYDRO_PIPE_WAIT(&ctrl->empty_b[s], ph ^ 1u);
           mbar_arrive_expect_tx(&ctrl->full_b[s], b_stage_bytes);
-          bulk_g2s_hint(smem + s * 16384u, w_tiled + static_cast<uint64_t>(kb) * b_stage_bytes, b_stage_bytes,
+          bulk_g2s_hint(smem + s * kTmBStageBytes, w_tiled + static_cast<uint64_t>(kb) * b_stage_bytes, b_stage_bytes,
                         &ctrl->full_b[s], pol_w);
         }
       }
@@ -1657,16 +1666,16 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * n_alloc;
         for (int g = 0; g < kGroups; ++g, ++gg) {
-          const uint32_t sa = gg % kTmASlots;
-          HYDRO_PIPE_WAIT(&ctrl->full_a[sa], (gg / kTmASlots) & 1u);
+          const uint32_t sa = gg % a_slots;
+          HYDRO_PIPE_WAIT(&ctrl->full_a[sa], (gg / a_slots) & 1u);
           tc_fence_after();
-          const uint32_t a_col = tmem_base + kTmAcol0 + sa * kTmGroupCols;
+          const uint32_t a_col = tmem_base + a_col0 + sa * kTmGroupCols;
 #pragma unroll
           for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr, ++itb) {
             const uint32_t sb = itb % kTmBStages, bph = (itb / kTmBStages) & 1u;
             HYDRO_PIPE_WAIT(&ctrl->full_b[sb], bph);
             tc_fence_after();
-            const uint32_t b_addr = b_ring + sb * 16384u;
+            const uint32_t b_addr = b_ring + sb * static_cast<uint32_t>(kTmBStageBytes);
 #pragma unroll
             for (int kk = 0; kk < kKBlock / 16; ++kk)
               tc_mma_ts(d_tmem, a_col + (kbr * 4 + kk) * 8, desc_sw128(b_addr + kk * 32), idesc,
@@ -1692,15 +1701,22 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
           __any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes));
       if (any_wide)
         tm_convert_tile<kDbg, true>(p, ctrl, tw.lim, pos0, cu, lane, ring, tmem_base, row_pitch, fp16, mm, band, gg,
-                                    stg_par);
+                                    stg_par, a_slots, a_col0);
       else
         tm_convert_tile<kDbg, false>(p, ctrl, tw.lim, pos0, cu, lane, ring, tmem_base, row_pitch, fp16, mm, band, gg,
-                                     stg_par);
+                                     stg_par, a_slots, a_col0);
     }
   } else {
     // ===================== epilogue warps 0..3 (TMEM lane quadrant = warp)
     const int q = warp;
     uint32_t n_in = 0, n_pass = 0, tl = 0;
+    // fused pair: head pair_a in columns [0, pair_npa), pair_b after; n_p1 = survivors of the first
+    const int pnpa = p.pair_npa;
+    const int pca = pair ? p.preds[st->pair_a].n_classes : 0, pcb = pair ? p.preds[st->pair_b].n_classes : 0;
+    const int pta = pair ? p.preds[st->pair_a].target : 0, ptb = pair ? p.preds[st->pair_b].target : 0;
+    const float pua = p.pair_unscale_a, pub = p.pair_unscale_b;
+    const bool first_is_a = pair && pred == st->pair_a;
+    uint32_t n_p1 = 0;
     for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step, ++tl) {
       const uint32_t pos0 = tw.pos0(unit);
       const uint32_t acc = tl % n_acc, aph = (tl / n_acc) & 1u;
@@ -1709,30 +1725,52 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
       const int m = q * 32 + lane;
       const uint32_t pos = pos0 + m;
       const bool valid = pos < tw.lim;
-      float best = -3.402823466e38f;
-      int bi = 0;
+      float best = -3.402823466e38f, best2 = -3.402823466e38f;
+      int bi = 0, bi2 = 0;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * n_alloc;
       for (int c0 = 0; c0 < n_pad; c0 += 16) {
         uint32_t v[16];
         tc_ld_32x32b_x16(taddr + c0, v);
         tc_wait_ld();
+        if (!pair || c0 < pnpa) {  // (the single head, or pair head pair_a: columns [0, pair_npa))
+          const int nc = pair ? pca : n_classes;
+          const float us = pair ? pua : unscale;
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const int c = c0 + jj;
-          if (c < n_classes) {
-            const float z = __uint_as_float(v[jj]) * unscale + ctrl->bias[c];  // 2^-k: exact
-            if (z > best) {  // strict: lowest index wins ties (R12)
-              best = z;
-              bi = c;
+          for (int jj = 0; jj < 16; ++jj) {
+            const int c = c0 + jj;
+            if (c < nc) {
+              const float z = __uint_as_float(v[jj]) * us + ctrl->bias[c];  // 2^-k: exact
+              if (z > best) {  // strict: lowest index wins ties (R12)
+                best = z;
+                bi = c;
+              }
+              if (kDbg && p.dbg_logits && valid) p.dbg_logits[static_cast<uint64_t>(pos) * n_classes + c] = z;
             }
-            if (kDbg && p.dbg_logits && valid) p.dbg_logits[static_cast<uint64_t>(pos) * n_classes + c] = z;
+          }
+        } else {  // pair head pair_b: columns [pair_npa, pair_npa + C_b)
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const int c = c0 + jj - pnpa;
+            if (c < pcb) {
+              const float z = __uint_as_float(v[jj]) * pub + ctrl->bias[c0 + jj];
+              if (z > best2) {
+                best2 = z;
+                bi2 = c;
+              }
+            }
           }
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctrl->tempty[acc]);
-      const bool verdict = valid && (bi == target);
+      bool verdict = valid && (bi == target);
+      if (pair) {  // verdicts of pair_a and pair_b -> the order's first and second head
+        const bool va = valid && bi == pta, vb = valid && bi2 == ptb;
+        const bool v1 = first_is_a ? va : vb, v2 = first_is_a ? vb : va;
+        n_p1 += __popc(__ballot_sync(0xFFFFFFFFu, v1));
+        verdict = v1 && v2;  // the hop's survivors pass both heads
+      }
       const uint32_t bv = __ballot_sync(0xFFFFFFFFu, verdict);
       const uint32_t bvalid = __ballot_sync(0xFFFFFFFFu, valid);
       cls_emit(p, bits_out, ind, list_in, base, pos0 + q * 32, pos, valid, verdict, pdg, fill);
@@ -1741,9 +1779,18 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
       n_pass += __popc(bv);
     }
     if (p.collect_stats && lane == 0) {
-      atomicAdd(&st->d_in[pred], static_cast<unsigned long long>(n_in));
-      atomicAdd(&st->d_pass[pred], static_cast<unsigned long long>(n_pass));
-      atomicAdd(&st->d_comp[pred], static_cast<unsigned long long>(n_in));
+      if (pair) {  // as if evaluated in turn: the second head sees the first head's survivors
+        atomicAdd(&st->d_in[pred], static_cast<unsigned long long>(n_in));
+        atomicAdd(&st->d_pass[pred], static_cast<unsigned long long>(n_p1));
+        atomicAdd(&st->d_comp[pred], static_cast<unsigned long long>(n_in));
+        atomicAdd(&st->d_in[pred2], static_cast<unsigned long long>(n_p1));
+        atomicAdd(&st->d_pass[pred2], static_cast<unsigned long long>(n_pass));
+        atomicAdd(&st->d_comp[pred2], static_cast<unsigned long long>(n_p1));
+      } else {
+        atomicAdd(&st->d_in[pred], static_cast<unsigned long long>(n_in));
+        atomicAdd(&st->d_pass[pred], static_cast<unsigned long long>(n_pass));
+        atomicAdd(&st->d_comp[pred], static_cast<unsigned long long>(n_in));
+      }
     }
   }
 
@@ -1753,7 +1800,18 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
-  if (tid == 0 && p.collect_stats) atomicAdd(&st->d_cost[pred], static_cast<unsigned long long>(clock64() - t_start));
+  if (tid == 0 && p.collect_stats) {
+    const unsigned long long cyc = static_cast<unsigned long long>(clock64() - t_start);
+    if (pair) {  // the CTA's cycles split between the two heads by their share of the N columns
+      const uint32_t n_first = pred == st->pair_a ? static_cast<uint32_t>(p.pair_npa)
+                                                  : static_cast<uint32_t>(n_pad - p.pair_npa);
+      const unsigned long long c1 = cyc * n_first / static_cast<uint32_t>(n_pad);
+      atomicAdd(&st->d_cost[pred], c1);
+      atomicAdd(&st->d_cost[pred2], cyc - c1);
+    } else {
+      atomicAdd(&st->d_cost[pred], cyc);
+    }
+  }
   if (tid == 0) ktimer_end(st, 1);
 }
 

@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(kRouteThreads, HYDRO_K2_MINB) hydro_compact_ke
       } else if (k1_runs(st, h, &run)) {
         next = h + run;
       } else if (h < P && is_classifier(st->kind[st->order[h]])) {
-        next = h + 1;
+        next = h + (is_pair_hop(st->order, P, h, st->pair_a, st->pair_b) ? 2 : 1);  // a fused pair covers two
       } else {
         work = 0;
         next = 0;
@@ -1132,7 +1132,7 @@ __device__ void order_by_keys(DevState* st) {
     for (int i = 0; i < P; ++i) st->order[i] = ord[i];
   }
   for (int i = 0; i < P; ++i) st->position[st->order[i]] = i;
-  build_sched(st->kind, st->order, P, st->sched);
+  build_sched(st->kind, st->order, P, st->sched, st->pair_a, st->pair_b);
 }
 
 // mode: bit 0 = PREP (batch deltas -> batch record + pending), bit 1 = APPLY (deltas -> decayed

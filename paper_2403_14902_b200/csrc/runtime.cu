@@ -176,6 +176,10 @@ struct hydro_ctx {
   bool fixed_order_set = false;
   bool has_area = false;
   bool k4_legacy = false;
+  int pair_a = -1, pair_b = -1;   // fused linear pair (pred ids), see freeze()
+  int pair_npa = 0, pair_n_pad = 0;
+  uint8_t* pair_w_tiled = nullptr;
+  float* pair_bias = nullptr;
   uint32_t* cache_idx = nullptr;    // K0c: uncached tuples of a cached classifier hop (batch indices)
   uint32_t* cache_pos = nullptr;    //      and their hop-input positions
   uint32_t* cache_count = nullptr;  //      their number (nullptr: no classifier cache)  // HYDRO_K4_LEGACY=1: nearest heads on the shared-memory-A kernel (A/B runs)
@@ -562,6 +566,24 @@ hydro_status hydro_cache_enable(hydro_ctx* ctx, int32_t k, uint64_t id_capacity,
   if (k < 0 || k >= static_cast<int32_t>(ctx->preds.size())) return set_err(HYDRO_EINVAL, "bad pred id");
   PredHost& ph = ctx->preds[k];
   if (ph.cache_known) return set_err(HYDRO_EINVAL, "cache already enabled");
+  if (k == ctx->pair_a || k == ctx->pair_b) {  // a cached head leaves the fused pair (K0c splits its hop)
+    ctx->pair_a = ctx->pair_b = -1;
+    if (ctx->frozen) {
+      const int32_t none[2] = {-1, -1};
+      CU(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, pair_a), none, sizeof(none),
+                         cudaMemcpyHostToDevice, ctx->stream));
+      int32_t kind[kMaxPred], order[kMaxPred], sched[kMaxPred];
+      const int P = static_cast<int>(ctx->preds.size());
+      CU(cudaMemcpyAsync(order, reinterpret_cast<char*>(ctx->st) + offsetof(DevState, order), sizeof(order),
+                         cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      for (int i = 0; i < P; ++i) kind[i] = ctx->preds[i].desc.kind;
+      build_sched(kind, order, P, sched);
+      CU(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, sched), sched, sizeof(sched),
+                         cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+    }
+  }
   if (is_classifier(ph.desc.kind) && !ctx->cache_count) {  // K0c's split lists (one set: hops run in order)
     const size_t cap = static_cast<size_t>(ctx->cfg.max_batch_tuples) + 64;
     CU(cudaMalloc(&ctx->cache_idx, cap * sizeof(uint32_t)));
@@ -638,7 +660,7 @@ hydro_status hydro_set_fixed_order(hydro_ctx* ctx, const int32_t* order, int32_t
     CU(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, position), pos, sizeof(int32_t) * P, cudaMemcpyHostToDevice, ctx->stream));
     int32_t kind[kMaxPred], sched[kMaxPred];
     for (int i = 0; i < P; ++i) kind[i] = ctx->preds[i].desc.kind;
-    build_sched(kind, ctx->fixed_order, P, sched);
+    build_sched(kind, ctx->fixed_order, P, sched, ctx->pair_a, ctx->pair_b);
     CU(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, sched), sched, sizeof(sched), cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
   }
@@ -713,7 +735,45 @@ static hydro_status freeze(hydro_ctx* ctx) {
     std::stable_sort(h.order, h.order + P, [&](int a, int b) { return h.key[a] < h.key[b]; });
   }
   for (int i = 0; i < P; ++i) h.position[h.order[i]] = i;
-  build_sched(h.kind, h.order, P, h.sched);
+  // fused linear pair (K4-T evaluates both heads in one contraction when the order puts them next
+  // to each other): two nearest LINEAR heads with the same operand type, N_a + N_b <= 144, no
+  // verdict cache, K4-T in use (no AREA head, not HYDRO_K4_LEGACY / HYDRO_NO_PAIR)
+  ctx->pair_a = ctx->pair_b = -1;
+  if (!ctx->has_area && !ctx->k4_legacy && !getenv_flag("HYDRO_NO_PAIR")) {
+    int la = -1, lb = -1;
+    for (int k = 0; k < P; ++k) {
+      const PredHost& ph = ctx->preds[k];
+      if (ph.desc.kind != HYDRO_PRED_LINEAR || ph.desc.crop_mode != HYDRO_CROP_NEAREST || ph.cache_known) continue;
+      if (la < 0) la = k;
+      else if (lb < 0) lb = k;
+    }
+    if (lb >= 0) {
+      const PredHost& A = ctx->preds[la];
+      const PredHost& B = ctx->preds[lb];
+      const int npa = A.n_pad, npb = B.n_pad, C_a = A.desc.n_classes, C_b = B.desc.n_classes;
+      if (A.a_fp16 == B.a_fp16 && npa + npb <= 144 && npa % 16 == 0 && npb % 16 == 0) {
+        const size_t pitch = static_cast<size_t>(npa + npb) * 128;
+        CU(cudaMalloc(&ctx->pair_w_tiled, pitch * (kFeatures / kKBlock)));
+        CU(cudaMemcpy2DAsync(ctx->pair_w_tiled, pitch, A.w_tiled_tm, static_cast<size_t>(npa) * 128,
+                             static_cast<size_t>(npa) * 128, kFeatures / kKBlock, cudaMemcpyDeviceToDevice, ctx->stream));
+        CU(cudaMemcpy2DAsync(ctx->pair_w_tiled + static_cast<size_t>(npa) * 128, pitch, B.w_tiled_tm,
+                             static_cast<size_t>(npb) * 128, static_cast<size_t>(npb) * 128, kFeatures / kKBlock,
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+        CU(cudaMalloc(&ctx->pair_bias, sizeof(float) * 144));
+        CU(cudaMemsetAsync(ctx->pair_bias, 0, sizeof(float) * 144, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->pair_bias, A.bias, sizeof(float) * C_a, cudaMemcpyDeviceToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->pair_bias + npa, B.bias, sizeof(float) * C_b, cudaMemcpyDeviceToDevice, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        ctx->pair_a = la;
+        ctx->pair_b = lb;
+        ctx->pair_npa = npa;
+        ctx->pair_n_pad = npa + npb;
+      }
+    }
+  }
+  h.pair_a = ctx->pair_a;
+  h.pair_b = ctx->pair_b;
+  build_sched(h.kind, h.order, P, h.sched, h.pair_a, h.pair_b);
   for (int i = 0; i < 8; ++i) h.kt_start[i] = ~0ull;
   CU(cudaMemcpy(ctx->st, &h, sizeof(h), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(ctx->preds_dev, pd.data(), sizeof(PredDev) * kMaxPred, cudaMemcpyHostToDevice));
@@ -817,6 +877,14 @@ static ClsParams cls_base(hydro_ctx* ctx, const uint32_t* fr, const uint64_t* bb
   c.warp_counts = ctx->seg_counts + ctx->max_segs;
   c.collect_stats = 1;
   c.explicit_pred = -1;
+  if (ctx->pair_a >= 0) {
+    c.pair_w_tiled = ctx->pair_w_tiled;
+    c.pair_bias = ctx->pair_bias;
+    c.pair_npa = ctx->pair_npa;
+    c.pair_n_pad = ctx->pair_n_pad;
+    c.pair_unscale_a = std::ldexp(1.0f, -ctx->preds[ctx->pair_a].w_scale_log2);
+    c.pair_unscale_b = std::ldexp(1.0f, -ctx->preds[ctx->pair_b].w_scale_log2);
+  }
   return c;
 }
 
@@ -1512,6 +1580,8 @@ hydro_status hydro_destroy(hydro_ctx* ctx) {
   cudaFree(ctx->counts);
   cudaFree(ctx->bits);
   cudaFree(ctx->warm_bits);
+  cudaFree(ctx->pair_w_tiled);
+  cudaFree(ctx->pair_bias);
   cudaFree(ctx->cache_idx);
   cudaFree(ctx->cache_pos);
   cudaFree(ctx->cache_count);
