@@ -302,6 +302,9 @@ def run_gpu(args):
     def lin_in():
         return sum(e.stats(k)["tuples_in"] for k in lin)
 
+    def lin_in_each():
+        return {k: e.stats(k)["tuples_in"] for k in lin}
+
     def mlp_in():
         return sum(e.stats(k)["tuples_in"] for k in mlps)
 
@@ -311,6 +314,7 @@ def run_gpu(args):
         dist.barrier()
     # classifier tuples in and the device launch timers, read around the timed region (outside it)
     in_t0, min_t0, hin_t0 = lin_in(), mlp_in(), hsv_in()
+    each_t0 = lin_in_each()
     for kind in (1, 4, 5):
         e.device_time(kind, reset=True)
     launches0 = e.launch_count()
@@ -334,7 +338,13 @@ def run_gpu(args):
     k4_ms, k4_n = e.device_time(1)
     km_ms, km_n = e.device_time(4)
     kh_ms, kh_n = e.device_time(5)
-    k4_tuples = lin_in() - in_t0
+    k4_evals = lin_in() - in_t0  # head evaluations as a sequential eddy counts them
+    # crops K4 gathered: a fused pair (two nearest heads next to each other in the order, one
+    # contraction) gathers each crop once for both heads, so its second head's inputs are not
+    # counted again (the second head's tuples_in = the first head's survivors)
+    each = {k: v - each_t0[k] for k, v in lin_in_each().items()}
+    pair_ks = [k for k in lin if e.stats(k)["fused_pair"]]
+    k4_tuples = k4_evals - (min(each[k] for k in pair_ks) if len(pair_ks) == 2 else 0)
     km_tuples = mlp_in() - min_t0
     kh_tuples = hsv_in() - hin_t0
     op_fp16 = [e.stats(k)["operand_fp16"] for k in lin + mlps]
@@ -424,6 +434,8 @@ def run_gpu(args):
                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_note,
                     "algorithmic_bytes_per_launch": k4_bytes / max(k4_n, 1),
                     "algorithmic_bytes_per_tuple": K4_BYTES_PER_TUPLE, "classifier_tuples_per_step": k4_tuples / args.steps,
+                    "head_evaluations_per_step": k4_evals / args.steps,
+                    "fused_pair": [w.preds[k]["name"] for k in pair_ks],
                     "avg_launch_ms": k4_ms / max(k4_n, 1), "launches": k4_n,
                     "share_of_step": k4_ms / ms, "time_source": "device launch timers inside the timed run",
                     "k2_ms_per_step": k2c_ms / args.steps,

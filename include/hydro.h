@@ -238,6 +238,9 @@ typedef struct {
   int32_t operand_scale_log2; /* LINEAR: k of the exact rescale W' = 2^k W that makes a general
                                  bf16 head fp16-exact (logits are multiplied by 2^-k, exactly,
                                  before the bias); 0 when none was needed or possible             */
+  int32_t fused_pair;         /* 1: this LINEAR head is one of the context's fused pair (two nearest
+                                 heads evaluated in one K4-T contraction whenever the order puts
+                                 them next to each other; counters as if evaluated in turn)      */
 } hydro_pred_stats;
 
 /* Per-batch record, available after the batch completed (hydro_batch_info). */

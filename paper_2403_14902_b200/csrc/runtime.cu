@@ -1347,6 +1347,7 @@ hydro_status hydro_get_stats(hydro_ctx* ctx, int32_t k, hydro_pred_stats* out) {
   out->cache_hit_rate = h.hit[k];
   out->operand_fp16 = ctx->preds[k].a_fp16;
   out->operand_scale_log2 = ctx->preds[k].w_scale_log2;
+  out->fused_pair = (k == ctx->pair_a || k == ctx->pair_b) ? 1 : 0;
   return HYDRO_OK;
 }
 

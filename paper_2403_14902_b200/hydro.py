@@ -69,7 +69,7 @@ class hydro_pred_stats(C.Structure):
                 ("selectivity", C.c_double), ("rank", C.c_double), ("position", C.c_int32),
                 ("s_in", C.c_double), ("s_pass", C.c_double), ("s_cost", C.c_double),
                 ("cost_raw_total", C.c_double), ("tuples_computed", C.c_int64), ("cache_hit_rate", C.c_double),
-                ("operand_fp16", C.c_int32), ("operand_scale_log2", C.c_int32)]
+                ("operand_fp16", C.c_int32), ("operand_scale_log2", C.c_int32), ("fused_pair", C.c_int32)]
 
 
 class hydro_batch_report(C.Structure):

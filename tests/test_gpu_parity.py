@@ -736,3 +736,35 @@ def test_hsv_every_rgb_colour():
     for a in range(0, n, 512):
         crops = np.stack([fr[int(fid[j]), int(y0[j]):int(y0[j]) + 64, int(x0[j]):int(x0[j]) + 64] for j in range(a, a + 512)])
         assert np.array_equal(got[a:a + 512], O.hsv_counts(crops)), a
+
+
+# ------------------------------------------------------------------------- fused linear pair
+
+@pytest.mark.parametrize("order", [[0, 1, 2], [0, 2, 1], [1, 0, 2], [1, 2, 0]])
+def test_fused_linear_pair_equals_separate_hops(small_dog, order, monkeypatch):
+    """The dog query's two nearest linear heads form K4-T's fused pair: when the order puts them
+    next to each other ([0,1,2], [0,2,1], [1,2,0]) one hop evaluates both; when the label sits
+    between them ([1,0,2]) they run as separate hops.  Rows and every per-batch counter (in, pass,
+    computed) equal the oracle's sequential evaluation and the run with the pair disabled."""
+    w, frames, fdev = small_dog
+    t = w.tuples(n=5000)
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, frames.numpy())
+    runs = []
+    for no_pair in (False, True):
+        if no_pair:
+            monkeypatch.setenv("HYDRO_NO_PAIR", "1")
+        e = make_eddy(w, fdev, policy="fixed", warmup=0, max_batch=2000)
+        e.set_fixed_order(order)
+        ids, bbs, infos = run_stream(e, t.to("cuda"), 2000)
+        fused = [e.stats(k)["fused_pair"] for k in range(3)]
+        e.close()
+        assert fused == ([0, 0, 0] if no_pair else [0, 1, 1]), fused
+        _assert_rows(ids, bbs, ref_ids, ref_bbox)
+        for b, info in enumerate(infos):
+            Vb = V[:, b * 2000:(b + 1) * 2000]
+            n_in, n_pass = expected_batch_counters(Vb, order, 0)
+            assert info["order_used"] == order
+            assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist(), (b, no_pair)
+            assert info["tuples_computed"] == n_in.tolist()
+        runs.append([(i["tuples_in"], i["tuples_passed"]) for i in infos])
+    assert runs[0] == runs[1]
