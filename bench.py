@@ -302,9 +302,6 @@ def run_gpu(args):
     def lin_in():
         return sum(e.stats(k)["tuples_in"] for k in lin)
 
-    def lin_in_each():
-        return {k: e.stats(k)["tuples_in"] for k in lin}
-
     def mlp_in():
         return sum(e.stats(k)["tuples_in"] for k in mlps)
 
@@ -314,9 +311,9 @@ def run_gpu(args):
         dist.barrier()
     # classifier tuples in and the device launch timers, read around the timed region (outside it)
     in_t0, min_t0, hin_t0 = lin_in(), mlp_in(), hsv_in()
-    each_t0 = lin_in_each()
     for kind in (1, 4, 5):
         e.device_time(kind, reset=True)
+        e.device_items(kind, reset=True)
     launches0 = e.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -338,15 +335,12 @@ def run_gpu(args):
     k4_ms, k4_n = e.device_time(1)
     km_ms, km_n = e.device_time(4)
     kh_ms, kh_n = e.device_time(5)
-    k4_evals = lin_in() - in_t0  # head evaluations as a sequential eddy counts them
-    # crops K4 gathered: a fused pair (two nearest heads next to each other in the order, one
-    # contraction) gathers each crop once for both heads, so its second head's inputs are not
-    # counted again (the second head's tuples_in = the first head's survivors)
-    each = {k: v - each_t0[k] for k, v in lin_in_each().items()}
+    k4_evals = lin_in() - in_t0  # head evaluations as a sequential eddy counts them (folded statistics)
+    # crops K4 gathered in the timed run, counted by the kernels (a fused pair's crops once)
+    k4_tuples = e.device_items(1)
     pair_ks = [k for k in lin if e.stats(k)["fused_pair"]]
-    k4_tuples = k4_evals - (min(each[k] for k in pair_ks) if len(pair_ks) == 2 else 0)
-    km_tuples = mlp_in() - min_t0
-    kh_tuples = hsv_in() - hin_t0
+    km_tuples = e.device_items(4)
+    kh_tuples = e.device_items(5)
     op_fp16 = [e.stats(k)["operand_fp16"] for k in lin + mlps]
     op_scale = [e.stats(k)["operand_scale_log2"] for k in lin]
     # ---- breakdown of the rest of the step (separate pass, CUDA events around every launch)

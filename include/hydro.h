@@ -395,6 +395,10 @@ hydro_status hydro_kernel_time(hydro_ctx* ctx, int32_t kind, double* total_ms, i
    milliseconds and the launch count (synchronises the context stream); reset = 1 then zeroes them. */
 hydro_status hydro_device_time(hydro_ctx* ctx, int32_t kind, int32_t reset, double* total_ms, int64_t* launches);
 
+/* The classifier-input tuples (crops) the same kinds' launches evaluated, counted on the device
+   (a fused linear pair's crops once); reset = 1 then zeroes the count.  Synchronises. */
+hydro_status hydro_device_items(hydro_ctx* ctx, int32_t kind, int32_t reset, int64_t* items);
+
 /* Destroys the context (synchronises first).  Safe on NULL. */
 hydro_status hydro_destroy(hydro_ctx* ctx);
 

@@ -147,6 +147,7 @@ struct DevState {
   // device launch timers (bench evidence, hydro_device_time): per kernel kind, %globaltimer of the
   // first CTA's start and the last CTA's end of every launch that did work, summed
   unsigned long long kt_start[8], kt_end[8], kt_total[8], kt_count[8];
+  unsigned long long kt_items[8];  // classifier-input tuples (crops) the kind's launches evaluated
   unsigned int kt_done[8];
 };
 

@@ -989,6 +989,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       atomicAdd(&st->d_pass[pred], static_cast<unsigned long long>(n_pass));
       atomicAdd(&st->d_comp[pred], static_cast<unsigned long long>(n_in));  // no verdict cache here
     }
+    if (lane == 0) atomicAdd(&st->kt_items[1], static_cast<unsigned long long>(n_in));
   }
 
   tc_fence_before();
@@ -1269,6 +1270,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_mlp_kernel(ClsParams p) 
       atomicAdd(&st->d_pass[pred], static_cast<unsigned long long>(n_pass));
       atomicAdd(&st->d_comp[pred], static_cast<unsigned long long>(n_in));  // no verdict cache here
     }
+    if (lane == 0) atomicAdd(&st->kt_items[4], static_cast<unsigned long long>(n_in));
   }
 
   tc_fence_before();
@@ -1792,6 +1794,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
         atomicAdd(&st->d_comp[pred], static_cast<unsigned long long>(n_in));
       }
     }
+    if (lane == 0) atomicAdd(&st->kt_items[1], static_cast<unsigned long long>(n_in));
   }
 
   tc_fence_before();

@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(kHsvThreads, 3) hydro_hsv_kernel(ClsParams p) 
     atomicAdd(&st->d_comp[pred], static_cast<unsigned long long>(n_in));
     atomicAdd(&st->d_cost[pred], cyc);
   }
+  if (lane == 0 && n_in) atomicAdd(&st->kt_items[5], static_cast<unsigned long long>(n_in));
   __syncthreads();
   if (threadIdx.x == 0) ktimer_end(st, 5);
 }

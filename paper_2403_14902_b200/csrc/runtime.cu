@@ -1465,6 +1465,20 @@ hydro_status hydro_device_time(hydro_ctx* ctx, int32_t kind, int32_t reset, doub
   return HYDRO_OK;
 }
 
+hydro_status hydro_device_items(hydro_ctx* ctx, int32_t kind, int32_t reset, int64_t* items) {
+  if (!ctx || !items) return set_err(HYDRO_EINVAL, "NULL argument");
+  if (kind != 1 && kind != 4 && kind != 5) return set_err(HYDRO_EINVAL, "device counters exist for kinds 1, 4, 5");
+  DevState h;
+  hydro_status s = read_state(ctx, &h);
+  if (s != HYDRO_OK) return s;
+  *items = static_cast<int64_t>(h.kt_items[kind]);
+  if (reset) {
+    const unsigned long long z = 0ull;
+    CU(cudaMemcpy(reinterpret_cast<char*>(ctx->st) + offsetof(DevState, kt_items) + 8 * kind, &z, 8, cudaMemcpyHostToDevice));
+  }
+  return HYDRO_OK;
+}
+
 hydro_status hydro_kernel_time(hydro_ctx* ctx, int32_t kind, double* total_ms, int64_t* launches) {
   if (!ctx || !total_ms || !launches) return set_err(HYDRO_EINVAL, "NULL argument");
   CU(cudaStreamSynchronize(ctx->stream));

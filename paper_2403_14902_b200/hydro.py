@@ -108,6 +108,7 @@ _SIGS = {
     "hydro_set_kernel_timing": ([_P, C.c_int32], C.c_int32),
     "hydro_kernel_time": ([_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int32),
     "hydro_device_time": ([_P, C.c_int32, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int32),
+    "hydro_device_items": ([_P, C.c_int32, C.c_int32, C.POINTER(C.c_int64)], C.c_int32),
     "hydro_debug_balance_bounds": ([_P, C.POINTER(C.c_uint32), C.c_int32, C.POINTER(C.c_int32)], C.c_int32),
     "hydro_destroy": ([_P], C.c_int32),
     "hydro_debug_linear": ([_P, C.c_int32, C.POINTER(hydro_tuples), _P, _P, _P], C.c_int32),
@@ -278,6 +279,12 @@ def hydro_device_time(ctx, kind: int, reset: bool = False):
     n = C.c_int64()
     _check(lib().hydro_device_time(ctx, kind, 1 if reset else 0, C.byref(ms), C.byref(n)))
     return ms.value, n.value
+
+
+def hydro_device_items(ctx, kind: int, reset: bool = False) -> int:
+    n = C.c_int64()
+    _check(lib().hydro_device_items(ctx, kind, 1 if reset else 0, C.byref(n)))
+    return n.value
 
 
 def hydro_debug_balance_bounds(ctx, capacity: int = 1024) -> List[int]:
@@ -504,6 +511,10 @@ class Eddy:
     def device_time(self, kind: int, reset: bool = False):
         """(ms, launches) summed by the classifier kernels' device timers (kind 1 / 4 / 5)."""
         return hydro_device_time(self.ctx, kind, reset)
+
+    def device_items(self, kind: int, reset: bool = False) -> int:
+        """Classifier-input tuples (crops) the kind's launches evaluated, counted on the device."""
+        return hydro_device_items(self.ctx, kind, reset)
 
     def debug_balance_bounds(self) -> List[int]:
         return hydro_debug_balance_bounds(self.ctx)
