@@ -268,6 +268,14 @@ __device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
 
 }  // namespace
 
+// RN(a / b) for an AREA bin sum a and its pixel count b, given y = RN(1 / b): one Markstein
+// correction step after a * y (checked equal to the IEEE quotient for every a <= 2^18, b <= 1100 by
+// tools/check_area_div.c, run in tests/test_oracle.py); the reciprocal is shared by a bin's channels
+__device__ __forceinline__ float area_div(float a, float b, float y) {
+  const float q = __fmul_rn(a, y);
+  return __fmaf_rn(__fmaf_rn(-q, b, a), y, q);
+}
+
 // One quad (4 crop rows x 8 lanes) of output pixels: lane (r, j) produces pixels j + 8k (k = 0..7,
 // the interleaved K order of crop_pos_feature) of row m from its staged segment `seg` (smem
 // address).  po[q] packs the byte offsets (relative to the segment) of pixels j+16q and j+16q+8.  Branch-free: both words around a pixel are always
@@ -369,10 +377,11 @@ __device__ __forceinline__ void convert_quad_area(const uint8_t* frames, uint32_
   uint32_t half[24];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const float cnt = static_cast<float>((ye - ys) * bw[k]);
+    const float cnt = static_cast<float>(max((ye - ys) * bw[k], 1u));
+    const float rcp = __frcp_rn(cnt);
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      const __nv_bfloat16 b = __float2bfloat16_rn(__fdiv_rn(static_cast<float>(s[k][ch]), cnt));
+      const __nv_bfloat16 b = __float2bfloat16_rn(area_div(static_cast<float>(s[k][ch]), cnt, rcp));
       const uint32_t bbits = __bfloat16_as_ushort(b);
       half[3 * k + ch] = kFp16 ? static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__bfloat162float(b)))) : bbits;
       if (kDbg && dbg) dbg[24 * k + ch] = static_cast<uint16_t>(bbits);
@@ -571,7 +580,9 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
     advance(cs);
     slot_stage = slot_stage + 1 == kQS ? 0 : slot_stage + 1;
   }
-  uint32_t sum[8][3];
+  // bin sums: channels 0 | 1 packed as u16 halves, channel 2 alone (a staged crop is <= 255 px
+  // wide, so a bin holds <= 5 x 13 pixels: every sum < 2^16)
+  uint32_t sum01[8], sum2[8];
   uint32_t set = 0, a_set = 0;
   while (cc.g < static_cast<uint32_t>(kGroups)) {
     if (cc.it == 0 && cc.i == 0) {  // first item of group g: its A stages must be free
@@ -583,7 +594,7 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
     }
     if (cc.i == 0) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) sum[k][0] = sum[k][1] = sum[k][2] = 0u;
+      for (int k = 0; k < 8; ++k) sum01[k] = sum2[k] = 0u;
     }
     stage_item(cs, slot_stage);
     advance(cs);
@@ -620,9 +631,8 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t pxl = __funnelshift_r(w0[k], w1[k], sh[k]);
-          sum[k][0] += pxl & 0xFFu;
-          sum[k][1] += (pxl >> 8) & 0xFFu;
-          sum[k][2] += (pxl >> 16) & 0xFFu;
+          sum01[k] += __byte_perm(pxl, 0u, 0x4140);  // (b0, 0, b1, 0): channels 0 and 1 as u16 halves
+          sum2[k] += __byte_perm(pxl, 0u, 0x4442);
         }
       }
     }
@@ -638,9 +648,11 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const float cnt = static_cast<float>(max(hb * bw[k], 1u));
+        const float rcp = __frcp_rn(cnt);
+        const uint32_t sk[3] = {sum01[k] & 0xFFFFu, sum01[k] >> 16, sum2[k]};
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
-          const __nv_bfloat16 b = __float2bfloat16_rn(__fdiv_rn(static_cast<float>(sum[k][ch]), cnt));
+          const __nv_bfloat16 b = __float2bfloat16_rn(area_div(static_cast<float>(sk[ch]), cnt, rcp));
           const uint32_t bbits = __bfloat16_as_ushort(b);
           half[3 * k + ch] =
               fp16 ? static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__bfloat162float(b)))) : bbits;

@@ -644,3 +644,19 @@ def test_pipeline_stage_times_counts_follow_eager_materialization():
     for b, row in enumerate(rows):
         n_in, _, _ = O.sequential_eval(V[:, 250 * b:250 * (b + 1)], [1, 0, 2])
         assert row == [n_in[1] * 2.0, n_in[0] * 1.0, n_in[2] * 3.0]
+
+
+def test_area_division_by_reciprocal_is_correctly_rounded(tmp_path):
+    """K4's AREA converter divides a bin sum by its pixel count as fma(fma(-q, b, a), y, q) with
+    y = RN(1/b), q = RN(a*y) instead of an IEEE division; R10 needs RN(a/b).  The C program checks
+    every integer a < 2^18 + 1 and count b <= 1100 (the largest AREA bin sum is 255 * 273)."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "check_area_div.c")
+    exe = str(tmp_path / "check_area_div")
+    subprocess.run([gcc, "-O2", "-mfma", "-ffp-contract=off", "-o", exe, src, "-lm"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.strip().startswith("bad 0 of"), r.stdout
