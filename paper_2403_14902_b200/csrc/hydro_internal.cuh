@@ -81,6 +81,15 @@ __host__ __device__ __forceinline__ uint32_t crop_pos_feature_tm(uint32_t g, uin
   return (g * 64u + 4u * k + t0) * 3u + f % 3u;
 }
 
+// K order of AREA heads (K4's row-cooperative AREA converter): lane q of a converter
+// warp makes output pixels q and q + 32 of one tuple's crop row and stores their 6 features as 3
+// consecutive words, so position p = 6q + 3*hi + ch of crop row g holds feature
+// (g*64 + q + 32*hi) * 3 + ch.
+__host__ __device__ __forceinline__ uint32_t crop_pos_feature_area(uint32_t g, uint32_t p) {
+  const uint32_t q = p / 6u, r = p % 6u;
+  return (g * 64u + q + 32u * (r / 3u)) * 3u + r % 3u;
+}
+
 enum PredKind : int32_t {
   kLabelEq = HYDRO_PRED_LABEL_EQ,
   kHash = HYDRO_PRED_HASH,

@@ -48,6 +48,8 @@ struct ClsCtrl {
   uint64_t full_b[kBStages], empty_b[kBStages];
   uint64_t tfull[2], tempty[2];
   uint64_t hready, tfull2;  // MLP: hidden layer written back to TMEM / second GEMM done
+  uint64_t astg[kConvWarps][8];  // AREA converter: staged items landed (bulk copies, complete_tx)
+  float area_rcp[32];            // AREA converter: RN(1 / n) for bin pixel counts n <= 25
   uint32_t tmem_base;
   uint32_t pad;
   float bias[HYDRO_MAX_CLASSES];
@@ -260,6 +262,11 @@ __device__ __forceinline__ void tc_st_32x32b_x8(uint32_t taddr, const uint32_t (
                : "memory");
 }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
   uint32_t d;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
@@ -334,7 +341,9 @@ __device__ __forceinline__ void convert_quad(uint32_t seg, const uint32_t (&po)[
 // AREA crop (R10, cfg4): output pixel (dy, dx) is the mean over the bin
 // [y0 + dy*h//64, y0 + ceil((dy+1)h/64)) x [x0 + dx*w//64, x0 + ceil((dx+1)w/64)), one IEEE f32
 // division then bf16 round-to-nearest-even; the bf16 value is staged exactly (fp16 or bf16).
-// Bins are read straight from global memory (L1-cached); lane (r, j) makes pixels j + 8k, k = 0..7.
+// Bins are read straight from global memory (L1-cached); used for tiles holding a crop wider than
+// a staging slot.  Lane (r, j) makes the 8 pixels of positions 24j .. 24j+23 of the AREA K order
+// (crop_pos_feature_area): pixel k is dx = 4j + k/2 + 32 (k % 2).  dbg: the crop row's features.
 template <bool kFp16, bool kDbg>
 __device__ __forceinline__ void convert_quad_area(const uint8_t* frames, uint32_t row0, uint32_t h, uint32_t x0,
                                                   uint32_t w, uint32_t pitch, uint32_t g, uint32_t row_base,
@@ -343,7 +352,7 @@ __device__ __forceinline__ void convert_quad_area(const uint8_t* frames, uint32_
   uint32_t xs[8], bw[8], bwmax = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const uint32_t dx = j + 8u * k;
+    const uint32_t dx = 4u * j + (k >> 1) + 32u * (k & 1);
     xs[k] = x0 + ((dx * w) >> 6);
     bw[k] = x0 + (((dx + 1u) * w + 63u) >> 6) - xs[k];
     bwmax = max(bwmax, bw[k]);
@@ -384,7 +393,7 @@ __device__ __forceinline__ void convert_quad_area(const uint8_t* frames, uint32_
       const __nv_bfloat16 b = __float2bfloat16_rn(area_div(static_cast<float>(s[k][ch]), cnt, rcp));
       const uint32_t bbits = __bfloat16_as_ushort(b);
       half[3 * k + ch] = kFp16 ? static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__bfloat162float(b)))) : bbits;
-      if (kDbg && dbg) dbg[24 * k + ch] = static_cast<uint16_t>(bbits);
+      if (kDbg && dbg) dbg[3u * (4u * j + (k >> 1) + 32u * (k & 1)) + ch] = static_cast<uint16_t>(bbits);
     }
   }
 #pragma unroll
@@ -497,8 +506,9 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
         const uint32_t ah = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.h), src_lane);
         const uint32_t ax0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src_lane);
         const uint32_t aw = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
-        if (fp16) convert_quad_area<true, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
-        else convert_quad_area<false, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg);
+        uint16_t* dbg_row = dbg ? dbg - 3 * j : nullptr;  // (AREA K order: the crop row's features)
+        if (fp16) convert_quad_area<true, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg_row);
+        else convert_quad_area<false, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg_row);
       } else {
         if (fp16) convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
         else convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
@@ -519,169 +529,230 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
   cp_async_wait<0>();
 }
 
-// AREA crops, staged (R10, cfg4): the bins of crop row g of a tuple cover its source rows
-// ys .. ye-1 (ys = g*h/64, ye = ceil((g+1)h/64)).  The converter walks "items" (g, quad it, source
-// row i < hbq = the quad's largest bin height): each item's 4 row segments are copied with
-// coalesced 16-byte cp.async into a staging slot kQD items ahead (the nearest path's ring); lane
-// (r, j) adds the pixels of its 8 bins (output pixels j + 8k) found in that row, and after the
-// quad's last row divides by the bin sizes (one f32 division, bf16 RNE) and stores the A row.
-template <bool kDbg, int kP, int kQD>
+// AREA crops, row-cooperative (R10, cfg4): the converter warp makes ONE tuple's crop
+// row at a time.  An "item" (crop row g, tuple t of the warp's 16) is the tuple's row segment in its
+// bin rows ys .. ye-1 (ys = g*h/64, ye = ceil((g+1)h/64), at most 5 rows): one 1-D bulk copy (TMA
+// engine) per source row into a per-warp byte ring, packed back to back, completion on the item's
+// mbarrier (8 in flight).  Then
+//   vertical:   lane l sums the 16-byte chunks l, l + 32 of the item's rows bytewise (u16 halves:
+//               <= 5 x 255) and stores them as V[b] (u16 per segment byte) in the warp's scratch;
+//   horizontal: lane q makes output pixels q and q + 32: each channel's bin sum is the sum of V over
+//               the bin's columns (<= 5 terms; the 3 channels of a column from two aligned words),
+//               then one f32 RN division (area_div with y = RN(1/count) from a table), bf16 RNE, and
+//               the 6 features go to A row 16*cu + t as 3 words at positions 6q .. 6q+5
+//               (crop_pos_feature_area).
+// Per source pixel the warp issues one shared load per 16 bytes (instead of 2 per pixel per bin),
+// and every lane works on the same tuple (no divergence between bin widths of different tuples).
+// Crops wider or taller than 256 px take the global-load converter (converter_role).
+constexpr int kAreaQ = 8;                                   // items in flight per converter warp
+static_assert(kAreaQ == sizeof(ClsCtrl::astg[0]) / sizeof(uint64_t), "one mbarrier per AREA item in flight");
+constexpr uint32_t kAreaVBytes = 2u * 784u + 16u;           // V scratch: u16 per byte of a segment (+ overread)
+constexpr uint32_t kAreaRing = 6144u;                       // item ring
+constexpr uint32_t kAreaRegion = 2u * kAreaVBytes + kAreaRing;  // per converter warp: 2 V buffers + ring
+static_assert(kAreaRing >= 5u * 784u, "one worst-case AREA item (5 source rows of 784 B) must fit the ring");
+static_assert(1023 + kARing * kAKBlockBytes + 3 * 16384 + sizeof(ClsCtrl) + 15 + kConvWarps * kAreaRegion <=
+                  kClsSmemBytes,
+              "AREA staging exceeds shared memory");
+
+__device__ __forceinline__ uint32_t f16x2_of_bf16x2(uint32_t b) {  // exact (bf16 means of u8 pixels)
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(__uint_as_float(b & 0xFFFF0000u)), "f"(__uint_as_float(b << 16)));
+  return d;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float ldsf(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t a) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(a) : "memory");
+}
+
+template <bool kDbg, int kP>
 __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* ctrl, uint32_t lim, uint32_t pos0,
-                                                  uint32_t crank, int cu, int lane, uint32_t slots, uint32_t a_ring,
-                                                  uint32_t row_pitch, bool fp16, const RowMeta& mm, uint32_t& gg) {
-  constexpr int kQS = kQD + 1;
-  const int r = lane >> 3, j = lane & 7;
+                                                  uint32_t crank, int cu, int lane, uint32_t region, uint32_t a_ring,
+                                                  uint32_t row_pitch, bool fp16, const RowMeta& mm, uint32_t& gg,
+                                                  uint32_t& qseq) {
   const uint8_t* frames = p.frames;
-  const uint32_t my_src = mm.row0 + mm.seg_lo;
-  const uint32_t my_len = (lane < 16 && mm.valid) ? mm.seg_len : 0u;
-  const uint32_t my_h = (lane < 16 && mm.valid) ? static_cast<uint32_t>(mm.h) : 0u;
-  // bin height of crop row g for the tuple of row r of quad it, and the quad's largest
-  auto bin_h = [&](uint32_t g, int it) {
-    const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, 4 * it + r);
-    return ((g + 1u) * h + 63u) / 64u - (g * h) / 64u;
-  };
-  // (at least 1: a quad of rows past the tile's count still stores its (masked) A rows)
-  auto quad_rows = [&](uint32_t g, int it) { return max(__reduce_max_sync(0xFFFFFFFFu, bin_h(g, it)), 1u); };
-  struct Cursor {
-    uint32_t g, i, hbq;
-    int it;
-  };
-  auto advance = [&](Cursor& c) {
-    if (++c.i < c.hbq) return;
-    c.i = 0;
-    if (++c.it == 4) {
-      c.it = 0;
-      ++c.g;
-    }
-    c.hbq = c.g < static_cast<uint32_t>(kGroups) ? quad_rows(c.g, c.it) : 1u;
-  };
-  // stage item c into a slot: row r's segment of source row ys(g) + i (nothing when i >= its bins)
-  auto stage_item = [&](const Cursor& c, uint32_t slot) {
-    if (c.g < static_cast<uint32_t>(kGroups)) {
-      const int src_lane = 4 * c.it + r;
-      const uint32_t len = __shfl_sync(0xFFFFFFFFu, my_len, src_lane);
-      const uint32_t off = __shfl_sync(0xFFFFFFFFu, my_src, src_lane);
-      const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
-      const uint32_t ys = (c.g * h) / 64u, hb = ((c.g + 1u) * h + 63u) / 64u - ys;
-      if (c.i < hb) {
-        const uint8_t* row = frames + (off + (ys + c.i) * row_pitch);
-        const uint32_t dst = slots + slot * kQuadSlotBytes + r * kSegPitch;
-        stage_segment(dst, row, j, len >> 4);
-      }
-    }
-    cp_async_commit();  // one group per item (possibly empty): uniform wait_group counting
-  };
-  Cursor cs{0u, 0u, quad_rows(0u, 0), 0};
-  Cursor cc = cs;
-  uint32_t slot_stage = 0, slot_use = 0;
+  const uint32_t vbuf = region, ring = region + 2u * kAreaVBytes;
+  const uint32_t rcp_tab = smem_u32(ctrl->area_rcp);
+  // tuple t of the band = lane t (valid tuples are a prefix: rows past the hop's count are masked)
+  const uint32_t nv = __popc(__ballot_sync(0xFFFFFFFFu, lane < 16 && mm.valid));
+  const uint32_t my_src = mm.row0 + mm.seg_lo, my_len = mm.seg_len, my_h = static_cast<uint32_t>(mm.h);
+  const uint32_t my_xw = static_cast<uint32_t>(mm.x0) | (static_cast<uint32_t>(mm.w) << 16);
+  const uint32_t total = kGroups * nv;
+  // this lane's 3 A words: byte o = 12q + 4i of the 384-byte crop row -> K-block o / 128, 16-byte
+  // chunk (o / 16) % 8 (swizzled with the row), byte o % 16
+  uint32_t st_off[3], st_chk[3];
 #pragma unroll
-  for (int k = 0; k < kQD; ++k) {
-    stage_item(cs, slot_stage);
-    advance(cs);
-    slot_stage = slot_stage + 1 == kQS ? 0 : slot_stage + 1;
+  for (int i = 0; i < 3; ++i) {
+    const uint32_t o = 12u * static_cast<uint32_t>(lane) + 4u * i;
+    st_off[i] = (o >> 7) * kAKBlockBytes + (o & 15u);
+    st_chk[i] = (o >> 4) & 7u;
   }
-  // bin sums: channels 0 | 1 packed as u16 halves, channel 2 alone (a staged crop is <= 255 px
-  // wide, so a bin holds <= 5 x 13 pixels: every sum < 2^16)
-  uint32_t sum01[8], sum2[8];
-  uint32_t set = 0, a_set = 0;
-  while (cc.g < static_cast<uint32_t>(kGroups)) {
-    if (cc.it == 0 && cc.i == 0) {  // first item of group g: its A stages must be free
-      set = (gg & 1u) * kKBlocksPerGroup;
-      const uint32_t aph = (gg >> 1) & 1u;
-#pragma unroll
-      for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_wait(&ctrl->empty_a[set + kbr], aph ^ 1u);
-      a_set = a_ring + set * kAKBlockBytes;
-    }
-    if (cc.i == 0) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) sum01[k] = sum2[k] = 0u;
-    }
-    stage_item(cs, slot_stage);
-    advance(cs);
-    slot_stage = slot_stage + 1 == kQS ? 0 : slot_stage + 1;
-    cp_async_wait<kQD>();  // this thread's copies of item cc have landed
-    __syncwarp();          // ... and every lane's
-    const int src_lane = 4 * cc.it + r;
-    const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src_lane);
-    const uint32_t w = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
-    const uint32_t slo = __shfl_sync(0xFFFFFFFFu, mm.seg_lo, src_lane);
-    const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
-    const uint32_t ys = (cc.g * h) / 64u, hb = ((cc.g + 1u) * h + 63u) / 64u - ys;
-    uint32_t xs[8], bw[8], bwmax = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t dx = static_cast<uint32_t>(j) + 8u * k;
-      xs[k] = x0 + ((dx * w) >> 6);
-      bw[k] = x0 + (((dx + 1u) * w + 63u) >> 6) - xs[k];
-      bwmax = max(bwmax, bw[k]);
-    }
-    if (cc.i < hb) {  // this row belongs to the tuple's bins: add it
-      const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kSegPitch;
-      for (uint32_t t = 0; t < bwmax; ++t) {
-        uint32_t w0[8], w1[8], sh[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const bool on = t < bw[k];
-          const uint32_t o = 3u * (xs[k] + t) - slo;
-          const uint32_t a = (seg + o) & ~3u;
-          sh[k] = o << 3;
-          w0[k] = on ? lds32(a) : 0u;
-          w1[k] = on ? lds32(a + 4) : 0u;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t pxl = __funnelshift_r(w0[k], w1[k], sh[k]);
-          sum01[k] += __byte_perm(pxl, 0u, 0x4140);  // (b0, 0, b1, 0): channels 0 and 1 as u16 halves
-          sum2[k] += __byte_perm(pxl, 0u, 0x4442);
-        }
+  // ring allocation (producer and consumer replay the same rule): an item starts at the cursor, or
+  // at the next ring start when it would cross the ring's end
+  auto place = [](uint32_t cur, uint32_t bytes) {
+    const uint32_t ph = cur % kAreaRing;
+    return ph + bytes > kAreaRing ? cur + (kAreaRing - ph) : cur;
+  };
+  uint32_t pk = 0, pg = 0, pt = 0, pcur = 0;  // producer: next item, its (g, t), ring cursor
+  uint32_t ccur = 0, ck = 0;                  // consumer: ring cursor, next item
+  // stage items ahead while the queue and the ring have room (oldest = start of item ck)
+  auto produce = [&](uint32_t oldest) {
+    while (pk < total && pk - ck < static_cast<uint32_t>(kAreaQ)) {
+      const uint32_t Lp = __shfl_sync(0xFFFFFFFFu, my_len, pt);
+      const uint32_t hp = __shfl_sync(0xFFFFFFFFu, my_h, pt);
+      const uint32_t srcp = __shfl_sync(0xFFFFFFFFu, my_src, pt);
+      const uint32_t ysp = (pg * hp) >> 6, hbp = (((pg + 1u) * hp + 63u) >> 6) - ysp;
+      const uint32_t bytes = hbp * Lp;
+      const uint32_t ps = place(pcur, bytes);
+      if (pk != ck && ps + bytes - oldest > kAreaRing) break;  // the ring is full
+      uint64_t* bar = &ctrl->astg[cu][(qseq + pk) % kAreaQ];
+      if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+      __syncwarp();
+      if (static_cast<uint32_t>(lane) < hbp)
+        bulk_g2s_u32(ring + ps % kAreaRing + lane * Lp, frames + (srcp + (ysp + lane) * row_pitch), Lp, bar);
+      pcur = ps + bytes;
+      ++pk;
+      if (++pt == nv) {
+        pt = 0;
+        ++pg;
       }
     }
-    slot_use = slot_use + 1 == kQS ? 0 : slot_use + 1;
-    __syncwarp();  // the slot is refilled kQD items later
-    if (cc.i + 1 == cc.hbq) {  // the quad's last row: bin means -> A row m
-      const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * cc.it + r);
-      const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
-      uint16_t* dbg = (kDbg && p.dbg_crops && pos0 + m < lim)
-                          ? p.dbg_crops + static_cast<uint64_t>(pos0 + m) * kFeatures + cc.g * 192 + 3 * j
-                          : nullptr;
-      uint32_t half[24];
+  };
+  // consume item ck (crop row g of tuple t): wait for its rows, vertical sums -> V at vb
+  auto consume = [&](uint32_t g, uint32_t t, uint32_t vb, uint32_t& hb_out, uint32_t& xw_out) {
+    const uint32_t L = __shfl_sync(0xFFFFFFFFu, my_len, t);
+    const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, t);
+    xw_out = __shfl_sync(0xFFFFFFFFu, my_xw, t);
+    const uint32_t ys = (g * h) >> 6, hb = (((g + 1u) * h + 63u) >> 6) - ys;
+    hb_out = hb;
+    const uint32_t cstart = place(ccur, hb * L);
+    produce(cstart);
+    mbar_wait(&ctrl->astg[cu][(qseq + ck) % kAreaQ], ((qseq + ck) / kAreaQ) & 1u);
+    const uint32_t item = ring + cstart % kAreaRing;
+    for (uint32_t c16 = static_cast<uint32_t>(lane); 16u * c16 < L; c16 += 32u) {
+      uint32_t s[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      uint32_t a = item + 16u * c16;
+      for (uint32_t i = 0; i < hb; ++i, a += L) {
+        const uint4 r = lds128(a);
+        s[0] += __byte_perm(r.x, 0u, 0x4140);  // bytes 0, 1 as u16 halves
+        s[1] += __byte_perm(r.x, 0u, 0x4342);  // bytes 2, 3
+        s[2] += __byte_perm(r.y, 0u, 0x4140);
+        s[3] += __byte_perm(r.y, 0u, 0x4342);
+        s[4] += __byte_perm(r.z, 0u, 0x4140);
+        s[5] += __byte_perm(r.z, 0u, 0x4342);
+        s[6] += __byte_perm(r.w, 0u, 0x4140);
+        s[7] += __byte_perm(r.w, 0u, 0x4342);
+      }
+      sts128(vb + 32u * c16, s[0], s[1], s[2], s[3]);
+      sts128(vb + 32u * c16 + 16u, s[4], s[5], s[6], s[7]);
+    }
+    ccur = cstart + hb * L;
+    ++ck;
+  };
+  for (uint32_t g = 0; g < static_cast<uint32_t>(kGroups); ++g, ++gg) {
+    const uint32_t set = (gg & 1u) * kKBlocksPerGroup, aph = (gg >> 1) & 1u;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float cnt = static_cast<float>(max(hb * bw[k], 1u));
-        const float rcp = __frcp_rn(cnt);
-        const uint32_t sk[3] = {sum01[k] & 0xFFFFu, sum01[k] >> 16, sum2[k]};
+    for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) mbar_wait(&ctrl->empty_a[set + kbr], aph ^ 1u);
+    const uint32_t a_set = a_ring + set * kAKBlockBytes;
+    // two tuples per pass: their vertical sums in turn (the ring holds one worst-case item), then
+    // the horizontal sums, divisions and stores of both interleaved
+    for (uint32_t t = 0; t < nv; t += 2) {
+      const bool two = t + 1 < nv;
+      uint32_t hb[2], xw[2];
+      consume(g, t, vbuf, hb[0], xw[0]);
+      if (two) consume(g, t + 1, vbuf + kAreaVBytes, hb[1], xw[1]);
+      else hb[1] = xw[1] = 0u;
+      __syncwarp();  // V complete (and the items' ring bytes read: reusable)
+      // ---- horizontal bin sums of pixels q and q + 32 of both tuples
+      uint32_t b2[2][2], bw[2][2], par[2][2], bwmax = 0;
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-          const __nv_bfloat16 b = __float2bfloat16_rn(area_div(static_cast<float>(sk[ch]), cnt, rcp));
-          const uint32_t bbits = __bfloat16_as_ushort(b);
-          half[3 * k + ch] =
-              fp16 ? static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__bfloat162float(b)))) : bbits;
-          if (kDbg && dbg) dbg[24 * k + ch] = static_cast<uint16_t>(bbits);
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t x0 = xw[u] & 0xFFFFu, w = xw[u] >> 16, slo = (3u * x0) & ~15u;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t dx = static_cast<uint32_t>(lane) + 32u * e;
+          const uint32_t xs = (dx * w) >> 6;
+          bw[u][e] = (((dx + 1u) * w + 63u) >> 6) - xs;  // 0 for an absent second tuple (w = 0)
+          const uint32_t b = 3u * (x0 + xs) - slo;  // V index of the bin's first column, channel 0
+          b2[u][e] = vbuf + u * kAreaVBytes + 2u * b;  // byte address of V[b]
+          par[u][e] = b & 1u;                          // V[b] is the high half of its word
+          bwmax = max(bwmax, bw[u][e]);
         }
       }
+      uint32_t s01[2][2] = {{0u, 0u}, {0u, 0u}}, s2[2][2] = {{0u, 0u}, {0u, 0u}};
+      for (uint32_t c = 0; c < bwmax; ++c) {
+        uint32_t w0[2][2], w1[2][2];
 #pragma unroll
-      for (int t = 0; t < 3; ++t) {
-        const uint32_t c = 3u * j + t;
-        const uint32_t addr = row_base + (c >> 3) * kAKBlockBytes + (((c & 7u) ^ (m & 7u)) << 4);
-        sts128(addr, half[8 * t] | (half[8 * t + 1] << 16), half[8 * t + 2] | (half[8 * t + 3] << 16),
-               half[8 * t + 4] | (half[8 * t + 5] << 16), half[8 * t + 6] | (half[8 * t + 7] << 16));
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool on = c < bw[u][e];
+            const uint32_t a = (b2[u][e] + 6u * c) & ~3u;  // column xs + c (V buffers are 16-byte aligned)
+            w0[u][e] = on ? lds32(a) : 0u;
+            w1[u][e] = on ? lds32(a + 4u) : 0u;
+          }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool odd = (par[u][e] ^ c) & 1u;
+            s01[u][e] += __byte_perm(w0[u][e], w1[u][e], odd ? 0x5432 : 0x3210);
+            s2[u][e] += __byte_perm(w1[u][e], 0u, odd ? 0x4432 : 0x4410);
+          }
       }
-      if (cc.it == 3) {  // group g complete: publish its A stages
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
+      // ---- means: one RN division each (area_div), bf16 RNE; 6 features = 3 words per tuple
 #pragma unroll
-          for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) {
-            if (kP == 2 && crank != 0) mbar_arrive_leader(&ctrl->full_a[set + kbr]);
-            else mbar_arrive(&ctrl->full_a[set + kbr]);
+      for (int u = 0; u < 2; ++u) {
+        if (u == 1 && !two) break;
+        float v[6];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint32_t n = hb[u] * bw[u][e];
+          const float cnt = static_cast<float>(n);
+          const float rcp = ldsf(rcp_tab + 4u * n);  // RN(1 / n), n <= 25
+          v[3 * e + 0] = area_div(static_cast<float>(s01[u][e] & 0xFFFFu), cnt, rcp);
+          v[3 * e + 1] = area_div(static_cast<float>(s01[u][e] >> 16), cnt, rcp);
+          v[3 * e + 2] = area_div(static_cast<float>(s2[u][e]), cnt, rcp);
+        }
+        const uint32_t m = static_cast<uint32_t>(cu * kConvRows) + t + u;
+        const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const uint32_t bb = bf16x2_rn(v[2 * i], v[2 * i + 1]);
+          sts32(row_base + st_off[i] + ((st_chk[i] ^ (m & 7u)) << 4), fp16 ? f16x2_of_bf16x2(bb) : bb);
+          if (kDbg && p.dbg_crops && pos0 + m < lim) {
+            uint16_t* dbg = p.dbg_crops + static_cast<uint64_t>(pos0 + m) * kFeatures + g * 192u;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              const uint32_t pp = 2u * i + hf;  // position 6q + pp
+              dbg[3u * (static_cast<uint32_t>(lane) + 32u * (pp / 3u)) + pp % 3u] =
+                  static_cast<uint16_t>(hf ? bb >> 16 : bb & 0xFFFFu);
+            }
           }
         }
-        ++gg;
+      }
+      __syncwarp();  // V is rewritten by the next pass
+    }
+    // group g complete: publish its A stages
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr) {
+        if (kP == 2 && crank != 0) mbar_arrive_leader(&ctrl->full_a[set + kbr]);
+        else mbar_arrive(&ctrl->full_a[set + kbr]);
       }
     }
-    advance(cc);
   }
-  cp_async_wait<0>();
+  qseq += total;
 }
 
 // Converter warps (shared by the linear and the MLP classifier kernels): cp.async-staged crop-row
@@ -699,7 +770,7 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
   // copied (16-byte cp.async, coalesced per row) kQD quads ahead into fixed slots.
   const int cu = warp - kConvWarp0;
   const uint32_t slots = staging_addr + static_cast<uint32_t>(cu) * (kQS * kQuadSlotBytes);
-  uint32_t gg = 0;
+  uint32_t gg = 0, qseq = 0;
   for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
     const uint32_t pos0 = tw.pos0(unit);
     // rows' metadata: lane l < 16 holds row 16*cu + l
@@ -707,9 +778,14 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
     // a tile with a crop wider than a staging slot (rare) runs the gather-staging variant
     const bool any_wide =
         __any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes));
-    if (kArea && area && !any_wide)
-      convert_tile_area<kDbg, kP, kQD>(p, ctrl, tw.lim, pos0, crank, cu, lane, slots, a_ring, row_pitch, fp16, mm, gg);
-    else if (any_wide)
+    // AREA: the row-cooperative converter takes bins of <= 5 x 5 pixels (w, h <= 256: a bin spans
+    // <= ceil(w/64) + 1 columns); a tile with a larger crop takes the direct global-load converter
+    const bool area_big = kArea && area &&
+                          __any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && (mm.w > 256 || mm.h > 256));
+    if (kArea && area && !any_wide && !area_big)
+      convert_tile_area<kDbg, kP>(p, ctrl, tw.lim, pos0, crank, cu, lane, staging_addr + cu * kAreaRegion, a_ring,
+                                  row_pitch, fp16, mm, gg, qseq);
+    else if (any_wide || area_big)
       convert_tile<kDbg, kArea, kP, kQD, true>(p, ctrl, list_in, tw.lim, pos0, crank, cu, lane, slots, a_ring, row_pitch,
                                                area, fp16, mm, gg);
     else
@@ -813,6 +889,9 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       mbar_init(&ctrl->tfull[a], 1);
       mbar_init(&ctrl->tempty[a], kEpiWarps * kPair);
     }
+    if (kArea)
+      for (int w = 0; w < kConvWarps; ++w)
+        for (int s = 0; s < kAreaQ; ++s) mbar_init(&ctrl->astg[w][s], 1);
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {
@@ -831,6 +910,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     }
   }
   if (tid < HYDRO_MAX_CLASSES) ctrl->bias[tid] = tid < n_classes ? pdg.bias[tid] : 0.0f;
+  if (kArea && tid < 32) ctrl->area_rcp[tid] = __frcp_rn(static_cast<float>(max(tid, 1)));
   tc_fence_before();
   if constexpr (kPair == 2) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive
   else __syncthreads();
@@ -854,7 +934,13 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           if (!mr[r].valid) continue;
-          if (area) {  // AREA: every source row of the crop row's bins, whole lines (all bytes are used)
+          if (area) {
+            // AREA: no L2 prefetch by default (the converters' bulk copies run up to 8 items ahead;
+            // prefetching 4 groups ahead measured 84 vs 52 GB of DRAM reads per 1M crops at the
+            // same speed).  HYDRO_AREA_PF: every source row of the crop row's bins, whole lines
+#ifndef HYDRO_AREA_PF
+            continue;
+#endif
             const uint32_t h = static_cast<uint32_t>(mr[r].h);
             const uint32_t ys = (static_cast<uint32_t>(g) * h) >> 6, ye = ((static_cast<uint32_t>(g) + 1u) * h + 63u) >> 6;
             for (uint32_t y = ys; y < ye; ++y) {
@@ -1365,11 +1451,6 @@ __device__ __forceinline__ void tc_st_16x256b_x2(uint32_t taddr, const uint32_t 
                : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
 
 // 8 staged pixels (byte offsets packed 2 per word, relative to `unit`) -> 12 words of fp16x2 (or
 // bf16x2) in feature order f = 3 * pixel + ch

@@ -1248,7 +1248,8 @@ __global__ void hydro_route_workers_kernel(WorkerRoute w, int32_t* order, double
 // re-tiles as bf16).
 // crop_order = 1 (matrices over the 12288 crop features: linear heads, MLP W1) places feature
 // crop_pos_feature(g, p) at position p of crop row g, the order K4's converters produce;
-// crop_order = 2 uses crop_pos_feature_tm, the order of K4-T (A in tensor memory).
+// crop_order = 2 uses crop_pos_feature_tm, the order of K4-T (A in tensor memory); crop_order = 3
+// crop_pos_feature_area, the order of K4's AREA converter.
 __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, int32_t n_classes, int32_t n_pad,
                                           int32_t k_features, int32_t to_fp16, int32_t crop_order, int32_t* inexact,
                                           float scale) {
@@ -1267,7 +1268,9 @@ __global__ void hydro_tile_weights_kernel(const uint16_t* w, uint8_t* w_tiled, i
         const uint32_t g = kb / kKBlocksPerGroup, p0 = (kb % kKBlocksPerGroup) * kKBlock + c * 8;
 #pragma unroll
         for (int t = 0; t < 8; ++t)
-          e[t] = wrow[crop_order == 2 ? crop_pos_feature_tm(g, p0 + t) : crop_pos_feature(g, p0 + t)];
+          e[t] = wrow[crop_order == 3   ? crop_pos_feature_area(g, p0 + t)
+                      : crop_order == 2 ? crop_pos_feature_tm(g, p0 + t)
+                                        : crop_pos_feature(g, p0 + t)];
         v = make_uint4(e[0] | (static_cast<uint32_t>(e[1]) << 16), e[2] | (static_cast<uint32_t>(e[3]) << 16),
                        e[4] | (static_cast<uint32_t>(e[5]) << 16), e[6] | (static_cast<uint32_t>(e[7]) << 16));
       } else {

@@ -265,7 +265,7 @@ static int fp16_scale_log2(hydro_ctx* ctx, const uint16_t* w, bool on_device, si
 }
 
 static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_device, int rows, int n_pad,
-                                 int k_features, bool try_fp16, uint8_t** out, int* fp16, bool tm_order,
+                                 int k_features, bool try_fp16, uint8_t** out, int* fp16, int order,
                                  float scale = 1.0f);
 
 // ------------------------------------------------------------------------------------------
@@ -454,11 +454,11 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
     ph.n_pad = next_pow2_pad(C);
     const cudaMemcpyKind kind = d->weights_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     hydro_status st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, H, H, kFeatures, true, &ph.w_tiled,
-                                   &ph.a_fp16, false);
+                                   &ph.a_fp16, 1);
     if (st != HYDRO_OK) return st;
     int w2_fp16 = 0;
     st = tile_weights(ctx, d->weight2_bf16, d->weights_on_device != 0, C, ph.n_pad, H, false, &ph.w2_tiled, &w2_fp16,
-                      false);
+                      0);
     if (st != HYDRO_OK) return st;
     CU(cudaMalloc(&ph.bias, sizeof(float) * HYDRO_MAX_CLASSES));
     CU(cudaMemsetAsync(ph.bias, 0, sizeof(float) * HYDRO_MAX_CLASSES, ctx->stream));
@@ -476,10 +476,12 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
       return set_err(HYDRO_EINVAL, "crop_mode must be HYDRO_CROP_NEAREST or HYDRO_CROP_AREA");
     const int C = d->n_classes;
     ph.n_pad = next_pow2_pad(C);
+    // K order of w_tiled: K4's (crop_pos_feature; AREA heads: the AREA converter's order)
+    const int k4_order = d->crop_mode == HYDRO_CROP_AREA ? 3 : 1;
     // stage operands as fp16 when every weight is exactly representable (u8 pixels always are):
     // same products, cheaper u8 -> fp16 operand construction in K4
     hydro_status st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, C, ph.n_pad, kFeatures, true,
-                                   &ph.w_tiled, &ph.a_fp16, false);
+                                   &ph.w_tiled, &ph.a_fp16, k4_order);
     if (st != HYDRO_OK) return st;
     const char* no_scale = getenv("HYDRO_NO_FP16_SCALE");  // test hook: keep general heads on bf16 operands
     if (!ph.a_fp16 && !(no_scale && no_scale[0] == '1')) {
@@ -490,7 +492,7 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
       if (k != 0 && k > -100 && k < 100) {
         uint8_t* w2 = nullptr;
         int ok = 0;
-        st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, C, ph.n_pad, kFeatures, true, &w2, &ok, false,
+        st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, C, ph.n_pad, kFeatures, true, &w2, &ok, k4_order,
                           std::ldexp(1.0f, k));
         if (st != HYDRO_OK) return st;
         if (ok) {
@@ -506,7 +508,7 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
     if (d->crop_mode == HYDRO_CROP_NEAREST) {  // K4-T's copy (same operand type and scale)
       int fp16_tm = 0;
       st = tile_weights(ctx, d->weight_bf16, d->weights_on_device != 0, C, ph.n_pad, kFeatures, ph.a_fp16 != 0,
-                        &ph.w_tiled_tm, &fp16_tm, true, std::ldexp(1.0f, ph.w_scale_log2));
+                        &ph.w_tiled_tm, &fp16_tm, 2, std::ldexp(1.0f, ph.w_scale_log2));
       if (st != HYDRO_OK) return st;
     }
     CU(cudaMalloc(&ph.bias, sizeof(float) * HYDRO_MAX_CLASSES));
@@ -527,7 +529,7 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
 }  // extern "C"
 
 static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_device, int rows, int n_pad,
-                                 int k_features, bool try_fp16, uint8_t** out, int* fp16, bool tm_order,
+                                 int k_features, bool try_fp16, uint8_t** out, int* fp16, int order,
                                  float scale) {
   const size_t wbytes = static_cast<size_t>(rows) * k_features * 2;
   uint16_t* wdev = nullptr;
@@ -538,7 +540,7 @@ static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_devi
   int32_t* inexact = reinterpret_cast<int32_t*>(ctx->zero_word + 1);
   int32_t bad = 1;
   if (try_fp16) {
-    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 1, k_features == kFeatures ? (tm_order ? 2 : 1) : 0, inexact, scale);
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 1, k_features == kFeatures ? order : 0, inexact, scale);
     ctx->launches += 1;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(&bad, inexact, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -546,7 +548,7 @@ static hydro_status tile_weights(hydro_ctx* ctx, const uint16_t* w, bool on_devi
   }
   *fp16 = bad ? 0 : 1;
   if (bad) {
-    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 0, k_features == kFeatures ? (tm_order ? 2 : 1) : 0, inexact, scale);
+    hydro_tile_weights_kernel<<<512, 256, 0, ctx->stream>>>(wdev, *out, rows, n_pad, k_features, 0, k_features == kFeatures ? order : 0, inexact, scale);
     ctx->launches += 1;
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(ctx->stream));

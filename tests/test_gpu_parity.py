@@ -529,6 +529,48 @@ def test_wide_crops_nearest_linear_and_mlp():
         e.close()
 
 
+def test_wide_and_tall_crops_area():
+    """AREA crops of every size on 720p frames: ordinary ones (row-cooperative converter, bin rows
+    staged by bulk copies), crops wider than a staging slot (w > 255 px) and crops taller than the
+    AREA item ring holds (bin row groups of up to 12 source rows) mixed in the same tiles (those
+    tiles take the global-load converter): crops bit-exact, logits within 1e-2, verdicts equal
+    where the oracle margin exceeds the tolerance."""
+    from synth import Tuples, make_frames
+
+    F = make_frames(10, 4, 720, 1280)
+    n = 640
+    g = torch.Generator().manual_seed(6)
+    w = torch.randint(1, 256, (n,), generator=g)
+    h = torch.randint(1, 256, (n,), generator=g)
+    w[200::7] = torch.tensor([300, 700, 1000, 1280])[torch.arange(200, n, 7) % 4]
+    h[384::5] = torch.tensor([600, 650, 700, 720])[torch.arange(384, n, 5) % 4]
+    x0 = (torch.rand(n, generator=g) * (1280 - w + 1).double()).long().clamp(min=0)
+    y0 = (torch.rand(n, generator=g) * (720 - h + 1).double()).long().clamp(min=0)
+    bbox = torch.stack([x0, y0, x0 + w, y0 + h], 1).to(torch.int16)
+    t = Tuples(torch.arange(n, dtype=torch.int64), torch.arange(n, dtype=torch.int32) % 4, bbox,
+               torch.full((n,), 16, dtype=torch.int16))
+    tup = O.as_numpy_tuples(t)
+    fr = F.numpy()
+    ref_crop = O.crop_area(fr, tup["frame_id"], tup["bbox"]).reshape(n, -1)
+    p = workload("cfg4", small=True, n=100).preds[3]
+    assert p["crop_mode"] == "area"
+    from paper_2403_14902_b200.hydro import Eddy
+
+    e = Eddy(frames=F.cuda(), policy="fixed", warmup_tuples=0, max_batch_tuples=4096)
+    k = e.add_predicate(p)
+    C = p["n_classes"]
+    logits = torch.full((n, C), float("nan"), device="cuda")
+    crops = torch.zeros((n, O.K_FEATURES), dtype=torch.int16, device="cuda")
+    verdict = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    e.debug_linear(k, t.to("cuda"), logits, crops, verdict)
+    assert np.array_equal(crops.view(torch.bfloat16).float().cpu().numpy(), ref_crop)
+    v_ref, z_ref = O.linear_verdict(p, fr, tup["frame_id"], tup["bbox"], return_logits=True)
+    assert np.abs(logits.double().cpu().numpy() - z_ref).max() <= LOGIT_TOL
+    away = np.abs(O.margin(z_ref, p["target"])) > LOGIT_TOL
+    assert np.array_equal(verdict.cpu().numpy().astype(bool)[away], v_ref[away])
+    e.close()
+
+
 # ------------------------------------------------------------- data-aware tile scheduling (f4, R28)
 
 @pytest.mark.parametrize("n", [700, 9000, 20000])
