@@ -50,6 +50,8 @@ struct ClsCtrl {
   uint64_t hready, tfull2;  // MLP: hidden layer written back to TMEM / second GEMM done
   uint64_t astg[kConvWarps][8];  // AREA converter: staged items landed (bulk copies, complete_tx)
   float area_rcp[32];            // AREA converter: RN(1 / n) for bin pixel counts n <= 25
+  uint32_t area_cost[kTileM];    // data-aware AREA tiles: estimated converter work of each tile row
+  uint8_t area_perm[kTileM];     //   tile rows of converter warp c = area_perm[16c .. 16c+15]
   uint32_t tmem_base;
   uint32_t pad;
   float bias[HYDRO_MAX_CLASSES];
@@ -97,6 +99,9 @@ __device__ __forceinline__ uint32_t lds32_if(uint32_t addr, bool pred) {
   return v;
 }
 #endif
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -429,7 +434,7 @@ template <bool kDbg, bool kArea, int kP, int kQD, bool kWide>
 __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, const uint32_t* list_in, uint32_t lim,
                                              uint32_t pos0, uint32_t crank, int cu, int lane, uint32_t slots, uint32_t a_ring,
                                              uint32_t row_pitch, bool area, bool fp16, const RowMeta& mm,
-                                             uint32_t& gg) {
+                                             uint32_t my_row, uint32_t& gg) {
   constexpr int kQS = kQD + 1;
   const int r = lane >> 3, j = lane & 7;
   const uint8_t* frames = p.frames;
@@ -494,7 +499,7 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
       cp_async_wait<kQD>();  // this thread's copies of quad k have landed
       __syncwarp();                 // ... and every lane's
       // rows past the tile's count convert stale bytes into A rows whose results are masked
-      const uint32_t m = static_cast<uint32_t>(cu * kConvRows + 4 * it + r);
+      const uint32_t m = __shfl_sync(0xFFFFFFFFu, my_row, 4 * it + r);  // tile row of this lane's tuple
       const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kSegPitch;
       const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
       uint16_t* dbg = (kDbg && p.dbg_crops && pos0 + m < lim)
@@ -545,6 +550,7 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
 // and every lane works on the same tuple (no divergence between bin widths of different tuples).
 // Crops wider or taller than 256 px take the global-load converter (converter_role).
 constexpr int kAreaQ = 8;                                   // items in flight per converter warp
+constexpr uint32_t kAreaFixedCost = 12288;  // data-aware warp balance: per-tuple fixed work, in (h+64)(w+16) units
 static_assert(kAreaQ == sizeof(ClsCtrl::astg[0]) / sizeof(uint64_t), "one mbarrier per AREA item in flight");
 constexpr uint32_t kAreaVBytes = 2u * 784u + 16u;           // V scratch: u16 per byte of a segment (+ overread)
 constexpr uint32_t kAreaRing = 6144u;                       // item ring
@@ -576,8 +582,8 @@ __device__ __forceinline__ void sts32(uint32_t addr, uint32_t a) {
 template <bool kDbg, int kP>
 __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* ctrl, uint32_t lim, uint32_t pos0,
                                                   uint32_t crank, int cu, int lane, uint32_t region, uint32_t a_ring,
-                                                  uint32_t row_pitch, bool fp16, const RowMeta& mm, uint32_t& gg,
-                                                  uint32_t& qseq) {
+                                                  uint32_t row_pitch, bool fp16, const RowMeta& mm, uint32_t my_row,
+                                                  uint32_t& gg, uint32_t& qseq) {
   const uint8_t* frames = p.frames;
   const uint32_t vbuf = region, ring = region + 2u * kAreaVBytes;
   const uint32_t rcp_tab = smem_u32(ctrl->area_rcp);
@@ -722,7 +728,7 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
           v[3 * e + 1] = area_div(static_cast<float>(s01[u][e] >> 16), cnt, rcp);
           v[3 * e + 2] = area_div(static_cast<float>(s2[u][e]), cnt, rcp);
         }
-        const uint32_t m = static_cast<uint32_t>(cu * kConvRows) + t + u;
+        const uint32_t m = __shfl_sync(0xFFFFFFFFu, my_row, t + u);  // tile row of the tuple
         const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
@@ -774,7 +780,37 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
   for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
     const uint32_t pos0 = tw.pos0(unit);
     // rows' metadata: lane l < 16 holds row 16*cu + l
-    const RowMeta mm = load_meta(p, list_in, base, pos0 + cu * kConvRows + (lane & 15), lane < 16 ? tw.lim : 0u);
+    uint32_t my_row = static_cast<uint32_t>(cu * kConvRows + (lane & 15));
+    RowMeta mm = load_meta(p, list_in, base, pos0 + my_row, lane < 16 ? tw.lim : 0u);
+#ifdef HYDRO_AREA_BAL_ALWAYS
+    if (kArea && area) {
+#else
+    if (kArea && area && tw.bal) {
+#endif
+      // data-aware AREA tiles (R28) at warp granularity: the converter warps are the tile's
+      // workers; each tile row's work is estimated from its input size, kAreaFixedCost + (h + 64)(w + 16)
+      // (~ source bytes staged and summed per crop, plus the per-tuple fixed part), the rows are
+      // ranked by it (ties: lower row first) and dealt to the warps in snake order (rank k -> warp
+      // k % 8, or 7 - k % 8 on odd rounds, slot k / 8), so every warp's load is within one row of
+      // the others' and the hop's invalid rows (ranked last) stay a suffix of every warp's slots
+      if (lane < 16)
+        ctrl->area_cost[my_row] =
+            mm.valid ? kAreaFixedCost + static_cast<uint32_t>((mm.h + 64) * (mm.w + 16)) : 0u;
+      named_bar_sync(1, kConvWarps * 32);
+      if (cu < kTileM / 32) {
+        const uint32_t m = static_cast<uint32_t>(cu * 32 + lane), cm = ctrl->area_cost[m];
+        uint32_t k = 0;
+        for (uint32_t j = 0; j < static_cast<uint32_t>(kTileM); ++j) {
+          const uint32_t cj = ctrl->area_cost[j];
+          k += (cj > cm || (cj == cm && j < m)) ? 1u : 0u;
+        }
+        const uint32_t s = k >> 3, c = (s & 1u) ? 7u - (k & 7u) : (k & 7u);
+        ctrl->area_perm[c * kConvRows + s] = static_cast<uint8_t>(m);
+      }
+      named_bar_sync(1, kConvWarps * 32);
+      my_row = ctrl->area_perm[cu * kConvRows + (lane & 15)];
+      mm = load_meta(p, list_in, base, pos0 + my_row, lane < 16 ? tw.lim : 0u);
+    }
     // a tile with a crop wider than a staging slot (rare) runs the gather-staging variant
     const bool any_wide =
         __any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes));
@@ -784,13 +820,13 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
                           __any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && (mm.w > 256 || mm.h > 256));
     if (kArea && area && !any_wide && !area_big)
       convert_tile_area<kDbg, kP>(p, ctrl, tw.lim, pos0, crank, cu, lane, staging_addr + cu * kAreaRegion, a_ring,
-                                  row_pitch, fp16, mm, gg, qseq);
+                                  row_pitch, fp16, mm, my_row, gg, qseq);
     else if (any_wide || area_big)
       convert_tile<kDbg, kArea, kP, kQD, true>(p, ctrl, list_in, tw.lim, pos0, crank, cu, lane, slots, a_ring, row_pitch,
-                                               area, fp16, mm, gg);
+                                               area, fp16, mm, my_row, gg);
     else
       convert_tile<kDbg, kArea, kP, kQD, false>(p, ctrl, list_in, tw.lim, pos0, crank, cu, lane, slots, a_ring,
-                                                row_pitch, area, fp16, mm, gg);
+                                                row_pitch, area, fp16, mm, my_row, gg);
   }
   if (kP == 2) {  // drain: both A sets released (the leader's commits land here)
     for (int e = 0; e < 2; ++e, ++gg) {
