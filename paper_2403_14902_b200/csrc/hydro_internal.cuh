@@ -315,6 +315,7 @@ struct ClsParams {
   uint32_t* bal_chunks;    // K6: estimated cost (sum of w*h) per 32-position chunk of the hop input
   uint32_t* bal_bounds;    // K6: output bounds, bal_ctas + 1 entries
   int32_t bal_ctas;        // CTAs of the K4 launch the bounds are for
+  int32_t area_only;       // K4: evaluate AREA hops only (nearest hops run in K4-T, launched beside it)
   // verdict caches on classifier hops (reuse; R26): K0c splits a cached hop's
   // input into cached verdicts (written straight into the hop bitmap) and the uncached tuples,
   // which the classifier kernel then evaluates through this redirection

@@ -871,6 +871,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   const uint32_t num_tiles = (count + kTileM - 1) / kTileM;
   const PredDev& pdg = p.preds[pred];
   const bool area = kArea && pdg.crop_mode == HYDRO_CROP_AREA;  // kArea: the context has an AREA head
+  if (p.area_only && !area) return;  // a nearest hop: K4-T (launched beside this kernel) evaluates it
   // work unit = kPair consecutive M-tiles (one per CTA of the cluster); both CTAs of a pair walk
   // the same units, so a pair's last unit may hold a tile past num_tiles (all rows invalid)
   const uint32_t crank = kPair == 2 ? cluster_ctarank() : 0u;
@@ -1703,6 +1704,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_tm_kernel(Cls
     bits_out = p.bits_out;
   }
   // cached classifier hop: only the uncached tuples (K0c's list), verdict bits by hop position
+  if (p.preds[pred].crop_mode != HYDRO_CROP_NEAREST) return;  // AREA hops run in K4 (launched beside)
   const uint32_t* ind = cls_redirect(p, p.preds[pred], list_in, count);
   const bool fill = p.preds[pred].cache_known && (p.preds[pred].cache_fill || p.force_fill);
   const uint32_t num_tiles = (count + kTileM - 1) / kTileM;

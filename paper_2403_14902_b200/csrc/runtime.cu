@@ -175,6 +175,7 @@ struct hydro_ctx {
   int32_t fixed_order[kMaxPred];
   bool fixed_order_set = false;
   bool has_area = false;
+  bool has_nearest_linear = false;  // a nearest LINEAR head (K4-T) next to an AREA head (K4)
   bool k4_legacy = false;
   int pair_a = -1, pair_b = -1;   // fused linear pair (pred ids), see freeze()
   int pair_npa = 0, pair_n_pad = 0;
@@ -521,6 +522,7 @@ hydro_status hydro_add_predicate(hydro_ctx* ctx, const hydro_predicate_desc* d, 
     return set_err(HYDRO_EINVAL, "unknown predicate kind");
   }
   if (d->kind == HYDRO_PRED_LINEAR && d->crop_mode == HYDRO_CROP_AREA) ctx->has_area = true;
+  if (d->kind == HYDRO_PRED_LINEAR && d->crop_mode == HYDRO_CROP_NEAREST) ctx->has_nearest_linear = true;
   ctx->preds.push_back(ph);
   if (pred_id) *pred_id = static_cast<int32_t>(ctx->preds.size() - 1);
   return HYDRO_OK;
@@ -739,9 +741,9 @@ static hydro_status freeze(hydro_ctx* ctx) {
   for (int i = 0; i < P; ++i) h.position[h.order[i]] = i;
   // fused linear pair (K4-T evaluates both heads in one contraction when the order puts them next
   // to each other): two nearest LINEAR heads with the same operand type, N_a + N_b <= 144, no
-  // verdict cache, K4-T in use (no AREA head, not HYDRO_K4_LEGACY / HYDRO_NO_PAIR)
+  // verdict cache, K4-T in use (not HYDRO_K4_LEGACY / HYDRO_NO_PAIR; AREA heads never pair)
   ctx->pair_a = ctx->pair_b = -1;
-  if (!ctx->has_area && !ctx->k4_legacy && !getenv_flag("HYDRO_NO_PAIR")) {
+  if (!ctx->k4_legacy && !getenv_flag("HYDRO_NO_PAIR")) {
     int la = -1, lb = -1;
     for (int k = 0; k < P; ++k) {
       const PredHost& ph = ctx->preds[k];
@@ -951,9 +953,19 @@ static hydro_status launch_cls(hydro_ctx* ctx, const ClsParams& c0, uint64_t max
     const bool dbg = c.dbg_crops || c.dbg_logits || c.dbg_verdict;
     if (kind == kClsMlp) hydro_mlp_launch(c, grid, ctx->stream, dbg);
     else if (kind == kClsHsv) hydro_hsv_launch(c, max_positions, ctx->num_sms, ctx->stream);
-    // kernel instantiation by context capability: AREA support only when an AREA head exists
+    // kernel instantiation by context capability: nearest heads on K4-T, AREA heads on K4 (its
+    // AREA instance); a context with both launches both per linear slot, each kernel exits on the
+    // other's hops (the hop's head is known on the device only)
     else if (!ctx->has_area && !ctx->k4_legacy) hydro_classifier_tm_launch(c, grid, ctx->stream, dbg);
-    else hydro_classifier_launch(c, grid, ctx->stream, dbg, ctx->has_area);
+    else if (ctx->has_area && !ctx->k4_legacy) {
+      if (ctx->has_nearest_linear) {
+        hydro_classifier_tm_launch(c, grid, ctx->stream, dbg);
+        ctx->launches += 1;
+      }
+      ClsParams ca = c;
+      ca.area_only = 1;
+      hydro_classifier_launch(ca, grid, ctx->stream, dbg, true);
+    } else hydro_classifier_launch(c, grid, ctx->stream, dbg, ctx->has_area);
   });
 }
 
