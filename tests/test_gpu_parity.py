@@ -307,6 +307,36 @@ def test_cfg4_small_end_to_end(balance, weights):
     e.close()
 
 
+@pytest.mark.parametrize("order", [[0, 1, 2, 4, 3], [3, 4, 2, 0, 1], [0, 2, 1, 4, 3]])
+@pytest.mark.parametrize("balance", ["round_robin", "data_aware"])
+def test_area_and_nearest_heads_in_one_context(order, balance):
+    """A context holding an AREA head and two nearest heads: every linear slot launches K4-T
+    (nearest hops, with the fused pair when the order puts the two nearest heads next to each other)
+    beside K4's AREA instance (AREA hops); each kernel leaves the other's hops alone.  cfg4's query
+    plus cfg2's nearest breed head, fixed orders with the nearest heads adjacent (fused) and apart:
+    rows and every per-batch counter equal the oracle's sequential evaluation."""
+    from synth import linear_pred
+    from synth.workload import SEED
+
+    w = workload("cfg4", small=True, n=6000)
+    w.preds = list(w.preds) + [linear_pred(SEED + 1, 120, 57, 0.254, name="breed=great dane (nearest)")]
+    frames = w.frames()
+    t = w.tuples()
+    V, ref_ids, ref_bbox, _ = oracle_result(w, t, frames.numpy())
+    e = make_eddy(w, frames.cuda(), policy="fixed", warmup=0, max_batch=2048, balance=balance)
+    e.set_fixed_order(order)
+    ids, bbs, infos = run_stream(e, t.to("cuda"), 2048)
+    fused = [e.stats(k)["fused_pair"] for k in range(5)]
+    e.close()
+    assert fused == [0, 0, 1, 0, 1], fused  # the context's pair (evaluated fused when adjacent)
+    _assert_rows(ids, bbs, ref_ids, ref_bbox)
+    for b, info in enumerate(infos):
+        Vb = V[:, b * 2048:(b + 1) * 2048]
+        n_in, n_pass = expected_batch_counters(Vb, order, 0)
+        assert info["order_used"] == order
+        assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist(), b
+
+
 # ------------------------------------------------------------------------------- MLP head (f1)
 
 @pytest.mark.parametrize("weights", ["grid", "bf16"])
