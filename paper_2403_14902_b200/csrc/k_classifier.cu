@@ -43,15 +43,19 @@ constexpr int kBStages = kBRing;  // pair mode: half-size stages, half the B-rin
 constexpr int kBStages = kBRing * kPair;  // same B-ring bytes; half-size stages in pair mode
 #endif
 
+#ifndef HYDRO_AREA_WARPS
+#define HYDRO_AREA_WARPS 16
+#endif
+constexpr int kMaxCW = HYDRO_AREA_WARPS > kConvWarps ? HYDRO_AREA_WARPS : kConvWarps;
 struct ClsCtrl {
   uint64_t full_a[kARing], empty_a[kARing];
   uint64_t full_b[kBStages], empty_b[kBStages];
   uint64_t tfull[2], tempty[2];
   uint64_t hready, tfull2;  // MLP: hidden layer written back to TMEM / second GEMM done
-  uint64_t astg[kConvWarps][8];  // AREA converter: staged items landed (bulk copies, complete_tx)
+  uint64_t astg[kMaxCW][8];      // AREA converter: staged items landed (bulk copies, complete_tx)
   float area_rcp[32];            // AREA converter: RN(1 / n) for bin pixel counts n <= 25
   uint32_t area_cost[kTileM];    // data-aware AREA tiles: estimated converter work of each tile row
-  uint8_t area_perm[kTileM];     //   tile rows of converter warp c = area_perm[16c .. 16c+15]
+  uint8_t area_perm[kMaxCW * 16];  // tile rows of converter warp c = area_perm[16c .. 16c+15] (0xFF: none)
   uint32_t tmem_base;
   uint32_t pad;
   float bias[HYDRO_MAX_CLASSES];
@@ -500,17 +504,22 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
       __syncwarp();                 // ... and every lane's
       // rows past the tile's count convert stale bytes into A rows whose results are masked
       const uint32_t m = __shfl_sync(0xFFFFFFFFu, my_row, 4 * it + r);  // tile row of this lane's tuple
+      const bool row_ok = m < static_cast<uint32_t>(kTileM);          // (a slot without a row: nothing to store)
       const uint32_t seg = slots + slot_use * kQuadSlotBytes + r * kSegPitch;
       const uint32_t row_base = a_set + (m >> 3) * 1024u + (m & 7u) * 128u;
       uint16_t* dbg = (kDbg && p.dbg_crops && pos0 + m < lim)
                           ? p.dbg_crops + static_cast<uint64_t>(pos0 + m) * kFeatures + g * 192 + 3 * j
                           : nullptr;
-      if (kArea && area) {
+      uint32_t ar0 = 0, ah = 0, ax0 = 0, aw = 0;
+      if (kArea && area) {  // (all lanes shuffle before the per-row branch below)
         const int src_lane = 4 * it + r;
-        const uint32_t ar0 = __shfl_sync(0xFFFFFFFFu, mm.row0, src_lane);
-        const uint32_t ah = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.h), src_lane);
-        const uint32_t ax0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src_lane);
-        const uint32_t aw = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
+        ar0 = __shfl_sync(0xFFFFFFFFu, mm.row0, src_lane);
+        ah = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.h), src_lane);
+        ax0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src_lane);
+        aw = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
+      }
+      if (!row_ok) {
+      } else if (kArea && area) {
         uint16_t* dbg_row = dbg ? dbg - 3 * j : nullptr;  // (AREA K order: the crop row's features)
         if (fp16) convert_quad_area<true, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg_row);
         else convert_quad_area<false, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg_row);
@@ -553,12 +562,19 @@ constexpr int kAreaQ = 8;                                   // items in flight p
 constexpr uint32_t kAreaFixedCost = 12288;  // data-aware warp balance: per-tuple fixed work, in (h+64)(w+16) units
 static_assert(kAreaQ == sizeof(ClsCtrl::astg[0]) / sizeof(uint64_t), "one mbarrier per AREA item in flight");
 constexpr uint32_t kAreaVBytes = 2u * 784u + 16u;           // V scratch: u16 per byte of a segment (+ overread)
-constexpr uint32_t kAreaRing = 6144u;                       // item ring
-constexpr uint32_t kAreaRegion = 2u * kAreaVBytes + kAreaRing;  // per converter warp: 2 V buffers + ring
-static_assert(kAreaRing >= 5u * 784u, "one worst-case AREA item (5 source rows of 784 B) must fit the ring");
-static_assert(1023 + kARing * kAKBlockBytes + 3 * 16384 + sizeof(ClsCtrl) + 15 + kConvWarps * kAreaRegion <=
-                  kClsSmemBytes,
-              "AREA staging exceeds shared memory");
+// per converter warp: V buffers (2 with two tuples per pass) + the item ring; the K4 AREA instance
+// with 12 converter warps (kAreaWarps) has room for one V buffer and a 5 KB ring per warp
+template <int kCW>
+struct AreaCfg {
+  static constexpr bool kPairItems = kCW == kConvWarps;
+  static constexpr uint32_t kRing = kCW == kConvWarps ? 6144u : (kCW <= 12 ? 5040u : 4384u);
+  static constexpr uint32_t kRegion = (kPairItems ? 2u : 1u) * kAreaVBytes + kRing;
+  static constexpr int kBS = kCW > 12 ? 2 : 3;  // the kernel's weight stages (16 KB each at N = 128)
+  static_assert(kRing >= 5u * 784u && kRing % 16u == 0, "one worst-case AREA item (5 source rows of 784 B) must fit the ring");
+  static_assert(1023 + kARing * kAKBlockBytes + kBS * 16384 + sizeof(ClsCtrl) + 15 + kCW * kRegion <= kClsSmemBytes,
+                "AREA staging exceeds shared memory");
+};
+constexpr int kAreaWarps = HYDRO_AREA_WARPS;  // converter warps of K4's AREA-only instance (launched beside K4-T)
 
 __device__ __forceinline__ uint32_t f16x2_of_bf16x2(uint32_t b) {  // exact (bf16 means of u8 pixels)
   uint32_t d;
@@ -579,13 +595,15 @@ __device__ __forceinline__ void sts32(uint32_t addr, uint32_t a) {
   asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(a) : "memory");
 }
 
-template <bool kDbg, int kP>
+template <bool kDbg, int kP, int kCW>
 __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* ctrl, uint32_t lim, uint32_t pos0,
                                                   uint32_t crank, int cu, int lane, uint32_t region, uint32_t a_ring,
                                                   uint32_t row_pitch, bool fp16, const RowMeta& mm, uint32_t my_row,
                                                   uint32_t& gg, uint32_t& qseq) {
   const uint8_t* frames = p.frames;
-  const uint32_t vbuf = region, ring = region + 2u * kAreaVBytes;
+  constexpr uint32_t kAreaRing = AreaCfg<kCW>::kRing;
+  constexpr bool kPairItems = AreaCfg<kCW>::kPairItems;
+  const uint32_t vbuf = region, ring = region + (kPairItems ? 2u : 1u) * kAreaVBytes;
   const uint32_t rcp_tab = smem_u32(ctrl->area_rcp);
   // tuple t of the band = lane t (valid tuples are a prefix: rows past the hop's count are masked)
   const uint32_t nv = __popc(__ballot_sync(0xFFFFFFFFu, lane < 16 && mm.valid));
@@ -670,8 +688,8 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
     const uint32_t a_set = a_ring + set * kAKBlockBytes;
     // two tuples per pass: their vertical sums in turn (the ring holds one worst-case item), then
     // the horizontal sums, divisions and stores of both interleaved
-    for (uint32_t t = 0; t < nv; t += 2) {
-      const bool two = t + 1 < nv;
+    for (uint32_t t = 0; t < nv; t += kPairItems ? 2u : 1u) {
+      const bool two = kPairItems && t + 1 < nv;
       uint32_t hb[2], xw[2];
       consume(g, t, vbuf, hb[0], xw[0]);
       if (two) consume(g, t + 1, vbuf + kAreaVBytes, hb[1], xw[1]);
@@ -764,7 +782,7 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
 // Converter warps (shared by the linear and the MLP classifier kernels): cp.async-staged crop-row
 // segments -> pixels -> the swizzled K-major A ring, one K-group (crop row g of all 128 tuples of
 // the CTA's M-tile) at a time, full_a / empty_a handshake with the MMA issuer.
-template <bool kDbg, bool kArea, int kP, int kQD>
+template <bool kDbg, bool kArea, int kP, int kQD, int kCW = kConvWarps>
 __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl, const uint32_t* list_in,
                                                uint32_t base, const TileWalk& tw, uint32_t crank, int warp, int lane,
                                                uint32_t staging_addr, uint32_t a_ring, uint32_t row_pitch, bool area,
@@ -779,9 +797,13 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
   uint32_t gg = 0, qseq = 0;
   for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
     const uint32_t pos0 = tw.pos0(unit);
-    // rows' metadata: lane l < 16 holds row 16*cu + l
-    uint32_t my_row = static_cast<uint32_t>(cu * kConvRows + (lane & 15));
-    RowMeta mm = load_meta(p, list_in, base, pos0 + my_row, lane < 16 ? tw.lim : 0u);
+    // rows' metadata: lane l < 16 holds this warp's l-th row (8 warps: rows 16*cu + l; 12 warps:
+    // 11 or 10 consecutive rows per warp, lanes past them hold none)
+    constexpr uint32_t kRowsLo = kTileM / kCW, kRowsRem = kTileM % kCW;
+    const uint32_t my_n = kRowsLo + (static_cast<uint32_t>(cu) < kRowsRem ? 1u : 0u);
+    const uint32_t my_base = static_cast<uint32_t>(cu) * kRowsLo + min(static_cast<uint32_t>(cu), kRowsRem);
+    uint32_t my_row = static_cast<uint32_t>(lane & 15) < my_n ? my_base + (lane & 15) : 0xFFu;
+    RowMeta mm = load_meta(p, list_in, base, pos0 + my_row, (lane < 16 && my_row < kTileM) ? tw.lim : 0u);
 #ifdef HYDRO_AREA_BAL_ALWAYS
     if (kArea && area) {
 #else
@@ -793,10 +815,11 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
       // ranked by it (ties: lower row first) and dealt to the warps in snake order (rank k -> warp
       // k % 8, or 7 - k % 8 on odd rounds, slot k / 8), so every warp's load is within one row of
       // the others' and the hop's invalid rows (ranked last) stay a suffix of every warp's slots
-      if (lane < 16)
+      if (lane < 16 && my_row < kTileM)
         ctrl->area_cost[my_row] =
             mm.valid ? kAreaFixedCost + static_cast<uint32_t>((mm.h + 64) * (mm.w + 16)) : 0u;
-      named_bar_sync(1, kConvWarps * 32);
+      if (kCW * 16 > kTileM && lane < 16) ctrl->area_perm[cu * 16 + lane] = 0xFFu;  // slots left empty
+      named_bar_sync(1, kCW * 32);
       if (cu < kTileM / 32) {
         const uint32_t m = static_cast<uint32_t>(cu * 32 + lane), cm = ctrl->area_cost[m];
         uint32_t k = 0;
@@ -804,12 +827,12 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
           const uint32_t cj = ctrl->area_cost[j];
           k += (cj > cm || (cj == cm && j < m)) ? 1u : 0u;
         }
-        const uint32_t s = k >> 3, c = (s & 1u) ? 7u - (k & 7u) : (k & 7u);
-        ctrl->area_perm[c * kConvRows + s] = static_cast<uint8_t>(m);
+        const uint32_t s = k / kCW, c = (s & 1u) ? kCW - 1u - k % kCW : k % kCW;
+        ctrl->area_perm[c * 16 + s] = static_cast<uint8_t>(m);
       }
-      named_bar_sync(1, kConvWarps * 32);
-      my_row = ctrl->area_perm[cu * kConvRows + (lane & 15)];
-      mm = load_meta(p, list_in, base, pos0 + my_row, lane < 16 ? tw.lim : 0u);
+      named_bar_sync(1, kCW * 32);
+      my_row = ctrl->area_perm[cu * 16 + (lane & 15)];
+      mm = load_meta(p, list_in, base, pos0 + my_row, (lane < 16 && my_row < kTileM) ? tw.lim : 0u);
     }
     // a tile with a crop wider than a staging slot (rare) runs the gather-staging variant
     const bool any_wide =
@@ -819,8 +842,9 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
     const bool area_big = kArea && area &&
                           __any_sync(0xFFFFFFFFu, lane < 16 && mm.valid && (mm.w > 256 || mm.h > 256));
     if (kArea && area && !any_wide && !area_big)
-      convert_tile_area<kDbg, kP>(p, ctrl, tw.lim, pos0, crank, cu, lane, staging_addr + cu * kAreaRegion, a_ring,
-                                  row_pitch, fp16, mm, my_row, gg, qseq);
+      convert_tile_area<kDbg, kP, kCW>(p, ctrl, tw.lim, pos0, crank, cu, lane,
+                                       staging_addr + cu * AreaCfg<kCW>::kRegion, a_ring, row_pitch, fp16, mm,
+                                       my_row, gg, qseq);
     else if (any_wide || area_big)
       convert_tile<kDbg, kArea, kP, kQD, true>(p, ctrl, list_in, tw.lim, pos0, crank, cu, lane, slots, a_ring, row_pitch,
                                                area, fp16, mm, my_row, gg);
@@ -838,8 +862,11 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
 
 extern __shared__ __align__(1024) uint8_t hydro_cls_smem[];
 
-template <bool kDbg, bool kArea>
-__global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsParams p) {
+template <bool kDbg, bool kArea, int kCW = kConvWarps>
+__global__ void __launch_bounds__((kConvWarp0 + kCW) * 32, 1) hydro_classifier_kernel(ClsParams p) {
+  // weight (B) stages: 3, or 2 for the instance with more than 12 converter warps (whose staging
+  // takes the third stage's 16 KB; the MMA is far from binding on AREA hops)
+  constexpr int kBS = kCW > 12 ? 2 : kBStages;
   DevState* st = p.st;
   // ---- dispatch (uniform across the CTA: every thread reads the same device words)
   int pred;
@@ -906,7 +933,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   uint8_t* smem = hydro_cls_smem + (((raw + 1023u) & ~1023u) - raw);
   const uint32_t a_ring = smem_u32(smem);
   const uint32_t b_ring = a_ring + kARing * kAKBlockBytes;
-  const uint32_t ctrl_off = kARing * kAKBlockBytes + kBStages * b_load_bytes;
+  const uint32_t ctrl_off = kARing * kAKBlockBytes + kBS * b_load_bytes;
   ClsCtrl* ctrl = reinterpret_cast<ClsCtrl*>(smem + ctrl_off);
   const uint32_t stg_off = (ctrl_off + static_cast<uint32_t>(sizeof(ClsCtrl)) + 15u) & ~15u;
   uint8_t* staging = smem + stg_off;
@@ -915,10 +942,10 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < kARing; ++s) {
-      mbar_init(&ctrl->full_a[s], kConvWarps * kPair);
+      mbar_init(&ctrl->full_a[s], kCW * kPair);
       mbar_init(&ctrl->empty_a[s], 1);
     }
-    for (int s = 0; s < kBStages; ++s) {
+    for (int s = 0; s < kBS; ++s) {
       mbar_init(&ctrl->full_b[s], crank == 0 ? kPair : 1);  // pair: + the peer's relay
       mbar_init(&ctrl->empty_b[s], 1);
     }
@@ -927,7 +954,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       mbar_init(&ctrl->tempty[a], kEpiWarps * kPair);
     }
     if (kArea)
-      for (int w = 0; w < kConvWarps; ++w)
+      for (int w = 0; w < kCW; ++w)
         for (int s = 0; s < kAreaQ; ++s) mbar_init(&ctrl->astg[w][s], 1);
     fence_mbar_init();
   }
@@ -1002,7 +1029,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
           if (g < kGroups) prefetch_group(g);
         }
         if (lane == 0) {
-          const uint32_t s = itb % kBStages, ph = (itb / kBStages) & 1u;
+          const uint32_t s = itb % kBS, ph = (itb / kBS) & 1u;
           HYDRO_PIPE_WAIT(&ctrl->empty_b[s], ph ^ 1u);
           mbar_arrive_expect_tx(&ctrl->full_b[s], b_load_bytes);
           bulk_g2s_hint(smem + (b_ring - a_ring) + s * b_load_bytes,
@@ -1013,7 +1040,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       }
     }
     if (kPair == 2 && lane == 0) {  // drain: every B stage released (the leader's commits land here)
-      for (int e = 0; e < kBStages; ++e, ++itb) mbar_wait(&ctrl->empty_b[itb % kBStages], ((itb / kBStages) & 1u) ^ 1u);
+      for (int e = 0; e < kBS; ++e, ++itb) mbar_wait(&ctrl->empty_b[itb % kBS], ((itb / kBS) & 1u) ^ 1u);
     }
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (single thread)
@@ -1022,8 +1049,8 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
       uint32_t itb = 0;
       for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
         for (int kb = 0; kb < kNumKBlocks; ++kb, ++itb) {
-          const uint32_t s = itb % kBStages;
-          mbar_wait(&ctrl->full_b[s], (itb / kBStages) & 1u);
+          const uint32_t s = itb % kBS;
+          mbar_wait(&ctrl->full_b[s], (itb / kBS) & 1u);
           mbar_arrive_leader(&ctrl->full_b[s]);
         }
       }
@@ -1040,7 +1067,7 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
 #pragma unroll
           for (int kbr = 0; kbr < kKBlocksPerGroup; ++kbr, ++itb) {
             const uint32_t sa = set + kbr;
-            const uint32_t sb = itb % kBStages, bph = (itb / kBStages) & 1u;
+            const uint32_t sb = itb % kBS, bph = (itb / kBS) & 1u;
             // (pair: the leader's barriers also count the peer's remote arrivals)
             HYDRO_PIPE_WAIT(&ctrl->full_a[sa], aph2);
             HYDRO_PIPE_WAIT(&ctrl->full_b[sb], bph);
@@ -1071,8 +1098,8 @@ __global__ void __launch_bounds__(kClsThreads, 1) hydro_classifier_kernel(ClsPar
     }
     __syncwarp();
   } else if (warp >= kConvWarp0) {
-    converter_role<kDbg, kArea, kPair, kQuadDepth>(p, ctrl, list_in, base, tw, crank,
-                                                   warp, lane, staging_addr, a_ring, row_pitch, area, fp16);
+    converter_role<kDbg, kArea, kPair, kQuadDepth, kCW>(p, ctrl, list_in, base, tw, crank, warp, lane, staging_addr,
+                                                        a_ring, row_pitch, area, fp16);
   } else {
     // ===================== epilogue warps 0..3 (TMEM lane quadrant = warp)
     const int q = warp;
@@ -2022,6 +2049,7 @@ __global__ void __launch_bounds__(256) hydro_cache_split_kernel(ClsParams p) {
 cudaError_t hydro_classifier_configure() {
   void (*ks[])(ClsParams) = {hydro_classifier_kernel<false, false>, hydro_classifier_kernel<true, false>,
                              hydro_classifier_kernel<false, true>, hydro_classifier_kernel<true, true>,
+                             hydro_classifier_kernel<false, true, kAreaWarps>, hydro_classifier_kernel<true, true, kAreaWarps>,
                              hydro_mlp_kernel<false>, hydro_mlp_kernel<true>,
                              hydro_classifier_tm_kernel<false>, hydro_classifier_tm_kernel<true>};
   for (auto k : ks) {
@@ -2057,6 +2085,12 @@ void launch_pairs(void (*k)(ClsParams), int* max_clusters, const ClsParams& c, i
 }  // namespace
 
 void hydro_classifier_launch(const ClsParams& c, int grid, cudaStream_t stream, bool debug, bool area) {
+  if (kPair == 1 && area && c.area_only) {  // AREA hops only: the instance with 12 converter warps
+    void (*ka)(ClsParams) = debug ? hydro_classifier_kernel<true, true, kAreaWarps>
+                                  : hydro_classifier_kernel<false, true, kAreaWarps>;
+    ka<<<grid, (kConvWarp0 + kAreaWarps) * 32, kClsSmemBytes, stream>>>(c);
+    return;
+  }
   void (*k)(ClsParams) = area ? (debug ? hydro_classifier_kernel<true, true> : hydro_classifier_kernel<false, true>)
                               : (debug ? hydro_classifier_kernel<true, false> : hydro_classifier_kernel<false, false>);
   if constexpr (kPair == 2) {
