@@ -19,4 +19,8 @@ ncu --set full --clock-control none --import-source on -k regex:hydro_classifier
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"hydro_route|hydro_compact" -s 20 -c 2 -o $O/route_full -f \
   python bench.py --workload rroute --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+# the AREA hop alone (cfg4's AREA head on 1M crops, 16-converter-warp K4 instance)
+python tools/area_probe.py 5 > $O/area_probe.json 2> $O/area_probe.err
+ncu --set full --clock-control none --import-source on -k regex:hydro_classifier_kernel -s 2 -c 1 -o $O/area_full -f \
+  python tools/area_probe.py 1 > /dev/null 2>&1
 ls -la $O
