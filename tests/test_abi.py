@@ -111,3 +111,19 @@ def test_no_gpu_fails_loudly():
     with pytest.raises(H.HydroError) as e:
         H.hydro_create(cfg)
     assert e.value.status == H.HYDRO_ECUDA
+
+
+def test_crop_k_orders_are_row_permutations(tmp_path):
+    """The three crop-row K orders of hydro_internal.cuh (K4, K4-T, K4's AREA converter; the weight
+    tiling applies the same maps) are permutations of each crop row's 192 features, and the AREA
+    order matches its converter's lane mapping (lane q -> pixels q, q + 32)."""
+    import shutil
+    import subprocess
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(nvcc):
+        pytest.skip("nvcc not available")
+    src = os.path.join(ROOT, "tools", "check_k_orders.cu")
+    exe = str(tmp_path / "check_k_orders")
+    subprocess.run([nvcc, "-std=c++17", "-o", exe, src], check=True, capture_output=True)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout
