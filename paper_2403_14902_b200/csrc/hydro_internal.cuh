@@ -55,6 +55,10 @@ constexpr int kQuadDepth = HYDRO_QUAD_DEPTH;                // quads staged ahea
 constexpr int kQuadSlots = kQuadDepth + 1;
 constexpr int kQuadSlotBytes = 4 * kSegPitch;               // 4 rows x worst-case segment
 constexpr int kClsSmemBytes = 232448;                       // 227 KB opt-in maximum
+// data-aware AREA hops (R28): K6's per-CTA position ranges are used while the hop has fewer than
+// this many 128-tuple tiles per CTA (the tail dominates); beyond, tiles are dealt round-robin and
+// the balance is the warp-level row assignment inside every tile
+constexpr uint32_t kBalRangeTilesPerCta = 4;
 
 // K order of the A operand inside one crop row (192 = 64 px x 3 ch elements):
 // converter lane j of a row produces output pixels dx = j + 8k (k = 0..7, interleaved so that the

@@ -57,7 +57,8 @@ __device__ __forceinline__ HopIn resolve_hop(const ClsParams& p) {
 
 __global__ void hydro_balance_cost_kernel(ClsParams p) {
   const HopIn hi = resolve_hop(p);
-  if (!hi.area) return;
+  // (a hop with >= kBalRangeTilesPerCta tiles per CTA runs round-robin tiles: no ranges needed)
+  if (!hi.area || hi.count >= kBalRangeTilesPerCta * kTileM * static_cast<uint32_t>(p.bal_ctas)) return;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t n_chunks = (hi.count + 31u) / 32u;
   const uint32_t warps = gridDim.x * (blockDim.x / 32u);
@@ -80,7 +81,8 @@ constexpr int kBalThreads = 1024;
 
 __global__ void __launch_bounds__(kBalThreads) hydro_balance_bounds_kernel(ClsParams p) {
   const HopIn hi = resolve_hop(p);
-  if (!hi.area) return;
+  // (a hop with >= kBalRangeTilesPerCta tiles per CTA runs round-robin tiles: no ranges needed)
+  if (!hi.area || hi.count >= kBalRangeTilesPerCta * kTileM * static_cast<uint32_t>(p.bal_ctas)) return;
   __shared__ unsigned long long warp_tot[kBalThreads / 32];
   const uint32_t G = static_cast<uint32_t>(p.bal_ctas);
   const uint32_t n_chunks = (hi.count + 31u) / 32u;

@@ -154,7 +154,8 @@ struct TileWalk {
   uint32_t first, step, end;  // units
   uint32_t lo, lim;           // positions >= lim are invalid
   uint32_t kp, crank;
-  bool bal;
+  bool bal;   // K6 position ranges (data-aware, few tiles per CTA)
+  bool wbal;  // data-aware: rows dealt to the converter warps by estimated work
   __device__ __forceinline__ uint32_t pos0(uint32_t unit) const {
     return bal ? lo + unit * static_cast<uint32_t>(kTileM) : (unit * kp + crank) * static_cast<uint32_t>(kTileM);
   }
@@ -807,7 +808,7 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
 #ifdef HYDRO_AREA_BAL_ALWAYS
     if (kArea && area) {
 #else
-    if (kArea && area && tw.bal) {
+    if (kArea && area && tw.wbal) {
 #endif
       // data-aware AREA tiles (R28) at warp granularity: the converter warps are the tile's
       // workers; each tile row's work is estimated from its input size, kAreaFixedCost + (h + 64)(w + 16)
@@ -903,7 +904,9 @@ __global__ void __launch_bounds__((kConvWarp0 + kCW) * 32, 1) hydro_classifier_k
   // the same units, so a pair's last unit may hold a tile past num_tiles (all rows invalid)
   const uint32_t crank = kPair == 2 ? cluster_ctarank() : 0u;
   TileWalk tw{blockIdx.x / kPair, gridDim.x / kPair, (num_tiles + kPair - 1) / kPair, 0u, count, kPair, crank, false};
-  if (kPair == 1 && area && p.bounds && !ind) {  // data-aware: this CTA's balanced position range
+  const bool data_aware = kPair == 1 && area && p.bounds && !ind;
+  tw.wbal = data_aware;
+  if (data_aware && count < kBalRangeTilesPerCta * kTileM * gridDim.x) {  // this CTA's balanced position range
     tw.bal = true;
     tw.lo = min(p.bounds[blockIdx.x], count);
     tw.lim = min(p.bounds[blockIdx.x + 1], count);
