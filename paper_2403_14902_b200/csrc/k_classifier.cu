@@ -568,7 +568,10 @@ constexpr uint32_t kAreaVBytes = 2u * 784u + 16u;           // V scratch: u16 pe
 template <int kCW>
 struct AreaCfg {
   static constexpr bool kPairItems = kCW == kConvWarps;
-  static constexpr uint32_t kRing = kCW == kConvWarps ? 6144u : (kCW <= 12 ? 5040u : 4384u);
+#ifndef HYDRO_AREA_RING16
+#define HYDRO_AREA_RING16 4096u
+#endif
+  static constexpr uint32_t kRing = kCW == kConvWarps ? 6144u : (kCW <= 12 ? 5040u : HYDRO_AREA_RING16);
   static constexpr uint32_t kRegion = (kPairItems ? 2u : 1u) * kAreaVBytes + kRing;
   static constexpr int kBS = kCW > 12 ? 2 : 3;  // the kernel's weight stages (16 KB each at N = 128)
   static_assert(kRing >= 5u * 784u && kRing % 16u == 0, "one worst-case AREA item (5 source rows of 784 B) must fit the ring");
