@@ -356,7 +356,8 @@ def run_gpu(args):
     traffic, traffic_note = _profile_traffic("k4_dram_traffic.json")
 
     # ---- e2e through the C ABI with pinned host buffers
-    host_batches = [batches[b].to("cpu", pin=True) for b in range(2)]
+    depth = args.e2e_depth  # batches in flight (2: measured no worse than 3, less noisy)
+    host_batches = [batches[b].to("cpu", pin=True) for b in range(depth)]
     out_ids = torch.empty(1 << 20, dtype=torch.int64).pin_memory()
     out_bb = torch.empty((1 << 20, 4), dtype=torch.int16).pin_memory()
     h2d = host_batches[0].nbytes()
@@ -365,8 +366,8 @@ def run_gpu(args):
     def e2e_steps(k):
         pend = []
         for s in range(k):
-            pend.append(e.submit(host_batches[s % 2]))
-            if len(pend) >= 2:
+            pend.append(e.submit(host_batches[s % depth]))
+            if len(pend) >= depth:
                 n = e.collect_into(pend.pop(0), out_ids, out_bb)
                 d2h.append(16 * n)
         for bid in pend:
@@ -969,6 +970,7 @@ def run_small(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--e2e-depth", type=int, default=2, help="batches in flight in the e2e (host buffer) run")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hydro", choices=["hydro", "reference"])
