@@ -143,7 +143,7 @@ typedef struct {
   const uint8_t* frames;     /* DEVICE frame pool, HWC uint8 [n_frames][frame_h][frame_w][3],
                                 BORROWED for the context's lifetime (R11); may be NULL when no
                                 LINEAR predicate is used                                      */
-  int32_t n_frames, frame_h, frame_w; /* frame_w % 16 == 0, frames 16-byte aligned, pool < 4 GiB */
+  int32_t n_frames, frame_h, frame_w; /* frame_w % 16 == 0, frames 16-byte aligned, pool < 64 GiB */
   int32_t balance;           /* HYDRO_BALANCE_*: how a classifier hop's tiles are spread over the
                                 SMs (default ROUND_ROBIN)                                     */
   int32_t max_sms;           /* SM budget of the context's persistent kernels (grids capped at

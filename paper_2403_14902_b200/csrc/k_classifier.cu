@@ -111,12 +111,17 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 }
 
 struct RowMeta {  // per alive tuple of the tile
-  uint32_t row0;     // byte offset of (frame, y0, 0) in the frame pool
+  uint32_t row16;    // offset of (frame, y0, 0) in the frame pool, in 16-byte units (pools < 64 GiB)
   uint32_t seg_lo;   // 16-byte aligned start of the crop's byte span inside a frame row
   uint32_t seg_len;  // bytes to stage per crop row (multiple of 16), 0 when invalid
   int32_t x0, w, h;
   int32_t valid;
 };
+
+// frame-pool address of a 16-byte-unit offset (64-bit: the pool may exceed 4 GiB)
+__device__ __forceinline__ const uint8_t* at16(const uint8_t* frames, uint32_t off16) {
+  return frames + (static_cast<uint64_t>(off16) << 4);
+}
 
 __device__ __forceinline__ RowMeta load_meta(const ClsParams& p, const uint32_t* list_in, uint32_t base,
                                              uint32_t pos, uint32_t count) {
@@ -135,7 +140,9 @@ __device__ __forceinline__ RowMeta load_meta(const ClsParams& p, const uint32_t*
   x1 = max(min(x1, p.frame_w), x0 + 1);
   y1 = max(min(y1, p.frame_h), y0 + 1);
   const uint32_t pitch = static_cast<uint32_t>(p.frame_w * 3);
-  m.row0 = fid * static_cast<uint32_t>(p.frame_h) * pitch + static_cast<uint32_t>(y0) * pitch;
+  // (the frame row pitch 3 * frame_w is a multiple of 48, so every row starts on 16 bytes)
+  m.row16 = static_cast<uint32_t>((static_cast<uint64_t>(fid) * static_cast<uint32_t>(p.frame_h) * pitch +
+                                   static_cast<uint64_t>(y0) * pitch) >> 4);
   m.seg_lo = (3u * x0) & ~15u;
   m.seg_len = ((3u * x1 + 15u) & ~15u) - m.seg_lo;  // frame_w % 16 == 0 keeps this inside the row
   m.x0 = x0;
@@ -443,7 +450,7 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
   constexpr int kQS = kQD + 1;
   const int r = lane >> 3, j = lane & 7;
   const uint8_t* frames = p.frames;
-  const uint32_t my_src = mm.row0 + mm.seg_lo;                 // + sy * pitch per crop row
+  const uint32_t my_src = mm.row16 + (mm.seg_lo >> 4);         // 16-byte units; + sy * pitch per crop row
   const bool my_wide = kWide && lane < 16 && mm.valid && mm.seg_len > static_cast<uint32_t>(kMaxSegBytes);
   // staged bytes per crop row: the segment, or (wide rows) a negative marker for the gather
   const uint32_t my_len = (lane < 16 && mm.valid) ? (my_wide ? 0xFFFFFFFFu : mm.seg_len) : 0u;
@@ -476,7 +483,7 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
       const uint32_t off = __shfl_sync(0xFFFFFFFFu, my_src, src_lane);
       const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, src_lane);
       const uint32_t xw = kWide ? __shfl_sync(0xFFFFFFFFu, my_xw, src_lane) : 0u;  // (all lanes: before the branch)
-      const uint8_t* row = frames + (off + (((2u * g + 1u) * h) >> 7) * row_pitch);
+      const uint8_t* row = at16(frames, off) + (((2u * g + 1u) * h) >> 7) * row_pitch;
       const uint32_t dst = slots + slot * kQuadSlotBytes + r * kSegPitch;
       if (!kWide || len != 0xFFFFFFFFu) {
         stage_segment(dst, row, j, len >> 4);
@@ -514,7 +521,7 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
       uint32_t ar0 = 0, ah = 0, ax0 = 0, aw = 0;
       if (kArea && area) {  // (all lanes shuffle before the per-row branch below)
         const int src_lane = 4 * it + r;
-        ar0 = __shfl_sync(0xFFFFFFFFu, mm.row0, src_lane);
+        ar0 = __shfl_sync(0xFFFFFFFFu, mm.row16, src_lane);
         ah = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.h), src_lane);
         ax0 = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.x0), src_lane);
         aw = __shfl_sync(0xFFFFFFFFu, static_cast<uint32_t>(mm.w), src_lane);
@@ -522,8 +529,8 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
       if (!row_ok) {
       } else if (kArea && area) {
         uint16_t* dbg_row = dbg ? dbg - 3 * j : nullptr;  // (AREA K order: the crop row's features)
-        if (fp16) convert_quad_area<true, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg_row);
-        else convert_quad_area<false, kDbg>(frames, ar0, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg_row);
+        if (fp16) convert_quad_area<true, kDbg>(at16(frames, ar0), 0u, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg_row);
+        else convert_quad_area<false, kDbg>(at16(frames, ar0), 0u, ah, ax0, aw, row_pitch, g, row_base, j, m, dbg_row);
       } else {
         if (fp16) convert_quad<true, kDbg>(seg, po[it], row_base, j, m, dbg);
         else convert_quad<false, kDbg>(seg, po[it], row_base, j, m, dbg);
@@ -611,7 +618,7 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
   const uint32_t rcp_tab = smem_u32(ctrl->area_rcp);
   // tuple t of the band = lane t (valid tuples are a prefix: rows past the hop's count are masked)
   const uint32_t nv = __popc(__ballot_sync(0xFFFFFFFFu, lane < 16 && mm.valid));
-  const uint32_t my_src = mm.row0 + mm.seg_lo, my_len = mm.seg_len, my_h = static_cast<uint32_t>(mm.h);
+  const uint32_t my_src = mm.row16 + (mm.seg_lo >> 4), my_len = mm.seg_len, my_h = static_cast<uint32_t>(mm.h);
   const uint32_t my_xw = static_cast<uint32_t>(mm.x0) | (static_cast<uint32_t>(mm.w) << 16);
   const uint32_t total = kGroups * nv;
   // this lane's 3 A words: byte o = 12q + 4i of the 384-byte crop row -> K-block o / 128, 16-byte
@@ -645,7 +652,7 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
       if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
       __syncwarp();
       if (static_cast<uint32_t>(lane) < hbp)
-        bulk_g2s_u32(ring + ps % kAreaRing + lane * Lp, frames + (srcp + (ysp + lane) * row_pitch), Lp, bar);
+        bulk_g2s_u32(ring + ps % kAreaRing + lane * Lp, at16(frames, srcp) + (ysp + lane) * row_pitch, Lp, bar);
       pcur = ps + bytes;
       ++pk;
       if (++pt == nv) {
@@ -1014,13 +1021,13 @@ __global__ void __launch_bounds__((kConvWarp0 + kCW) * 32, 1) hydro_classifier_k
             const uint32_t h = static_cast<uint32_t>(mr[r].h);
             const uint32_t ys = (static_cast<uint32_t>(g) * h) >> 6, ye = ((static_cast<uint32_t>(g) + 1u) * h + 63u) >> 6;
             for (uint32_t y = ys; y < ye; ++y) {
-              const uint8_t* a = p.frames + mr[r].row0 + y * row_pitch + mr[r].seg_lo;
+              const uint8_t* a = at16(p.frames, mr[r].row16) + y * row_pitch + mr[r].seg_lo;
               for (uint32_t c = 0; c < mr[r].seg_len; c += 128u) prefetch_line_l2(a + c);
             }
             continue;
           }
           const uint32_t sy = static_cast<uint32_t>(((2 * g + 1) * mr[r].h) >> 7);
-          const uint8_t* a = p.frames + mr[r].row0 + sy * row_pitch + mr[r].seg_lo;
+          const uint8_t* a = at16(p.frames, mr[r].row16) + sy * row_pitch + mr[r].seg_lo;
 #if defined(HYDRO_L2_PREFETCH)  // measured slightly slower on B200 (line-granular overfetch, L2 pressure)
           for (uint32_t c = 0; c < mr[r].seg_len; c += 128u) prefetch_line_l2(a + c);
 #else
@@ -1602,7 +1609,7 @@ __device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl
   }
   // staging: lanes (r = lane/8, j = lane%8) copy segment 4*pass + r in 16-byte chunks j + 8c
   const int r = lane >> 3, j = lane & 7;
-  const uint32_t my_src = mm.row0 + mm.seg_lo;
+  const uint32_t my_src = mm.row16 + (mm.seg_lo >> 4);  // 16-byte units
   const uint32_t my_h = static_cast<uint32_t>(mm.h);
   const uint32_t my_lo = slen | (soff << 16);
   const uint32_t my_xw =
@@ -1617,7 +1624,7 @@ __device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl
         if (lane == 0) mbar_arrive_expect_tx(bar, utot);
         __syncwarp();
         if (slen != 0) {
-          const uint8_t* row = frames + (my_src + (((2u * g + 1u) * my_h) >> 7) * row_pitch);
+          const uint8_t* row = at16(frames, my_src) + (((2u * g + 1u) * my_h) >> 7) * row_pitch;
           bulk_g2s_u32(ring + slot * ubytes + soff, row, slen, bar);
         }
       }
@@ -1633,7 +1640,7 @@ __device__ __forceinline__ void tm_convert_tile(const ClsParams& p, TmCtrl* ctrl
         const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, L);
         const uint32_t xw = kWide ? __shfl_sync(0xFFFFFFFFu, my_xw, L) : 0u;
         const uint32_t len = lo & 0xFFFFu;
-        const uint8_t* row = frames + (off + (((2u * g + 1u) * h) >> 7) * row_pitch);
+        const uint8_t* row = at16(frames, off) + (((2u * g + 1u) * h) >> 7) * row_pitch;
         const uint32_t dst = dst0 + (lo >> 16);
         if (!kWide || !(xw >> 31)) stage_segment(dst, row, j, len >> 4);
         else stage_wide_row(dst, row, xw & 0x7FFFFFFFu, j);  // wide crop (rare): 64-pixel gather

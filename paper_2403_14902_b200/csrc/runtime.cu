@@ -335,8 +335,8 @@ hydro_status hydro_create(const hydro_config* cfg, hydro_ctx** out) {
         cfg->frame_h > 65535 || cfg->frame_w > 65535)
       return set_err(HYDRO_EINVAL, "frame pool: n_frames, frame_h >= 1; frame_w % 16 == 0; dims <= 65535");
     if ((reinterpret_cast<uintptr_t>(cfg->frames) & 15u) != 0) return set_err(HYDRO_EINVAL, "frames must be 16-byte aligned");
-    if (static_cast<double>(cfg->n_frames) * cfg->frame_h * cfg->frame_w * 3 >= 4294967296.0)
-      return set_err(HYDRO_EINVAL, "frame pool must be < 4 GiB");
+    if (static_cast<double>(cfg->n_frames) * cfg->frame_h * cfg->frame_w * 3 >= 68719476736.0)
+      return set_err(HYDRO_EINVAL, "frame pool must be < 64 GiB");  // row offsets in 16-byte units (u32)
   }
   ctx = new hydro_ctx();
   ctx->cfg = *cfg;

@@ -601,6 +601,46 @@ def test_wide_and_tall_crops_area():
     e.close()
 
 
+def test_frame_pool_beyond_4_gib():
+    """A 4.4 GB frame pool (1600 720p frames): tuples in the last frames, past the 4 GiB offset
+    (frame rows addressed in 16-byte units): nearest crops on K4-T and AREA crops on K4 are bit-exact,
+    and the linear heads' logits are within 1e-2 of the oracle's."""
+    from synth import Tuples, make_frames
+    from paper_2403_14902_b200.hydro import Eddy
+
+    F, H, W = 1600, 720, 1280
+    pool = torch.empty((F, H, W, 3), dtype=torch.uint8, device="cuda")
+    fids = list(range(F - 8, F))
+    make_frames(12, F, H, W, device="cuda", frame_ids=fids, out=pool[F - 8:])
+    assert (F - 8) * H * W * 3 > 2 ** 32
+    fr = make_frames(12, F, H, W, frame_ids=fids).numpy()  # the same frames on the host (oracle)
+    n = 300
+    g = torch.Generator().manual_seed(7)
+    w = torch.randint(1, 256, (n,), generator=g)
+    h = torch.randint(1, 256, (n,), generator=g)
+    x0 = (torch.rand(n, generator=g) * (W - w + 1).double()).long()
+    y0 = (torch.rand(n, generator=g) * (H - h + 1).double()).long()
+    bbox = torch.stack([x0, y0, x0 + w, y0 + h], 1).to(torch.int16)
+    local = torch.arange(n, dtype=torch.int32) % 8
+    t = Tuples(torch.arange(n, dtype=torch.int64), local + (F - 8), bbox, torch.full((n,), 16, dtype=torch.int16))
+    tup = O.as_numpy_tuples(t)
+    for mode, p in (("nearest", workload("cfg2", small=True, n=100).preds[1]),
+                    ("area", workload("cfg4", small=True, n=100).preds[3])):
+        e = Eddy(frames=pool, policy="fixed", warmup_tuples=0, max_batch_tuples=4096)
+        k = e.add_predicate(p)
+        C = p["n_classes"]
+        logits = torch.full((n, C), float("nan"), device="cuda")
+        crops = torch.zeros((n, O.K_FEATURES), dtype=torch.int16, device="cuda")
+        e.debug_linear(k, t.to("cuda"), logits, crops, None)
+        e.close()
+        crop_fn = O.crop_area if mode == "area" else O.crop_nearest
+        ref = crop_fn(fr, local.numpy(), tup["bbox"]).reshape(n, -1)
+        assert np.array_equal(crops.view(torch.bfloat16).float().cpu().numpy(), ref.astype(np.float32)), mode
+        _, z_ref = O.linear_verdict(p, fr, local.numpy(), tup["bbox"], return_logits=True)
+        assert np.abs(logits.double().cpu().numpy() - z_ref).max() <= LOGIT_TOL, mode
+    del pool
+
+
 # ------------------------------------------------------------- data-aware tile scheduling (f4, R28)
 
 @pytest.mark.parametrize("n", [700, 9000, 20000])
