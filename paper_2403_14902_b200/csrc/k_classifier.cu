@@ -561,7 +561,7 @@ __device__ __forceinline__ void convert_tile(const ClsParams& p, ClsCtrl* ctrl, 
 //   horizontal: lane q makes output pixels q and q + 32: each channel's bin sum is the sum of V over
 //               the bin's columns (<= 5 terms; the 3 channels of a column from two aligned words),
 //               then one f32 RN division (area_div with y = RN(1/count) from a table), bf16 RNE, and
-//               the 6 features go to A row 16*cu + t as 3 words at positions 6q .. 6q+5
+//               the 6 features go to the tuple's A row as 3 words at positions 6q .. 6q+5
 //               (crop_pos_feature_area).
 // Per source pixel the warp issues one shared load per 16 bytes (instead of 2 per pixel per bin),
 // and every lane works on the same tuple (no divergence between bin widths of different tuples).
@@ -800,16 +800,18 @@ __device__ __forceinline__ void converter_role(const ClsParams& p, ClsCtrl* ctrl
                                                bool fp16) {
   constexpr int kQS = kQD + 1;
   // ===================== converters: cp.async-staged segments -> pixels -> swizzled A ring
-  // Warp cu owns rows 16*cu .. 16*cu+15; it walks them as "quads" of 4 rows (one warp
-  // instruction = 4 rows x 8 lanes x 8 output pixels).  Quad k's source segments are
-  // copied (16-byte cp.async, coalesced per row) kQD quads ahead into fixed slots.
+  // Warp cu owns up to 16 rows of the tile (kCW = 8: rows 16*cu .. 16*cu+15; the AREA instance's
+  // 16 warps: 8 rows each; data-aware AREA tiles: the rows dealt to it by estimated work).  Nearest
+  // and wide tiles walk them as "quads" of 4 rows (one warp instruction = 4 rows x 8 lanes x 8
+  // output pixels), their source segments copied (16-byte cp.async) kQD quads ahead into fixed
+  // slots; AREA tiles run the row-cooperative converter (convert_tile_area).
   const int cu = warp - kConvWarp0;
   const uint32_t slots = staging_addr + static_cast<uint32_t>(cu) * (kQS * kQuadSlotBytes);
   uint32_t gg = 0, qseq = 0;
   for (uint32_t unit = tw.first; unit < tw.end; unit += tw.step) {
     const uint32_t pos0 = tw.pos0(unit);
-    // rows' metadata: lane l < 16 holds this warp's l-th row (8 warps: rows 16*cu + l; 12 warps:
-    // 11 or 10 consecutive rows per warp, lanes past them hold none)
+    // rows' metadata: lane l < 16 holds this warp's l-th row (8 warps: rows 16*cu + l; 16 warps:
+    // rows 8*cu + l; other counts: floor or ceil of 128/kCW consecutive rows; lanes past them hold none)
     constexpr uint32_t kRowsLo = kTileM / kCW, kRowsRem = kTileM % kCW;
     const uint32_t my_n = kRowsLo + (static_cast<uint32_t>(cu) < kRowsRem ? 1u : 0u);
     const uint32_t my_base = static_cast<uint32_t>(cu) * kRowsLo + min(static_cast<uint32_t>(cu), kRowsRem);
