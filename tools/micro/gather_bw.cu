@@ -12,7 +12,7 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 }
 extern __shared__ __align__(128) uint8_t smem[];
 __global__ void gather(const uint8_t* pool, uint64_t pool_rows, uint32_t pitch, int units_per_warp, int slots,
-                       int slot_bytes, unsigned long long* bytes_out) {
+                       int slot_bytes, unsigned long long* bytes_out, uint32_t wmin) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint8_t* ring = smem + 4096 + warp * slots * slot_bytes;  // [32 warps x 16 mbarriers][rings]
@@ -23,7 +23,7 @@ __global__ void gather(const uint8_t* pool, uint64_t pool_rows, uint32_t pitch, 
   uint32_t par = 0;
   auto seg = [&](int u, uint32_t& off, uint32_t& len, uint64_t& row) {
     const uint32_t h = hash32((blockIdx.x * nw + warp) * 1000003u + u * 131u + lane);
-    const uint32_t oct = h % 3, w = (32u << oct) + ((h >> 8) % (32u << oct));
+    const uint32_t oct = h % 3, w = (wmin << oct) + ((h >> 8) % (wmin << oct));
     const uint32_t x0 = (h >> 16) % (1280u - w);
     off = (3u * x0) & ~15u;
     len = ((3u * (x0 + w) + 15u) & ~15u) - off;
@@ -71,23 +71,26 @@ int main() {
   unsigned long long* b; cudaMalloc(&b, 8);
   cudaFuncSetAttribute(gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
   const int slot_bytes = 6144;  // cfg2's units average ~5.6 KB (K4-T packs them into 22 KB rings)
-  int cfgs[][2] = {{8, 2}, {8, 3}, {8, 4}, {16, 2}, {24, 1}, {32, 1}};
+  int cfgs[][3] = {{8, 2, 32}, {8, 3, 32}, {16, 2, 32}, {32, 1, 32}, {8, 3, 16}, {16, 2, 16}, {8, 3, 8}, {16, 2, 8}};
   for (auto& c : cfgs) {
     const int wpc = c[0], slots = c[1];
+    const uint32_t wmin = c[2];
     const size_t sm = 4096 + (size_t)wpc * slots * slot_bytes;
     if (sm > 232448) { printf("W %d S %d: smem %zu too big\n", wpc, slots, sm); continue; }
     const int units = 4000;
     cudaMemset(b, 0, 8);
-    gather<<<148, wpc * 32, sm>>>(pool, rows, pitch, 200, slots, slot_bytes, b);  // warm
+    gather<<<148, wpc * 32, sm>>>(pool, rows, pitch, 200, slots, slot_bytes, b, wmin);  // warm
     cudaMemset(b, 0, 8);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    gather<<<148, wpc * 32, sm>>>(pool, rows, pitch, units, slots, slot_bytes, b);
+    gather<<<148, wpc * 32, sm>>>(pool, rows, pitch, units, slots, slot_bytes, b, wmin);
     cudaEventRecord(e1);
     cudaError_t err = cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long hb; cudaMemcpy(&hb, b, 8, cudaMemcpyDeviceToHost);
-    printf("W %2d S %d: %.1f GB/s of segment bytes (%.2f GB in %.2f ms) %s\n", wpc, slots, hb / (ms * 1e6), hb / 1e9, ms,
+    const double copies = 148.0 * wpc * units * 16;
+    printf("w >= %2u W %2d S %d: %.1f GB/s of segment bytes (%.2f GB in %.2f ms), %.1f M copies/ms/SM %s\n", wmin, wpc, slots,
+           hb / (ms * 1e6), hb / 1e9, ms, copies / ms / 148 / 1e6,
            err ? cudaGetErrorString(err) : "");
     fflush(stdout);
   }
