@@ -530,6 +530,14 @@ def run_route(args):
     peaks = _peaks()
     achieved = alg_bytes / ((k1_ms + k2_ms) / 1000.0) / 1e9
     achieved_step = alg_bytes / (ms / 1000.0) / 1e9
+    # bytes K1 + K2 actually move per 16M-tuple batch (ncu dram__bytes of one working launch of each,
+    # profiles/route_k{1,2}_dram_traffic.json stamped with the sources they were captured on)
+    t1, n1_note = _profile_traffic("route_k1_dram_traffic.json")
+    t2, n2_note = _profile_traffic("route_k2_dram_traffic.json")
+    route_traffic = (t1 + t2) if (t1 and t2) else None
+    route_traffic_note = n1_note + "; " + n2_note
+    route_traffic_frac = (route_traffic * args.steps * nb / ((k1_ms + k2_ms) / 1000.0) / 1e9 / peaks["hbm_gbs"]
+                          if route_traffic and k1_ms + k2_ms > 0 else None)
     out = {"metric": "tuples/s through the 3-predicate cheap conjunction (R-route evidence for K1+K2)",
            "value": tuples / (ms / 1000.0), "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -542,7 +550,9 @@ def run_route(args):
                         "bound": "hbm", "achieved": achieved,
                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                         "achieved_over_step": achieved_step, "frac_over_step": achieved_step / peaks["hbm_gbs"],
-                        "traffic": None, "algorithmic_bytes_per_tuple": 8,
+                        "traffic": route_traffic, "traffic_source": route_traffic_note,
+                        "traffic_bytes_per_tuple": route_traffic / batch if route_traffic else None,
+                        "traffic_frac": route_traffic_frac, "algorithmic_bytes_per_tuple": 8,
                         "bytes_note": "SURVEY.md §8(d): 2 B label + 8 B id x 1/2 + 8 B id x 1/4; the emitted "
                                       "(id, bbox) rows (16 B x 1/8 read + written) are not counted",
                         "k1_ms_per_step": k1_ms / args.steps, "k2_ms_per_step": k2_ms / args.steps,
@@ -551,6 +561,9 @@ def run_route(args):
     e.close()
     # routing + compaction alone (no UDF arithmetic): label='dog' then emit; K1 reads the label
     # column (2 B/tuple), K2 reads the survivors' id + bbox and writes the (id, bbox) rows
+    if os.environ.get("HYDRO_ROUTE_ONLY") == "1":  # (ncu launch lists of the R-route run alone)
+        print(json.dumps(out))
+        return
     e = H.Eddy(policy="score", warmup_tuples=65536, max_batch_tuples=batch, max_inflight=4, stream=stream)
     e.add_predicate(label_pred())
     run_steps(2)

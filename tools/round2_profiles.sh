@@ -19,6 +19,11 @@ ncu --set full --clock-control none --import-source on -k regex:hydro_classifier
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"hydro_route|hydro_compact" -s 20 -c 2 -o $O/route_full -f \
   python bench.py --workload rroute --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+# R-route launch list: DRAM bytes of K1 and K2 per 16M-tuple batch (stamped, bench.py's rroute traffic)
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"hydro_route|hydro_compact" \
+  --csv --log-file $O/launches_rroute.csv env HYDRO_ROUTE_ONLY=1 python bench.py --workload rroute --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+python tools/traffic_json.py $O/launches_rroute.csv hydro_route_kernel > $O/route_k1_dram_traffic.json
+python tools/traffic_json.py $O/launches_rroute.csv hydro_compact_kernel > $O/route_k2_dram_traffic.json
 # the AREA hop alone (cfg4's AREA head on 1M crops, 16-converter-warp K4 instance)
 python tools/area_probe.py 5 > $O/area_probe.json 2> $O/area_probe.err
 ncu --set full --clock-control none --import-source on -k regex:hydro_classifier_kernel -s 2 -c 1 -o $O/area_full -f \
