@@ -742,13 +742,45 @@ def run_area(args):
         a, b = out_modes[f"round_robin@{batch}"], out_modes[f"data_aware@{batch}"]
         assert a["results"] == b["results"], (a, b)  # the schedule never changes the result
     best = out_modes[f"data_aware@{1 << 20}"]
+    # the AREA hop alone (cfg4's AREA breed head on the first 1M tuples, every tuple a crop; K4's
+    # 16-converter-warp AREA instance): device launch timers; algorithmic bytes = the crop's source
+    # pixels (3 w h) + 16 B of metadata per crop
+    na = 1 << 20
+    ta = t.slice(0, na)
+    ea = H.Eddy(frames=frames, policy="fixed", warmup_tuples=0, max_batch_tuples=na, stream=stream)
+    ea.add_predicate(w.preds[3])
+    res_ids = torch.empty(na, dtype=torch.int64, device="cuda")
+    res_bb = torch.empty((na, 4), dtype=torch.int16, device="cuda")
+    for _ in range(2):
+        ea.collect_into(ea.submit(ta), res_ids, res_bb)
+    torch.cuda.synchronize()
+    ea.device_time(1, reset=True)
+    ea.device_items(1, reset=True)
+    for _ in range(max(args.steps, 3)):
+        ea.collect_into(ea.submit(ta), res_ids, res_bb)
+    torch.cuda.synchronize()
+    a_ms, a_n = ea.device_time(1)
+    a_crops = ea.device_items(1)
+    ea.close()
+    bb = ta.bbox.long()
+    a_bytes_per_crop = float((3 * (bb[:, 2] - bb[:, 0]) * (bb[:, 3] - bb[:, 1])).double().mean().item()) + 16.0
+    a_gbs = a_crops * a_bytes_per_crop / (a_ms / 1000.0) / 1e9 if a_ms > 0 else 0.0
+    peaks = _peaks()
+    roofline = {"kernel": "hydro_classifier_kernel<.., AREA, 16 converter warps> (row-cooperative AREA converter, "
+                          "tcgen05 linear head), the AREA hop alone on 1M cfg4 crops",
+                "bound": "hbm", "achieved": a_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": a_gbs / peaks["hbm_gbs"], "crops_per_s": a_crops / (a_ms / 1000.0) if a_ms > 0 else None,
+                "algorithmic_bytes_per_crop": a_bytes_per_crop, "launches": a_n,
+                "time_source": "device launch timers",
+                "note": "instruction-issue bound in practice (ncu: issue active 73%, DRAM 14% of peak; "
+                        "profiles/round2_ncu_summary.md)"}
     out = {"metric": "tuples/s through cfg4 with data-aware tile scheduling of the AREA hop (SURVEY.md §8(f) f4)",
            "value": n / (best["ms_per_step"] / 1000.0), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": best["ms_per_step"], "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
            "config": {"workload": "cfg4: 10M tuples per step (label, area-weighted HASH, colour nearest, breed "
                                   "AREA), routing batches of 1M and 256K", "frames": "1024 x 720x1280x3"},
-           "modes": out_modes,
+           "modes": out_modes, "roofline": roofline,
            "speedup_data_aware_1M": out_modes[f"round_robin@{1 << 20}"]["ms_per_step"] / best["ms_per_step"],
            "speedup_data_aware_256K": out_modes[f"round_robin@{1 << 18}"]["ms_per_step"]
            / out_modes[f"data_aware@{1 << 18}"]["ms_per_step"],
