@@ -12,8 +12,32 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 }
 extern __shared__ __align__(128) uint8_t smem[];
 __global__ void gather(const uint8_t* pool, uint64_t pool_rows, uint32_t pitch, int units_per_warp, int slots,
-                       int slot_bytes, unsigned long long* bytes_out, uint32_t wmin) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+                       int slot_bytes, unsigned long long* bytes_out, uint32_t wmin, const uint8_t* weights, int wchunks) {
+  // optional weight stream (K4-T's B operand): the last warp bulk-copies wchunks 18 KB K-blocks of a
+  // 3.5 MB L2-resident matrix through a 3-stage ring while the other warps gather
+  const int nw_all = blockDim.x >> 5;
+  if (wchunks > 0 && (threadIdx.x >> 5) == nw_all - 1) {
+    uint64_t* wb = reinterpret_cast<uint64_t*>(smem) + 31 * 16;  // 3 barriers in warp 31's (unused) block
+    uint8_t* wring = smem + 4096 + (nw_all - 1) * slots * slot_bytes;
+    if ((threadIdx.x & 31) == 0) {
+      for (int st = 0; st < 3; ++st) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&wb[st])));
+      uint32_t wpar = 0;
+      for (int k = 0; k < wchunks; ++k) {
+        const int st = k % 3;
+        if (k >= 3) {
+          asm volatile("{\n.reg .pred P;\nW%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n@!P bra W%=;\n}" ::"r"(smem_u32(&wb[st])), "r"((wpar >> st) & 1u) : "memory");
+          wpar ^= 1u << st;
+        }
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&wb[st])), "r"(18432u) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(wring + st * 18432)),
+                     "l"(weights + (k % 192) * 18432ull), "r"(18432u), "r"(smem_u32(&wb[st])) : "memory");
+      }
+      for (int st = 0; st < 3; ++st)
+        asm volatile("{\n.reg .pred P;\nW%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n@!P bra W%=;\n}" ::"r"(smem_u32(&wb[(wchunks + st) % 3])), "r"(((wpar >> ((wchunks + st) % 3)) & 1u)) : "memory");
+    }
+    return;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = wchunks > 0 ? nw_all - 1 : nw_all;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint8_t* ring = smem + 4096 + warp * slots * slot_bytes;  // [32 warps x 16 mbarriers][rings]
   if (lane == 0)
@@ -71,25 +95,32 @@ int main() {
   unsigned long long* b; cudaMalloc(&b, 8);
   cudaFuncSetAttribute(gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
   const int slot_bytes = 6144;  // cfg2's units average ~5.6 KB (K4-T packs them into 22 KB rings)
-  int cfgs[][3] = {{8, 2, 32}, {8, 3, 32}, {16, 2, 32}, {32, 1, 32}, {8, 3, 16}, {16, 2, 16}, {8, 3, 8}, {16, 2, 8}};
+  uint8_t* wts; cudaMalloc(&wts, 192 * 18432);
+  cudaMemset(wts, 2, 192 * 18432);
+  // {gather warps, slots, w_min, weight stream}: the weight warp streams 3.5 MB per 128 x 64 crop rows
+  // of gathered tuples, as K4-T does for the fused pair (192 K-blocks of 18 KB per 128-tuple tile)
+  int cfgs[][4] = {{8, 3, 32, 0}, {8, 3, 32, 1}, {8, 2, 32, 1}, {16, 2, 32, 0}, {16, 2, 32, 1}};
   for (auto& c : cfgs) {
     const int wpc = c[0], slots = c[1];
     const uint32_t wmin = c[2];
-    const size_t sm = 4096 + (size_t)wpc * slots * slot_bytes;
+    const bool wstream = c[3] != 0;
+    const size_t sm = 4096 + (size_t)(wpc + (wstream ? 1 : 0)) * slots * slot_bytes + (wstream ? 3 * 18432 : 0);
     if (sm > 232448) { printf("W %d S %d: smem %zu too big\n", wpc, slots, sm); continue; }
     const int units = 4000;
     cudaMemset(b, 0, 8);
-    gather<<<148, wpc * 32, sm>>>(pool, rows, pitch, 200, slots, slot_bytes, b, wmin);  // warm
+    // units are crop rows of 16 tuples; per 128 tuples x 64 rows (= 512 units) the tile streams 192 K-blocks
+    const int threads = (wpc + (wstream ? 1 : 0)) * 32;
+    gather<<<148, threads, sm>>>(pool, rows, pitch, 200, slots, slot_bytes, b, wmin, wts, wstream ? 200 * wpc * 192 / 512 : 0);  // warm
     cudaMemset(b, 0, 8);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    gather<<<148, wpc * 32, sm>>>(pool, rows, pitch, units, slots, slot_bytes, b, wmin);
+    gather<<<148, threads, sm>>>(pool, rows, pitch, units, slots, slot_bytes, b, wmin, wts, wstream ? units * wpc * 192 / 512 : 0);
     cudaEventRecord(e1);
     cudaError_t err = cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     unsigned long long hb; cudaMemcpy(&hb, b, 8, cudaMemcpyDeviceToHost);
     const double copies = 148.0 * wpc * units * 16;
-    printf("w >= %2u W %2d S %d: %.1f GB/s of segment bytes (%.2f GB in %.2f ms), %.1f M copies/ms/SM %s\n", wmin, wpc, slots,
+    printf("%s w >= %2u W %2d S %d: %.1f GB/s of segment bytes (%.2f GB in %.2f ms), %.1f M copies/ms/SM %s\n", wstream ? "+weights" : "        ", wmin, wpc, slots,
            hb / (ms * 1e6), hb / 1e9, ms, copies / ms / 148 / 1e6,
            err ? cudaGetErrorString(err) : "");
     fflush(stdout);
