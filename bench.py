@@ -471,6 +471,76 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
+def run_orders(args):
+    """--workload orders: the eddy against every fixed order (the
+    adaptive routing claim).  cfg2's query over 1M tuples per step: each of the 3! fixed predicate
+    orders (policy fixed, no routing decisions) and the adaptive score policy (measured costs and
+    selectivities), device-timed the same way as the headline run; reports each order's tuples/s, the
+    order the eddy settles on and its throughput relative to the best fixed order."""
+    import itertools
+
+    import torch
+
+    from paper_2403_14902_b200 import build as B
+    from paper_2403_14902_b200 import hydro as H
+    from synth import workload
+
+    torch.cuda.set_device(0)
+    B.build()
+    w = workload("cfg2", weights=args.weights)
+    frames = w.frames(device="cuda")
+    stream = torch.cuda.current_stream()
+    batches = [w.tuples(id_start=b * TUPLES_PER_STEP, n=TUPLES_PER_STEP, device="cuda") for b in range(ROTATING_BATCHES)]
+    res_ids = torch.empty(1 << 20, dtype=torch.int64, device="cuda")
+    res_bb = torch.empty((1 << 20, 4), dtype=torch.int16, device="cuda")
+    names = [p["name"] for p in w.preds]
+
+    def measure(order):
+        e = H.Eddy(frames=frames, policy="fixed" if order else "score", warmup_tuples=65536,
+                   max_batch_tuples=1 << 20, max_inflight=4, stream=stream)
+        for p in w.preds:
+            e.add_predicate(p)
+        if order:
+            e.set_fixed_order(list(order))
+
+        def run(k, off):
+            pend = []
+            for st in range(k):
+                pend.append(e.submit(batches[(off + st) % ROTATING_BATCHES]))
+                if len(pend) >= 3:
+                    e.collect_into(pend.pop(0), res_ids, res_bb)
+            for bid in pend:
+                e.collect_into(bid, res_ids, res_bb)
+
+        run(max(args.warmup, 3), 0)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        run(args.steps, 1)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / args.steps
+        final = [names[k] for k in e.order()]
+        e.close()
+        return TUPLES_PER_STEP / (ms / 1000.0), ms, final
+
+    fixed = {}
+    for order in itertools.permutations(range(len(w.preds))):
+        tps, ms, _ = measure(order)
+        fixed[" -> ".join(names[k] for k in order)] = {"tuples_per_s": tps, "ms_per_step": ms}
+    tps, ms, final = measure(None)
+    best = max(fixed.items(), key=lambda kv: kv[1]["tuples_per_s"])
+    worst = min(fixed.items(), key=lambda kv: kv[1]["tuples_per_s"])
+    out = {"metric": "tuples/s of the adaptive eddy (score policy) against every fixed predicate order, cfg2",
+           "value": tps, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
+           "config": {"workload": WORKLOAD, "weights": args.weights},
+           "eddy_final_order": final, "fixed_orders": fixed,
+           "best_fixed": best[0], "eddy_over_best_fixed": tps / best[1]["tuples_per_s"],
+           "best_over_worst_fixed": best[1]["tuples_per_s"] / worst[1]["tuples_per_s"]}
+    print(json.dumps(out))
+
+
 def run_route(args):
     """--workload rroute: evidence run for the route/compaction kernel K1 (SURVEY.md §8(d) R-route):
     label='dog' (0.5) AND HASH (0.5, 1 unit) AND HASH (0.5, 1 unit) over 16M-tuple batches (352 MB of
@@ -1045,7 +1115,7 @@ def main():
                     help="classifier heads: fp16-exact 'grid' weights or general bf16 weights (N(0, 2.5e-4^2))")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "rroute", "mlp", "uc2", "uc2cls", "hsv", "area", "concurrent",
-                                                          "small"],
+                                                          "small", "orders"],
                     help="cfg2 = the BASELINE metric (default); rroute = K1 HBM evidence run; "
                          "mlp = cfg2 with the 12288-512-120 MLP breed head (SURVEY.md §8(f) f1, tensor roofline)")
     args = ap.parse_args()
@@ -1063,6 +1133,8 @@ def main():
         run_concurrent(args)
     elif args.workload == "small":
         run_small(args)
+    elif args.workload == "orders":
+        run_orders(args)
     else:
         run_gpu(args)
 
