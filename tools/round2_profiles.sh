@@ -7,7 +7,7 @@ mkdir -p gpurun_out/r2
 O=gpurun_out/r2
 python bench.py > $O/bench_cfg2.json 2> $O/bench_cfg2.err
 python bench.py --weights bf16 --no-cpu-baseline > $O/bench_cfg2_bf16.json 2> $O/bench_cfg2_bf16.err
-for wl in rroute mlp hsv uc2 uc2cls area small concurrent; do
+for wl in rroute mlp hsv uc2 uc2cls area small concurrent orders; do
   timeout 900 python bench.py --workload $wl --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_$wl.json 2> $O/bench_$wl.err
 done
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:hydro \
