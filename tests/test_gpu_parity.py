@@ -245,15 +245,21 @@ def test_errors_erange_ebusy_einval(small_dog):
 
 # ---------------------------------------------------------------- full-size (BASELINE sizes)
 
-def test_route_full_scale_label_and_hash_exact():
-    """R-route shape (label + 2 hash predicates) at 2M tuples: bit-exact against the oracle."""
-    w = workload("cfg2", n=2_000_000)
+@pytest.mark.parametrize("n,batch", [(2_000_000, 1 << 20), (6_000_000, 3 << 20)])
+def test_route_full_scale_label_and_hash_exact(n, batch):
+    """R-route shape (label + 2 hash predicates) bit-exact against the oracle, rows and per-batch
+    counters: 1M-tuple batches (one wave of tiles: the fused K1F) and 3M-tuple batches (the
+    streaming K1 + K2)."""
+    w = workload("cfg2", n=n)
     w.preds = [label_pred(), hash_pred(31, 0.5, units=1), hash_pred(32, 0.5, units=1)]
     t = w.tuples()
     V, ref_ids, ref_bbox, _ = oracle_result(w, t, None)
-    e = make_eddy(w, None, policy="score", warmup=65536, max_batch=1 << 20)
-    ids, bbs, infos = run_stream(e, t.to("cuda"), 1 << 20)
+    e = make_eddy(w, None, policy="score", warmup=65536, max_batch=batch)
+    ids, bbs, infos = run_stream(e, t.to("cuda"), batch)
     _assert_rows(ids, bbs, ref_ids, ref_bbox)
+    for b, info in enumerate(infos):
+        n_in, n_pass = expected_batch_counters(V[:, b * batch:(b + 1) * batch], info["order_used"], 65536 if b == 0 else 0)
+        assert info["tuples_in"] == n_in.tolist() and info["tuples_passed"] == n_pass.tolist(), b
     e.close()
 
 
