@@ -44,7 +44,7 @@ constexpr int kBStages = kBRing * kPair;  // same B-ring bytes; half-size stages
 #endif
 
 #ifndef HYDRO_AREA_WARPS
-#define HYDRO_AREA_WARPS 16
+#define HYDRO_AREA_WARPS 20
 #endif
 constexpr int kMaxCW = HYDRO_AREA_WARPS > kConvWarps ? HYDRO_AREA_WARPS : kConvWarps;
 struct ClsCtrl {
@@ -572,16 +572,25 @@ static_assert(kAreaQ == sizeof(ClsCtrl::astg[0]) / sizeof(uint64_t), "one mbarri
 constexpr uint32_t kAreaVBytes = 2u * 784u + 16u;           // V scratch: u16 per byte of a segment (+ overread)
 // per converter warp: V buffers (2 with two tuples per pass) + the item ring; the K4 AREA instance
 // with 12 converter warps (kAreaWarps) has room for one V buffer and a 5 KB ring per warp
+// Per converter warp: one item ring; an item's vertical sums V (2 bytes per segment byte) are written
+// over its own staged rows (an item is allocated max(hb, 2) rows), so no separate V buffer; 16 bytes
+// of slack after the ring keep the last column's second word inside the warp's region.
 template <int kCW>
 struct AreaCfg {
-  static constexpr bool kPairItems = kCW == kConvWarps;
-#ifndef HYDRO_AREA_RING16
-#define HYDRO_AREA_RING16 4096u
-#endif
-  static constexpr uint32_t kRing = kCW == kConvWarps ? 6144u : (kCW <= 12 ? 5040u : HYDRO_AREA_RING16);
-  static constexpr uint32_t kRegion = (kPairItems ? 2u : 1u) * kAreaVBytes + kRing;
+  static constexpr bool kPairItems = kCW == kConvWarps;  // (two tuples per pass: the ring holds two items)
   static constexpr int kBS = kCW > 12 ? 2 : 3;  // the kernel's weight stages (16 KB each at N = 128)
-  static_assert(kRing >= 5u * 784u && kRing % 16u == 0, "one worst-case AREA item (5 source rows of 784 B) must fit the ring");
+  static constexpr uint32_t kAvail =
+      static_cast<uint32_t>(kClsSmemBytes - 1023 - kARing * kAKBlockBytes - kBS * 16384 - sizeof(ClsCtrl) - 15);
+  static constexpr uint32_t kFit = ((kAvail / kCW - 16u) & ~15u) < 9600u ? ((kAvail / kCW - 16u) & ~15u) : 9600u;
+#ifndef HYDRO_AREA_RING_FIT  // a power-of-two ring (offsets by mask) when it still holds the pass's items
+  static constexpr uint32_t kPow2 = kFit >= 8192u ? 8192u : (kFit >= 4096u ? 4096u : kFit);
+  static constexpr uint32_t kRing = kPow2 >= (kCW == kConvWarps ? 2u : 1u) * 3920u ? kPow2 : kFit;
+#else
+  static constexpr uint32_t kRing = kFit;
+#endif
+  static constexpr uint32_t kRegion = kRing + 16u;
+  static_assert(kRing >= (kPairItems ? 2u : 1u) * 5u * 784u && kRing % 16u == 0,
+                "the worst-case AREA items of a pass (5 source rows of 784 B each) must fit the ring");
   static_assert(1023 + kARing * kAKBlockBytes + kBS * 16384 + sizeof(ClsCtrl) + 15 + kCW * kRegion <= kClsSmemBytes,
                 "AREA staging exceeds shared memory");
 };
@@ -614,7 +623,7 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
   const uint8_t* frames = p.frames;
   constexpr uint32_t kAreaRing = AreaCfg<kCW>::kRing;
   constexpr bool kPairItems = AreaCfg<kCW>::kPairItems;
-  const uint32_t vbuf = region, ring = region + (kPairItems ? 2u : 1u) * kAreaVBytes;
+  const uint32_t ring = region;
   const uint32_t rcp_tab = smem_u32(ctrl->area_rcp);
   // tuple t of the band = lane t (valid tuples are a prefix: rows past the hop's count are masked)
   const uint32_t nv = __popc(__ballot_sync(0xFFFFFFFFu, lane < 16 && mm.valid));
@@ -637,7 +646,7 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
     return ph + bytes > kAreaRing ? cur + (kAreaRing - ph) : cur;
   };
   uint32_t pk = 0, pg = 0, pt = 0, pcur = 0;  // producer: next item, its (g, t), ring cursor
-  uint32_t ccur = 0, ck = 0;                  // consumer: ring cursor, next item
+  uint32_t cnext = 0, clive = 0, ck = 0;      // consumer: end of the last consumed item, oldest live byte, next item
   // stage items ahead while the queue and the ring have room (oldest = start of item ck)
   auto produce = [&](uint32_t oldest) {
     while (pk < total && pk - ck < static_cast<uint32_t>(kAreaQ)) {
@@ -645,11 +654,11 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
       const uint32_t hp = __shfl_sync(0xFFFFFFFFu, my_h, pt);
       const uint32_t srcp = __shfl_sync(0xFFFFFFFFu, my_src, pt);
       const uint32_t ysp = (pg * hp) >> 6, hbp = (((pg + 1u) * hp + 63u) >> 6) - ysp;
-      const uint32_t bytes = hbp * Lp;
+      const uint32_t bytes = max(hbp, 2u) * Lp;  // (V is written over the item: 2 bytes per segment byte)
       const uint32_t ps = place(pcur, bytes);
-      if (pk != ck && ps + bytes - oldest > kAreaRing) break;  // the ring is full
+      if (ps + bytes - min(oldest, ps) > kAreaRing) break;  // the ring is full
       uint64_t* bar = &ctrl->astg[cu][(qseq + pk) % kAreaQ];
-      if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+      if (lane == 0) mbar_arrive_expect_tx(bar, hbp * Lp);
       __syncwarp();
       if (static_cast<uint32_t>(lane) < hbp)
         bulk_g2s_u32(ring + ps % kAreaRing + lane * Lp, at16(frames, srcp) + (ysp + lane) * row_pitch, Lp, bar);
@@ -661,35 +670,51 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
       }
     }
   };
-  // consume item ck (crop row g of tuple t): wait for its rows, vertical sums -> V at vb
-  auto consume = [&](uint32_t g, uint32_t t, uint32_t vb, uint32_t& hb_out, uint32_t& xw_out) {
+  // consume item ck (crop row g of tuple t): wait for its rows, vertical sums -> V over the item
+  // (every lane's loads of both of its chunks before any V store; the item stays live until the
+  // pass's horizontal sums are done: clive)
+  auto consume = [&](uint32_t g, uint32_t t, uint32_t& vb_out, uint32_t& hb_out, uint32_t& xw_out) {
     const uint32_t L = __shfl_sync(0xFFFFFFFFu, my_len, t);
     const uint32_t h = __shfl_sync(0xFFFFFFFFu, my_h, t);
     xw_out = __shfl_sync(0xFFFFFFFFu, my_xw, t);
     const uint32_t ys = (g * h) >> 6, hb = (((g + 1u) * h + 63u) >> 6) - ys;
     hb_out = hb;
-    const uint32_t cstart = place(ccur, hb * L);
-    produce(cstart);
+    const uint32_t cstart = place(cnext, max(hb, 2u) * L);
+    produce(clive == cnext ? cstart : clive);
     mbar_wait(&ctrl->astg[cu][(qseq + ck) % kAreaQ], ((qseq + ck) / kAreaQ) & 1u);
     const uint32_t item = ring + cstart % kAreaRing;
-    for (uint32_t c16 = static_cast<uint32_t>(lane); 16u * c16 < L; c16 += 32u) {
-      uint32_t s[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-      uint32_t a = item + 16u * c16;
-      for (uint32_t i = 0; i < hb; ++i, a += L) {
-        const uint4 r = lds128(a);
-        s[0] += __byte_perm(r.x, 0u, 0x4140);  // bytes 0, 1 as u16 halves
-        s[1] += __byte_perm(r.x, 0u, 0x4342);  // bytes 2, 3
-        s[2] += __byte_perm(r.y, 0u, 0x4140);
-        s[3] += __byte_perm(r.y, 0u, 0x4342);
-        s[4] += __byte_perm(r.z, 0u, 0x4140);
-        s[5] += __byte_perm(r.z, 0u, 0x4342);
-        s[6] += __byte_perm(r.w, 0u, 0x4140);
-        s[7] += __byte_perm(r.w, 0u, 0x4342);
+    uint32_t s[2][8];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s[k][q] = 0u;
+      const uint32_t c16 = static_cast<uint32_t>(lane) + 32u * k;
+      if (16u * c16 < L) {
+        uint32_t a = item + 16u * c16;
+        for (uint32_t i = 0; i < hb; ++i, a += L) {
+          const uint4 r = lds128(a);
+          s[k][0] += __byte_perm(r.x, 0u, 0x4140);  // bytes 0, 1 as u16 halves
+          s[k][1] += __byte_perm(r.x, 0u, 0x4342);  // bytes 2, 3
+          s[k][2] += __byte_perm(r.y, 0u, 0x4140);
+          s[k][3] += __byte_perm(r.y, 0u, 0x4342);
+          s[k][4] += __byte_perm(r.z, 0u, 0x4140);
+          s[k][5] += __byte_perm(r.z, 0u, 0x4342);
+          s[k][6] += __byte_perm(r.w, 0u, 0x4140);
+          s[k][7] += __byte_perm(r.w, 0u, 0x4342);
+        }
       }
-      sts128(vb + 32u * c16, s[0], s[1], s[2], s[3]);
-      sts128(vb + 32u * c16 + 16u, s[4], s[5], s[6], s[7]);
     }
-    ccur = cstart + hb * L;
+    __syncwarp();  // every lane's loads of the item are done: V may overwrite it
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t c16 = static_cast<uint32_t>(lane) + 32u * k;
+      if (16u * c16 < L) {
+        sts128(item + 32u * c16, s[k][0], s[k][1], s[k][2], s[k][3]);
+        sts128(item + 32u * c16 + 16u, s[k][4], s[k][5], s[k][6], s[k][7]);
+      }
+    }
+    vb_out = item;
+    cnext = cstart + max(hb, 2u) * L;
     ++ck;
   };
   for (uint32_t g = 0; g < static_cast<uint32_t>(kGroups); ++g, ++gg) {
@@ -701,11 +726,11 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
     // the horizontal sums, divisions and stores of both interleaved
     for (uint32_t t = 0; t < nv; t += kPairItems ? 2u : 1u) {
       const bool two = kPairItems && t + 1 < nv;
-      uint32_t hb[2], xw[2];
-      consume(g, t, vbuf, hb[0], xw[0]);
-      if (two) consume(g, t + 1, vbuf + kAreaVBytes, hb[1], xw[1]);
-      else hb[1] = xw[1] = 0u;
-      __syncwarp();  // V complete (and the items' ring bytes read: reusable)
+      uint32_t hb[2], xw[2], vbs[2];
+      consume(g, t, vbs[0], hb[0], xw[0]);
+      if (two) consume(g, t + 1, vbs[1], hb[1], xw[1]);
+      else hb[1] = xw[1] = 0u, vbs[1] = vbs[0];
+      __syncwarp();  // V complete
       // ---- horizontal bin sums of pixels q and q + 32 of both tuples
       uint32_t b2[2][2], bw[2][2], par[2][2], bwmax = 0;
 #pragma unroll
@@ -717,7 +742,7 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
           const uint32_t xs = (dx * w) >> 6;
           bw[u][e] = (((dx + 1u) * w + 63u) >> 6) - xs;  // 0 for an absent second tuple (w = 0)
           const uint32_t b = 3u * (x0 + xs) - slo;  // V index of the bin's first column, channel 0
-          b2[u][e] = vbuf + u * kAreaVBytes + 2u * b;  // byte address of V[b]
+          b2[u][e] = vbs[u] + 2u * b;  // byte address of V[b]
           par[u][e] = b & 1u;                          // V[b] is the high half of its word
           bwmax = max(bwmax, bw[u][e]);
         }
@@ -774,7 +799,8 @@ __device__ __forceinline__ void convert_tile_area(const ClsParams& p, ClsCtrl* c
           }
         }
       }
-      __syncwarp();  // V is rewritten by the next pass
+      __syncwarp();  // the pass's items (V) are released
+      clive = cnext;
     }
     // group g complete: publish its A stages
     fence_proxy_async_smem();
