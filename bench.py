@@ -813,7 +813,7 @@ def run_area(args):
         assert a["results"] == b["results"], (a, b)  # the schedule never changes the result
     best = out_modes[f"data_aware@{1 << 20}"]
     # the AREA hop alone (cfg4's AREA breed head on the first 1M tuples, every tuple a crop; K4's
-    # 16-converter-warp AREA instance): device launch timers; algorithmic bytes = the crop's source
+    # 20-converter-warp AREA instance): device launch timers; algorithmic bytes = the crop's source
     # pixels (3 w h) + 16 B of metadata per crop
     na = 1 << 20
     ta = t.slice(0, na)
@@ -836,7 +836,7 @@ def run_area(args):
     a_bytes_per_crop = float((3 * (bb[:, 2] - bb[:, 0]) * (bb[:, 3] - bb[:, 1])).double().mean().item()) + 16.0
     a_gbs = a_crops * a_bytes_per_crop / (a_ms / 1000.0) / 1e9 if a_ms > 0 else 0.0
     peaks = _peaks()
-    roofline = {"kernel": "hydro_classifier_kernel<.., AREA, 16 converter warps> (row-cooperative AREA converter, "
+    roofline = {"kernel": "hydro_classifier_kernel<.., AREA, 20 converter warps> (row-cooperative AREA converter, "
                           "tcgen05 linear head), the AREA hop alone on 1M cfg4 crops",
                 "bound": "hbm", "achieved": a_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": a_gbs / peaks["hbm_gbs"], "crops_per_s": a_crops / (a_ms / 1000.0) if a_ms > 0 else None,
