@@ -842,7 +842,7 @@ def run_area(args):
                 "frac": a_gbs / peaks["hbm_gbs"], "crops_per_s": a_crops / (a_ms / 1000.0) if a_ms > 0 else None,
                 "algorithmic_bytes_per_crop": a_bytes_per_crop, "launches": a_n,
                 "time_source": "device launch timers",
-                "note": "instruction-issue bound in practice (ncu: issue active 73%, DRAM 14% of peak; "
+                "note": "instruction-issue bound in practice (ncu: issue active 76%, DRAM 15% of peak; "
                         "profiles/round2_ncu_summary.md)"}
     out = {"metric": "tuples/s through cfg4 with data-aware tile scheduling of the AREA hop (SURVEY.md §8(f) f4)",
            "value": n / (best["ms_per_step"] / 1000.0), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
